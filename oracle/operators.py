@@ -1,0 +1,132 @@
+"""O1: the operators of the shifted family, written out literally (oracle, test-only).
+
+Images are n x n arrays, row index i (y), column index j (x); a vector x of
+length N = n^2 is the row-major flattening (pixel (i, j) at i*n + j).
+
+PAPER.md:
+  * forward model d = C x + e                         eq:forward
+  * normal equations (C^T C + lambda^2 L^T D^2 L) x = C^T d   eq:blkeqn P:126-128
+  * A = C^T C, E_0 = L^T L, b = C^T d, gamma = lambda^2
+  * E_k = L^T D_k^2 L                                 P:147, eq:shift P:365
+  * L = [Delta_x; Delta_y], discrete derivatives
+  * C: symmetric Gaussian blur, zero boundary
+North-star (BASELINE.json): E_k = L^T W_k L with the IRN weights
+  w_i = ((L x)_i^2 + tau^2)^(-1/2), W_0 = I            (reading G2/G3)
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def _psf_r(h: np.ndarray) -> int:
+    ph, pw = h.shape
+    if ph != pw or ph % 2 != 1:
+        raise ValueError("PSF must be square with odd size")
+    return ph // 2
+
+
+def conv(h: np.ndarray, x: np.ndarray) -> np.ndarray:
+    """C x: 'same'-size 2-D convolution with zero boundary (reading G20).
+
+    y[i, j] = sum_{a, b = -r..r} h[a+r, b+r] * x[i-a, j-b], summed over the
+    in-range pixels (i-a, j-b) only.
+    """
+    r = _psf_r(h)
+    n0, n1 = x.shape
+    xp = np.zeros((n0 + 2 * r, n1 + 2 * r))
+    xp[r:r + n0, r:r + n1] = x
+    y = np.zeros((n0, n1))
+    for a in range(-r, r + 1):
+        for b in range(-r, r + 1):
+            # x[i-a, j-b] = xp[r+i-a, r+j-b]
+            y += h[a + r, b + r] * xp[r - a:r - a + n0, r - b:r - b + n1]
+    return y
+
+
+def conv_t(h: np.ndarray, y: np.ndarray) -> np.ndarray:
+    """C^T y: the literal scatter adjoint of `conv`.
+
+    For every (i, j) and (a, b) with (i-a, j-b) in range:
+        out[i-a, j-b] += h[a+r, b+r] * y[i, j].
+    """
+    r = _psf_r(h)
+    n0, n1 = y.shape
+    op = np.zeros((n0 + 2 * r, n1 + 2 * r))
+    for a in range(-r, r + 1):
+        for b in range(-r, r + 1):
+            op[r - a:r - a + n0, r - b:r - b + n1] += h[a + r, b + r] * y
+    return op[r:r + n0, r:r + n1].copy()
+
+
+def apply_A(h: np.ndarray, x: np.ndarray) -> np.ndarray:
+    """A x = C^T (C x)."""
+    return conv_t(h, conv(h, x))
+
+
+def grad(x: np.ndarray):
+    """L x = (Dx x, Dy x), forward differences without boundary rows (reading G4):
+    (Dx x)[i, j] = x[i, j+1] - x[i, j] for j <= n-2; (Dy x)[i, j] = x[i+1, j] - x[i, j]
+    for i <= n-2. Shapes (n, n-1) and (n-1, n)."""
+    return x[:, 1:] - x[:, :-1], x[1:, :] - x[:-1, :]
+
+
+def grad_t(qx: np.ndarray, qy: np.ndarray) -> np.ndarray:
+    """L^T (qx, qy): the literal scatter adjoint of `grad`."""
+    n = qx.shape[0]
+    out = np.zeros((n, n))
+    for j in range(n - 1):
+        out[:, j + 1] += qx[:, j]
+        out[:, j] -= qx[:, j]
+    for i in range(n - 1):
+        out[i + 1, :] += qy[i, :]
+        out[i, :] -= qy[i, :]
+    return out
+
+
+def identity_weights(n: int):
+    """W_0 = I on the n(n-1) rows of each derivative; padded layout (n, n) with
+    wx[:, n-1] = 0 and wy[n-1, :] = 0 (SURVEY §8.0 data layout)."""
+    wx = np.ones((n, n))
+    wy = np.ones((n, n))
+    wx[:, n - 1] = 0.0
+    wy[n - 1, :] = 0.0
+    return wx, wy
+
+
+def apply_E(wx: np.ndarray, wy: np.ndarray, x: np.ndarray) -> np.ndarray:
+    """E x = L^T (W (L x)) with W = diag(wx, wy) (P:147 with W_k = D_k^2)."""
+    qx, qy = grad(x)
+    return grad_t(wx[:, :-1] * qx, wy[:-1, :] * qy)
+
+
+def apply_shifted(h, wx, wy, gamma: float, x: np.ndarray) -> np.ndarray:
+    """(A + gamma E_k) x  (eq:seqsys P:47, eq:shift P:361-365)."""
+    return apply_A(h, x) + gamma * apply_E(wx, wy, x)
+
+
+def irn_weights(x: np.ndarray, tau: float):
+    """IRN weights w_i = ((L x)_i^2 + tau^2)^(-1/2) (north_star; IRN family P:60),
+    one weight per row of L (anisotropic, reading G3), pads = 0."""
+    n = x.shape[0]
+    qx, qy = grad(x)
+    wx = np.zeros((n, n))
+    wy = np.zeros((n, n))
+    wx[:, :-1] = 1.0 / np.sqrt(qx * qx + tau * tau)
+    wy[:-1, :] = 1.0 / np.sqrt(qy * qy + tau * tau)
+    return wx, wy
+
+
+def seminorm2(wx, wy, x) -> float:
+    """||W^(1/2) L x||^2 = sum wx (Dx x)^2 + sum wy (Dy x)^2, the L-curve's
+    vertical coordinate under the current E_k (reading G25)."""
+    qx, qy = grad(x)
+    return float(np.sum(wx[:, :-1] * qx * qx) + np.sum(wy[:-1, :] * qy * qy))
+
+
+def make_data(h, x_true, xi, nu):
+    """d = C x_true + e with ||e|| = nu ||C x_true|| and e parallel to xi (eq:forward P:107,
+    reading G21); b = C^T d."""
+    cx = conv(h, x_true)
+    e = nu * np.linalg.norm(cx) * xi / np.linalg.norm(xi)
+    d = cx + e
+    return d, conv_t(h, d)

@@ -1,0 +1,169 @@
+"""O6: L-curve and the outer IRN loop (Alg. 5) -- oracle, test-only.
+
+One outer step k (reading D3: all shifts of a step are independent):
+  1. k = 0: seed solves at gamma_i1, gamma_i2 (plain CG, residual store) and
+     Ritz spaces V_i1, V_i2;  U~ = [x^(0,i1), x^(0,i2), V_i1, V_i2]
+     k >= 1: U~ = [V_i1, x^(k-1,1), ..., x^(k-1,M)]      (eq:tildeUupdate, G10)
+  2. U~ <- stabilize(U~, cap n_c)                         (Alg. 1)
+  3. anchor at gamma_* = gamma_{i*}                       (eq:establishU)
+  4. x_0^(k,l) = U q_l from eq:orthupdate
+  5. groups L = {l <= I}, R = {l > I}; W from gamma_{J_L}, gamma_{J_R} (Alg. 4)
+  6. per shift: U_l = [W_g(l), g-hat^(k-1,l)] and deflated CG (O4)
+  7. L-curve corner l* (P:138-140), x* = x^(k,l*)
+  8. W_{k+1} = IRN weights of x* (north_star; reading G2)
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+
+import numpy as np
+
+from . import defcg as dcg
+from . import operators as ops
+from . import recycle as rc
+
+
+def lcurve_corner(rho: np.ndarray, eta: np.ndarray) -> tuple[int, np.ndarray]:
+    """Corner of the discrete L-curve (log rho_l, log eta_l): maximum curvature
+     with centred differences on the uniform t = log10 lambda
+    grid, endpoints excluded, ties to the smallest index (reading G25).
+    kappa = (rho' eta'' - rho'' eta') / (rho'^2 + eta'^2)^(3/2). Returns 0-based l*."""
+    M = len(rho)
+    lr = np.log(np.asarray(rho, dtype=np.float64))
+    le = np.log(np.asarray(eta, dtype=np.float64))
+    kappa = np.full(M, -np.inf)
+    for l in range(1, M - 1):
+        r1 = (lr[l + 1] - lr[l - 1]) / 2.0
+        e1 = (le[l + 1] - le[l - 1]) / 2.0
+        r2 = lr[l + 1] - 2.0 * lr[l] + lr[l - 1]
+        e2 = le[l + 1] - 2.0 * le[l] + le[l - 1]
+        den = (r1 * r1 + e1 * e1) ** 1.5
+        kappa[l] = (r1 * e2 - r2 * e1) / den if den > 0 else -np.inf
+    if M < 3:
+        return 0, kappa
+    best = 1 + int(np.argmax(kappa[1:M - 1]))   # np.argmax: first maximum -> smallest l
+    return best, kappa
+
+
+@dataclasses.dataclass
+class StepState:
+    """Everything outer step k needs from step k-1 (the stepwise parity handoff, G28)."""
+    k: int
+    wx: np.ndarray
+    wy: np.ndarray
+    X_prev: np.ndarray | None      # N x M solutions of step k-1
+    G_prev: np.ndarray | None      # N x M corrections g^(k-1,l)
+    V_i1: np.ndarray | None        # Ritz block kept from k = 0
+
+
+@dataclasses.dataclass
+class StepResult:
+    X: np.ndarray
+    G: np.ndarray
+    Xp: np.ndarray
+    iters: np.ndarray
+    applies: np.ndarray
+    status: np.ndarray
+    relres: np.ndarray
+    guess_relres: np.ndarray
+    nc: int
+    lstar: int
+    rho: np.ndarray
+    eta: np.ndarray
+    overhead_applies: int          # seeds + Ritz + anchoring + g-hat images
+    V_i1: np.ndarray | None
+    Ut: np.ndarray | None = None
+    anchor: rc.Anchor | None = None
+
+
+def outer_step(cfg, h, b, d, gamma, st: StepState, shifts=None) -> StepResult:
+    """One outer step (Alg. 5 body) under the readings listed above.
+    `shifts` optionally restricts the CG solves to a subset of 0-based indices
+    (the others are left at zero) -- used for bounded-cost samples."""
+    n, M, N = cfg.n, cfg.M, cfg.N
+    wx, wy = st.wx, st.wy
+
+    def A_g(g):
+        return lambda v: ops.apply_shifted(h, wx, wy, g, v.reshape(n, n)).ravel()
+
+    overhead = 0
+    i1, i2 = cfg.i1 - 1, cfg.i2 - 1
+    V_i1 = st.V_i1
+    if st.k == 0:
+        n1 = math.ceil(2 * (cfg.n_c - 2) / 3)
+        n2 = cfg.n_c - 2 - n1
+        s1 = dcg.defcg(A_g(gamma[i1]), b, tol=cfg.tol, maxit=cfg.maxit, store_cap=100)
+        s2 = dcg.defcg(A_g(gamma[i2]), b, tol=cfg.tol, maxit=cfg.maxit, store_cap=100)
+        V_i1, _, a1 = rc.ritz_space(A_g(gamma[i1]), s1.store, n1)
+        V_i2, _, a2 = rc.ritz_space(A_g(gamma[i2]), s2.store, n2)
+        overhead += s1.applies + s2.applies + a1 + a2
+        raw = np.column_stack([s1.x, s2.x, V_i1, V_i2])
+    else:
+        raw = np.column_stack([V_i1, st.X_prev])
+    Ut = rc.stabilize(raw, cfg.n_c)
+    gstar = gamma[cfg.istar - 1]
+    an = rc.anchor(h, wx, wy, Ut, b, gstar, n)
+    overhead += Ut.shape[1]
+
+    groups = {}
+    for gname, jidx in (("L", cfg.J_L - 1), ("R", cfg.J_R - 1)):
+        W, AW, EW, _, _ = rc.group_ritz(an, gamma[jidx], cfg.J)
+        groups[gname] = (W, AW, EW)
+
+    X = np.zeros((N, M)); G = np.zeros((N, M)); Xp = np.zeros((N, M))
+    iters = np.zeros(M, dtype=np.int64); applies = np.zeros(M, dtype=np.int64)
+    status = np.zeros(M, dtype=np.int64); relres = np.zeros(M); grel = np.zeros(M)
+    nb = np.linalg.norm(b)
+    todo = range(M) if shifts is None else shifts
+    for l in todo:
+        W, AW, EW = groups["L" if (l + 1) <= cfg.I_split else "R"]
+        xp = rc.principal_guess(an, gamma[l])
+        cols_U = [W]
+        cols_Z = [AW + gamma[l] * EW]
+        n_carry = 0
+        if st.k >= 1 and st.G_prev is not None:
+            gh = rc.carried_direction(W, st.G_prev[:, l])
+            if gh is not None:
+                img = gh.reshape(n, n)
+                zg = (ops.apply_A(h, img) + gamma[l] * ops.apply_E(wx, wy, img)).ravel()
+                overhead += 1
+                cols_U.append(gh[:, None]); cols_Z.append(zg[:, None]); n_carry = 1
+        U = np.column_stack(cols_U); Z = np.column_stack(cols_Z)
+        res = dcg.defcg(A_g(gamma[l]), b, x_p=xp, U=U, Z=Z, tol=cfg.tol,
+                        maxit=cfg.maxit, n_carry=n_carry)
+        X[:, l] = res.x
+        Xp[:, l] = 0.0 if xp is None else xp
+        G[:, l] = res.x - Xp[:, l]
+        iters[l] = res.iters; applies[l] = res.applies; status[l] = res.status
+        relres[l] = res.relres_true
+        grel[l] = (np.linalg.norm(b - A_g(gamma[l])(Xp[:, l])) / nb) if xp is not None else 1.0
+
+    rho = np.zeros(M); eta = np.zeros(M)
+    for l in range(M):
+        img = X[:, l].reshape(n, n)
+        rho[l] = np.linalg.norm(ops.conv(h, img) - d)
+        eta[l] = math.sqrt(ops.seminorm2(wx, wy, img))
+    lstar = lcurve_corner(rho, eta)[0] if shifts is None else -1
+    return StepResult(X, G, Xp, iters, applies, status, relres, grel, Ut.shape[1], lstar,
+                      rho, eta, overhead, V_i1, Ut, an)
+
+
+def run(cfg, inputs, K_out=None, keep_steps=False):
+    """The outer IRN loop: K_out outer steps (configs fix the count, reading of A28)."""
+    n = cfg.n
+    h = inputs["psf"]
+    d, b2 = ops.make_data(h, inputs["x_true"], inputs["xi"], cfg.noise)
+    b = b2.ravel(); dd = d
+    gamma = inputs["gamma"]
+    wx, wy = ops.identity_weights(n)
+    st = StepState(0, wx, wy, None, None, None)
+    steps = []
+    for k in range(K_out or cfg.K_out):
+        st.k = k
+        res = outer_step(cfg, h, b, dd, gamma, st)
+        steps.append(res if keep_steps else dataclasses.replace(res, Ut=None, anchor=None))
+        xstar = res.X[:, res.lstar].reshape(n, n)
+        wx, wy = ops.irn_weights(xstar, cfg.tau)
+        st = StepState(k + 1, wx, wy, res.X, res.G, res.V_i1)
+    return {"b": b, "d": dd, "steps": steps, "final_weights": (wx, wy)}

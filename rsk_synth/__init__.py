@@ -1,0 +1,195 @@
+"""Seeded synthetic inputs shared by the oracle and the CUDA path.
+
+This module holds NO arithmetic of the method (no convolution, no gradient,
+no solver step). It only draws the problem's raw ingredients from a seeded
+generator so that `oracle/` and `paper_2306_15049_b200/` see the same bytes:
+
+* x_true  -- piecewise-constant phantom (rectangles / discs, values U[0,1)),
+             the edge-rich natural-image surrogate of PAPER.md §2.1
+* psf     -- (2r+1)^2 Gaussian point-spread function normalised to sum 1,
+             centred, the "symmetric, Gaussian blur" of §8.2
+* xi      -- raw N(0, I) draw; each side scales it to the configured noise
+             level itself (d = Cx + nu*||Cx|| xi/||xi||)
+* gamma   -- the shift ladder, log-evenly spaced, ascending
+
+Recipe: SURVEY.md §8(d) d1 (seed = 230615049 + config index, PCG64).
+The per-config sizes follow BASELINE.json `configs` (C1..C5); readings of the
+values BASELINE.json leaves open are the G-list of SURVEY.md §8(c), repeated
+in DESIGN.md.
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+
+import numpy as np
+
+SEED_BASE = 230615049
+
+
+@dataclasses.dataclass(frozen=True)
+class Config:
+    name: str
+    index: int            # 1-based config index (C1..C5)
+    n: int                # image is n x n, N = n*n
+    M: int                # number of shifts
+    gamma_lo: float
+    gamma_hi: float
+    r: int                # PSF half width, PSF is (2r+1)^2
+    sigma: float
+    noise: float          # relative noise level nu
+    n_c: int              # principal recycle-space cap
+    J: int                # Ritz vectors per shift group (|J|)
+    K_out: int            # outer IRN steps
+    tau: float            # IRN smoothing
+    tol: float            # CG relative residual tolerance
+    shapes: str           # phantom recipe key
+    n_shapes: int
+    maxit: int = 20000
+
+    @property
+    def N(self) -> int:
+        return self.n * self.n
+
+    # Index readings of SURVEY G11 (1-based, as in the paper's Table)
+    @property
+    def i1(self) -> int:
+        return 1
+
+    @property
+    def i2(self) -> int:
+        return self.M // 2
+
+    @property
+    def istar(self) -> int:
+        return self.M // 2
+
+    @property
+    def I_split(self) -> int:
+        return int(round(0.75 * self.M))
+
+    @property
+    def J_L(self) -> int:
+        return self.I_split
+
+    @property
+    def J_R(self) -> int:
+        return self.M - 1
+
+
+CONFIGS = {
+    "C1": Config("C1", 1, 32, 8, 1e-4, 1.0, 4, 1.5, 0.01, 10, 2, 3, 1e-3, 1e-8, "rects", 6),
+    "C2": Config("C2", 2, 256, 32, 1e-5, 10.0, 4, 2.0, 0.01, 40, 8, 5, 1e-3, 1e-8, "rects", 20),
+    "C3": Config("C3", 3, 512, 64, 1e-6, 10.0, 7, 3.0, 0.02, 60, 10, 6, 1e-3, 1e-8, "rects+discs", 60),
+    "C4": Config("C4", 4, 1024, 128, 1e-6, 100.0, 7, 4.0, 0.01, 80, 12, 8, 1e-4, 1e-8, "alternate", 200),
+    "C5": Config("C5", 5, 4096, 16, 1e-5, 10.0, 10, 5.0, 0.01, 40, 8, 4, 1e-3, 1e-8, "alternate", 2000),
+}
+
+
+def small_config(n: int = 16, M: int = 6, r: int = 2, sigma: float = 1.0, n_c: int = 8,
+                 J: int = 2, K_out: int = 2, name: str = "tiny", n_shapes: int = 4,
+                 gamma_lo: float = 1e-3, gamma_hi: float = 1.0, tau: float = 1e-3,
+                 tol: float = 1e-10, noise: float = 0.01) -> Config:
+    """A tiny configuration with the C1 recipe, for oracle pins and fast parity."""
+    return Config(name, 1, n, M, gamma_lo, gamma_hi, r, sigma, noise, n_c, J, K_out,
+                  tau, tol, "rects", n_shapes)
+
+
+def rng_for(cfg: Config) -> np.random.Generator:
+    return np.random.Generator(np.random.PCG64(SEED_BASE + cfg.index))
+
+
+def _shape_params(cfg: Config):
+    n = cfg.n
+    if cfg.shapes in ("rects", "rects+discs"):
+        s = (math.ceil(n / 16), math.ceil(n / 4))
+        q = (math.ceil(n / 32), math.ceil(n / 8))
+    else:  # "alternate" (C4, C5)
+        if n <= 1024:
+            s = (math.ceil(n / 64), math.ceil(n / 8))
+            q = (math.ceil(n / 128), math.ceil(n / 16))
+        else:
+            s = (math.ceil(n / 256), math.ceil(n / 16))
+            q = (math.ceil(n / 512), math.ceil(n / 32))
+    return s, q
+
+
+def phantom(cfg: Config, rng: np.random.Generator) -> np.ndarray:
+    """Piecewise-constant phantom, later shapes overwrite earlier ones."""
+    n = cfg.n
+    x = np.zeros((n, n), dtype=np.float64)
+    (s_lo, s_hi), (q_lo, q_hi) = _shape_params(cfg)
+    s_hi = min(s_hi, n)
+    if cfg.shapes == "rects":
+        kinds = ["rect"] * cfg.n_shapes
+    elif cfg.shapes == "rects+discs":
+        kinds = ["rect"] * 50 + ["disc"] * 10
+    else:
+        kinds = ["rect" if k % 2 == 0 else "disc" for k in range(cfg.n_shapes)]
+    ii, jj = np.mgrid[0:n, 0:n]
+    for kind in kinds:
+        val = rng.random()
+        if kind == "rect":
+            h = int(rng.integers(s_lo, s_hi + 1))
+            w = int(rng.integers(s_lo, s_hi + 1))
+            i0 = int(rng.integers(0, n - h + 1))
+            j0 = int(rng.integers(0, n - w + 1))
+            x[i0:i0 + h, j0:j0 + w] = val
+        else:
+            q = int(rng.integers(q_lo, q_hi + 1))
+            ci = int(rng.integers(q, n - q))
+            cj = int(rng.integers(q, n - q))
+            i_a, i_b = max(0, ci - q), min(n, ci + q + 1)
+            j_a, j_b = max(0, cj - q), min(n, cj + q + 1)
+            sub = (ii[i_a:i_b, j_a:j_b] - ci) ** 2 + (jj[i_a:i_b, j_a:j_b] - cj) ** 2 <= q * q
+            x[i_a:i_b, j_a:j_b][sub] = val
+    return x
+
+
+def gaussian_psf(r: int, sigma: float) -> np.ndarray:
+    """h[a+r, b+r] proportional to exp(-(a^2+b^2)/(2 sigma^2)), sum(h) = 1."""
+    a = np.arange(-r, r + 1, dtype=np.float64)
+    h = np.exp(-(a[:, None] ** 2 + a[None, :] ** 2) / (2.0 * sigma * sigma))
+    return h / h.sum()
+
+
+def gamma_ladder(cfg: Config) -> np.ndarray:
+    """gamma_l = 10^(log10 lo + (l-1)(log10 hi - log10 lo)/(M-1)), ascending."""
+    lo, hi = math.log10(cfg.gamma_lo), math.log10(cfg.gamma_hi)
+    if cfg.M == 1:
+        return np.array([cfg.gamma_lo])
+    return np.array([10.0 ** (lo + l * (hi - lo) / (cfg.M - 1)) for l in range(cfg.M)])
+
+
+def make_inputs(cfg: Config) -> dict:
+    """All seeded raw inputs of one configuration (fp64, C-contiguous)."""
+    rng = rng_for(cfg)
+    x_true = phantom(cfg, rng)
+    xi = rng.standard_normal((cfg.n, cfg.n))
+    return {
+        "x_true": np.ascontiguousarray(x_true),
+        "psf": gaussian_psf(cfg.r, cfg.sigma),
+        "xi": np.ascontiguousarray(xi),
+        "gamma": gamma_ladder(cfg),
+    }
+
+
+def random_vectors(seed: int, shape, dist: str = "normal") -> np.ndarray:
+    """Seeded test vectors (parity cases, not part of any workload)."""
+    g = np.random.Generator(np.random.PCG64(seed))
+    if dist == "normal":
+        return g.standard_normal(shape)
+    if dist == "uniform":
+        return g.random(shape)
+    raise ValueError(dist)
+
+
+def random_weights(seed: int, n: int, lo: float = 0.1, hi: float = 1000.0) -> tuple:
+    """Bimodal positive weight planes with zero pads, the shape IRN weights take
+    (about 1/tau on flats, about 1/|jump| on edges; SURVEY d1 'value structure')."""
+    g = np.random.Generator(np.random.PCG64(seed))
+    wx = np.exp(g.uniform(math.log(lo), math.log(hi), (n, n)))
+    wy = np.exp(g.uniform(math.log(lo), math.log(hi), (n, n)))
+    wx[:, n - 1] = 0.0
+    wy[n - 1, :] = 0.0
+    return wx, wy
