@@ -1,0 +1,324 @@
+// Small dense linear algebra on the host (n_c x n_c and smaller): Cholesky,
+// cyclic Jacobi symmetric eigensolver (Alg. 2), one-sided Jacobi SVD
+// (Alg. 1 applied to R), the per-shift initial-guess solves of
+// eq:orthupdate and the L-curve corner.
+// Written independently of the oracle (which uses numpy.linalg).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+#include <vector>
+
+#include "rsk_internal.h"
+
+namespace rsk {
+
+// In-place Cholesky of a column-major n x n SPD matrix: lower triangle <- L.
+bool chol_lower(int n, double* A) {
+  for (int j = 0; j < n; ++j) {
+    double d = A[j + j * n];
+    for (int k = 0; k < j; ++k) d -= A[j + k * n] * A[j + k * n];
+    if (!(d > 0.0) || !std::isfinite(d)) return false;
+    d = std::sqrt(d);
+    A[j + j * n] = d;
+    for (int i = j + 1; i < n; ++i) {
+      double t = A[i + j * n];
+      for (int k = 0; k < j; ++k) t -= A[i + k * n] * A[j + k * n];
+      A[i + j * n] = t / d;
+    }
+    for (int i = 0; i < j; ++i) A[i + j * n] = 0.0;
+  }
+  return true;
+}
+
+void chol_solve_lower(int n, const double* L, double* x) {
+  for (int i = 0; i < n; ++i) {
+    double t = x[i];
+    for (int j = 0; j < i; ++j) t -= L[i + j * n] * x[j];
+    x[i] = t / L[i + i * n];
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double t = x[i];
+    for (int j = i + 1; j < n; ++j) t -= L[j + i * n] * x[j];
+    x[i] = t / L[i + i * n];
+  }
+}
+
+// Cyclic Jacobi on sym(H); eigenvalues ascending, eigenvectors in columns of V.
+void jacobi_eig(int n, const double* H, double* theta, double* V) {
+  std::vector<double> A(n * n);
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) A[i + j * n] = 0.5 * (H[i + j * n] + H[j + i * n]);
+  std::vector<double> Q(n * n, 0.0);
+  for (int i = 0; i < n; ++i) Q[i + i * n] = 1.0;
+  for (int sweep = 0; sweep < 100; ++sweep) {
+    double off = 0.0, tot = 0.0;
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < n; ++i) {
+        tot += A[i + j * n] * A[i + j * n];
+        if (i != j) off += A[i + j * n] * A[i + j * n];
+      }
+    if (off <= 1e-32 * tot || off == 0.0) break;
+    for (int p = 0; p < n - 1; ++p) {
+      for (int q = p + 1; q < n; ++q) {
+        const double apq = A[p + q * n];
+        if (apq == 0.0) continue;
+        const double app = A[p + p * n], aqq = A[q + q * n];
+        const double tau = (aqq - app) / (2.0 * apq);
+        const double t = (tau >= 0 ? 1.0 : -1.0) / (std::fabs(tau) + std::sqrt(1.0 + tau * tau));
+        const double c = 1.0 / std::sqrt(1.0 + t * t), s = t * c;
+        for (int k = 0; k < n; ++k) {  // A <- J^T A J (columns)
+          const double akp = A[k + p * n], akq = A[k + q * n];
+          A[k + p * n] = c * akp - s * akq;
+          A[k + q * n] = s * akp + c * akq;
+        }
+        for (int k = 0; k < n; ++k) {  // rows
+          const double apk = A[p + k * n], aqk = A[q + k * n];
+          A[p + k * n] = c * apk - s * aqk;
+          A[q + k * n] = s * apk + c * aqk;
+        }
+        A[p + q * n] = A[q + p * n] = 0.0;
+        for (int k = 0; k < n; ++k) {
+          const double qkp = Q[k + p * n], qkq = Q[k + q * n];
+          Q[k + p * n] = c * qkp - s * qkq;
+          Q[k + q * n] = s * qkp + c * qkq;
+        }
+      }
+    }
+  }
+  std::vector<int> idx(n);
+  std::iota(idx.begin(), idx.end(), 0);
+  std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return A[a + a * n] < A[b + b * n]; });
+  for (int j = 0; j < n; ++j) {
+    theta[j] = A[idx[j] + idx[j] * n];
+    for (int i = 0; i < n; ++i) V[i + j * n] = Q[i + idx[j] * n];
+  }
+}
+
+// One-sided Jacobi SVD of a k x k matrix: R = Ur diag(s) Vr^T, s descending.
+void jacobi_svd(int k, const double* R, double* Ur, double* s, double* Vr) {
+  std::vector<double> A(R, R + (size_t)k * k);
+  std::vector<double> V((size_t)k * k, 0.0);
+  for (int i = 0; i < k; ++i) V[i + i * k] = 1.0;
+  for (int sweep = 0; sweep < 80; ++sweep) {
+    bool rotated = false;
+    for (int p = 0; p < k - 1; ++p) {
+      for (int q = p + 1; q < k; ++q) {
+        double alpha = 0, beta = 0, gamma = 0;
+        for (int i = 0; i < k; ++i) {
+          alpha += A[i + p * k] * A[i + p * k];
+          beta += A[i + q * k] * A[i + q * k];
+          gamma += A[i + p * k] * A[i + q * k];
+        }
+        if (gamma == 0.0 || std::fabs(gamma) <= 1e-15 * std::sqrt(alpha * beta)) continue;
+        rotated = true;
+        const double zeta = (beta - alpha) / (2.0 * gamma);
+        const double t = (zeta >= 0 ? 1.0 : -1.0) / (std::fabs(zeta) + std::sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / std::sqrt(1.0 + t * t), sn = c * t;
+        for (int i = 0; i < k; ++i) {
+          const double ap = A[i + p * k], aq = A[i + q * k];
+          A[i + p * k] = c * ap - sn * aq;
+          A[i + q * k] = sn * ap + c * aq;
+          const double vp = V[i + p * k], vq = V[i + q * k];
+          V[i + p * k] = c * vp - sn * vq;
+          V[i + q * k] = sn * vp + c * vq;
+        }
+      }
+    }
+    if (!rotated) break;
+  }
+  std::vector<double> nrm(k);
+  for (int j = 0; j < k; ++j) {
+    double t = 0;
+    for (int i = 0; i < k; ++i) t += A[i + j * k] * A[i + j * k];
+    nrm[j] = std::sqrt(t);
+  }
+  std::vector<int> idx(k);
+  std::iota(idx.begin(), idx.end(), 0);
+  std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return nrm[a] > nrm[b]; });
+  for (int j = 0; j < k; ++j) {
+    const int src = idx[j];
+    s[j] = nrm[src];
+    for (int i = 0; i < k; ++i) {
+      Ur[i + j * k] = nrm[src] > 0 ? A[i + src * k] / nrm[src] : (i == j ? 1.0 : 0.0);
+      Vr[i + j * k] = V[i + src * k];
+    }
+  }
+}
+
+}  // namespace rsk
+
+using namespace rsk;
+
+namespace {
+// X <- X R^-1 for upper-triangular R (X is rows x nc, column-major, ld rows)
+void right_trsm_upper(int rows, int nc, const double* R, double* X) {
+  for (int j = 0; j < nc; ++j) {
+    for (int q = 0; q < j; ++q) {
+      const double rq = R[q + j * nc];
+      if (rq == 0.0) continue;
+      for (int i = 0; i < rows; ++i) X[i + j * rows] -= X[i + q * rows] * rq;
+    }
+    const double d = R[j + j * nc];
+    for (int i = 0; i < rows; ++i) X[i + j * rows] /= d;
+  }
+}
+// x <- R^-T x (forward substitution with R^T lower)
+void trsv_upper_t(int nc, const double* R, double* x) {
+  for (int i = 0; i < nc; ++i) {
+    double t = x[i];
+    for (int q = 0; q < i; ++q) t -= R[q + i * nc] * x[q];
+    x[i] = t / R[i + i * nc];
+  }
+}
+}  // namespace
+
+extern "C" rsk_status rsk_orth_guess(int nc, const double* R_h, const double* KtZE_h,
+                                     const double* ZEtZE_h, const double* ZEtb_h,
+                                     const double* Ktb_h, double gamma_star, int m,
+                                     const double* gamma_h, double* C_h, int* status_h) {
+  if (nc <= 0 || m < 0 || !R_h || !KtZE_h || !ZEtZE_h || !ZEtb_h || !Ktb_h ||
+      (m > 0 && (!gamma_h || !C_h || !status_h)))
+    return RSK_EINVAL;
+  for (int i = 0; i < nc; ++i)
+    if (!(R_h[i + i * nc] != 0.0)) return RSK_EINVAL;
+  // P = KtZE R^-1
+  std::vector<double> P_(KtZE_h, KtZE_h + (size_t)nc * nc);
+  right_trsm_upper(nc, nc, R_h, P_.data());
+  // Q2 = R^-T (ZEtZE R^-1): right solve, then transpose-left solve column by column
+  std::vector<double> T(ZEtZE_h, ZEtZE_h + (size_t)nc * nc);
+  right_trsm_upper(nc, nc, R_h, T.data());
+  for (int j = 0; j < nc; ++j) trsv_upper_t(nc, R_h, &T[(size_t)j * nc]);
+  std::vector<double> Q2_((size_t)nc * nc);
+  for (int j = 0; j < nc; ++j)
+    for (int i = 0; i < nc; ++i) Q2_[i + j * nc] = 0.5 * (T[i + j * nc] + T[j + i * nc]);
+  std::vector<double> u_(ZEtb_h, ZEtb_h + nc);
+  trsv_upper_t(nc, R_h, u_.data());
+  const double* P_h = P_.data();
+  const double* Q2_h = Q2_.data();
+  const double* u_h = u_.data();
+  const double* v_h = Ktb_h;
+  std::vector<double> G((size_t)nc * nc), q(nc);
+  for (int l = 0; l < m; ++l) {
+    const double d = gamma_h[l] - gamma_star;
+    for (int j = 0; j < nc; ++j)
+      for (int i = 0; i < nc; ++i)
+        G[i + j * nc] = (i == j ? 1.0 : 0.0) + d * (P_h[i + j * nc] + P_h[j + i * nc]) +
+                        d * d * 0.5 * (Q2_h[i + j * nc] + Q2_h[j + i * nc]);
+    double* c = C_h + (size_t)l * nc;
+    if (!chol_lower(nc, G.data())) {
+      status_h[l] = RSK_NOT_SPD;
+      for (int i = 0; i < nc; ++i) c[i] = 0.0;
+      continue;
+    }
+    for (int i = 0; i < nc; ++i) q[i] = v_h[i] + d * u_h[i];
+    chol_solve_lower(nc, G.data(), q.data());
+    // c = R^-1 q (upper triangular back substitution)
+    for (int i = nc - 1; i >= 0; --i) {
+      double t = q[i];
+      for (int j = i + 1; j < nc; ++j) t -= R_h[i + j * nc] * c[j];
+      c[i] = t / R_h[i + i * nc];
+    }
+    status_h[l] = 0;
+  }
+  return RSK_OK;
+}
+
+extern "C" rsk_status rsk_pencil_ritz(int nc, const double* Ahat_h, const double* Ehat_h, double gamma,
+                                      int J, double* Wt_h, double* theta_h) {
+  if (nc <= 0 || J < 0 || J > nc || !Ahat_h || !Ehat_h || (J > 0 && (!Wt_h || !theta_h)) ||
+      !std::isfinite(gamma))
+    return RSK_EINVAL;
+  std::vector<double> H((size_t)nc * nc), th(nc), V((size_t)nc * nc);
+  for (int j = 0; j < nc; ++j)
+    for (int i = 0; i < nc; ++i)
+      H[i + j * nc] = 0.5 * (Ahat_h[i + j * nc] + Ahat_h[j + i * nc]) +
+                      gamma * 0.5 * (Ehat_h[i + j * nc] + Ehat_h[j + i * nc]);
+  jacobi_eig(nc, H.data(), th.data(), V.data());
+  for (int j = 0; j < J; ++j) {
+    theta_h[j] = th[j];
+    for (int i = 0; i < nc; ++i) Wt_h[i + j * nc] = V[i + j * nc];
+  }
+  return RSK_OK;
+}
+
+extern "C" rsk_status rsk_stabilize_small(int k, const double* R_h, const double* colnorm2_h,
+                                          double condcap, int cap, double* Zs_h, int* nkeep) {
+  if (k <= 0 || !R_h || !colnorm2_h || !Zs_h || !nkeep || !(condcap > 1.0)) return RSK_EINVAL;
+  std::vector<double> Rs((size_t)k * k), Ur((size_t)k * k), s(k), Vr((size_t)k * k);
+  for (int j = 0; j < k; ++j) {
+    if (!(colnorm2_h[j] > 0.0)) return RSK_EINVAL;
+    const double sc = 1.0 / std::sqrt(colnorm2_h[j]);
+    for (int i = 0; i < k; ++i) Rs[i + j * k] = R_h[i + j * k] * sc;
+  }
+  jacobi_svd(k, Rs.data(), Ur.data(), s.data(), Vr.data());
+  int nk = 0;
+  for (int i = 0; i < k; ++i)
+    if (s[i] > 0.0 && s[0] / s[i] < condcap) nk = i + 1; else break;
+  if (cap > 0 && nk > cap) nk = cap;
+  for (int j = 0; j < nk; ++j)
+    for (int i = 0; i < k; ++i) Zs_h[i + j * k] = Ur[i + j * k];
+  *nkeep = nk;
+  return RSK_OK;
+}
+
+extern "C" rsk_status rsk_carried_select(int m, const double* g2, const double* gh2, double thr,
+                                         double* scale_h, int* keep_h) {
+  if (m < 0 || (m > 0 && (!g2 || !gh2 || !scale_h || !keep_h))) return RSK_EINVAL;
+  for (int l = 0; l < m; ++l) {
+    const bool keep = g2[l] > 0.0 && gh2[l] > 0.0 && std::sqrt(gh2[l] / g2[l]) >= thr;
+    keep_h[l] = keep ? 1 : 0;
+    scale_h[l] = keep ? 1.0 / std::sqrt(gh2[l]) : 0.0;
+  }
+  return RSK_OK;
+}
+
+extern "C" rsk_status rsk_sym_eig(int n, const double* H_h, double* theta_h, double* V_h) {
+  if (n <= 0 || !H_h || !theta_h || !V_h) return RSK_EINVAL;
+  jacobi_eig(n, H_h, theta_h, V_h);
+  return RSK_OK;
+}
+
+extern "C" rsk_status rsk_svd_small(int k, const double* R_h, double* Ur_h, double* s_h, double* Vr_h) {
+  if (k <= 0 || !R_h || !Ur_h || !s_h || !Vr_h) return RSK_EINVAL;
+  jacobi_svd(k, R_h, Ur_h, s_h, Vr_h);
+  return RSK_OK;
+}
+
+extern "C" rsk_status rsk_chol_solve_small(int n, const double* G_h, int nrhs, const double* Z_h,
+                                           double* X_h) {
+  if (n <= 0 || nrhs < 0 || !G_h || !Z_h || !X_h) return RSK_EINVAL;
+  std::vector<double> L((size_t)n * n);
+  for (int j = 0; j < n; ++j)
+    for (int i = 0; i < n; ++i) L[i + j * n] = 0.5 * (G_h[i + j * n] + G_h[j + i * n]);
+  if (!chol_lower(n, L.data())) return RSK_EPARTIAL;
+  for (int c = 0; c < nrhs; ++c) {
+    std::memcpy(X_h + (size_t)c * n, Z_h + (size_t)c * n, sizeof(double) * n);
+    chol_solve_lower(n, L.data(), X_h + (size_t)c * n);
+  }
+  return RSK_OK;
+}
+
+extern "C" rsk_status rsk_lcurve_corner(int M, const double* rho_h, const double* eta_h, int* lstar,
+                                        double* kappa_h) {
+  if (M <= 0 || !rho_h || !eta_h || !lstar) return RSK_EINVAL;
+  std::vector<double> kap(M, -INFINITY);
+  for (int l = 1; l + 1 < M; ++l) {
+    const double a0 = std::log(rho_h[l - 1]), a1 = std::log(rho_h[l]), a2 = std::log(rho_h[l + 1]);
+    const double b0 = std::log(eta_h[l - 1]), b1 = std::log(eta_h[l]), b2 = std::log(eta_h[l + 1]);
+    const double r1 = 0.5 * (a2 - a0), e1 = 0.5 * (b2 - b0);
+    const double r2 = a2 - 2.0 * a1 + a0, e2 = b2 - 2.0 * b1 + b0;
+    const double den = std::pow(r1 * r1 + e1 * e1, 1.5);
+    kap[l] = den > 0 ? (r1 * e2 - r2 * e1) / den : -INFINITY;
+  }
+  int best = 0;
+  if (M >= 3) {
+    best = 1;
+    for (int l = 2; l + 1 < M; ++l)
+      if (kap[l] > kap[best]) best = l;
+  }
+  *lstar = best;
+  if (kappa_h)
+    for (int l = 0; l < M; ++l) kappa_h[l] = kap[l];
+  return RSK_OK;
+}

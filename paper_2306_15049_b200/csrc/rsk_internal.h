@@ -1,0 +1,156 @@
+// Internal declarations of librsk (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <string>
+#include <vector>
+
+#include "../../include/rsk.h"
+
+namespace rsk {
+
+constexpr int kMaxR = 12;                 // PSF half width supported by the fused apply
+constexpr int kMaxTaps = 4 * kMaxR + 1;   // taps of B = G^T G
+constexpr int kMaxM = RSK_MAX_LOCAL;      // local recycle dimension
+constexpr int kNT = 256;                  // threads per CTA for streaming kernels
+constexpr size_t kAuxBytes = sizeof(double) * (2 * 256 * 256 + 8192);
+
+// apply tile (output pixels per CTA)
+constexpr int kTY = 32;
+constexpr int kTX = 64;
+
+// ---- per-shift CG status on the device
+enum DevStatus : int {
+  ST_ACTIVE = 0,      // iterating
+  ST_RCONV = 1,       // recursive residual below tol: needs the true-residual confirm
+  ST_DONE = 2,        // confirmed
+  ST_BREAKDOWN = 3,
+  ST_MAXIT = 4,
+  ST_IDLE = 5         // not in this solve (ZERO_RHS, finished)
+};
+
+struct GroupPtrs {
+  const double* W[RSK_MAX_GROUPS];
+  const double* AW[RSK_MAX_GROUPS];
+  const double* EW[RSK_MAX_GROUPS];
+  int J[RSK_MAX_GROUPS];
+  int64_t ldw;
+};
+
+// Device-resident state of one rsk_cg_recycled_batch call (carved from ws).
+struct CgDev {
+  int nshift;
+  int64_t N;
+  double* R;        // residuals      N x nshift (ld N)
+  double* P;        // directions     N x nshift
+  double* Wv;       // A_g p / scratch N x nshift
+  double* X;        // caller x       (ldx)
+  int64_t ldx;
+  const double* b;
+  const double* Ghat;   // (ldgh) or null
+  const double* ZGhat;
+  int64_t ldgh;
+  double* store;    // residual store or null
+  int64_t lds;
+  int store_cap;
+  // scalars per shift
+  double* gam;      // gamma_s
+  double* rho;
+  double* alpha;
+  double* beta;
+  double* coef;     // [nshift][kMaxM]  mu (loop) or c (Galerkin start)
+  double* Lf;       // [nshift][kMaxM*kMaxM] Cholesky factor (lower, column-major)
+  double* rho_true; // true residual^2 at last confirm
+  int* status;
+  int* iters;
+  int* mloc;        // local dimension (after drops)
+  int* hasg;        // carried column present (after drops)
+  int* group;
+  int* store_cnt;
+  unsigned* cnt;    // [nshift][4] last-CTA counters
+  double* partA;    // [nshift][nblkA]
+  double* partB;    // [nshift][nblkB][kMaxM+1]
+  int nblkA;
+  int nblkB;
+  double bnorm;     // ||b||
+  double tol;
+  int maxit;
+  GroupPtrs grp;
+};
+
+// ---- handle
+struct Handle {
+  int device = 0;
+  int64_t ny = 0, nx = 0;
+  int r = 0;
+  double u[2 * kMaxR + 1];    // PSF column factor (rows, y)
+  double v[2 * kMaxR + 1];    // PSF row factor (cols, x)
+  double cBx[kMaxTaps], cBy[kMaxTaps];      // interior taps of B = G^T G
+  double cCx[kMaxTaps], cCy[kMaxTaps];      // taps of C   (window form)
+  double cTx[kMaxTaps], cTy[kMaxTaps];      // taps of C^T (window form)
+  double* tabBx = nullptr;    // [nx][4r+1]
+  double* tabBy = nullptr;    // [ny][4r+1]
+  double* wx = nullptr;       // weights copy
+  double* wy = nullptr;
+  double* scratch = nullptr;  // reduction scratch
+  size_t scratch_bytes = 0;
+  double* scal = nullptr;     // small device scalars
+  double* aux = nullptr;      // small device buffers for host-driven helpers (kAuxBytes)
+  int64_t nA = 0, nE = 0, nC = 0;
+  std::string err;
+  int sm_count = 148;
+  bool sticky = false;
+};
+
+// ---- launchers (apply.cu)
+struct ApplyLaunch {
+  const double* X; int64_t ldx;
+  double* Y; int64_t ldy;
+  double* EY; int64_t ldey;
+  const double* gamma;        // indexed by shift id
+  const int* list;            // device list of shift ids (nullable => identity)
+  int nlist;
+  int mode;                   // RSK_APPLY_*
+  double* xdoty;              // nullable, indexed by shift id
+  CgDev* cg;                  // nullable => plain apply; else CG "w = A p" step
+  bool cg_alpha;              // CG: compute alpha = rho / (p.w) in last CTA
+};
+cudaError_t launch_apply(Handle* h, const ApplyLaunch& a, cudaStream_t st);
+int apply_tiles(const Handle* h);
+
+// ---- vector kernels (vec.cu)
+cudaError_t launch_gemm_tn(Handle* h, int64_t n, int k, const double* U, int64_t ldu, int nv,
+                           const double* V, int64_t ldv, double* C, int64_t ldc, cudaStream_t st);
+cudaError_t launch_gemm_nn(Handle* h, int64_t n, int k, const double* U, int64_t ldu, int nv,
+                           double* V, int64_t ldv, const double* C, int64_t ldc, double sign,
+                           cudaStream_t st);
+cudaError_t launch_batch_dot(Handle* h, int64_t n, int nv, const double* X, int64_t ldx,
+                             const double* Y, int64_t ldy, double* out, cudaStream_t st);
+cudaError_t launch_batch_axpby(int64_t n, int nv, const double* a, const double* X,
+                               int64_t ldx, const double* b, double* Y, int64_t ldy,
+                               cudaStream_t st);  // a, b DEVICE arrays (b nullable)
+cudaError_t launch_irn(Handle* h, const double* x, double tau, double* wx, double* wy,
+                       double* eta2, cudaStream_t st);
+cudaError_t launch_seminorm_batch(Handle* h, int nvec, const double* X, int64_t ldx,
+                                  double* eta2, cudaStream_t st, int do_sqrt = 0);
+cudaError_t launch_diffnorm_batch(Handle* h, int nvec, const double* Y, int64_t ldy,
+                                  const double* d, double* out, cudaStream_t st);
+cudaError_t launch_scale_noise(int64_t n, const double* cx, const double* xi, const double* s2,
+                               double nu, double* d, cudaStream_t st);
+
+// CG kernels (vec.cu)
+enum UpdMode { UPD_LOOP = 0, UPD_START = 1, UPD_GALERKIN = 2, UPD_CONFIRM = 3 };
+cudaError_t launch_cg_update(CgDev* dev, const CgDev& host, const int* list, int nlist, int mode,
+                             cudaStream_t st);
+enum CmbMode { CMB_LOOP = 0, CMB_GALERKIN = 1, CMB_RESID = 2, CMB_GOUT = 3 };
+cudaError_t launch_cg_combine(CgDev* dev, const CgDev& host, const int* list, int nlist, int mode,
+                              cudaStream_t st);
+int cg_nblkB(int64_t N);
+
+// host dense (host_dense.cpp)
+bool chol_lower(int n, double* A);  // in-place, column-major lower; false if not SPD
+void chol_solve_lower(int n, const double* L, double* x);
+void jacobi_eig(int n, const double* H, double* theta, double* V);
+void jacobi_svd(int k, const double* R, double* Ur, double* s, double* Vr);
+
+}  // namespace rsk

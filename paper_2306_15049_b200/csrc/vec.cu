@@ -1,0 +1,604 @@
+// Streaming kernels of librsk: tall-skinny recycle projections (U^T V, V +- U C),
+// batched dots / axpby, the IRN weight update, L-curve norms, and the two CG
+// vector kernels (update + dots, combine). All fp64, all reductions deterministic
+// (fixed per-thread order, fixed shuffle tree, fixed-order sum of CTA partials).
+#include <cuda_runtime.h>
+
+#include "rsk_internal.h"
+
+namespace rsk {
+
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// ============================================================== projections
+// U^T V partials: CTA (chunk, k-tile, nv-tile) computes a 32 x 32 block of
+// U[rows of chunk]^T V[rows of chunk]; part[chunk][k][nv] (column-major k x nv).
+__global__ void __launch_bounds__(256) gemm_tn_part(int64_t n, int k, const double* __restrict__ U,
+                                                    int64_t ldu, int nv, const double* __restrict__ V,
+                                                    int64_t ldv, double* __restrict__ part,
+                                                    int64_t rows_per_chunk) {
+  __shared__ double sU[32][33];
+  __shared__ double sV[32][33];
+  const int chunk = blockIdx.x;
+  const int kt = blockIdx.y * 32, vt = blockIdx.z * 32;
+  const int64_t rbeg = (int64_t)chunk * rows_per_chunk;
+  const int64_t rend = min(n, rbeg + rows_per_chunk);
+  const int tid = threadIdx.x;
+  const int i0 = (tid >> 4) * 2, j0 = (tid & 15) * 2;
+  double acc00 = 0, acc01 = 0, acc10 = 0, acc11 = 0;
+  for (int64_t r0 = rbeg; r0 < rend; r0 += 32) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int idx = tid + e * 256;
+      const int row = idx & 31, col = idx >> 5;
+      const int64_t gr = r0 + row;
+      const bool rin = gr < rend;
+      sU[col][row] = (rin && kt + col < k) ? __ldg(U + gr + (int64_t)(kt + col) * ldu) : 0.0;
+      sV[col][row] = (rin && vt + col < nv) ? __ldg(V + gr + (int64_t)(vt + col) * ldv) : 0.0;
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int rr = 0; rr < 32; ++rr) {
+      const double u0 = sU[i0][rr], u1 = sU[i0 + 1][rr];
+      const double v0 = sV[j0][rr], v1 = sV[j0 + 1][rr];
+      acc00 = fma(u0, v0, acc00);
+      acc01 = fma(u0, v1, acc01);
+      acc10 = fma(u1, v0, acc10);
+      acc11 = fma(u1, v1, acc11);
+    }
+    __syncthreads();
+  }
+  double* pc = part + (int64_t)chunk * k * nv;
+  const int gi = kt + i0, gj = vt + j0;
+  if (gi < k && gj < nv) pc[gi + (int64_t)gj * k] = acc00;
+  if (gi < k && gj + 1 < nv) pc[gi + (int64_t)(gj + 1) * k] = acc01;
+  if (gi + 1 < k && gj < nv) pc[gi + 1 + (int64_t)gj * k] = acc10;
+  if (gi + 1 < k && gj + 1 < nv) pc[gi + 1 + (int64_t)(gj + 1) * k] = acc11;
+}
+
+__global__ void gemm_tn_reduce(int k, int nv, int nchunk, const double* __restrict__ part,
+                               double* __restrict__ C, int64_t ldc) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)k * nv) return;
+  double t = 0.0;
+  for (int c = 0; c < nchunk; ++c) t += part[(int64_t)c * k * nv + idx];
+  const int i = (int)(idx % k), j = (int)(idx / k);
+  C[i + (int64_t)j * ldc] = t;
+}
+
+cudaError_t launch_gemm_tn(Handle* h, int64_t n, int k, const double* U, int64_t ldu, int nv,
+                           const double* V, int64_t ldv, double* C, int64_t ldc, cudaStream_t st) {
+  const int tk = (k + 31) / 32, tv = (nv + 31) / 32;
+  int64_t nchunk = (2 * h->sm_count + tk * tv - 1) / (tk * tv);
+  const int64_t maxchunk = (n + 255) / 256;
+  if (nchunk > maxchunk) nchunk = maxchunk;
+  if (nchunk < 1) nchunk = 1;
+  const size_t cap = h->scratch_bytes / (sizeof(double) * (size_t)k * nv);
+  if ((size_t)nchunk > cap) nchunk = (int64_t)cap;
+  if (nchunk < 1) return cudaErrorMemoryAllocation;
+  int64_t rpc = (n + nchunk - 1) / nchunk;
+  rpc = (rpc + 31) / 32 * 32;
+  nchunk = (n + rpc - 1) / rpc;
+  dim3 grid((unsigned)nchunk, tk, tv);
+  gemm_tn_part<<<grid, 256, 0, st>>>(n, k, U, ldu, nv, V, ldv, h->scratch, rpc);
+  const int64_t tot = (int64_t)k * nv;
+  gemm_tn_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(k, nv, (int)nchunk, h->scratch, C, ldc);
+  return cudaGetLastError();
+}
+
+// V (n x nv) += sign * U (n x k) C (k x nv). CTA: 64 rows x 32 cols of V.
+__global__ void __launch_bounds__(256) gemm_nn_kernel(int64_t n, int k, const double* __restrict__ U,
+                                                      int64_t ldu, int nv, double* __restrict__ V,
+                                                      int64_t ldv, const double* __restrict__ C,
+                                                      int64_t ldc, double sign) {
+  __shared__ double sU[16][65];
+  __shared__ double sC[16][33];
+  const int tid = threadIdx.x;
+  const int64_t row0 = (int64_t)blockIdx.x * 64;
+  const int col0 = blockIdx.y * 32;
+  const int r = tid & 63;
+  const int jb = (tid >> 6) * 8;
+  double acc[8];
+#pragma unroll
+  for (int c = 0; c < 8; ++c) acc[c] = 0.0;
+  for (int k0 = 0; k0 < k; k0 += 16) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int idx = tid + e * 256;
+      const int rr = idx & 63, kk = idx >> 6;
+      const int64_t gr = row0 + rr;
+      sU[kk][rr] = (gr < n && k0 + kk < k) ? __ldg(U + gr + (int64_t)(k0 + kk) * ldu) : 0.0;
+    }
+    for (int idx = tid; idx < 16 * 32; idx += 256) {
+      const int kk = idx & 15, cc = idx >> 4;
+      sC[kk][cc] = (k0 + kk < k && col0 + cc < nv) ? __ldg(C + (k0 + kk) + (int64_t)(col0 + cc) * ldc) : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      const double u = sU[kk][r];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) acc[c] = fma(u, sC[kk][jb + c], acc[c]);
+    }
+    __syncthreads();
+  }
+  const int64_t gr = row0 + r;
+  if (gr >= n) return;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    const int gc = col0 + jb + c;
+    if (gc < nv) {
+      double* pv = V + gr + (int64_t)gc * ldv;
+      *pv = fma(sign, acc[c], *pv);
+    }
+  }
+}
+
+cudaError_t launch_gemm_nn(Handle* h, int64_t n, int k, const double* U, int64_t ldu, int nv,
+                           double* V, int64_t ldv, const double* C, int64_t ldc, double sign,
+                           cudaStream_t st) {
+  (void)h;
+  dim3 grid((unsigned)((n + 63) / 64), (nv + 31) / 32);
+  gemm_nn_kernel<<<grid, 256, 0, st>>>(n, k, U, ldu, nv, V, ldv, C, ldc, sign);
+  return cudaGetLastError();
+}
+
+// ============================================================== batched BLAS-1
+constexpr int kChunk = 2048;   // pixels per CTA for the streaming reductions
+
+__global__ void reduce_partials(const double* __restrict__ part, int nchunk, double* out,
+                                int do_sqrt) {
+  const int s = blockIdx.x;
+  double t = 0.0;
+  for (int j = threadIdx.x; j < nchunk; j += 32) t += part[(int64_t)s * nchunk + j];
+  t = wsum(t);
+  if (threadIdx.x == 0) out[s] = do_sqrt ? sqrt(t) : t;
+}
+
+__device__ __forceinline__ void block_partial(double v, double* red, double* dst) {
+  v = wsum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  if (wid == 0) {
+    double t = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.0;
+    t = wsum(t);
+    if (lane == 0) *dst = t;
+  }
+}
+
+__global__ void __launch_bounds__(256) dot_part(int64_t n, const double* __restrict__ X, int64_t ldx,
+                                                const double* __restrict__ Y, int64_t ldy,
+                                                double* __restrict__ part, int nchunk) {
+  __shared__ double red[8];
+  const int s = blockIdx.y;
+  const double* x = X + (int64_t)s * ldx;
+  const double* y = Y + (int64_t)s * ldy;
+  const int64_t base = (int64_t)blockIdx.x * kChunk;
+  double t = 0.0;
+#pragma unroll
+  for (int e = 0; e < kChunk / 256; ++e) {
+    const int64_t i = base + e * 256 + threadIdx.x;
+    if (i < n) t = fma(__ldg(x + i), __ldg(y + i), t);
+  }
+  block_partial(t, red, part + (int64_t)s * nchunk + blockIdx.x);
+}
+
+cudaError_t launch_batch_dot(Handle* h, int64_t n, int nv, const double* X, int64_t ldx,
+                             const double* Y, int64_t ldy, double* out, cudaStream_t st) {
+  const int nchunk = (int)((n + kChunk - 1) / kChunk);
+  if (sizeof(double) * (size_t)nchunk * nv > h->scratch_bytes) return cudaErrorMemoryAllocation;
+  dot_part<<<dim3(nchunk, nv), 256, 0, st>>>(n, X, ldx, Y, ldy, h->scratch, nchunk);
+  reduce_partials<<<nv, 32, 0, st>>>(h->scratch, nchunk, out, 0);
+  return cudaGetLastError();
+}
+
+__global__ void axpby_kernel(int64_t n, const double* __restrict__ a, const double* __restrict__ X,
+                             int64_t ldx, const double* __restrict__ b, double* __restrict__ Y,
+                             int64_t ldy) {
+  const int s = blockIdx.y;
+  const double as = a ? a[s] : 0.0;
+  const double bs = b ? b[s] : 1.0;
+  double* y = Y + (int64_t)s * ldy;
+  const double* x = X ? X + (int64_t)s * ldx : nullptr;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const double xv = x ? x[i] : 0.0;
+    y[i] = fma(as, xv, bs * y[i]);
+  }
+}
+
+cudaError_t launch_batch_axpby(int64_t n, int nv, const double* a, const double* X, int64_t ldx,
+                               const double* b, double* Y, int64_t ldy, cudaStream_t st) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 1184) blocks = 1184;
+  axpby_kernel<<<dim3((unsigned)blocks, nv), 256, 0, st>>>(n, a, X, ldx, b, Y, ldy);
+  return cudaGetLastError();
+}
+
+// ============================================================== IRN weights
+// wx = ((Dx x)^2 + tau^2)^(-1/2), wy likewise; eta2 partials under the handle weights.
+__global__ void __launch_bounds__(256) irn_kernel(int ny, int nx, const double* __restrict__ x,
+                                                  double tau, double* __restrict__ wx,
+                                                  double* __restrict__ wy,
+                                                  const double* __restrict__ hwx,
+                                                  const double* __restrict__ hwy,
+                                                  double* __restrict__ part) {
+  __shared__ double red[8];
+  const int64_t N = (int64_t)ny * nx;
+  const int64_t base = (int64_t)blockIdx.x * kChunk;
+  const double t2 = tau * tau;
+  double acc = 0.0;
+  for (int e = 0; e < kChunk / 256; ++e) {
+    const int64_t p = base + e * 256 + threadIdx.x;
+    if (p >= N) break;
+    const int i = (int)(p / nx), j = (int)(p - (int64_t)i * nx);
+    const double xc = x[p];
+    double dx = 0.0, dy = 0.0;
+    const bool hx = j < nx - 1, hy = i < ny - 1;
+    if (hx) dx = x[p + 1] - xc;
+    if (hy) dy = x[p + nx] - xc;
+    if (wx) {
+      wx[p] = hx ? 1.0 / sqrt(fma(dx, dx, t2)) : 0.0;
+      wy[p] = hy ? 1.0 / sqrt(fma(dy, dy, t2)) : 0.0;
+    }
+    if (part) acc += hwx[p] * dx * dx + hwy[p] * dy * dy;
+  }
+  if (part) block_partial(acc, red, part + blockIdx.x);
+}
+
+cudaError_t launch_irn(Handle* h, const double* x, double tau, double* wx, double* wy,
+                       double* eta2, cudaStream_t st) {
+  const int64_t N = h->ny * h->nx;
+  const int nchunk = (int)((N + kChunk - 1) / kChunk);
+  irn_kernel<<<nchunk, 256, 0, st>>>((int)h->ny, (int)h->nx, x, tau, wx, wy, h->wx, h->wy,
+                                     eta2 ? h->scratch : nullptr);
+  if (eta2) reduce_partials<<<1, 32, 0, st>>>(h->scratch, nchunk, eta2, 0);
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(256) seminorm_part(int ny, int nx, const double* __restrict__ X,
+                                                     int64_t ldx, const double* __restrict__ hwx,
+                                                     const double* __restrict__ hwy,
+                                                     double* __restrict__ part, int nchunk) {
+  __shared__ double red[8];
+  const int s = blockIdx.y;
+  const double* x = X + (int64_t)s * ldx;
+  const int64_t N = (int64_t)ny * nx;
+  const int64_t base = (int64_t)blockIdx.x * kChunk;
+  double acc = 0.0;
+  for (int e = 0; e < kChunk / 256; ++e) {
+    const int64_t p = base + e * 256 + threadIdx.x;
+    if (p >= N) break;
+    const int i = (int)(p / nx), j = (int)(p - (int64_t)i * nx);
+    const double xc = x[p];
+    const double dx = j < nx - 1 ? x[p + 1] - xc : 0.0;
+    const double dy = i < ny - 1 ? x[p + nx] - xc : 0.0;
+    acc += hwx[p] * dx * dx + hwy[p] * dy * dy;
+  }
+  block_partial(acc, red, part + (int64_t)s * nchunk + blockIdx.x);
+}
+
+cudaError_t launch_seminorm_batch(Handle* h, int nvec, const double* X, int64_t ldx, double* eta2,
+                                  cudaStream_t st, int do_sqrt) {
+  const int64_t N = h->ny * h->nx;
+  const int nchunk = (int)((N + kChunk - 1) / kChunk);
+  if (sizeof(double) * (size_t)nchunk * nvec > h->scratch_bytes) return cudaErrorMemoryAllocation;
+  seminorm_part<<<dim3(nchunk, nvec), 256, 0, st>>>((int)h->ny, (int)h->nx, X, ldx, h->wx, h->wy,
+                                                    h->scratch, nchunk);
+  reduce_partials<<<nvec, 32, 0, st>>>(h->scratch, nchunk, eta2, do_sqrt);
+  return cudaGetLastError();
+}
+
+__global__ void __launch_bounds__(256) diffnorm_part(int64_t n, const double* __restrict__ Y,
+                                                     int64_t ldy, const double* __restrict__ d,
+                                                     double* __restrict__ part, int nchunk) {
+  __shared__ double red[8];
+  const int s = blockIdx.y;
+  const double* y = Y + (int64_t)s * ldy;
+  const int64_t base = (int64_t)blockIdx.x * kChunk;
+  double acc = 0.0;
+  for (int e = 0; e < kChunk / 256; ++e) {
+    const int64_t i = base + e * 256 + threadIdx.x;
+    if (i < n) {
+      const double t = y[i] - d[i];
+      acc = fma(t, t, acc);
+    }
+  }
+  block_partial(acc, red, part + (int64_t)s * nchunk + blockIdx.x);
+}
+
+cudaError_t launch_diffnorm_batch(Handle* h, int nvec, const double* Y, int64_t ldy, const double* d,
+                                  double* out, cudaStream_t st) {
+  const int64_t N = h->ny * h->nx;
+  const int nchunk = (int)((N + kChunk - 1) / kChunk);
+  if (sizeof(double) * (size_t)nchunk * nvec > h->scratch_bytes) return cudaErrorMemoryAllocation;
+  diffnorm_part<<<dim3(nchunk, nvec), 256, 0, st>>>(N, Y, ldy, d, h->scratch, nchunk);
+  reduce_partials<<<nvec, 32, 0, st>>>(h->scratch, nchunk, out, 1);
+  return cudaGetLastError();
+}
+
+// d = cx + nu * sqrt(s2[0]) / sqrt(s2[1]) * xi  (s2 = {||cx||^2, ||xi||^2} on device)
+__global__ void scale_noise_kernel(int64_t n, const double* __restrict__ cx,
+                                   const double* __restrict__ xi, const double* __restrict__ s2,
+                                   double nu, double* __restrict__ d) {
+  const double sc = nu * sqrt(s2[0]) / sqrt(s2[1]);
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    d[i] = fma(sc, xi[i], cx[i]);
+}
+
+cudaError_t launch_scale_noise(int64_t n, const double* cx, const double* xi, const double* s2,
+                               double nu, double* d, cudaStream_t st) {
+  int64_t blocks = (n + 255) / 256;
+  if (blocks > 1184) blocks = 1184;
+  scale_noise_kernel<<<(unsigned)blocks, 256, 0, st>>>(n, cx, xi, s2, nu, d);
+  return cudaGetLastError();
+}
+
+// ============================================================== CG vector kernels
+constexpr int kCgPPT = 8;                 // pixels per thread
+constexpr int kCgChunk = kCgPPT * kNT;    // 2048 pixels per CTA
+
+int cg_nblkB(int64_t N) { return (int)((N + kCgChunk - 1) / kCgChunk); }
+
+// Solve L L^T x = z in place (L lower, column-major m x m, m <= kMaxM).
+__device__ void dev_chol_solve(int m, const double* L, double* x) {
+  for (int i = 0; i < m; ++i) {
+    double t = x[i];
+    for (int j = 0; j < i; ++j) t -= L[i + j * kMaxM] * x[j];
+    x[i] = t / L[i + i * kMaxM];
+  }
+  for (int i = m - 1; i >= 0; --i) {
+    double t = x[i];
+    for (int j = i + 1; j < m; ++j) t -= L[j + i * kMaxM] * x[j];
+    x[i] = t / L[i + i * kMaxM];
+  }
+}
+
+// KB: r -= alpha w (LOOP), then rho' = r.r and z = Z^T r (or U^T r for GALERKIN);
+// last CTA of the shift reduces the partials in fixed order and forms the scalars.
+__global__ void __launch_bounds__(kNT) cg_update_kernel(CgDev* __restrict__ cg, const int* list,
+                                                        int mode) {
+  __shared__ double red[8][kMaxM + 1];
+  __shared__ double tot[kMaxM + 1];
+  __shared__ int s_last;
+  const int s = list[blockIdx.y];
+  const int st0 = cg->status[s];
+  if (mode == UPD_LOOP) {
+    if (st0 != ST_ACTIVE) return;
+  } else if (st0 == ST_IDLE || st0 == ST_BREAKDOWN || st0 == ST_MAXIT || st0 == ST_DONE) {
+    return;
+  }
+  const int64_t N = cg->N;
+  const int m = cg->mloc[s];
+  const int hasg = cg->hasg[s];
+  const int nw = m - hasg;          // W columns in use
+  const int g = cg->group[s];
+  const double gam = cg->gam[s];
+  const double alpha = (mode == UPD_LOOP) ? cg->alpha[s] : 0.0;
+  double* __restrict__ r = cg->R + (int64_t)s * N;
+  const double* __restrict__ w = cg->Wv + (int64_t)s * N;
+  const double* __restrict__ W = cg->grp.W[g];
+  const double* __restrict__ AW = cg->grp.AW[g];
+  const double* __restrict__ EW = cg->grp.EW[g];
+  const int64_t ldw = cg->grp.ldw;
+  const double* __restrict__ gh = hasg ? cg->Ghat + (int64_t)s * cg->ldgh : nullptr;
+  const double* __restrict__ zg = hasg ? cg->ZGhat + (int64_t)s * cg->ldgh : nullptr;
+  const bool galerkin = (mode == UPD_GALERKIN);
+
+  double acc[kMaxM + 1];
+#pragma unroll
+  for (int j = 0; j <= kMaxM; ++j) acc[j] = 0.0;
+  const int64_t base = (int64_t)blockIdx.x * kCgChunk;
+#pragma unroll 2
+  for (int e = 0; e < kCgPPT; ++e) {
+    const int64_t i = base + e * kNT + threadIdx.x;
+    if (i >= N) break;
+    double rv = r[i];
+    if (mode == UPD_LOOP) {
+      rv = fma(-alpha, w[i], rv);
+      r[i] = rv;
+    }
+    acc[0] = fma(rv, rv, acc[0]);
+#pragma unroll
+    for (int j = 0; j < kMaxM; ++j) {
+      if (j < nw) {
+        const double col = galerkin ? __ldg(W + i + (int64_t)j * ldw)
+                                    : fma(gam, __ldg(EW + i + (int64_t)j * ldw), __ldg(AW + i + (int64_t)j * ldw));
+        acc[1 + j] = fma(col, rv, acc[1 + j]);
+      } else if (j == nw && hasg) {
+        const double col = galerkin ? __ldg(gh + i) : __ldg(zg + i);
+        acc[1 + j] = fma(col, rv, acc[1 + j]);
+      }
+    }
+  }
+  // block reduction of the m+1 values (fixed tree)
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+#pragma unroll
+  for (int j = 0; j <= kMaxM; ++j) {
+    if (j <= m) {
+      const double v = wsum(acc[j]);
+      if (lane == 0) red[wid][j] = v;
+    }
+  }
+  __syncthreads();
+  const int nblk = gridDim.x;
+  double* pb = cg->partB + ((int64_t)s * cg->nblkB + blockIdx.x) * (kMaxM + 1);
+  if (threadIdx.x <= m) {
+    double t = 0.0;
+#pragma unroll
+    for (int q = 0; q < kNT / 32; ++q) t += red[q][threadIdx.x];
+    pb[threadIdx.x] = t;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    const unsigned tk = atomicAdd(cg->cnt + 4 * s + 1, 1u);
+    s_last = (tk == (unsigned)(nblk - 1));
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (threadIdx.x <= m) {
+    const double* p0 = cg->partB + (int64_t)s * cg->nblkB * (kMaxM + 1);
+    double t = 0.0;
+    for (int bq = 0; bq < nblk; ++bq) t += __ldcg(p0 + (int64_t)bq * (kMaxM + 1) + threadIdx.x);
+    tot[threadIdx.x] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x != 0) return;
+  cg->cnt[4 * s + 1] = 0u;
+  double z[kMaxM];
+  for (int j = 0; j < m; ++j) z[j] = tot[1 + j];
+  if (m > 0) dev_chol_solve(m, cg->Lf + (int64_t)s * kMaxM * kMaxM, z);
+  double* cf = cg->coef + (int64_t)s * kMaxM;
+  for (int j = 0; j < kMaxM; ++j) cf[j] = j < m ? z[j] : 0.0;
+  if (galerkin) return;
+  const double rho_new = tot[0];
+  const double thr = cg->tol * cg->bnorm;
+  const bool conv = sqrt(rho_new) <= thr;
+  if (mode == UPD_LOOP) {
+    const int it = cg->iters[s] + 1;
+    cg->iters[s] = it;
+    cg->beta[s] = rho_new / cg->rho[s];
+    cg->rho[s] = rho_new;
+    if (conv) cg->status[s] = ST_RCONV;
+    else if (it >= cg->maxit) cg->status[s] = ST_MAXIT;
+  } else {
+    cg->beta[s] = 0.0;
+    cg->alpha[s] = 0.0;
+    cg->rho[s] = rho_new;
+    if (mode == UPD_CONFIRM) {
+      cg->rho_true[s] = rho_new;
+      cg->status[s] = conv ? ST_DONE : (cg->iters[s] >= cg->maxit ? ST_MAXIT : ST_ACTIVE);
+    } else {
+      cg->status[s] = conv ? ST_RCONV : ST_ACTIVE;
+    }
+  }
+}
+
+cudaError_t launch_cg_update(CgDev* dev, const CgDev& host, const int* list, int nlist, int mode,
+                             cudaStream_t st) {
+  if (nlist <= 0) return cudaSuccess;
+  dim3 grid(host.nblkB, nlist);
+  cg_update_kernel<<<grid, kNT, 0, st>>>(dev, list, mode);
+  return cudaGetLastError();
+}
+
+// KC: LOOP: x += alpha p; p = r + beta p - U mu; store r/||r||.
+//     GALERKIN: x += U c; r -= Z c.    RESID: r = b - w.
+__global__ void __launch_bounds__(kNT) cg_combine_kernel(CgDev* __restrict__ cg, const int* list,
+                                                         int mode) {
+  __shared__ int s_last;
+  const int s = list[blockIdx.y];
+  const int st0 = cg->status[s];
+  const int64_t N = cg->N;
+  double* __restrict__ x = cg->X + (int64_t)s * cg->ldx;
+  double* __restrict__ r = cg->R + (int64_t)s * N;
+  const int64_t base = (int64_t)blockIdx.x * kCgChunk;
+  if (mode == CMB_RESID) {
+    if (st0 == ST_IDLE) return;
+    const double* __restrict__ w = cg->Wv + (int64_t)s * N;
+    for (int e = 0; e < kCgPPT; ++e) {
+      const int64_t i = base + e * kNT + threadIdx.x;
+      if (i >= N) break;
+      r[i] = __ldg(cg->b + i) - w[i];
+    }
+    return;
+  }
+  const int m = cg->mloc[s];
+  const int hasg = cg->hasg[s];
+  const int nw = m - hasg;
+  const int g = cg->group[s];
+  const double gam = cg->gam[s];
+  const double* __restrict__ W = cg->grp.W[g];
+  const double* __restrict__ AW = cg->grp.AW[g];
+  const double* __restrict__ EW = cg->grp.EW[g];
+  const int64_t ldw = cg->grp.ldw;
+  const double* __restrict__ gh = hasg ? cg->Ghat + (int64_t)s * cg->ldgh : nullptr;
+  const double* __restrict__ zg = hasg ? cg->ZGhat + (int64_t)s * cg->ldgh : nullptr;
+  double cf[kMaxM];
+#pragma unroll
+  for (int j = 0; j < kMaxM; ++j) cf[j] = cg->coef[(int64_t)s * kMaxM + j];
+
+  if (mode == CMB_GALERKIN) {
+    if (m == 0 || st0 == ST_IDLE) return;
+    for (int e = 0; e < kCgPPT; ++e) {
+      const int64_t i = base + e * kNT + threadIdx.x;
+      if (i >= N) break;
+      double xv = x[i], rv = r[i];
+#pragma unroll
+      for (int j = 0; j < kMaxM; ++j) {
+        if (j < nw) {
+          xv = fma(cf[j], __ldg(W + i + (int64_t)j * ldw), xv);
+          const double zc = fma(gam, __ldg(EW + i + (int64_t)j * ldw), __ldg(AW + i + (int64_t)j * ldw));
+          rv = fma(-cf[j], zc, rv);
+        } else if (j == nw && hasg) {
+          xv = fma(cf[j], __ldg(gh + i), xv);
+          rv = fma(-cf[j], __ldg(zg + i), rv);
+        }
+      }
+      x[i] = xv;
+      r[i] = rv;
+    }
+    return;
+  }
+  // CMB_LOOP
+  const double alpha = cg->alpha[s];
+  if (st0 == ST_RCONV || st0 == ST_MAXIT) {
+    if (alpha == 0.0) return;       // the final x update has been applied already
+  } else if (st0 != ST_ACTIVE) {
+    return;
+  }
+  const bool upd_p = (st0 == ST_ACTIVE);
+  const double beta = cg->beta[s];
+  double* __restrict__ p = cg->P + (int64_t)s * N;
+  const bool do_store = upd_p && cg->store && cg->store_cnt[s] < cg->store_cap;
+  double* __restrict__ sto = do_store
+      ? cg->store + ((int64_t)s * cg->store_cap + cg->store_cnt[s]) * cg->lds : nullptr;
+  const double rinv = do_store ? 1.0 / sqrt(cg->rho[s]) : 0.0;
+  for (int e = 0; e < kCgPPT; ++e) {
+    const int64_t i = base + e * kNT + threadIdx.x;
+    if (i >= N) break;
+    const double pv = p[i];
+    x[i] = fma(alpha, pv, x[i]);
+    if (upd_p) {
+      const double rv = r[i];
+      double pn = fma(beta, pv, rv);
+#pragma unroll
+      for (int j = 0; j < kMaxM; ++j) {
+        if (j < nw) pn = fma(-cf[j], __ldg(W + i + (int64_t)j * ldw), pn);
+        else if (j == nw && hasg) pn = fma(-cf[j], __ldg(gh + i), pn);
+      }
+      p[i] = pn;
+      if (do_store) sto[i] = rv * rinv;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned tk = atomicAdd(cg->cnt + 4 * s + 2, 1u);
+    s_last = (tk == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (s_last && threadIdx.x == 0) {
+    cg->cnt[4 * s + 2] = 0u;
+    cg->alpha[s] = 0.0;
+    if (do_store) cg->store_cnt[s] += 1;
+  }
+}
+
+cudaError_t launch_cg_combine(CgDev* dev, const CgDev& host, const int* list, int nlist, int mode,
+                              cudaStream_t st) {
+  if (nlist <= 0) return cudaSuccess;
+  dim3 grid(host.nblkB, nlist);
+  cg_combine_kernel<<<grid, kNT, 0, st>>>(dev, list, mode);
+  return cudaGetLastError();
+}
+
+}  // namespace rsk

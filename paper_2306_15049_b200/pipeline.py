@@ -1,0 +1,302 @@
+"""The outer IRN loop of Alg. 5 on the B200, driving librsk.
+
+Orchestration only: every arithmetic step on data is a librsk call (device
+kernels, or the host small-dense helpers of include/rsk.h). torch provides
+memory (fp64 CUDA tensors), streams and copies. The readings of the paper
+(D1-D4, G1-G29) are the ones listed in DESIGN.md and followed by the oracle.
+
+One outer step k:
+  1. k = 0: seed solves at gamma_i1, gamma_i2 (plain CG with a residual store)
+     and Rayleigh-Ritz spaces V_i1, V_i2 (§5.1)
+     k >= 1: raw block [V_i1, x^(k-1,1..M)] (eq:tildeUupdate P:654, reading G10)
+  2. stabilize (Alg. 1): shifted Cholesky-QR3 + Jacobi SVD of R
+  3. anchor (A + gamma_* E) U~ = K R (eq:establishU) and the Grams
+  4. principal guesses x_0 = U~ C (eq:orthupdate)
+  5. group Ritz blocks W_g, A W_g, E W_g from the pencil (Alg. 2/4)
+  6. carried corrections g-hat (Alg. 3, reading D3) and their images
+  7. batched deflated CG over all shifts (rsk_cg_recycled_batch)
+  8. L-curve corner and the IRN weights of x* (north_star)
+"""
+from __future__ import annotations
+
+import dataclasses
+import math
+import time
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from .rsk import (Handle, carried_select, lcurve_corner, orth_guess, pencil_ritz,
+                  stabilize_small, sym_eig)
+
+COND_CAP = 1e10
+DUP_SIN = math.sqrt(1.0 - 0.999 ** 2)
+STORE_CAP = 100
+
+
+@dataclasses.dataclass
+class StepOut:
+    k: int
+    iters: np.ndarray
+    applies: np.ndarray
+    status: np.ndarray
+    relres: np.ndarray
+    m_used: np.ndarray
+    nc: int
+    lstar: int
+    rho: np.ndarray
+    eta: np.ndarray
+    overhead_applies: int
+    has_xp: np.ndarray
+    keep_ghat: np.ndarray | None
+    ms: float = 0.0
+    prof: np.ndarray | None = None
+
+
+def _host(t: torch.Tensor) -> np.ndarray:
+    return t.detach().cpu().numpy()
+
+
+class GpuSolver:
+    """All device state of one configuration (one image grid, one PSF, M shifts)."""
+
+    def __init__(self, cfg, psf: np.ndarray, gamma: np.ndarray, device: int = 0,
+                 check_every: int = 8, profile: bool = False, stream=None):
+        torch.cuda.set_device(device)
+        self.dev = torch.device("cuda", device)
+        self.cfg = cfg
+        self.n, self.N, self.M = cfg.n, cfg.N, cfg.M
+        self.gamma = np.ascontiguousarray(gamma, dtype=np.float64)
+        self.h = Handle(cfg.n, cfg.n, psf, device)
+        self.check_every = check_every
+        self.profile = profile
+        self.stream = stream
+        f = dict(dtype=torch.float64, device=self.dev)
+        N, M = self.N, self.M
+        self.f = f
+        self.gam_dev = torch.from_numpy(self.gamma).to(self.dev)
+        self.b = torch.empty(N, **f)
+        self.d = torch.empty(N, **f)
+        w0 = torch.ones(self.n, self.n, **f)
+        w0[:, -1] = 0.0
+        self.w0x = w0.reshape(-1).contiguous()
+        self.w0y = w0.t().contiguous().reshape(-1).contiguous()
+        self.wx = torch.empty(N, **f)
+        self.wy = torch.empty(N, **f)
+        self.ws = torch.empty(self.h.cg_workspace_bytes(max(M, 2)), dtype=torch.uint8, device=self.dev)
+        self.lc_scratch = torch.empty(M, N, **f)
+        self.rho_dev = torch.empty(M, **f)
+        self.eta_dev = torch.empty(M, **f)
+        self.grp = np.array([0 if (l + 1) <= cfg.I_split else 1 for l in range(M)], dtype=np.int32)
+
+    # ------------------------------------------------------------------ data
+    def set_data(self, x_true: torch.Tensor, xi: torch.Tensor):
+        """d = C x_true + e, b = C^T d on the device (rsk_make_rhs)."""
+        self.h.make_rhs(x_true.reshape(-1), xi.reshape(-1), self.cfg.noise, self.d, self.b,
+                        stream=self.stream)
+
+    def reset_weights(self):
+        self.h.set_weights(self.w0x, self.w0y, stream=self.stream)
+
+    # ------------------------------------------------------------- building blocks
+    def cg(self, gammas_idx, X, has_xp, Gout=None, groups=None, ghat=None, store=None,
+           flags=0):
+        cfg = self.cfg
+        ns = len(gammas_idx)
+        gam = np.ascontiguousarray(self.gamma[gammas_idx])
+        d = L.CgDesc()
+        d.nshift = ns
+        d.gamma_h = gam.ctypes.data_as(L._hp)
+        d.b = self.b.data_ptr()
+        d.X = X.data_ptr(); d.ldx = self.N
+        hx = np.ascontiguousarray(has_xp, dtype=np.int32)
+        d.has_xp_h = hx.ctypes.data_as(L.C.POINTER(L.C.c_int))
+        d.Gout = Gout.data_ptr() if Gout is not None else None
+        d.ldg = self.N
+        keep = []
+        if groups is not None:
+            gos = np.ascontiguousarray(groups["of_shift"], dtype=np.int32)
+            keep.append(gos)
+            d.ngroups = len(groups["W"])
+            d.group_of_shift_h = gos.ctypes.data_as(L.C.POINTER(L.C.c_int))
+            for g in range(d.ngroups):
+                d.W[g] = groups["W"][g].data_ptr()
+                d.AW[g] = groups["AW"][g].data_ptr()
+                d.EW[g] = groups["EW"][g].data_ptr()
+                d.J[g] = groups["W"][g].shape[0]
+            d.ldw = self.N
+        else:
+            d.ngroups = 0
+            flags |= L.RSK_CG_NO_DEFLATION
+        if ghat is not None:
+            Gh, ZGh, hg = ghat
+            hg = np.ascontiguousarray(hg, dtype=np.int32)
+            keep.append(hg)
+            d.Ghat = Gh.data_ptr(); d.ZGhat = ZGh.data_ptr(); d.ldgh = self.N
+            d.has_ghat_h = hg.ctypes.data_as(L.C.POINTER(L.C.c_int))
+        if store is not None:
+            d.store = store.data_ptr(); d.lds = self.N; d.store_cap = STORE_CAP
+            flags |= L.RSK_CG_STORE_RES
+        if self.profile:
+            flags |= L.RSK_CG_PROFILE
+        d.tol = cfg.tol; d.maxit = cfg.maxit; d.check_every = self.check_every; d.flags = flags
+        out = L.CgOut()
+        iters = np.zeros(ns, dtype=np.int32); apl = np.zeros(ns, dtype=np.int64)
+        rel = np.zeros(ns); stt = np.zeros(ns, dtype=np.int32); mu = np.zeros(ns, dtype=np.int32)
+        sc = np.zeros(ns, dtype=np.int32); ms = np.zeros(4)
+        P = L.C.POINTER
+        out.iters = iters.ctypes.data_as(P(L.C.c_int)); out.applies = apl.ctypes.data_as(P(L.C.c_int64))
+        out.relres_true = rel.ctypes.data_as(L._hp); out.status = stt.ctypes.data_as(P(L.C.c_int))
+        out.m_used = mu.ctypes.data_as(P(L.C.c_int)); out.store_count = sc.ctypes.data_as(P(L.C.c_int))
+        out.ms_loop = ms.ctypes.data_as(L._hp)
+        self.h.cg_recycled_batch(d, out, self.ws, stream=self.stream)
+        return dict(iters=iters, applies=apl, relres=rel, status=stt, m_used=mu, store_count=sc, prof=ms)
+
+    def stabilize(self, raw: torch.Tensor, cap: int | None) -> torch.Tensor:
+        """Alg. 1 with column scaling (reading G6); zero columns are discarded."""
+        k = raw.shape[0]
+        nrm = torch.empty(k, **self.f)
+        self.h.batch_dot(raw, raw, nrm, stream=self.stream)
+        n2 = _host(nrm)
+        nz = np.nonzero(n2 > 0)[0]
+        V = raw[torch.from_numpy(nz).to(self.dev)].contiguous() if len(nz) < k else raw.clone()
+        Q = torch.empty_like(V)
+        R = self.h.qr_tall(V, Q, stream=self.stream)
+        Zs, nk = stabilize_small(R, n2[nz], COND_CAP, cap or 0)
+        Ut = torch.zeros(nk, self.N, **self.f)
+        Cm = torch.from_numpy(np.ascontiguousarray(Zs.T)).to(self.dev)
+        self.h.recycle_project(L.RSK_ADD_UC, Q, Ut, Cm, stream=self.stream)
+        return Ut
+
+    def utv(self, U, V):
+        Cm = torch.empty(V.shape[0] if V.dim() > 1 else 1, U.shape[0], **self.f)
+        self.h.recycle_project(L.RSK_PROJ_UTV, U, V, Cm, stream=self.stream)
+        return Cm
+
+    def combine(self, U, Cm_host_kxnv: np.ndarray) -> torch.Tensor:
+        """U (k, N) times the k x nv host matrix -> (nv, N) via ADD_UC into zeros."""
+        Cm = torch.from_numpy(np.ascontiguousarray(np.asarray(Cm_host_kxnv).T)).to(self.dev)
+        out = torch.zeros(Cm.shape[0], self.N, **self.f)
+        self.h.recycle_project(L.RSK_ADD_UC, U, out, Cm, stream=self.stream)
+        return out
+
+    def ritz(self, store_blk: torch.Tensor, gamma_idx: int, n_keep: int):
+        """Rayleigh-Ritz on a seed's stored residuals (reading G9)."""
+        Q = self.stabilize(store_blk, None)
+        q = Q.shape[0]
+        AQ = torch.empty_like(Q)
+        gq = self.gam_dev[gamma_idx].repeat(q).contiguous()
+        self.h.apply_shifted(Q, AQ, gamma=gq, stream=self.stream)
+        H = _host(self.utv(Q, AQ)).T          # q x q  (column-major view)
+        th, Z = sym_eig(H)
+        kk = min(n_keep, q)
+        return self.combine(Q, Z[:, :kk]), q
+
+    # ------------------------------------------------------------- one outer step
+    def outer_step(self, k: int, st: dict) -> tuple[StepOut, dict]:
+        cfg = self.cfg
+        N, M, nc_cap = self.N, self.M, cfg.n_c
+        t0 = time.perf_counter()
+        overhead = 0
+        i1, i2 = cfg.i1 - 1, cfg.i2 - 1
+        V_i1 = st.get("V_i1")
+        if k == 0:
+            n1 = math.ceil(2 * (nc_cap - 2) / 3)
+            n2 = nc_cap - 2 - n1
+            Xs = torch.empty(2, N, **self.f)
+            store = torch.empty(2 * STORE_CAP, N, **self.f)
+            rs = self.cg([i1, i2], Xs, [0, 0], store=store)
+            overhead += int(rs["applies"].sum())
+            c1, c2 = int(rs["store_count"][0]), int(rs["store_count"][1])
+            V_i1, q1 = self.ritz(store[:c1], i1, n1) if n1 > 0 and c1 > 0 else (Xs[:0], 0)
+            V_i2, q2 = self.ritz(store[STORE_CAP:STORE_CAP + c2], i2, n2) if n2 > 0 and c2 > 0 else (Xs[:0], 0)
+            overhead += q1 + q2
+            raw = torch.cat([Xs, V_i1, V_i2], 0)
+            del store
+        else:
+            raw = torch.cat([V_i1, st["X_prev"]], 0)
+        Ut = self.stabilize(raw, nc_cap)
+        nc = Ut.shape[0]
+        del raw
+        # ---- anchoring (eq:establishU) and Grams
+        ZA = torch.empty(nc, N, **self.f)
+        ZE = torch.empty(nc, N, **self.f)
+        self.h.apply_shifted(Ut, ZA, EY=ZE, mode=L.RSK_APPLY_SPLIT, stream=self.stream)
+        overhead += nc
+        gstar = float(self.gamma[cfg.istar - 1])
+        Y = ZA.clone()
+        self.h.batch_axpby(np.full(nc, gstar), ZE, None, Y, stream=self.stream)
+        K = torch.empty_like(Y)
+        R = self.h.qr_tall(Y, K, stream=self.stream)
+        del Y
+        KtZE = _host(self.utv(K, ZE)).T
+        ZEtZE = _host(self.utv(ZE, ZE)).T
+        ZEtb = _host(self.utv(ZE, self.b)).ravel()
+        Ktb = _host(self.utv(K, self.b)).ravel()
+        Ahat = _host(self.utv(Ut, ZA)).T
+        Ehat = _host(self.utv(Ut, ZE)).T
+        del K
+        # ---- principal guesses (eq:orthupdate)
+        Cg, gst = orth_guess(R, KtZE, ZEtZE, ZEtb, Ktb, gstar, self.gamma)
+        has_xp = (gst == 0).astype(np.int32)
+        X = self.combine(Ut, Cg)               # x_0 = U~ C   (zero where NOT_SPD)
+        # ---- group Ritz blocks (Alg. 2 / Alg. 4)
+        Wg, AWg, EWg = [], [], []
+        for jidx in (cfg.J_L - 1, cfg.J_R - 1):
+            Wt, _ = pencil_ritz(Ahat, Ehat, float(self.gamma[jidx]), min(cfg.J, nc))
+            Wg.append(self.combine(Ut, Wt)); AWg.append(self.combine(ZA, Wt)); EWg.append(self.combine(ZE, Wt))
+        del ZA, ZE
+        groups = dict(W=Wg, AW=AWg, EW=EWg, of_shift=self.grp)
+        # ---- carried corrections (Alg. 3, reading D3 / G12)
+        ghat = None
+        keep = None
+        if k >= 1 and st.get("G_prev") is not None:
+            Gp = st["G_prev"]
+            Gh = Gp.clone()
+            bounds = [(0, cfg.I_split), (cfg.I_split, M)]
+            for _ in range(2):
+                for g, (a, bnd) in enumerate(bounds):
+                    if bnd > a:
+                        cf = self.utv(Wg[g], Gh[a:bnd])
+                        self.h.recycle_project(L.RSK_SUB_UC, Wg[g], Gh[a:bnd], cf, stream=self.stream)
+            g2 = torch.empty(M, **self.f); gh2 = torch.empty(M, **self.f)
+            self.h.batch_dot(Gp, Gp, g2, stream=self.stream)
+            self.h.batch_dot(Gh, Gh, gh2, stream=self.stream)
+            scale, keep = carried_select(_host(g2), _host(gh2), DUP_SIN)
+            self.h.batch_axpby(np.zeros(M), None, scale, Gh, stream=self.stream)
+            ZGh = torch.empty_like(Gh)
+            self.h.apply_shifted(Gh, ZGh, gamma=self.gam_dev, stream=self.stream)
+            overhead += int(keep.sum())
+            ghat = (Gh, ZGh, keep)
+        # ---- batched deflated CG
+        G = torch.empty(M, N, **self.f)
+        res = self.cg(list(range(M)), X, has_xp, Gout=G, groups=groups, ghat=ghat)
+        # ---- L-curve and the next weights
+        self.h.lcurve_norms(X, self.d, self.rho_dev, self.eta_dev, self.lc_scratch, stream=self.stream)
+        rho, eta = _host(self.rho_dev), _host(self.eta_dev)
+        lstar, _ = lcurve_corner(rho, eta)
+        torch.cuda.synchronize(self.dev)
+        out = StepOut(k, res["iters"], res["applies"], res["status"], res["relres"], res["m_used"], nc,
+                      lstar, rho, eta, overhead, has_xp, keep, time.perf_counter() - t0, res["prof"])
+        nst = dict(X_prev=X, G_prev=G, V_i1=V_i1, xstar=X[lstar])
+        return out, nst
+
+    def next_weights(self, xstar: torch.Tensor):
+        """W_{k+1} from x* (north_star IRN rule, reading G2), adopted by the handle."""
+        self.h.irn_weights(xstar, self.cfg.tau, self.wx, self.wy, stream=self.stream)
+        self.h.set_weights(self.wx, self.wy, stream=self.stream)
+
+    def run(self, K_out: int | None = None):
+        """The whole nested solve: K_out outer steps from W_0 = I."""
+        self.reset_weights()
+        st: dict = {}
+        outs = []
+        K = K_out or self.cfg.K_out
+        for k in range(K):
+            o, st = self.outer_step(k, st)
+            outs.append(o)
+            if k + 1 < K:
+                self.next_weights(st["xstar"])
+        self.final = st
+        return outs

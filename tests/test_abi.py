@@ -1,0 +1,98 @@
+"""CPU-side checks of the boundary: librsk builds for sm_100a, loads, exports every
+symbol include/rsk.h declares, and the host-only helpers agree with closed forms."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+HDR = os.path.join(ROOT, "include", "rsk.h")
+
+
+def _declared():
+    txt = open(HDR).read()
+    return sorted(set(re.findall(r"^\s*(?:rsk_status|size_t|const char\*)\s+(rsk_\w+)\s*\(", txt, re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2306_15049_b200 import build
+    build.build()
+    from paper_2306_15049_b200 import _lib
+    return _lib.load()
+
+
+def test_every_declared_symbol_is_exported_and_bound(lib):
+    from paper_2306_15049_b200 import _lib
+    decl = _declared()
+    assert len(decl) >= 20
+    for name in decl:
+        assert hasattr(lib, name), name
+        assert name in _lib.EXPORTED, f"{name} has no ctypes signature"
+
+
+def test_sm100a_cubin_present():
+    import subprocess
+    so = os.path.join(ROOT, "paper_2306_15049_b200", "librsk.so")
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", so], capture_output=True, text=True)
+    assert "sm_100a" in out.stdout
+
+
+def test_version(lib):
+    assert b"sm_100a" in lib.rsk_version()
+
+
+def test_host_sym_eig_and_svd():
+    from paper_2306_15049_b200 import rsk
+    rng = np.random.default_rng(3)
+    A = rng.standard_normal((9, 9)); H = A + A.T
+    th, V = rsk.sym_eig(H)
+    np.testing.assert_allclose(th, np.linalg.eigvalsh(H), rtol=1e-12, atol=1e-12)
+    np.testing.assert_allclose(H @ V, V * th, atol=1e-11)
+    R = np.triu(rng.standard_normal((7, 7)))
+    U, s, Vt = rsk.svd_small(R)
+    np.testing.assert_allclose(s, np.linalg.svd(R, compute_uv=False), rtol=1e-12)
+    np.testing.assert_allclose(U @ np.diag(s) @ Vt.T, R, atol=1e-12)
+
+
+def test_host_orth_guess_matches_normal_equations():
+    """rsk_orth_guess vs eq:orthupdate solved densely (independent numpy formulation)."""
+    from paper_2306_15049_b200 import rsk
+    rng = np.random.default_rng(4)
+    N, nc = 60, 6
+    Ut, _ = np.linalg.qr(rng.standard_normal((N, nc)))
+    Ad = rng.standard_normal((N, N)); Ad = Ad @ Ad.T / N + np.eye(N)
+    Ed = rng.standard_normal((N, N)); Ed = Ed @ Ed.T / N
+    b = rng.standard_normal(N)
+    gs = 0.3
+    ZA, ZE = Ad @ Ut, Ed @ Ut
+    K, R = np.linalg.qr(ZA + gs * ZE)
+    sg = np.sign(np.diag(R)); K = K * sg; R = R * sg[:, None]
+    gammas = np.array([0.0, 0.01, 0.3, 5.0])
+    C, st = rsk.orth_guess(R, K.T @ ZE, ZE.T @ ZE, ZE.T @ b, K.T @ b, gs, gammas)
+    assert np.all(st == 0)
+    for l, g in enumerate(gammas):
+        coef, *_ = np.linalg.lstsq((Ad + g * Ed) @ Ut, b, rcond=None)
+        np.testing.assert_allclose(C[:, l], coef, rtol=1e-8, atol=1e-10)
+
+
+def test_host_lcurve_corner_matches_oracle():
+    from oracle import pipeline
+    from paper_2306_15049_b200 import rsk
+    rng = np.random.default_rng(5)
+    rho = np.exp(np.cumsum(rng.uniform(0, 1, 20)))
+    eta = np.exp(-np.cumsum(rng.uniform(0, 1, 20)))
+    assert rsk.lcurve_corner(rho, eta)[0] == pipeline.lcurve_corner(rho, eta)[0]
+
+
+def test_host_stabilize_small_cut():
+    from paper_2306_15049_b200 import rsk
+    rng = np.random.default_rng(6)
+    Qa, _ = np.linalg.qr(rng.standard_normal((10, 10)))
+    Qb, _ = np.linalg.qr(rng.standard_normal((10, 10)))
+    R = Qa @ np.diag(np.logspace(0, -16, 10)) @ Qb.T
+    Zs, nk = rsk.stabilize_small(R, np.ones(10), 1e10, 0)
+    assert nk == int(np.sum(1.0 / np.logspace(0, -16, 10) < 1e10))
+    Zs3, nk3 = rsk.stabilize_small(R, np.ones(10), 1e10, 3)
+    assert nk3 == 3
