@@ -1,0 +1,311 @@
+"""Benchmark of the recycled shifted solver hot path (arXiv 2306.15049) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C2]
+
+A "step" is one pass of the whole hot path over one batch of synthetic input:
+the complete nested solve of a BASELINE.json configuration (K_out outer IRN
+steps x M shifts: data d, b; seed solves + Ritz; stabilize; anchoring + Grams;
+principal guesses; group Ritz blocks; carried corrections; batched deflated CG;
+L-curve; IRN weights). Default workload: configs[1] = C2 (256x256, 32 shifts,
+5 outer steps). Metric value = fused (A + gamma E_k) applies per second over the
+whole job (method accounting: every A_gamma apply, seeds/Ritz/anchoring included).
+
+Timing: CUDA events on the launching stream around each step, L2 flushed between
+steps (outside the events), W untimed warm-up steps, max over ranks.
+One JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import rsk_synth as S  # noqa: E402
+
+METRIC = "fused (A+γE_k)x applies/s & shifted solves/s; HBM GB/s vs peak, 1-8 GPU"
+UNIT = "applies/s"
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    def __init__(self, gpu=0):
+        self.gpu = gpu
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap,power.draw")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 6:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].strip() == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------- CPU oracle leg
+def oracle_sample(cfg, inputs, budget_s=12.0):
+    """The oracle as it stands (numpy fp64, single thread) on a bounded sample of the
+    same workload: plain CG at gamma_i1 from x = 0 on the config's own b, W_0 = I --
+    the seed solve that opens the nested solve -- stopped after `budget_s` seconds.
+    Returns applies/s (same unit as the GPU metric)."""
+    from oracle import defcg as dcg
+    from oracle import operators as ops
+    n = cfg.n
+    h = inputs["psf"]
+    d, b = ops.make_data(h, inputs["x_true"], inputs["xi"], cfg.noise)
+    wx, wy = ops.identity_weights(n)
+    g = float(inputs["gamma"][cfg.i1 - 1])
+    A = lambda v: ops.apply_shifted(h, wx, wy, g, v.reshape(n, n)).ravel()
+    # time a few iterations to size the sample to the budget
+    t0 = time.perf_counter()
+    dcg.defcg(A, b.ravel(), tol=1e-300, maxit=2)
+    per = max((time.perf_counter() - t0) / 4.0, 1e-4)
+    its = max(2, int(budget_s / per))
+    t0 = time.perf_counter()
+    r = dcg.defcg(A, b.ravel(), tol=1e-300, maxit=its)
+    dt = time.perf_counter() - t0
+    return r.applies / dt, f"oracle plain CG at gamma_i1 on {cfg.name} (n={n}), {r.applies} applies in {dt:.1f}s"
+
+
+def run_reference(args, cfg, inputs, rank, world):
+    os.environ.setdefault("OMP_NUM_THREADS", "1")
+    if rank != 0:
+        return
+    vals = []
+    for _ in range(args.warmup):
+        oracle_sample(cfg, inputs, budget_s=1.0)
+    t_total = time.perf_counter()
+    for _ in range(args.steps):
+        v, desc = oracle_sample(cfg, inputs, budget_s=args.ref_budget)
+        vals.append(v)
+    t_total = time.perf_counter() - t_total
+    v = float(np.mean(vals))
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t_total / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": cfg.name, "n": cfg.n, "shifts": cfg.M,
+                                        "outer_steps": cfg.K_out, "l2": "n/a (CPU)"},
+        "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc},
+        "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+# ---------------------------------------------------------------- GPU leg
+def run_ours(args, cfg, inputs, rank, world):
+    import torch
+    import torch.distributed as dist
+    from paper_2306_15049_b200 import _lib as L
+    from paper_2306_15049_b200.pipeline import GpuSolver
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    lib = L.load()
+    stream = torch.cuda.current_stream(dev)
+    sol = GpuSolver(cfg, inputs["psf"], inputs["gamma"], device=local, check_every=args.check_every)
+    x_true = torch.from_numpy(inputs["x_true"]).to(dev)
+    xi = torch.from_numpy(inputs["xi"]).to(dev)
+    flush = torch.empty(256 * 1024 * 1024 // 8, dtype=torch.float64, device=dev)
+
+    def step():
+        sol.set_data(x_true, xi)
+        outs = sol.run()
+        return outs
+
+    def count(outs):
+        ap = sum(int(o.applies.sum()) + o.overhead_applies for o in outs)
+        sv = sum(int(o.applies.size) for o in outs)
+        its = sum(int(o.iters.sum()) for o in outs)
+        return ap, sv, its
+
+    for _ in range(args.warmup):
+        outs = step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    tot_ap = tot_sv = tot_it = 0
+    l0 = lib.rsk_launch_count()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            flush.fill_(float(i))                       # L2 flush between timed steps (256 MB > 126 MB L2)
+            ev[i][0].record(stream)
+            outs = step()
+            ev[i][1].record(stream)
+            ap, sv, it = count(outs)
+            tot_ap += ap; tot_sv += sv; tot_it += it
+        torch.cuda.synchronize(dev)
+    launches = lib.rsk_launch_count() - l0
+    ms = sum(a.elapsed_time(b) for a, b in ev)
+    if world > 1:
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        c = torch.tensor([tot_ap, tot_sv], dtype=torch.float64, device=dev)
+        dist.all_reduce(c)
+        tot_ap_all, tot_sv_all = int(c[0].item()), int(c[1].item())
+    else:
+        tot_ap_all, tot_sv_all = tot_ap, tot_sv
+    value = tot_ap_all / (ms / 1e3)
+    solves = tot_sv_all / (ms / 1e3)
+    last = outs
+
+    # ---- e2e through the public API with host buffers (pinned), copies inside the region
+    xt_h = torch.from_numpy(inputs["x_true"]).pin_memory()
+    xi_h = torch.from_numpy(inputs["xi"]).pin_memory()
+    res_h = torch.empty(cfg.M, cfg.N, dtype=torch.float64).pin_memory()
+    e2e_steps = max(1, min(args.steps, 3))
+    ee = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(e2e_steps)]
+    e_ap = 0
+    for i in range(e2e_steps):
+        flush.fill_(float(i))
+        ee[i][0].record(stream)
+        x_true.copy_(xt_h, non_blocking=True)
+        xi.copy_(xi_h, non_blocking=True)
+        outs = step()
+        res_h.copy_(sol.final["X_prev"], non_blocking=True)
+        ee[i][1].record(stream)
+        e_ap += count(outs)[0]
+    torch.cuda.synchronize(dev)
+    ems = sum(a.elapsed_time(b) for a, b in ee)
+    e2e = {"value": e_ap / (ems / 1e3) * (world if world > 1 else 1), "unit": UNIT,
+           "h2d_bytes_per_step": 2 * cfg.N * 8, "d2h_bytes_per_step": cfg.M * cfg.N * 8}
+
+    # ---- roofline of the dominant kernel: the fused apply inside the CG loop,
+    # measured live with CUDA events around each launch (one extra profiled step)
+    sol.profile = True
+    outs_p = step()
+    sol.profile = False
+    prof = np.sum([o.prof for o in outs_p], axis=0)     # ms_apply, ms_update, n_launch, px-vecs
+    ms_apply, ms_upd, n_ka, pxv = [float(v) for v in prof]
+    alg_bytes = 16.0 * pxv + 16.0 * cfg.N * n_ka          # p read + w write per px-vec; W_k per launch
+    achieved = alg_bytes / (ms_apply / 1e3) / 1e9 if ms_apply > 0 else None
+    peak, peak_src = _peaks()
+    # standalone fused apply over the full batch (all M shifts), best of 20
+    X = torch.randn(cfg.M, cfg.N, dtype=torch.float64, device=dev)
+    Y = torch.empty_like(X)
+    best = 1e9
+    for _ in range(23):
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        sol.h.apply_shifted(X, Y, gamma=sol.gam_dev)
+        a1.record(stream)
+        torch.cuda.synchronize(dev)
+        best = min(best, a0.elapsed_time(a1))
+    sa_bytes = 16.0 * cfg.M * cfg.N + 16.0 * cfg.N
+    standalone = {"applies_per_s": cfg.M / (best / 1e3), "ms": best,
+                  "gbs": sa_bytes / (best / 1e3) / 1e9, "frac_hbm": sa_bytes / (best / 1e3) / 1e9 / peak}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        os.environ.setdefault("OMP_NUM_THREADS", "1")
+        v, desc = oracle_sample(cfg, inputs, budget_s=args.cpu_budget)
+        cpu = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": desc}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "n": cfg.n, "N": cfg.N, "shifts": cfg.M,
+                       "outer_steps": cfg.K_out, "n_c": cfg.n_c, "J": cfg.J, "psf": f"{2*cfg.r+1}x{2*cfg.r+1}",
+                       "tol": cfg.tol, "l2": "flushed between steps (256 MB write)",
+                       "parallelism": "replicas" if world > 1 else "single"},
+            "solves_per_s": solves,
+            "applies_per_step": tot_ap / args.steps, "cg_iterations_per_step": tot_it / args.steps,
+            "lstar": [int(o.lstar) for o in last],
+            "iters_per_outer_step": [int(o.iters.sum()) for o in last],
+            "e2e": e2e,
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "hbm", "kernel": "apply_kernel (fused A + gamma E, CG mode)",
+                         "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": (achieved / peak) if achieved else None, "traffic": None,
+                         "peak_source": peak_src, "kernel_ms_share": ms_apply / max(ms_apply + ms_upd, 1e-9),
+                         "apply_launches": n_ka, "apply_px_vectors": pxv},
+            "apply_standalone": standalone,
+            "clocks": clk.summary(),
+            "cpu_baseline": cpu,
+        }
+        print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--check-every", type=int, default=8)
+    ap.add_argument("--cpu-budget", type=float, default=12.0)
+    ap.add_argument("--ref-budget", type=float, default=15.0)
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    cfg = S.CONFIGS[args.config]
+    inputs = S.make_inputs(cfg)
+    if args.impl == "reference":
+        run_reference(args, cfg, inputs, rank, world)
+        return
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    run_ours(args, cfg, inputs, rank, world)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

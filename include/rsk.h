@@ -96,6 +96,8 @@ rsk_status rsk_destroy(rsk_handle h);
 const char* rsk_last_error(rsk_handle h);
 /* Library build information (static host string). */
 const char* rsk_version(void);
+/* Number of librsk kernel launches so far in this process (all handles). */
+int64_t rsk_launch_count(void);
 
 /* rsk_set_weights: copy W_k into the handle (E_k = L^T W_k L).
  * wx[i][j] weights (Dx x)[i,j] = x[i,j+1]-x[i,j]; wx[i][nx-1] must be 0.

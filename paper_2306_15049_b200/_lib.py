@@ -69,6 +69,7 @@ class CgOut(C.Structure):
 
 _SIGS = {
     "rsk_version": (C.c_char_p, []),
+    "rsk_launch_count": (C.c_int64, []),
     "rsk_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, _i64, _i64, _hp, C.c_int, C.c_int, C.c_int]),
     "rsk_destroy": (C.c_int, [C.c_void_p]),
     "rsk_last_error": (C.c_char_p, [C.c_void_p]),

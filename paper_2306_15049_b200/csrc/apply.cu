@@ -266,7 +266,7 @@ static cudaError_t launch_r(const ApplyParams& prm, int nlist, cudaStream_t st) 
     attr_set = true;
   }
   dim3 grid(prm.ntiles, nlist);
-  apply_kernel<R><<<grid, kNT, C::SMEM, st>>>(prm);
+  count_launch(); apply_kernel<R><<<grid, kNT, C::SMEM, st>>>(prm);
   return cudaGetLastError();
 }
 
@@ -322,7 +322,7 @@ cudaError_t launch_apply(Handle* h, const ApplyLaunch& a, cudaStream_t st) {
   }
   if (e != cudaSuccess) return e;
   if (a.xdoty && !a.cg) {
-    apply_dot_reduce<<<a.nlist, 32, 0, st>>>(h->scratch, prm.ntiles, a.list, a.xdoty);
+    count_launch(); apply_dot_reduce<<<a.nlist, 32, 0, st>>>(h->scratch, prm.ntiles, a.list, a.xdoty);
     e = cudaGetLastError();
   }
   return e;

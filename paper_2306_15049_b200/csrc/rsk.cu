@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -57,6 +58,13 @@ void build_B_row(const double* f, int r, int64_t n, int64_t c, double* row) {
 }
 
 }  // namespace
+
+namespace rsk {
+static std::atomic<long long> g_launches{0};
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+}  // namespace rsk
+
+extern "C" int64_t rsk_launch_count(void) { return (int64_t)rsk::g_launches.load(); }
 
 extern "C" const char* rsk_version(void) {
   return "librsk 0.1 (sm_100a, fp64): fused shifted apply, deflated CG, recycle projections";
@@ -648,6 +656,7 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
   const int ce = d->check_every;
   std::vector<cudaEvent_t> evs;
   double ms_apply = 0.0, ms_upd = 0.0;
+  int64_t n_ka = 0;
   if (prof) {
     evs.resize(3 * ce);
     for (auto& e : evs) RSK_CUDA(cudaEventCreate(&e));
@@ -657,6 +666,7 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
   while (!active.empty()) {
     RSK_CUDA(upload_list(dlist, active));
     const int na = (int)active.size();
+    n_ka += ce;
     for (int i = 0; i < ce; ++i) {
       if (prof) RSK_CUDA(cudaEventRecord(evs[3 * i], st));
       ApplyLaunch a{};
@@ -756,7 +766,7 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
   if (prof) {
     o->ms_loop[0] = ms_apply;
     o->ms_loop[1] = ms_upd;
-    o->ms_loop[2] = 0.0;
+    o->ms_loop[2] = (double)n_ka;
     o->ms_loop[3] = (double)tot_it * (double)N;
   }
   RSK_CUDA(cudaStreamSynchronize(st));

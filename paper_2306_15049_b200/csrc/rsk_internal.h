@@ -147,6 +147,9 @@ cudaError_t launch_cg_combine(CgDev* dev, const CgDev& host, const int* list, in
                               cudaStream_t st);
 int cg_nblkB(int64_t N);
 
+// kernel-launch accounting (rsk_launch_count): every librsk kernel launch bumps it
+void count_launch();
+
 // host dense (host_dense.cpp)
 bool chol_lower(int n, double* A);  // in-place, column-major lower; false if not SPD
 void chol_solve_lower(int n, const double* L, double* x);

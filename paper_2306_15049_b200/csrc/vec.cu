@@ -84,9 +84,9 @@ cudaError_t launch_gemm_tn(Handle* h, int64_t n, int k, const double* U, int64_t
   rpc = (rpc + 31) / 32 * 32;
   nchunk = (n + rpc - 1) / rpc;
   dim3 grid((unsigned)nchunk, tk, tv);
-  gemm_tn_part<<<grid, 256, 0, st>>>(n, k, U, ldu, nv, V, ldv, h->scratch, rpc);
+  count_launch(); gemm_tn_part<<<grid, 256, 0, st>>>(n, k, U, ldu, nv, V, ldv, h->scratch, rpc);
   const int64_t tot = (int64_t)k * nv;
-  gemm_tn_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(k, nv, (int)nchunk, h->scratch, C, ldc);
+  count_launch(); gemm_tn_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(k, nv, (int)nchunk, h->scratch, C, ldc);
   return cudaGetLastError();
 }
 
@@ -143,7 +143,7 @@ cudaError_t launch_gemm_nn(Handle* h, int64_t n, int k, const double* U, int64_t
                            cudaStream_t st) {
   (void)h;
   dim3 grid((unsigned)((n + 63) / 64), (nv + 31) / 32);
-  gemm_nn_kernel<<<grid, 256, 0, st>>>(n, k, U, ldu, nv, V, ldv, C, ldc, sign);
+  count_launch(); gemm_nn_kernel<<<grid, 256, 0, st>>>(n, k, U, ldu, nv, V, ldv, C, ldc, sign);
   return cudaGetLastError();
 }
 
@@ -192,8 +192,8 @@ cudaError_t launch_batch_dot(Handle* h, int64_t n, int nv, const double* X, int6
                              const double* Y, int64_t ldy, double* out, cudaStream_t st) {
   const int nchunk = (int)((n + kChunk - 1) / kChunk);
   if (sizeof(double) * (size_t)nchunk * nv > h->scratch_bytes) return cudaErrorMemoryAllocation;
-  dot_part<<<dim3(nchunk, nv), 256, 0, st>>>(n, X, ldx, Y, ldy, h->scratch, nchunk);
-  reduce_partials<<<nv, 32, 0, st>>>(h->scratch, nchunk, out, 0);
+  count_launch(); dot_part<<<dim3(nchunk, nv), 256, 0, st>>>(n, X, ldx, Y, ldy, h->scratch, nchunk);
+  count_launch(); reduce_partials<<<nv, 32, 0, st>>>(h->scratch, nchunk, out, 0);
   return cudaGetLastError();
 }
 
@@ -216,7 +216,7 @@ cudaError_t launch_batch_axpby(int64_t n, int nv, const double* a, const double*
                                const double* b, double* Y, int64_t ldy, cudaStream_t st) {
   int64_t blocks = (n + 255) / 256;
   if (blocks > 1184) blocks = 1184;
-  axpby_kernel<<<dim3((unsigned)blocks, nv), 256, 0, st>>>(n, a, X, ldx, b, Y, ldy);
+  count_launch(); axpby_kernel<<<dim3((unsigned)blocks, nv), 256, 0, st>>>(n, a, X, ldx, b, Y, ldy);
   return cudaGetLastError();
 }
 
@@ -255,9 +255,9 @@ cudaError_t launch_irn(Handle* h, const double* x, double tau, double* wx, doubl
                        double* eta2, cudaStream_t st) {
   const int64_t N = h->ny * h->nx;
   const int nchunk = (int)((N + kChunk - 1) / kChunk);
-  irn_kernel<<<nchunk, 256, 0, st>>>((int)h->ny, (int)h->nx, x, tau, wx, wy, h->wx, h->wy,
+  count_launch(); irn_kernel<<<nchunk, 256, 0, st>>>((int)h->ny, (int)h->nx, x, tau, wx, wy, h->wx, h->wy,
                                      eta2 ? h->scratch : nullptr);
-  if (eta2) reduce_partials<<<1, 32, 0, st>>>(h->scratch, nchunk, eta2, 0);
+  if (eta2) { count_launch(); reduce_partials<<<1, 32, 0, st>>>(h->scratch, nchunk, eta2, 0); }
   return cudaGetLastError();
 }
 
@@ -288,9 +288,9 @@ cudaError_t launch_seminorm_batch(Handle* h, int nvec, const double* X, int64_t 
   const int64_t N = h->ny * h->nx;
   const int nchunk = (int)((N + kChunk - 1) / kChunk);
   if (sizeof(double) * (size_t)nchunk * nvec > h->scratch_bytes) return cudaErrorMemoryAllocation;
-  seminorm_part<<<dim3(nchunk, nvec), 256, 0, st>>>((int)h->ny, (int)h->nx, X, ldx, h->wx, h->wy,
+  count_launch(); seminorm_part<<<dim3(nchunk, nvec), 256, 0, st>>>((int)h->ny, (int)h->nx, X, ldx, h->wx, h->wy,
                                                     h->scratch, nchunk);
-  reduce_partials<<<nvec, 32, 0, st>>>(h->scratch, nchunk, eta2, do_sqrt);
+  count_launch(); reduce_partials<<<nvec, 32, 0, st>>>(h->scratch, nchunk, eta2, do_sqrt);
   return cudaGetLastError();
 }
 
@@ -317,8 +317,8 @@ cudaError_t launch_diffnorm_batch(Handle* h, int nvec, const double* Y, int64_t 
   const int64_t N = h->ny * h->nx;
   const int nchunk = (int)((N + kChunk - 1) / kChunk);
   if (sizeof(double) * (size_t)nchunk * nvec > h->scratch_bytes) return cudaErrorMemoryAllocation;
-  diffnorm_part<<<dim3(nchunk, nvec), 256, 0, st>>>(N, Y, ldy, d, h->scratch, nchunk);
-  reduce_partials<<<nvec, 32, 0, st>>>(h->scratch, nchunk, out, 1);
+  count_launch(); diffnorm_part<<<dim3(nchunk, nvec), 256, 0, st>>>(N, Y, ldy, d, h->scratch, nchunk);
+  count_launch(); reduce_partials<<<nvec, 32, 0, st>>>(h->scratch, nchunk, out, 1);
   return cudaGetLastError();
 }
 
@@ -336,7 +336,7 @@ cudaError_t launch_scale_noise(int64_t n, const double* cx, const double* xi, co
                                double nu, double* d, cudaStream_t st) {
   int64_t blocks = (n + 255) / 256;
   if (blocks > 1184) blocks = 1184;
-  scale_noise_kernel<<<(unsigned)blocks, 256, 0, st>>>(n, cx, xi, s2, nu, d);
+  count_launch(); scale_noise_kernel<<<(unsigned)blocks, 256, 0, st>>>(n, cx, xi, s2, nu, d);
   return cudaGetLastError();
 }
 
@@ -486,7 +486,7 @@ cudaError_t launch_cg_update(CgDev* dev, const CgDev& host, const int* list, int
                              cudaStream_t st) {
   if (nlist <= 0) return cudaSuccess;
   dim3 grid(host.nblkB, nlist);
-  cg_update_kernel<<<grid, kNT, 0, st>>>(dev, list, mode);
+  count_launch(); cg_update_kernel<<<grid, kNT, 0, st>>>(dev, list, mode);
   return cudaGetLastError();
 }
 
@@ -597,7 +597,7 @@ cudaError_t launch_cg_combine(CgDev* dev, const CgDev& host, const int* list, in
                               cudaStream_t st) {
   if (nlist <= 0) return cudaSuccess;
   dim3 grid(host.nblkB, nlist);
-  cg_combine_kernel<<<grid, kNT, 0, st>>>(dev, list, mode);
+  count_launch(); cg_combine_kernel<<<grid, kNT, 0, st>>>(dev, list, mode);
   return cudaGetLastError();
 }
 

@@ -274,10 +274,12 @@ def _state_to_dev(torch, dev, st):
 @pytest.mark.parametrize("cfgname", ["C1"])
 def test_outer_steps_stepwise_handoff(torch_dev, cfgname):
     """Stepwise parity (reading G28): the oracle runs the IRN loop; at every step k the GPU
-    starts from the oracle's state (W_k, X^(k-1), G^(k-1), V_i1) and runs step k itself."""
+    starts from the oracle's state (W_k, X^(k-1), G^(k-1), V_i1) and runs step k itself.
+    north_star: converged solutions, both sides at relative residual 1e-10, agree to 1e-8."""
+    import dataclasses
     torch, dev = torch_dev
     from paper_2306_15049_b200.pipeline import GpuSolver
-    cfg = S.CONFIGS[cfgname]
+    cfg = dataclasses.replace(S.CONFIGS[cfgname], tol=1e-10)
     inp = S.make_inputs(cfg)
     ref = opipe.run(cfg, inp, keep_steps=True)
     sol = GpuSolver(cfg, inp["psf"], inp["gamma"], check_every=4)
@@ -294,7 +296,7 @@ def test_outer_steps_stepwise_handoff(torch_dev, cfgname):
         for l in range(cfg.M):
             xg = X["X_prev"][l].cpu().numpy()
             rel = np.linalg.norm(xg - rs.X[:, l]) / np.linalg.norm(rs.X[:, l])
-            assert rel <= 5e-8, (k, l, rel)
+            assert rel <= 1e-8, (k, l, rel)
         d_it = np.abs(o.iters - rs.iters)
         assert np.mean(d_it <= 2) >= 0.95 and np.all(d_it <= np.maximum(2, 0.01 * rs.iters) + 2), (o.iters, rs.iters)
         assert o.lstar == rs.lstar
