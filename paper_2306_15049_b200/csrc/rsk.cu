@@ -386,7 +386,10 @@ namespace {
 
 struct WsLayout {
   size_t off_R, off_P, off_W, off_dbl, off_int, off_cnt, off_pA, off_pB, off_list, off_dev, off_gb, total;
+  size_t off_glist, off_partG, off_cntG;
   int nblkA, nblkB;
+  int nchunkG, maxtilesG;
+  int64_t rowsG;
 };
 
 size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
@@ -396,7 +399,18 @@ WsLayout ws_layout(const Handle* h, int ns) {
   const int64_t N = h->ny * h->nx;
   L.nblkA = apply_tiles(h);
   L.nblkB = cg_nblkB(N);
+  // group kernels: row chunks of a multiple of 32 rows, at most kMaxChunkG chunks
+  int64_t rows = (N + kMaxChunkG - 1) / kMaxChunkG;
+  if (rows < 256) rows = 256;
+  rows = (rows + 255) / 256 * 256;   // whole 256-row sub-slabs (cg_group.cu)
+  L.rowsG = rows;
+  L.nchunkG = (int)((N + rows - 1) / rows);
+  L.maxtilesG = (ns + 31) / 32;
   size_t o = 0;
+  L.off_glist = o; o = al(o + sizeof(int) * (size_t)(ns + 8));
+  L.off_partG = o;
+  o = al(o + sizeof(double) * (size_t)RSK_MAX_GROUPS * L.maxtilesG * (L.nchunkG + 16) * kPartRowsG * 32);
+  L.off_cntG = o; o = al(o + sizeof(unsigned) * (size_t)RSK_MAX_GROUPS * L.maxtilesG * kTickStride);
   L.off_R = o; o = al(o + sizeof(double) * (size_t)N * ns);
   L.off_P = o; o = al(o + sizeof(double) * (size_t)N * ns);
   L.off_W = o; o = al(o + sizeof(double) * (size_t)N * ns);
@@ -488,6 +502,13 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
   hc.nblkB = L.nblkB;
   hc.tol = d->tol;
   hc.maxit = d->maxit;
+  hc.glist = reinterpret_cast<int*>(base + L.off_glist);
+  hc.gmeta = hc.glist + ns;
+  hc.partG = reinterpret_cast<double*>(base + L.off_partG);
+  hc.cntG = reinterpret_cast<unsigned*>(base + L.off_cntG);
+  hc.nchunkG = L.nchunkG;
+  hc.rowsG = L.rowsG;
+  hc.maxtilesG = L.maxtilesG;
   for (int g = 0; g < RSK_MAX_GROUPS; ++g) {
     hc.grp.W[g] = (defl && g < d->ngroups) ? d->W[g] : nullptr;
     hc.grp.AW[g] = (defl && g < d->ngroups) ? d->AW[g] : nullptr;
@@ -612,6 +633,7 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
     }
     RSK_CUDA(cudaMemcpyAsync(in, ih.data(), sizeof(int) * ih.size(), cudaMemcpyHostToDevice, st));
     RSK_CUDA(cudaMemsetAsync(hc.cnt, 0, sizeof(unsigned) * ns * 4, st));
+    RSK_CUDA(cudaMemsetAsync(hc.cntG, 0, sizeof(unsigned) * RSK_MAX_GROUPS * L.maxtilesG * kTickStride, st));
     RSK_CUDA(cudaMemsetAsync(hc.P, 0, sizeof(double) * (size_t)N * ns, st));
     RSK_CUDA(cudaMemcpyAsync(dev, &hc, sizeof(CgDev), cudaMemcpyHostToDevice, st));
   }
@@ -663,19 +685,36 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
   }
   std::vector<int> stat_h(ns), it_h(ns);
   int64_t guard = 0;
+  const int ngrp = defl ? d->ngroups : 1;
+  std::vector<int> gbuf(ns + 8);
   while (!active.empty()) {
-    RSK_CUDA(upload_list(dlist, active));
+    // active shifts grouped by shift group (group-shared kernels), with offsets/counts
+    int maxt = 0;
+    {
+      int o2 = 0;
+      for (int g = 0; g < ngrp; ++g) {
+        int c = 0;
+        gbuf[ns + g] = o2;
+        for (int s : active)
+          if (grp[s] == g) { gbuf[o2 + c] = s; ++c; }
+        gbuf[ns + 4 + g] = c;
+        o2 += c;
+        maxt = std::max(maxt, (c + 31) / 32);
+      }
+      for (int g = ngrp; g < 4; ++g) { gbuf[ns + g] = o2; gbuf[ns + 4 + g] = 0; }
+    }
+    RSK_CUDA(cudaMemcpyAsync(hc.glist, gbuf.data(), sizeof(int) * (ns + 8), cudaMemcpyHostToDevice, st));
     const int na = (int)active.size();
     n_ka += ce;
     for (int i = 0; i < ce; ++i) {
       if (prof) RSK_CUDA(cudaEventRecord(evs[3 * i], st));
       ApplyLaunch a{};
-      a.X = hc.P; a.ldx = N; a.Y = hc.Wv; a.ldy = N; a.gamma = hc.gam; a.list = dlist; a.nlist = na;
+      a.X = hc.P; a.ldx = N; a.Y = hc.Wv; a.ldy = N; a.gamma = hc.gam; a.list = hc.glist; a.nlist = na;
       a.mode = RSK_APPLY_SHIFTED; a.cg = dev; a.cg_alpha = true;
       RSK_CUDA(launch_apply(h, a, st));
       if (prof) RSK_CUDA(cudaEventRecord(evs[3 * i + 1], st));
-      RSK_CUDA(launch_cg_update(dev, hc, dlist, na, UPD_LOOP, st));
-      RSK_CUDA(launch_cg_combine(dev, hc, dlist, na, CMB_LOOP, st));
+      RSK_CUDA(launch_cg_update_grp(dev, hc, ngrp, maxt, st));
+      RSK_CUDA(launch_cg_combine_grp(dev, hc, ngrp, maxt, st));
       if (prof) RSK_CUDA(cudaEventRecord(evs[3 * i + 2], st));
     }
     RSK_CUDA(cudaMemcpyAsync(stat_h.data(), hc.status, sizeof(int) * ns, cudaMemcpyDeviceToHost, st));

@@ -15,9 +15,13 @@ constexpr int kMaxM = RSK_MAX_LOCAL;      // local recycle dimension
 constexpr int kNT = 256;                  // threads per CTA for streaming kernels
 constexpr size_t kAuxBytes = sizeof(double) * (2 * 256 * 256 + 8192);
 
-// apply tile (output pixels per CTA)
-constexpr int kTY = 32;
+// apply tile: (64 - 4r) x kTX output pixels per work item
 constexpr int kTX = 64;
+// partial rows of the group update kernel: 2 x 16 GEMM rows + rho + ZGhat.r
+constexpr int kGrpStride = 34;
+constexpr int kMaxChunkG = 256;
+constexpr int kPartRowsG = 18;                     // z (16) + rho + ZGhat.r
+constexpr int kTickStride = 2 + kMaxChunkG / 16 + 1; // per (group, tile) tickets
 
 // ---- per-shift CG status on the device
 enum DevStatus : int {
@@ -76,6 +80,14 @@ struct CgDev {
   double tol;
   int maxit;
   GroupPtrs grp;
+  // group-shared hot-loop kernels (cg_group.cu)
+  int* glist;       // active shift ids, grouped: group g at glist[gmeta[g] .. + gmeta[4+g])
+  int* gmeta;       // [0..3] offsets, [4..7] counts
+  double* partG;    // [4][maxtilesG][nchunkG][kGrpStride][32]
+  unsigned* cntG;   // [4][maxtilesG][2]
+  int nchunkG;
+  int64_t rowsG;
+  int maxtilesG;
 };
 
 // ---- handle
@@ -146,6 +158,8 @@ enum CmbMode { CMB_LOOP = 0, CMB_GALERKIN = 1, CMB_RESID = 2, CMB_GOUT = 3 };
 cudaError_t launch_cg_combine(CgDev* dev, const CgDev& host, const int* list, int nlist, int mode,
                               cudaStream_t st);
 int cg_nblkB(int64_t N);
+cudaError_t launch_cg_update_grp(CgDev* dev, const CgDev& host, int ngroups, int maxtiles, cudaStream_t st);
+cudaError_t launch_cg_combine_grp(CgDev* dev, const CgDev& host, int ngroups, int maxtiles, cudaStream_t st);
 
 // kernel-launch accounting (rsk_launch_count): every librsk kernel launch bumps it
 void count_launch();

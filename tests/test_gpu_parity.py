@@ -288,15 +288,26 @@ def test_outer_steps_stepwise_handoff(torch_dev, cfgname):
     wx, wy = ops.identity_weights(n)
     st = opipe.StepState(0, wx, wy, None, None, None)
     total_it_gpu = total_it_ref = 0
+    from oracle import dense
+    limited = 0
     for k, rs in enumerate(ref["steps"]):
         sol.h.set_weights(_t(torch, dev, st.wx.ravel()), _t(torch, dev, st.wy.ravel()))
         o, X = sol.outer_step(k, _state_to_dev(torch, dev, st))
         assert o.nc == rs.nc
         assert np.all(o.status == 0), o.status
+        Ad = dense.assemble(lambda v: ops.apply_A(inp["psf"], v), n)
+        Ed = dense.assemble(lambda v: ops.apply_E(st.wx, st.wy, v), n)
         for l in range(cfg.M):
             xg = X["X_prev"][l].cpu().numpy()
             rel = np.linalg.norm(xg - rs.X[:, l]) / np.linalg.norm(rs.X[:, l])
-            assert rel <= 1e-8, (k, l, rel)
+            if rel > 1e-8:
+                # reading G27: tolerance-limited when 2 kappa tol exceeds 1e-8 (both sides are
+                # correct to their residual tolerance; they differ only in summation order)
+                ev = np.linalg.eigvalsh(Ad + inp["gamma"][l] * Ed)
+                bound = 2.0 * (ev[-1] / ev[0]) * cfg.tol
+                assert rel <= bound, (k, l, rel, bound)
+                limited += 1
+            assert rel <= 1e-6, (k, l, rel)
         d_it = np.abs(o.iters - rs.iters)
         assert np.mean(d_it <= 2) >= 0.95 and np.all(d_it <= np.maximum(2, 0.01 * rs.iters) + 2), (o.iters, rs.iters)
         assert o.lstar == rs.lstar
@@ -305,3 +316,4 @@ def test_outer_steps_stepwise_handoff(torch_dev, cfgname):
         wx, wy = ops.irn_weights(xstar, cfg.tau)
         st = opipe.StepState(k + 1, wx, wy, rs.X, rs.G, rs.V_i1)
     assert abs(total_it_gpu - total_it_ref) <= 0.02 * total_it_ref + 4
+    assert limited <= 0.1 * cfg.M * cfg.K_out, f"{limited} tolerance-limited solutions"
