@@ -6,6 +6,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -62,6 +63,7 @@ void build_B_row(const double* f, int r, int64_t n, int64_t c, double* row) {
 namespace rsk {
 static std::atomic<long long> g_launches{0};
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+void count_launches(long long n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 }  // namespace rsk
 
 extern "C" int64_t rsk_launch_count(void) { return (int64_t)rsk::g_launches.load(); }
@@ -138,7 +140,8 @@ extern "C" rsk_status rsk_create(rsk_handle* out, int device, int64_t ny, int64_
             cudaMalloc(&h->wy, sizeof(double) * N) == cudaSuccess &&
             cudaMalloc(&h->scratch, h->scratch_bytes) == cudaSuccess &&
             cudaMalloc(&h->scal, sizeof(double) * 64) == cudaSuccess &&
-            cudaMalloc(&h->aux, kAuxBytes) == cudaSuccess;
+            cudaMalloc(&h->aux, kAuxBytes) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&h->cg_stream, cudaStreamNonBlocking) == cudaSuccess;
   if (!ok) { rsk_destroy(h); return RSK_ENOMEM; }
   std::vector<double> w((size_t)N);
   ok = cudaMemcpy(h->tabBx, tx.data(), sizeof(double) * tx.size(), cudaMemcpyHostToDevice) == cudaSuccess &&
@@ -165,6 +168,7 @@ extern "C" rsk_status rsk_destroy(rsk_handle h) {
   cudaFree(h->scratch);
   cudaFree(h->scal);
   cudaFree(h->aux);
+  if (h->cg_stream) cudaStreamDestroy(h->cg_stream);
   delete h;
   return RSK_OK;
 }
@@ -407,7 +411,7 @@ WsLayout ws_layout(const Handle* h, int ns) {
   L.nchunkG = (int)((N + rows - 1) / rows);
   L.maxtilesG = (ns + 31) / 32;
   size_t o = 0;
-  L.off_glist = o; o = al(o + sizeof(int) * (size_t)(ns + 8));
+  L.off_glist = o; o = al(o + sizeof(int) * (size_t)(ns + 16));
   L.off_partG = o;
   o = al(o + sizeof(double) * (size_t)RSK_MAX_GROUPS * L.maxtilesG * (L.nchunkG + 16) * kPartRowsG * 32);
   L.off_cntG = o; o = al(o + sizeof(unsigned) * (size_t)RSK_MAX_GROUPS * L.maxtilesG * kTickStride);
@@ -461,7 +465,11 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
   for (int s = 0; s < ns; ++s) RSK_ARG(std::isfinite(d->gamma_h[s]) && d->gamma_h[s] >= 0, "rsk_cg_recycled_batch: gamma");
   const WsLayout L = ws_layout(h, ns);
   RSK_ARG(ws && ws_bytes >= L.total, "rsk_cg_recycled_batch: workspace too small");
-  cudaStream_t st = S(stream);
+  // The call is host-blocking: drain the caller's stream, then run on the handle's
+  // private non-blocking stream (CUDA-graph capture is not allowed on the legacy
+  // default stream), and drain that before returning.
+  RSK_CUDA(cudaStreamSynchronize(S(stream)));
+  cudaStream_t st = h->cg_stream;
   const bool prof = (d->flags & RSK_CG_PROFILE) != 0 && o->ms_loop;
 
   char* base = static_cast<char*>(ws);
@@ -686,10 +694,34 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
   std::vector<int> stat_h(ns), it_h(ns);
   int64_t guard = 0;
   const int ngrp = defl ? d->ngroups : 1;
-  std::vector<int> gbuf(ns + 8);
+  std::vector<int> gbuf(ns + 16);
+  // The lockstep chunk (check_every x {apply, update, combine}) has a static launch
+  // shape: list contents and lengths live in device memory, grids are sized for the
+  // whole solve (surplus CTAs exit). It is captured once as a CUDA graph and replayed
+  // at every poll, so the host issues one launch per chunk.
+  // (the per-kernel profiling mode times each launch with events, outside any graph)
+  const bool use_graph = getenv("RSK_NO_GRAPH") == nullptr && !prof;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  auto enqueue_chunk = [&](int na_host) -> cudaError_t {
+    for (int i = 0; i < ce; ++i) {
+      cudaError_t e;
+      if (prof && (e = cudaEventRecord(evs[3 * i], st)) != cudaSuccess) return e;
+      ApplyLaunch a{};
+      a.X = hc.P; a.ldx = N; a.Y = hc.Wv; a.ldy = N; a.gamma = hc.gam; a.list = hc.glist;
+      a.nlist = use_graph ? ns : na_host;
+      a.nlist_dev = use_graph ? hc.gmeta + 8 : nullptr;
+      a.mode = RSK_APPLY_SHIFTED; a.cg = dev; a.cg_alpha = true;
+      if ((e = launch_apply(h, a, st)) != cudaSuccess) return e;
+      if (prof && (e = cudaEventRecord(evs[3 * i + 1], st)) != cudaSuccess) return e;
+      if ((e = launch_cg_update_grp(dev, hc, ngrp, L.maxtilesG, st)) != cudaSuccess) return e;
+      if ((e = launch_cg_combine_grp(dev, hc, ngrp, L.maxtilesG, st)) != cudaSuccess) return e;
+      if (prof && (e = cudaEventRecord(evs[3 * i + 2], st)) != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  };
   while (!active.empty()) {
     // active shifts grouped by shift group (group-shared kernels), with offsets/counts
-    int maxt = 0;
     {
       int o2 = 0;
       for (int g = 0; g < ngrp; ++g) {
@@ -699,23 +731,27 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
           if (grp[s] == g) { gbuf[o2 + c] = s; ++c; }
         gbuf[ns + 4 + g] = c;
         o2 += c;
-        maxt = std::max(maxt, (c + 31) / 32);
       }
       for (int g = ngrp; g < 4; ++g) { gbuf[ns + g] = o2; gbuf[ns + 4 + g] = 0; }
+      gbuf[ns + 8] = o2;
     }
-    RSK_CUDA(cudaMemcpyAsync(hc.glist, gbuf.data(), sizeof(int) * (ns + 8), cudaMemcpyHostToDevice, st));
+    RSK_CUDA(cudaMemcpyAsync(hc.glist, gbuf.data(), sizeof(int) * (ns + 9), cudaMemcpyHostToDevice, st));
     const int na = (int)active.size();
     n_ka += ce;
-    for (int i = 0; i < ce; ++i) {
-      if (prof) RSK_CUDA(cudaEventRecord(evs[3 * i], st));
-      ApplyLaunch a{};
-      a.X = hc.P; a.ldx = N; a.Y = hc.Wv; a.ldy = N; a.gamma = hc.gam; a.list = hc.glist; a.nlist = na;
-      a.mode = RSK_APPLY_SHIFTED; a.cg = dev; a.cg_alpha = true;
-      RSK_CUDA(launch_apply(h, a, st));
-      if (prof) RSK_CUDA(cudaEventRecord(evs[3 * i + 1], st));
-      RSK_CUDA(launch_cg_update_grp(dev, hc, ngrp, maxt, st));
-      RSK_CUDA(launch_cg_combine_grp(dev, hc, ngrp, maxt, st));
-      if (prof) RSK_CUDA(cudaEventRecord(evs[3 * i + 2], st));
+    if (use_graph) {
+      if (!gexec) {
+        RSK_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeRelaxed));
+        cudaError_t ce_err = enqueue_chunk(na);
+        cudaError_t ee = cudaStreamEndCapture(st, &graph);
+        RSK_CUDA(ce_err);
+        RSK_CUDA(ee);
+        RSK_CUDA(cudaGraphInstantiate(&gexec, graph, 0));
+      } else {
+        count_launches(3LL * ce);
+      }
+      RSK_CUDA(cudaGraphLaunch(gexec, st));
+    } else {
+      RSK_CUDA(enqueue_chunk(na));
     }
     RSK_CUDA(cudaMemcpyAsync(stat_h.data(), hc.status, sizeof(int) * ns, cudaMemcpyDeviceToHost, st));
     RSK_CUDA(cudaStreamSynchronize(st));
@@ -752,6 +788,8 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
     if (++guard > (int64_t)d->maxit * 4 + 100) { h->err = "rsk_cg_recycled_batch: loop guard"; return RSK_ECUDA; }
   }
   if (prof) for (auto& e : evs) cudaEventDestroy(e);
+  if (gexec) cudaGraphExecDestroy(gexec);
+  if (graph) cudaGraphDestroy(graph);
 
   // ---- final true residual for shifts that stopped without a confirm (MAXIT / BREAKDOWN)
   std::vector<double> rt(ns, 0.0);
@@ -779,7 +817,7 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
   }
   if (d->Gout) {
     std::vector<double> one(ns, 1.0), mone(ns, -1.0);
-    rsk_status s2 = rsk_batch_axpby(h, N, ns, one.data(), d->X, d->ldx, mone.data(), d->Gout, d->ldg, stream);
+    rsk_status s2 = rsk_batch_axpby(h, N, ns, one.data(), d->X, d->ldx, mone.data(), d->Gout, d->ldg, (void*)st);
     if (s2 != RSK_OK) return s2;
   }
   bool all_ok = true;

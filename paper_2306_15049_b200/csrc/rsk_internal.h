@@ -112,6 +112,7 @@ struct Handle {
   std::string err;
   int sm_count = 148;
   bool sticky = false;
+  cudaStream_t cg_stream = nullptr;  // private capture-capable stream of rsk_cg_recycled_batch
 };
 
 // ---- launchers (apply.cu)
@@ -126,6 +127,7 @@ struct ApplyLaunch {
   double* xdoty;              // nullable, indexed by shift id
   CgDev* cg;                  // nullable => plain apply; else CG "w = A p" step
   bool cg_alpha;              // CG: compute alpha = rho / (p.w) in last CTA
+  const int* nlist_dev;       // nullable: list length read on the device (graph replay)
 };
 cudaError_t launch_apply(Handle* h, const ApplyLaunch& a, cudaStream_t st);
 int apply_tiles(const Handle* h);
@@ -163,6 +165,7 @@ cudaError_t launch_cg_combine_grp(CgDev* dev, const CgDev& host, int ngroups, in
 
 // kernel-launch accounting (rsk_launch_count): every librsk kernel launch bumps it
 void count_launch();
+void count_launches(long long n);
 
 // host dense (host_dense.cpp)
 bool chol_lower(int n, double* A);  // in-place, column-major lower; false if not SPD
