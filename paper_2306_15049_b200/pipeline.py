@@ -27,6 +27,7 @@ import numpy as np
 import torch
 
 from . import _lib as L
+from . import shard
 from .rsk import (Handle, carried_select, lcurve_corner, orth_guess, pencil_ritz,
                   stabilize_small, sym_eig)
 
@@ -62,7 +63,7 @@ class GpuSolver:
     """All device state of one configuration (one image grid, one PSF, M shifts)."""
 
     def __init__(self, cfg, psf: np.ndarray, gamma: np.ndarray, device: int = 0,
-                 check_every: int = 8, profile: bool = False, stream=None):
+                 check_every: int = 8, profile: bool = False, stream=None, dist=None):
         torch.cuda.set_device(device)
         self.dev = torch.device("cuda", device)
         self.cfg = cfg
@@ -72,6 +73,7 @@ class GpuSolver:
         self.check_every = check_every
         self.profile = profile
         self.stream = stream
+        self.dist = dist if dist is not None else shard.Dist(False)
         f = dict(dtype=torch.float64, device=self.dev)
         N, M = self.N, self.M
         self.f = f
@@ -194,10 +196,11 @@ class GpuSolver:
         return self.combine(Q, Z[:, :kk]), q
 
     # ------------------------------------------------------------- one outer step
-    def outer_step(self, k: int, st: dict) -> tuple[StepOut, dict]:
+    def _principal(self, k: int, st: dict):
+        """Rank-0 part of the outer step: raw block, stabilize (Alg. 1) and the anchor
+        images A U~, E U~ (n_c split applies). Returns (Ut, ZA, ZE, V_i1, overhead)."""
         cfg = self.cfg
-        N, M, nc_cap = self.N, self.M, cfg.n_c
-        t0 = time.perf_counter()
+        N, nc_cap = self.N, cfg.n_c
         overhead = 0
         i1, i2 = cfg.i1 - 1, cfg.i2 - 1
         V_i1 = st.get("V_i1")
@@ -219,11 +222,35 @@ class GpuSolver:
         Ut = self.stabilize(raw, nc_cap)
         nc = Ut.shape[0]
         del raw
-        # ---- anchoring (eq:establishU) and Grams
         ZA = torch.empty(nc, N, **self.f)
         ZE = torch.empty(nc, N, **self.f)
         self.h.apply_shifted(Ut, ZA, EY=ZE, mode=L.RSK_APPLY_SPLIT, stream=self.stream)
         overhead += nc
+        return Ut, ZA, ZE, V_i1, overhead
+
+    def outer_step(self, k: int, st: dict) -> tuple[StepOut, dict]:
+        cfg = self.cfg
+        N, M = self.N, self.M
+        dist = self.dist
+        t0 = time.perf_counter()
+        owners = shard.assignment(k, M, dist.world, st.get("prev_iters"))
+        mine = owners[dist.rank]
+        ml = len(mine)
+        # ---- principal space on rank 0, broadcast once per outer step (§8(e1))
+        V_i1 = st.get("V_i1")
+        overhead = 0
+        if dist.rank == 0:
+            Ut, ZA, ZE, V_i1, overhead = self._principal(k, st)
+            nc = Ut.shape[0]
+        nc = dist.bcast_int(nc if dist.rank == 0 else 0, self.dev)
+        if dist.rank != 0:
+            Ut = torch.empty(nc, N, **self.f)
+            ZA = torch.empty(nc, N, **self.f)
+            ZE = torch.empty(nc, N, **self.f)
+        if dist.enabled:
+            torch.cuda.synchronize(self.dev)
+            dist.bcast(Ut); dist.bcast(ZA); dist.bcast(ZE)
+        # ---- anchoring (eq:establishU) and Grams: identical on every rank
         gstar = float(self.gamma[cfg.istar - 1])
         Y = ZA.clone()
         self.h.batch_axpby(np.full(nc, gstar), ZE, None, Y, stream=self.stream)
@@ -237,49 +264,70 @@ class GpuSolver:
         Ahat = _host(self.utv(Ut, ZA)).T
         Ehat = _host(self.utv(Ut, ZE)).T
         del K
-        # ---- principal guesses (eq:orthupdate)
+        # ---- principal guesses (eq:orthupdate) for this rank's shifts
         Cg, gst = orth_guess(R, KtZE, ZEtZE, ZEtb, Ktb, gstar, self.gamma)
         has_xp = (gst == 0).astype(np.int32)
-        X = self.combine(Ut, Cg)               # x_0 = U~ C   (zero where NOT_SPD)
+        X = self.combine(Ut, Cg[:, mine]) if ml else torch.zeros(0, N, **self.f)
         # ---- group Ritz blocks (Alg. 2 / Alg. 4)
         Wg, AWg, EWg = [], [], []
         for jidx in (cfg.J_L - 1, cfg.J_R - 1):
             Wt, _ = pencil_ritz(Ahat, Ehat, float(self.gamma[jidx]), min(cfg.J, nc))
             Wg.append(self.combine(Ut, Wt)); AWg.append(self.combine(ZA, Wt)); EWg.append(self.combine(ZE, Wt))
         del ZA, ZE
-        groups = dict(W=Wg, AW=AWg, EW=EWg, of_shift=self.grp)
-        # ---- carried corrections (Alg. 3, reading D3 / G12)
+        groups = dict(W=Wg, AW=AWg, EW=EWg, of_shift=self.grp[mine])
+        # ---- carried corrections (Alg. 3, reading D3 / G12) for this rank's shifts
         ghat = None
         keep = None
-        if k >= 1 and st.get("G_prev") is not None:
-            Gp = st["G_prev"]
+        nL = int(np.sum(np.asarray(mine) < cfg.I_split))
+        if k >= 1 and st.get("G_prev") is not None and ml:
+            idx = torch.tensor(mine, dtype=torch.long, device=self.dev)
+            Gp = st["G_prev"][idx].contiguous()
             Gh = Gp.clone()
-            bounds = [(0, cfg.I_split), (cfg.I_split, M)]
+            bounds = [(0, nL), (nL, ml)]
             for _ in range(2):
                 for g, (a, bnd) in enumerate(bounds):
                     if bnd > a:
                         cf = self.utv(Wg[g], Gh[a:bnd])
                         self.h.recycle_project(L.RSK_SUB_UC, Wg[g], Gh[a:bnd], cf, stream=self.stream)
-            g2 = torch.empty(M, **self.f); gh2 = torch.empty(M, **self.f)
+            g2 = torch.empty(ml, **self.f); gh2 = torch.empty(ml, **self.f)
             self.h.batch_dot(Gp, Gp, g2, stream=self.stream)
             self.h.batch_dot(Gh, Gh, gh2, stream=self.stream)
             scale, keep = carried_select(_host(g2), _host(gh2), DUP_SIN)
-            self.h.batch_axpby(np.zeros(M), None, scale, Gh, stream=self.stream)
+            self.h.batch_axpby(np.zeros(ml), None, scale, Gh, stream=self.stream)
             ZGh = torch.empty_like(Gh)
-            self.h.apply_shifted(Gh, ZGh, gamma=self.gam_dev, stream=self.stream)
+            self.h.apply_shifted(Gh, ZGh, gamma=self.gam_dev[idx].contiguous(), stream=self.stream)
             overhead += int(keep.sum())
             ghat = (Gh, ZGh, keep)
-        # ---- batched deflated CG
-        G = torch.empty(M, N, **self.f)
-        res = self.cg(list(range(M)), X, has_xp, Gout=G, groups=groups, ghat=ghat)
-        # ---- L-curve and the next weights
-        self.h.lcurve_norms(X, self.d, self.rho_dev, self.eta_dev, self.lc_scratch, stream=self.stream)
-        rho, eta = _host(self.rho_dev), _host(self.eta_dev)
+        # ---- batched deflated CG on this rank's shifts
+        G = torch.empty(ml, N, **self.f)
+        if ml:
+            res = self.cg(mine, X, has_xp[mine], Gout=G, groups=groups, ghat=ghat)
+            self.h.lcurve_norms(X, self.d, self.rho_dev, self.eta_dev, self.lc_scratch, stream=self.stream)
+            rho_l, eta_l = _host(self.rho_dev)[:ml], _host(self.eta_dev)[:ml]
+        else:
+            res = dict(iters=np.zeros(0, np.int32), applies=np.zeros(0, np.int64), status=np.zeros(0, np.int32),
+                       relres=np.zeros(0), m_used=np.zeros(0, np.int32), prof=np.zeros(4))
+            rho_l = eta_l = np.zeros(0)
+        # ---- exchange (allgather) and the L-curve
+        if dist.enabled:
+            torch.cuda.synchronize(self.dev)
+            Xf = dist.gather_rows(X, owners, M)
+            Gf = dist.gather_rows(G, owners, M)
+            packed = np.stack([res["iters"], res["applies"], res["status"], res["relres"], res["m_used"],
+                               rho_l, eta_l, has_xp[mine]], 1) if ml else np.zeros((0, 8))
+            allp = dist.gather_np(packed, owners, M, self.dev)
+            iters, applies, status = allp[:, 0].astype(np.int64), allp[:, 1].astype(np.int64), allp[:, 2].astype(np.int64)
+            relres, m_used, rho, eta = allp[:, 3], allp[:, 4].astype(np.int64), allp[:, 5], allp[:, 6]
+            overhead = dist.bcast_int(overhead, self.dev)
+        else:
+            Xf, Gf = X, G
+            iters, applies, status = res["iters"], res["applies"], res["status"]
+            relres, m_used, rho, eta = res["relres"], res["m_used"], rho_l, eta_l
         lstar, _ = lcurve_corner(rho, eta)
         torch.cuda.synchronize(self.dev)
-        out = StepOut(k, res["iters"], res["applies"], res["status"], res["relres"], res["m_used"], nc,
-                      lstar, rho, eta, overhead, has_xp, keep, time.perf_counter() - t0, res["prof"])
-        nst = dict(X_prev=X, G_prev=G, V_i1=V_i1, xstar=X[lstar])
+        out = StepOut(k, iters, applies, status, relres, m_used, nc, lstar, rho, eta, overhead,
+                      has_xp, keep, time.perf_counter() - t0, res["prof"])
+        nst = dict(X_prev=Xf, G_prev=Gf, V_i1=V_i1, xstar=Xf[lstar], prev_iters=np.asarray(iters))
         return out, nst
 
     def next_weights(self, xstar: torch.Tensor):
