@@ -194,8 +194,8 @@ typedef struct {                /* host arrays [nshift], filled on return       
   int* status;                  /* RSK_CG_*                                      */
   int* m_used;                  /* recycle columns used                           */
   int* store_count;             /* residuals stored (RSK_CG_STORE_RES) or NULL   */
-  double* ms_loop;              /* RSK_CG_PROFILE: [4] = {apply kernel ms, update  */
-                                /*  kernels ms, unused, apply px-vectors}        */
+  double* ms_loop;              /* RSK_CG_PROFILE: [5] = {apply ms, update ms,     */
+                                /*  apply launches, apply px-vectors, combine ms} */
 } rsk_cg_out;
 
 size_t rsk_cg_workspace_bytes(rsk_handle h, int nshift, int flags);

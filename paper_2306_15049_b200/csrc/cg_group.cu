@@ -50,6 +50,14 @@ constexpr int kLvl = 16;        // chunks per level-1 group
 constexpr int kSub = 256;       // rows per combine sub-slab (= threads)
 constexpr int kHalf = 128;      // rows per update sub-slab (2 threads per row)
 constexpr int kHP = kHalf + 1;  // odd pitch
+constexpr int kQ = 64;          // rows per update sub-slab (cp.async staged)
+constexpr int kQP = kQ + 1;     // odd pitch
+
+__device__ __forceinline__ void cp_async8g(double* sdst, const double* gsrc, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  const int sz = valid ? 8 : 0;
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(gsrc), "r"(sz) : "memory");
+}
 
 // sum `cnt` partial blocks (kPV x 32 each, stride kPV*32) into dst, fixed order, with
 // every thread loading its (value, block) pairs before adding
@@ -77,8 +85,8 @@ struct TileInfo {
 }  // namespace
 
 // ------------------------------------------------------------------ KB (update)
-__global__ void __launch_bounds__(kNT, 2) cg_update_grp(CgDev* __restrict__ cg) {
-  // dynamic smem: sA [2J][kHP] | sR [32][kHP] | sZ [32][kHP]
+__global__ void __launch_bounds__(kNT, 3) cg_update_grp(CgDev* __restrict__ cg) {
+  // dynamic smem: sA [32][kQP] | sR [32][kQP] | sW [32][kQP] | sZ [32][kQP]
   extern __shared__ double dsm[];
   __shared__ TileInfo ti;
   __shared__ double tot[kPV * 32];
@@ -90,8 +98,9 @@ __global__ void __launch_bounds__(kNT, 2) cg_update_grp(CgDev* __restrict__ cg) 
   const int J = cg->grp.J[g];
   const int J2 = 2 * J;
   double* sA = dsm;
-  double* sR = dsm + J2 * kHP;
-  double* sZ = sR + 32 * kHP;
+  double* sR = dsm + 32 * kQP;
+  double* sWv = sR + 32 * kQP;
+  double* sZ = sWv + 32 * kQP;
   const int64_t N = cg->N;
   const int64_t ldw = cg->grp.ldw;
   const double* __restrict__ AW = cg->grp.AW[g];
@@ -107,15 +116,17 @@ __global__ void __launch_bounds__(kNT, 2) cg_update_grp(CgDev* __restrict__ cg) 
     ti.hasg[tid] = v ? cg->hasg[s] : 0;
   }
   __syncthreads();
-  // streaming role: row sr (of kHalf), shifts k = sh + 2u
-  const int sr = tid & (kHalf - 1), sh = tid >> 7;
-  // rho / zeta role: shift tk, 16-row segment tseg
+  bool anyz = false;
+  for (int k = 0; k < S; ++k) anyz |= (ti.hasg[k] != 0);
+  // update role: row ur (of kQ), shifts k = uq + 4u
+  const int ur = tid & (kQ - 1), uq = tid >> 6;
+  // rho / zeta role: shift tk, 8-row segment tseg
   const int tk = tid & 31, tseg = tid >> 5;
   double prho = 0.0, pzet = 0.0;
   // GEMM role: k-block kb (4 shifts), j-block jb (4 rows of [AW;EW]), row group rg
   const int njb = (J2 > 16) ? 8 : 4;
   const int nrg = 32 / njb;
-  const int rpg = kHalf / nrg;
+  const int rpg = kQ / nrg;
   const int kb = tid & 7, jb = (tid >> 3) & (njb - 1), rg = (tid >> 3) / njb;
   double acc[4][4];
 #pragma unroll
@@ -125,63 +136,60 @@ __global__ void __launch_bounds__(kNT, 2) cg_update_grp(CgDev* __restrict__ cg) 
 
   const int64_t rbeg = (int64_t)chunk * cg->rowsG;
   const int64_t rend = min(N, rbeg + cg->rowsG);
-  for (int64_t r0 = rbeg; r0 < rend; r0 += kHalf) {
-    const int64_t i = r0 + sr;
-    const bool rin = i < rend;
-    // stage the [AW; EW] sub-slab (rows split over the two halves)
-    for (int j = sh; j < J2; j += 2)
-      sA[j * kHP + sr] = rin ? __ldg((j < J ? AW + (int64_t)j * ldw : EW + (int64_t)(j - J) * ldw) + i) : 0.0;
-    // streaming pass: loads -> shared memory only (no global stores: loads can be hoisted)
-#pragma unroll
-    for (int u0 = 0; u0 < 16; u0 += 4) {
-      double rv[4], wv[4], zv[4];
-#pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int k = sh + 2 * (u0 + v);
-        rv[v] = wv[v] = zv[v] = 0.0;
-        if (k < S && rin) {
-          const int64_t off = (int64_t)ti.sid[k] * N + i;
-          rv[v] = __ldcg(cg->R + off);
-          wv[v] = __ldcg(cg->Wv + off);
-          if (ti.hasg[k]) zv[v] = __ldg(cg->ZGhat + (int64_t)ti.sid[k] * cg->ldgh + i);
-        }
+  for (int64_t r0 = rbeg; r0 < rend; r0 += kQ) {
+    // ---- stage every operand of the sub-slab with cp.async (all loads in flight at once)
+    const int nrow = (int)min((int64_t)kQ, rend - r0);
+    for (int e = tid; e < J2 * kQ; e += kNT) {
+      const int j = e / kQ, rr = e - j * kQ;
+      const bool v = rr < nrow;
+      const double* src = (j < J ? AW + (int64_t)j * ldw : EW + (int64_t)(j - J) * ldw) + r0 + rr;
+      cp_async8g(sA + j * kQP + rr, v ? src : AW, v);
+    }
+    for (int e = tid; e < S * kQ; e += kNT) {
+      const int k = e / kQ, rr = e - k * kQ;
+      const bool v = rr < nrow;
+      const int64_t off = (int64_t)ti.sid[k] * N + r0 + rr;
+      cp_async8g(sR + k * kQP + rr, v ? cg->R + off : cg->R, v);
+      cp_async8g(sWv + k * kQP + rr, v ? cg->Wv + off : cg->Wv, v);
+      if (anyz) {
+        const bool vz = v && ti.hasg[k];
+        cp_async8g(sZ + k * kQP + rr, vz ? cg->ZGhat + (int64_t)ti.sid[k] * cg->ldgh + r0 + rr : cg->R, vz);
       }
+    }
+    asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+    // ---- r' = r - alpha w (in shared memory), write back, zeta products
+    const int64_t i = r0 + ur;
 #pragma unroll
-      for (int v = 0; v < 4; ++v) {
-        const int k = sh + 2 * (u0 + v);
-        if (k < S) {
-          const double rn = fma(-ti.al[k], wv[v], rv[v]);
-          sR[k * kHP + sr] = rn;
-          sZ[k * kHP + sr] = zv[v] * rn;
-        }
+    for (int u = 0; u < 8; ++u) {
+      const int k = uq + 4 * u;
+      if (k < S) {
+        const double rn = fma(-ti.al[k], sWv[k * kQP + ur], sR[k * kQP + ur]);
+        sR[k * kQP + ur] = rn;
+        if (anyz) sZ[k * kQP + ur] *= rn;
+        if (ti.act[k] && ur < nrow) cg->R[(int64_t)ti.sid[k] * N + i] = rn;
       }
     }
     __syncthreads();
-    // write the updated residuals back (coalesced)
-#pragma unroll 4
-    for (int u = 0; u < 16; ++u) {
-      const int k = sh + 2 * u;
-      if (k < S && ti.act[k] && rin) cg->R[(int64_t)ti.sid[k] * N + i] = sR[k * kHP + sr];
-    }
-    // rho, zeta partials over this thread's 16-row segment
+    // ---- rho, zeta partials over this thread's 8-row segment
     if (tk < S) {
 #pragma unroll
-      for (int q = 0; q < 16; ++q) {
-        const double rn = sR[tk * kHP + tseg * 16 + q];
+      for (int q = 0; q < 8; ++q) {
+        const double rn = sR[tk * kQP + tseg * 8 + q];
         prho = fma(rn, rn, prho);
-        pzet += sZ[tk * kHP + tseg * 16 + q];
+        if (anyz) pzet += sZ[tk * kQP + tseg * 8 + q];
       }
     }
-    // GEMM over this sub-slab: acc[a][b] += sum_rows sA[4jb+a][row] * sR[4kb+b][row]
+    // ---- GEMM over this sub-slab: acc[a][b] += sum_rows sA[4jb+a][row] * sR[4kb+b][row]
     if (4 * jb < J2 && 4 * kb < S) {
 #pragma unroll 4
       for (int rr = 0; rr < rpg; ++rr) {
         const int row = rg * rpg + rr;
         double av[4], bv[4];
 #pragma unroll
-        for (int a = 0; a < 4; ++a) av[a] = sA[min(4 * jb + a, J2 - 1) * kHP + row];
+        for (int a = 0; a < 4; ++a) av[a] = sA[min(4 * jb + a, J2 - 1) * kQP + row];
 #pragma unroll
-        for (int b = 0; b < 4; ++b) bv[b] = sR[(4 * kb + b) * kHP + row];
+        for (int b = 0; b < 4; ++b) bv[b] = sR[(4 * kb + b) * kQP + row];
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
@@ -191,8 +199,9 @@ __global__ void __launch_bounds__(kNT, 2) cg_update_grp(CgDev* __restrict__ cg) 
     __syncthreads();
   }
   // ---- CTA-level reductions (once per chunk), fixed order through shared memory
-  double* red = sR;                  // [nrg][4 njb][33] = 4224 doubles (inside sR | sZ)
-  double* red2 = sZ + 256;           // [8][64]
+  double* red = sR;                  // [nrg][4 njb][33] = 4224 doubles (spans sR | sWv | sZ head)
+  double* red2 = sA;                 // [8][64] (sA is free after the last sub-slab)
+  static_assert(3 * 32 * kQP >= 4224 && 32 * kQP >= 512, "reduction scratch");
   const int RJ = 4 * njb;
 #pragma unroll
   for (int a = 0; a < 4; ++a)
@@ -335,44 +344,52 @@ __global__ void __launch_bounds__(kNT) cg_combine_grp(CgDev* __restrict__ cg) {
     double wv[16];
 #pragma unroll
     for (int j = 0; j < 16; ++j) wv[j] = j < J ? __ldg(W + (int64_t)j * ldw + i) : 0.0;
+    // software-pipelined over 4-shift batches: the loads of batch b+1 are issued before
+    // the stores of batch b (program order keeps possibly-aliasing accesses in place)
+    double buf[2][4][4];   // [parity][p, x, r, ghat][shift in batch]
+    auto ld = [&](int k0, double (*v)[4]) {
 #pragma unroll
-    for (int k0 = 0; k0 < 32; k0 += 4) {
-      if (k0 < S) {
-        double pv[4], xv[4], rv[4], gv[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int k = k0 + u;
-          pv[u] = xv[u] = rv[u] = gv[u] = 0.0;
-          if (k < S && ci.mode[k]) {
-            const int s = ci.sid[k];
-            pv[u] = cg->P[(int64_t)s * N + i];
-            xv[u] = cg->X[(int64_t)s * cg->ldx + i];
-            if (ci.mode[k] == 2) {
-              rv[u] = cg->R[(int64_t)s * N + i];
-              if (ci.hasg[k]) gv[u] = __ldg(cg->Ghat + (int64_t)s * cg->ldgh + i);
-            }
-          }
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int k = k0 + u;
-          if (k < S && ci.mode[k]) {
-            const int s = ci.sid[k];
-            cg->X[(int64_t)s * cg->ldx + i] = fma(ci.al[k], pv[u], xv[u]);
-            if (ci.mode[k] == 2) {
-              double pn = fma(ci.be[k], pv[u], rv[u]);
-              const int nw = ci.nw[k];
-#pragma unroll
-              for (int j = 0; j < 16; ++j)
-                if (j < nw) pn = fma(-sMu[k][j], wv[j], pn);
-              if (ci.hasg[k]) pn = fma(-sMu[k][nw], gv[u], pn);
-              cg->P[(int64_t)s * N + i] = pn;
-              if (ci.sto[k] >= 0)
-                cg->store[((int64_t)s * cg->store_cap + ci.sto[k]) * cg->lds + i] = rv[u] * ci.rinv[k];
-            }
+      for (int u = 0; u < 4; ++u) {
+        const int k = k0 + u;
+        v[0][u] = v[1][u] = v[2][u] = v[3][u] = 0.0;
+        if (k < S && ci.mode[k]) {
+          const int s = ci.sid[k];
+          v[0][u] = cg->P[(int64_t)s * N + i];
+          v[1][u] = cg->X[(int64_t)s * cg->ldx + i];
+          if (ci.mode[k] == 2) {
+            v[2][u] = cg->R[(int64_t)s * N + i];
+            if (ci.hasg[k]) v[3][u] = __ldg(cg->Ghat + (int64_t)s * cg->ldgh + i);
           }
         }
       }
+    };
+    auto st = [&](int k0, double (*v)[4]) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = k0 + u;
+        if (k < S && ci.mode[k]) {
+          const int s = ci.sid[k];
+          cg->X[(int64_t)s * cg->ldx + i] = fma(ci.al[k], v[0][u], v[1][u]);
+          if (ci.mode[k] == 2) {
+            double pn = fma(ci.be[k], v[0][u], v[2][u]);
+            const int nw = ci.nw[k];
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (j < nw) pn = fma(-sMu[k][j], wv[j], pn);
+            if (ci.hasg[k]) pn = fma(-sMu[k][nw], v[3][u], pn);
+            cg->P[(int64_t)s * N + i] = pn;
+            if (ci.sto[k] >= 0)
+              cg->store[((int64_t)s * cg->store_cap + ci.sto[k]) * cg->lds + i] = v[2][u] * ci.rinv[k];
+          }
+        }
+      }
+    };
+    ld(0, buf[0]);
+#pragma unroll
+    for (int k0 = 0; k0 < 32; k0 += 4) {
+      if (k0 >= S) break;
+      if (k0 + 4 < S) ld(k0 + 4, buf[((k0 >> 2) + 1) & 1]);
+      st(k0, buf[(k0 >> 2) & 1]);
     }
   }
   __threadfence();
@@ -393,7 +410,7 @@ __global__ void __launch_bounds__(kNT) cg_combine_grp(CgDev* __restrict__ cg) {
   }
 }
 
-static size_t update_smem() { return sizeof(double) * (32 + 32 + 32) * kHP; }
+static size_t update_smem() { return sizeof(double) * 4 * 32 * kQP; }
 
 cudaError_t launch_cg_update_grp(CgDev* dev, const CgDev& host, int ngroups, int maxtiles, cudaStream_t st) {
   static bool attr = false;

@@ -685,10 +685,10 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
   std::vector<int> confirms(ns, 0);
   const int ce = d->check_every;
   std::vector<cudaEvent_t> evs;
-  double ms_apply = 0.0, ms_upd = 0.0;
+  double ms_apply = 0.0, ms_upd = 0.0, ms_cmb = 0.0;
   int64_t n_ka = 0;
   if (prof) {
-    evs.resize(3 * ce);
+    evs.resize(4 * ce);
     for (auto& e : evs) RSK_CUDA(cudaEventCreate(&e));
   }
   std::vector<int> stat_h(ns), it_h(ns);
@@ -706,17 +706,18 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
   auto enqueue_chunk = [&](int na_host) -> cudaError_t {
     for (int i = 0; i < ce; ++i) {
       cudaError_t e;
-      if (prof && (e = cudaEventRecord(evs[3 * i], st)) != cudaSuccess) return e;
+      if (prof && (e = cudaEventRecord(evs[4 * i], st)) != cudaSuccess) return e;
       ApplyLaunch a{};
       a.X = hc.P; a.ldx = N; a.Y = hc.Wv; a.ldy = N; a.gamma = hc.gam; a.list = hc.glist;
       a.nlist = use_graph ? ns : na_host;
       a.nlist_dev = use_graph ? hc.gmeta + 8 : nullptr;
       a.mode = RSK_APPLY_SHIFTED; a.cg = dev; a.cg_alpha = true;
       if ((e = launch_apply(h, a, st)) != cudaSuccess) return e;
-      if (prof && (e = cudaEventRecord(evs[3 * i + 1], st)) != cudaSuccess) return e;
+      if (prof && (e = cudaEventRecord(evs[4 * i + 1], st)) != cudaSuccess) return e;
       if ((e = launch_cg_update_grp(dev, hc, ngrp, L.maxtilesG, st)) != cudaSuccess) return e;
+      if (prof && (e = cudaEventRecord(evs[4 * i + 2], st)) != cudaSuccess) return e;
       if ((e = launch_cg_combine_grp(dev, hc, ngrp, L.maxtilesG, st)) != cudaSuccess) return e;
-      if (prof && (e = cudaEventRecord(evs[3 * i + 2], st)) != cudaSuccess) return e;
+      if (prof && (e = cudaEventRecord(evs[4 * i + 3], st)) != cudaSuccess) return e;
     }
     return cudaSuccess;
   };
@@ -758,10 +759,13 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
     if (prof) {
       for (int i = 0; i < ce; ++i) {
         float t1 = 0, t2 = 0;
-        cudaEventElapsedTime(&t1, evs[3 * i], evs[3 * i + 1]);
-        cudaEventElapsedTime(&t2, evs[3 * i + 1], evs[3 * i + 2]);
+        float t3 = 0;
+        cudaEventElapsedTime(&t1, evs[4 * i], evs[4 * i + 1]);
+        cudaEventElapsedTime(&t2, evs[4 * i + 1], evs[4 * i + 2]);
+        cudaEventElapsedTime(&t3, evs[4 * i + 2], evs[4 * i + 3]);
         ms_apply += t1;
         ms_upd += t2;
+        ms_cmb += t3;
       }
     }
     // confirm the shifts whose recursive residual converged
@@ -845,6 +849,7 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
     o->ms_loop[1] = ms_upd;
     o->ms_loop[2] = (double)n_ka;
     o->ms_loop[3] = (double)tot_it * (double)N;
+    o->ms_loop[4] = ms_cmb;
   }
   RSK_CUDA(cudaStreamSynchronize(st));
   return all_ok ? RSK_OK : RSK_EPARTIAL;

@@ -146,7 +146,7 @@ class GpuSolver:
         out = L.CgOut()
         iters = np.zeros(ns, dtype=np.int32); apl = np.zeros(ns, dtype=np.int64)
         rel = np.zeros(ns); stt = np.zeros(ns, dtype=np.int32); mu = np.zeros(ns, dtype=np.int32)
-        sc = np.zeros(ns, dtype=np.int32); ms = np.zeros(4)
+        sc = np.zeros(ns, dtype=np.int32); ms = np.zeros(5)
         P = L.C.POINTER
         out.iters = iters.ctypes.data_as(P(L.C.c_int)); out.applies = apl.ctypes.data_as(P(L.C.c_int64))
         out.relres_true = rel.ctypes.data_as(L._hp); out.status = stt.ctypes.data_as(P(L.C.c_int))
@@ -306,7 +306,7 @@ class GpuSolver:
             rho_l, eta_l = _host(self.rho_dev)[:ml], _host(self.eta_dev)[:ml]
         else:
             res = dict(iters=np.zeros(0, np.int32), applies=np.zeros(0, np.int64), status=np.zeros(0, np.int32),
-                       relres=np.zeros(0), m_used=np.zeros(0, np.int32), prof=np.zeros(4))
+                       relres=np.zeros(0), m_used=np.zeros(0, np.int32), prof=np.zeros(5))
             rho_l = eta_l = np.zeros(0)
         # ---- exchange (allgather) and the L-curve
         if dist.enabled:
