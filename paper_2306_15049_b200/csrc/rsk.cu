@@ -143,6 +143,21 @@ extern "C" rsk_status rsk_create(rsk_handle* out, int device, int64_t ny, int64_
             cudaMalloc(&h->aux, kAuxBytes) == cudaSuccess &&
             cudaStreamCreateWithFlags(&h->cg_stream, cudaStreamNonBlocking) == cudaSuccess;
   if (!ok) { rsk_destroy(h); return RSK_ENOMEM; }
+  {
+    const int tyr = apply_tile_rows(r);
+    const int64_t nbx = (nx + kTX - 1) / kTX * (kTX / 8);
+    const int64_t nby = (ny + tyr - 1) / tyr * (tyr / 8);
+    std::vector<double> fx, fy;
+    build_frag_tables(r, nx, nbx, tx.data(), fx);
+    build_frag_tables(r, ny, nby, ty.data(), fy);
+    apply_interior_blocks(r, nx, &h->bx_lo, &h->bx_hi);
+    apply_interior_blocks(r, ny, &h->by_lo, &h->by_hi);
+    ok = cudaMalloc(&h->fragx, sizeof(double) * fx.size()) == cudaSuccess &&
+         cudaMalloc(&h->fragy, sizeof(double) * fy.size()) == cudaSuccess &&
+         cudaMemcpy(h->fragx, fx.data(), sizeof(double) * fx.size(), cudaMemcpyHostToDevice) == cudaSuccess &&
+         cudaMemcpy(h->fragy, fy.data(), sizeof(double) * fy.size(), cudaMemcpyHostToDevice) == cudaSuccess;
+    if (!ok) { rsk_destroy(h); return RSK_ENOMEM; }
+  }
   std::vector<double> w((size_t)N);
   ok = cudaMemcpy(h->tabBx, tx.data(), sizeof(double) * tx.size(), cudaMemcpyHostToDevice) == cudaSuccess &&
        cudaMemcpy(h->tabBy, ty.data(), sizeof(double) * ty.size(), cudaMemcpyHostToDevice) == cudaSuccess;
@@ -163,6 +178,8 @@ extern "C" rsk_status rsk_destroy(rsk_handle h) {
   cudaSetDevice(h->device);
   cudaFree(h->tabBx);
   cudaFree(h->tabBy);
+  cudaFree(h->fragx);
+  cudaFree(h->fragy);
   cudaFree(h->wx);
   cudaFree(h->wy);
   cudaFree(h->scratch);
@@ -663,7 +680,7 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
     RSK_CUDA(upload_list(dlist2, withxp));
     ApplyLaunch a{};
     a.X = d->X; a.ldx = d->ldx; a.Y = hc.Wv; a.ldy = N; a.gamma = hc.gam; a.list = dlist2;
-    a.nlist = (int)withxp.size(); a.mode = RSK_APPLY_SHIFTED;
+    a.nlist = (int)withxp.size(); a.mode = RSK_APPLY_SHIFTED; a.nvec_total = ns;
     RSK_CUDA(launch_apply(h, a, st));
     for (int s : withxp) applies[s] += 1;
   }
@@ -709,7 +726,7 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
       if (prof && (e = cudaEventRecord(evs[4 * i], st)) != cudaSuccess) return e;
       ApplyLaunch a{};
       a.X = hc.P; a.ldx = N; a.Y = hc.Wv; a.ldy = N; a.gamma = hc.gam; a.list = hc.glist;
-      a.nlist = use_graph ? ns : na_host;
+      a.nlist = use_graph ? ns : na_host; a.nvec_total = ns;
       a.nlist_dev = use_graph ? hc.gmeta + 8 : nullptr;
       a.mode = RSK_APPLY_SHIFTED; a.cg = dev; a.cg_alpha = true;
       if ((e = launch_apply(h, a, st)) != cudaSuccess) return e;
@@ -776,7 +793,7 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
       RSK_CUDA(upload_list(dlist2, conf));
       ApplyLaunch a{};
       a.X = d->X; a.ldx = d->ldx; a.Y = hc.Wv; a.ldy = N; a.gamma = hc.gam; a.list = dlist2;
-      a.nlist = (int)conf.size(); a.mode = RSK_APPLY_SHIFTED;
+      a.nlist = (int)conf.size(); a.mode = RSK_APPLY_SHIFTED; a.nvec_total = ns;
       RSK_CUDA(launch_apply(h, a, st));
       RSK_CUDA(launch_cg_combine(dev, hc, dlist2, (int)conf.size(), CMB_RESID, st));
       RSK_CUDA(launch_cg_update(dev, hc, dlist2, (int)conf.size(), UPD_CONFIRM, st));
@@ -809,7 +826,7 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
     RSK_CUDA(upload_list(dlist2, unconf));
     ApplyLaunch a{};
     a.X = d->X; a.ldx = d->ldx; a.Y = hc.Wv; a.ldy = N; a.gamma = hc.gam; a.list = dlist2;
-    a.nlist = (int)unconf.size(); a.mode = RSK_APPLY_SHIFTED;
+    a.nlist = (int)unconf.size(); a.mode = RSK_APPLY_SHIFTED; a.nvec_total = ns;
     RSK_CUDA(launch_apply(h, a, st));
     RSK_CUDA(launch_cg_combine(dev, hc, dlist2, (int)unconf.size(), CMB_RESID, st));
     double* dd = h->aux + 2 * 256 * 256 + 4096;

@@ -102,6 +102,9 @@ struct Handle {
   double cTx[kMaxTaps], cTy[kMaxTaps];      // taps of C^T (window form)
   double* tabBx = nullptr;    // [nx][4r+1]
   double* tabBy = nullptr;    // [ny][4r+1]
+  double* fragx = nullptr;    // fragment-ordered B_x rows per 8-column block (apply_core.cuh)
+  double* fragy = nullptr;    // fragment-ordered B_y rows per 8-row block
+  int bx_lo = 0, bx_hi = -1, by_lo = 0, by_hi = -1;  // interior block ranges
   double* wx = nullptr;       // weights copy
   double* wy = nullptr;
   double* scratch = nullptr;  // reduction scratch
@@ -128,9 +131,15 @@ struct ApplyLaunch {
   CgDev* cg;                  // nullable => plain apply; else CG "w = A p" step
   bool cg_alpha;              // CG: compute alpha = rho / (p.w) in last CTA
   const int* nlist_dev;       // nullable: list length read on the device (graph replay)
+  const double* X2; int64_t ldx2;  // CG: source of items whose shift is ST_RCONV (confirm)
+  bool src2_rconv;
+  int nvec_total;              // vectors addressable in X (and X2): TMA map extent
 };
 cudaError_t launch_apply(Handle* h, const ApplyLaunch& a, cudaStream_t st);
 int apply_tiles(const Handle* h);
+int apply_tile_rows(int r);
+void build_frag_tables(int r, int64_t n, int64_t nblk, const double* tab, std::vector<double>& out);
+void apply_interior_blocks(int r, int64_t n, int* lo, int* hi);
 
 // ---- vector kernels (vec.cu)
 cudaError_t launch_gemm_tn(Handle* h, int64_t n, int k, const double* U, int64_t ldu, int nv,
