@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librsk.so")
-SOURCES = ["apply.cu", "vec.cu", "cg_group.cu", "rsk.cu", "host_dense.cpp"]
+SOURCES = ["apply.cu", "cg_persist.cu", "cg_cluster.cu", "vec.cu", "cg_group.cu", "rsk.cu", "host_dense.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
@@ -27,6 +27,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB
     objs = []
     os.makedirs(os.path.join(HERE, "build"), exist_ok=True)
+    cmds = []
     for src in SOURCES:
         obj = os.path.join(HERE, "build", src + ".o")
         cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
@@ -34,12 +35,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if src.endswith(".cpp"):
             cmd = [NVCC, "-O3", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-x", "c++", "-c",
                    os.path.join(CSRC, src), "-o", obj]
-        r = subprocess.run(cmd, capture_output=True, text=True)
+        cmds.append((src, cmd))
+        objs.append(obj)
+    from concurrent.futures import ThreadPoolExecutor
+    with ThreadPoolExecutor(max_workers=len(cmds)) as ex:
+        results = list(ex.map(lambda sc: (sc[0], subprocess.run(sc[1], capture_output=True, text=True)), cmds))
+    for src, r in results:
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stdout}\n{r.stderr}")
         if verbose:
             sys.stderr.write(r.stderr)
-        objs.append(obj)
     tmp = LIB + ".tmp"
     cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcudart"]
     r = subprocess.run(cmd, capture_output=True, text=True)

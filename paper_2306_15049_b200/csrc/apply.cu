@@ -19,13 +19,13 @@ template <int R, bool kTma>
 __global__ void __launch_bounds__(kAT, kApplyCtasPerSm) apply_kernel(const __grid_constant__ ApplyParams p) {
   extern __shared__ __align__(128) double smem[];
   using Core = ApplyCore<R, kTma>;
-  Core::init_bars(smem);
+  Core::init_bars(smem, p);
   const int nl = p.nlist_dev ? *p.nlist_dev : p.nlist;
   const int nitems = nl * p.ntiles;
   const int per = (nitems + gridDim.x - 1) / gridDim.x;
   const int ibeg = blockIdx.x * per;
   const int iend = min(nitems, ibeg + per);
-  ApplyPipe pp{0u};
+  ApplyPipe pp{{0u, 0u}, 0};
   Core::run(p, smem, ibeg, iend, nl, pp);
 }
 
@@ -40,6 +40,28 @@ __global__ void apply_dot_reduce(const double* part, int ntiles, const int* list
 }
 
 int apply_tile_rows(int r) { return tc_tile_rows(r); }
+
+// optional per-phase timestamps of block 0 (RSK_APPLY_PROF=1; debugging only)
+static unsigned long long* apply_prof_buf() {
+  static unsigned long long* ap = nullptr;
+  static int on = -1;
+  if (on < 0) {
+    on = getenv("RSK_APPLY_PROF") ? 1 : 0;
+    if (on && cudaMalloc(&ap, 8 * sizeof(unsigned long long)) == cudaSuccess)
+      cudaMemset(ap, 0, 8 * sizeof(unsigned long long));
+  }
+  return ap;
+}
+
+extern "C" int rsk_debug_apply_prof(double* out8, int reset) {
+  unsigned long long* ap = apply_prof_buf();
+  if (!ap) return -1;
+  unsigned long long v[8];
+  if (cudaMemcpy(v, ap, sizeof(v), cudaMemcpyDeviceToHost) != cudaSuccess) return -1;
+  for (int i = 0; i < 8; ++i) out8[i] = (double)v[i];
+  if (reset) cudaMemset(ap, 0, sizeof(v));
+  return 0;
+}
 
 int apply_tiles(const Handle* h) {
   const int ty = tc_tile_rows(h->r);
@@ -89,31 +111,6 @@ bool make_map2(CUtensorMap* m, const double* base, int64_t nx, int64_t ny, int b
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// ---------------------------------------------------------------- edge fragment tables
-// fragx[b][ks][lane] = Bx(row col = 8b + g, tap t = 4ks + q - g) (0 outside the band or
-// the image), for every 8-column block of the tiled width; fragy likewise for rows.
-void build_frag_tables(int r, int64_t n, int64_t nblk, const double* tab, std::vector<double>& out) {
-  const int T = 4 * r + 1, KS = r + 2;
-  out.assign((size_t)nblk * KS * 32, 0.0);
-  for (int64_t b = 0; b < nblk; ++b)
-    for (int ks = 0; ks < KS; ++ks)
-      for (int lane = 0; lane < 32; ++lane) {
-        const int g = lane >> 2, q = lane & 3;
-        const int64_t col = 8 * b + g;
-        const int t = 4 * ks + q - g;
-        double v = 0.0;
-        if (t >= 0 && t < T && col < n) v = tab[(size_t)col * T + t];
-        out[((size_t)b * KS + ks) * 32 + lane] = v;
-      }
-}
-
-void apply_interior_blocks(int r, int64_t n, int* lo, int* hi) {
-  // block b is interior iff every index i in [8b, 8b+8) has 2r <= i <= n-1-2r
-  *lo = (2 * r + 7) / 8;
-  const int64_t last = n - 1 - 2 * r - 7;
-  *hi = last >= 0 ? (int)(last / 8) : -1;
-}
-
 // ---------------------------------------------------------------- launch
 template <int R>
 static cudaError_t launch_r(const ApplyParams& prm, bool tma, int sm_count, cudaStream_t st) {
@@ -146,7 +143,7 @@ bool fill_apply_params(Handle* h, const ApplyLaunch& a, ApplyParams& prm) {
   prm.gamma = a.gamma;
   prm.list = a.list;
   prm.wx = h->wx; prm.wy = h->wy;
-  prm.fragx = h->fragx; prm.fragy = h->fragy;
+  prm.dcorr = h->dcorr;
   prm.cg = a.cg;
   prm.ny = (int)h->ny; prm.nx = (int)h->nx;
   prm.tiles_x = (int)((h->nx + kTX - 1) / kTX);
@@ -158,17 +155,17 @@ bool fill_apply_params(Handle* h, const ApplyLaunch& a, ApplyParams& prm) {
   prm.src2_rconv = a.src2_rconv ? 1 : 0;
   prm.want_dot = (a.xdoty != nullptr || a.cg_alpha) ? 1 : 0;
   prm.part = h->scratch;
-  prm.bx_lo = h->bx_lo; prm.bx_hi = h->bx_hi;
-  prm.by_lo = h->by_lo; prm.by_hi = h->by_hi;
+  prm.aprof = apply_prof_buf();
+  prm.aprof_block = getenv("RSK_APPLY_PROF") ? atoi(getenv("RSK_APPLY_PROF")) : -1;
   const int T = 4 * h->r + 1;
   if (a.mode == RSK_APPLY_C_ONLY) {
-    prm.use_tab = 0;
+    prm.edge_fix = 0;
     for (int t = 0; t < T; ++t) { prm.cx[t] = h->cCx[t]; prm.cy[t] = h->cCy[t]; }
   } else if (a.mode == RSK_APPLY_CT_ONLY) {
-    prm.use_tab = 0;
+    prm.edge_fix = 0;
     for (int t = 0; t < T; ++t) { prm.cx[t] = h->cTx[t]; prm.cy[t] = h->cTy[t]; }
   } else {
-    prm.use_tab = 1;
+    prm.edge_fix = 1;
     for (int t = 0; t < T; ++t) { prm.cx[t] = h->cBx[t]; prm.cy[t] = h->cBy[t]; }
   }
   // TMA map (box = the staged halo tile); any failure -> cp.async path
@@ -177,7 +174,7 @@ bool fill_apply_params(Handle* h, const ApplyLaunch& a, ApplyParams& prm) {
   const int hy = ((ty + 4 * r + 7) / 8) * 8;
   const int px = pad4mod8(kTX + 4 * r);
   bool tma = getenv("RSK_NO_TMA") == nullptr;
-  const int64_t nv = a.list ? a.nvec_total : a.nlist;
+  const int64_t nv = (a.list || a.nvec_total > 0) ? a.nvec_total : a.nlist;
   tma = tma && make_map3(&prm.mapX, a.X, h->nx, h->ny, a.ldx, nv, px, hy);
   if (tma && a.X2) tma = make_map3(&prm.mapX2, a.X2, h->nx, h->ny, a.ldx2, nv, px, hy);
   return tma;

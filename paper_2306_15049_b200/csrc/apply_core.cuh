@@ -8,9 +8,10 @@
 //    A X = By X Bx, two banded passes of 4r+1 taps.
 //  * Both passes run on the FP64 tensor cores (mma.sync.m8n8k4.f64 -> DMMA): an 8x8
 //    output block of the x-pass is  S[8 rows][cb .. cb+8+4r) x Toeplitz(Bx)[(8+4r) x 8]
-//    (r+2 DMMA k-steps); the y-pass is Toeplitz(By) x T[(8+4r) x 8]. Interior blocks take
-//    the Toeplitz fragments from registers; blocks within 2r of an image edge (where the
-//    zero boundary truncates B) take them from a fragment-ordered table (coalesced LDG).
+//    (r+2 DMMA k-steps); the y-pass is Toeplitz(By) x T[(8+4r) x 8], Toeplitz fragments
+//    in registers. The zero boundary truncates B = G^T G only in an r x r corner at each
+//    end (B = Toeplitz - D_lo - D_hi, D_lo(c,m) = sum_{j<0} f[j-c+r] f[j-m+r]), so outputs
+//    within r of an edge get a small register-level correction instead of another path.
 //  * Work item = (tile, shift); tile = TY x 64 outputs; the halo tile HY x PX (HY =
 //    roundup8(TY + 4r), PX = 64 + 4r padded to 4 mod 8 doubles: conflict-free A-fragment
 //    loads) is fetched by ONE TMA box load (3-D map {nx, ny, vector}); out-of-image
@@ -44,18 +45,18 @@ struct alignas(64) ApplyParams {
   const int* list;
   const double* wx;
   const double* wy;
-  const double* fragx;  // [col block][KS][32] B_x fragments (A mode)
-  const double* fragy;  // [row block][KS][32] B_y fragments (A mode)
+  const double* dcorr;  // [4][kMaxR][kMaxR] zero-boundary corrections of B (see below)
   double* part;         // [list index][ntiles] (plain mode dot partials)
   CgDev* cg;
   int ny, nx, tiles_x, ntiles, nlist;
   const int* nlist_dev;  // if set, the list length is read on the device
   int mode;
-  int use_tab;   // 1: A (edge fragments from tables), 0: C / C^T (interior taps everywhere)
+  int edge_fix;  // 1: A (B truncated at the image edges), 0: C / C^T (exact with the zero halo)
   int want_dot;
   int cg_alpha;
   int src2_rconv;  // CG: items whose shift status is ST_RCONV read X2 (true-residual confirm)
-  int bx_lo, bx_hi, by_lo, by_hi;  // interior 8-column / 8-row block ranges (inclusive)
+  unsigned long long* aprof;       // optional per-phase ns of one block (RSK_APPLY_PROF=<block>)
+  int aprof_block;
   double cx[kMaxTaps];
   double cy[kMaxTaps];
 };
@@ -69,7 +70,8 @@ __host__ __device__ constexpr int pad4mod8(int w) { return w + ((4 - (w & 7)) & 
 __host__ __device__ constexpr int al16(int n) { return (n + 15) & ~15; }  // 128-byte multiples
 
 constexpr int kAT = 256;   // threads per apply CTA (8 warps); 2 CTAs per SM
-constexpr int kApplyCtasPerSm = 2;
+constexpr int kApplyCtasPerSm = 1;   // one CTA per SM: 255 registers, double-buffered stage
+constexpr int kStages = 2;
 
 template <int R>
 struct TcCfg {
@@ -87,10 +89,11 @@ struct TcCfg {
   static constexpr int KUY = 2 * RBY + R;    // y-pass B-fragment window (8 RBY + 4r rows)
   static constexpr int SBUF = al16(HY * PX);
   static constexpr int TBUF = al16(HY * PT);
-  static constexpr int OFF_T = SBUF;
+  static constexpr int OFF_T = kStages * SBUF;
   static constexpr int OFF_RED = OFF_T + TBUF;
-  static constexpr int OFF_BAR = OFF_RED + 16;        // 1 mbarrier (8 B)
-  static constexpr int DBL = OFF_BAR + 2;
+  static constexpr int OFF_DC = OFF_RED + 16;         // 4 r x r boundary corrections
+  static constexpr int OFF_BAR = OFF_DC + al16(4 * R * R);   // kStages mbarriers (8 B each)
+  static constexpr int DBL = OFF_BAR + kStages;
   static constexpr size_t SMEM = sizeof(double) * (size_t)DBL;
   static constexpr unsigned XBYTES = 8u * HY * PX;
   static_assert(TY >= 8 && TY % 8 == 0, "tile rows");
@@ -135,29 +138,35 @@ __device__ __forceinline__ void prefetch_l1(const void* p) {
 
 // mbarrier use counter (parity of the next wait); every thread runs the same sequence
 struct ApplyPipe {
-  unsigned use;
+  unsigned use[kStages];
+  int stage;   // stage buffer of the next item
 };
 
 template <int R, bool kTma>
 struct ApplyCore {
   using C = TcCfg<R>;
 
-  __device__ static void init_bars(double* smem) {
+  __device__ static void init_bars(double* smem, const ApplyParams& p) {
+    // boundary corrections of B (tiny, read at every edge output)
+    for (int e = threadIdx.x; e < 4 * R * R; e += blockDim.x) {
+      const int sl = e / (R * R), rem = e - sl * R * R, a = rem / R, b = rem - a * R;
+      smem[C::OFF_DC + e] = p.dcorr ? p.dcorr[((size_t)sl * kMaxR + a) * kMaxR + b] : 0.0;
+    }
     if (kTma && threadIdx.x == 0) {
-      mbar_init(reinterpret_cast<uint64_t*>(smem + C::OFF_BAR), 1);
+      for (int b = 0; b < kStages; ++b) mbar_init(reinterpret_cast<uint64_t*>(smem + C::OFF_BAR) + b, 1);
       mbar_fence_init();
     }
     __syncthreads();
   }
 
   // stage the halo tile of (tile, shift s)
-  __device__ static void issue_x(const ApplyParams& p, double* smem, int tile, int s, bool src2) {
-    double* S = smem;
+  __device__ static void issue_x(const ApplyParams& p, double* smem, int stage, int tile, int s, bool src2) {
+    double* S = smem + stage * C::SBUF;
     const int tyi = tile / p.tiles_x, txi = tile - tyi * p.tiles_x;
     const int gr0 = tyi * C::TY - C::H, gc0 = txi * kTX - C::H;
     if (kTma) {
       if (threadIdx.x == 0) {
-        uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
+        uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR) + stage;
         mbar_expect_tx(bar, C::XBYTES);
         tma_load_3d(S, src2 ? &p.mapX2 : &p.mapX, bar, gc0, gr0, s);
       }
@@ -195,8 +204,11 @@ struct ApplyCore {
   }
 
   // Process work items [ibeg, iend) of the tile-major item space item = tile * nl + li.
-  __device__ static void run(const ApplyParams& p, double* smem, int ibeg, int iend, int nl, ApplyPipe& pp) {
-    const double* S = smem;
+  // list / smode (optional, e.g. shared-memory snapshots) override p.list and the
+  // status-based choice of the source vector.
+  // dot_acc (optional): thread 0 accumulates the items' X.Y block sums in item order
+  __device__ __forceinline__ static void run(const ApplyParams& p, double* smem, int ibeg, int iend, int nl, ApplyPipe& pp,
+                             const int* list = nullptr, const int* smode = nullptr, double* dot_acc = nullptr) {
     double* Tm = smem + C::OFF_T;
     double* red = smem + C::OFF_RED;
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR);
@@ -210,42 +222,58 @@ struct ApplyCore {
     const int mode = p.mode;
     const bool withE = (mode == RSK_APPLY_SHIFTED || mode == RSK_APPLY_SPLIT);
     if (ibeg >= iend) return;
-    // interior Toeplitz fragments: x-pass B[k][n] = cx[k - n], y-pass A[m][k] = cy[k - m]
-    double bx[C::KS], ay[C::KS];
-#pragma unroll
-    for (int ks = 0; ks < C::KS; ++ks) {
-      const int t = 4 * ks + q - g;
-      bx[ks] = (t >= 0 && t < C::T) ? p.cx[t] : 0.0;
-      ay[ks] = (t >= 0 && t < C::T) ? p.cy[t] : 0.0;
-    }
-    auto sid_of = [&](int li) -> int { return p.list ? p.list[li] : li; };
-    auto src2_of = [&](int s) -> bool { return p.src2_rconv && p.cg->status[s] == ST_RCONV; };
+    const int* lst = list ? list : p.list;
+    auto sid_of = [&](int li) -> int { return lst ? lst[li] : li; };
+    auto src2_of = [&](int li, int s) -> bool {
+      return smode ? (smode[li] == ST_RCONV) : (p.src2_rconv && p.cg->status[s] == ST_RCONV);
+    };
 
-    int wtile = -1;
+    unsigned long long tp0 = 0;
+    auto amark = [&](int ph) {
+      if (p.aprof && (int)blockIdx.x == (p.aprof_block < 0 ? (int)gridDim.x / 2 : p.aprof_block) && tid == 0) {
+        unsigned long long t1;
+        asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t1));
+        if (tp0) atomicAdd(p.aprof + ph, t1 - tp0);
+        tp0 = t1;
+      }
+    };
+    amark(7);
     {
-      const int tile = ibeg / nl, s = sid_of(ibeg - tile * nl);
-      issue_x(p, smem, tile, s, src2_of(s));
+      const int tile = ibeg / nl, li0 = ibeg - tile * nl, s = sid_of(li0);
+      issue_x(p, smem, pp.stage, tile, s, src2_of(li0, s));
     }
     for (int it = ibeg; it < iend; ++it) {
       const int tile = it / nl, li = it - tile * nl;
       const int s = sid_of(li);
       const int tyi = tile / p.tiles_x, txi = tile - tyi * p.tiles_x;
       const int r0 = tyi * C::TY, c0 = txi * kTX;
-      if (withE && tile != wtile) {
-        prefetch_w(p, tile);
-        wtile = tile;
+      const int stage = pp.stage;
+      const bool more = it + 1 < iend;
+      if (more) {   // the other stage was released by the previous item's final barrier
+        const int t2 = (it + 1) / nl, l2 = it + 1 - t2 * nl, s2 = sid_of(l2);
+        issue_x(p, smem, stage ^ 1, t2, s2, src2_of(l2, s2));
       }
+      amark(0);
       if (kTma) {
-        mbar_wait(bar, pp.use & 1);
-        pp.use += 1;
+        mbar_wait(bar + stage, pp.use[stage] & 1);
+        pp.use[stage] += 1;
       } else {
-        cp_async_wait0();
+        if (more) cp_async_wait1(); else cp_async_wait0();
         __syncthreads();
       }
+      const double* S = smem + stage * C::SBUF;
+      amark(1);
 
       // ---- x-pass on the tensor cores: T[rb-rows][cols] = S[rb-rows][cols .. cols+8+4r) x Bx.
       // Work unit = (row block rb, half): 4 adjacent 8-column blocks share one window of
       // A fragments (32 + 4r columns = 8 + r k-steps), block c uses window steps 2c .. 2c+r+1.
+      // interior Toeplitz fragments: x-pass B[k][n] = cx[k - n] (from the parameter bank)
+      double bx[C::KS];
+#pragma unroll
+      for (int ks = 0; ks < C::KS; ++ks) {
+        const int t = 4 * ks + q - g;
+        bx[ks] = (t >= 0 && t < C::T) ? p.cx[t] : 0.0;
+      }
 #pragma unroll 1
       for (int u = warp; u < 2 * C::RBX; u += kAT / 32) {
         const int rb = u >> 1, half = u & 1;
@@ -257,18 +285,33 @@ struct ApplyCore {
         double d0[4], d1[4];
 #pragma unroll
         for (int c = 0; c < 4; ++c) { d0[c] = 0.0; d1[c] = 0.0; }
-        const int blk0 = (c0 + cl0) >> 3;
-        if (!p.use_tab || (blk0 >= p.bx_lo && blk0 + 3 <= p.bx_hi)) {
 #pragma unroll
-          for (int ks = 0; ks < C::KS; ++ks)
+        for (int ks = 0; ks < C::KS; ++ks)
 #pragma unroll
-            for (int c = 0; c < 4; ++c) dmma(d0[c], d1[c], a[2 * c + ks], bx[ks]);
-        } else {
+          for (int c = 0; c < 4; ++c) dmma(d0[c], d1[c], a[2 * c + ks], bx[ks]);
+        if (p.edge_fix) {
+          const int cu = c0 + cl0;   // first global column of the unit
+          if (cu < R || cu + 32 > nx - R) {
+            const double* srow = S + (rb * 8 + g) * C::PX - (c0 - C::H);   // srow[m] = x(row, m)
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const double* fb = p.fragx + (int64_t)(blk0 + c) * (C::KS * 32) + lane;
+            for (int c = 0; c < 4; ++c) {
 #pragma unroll
-            for (int ks = 0; ks < C::KS; ++ks) dmma(d0[c], d1[c], a[2 * c + ks], __ldg(fb + ks * 32));
+              for (int h2 = 0; h2 < 2; ++h2) {
+                const int col = cu + 8 * c + 2 * q + h2;
+                double corr = 0.0;
+                if (col < R) {
+                  const double* dl = smem + C::OFF_DC + col * R;
+#pragma unroll
+                  for (int m = 0; m < R; ++m) corr = fma(dl[m], srow[m], corr);
+                }
+                if (col >= nx - R && col < nx) {
+                  const double* dr = smem + C::OFF_DC + (R + col - (nx - R)) * R;
+#pragma unroll
+                  for (int m = 0; m < R; ++m) corr = fma(dr[m], srow[nx - R + m], corr);
+                }
+                if (h2 == 0) d0[c] -= corr; else d1[c] -= corr;
+              }
+            }
           }
         }
 #pragma unroll
@@ -278,15 +321,53 @@ struct ApplyCore {
         }
       }
       __syncthreads();
+      amark(2);
 
       // ---- y-pass on the tensor cores + fused epilogue: warp = 8-column block, all RBY
-      // row blocks share one window of T rows (B fragments).
+      // row blocks share one window of T rows (B fragments). The weights of the first
+      // EJ row blocks are requested before the DMMAs so their latency hides behind them.
       const int cbl = warp * 8;
       const double gm = (mode == RSK_APPLY_SHIFTED) ? __ldg(p.gamma + s) : 0.0;
       double* __restrict__ ys = p.Y + (int64_t)s * p.ldy;
       double* __restrict__ eys = (mode == RSK_APPLY_SPLIT) ? p.EY + (int64_t)s * p.ldey : nullptr;
       double dot = 0.0;
       {
+        const bool vec = ((nx & 1) == 0);
+        const int lc = cbl + 2 * q;
+        const int gj = c0 + lc;
+        constexpr int EJ = C::RBY;   // all weight loads issued before the y-pass DMMAs
+        double wl[EJ], wm[EJ], wr[EJ], yu0[EJ], yu1[EJ], yd0[EJ], yd1[EJ];
+        auto load_w = [&](int j, int jj) {
+          const int gi = r0 + j * 8 + g;
+          const bool v0 = gi < ny && gj < nx, v1 = gi < ny && gj + 1 < nx;
+          wl[jj] = wm[jj] = wr[jj] = yu0[jj] = yu1[jj] = yd0[jj] = yd1[jj] = 0.0;
+          if (!v0) return;
+          const int64_t o = (int64_t)gi * nx + gj;
+          if (gj > 0) wl[jj] = __ldg(p.wx + o - 1);
+          if (vec) {
+            const double2 a2 = __ldg(reinterpret_cast<const double2*>(p.wx + o));
+            wm[jj] = a2.x; wr[jj] = a2.y;
+            const double2 d2 = __ldg(reinterpret_cast<const double2*>(p.wy + o));
+            yd0[jj] = d2.x; yd1[jj] = d2.y;
+            if (gi > 0) {
+              const double2 u2 = __ldg(reinterpret_cast<const double2*>(p.wy + o - nx));
+              yu0[jj] = u2.x; yu1[jj] = u2.y;
+            }
+          } else {
+            wm[jj] = __ldg(p.wx + o);
+            yd0[jj] = __ldg(p.wy + o);
+            if (gi > 0) yu0[jj] = __ldg(p.wy + o - nx);
+            if (v1) {
+              wr[jj] = __ldg(p.wx + o + 1);
+              yd1[jj] = __ldg(p.wy + o + 1);
+              if (gi > 0) yu1[jj] = __ldg(p.wy + o - nx + 1);
+            }
+          }
+        };
+        if (withE) {
+#pragma unroll
+          for (int jj = 0; jj < EJ; ++jj) load_w(jj, jj);
+        }
         double bw[C::KUY];
         const double* tb = Tm + q * C::PT + cbl + g;   // B[k][n] = T[k][cbl + n]
 #pragma unroll
@@ -294,86 +375,97 @@ struct ApplyCore {
         double e0[C::RBY], e1[C::RBY];
 #pragma unroll
         for (int j = 0; j < C::RBY; ++j) { e0[j] = 0.0; e1[j] = 0.0; }
-        const int rblk0 = r0 >> 3;
-        if (!p.use_tab || (rblk0 >= p.by_lo && rblk0 + C::RBY - 1 <= p.by_hi)) {
 #pragma unroll
-          for (int ks = 0; ks < C::KS; ++ks)
+        for (int ks = 0; ks < C::KS; ++ks) {
+          const int t = 4 * ks + q - g;   // y-pass A[m][k] = cy[k - m]
+          const double ay = (t >= 0 && t < C::T) ? p.cy[t] : 0.0;
 #pragma unroll
-            for (int j = 0; j < C::RBY; ++j) dmma(e0[j], e1[j], ay[ks], bw[2 * j + ks]);
-        } else {
+          for (int j = 0; j < C::RBY; ++j) dmma(e0[j], e1[j], ay, bw[2 * j + ks]);
+        }
+        if (p.edge_fix && (r0 < R || r0 + C::TY > ny - R)) {
+          const double* tcol = Tm - (r0 - C::H) * C::PT + lc;   // tcol[m * PT] = T(row m, col lc)
 #pragma unroll
           for (int j = 0; j < C::RBY; ++j) {
-            const double* fa = p.fragy + (int64_t)(rblk0 + j) * (C::KS * 32) + lane;
+            const int gi = r0 + 8 * j + g;
+            double c0v = 0.0, c1v = 0.0;
+            if (gi < R) {
+              const double* dt = smem + C::OFF_DC + (2 * R + gi) * R;
 #pragma unroll
-            for (int ks = 0; ks < C::KS; ++ks) dmma(e0[j], e1[j], __ldg(fa + ks * 32), bw[2 * j + ks]);
+              for (int m = 0; m < R; ++m) {
+                const double dv = dt[m];
+                c0v = fma(dv, tcol[m * C::PT], c0v);
+                c1v = fma(dv, tcol[m * C::PT + 1], c1v);
+              }
+            }
+            if (gi >= ny - R && gi < ny) {
+              const double* db = smem + C::OFF_DC + (3 * R + gi - (ny - R)) * R;
+#pragma unroll
+              for (int m = 0; m < R; ++m) {
+                const double dv = db[m];
+                c0v = fma(dv, tcol[(ny - R + m) * C::PT], c0v);
+                c1v = fma(dv, tcol[(ny - R + m) * C::PT + 1], c1v);
+              }
+            }
+            e0[j] -= c0v;
+            e1[j] -= c1v;
           }
         }
         // epilogue: lane holds rows r0 + 8j + g, columns c0 + cbl + 2q, +1
-        const bool vec = ((nx & 1) == 0);
-        const int lc = cbl + 2 * q;
-        const int gj = c0 + lc;
 #pragma unroll
-        for (int j = 0; j < C::RBY; ++j) {
-          const int lr = j * 8 + g;
-          const int gi = r0 + lr;
-          const bool v0 = gi < ny && gj < nx, v1 = gi < ny && gj + 1 < nx;
-          const int so = (lr + C::H) * C::PX + lc + C::H;
-          const double x0 = S[so], x1 = S[so + 1];
-          double o0 = e0[j], o1 = e1[j];
-          if (withE && v0) {
-            // 5-point E_k stencil for the two columns; weights through L1 (prefetched)
-            const int64_t o = (int64_t)gi * nx + gj;
-            double wl, wm, wr, yu0, yu1, yd0, yd1;
-            wl = gj > 0 ? __ldg(p.wx + o - 1) : 0.0;
-            if (vec) {
-              const double2 wmr = __ldg(reinterpret_cast<const double2*>(p.wx + o));
-              wm = wmr.x; wr = wmr.y;
-              const double2 yd = __ldg(reinterpret_cast<const double2*>(p.wy + o));
-              yd0 = yd.x; yd1 = yd.y;
-              if (gi > 0) {
-                const double2 yu = __ldg(reinterpret_cast<const double2*>(p.wy + o - nx));
-                yu0 = yu.x; yu1 = yu.y;
-              } else { yu0 = 0.0; yu1 = 0.0; }
-            } else {
-              wm = __ldg(p.wx + o);
-              wr = v1 ? __ldg(p.wx + o + 1) : 0.0;
-              yd0 = __ldg(p.wy + o);
-              yd1 = v1 ? __ldg(p.wy + o + 1) : 0.0;
-              yu0 = gi > 0 ? __ldg(p.wy + o - nx) : 0.0;
-              yu1 = (gi > 0 && v1) ? __ldg(p.wy + o - nx + 1) : 0.0;
-            }
-            const double xl = S[so - 1], xr = S[so + 2];
-            const double u0 = S[so - C::PX], u1 = S[so - C::PX + 1];
-            const double d0v = S[so + C::PX], d1v = S[so + C::PX + 1];
-            const double ex0 = wl * (x0 - xl) - wm * (x1 - x0) + yu0 * (x0 - u0) - yd0 * (d0v - x0);
-            const double ex1 = wm * (x1 - x0) - wr * (xr - x1) + yu1 * (x1 - u1) - yd1 * (d1v - x1);
-            if (mode == RSK_APPLY_SHIFTED) {
-              o0 = fma(gm, ex0, o0);
-              o1 = fma(gm, ex1, o1);
-            } else if (v1) {
-              double* ep = eys + (int64_t)gi * nx + gj;
-              if (vec && (p.ldey % 2 == 0)) *reinterpret_cast<double2*>(ep) = make_double2(ex0, ex1);
-              else { ep[0] = ex0; ep[1] = ex1; }
-            } else {
-              eys[(int64_t)gi * nx + gj] = ex0;
-            }
+        for (int jc = 0; jc < C::RBY; jc += EJ) {
+          if (withE && jc > 0) {
+#pragma unroll
+            for (int jj = 0; jj < EJ; ++jj)
+              if (jc + jj < C::RBY) load_w(jc + jj, jj);
           }
-          if (v1) {
-            double* yp = ys + (int64_t)gi * nx + gj;
-            if (vec && (p.ldy % 2 == 0)) *reinterpret_cast<double2*>(yp) = make_double2(o0, o1);
-            else { yp[0] = o0; yp[1] = o1; }
-            dot = fma(x0, o0, dot);
-            dot = fma(x1, o1, dot);
-          } else if (v0) {
-            ys[(int64_t)gi * nx + gj] = o0;
-            dot = fma(x0, o0, dot);
+#pragma unroll
+          for (int jj = 0; jj < EJ; ++jj) {
+            const int j = jc + jj;
+            if (j >= C::RBY) break;
+            const int lr = j * 8 + g;
+            const int gi = r0 + lr;
+            const bool v0 = gi < ny && gj < nx, v1 = gi < ny && gj + 1 < nx;
+            const int so = (lr + C::H) * C::PX + lc + C::H;
+            const double x0 = S[so], x1 = S[so + 1];
+            double o0 = e0[j], o1 = e1[j];
+            if (withE && v0) {
+              // 5-point E_k stencil for the two columns
+              const double xl = S[so - 1], xr = S[so + 2];
+              const double u0 = S[so - C::PX], u1 = S[so - C::PX + 1];
+              const double d0v = S[so + C::PX], d1v = S[so + C::PX + 1];
+              const double ex0 = wl[jj] * (x0 - xl) - wm[jj] * (x1 - x0) + yu0[jj] * (x0 - u0) - yd0[jj] * (d0v - x0);
+              const double ex1 = wm[jj] * (x1 - x0) - wr[jj] * (xr - x1) + yu1[jj] * (x1 - u1) - yd1[jj] * (d1v - x1);
+              if (mode == RSK_APPLY_SHIFTED) {
+                o0 = fma(gm, ex0, o0);
+                o1 = fma(gm, ex1, o1);
+              } else if (v1) {
+                double* ep = eys + (int64_t)gi * nx + gj;
+                if (vec && (p.ldey % 2 == 0)) *reinterpret_cast<double2*>(ep) = make_double2(ex0, ex1);
+                else { ep[0] = ex0; ep[1] = ex1; }
+              } else {
+                eys[(int64_t)gi * nx + gj] = ex0;
+              }
+            }
+            if (v1) {
+              double* yp = ys + (int64_t)gi * nx + gj;
+              if (vec && (p.ldy % 2 == 0)) *reinterpret_cast<double2*>(yp) = make_double2(o0, o1);
+              else { yp[0] = o0; yp[1] = o1; }
+              dot = fma(x0, o0, dot);
+              dot = fma(x1, o1, dot);
+            } else if (v0) {
+              ys[(int64_t)gi * nx + gj] = o0;
+              dot = fma(x0, o0, dot);
+            }
           }
         }
       }
 
+      amark(3);
       if (p.want_dot) {
         const double bs = block_sum(dot, red);
-        if (!p.cg) {
+        if (dot_acc) {
+          if (tid == 0) *dot_acc += bs;
+        } else if (!p.cg) {
           if (tid == 0) p.part[(int64_t)li * p.ntiles + tile] = bs;
         } else {
           CgDev* cg = p.cg;
@@ -408,11 +500,10 @@ struct ApplyCore {
           }
         }
       }
+      amark(4);
       __syncthreads();   // everyone is done with S and T
-      if (it + 1 < iend) {
-        const int t2 = (it + 1) / nl, s2 = sid_of(it + 1 - t2 * nl);
-        issue_x(p, smem, t2, s2, src2_of(s2));
-      }
+      amark(5);
+      pp.stage ^= 1;
     }
   }
 };

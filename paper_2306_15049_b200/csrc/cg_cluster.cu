@@ -1,0 +1,406 @@
+// Cluster-per-shift deflated CG (rsk_cg_recycled_batch, images whose working set sits
+// in L2): a thread-block cluster of kCS CTAs (one per SM) owns ONE shift at a time and
+// iterates it to completion; clusters take shifts from a device queue, so shifts with
+// 20 iterations and shifts with 2000 never wait on each other (no lockstep tail). All
+// reductions cross the cluster through distributed shared memory (DSMEM) in a fixed
+// CTA-rank order, and the only synchronisation is the hardware cluster barrier
+// (3 per iteration), instead of grid barriers or kernel boundaries.
+//
+// Recurrences are exactly those of the oracle O4 (oracle/defcg.py; reading D1):
+//   A  w = A_gamma p (LOOP) or A_gamma x (CONFIRM); pi = p.w; alpha = rho / pi
+//   B  r = r - alpha w (LOOP) or b - w (CONFIRM); rho' = r.r; z = Z^T r
+//      -> mu = G^-1 z, beta, status (replicated identically in every CTA)
+//   C  x += alpha p; p = r + beta p - W mu_W - ghat mu_g; residual store
+// A shift's arithmetic depends only on N and the cluster size: results are bitwise
+// independent of the batch composition and of the GPU count under shift sharding.
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+
+#include "apply_core.cuh"
+
+namespace rsk {
+
+namespace cgx = cooperative_groups;
+
+constexpr int kCV = kMaxM + 1;   // partial slots: z_0..z_{m-1}, rho at kMaxM
+constexpr int kCW = kAT / 32;
+
+__device__ unsigned long long g_cprof[8];   // per-phase ns of cluster 0 rank 0 (RSK_CLUSTER_PROF)
+
+struct alignas(64) ClusterParams {
+  ApplyParams ap;      // X = P, X2 = caller x, Y = Wv, want_dot, cg = null
+  CgDev* cg;
+  unsigned* queue;     // next shift index (device counter, zeroed by the host)
+  int nshift;
+  int64_t rows;        // rows per CTA of a cluster
+  int prof;
+};
+
+__device__ __forceinline__ void cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+template <int R, bool kTma>
+__global__ void __launch_bounds__(kAT, 1) cg_cluster_kernel(const __grid_constant__ ClusterParams P) {
+  extern __shared__ __align__(128) double smem[];
+  using Core = ApplyCore<R, kTma>;
+  cgx::cluster_group cl = cgx::this_cluster();
+  const int crank = (int)cl.block_rank();
+  const int csz = (int)cl.num_blocks();
+  __shared__ double s_part[kCV];       // this CTA's partial sums (read by the whole cluster)
+  __shared__ double s_dot;
+  __shared__ int s_next;
+  __shared__ double s_z[kCV];
+  __shared__ double s_red[kCW][kCV];
+  __shared__ double s_L[kMaxM * kMaxM];
+  __shared__ double s_mu[kMaxM];
+  __shared__ double s_alpha, s_beta, s_rinv;
+  __shared__ int s_mode, s_nst, s_slot, s_brk;
+  __shared__ int s_list[1], s_lmode[1];
+
+  CgDev* cg = P.cg;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t N = cg->N;
+  Core::init_bars(smem, P.ap);
+  ApplyPipe pp{{0u, 0u}, 0};
+  const int64_t rbeg = (int64_t)crank * P.rows;
+  const int64_t rend = min(N, rbeg + P.rows);
+  const int ntiles = P.ap.ntiles;
+  const int tper = (ntiles + csz - 1) / csz;
+  const int ibeg = min(ntiles, crank * tper), iend = min(ntiles, ibeg + tper);
+
+  unsigned long long t0 = 0;
+  auto mark = [&](int ph) {
+    if (P.prof && blockIdx.x == 0 && tid == 0) {
+      unsigned long long t1;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t1));
+      if (t0 && ph >= 0) g_cprof[ph] += t1 - t0;
+      t0 = t1;
+    }
+  };
+  for (;;) {
+    if (crank == 0 && tid == 0) s_next = (int)atomicAdd(P.queue, 1u);
+    cl_sync();
+    const int idx = *cl.map_shared_rank(&s_next, 0);
+    cl_sync();
+    if (idx >= P.nshift) break;
+    const int s = idx;
+    // ---- per-shift state (replicated in every CTA of the cluster)
+    int mode = cg->status[s];
+    if (mode != ST_ACTIVE && mode != ST_RCONV) continue;
+    const int m = cg->mloc[s], hg = cg->hasg[s], nw = m - hg;
+    const int grp = cg->group[s];
+    const int J = cg->grp.J[grp];
+    const double gam = cg->gam[s];
+    const double thr = cg->tol * cg->bnorm;
+    double rho = cg->rho[s];
+    int iters = cg->iters[s], nconf = cg->nconf[s], scnt = cg->store_cnt[s];
+    double rho_true = cg->rho_true[s];
+    for (int e = tid; e < kMaxM * kMaxM; e += kAT) s_L[e] = cg->Lf[(int64_t)s * kMaxM * kMaxM + e];
+    for (int j = tid; j < kMaxM; j += kAT) s_mu[j] = 0.0;
+    if (tid == 0) { s_list[0] = s; }
+    const double* AWg = cg->grp.AW[grp];
+    const double* EWg = cg->grp.EW[grp];
+    const double* Wg = cg->grp.W[grp];
+    const int64_t ldw = cg->grp.ldw;
+    double* __restrict__ Rv = cg->R + (int64_t)s * N;
+    double* __restrict__ Pv = cg->P + (int64_t)s * N;
+    double* __restrict__ Wv = cg->Wv + (int64_t)s * N;
+    double* __restrict__ Xv = cg->X + (int64_t)s * cg->ldx;
+    const double* __restrict__ Gh = hg ? cg->Ghat + (int64_t)s * cg->ldgh : nullptr;
+    const double* __restrict__ Zg = hg ? cg->ZGhat + (int64_t)s * cg->ldgh : nullptr;
+    int status = mode;
+    __syncthreads();
+
+    for (;;) {
+      // ================= A: w = A_gamma p (LOOP) or A_gamma x (CONFIRM)
+      if (tid == 0) { s_lmode[0] = mode; s_dot = 0.0; }
+      __syncthreads();
+      mark(-1);
+      Core::run(P.ap, smem, ibeg, iend, 1, pp, s_list, s_lmode, &s_dot);
+      mark(0);
+      cl_sync();
+      mark(1);
+      double alpha = 0.0;
+      if (mode == ST_ACTIVE) {
+        if (tid == 0) {
+          double pi = 0.0;
+          for (int c = 0; c < csz; ++c) pi += *cl.map_shared_rank(&s_dot, c);
+          s_brk = !(pi > 0.0) || !isfinite(pi);
+          s_alpha = s_brk ? 0.0 : rho / pi;
+        }
+        __syncthreads();
+        if (s_brk) { status = ST_BREAKDOWN; break; }
+        alpha = s_alpha;
+      }
+      mark(2);
+      // ================= B: r update; partials of z = Z^T r and rho' = r.r
+      double acc[16], accg = 0.0, accr = 0.0;
+#pragma unroll
+      for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+#pragma unroll 2
+      for (int64_t i = rbeg + tid; i < rend; i += kAT) {
+        const double wv = Wv[i];
+        const double rn = (mode == ST_ACTIVE) ? fma(-alpha, wv, Rv[i]) : __ldg(cg->b + i) - wv;
+        Rv[i] = rn;
+#pragma unroll
+        for (int j = 0; j < 16; ++j)
+          if (j < nw) acc[j] = fma(fma(gam, __ldg(EWg + (int64_t)j * ldw + i), __ldg(AWg + (int64_t)j * ldw + i)), rn, acc[j]);
+        if (hg) accg = fma(__ldg(Zg + i), rn, accg);
+        accr = fma(rn, rn, accr);
+      }
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        if (j < nw) {
+          const double v = warp_sum(acc[j]);
+          if (lane == 0) s_red[warp][j] = v;
+        }
+      }
+      if (hg) {
+        const double v = warp_sum(accg);
+        if (lane == 0) s_red[warp][nw] = v;
+      }
+      {
+        const double v = warp_sum(accr);
+        if (lane == 0) s_red[warp][kMaxM] = v;
+      }
+      __syncthreads();
+      mark(3);
+      if (tid < kCV) {
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < kCW; ++w) t += s_red[w][tid];
+        s_part[tid] = t;
+      }
+      cl_sync();
+      mark(1);
+      if (tid < kCV && (tid < m || tid == kMaxM)) {
+        double t = 0.0;
+        for (int c = 0; c < csz; ++c) t += *cl.map_shared_rank(&s_part[tid], c);
+        s_z[tid] = t;
+      }
+      __syncthreads();
+      // ---- scalars and status (identical in every CTA)
+      if (tid == 0) {
+        const double rho_new = s_z[kMaxM];
+        const bool conv = sqrt(rho_new) <= thr;
+        int nst = mode;
+        bool newp = false;
+        double beta = 0.0;
+        if (mode == ST_ACTIVE) {
+          iters += 1;
+          beta = rho_new / rho;
+          rho = rho_new;
+          if (conv) nst = ST_RCONV;
+          else if (iters >= cg->maxit) nst = ST_MAXIT;
+          else newp = true;
+        } else {
+          rho_true = rho_new;
+          nconf += 1;
+          if (conv) nst = ST_DONE;
+          else if (iters >= cg->maxit) nst = ST_MAXIT;
+          else { nst = ST_ACTIVE; beta = 0.0; rho = rho_new; newp = true; }
+        }
+        int slot = -1;
+        if (newp) {
+          double x[kMaxM];
+#pragma unroll
+          for (int i = 0; i < kMaxM; ++i) {
+            if (i < m) {
+              double t = s_z[i];
+#pragma unroll
+              for (int j = 0; j < i; ++j) t -= s_L[i + j * kMaxM] * x[j];
+              x[i] = t / s_L[i + i * kMaxM];
+            }
+          }
+#pragma unroll
+          for (int i = kMaxM - 1; i >= 0; --i) {
+            if (i < m) {
+              double t = x[i];
+#pragma unroll
+              for (int j = i + 1; j < kMaxM; ++j)
+                if (j < m) t -= s_L[j + i * kMaxM] * x[j];
+              x[i] = t / s_L[i + i * kMaxM];
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < kMaxM; ++j) s_mu[j] = j < m ? x[j] : 0.0;
+          if (cg->store && scnt < cg->store_cap) slot = scnt++;
+        }
+        s_nst = nst;
+        s_beta = beta;
+        s_slot = slot;
+        s_rinv = (slot >= 0) ? 1.0 / sqrt(rho) : 0.0;
+      }
+      __syncthreads();
+      const int nst = s_nst;
+      mark(4);
+      // ================= C: x += alpha p (LOOP); p = r + beta p - W mu_W - ghat mu_g
+      {
+        const bool upd_x = (mode == ST_ACTIVE) && alpha != 0.0;
+        const bool upd_p = (nst == ST_ACTIVE);
+        const double beta = s_beta;
+        const int slot = s_slot;
+        const double rinv = s_rinv;
+        double* sto = (slot >= 0) ? cg->store + ((int64_t)s * cg->store_cap + slot) * cg->lds : nullptr;
+        double mu[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) mu[j] = s_mu[j];
+        const double mug = hg ? s_mu[nw] : 0.0;
+        if (upd_x || upd_p) {
+#pragma unroll 2
+          for (int64_t i = rbeg + tid; i < rend; i += kAT) {
+            const double pv = Pv[i];
+            if (upd_x) Xv[i] = fma(alpha, pv, Xv[i]);
+            if (upd_p) {
+              const double rv = Rv[i];
+              double pn = fma(beta, pv, rv);
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                if (j < nw) pn = fma(-mu[j], __ldg(Wg + (int64_t)j * ldw + i), pn);
+              if (hg) pn = fma(-mug, __ldg(Gh + i), pn);
+              Pv[i] = pn;
+              if (sto) sto[i] = rv * rinv;
+            }
+          }
+        }
+      }
+      asm volatile("fence.proxy.async.global;\n" ::: "memory");   // p / x stores -> next TMA reads
+      mark(5);
+      cl_sync();
+      mark(1);
+      if (P.prof && blockIdx.x == 0 && tid == 0) g_cprof[6] += 1;
+      mode = nst;
+      status = nst;
+      if (nst != ST_ACTIVE && nst != ST_RCONV) break;
+    }
+    // ---- per-shift outputs (leader CTA)
+    if (crank == 0 && tid == 0) {
+      cg->status[s] = status;
+      cg->iters[s] = iters;
+      cg->rho[s] = rho;
+      cg->rho_true[s] = rho_true;
+      cg->nconf[s] = nconf;
+      cg->store_cnt[s] = scnt;
+      cg->alpha[s] = 0.0;
+    }
+    __syncthreads();
+  }
+}
+
+// ------------------------------------------------------------------ host side
+bool fill_apply_params(Handle* h, const ApplyLaunch& a, ApplyParams& prm);
+
+template <int R>
+static cudaError_t launch_cluster_r(ClusterParams& prm, bool tma, int csize, int nclusters, cudaStream_t st,
+                                    bool* ok) {
+  using C = TcCfg<R>;
+  auto kfn = tma ? cg_cluster_kernel<R, true> : cg_cluster_kernel<R, false>;
+  const size_t smem = C::SMEM;
+  static int inited[2] = {0, 0};
+  static int maxcl[2] = {0, 0};
+  const int ti = tma ? 1 : 0;
+  if (!inited[ti]) {
+    inited[ti] = 1;
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess && csize > 8) e = cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) { cudaGetLastError(); maxcl[ti] = 0; }
+    else {
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = csize; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(csize * 64); cfg.blockDim = dim3(kAT); cfg.dynamicSmemBytes = smem;
+      cfg.attrs = at; cfg.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, (void*)kfn, &cfg) != cudaSuccess) { cudaGetLastError(); n = 0; }
+      maxcl[ti] = n;
+    }
+  }
+  const int ncl = nclusters < maxcl[ti] ? nclusters : maxcl[ti];
+  if (ncl < 1) { *ok = false; return cudaSuccess; }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = csize; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(csize * ncl); cfg.blockDim = dim3(kAT); cfg.dynamicSmemBytes = smem; cfg.stream = st;
+  cfg.attrs = at; cfg.numAttrs = 1;
+  count_launch();
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kfn, prm);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "librsk: cluster launch failed (%s); lockstep CG loop\n", cudaGetErrorString(e));
+    cudaGetLastError();
+    *ok = false;
+    return cudaSuccess;
+  }
+  *ok = true;
+  return cudaSuccess;
+}
+
+extern "C" int rsk_debug_cluster_prof(double* out8, int reset) {
+  unsigned long long v[8];
+  if (cudaMemcpyFromSymbol(v, g_cprof, sizeof(v)) != cudaSuccess) return -1;
+  for (int i = 0; i < 8; ++i) out8[i] = (double)v[i];
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_cprof, z, sizeof(z));
+  }
+  return 0;
+}
+
+int cluster_size_for(const Handle* h) {
+  (void)h;
+  const char* e = getenv("RSK_CG_CLUSTER");
+  int cs = e ? atoi(e) : 16;
+  if (cs != 2 && cs != 4 && cs != 8 && cs != 16) cs = 16;
+  return cs;
+}
+
+// Runs every ACTIVE / RCONV shift to completion with one cluster per shift.
+cudaError_t launch_cg_cluster(Handle* h, CgDev* dev, const CgDev& hc, unsigned* queue, cudaStream_t st, bool* ok) {
+  ClusterParams prm;
+  ApplyLaunch a{};
+  a.X = hc.P; a.ldx = hc.N;
+  a.X2 = hc.X; a.ldx2 = hc.ldx;
+  a.Y = hc.Wv; a.ldy = hc.N;
+  a.gamma = hc.gam;
+  a.nlist = 1;
+  a.nvec_total = hc.nshift;
+  a.mode = RSK_APPLY_SHIFTED;
+  a.src2_rconv = true;
+  a.xdoty = reinterpret_cast<double*>(1);   // want_dot (accumulated through dot_acc)
+  const bool tma = fill_apply_params(h, a, prm.ap);
+  prm.ap.cg = nullptr;
+  prm.cg = dev;
+  prm.queue = queue;
+  prm.nshift = hc.nshift;
+  int cs = cluster_size_for(h);
+  int64_t rows = (hc.N + cs - 1) / cs;
+  rows = (rows + 1) / 2 * 2;
+  prm.rows = rows;
+  prm.prof = getenv("RSK_CLUSTER_PROF") ? 1 : 0;
+  *ok = false;
+  const int ncl = hc.nshift;
+  cudaError_t e = cudaSuccess;
+  switch (h->r) {
+    case 1: e = launch_cluster_r<1>(prm, tma, cs, ncl, st, ok); break;
+    case 2: e = launch_cluster_r<2>(prm, tma, cs, ncl, st, ok); break;
+    case 3: e = launch_cluster_r<3>(prm, tma, cs, ncl, st, ok); break;
+    case 4: e = launch_cluster_r<4>(prm, tma, cs, ncl, st, ok); break;
+    case 5: e = launch_cluster_r<5>(prm, tma, cs, ncl, st, ok); break;
+    case 6: e = launch_cluster_r<6>(prm, tma, cs, ncl, st, ok); break;
+    case 7: e = launch_cluster_r<7>(prm, tma, cs, ncl, st, ok); break;
+    case 8: e = launch_cluster_r<8>(prm, tma, cs, ncl, st, ok); break;
+    case 9: e = launch_cluster_r<9>(prm, tma, cs, ncl, st, ok); break;
+    case 10: e = launch_cluster_r<10>(prm, tma, cs, ncl, st, ok); break;
+    case 11: e = launch_cluster_r<11>(prm, tma, cs, ncl, st, ok); break;
+    case 12: e = launch_cluster_r<12>(prm, tma, cs, ncl, st, ok); break;
+    default: break;
+  }
+  return e;
+}
+
+}  // namespace rsk

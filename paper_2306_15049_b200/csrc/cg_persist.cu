@@ -1,0 +1,619 @@
+// Persistent lockstep loop of the batched deflated CG (rsk_cg_recycled_batch).
+//
+// One cooperative launch runs up to `max_iters` lockstep iterations of every active
+// shift, with grid-wide barriers between the phases instead of kernel boundaries (the
+// host-polled three-kernels-per-iteration loop was launch- and latency-bound: ~85 us
+// per lockstep iteration at C2 with a few shifts left).  Recurrences are exactly those
+// of the oracle O4 (oracle/defcg.py; reading D1 in DESIGN.md):
+//
+//   A  w = A_gamma p  (ACTIVE)  or  w = A_gamma x  (RCONV: true-residual confirm)
+//      fused apply (apply_core.cuh) + per-tile p.w partials; last CTA of a shift forms
+//      alpha = rho / p.w (BREAKDOWN if p.w <= 0)                          -- barrier
+//   B  r = r - alpha w  (ACTIVE)  or  r = b - w  (RCONV); per row chunk the partials of
+//      rho' = r.r  and  z = Z^T r = [(AW + gamma EW)^T r ; ZGhat^T r]     -- barrier
+//   B2 one warp per shift: fixed-order sum over chunks; mu = G^-1 z; beta = rho'/rho;
+//      status (RCONV on the recursive residual; DONE / MAXIT / restart after a confirm) -- barrier
+//   C  x += alpha p ;  p = r + beta p - W mu_W - ghat mu_g ; residual store  -- barrier
+//
+// Every sum has a fixed order that depends only on N and the launch geometry, so the
+// result of a shift does not depend on which other shifts share the batch (bitwise
+// reproducible across shift shardings).
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+
+#include "apply_core.cuh"
+
+namespace rsk {
+
+constexpr int kPMaxShift = 256;   // shifts per persistent solve
+constexpr int kPV = kMaxM + 1;    // partial slots per (shift, chunk): z_0..z_{m-1}, rho at kMaxM
+constexpr int kPT = 32;           // shifts per phase-B tile
+constexpr int kPW = kAT / 32;     // warps per CTA
+
+__device__ unsigned long long g_pprof[8];   // per-phase ns (RSK_PERSIST_PROF), block 0's view
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+struct alignas(64) PersistParams {
+  ApplyParams ap;      // CG-mode apply: X = P, X2 = caller x, Y = Wv
+  CgDev* cg;
+  double* partP;       // [shift][kPV][chunk]
+  unsigned* bar;       // grid barrier {count, generation}
+  int* nactive;        // out: shifts still ACTIVE / RCONV when the launch returns
+  int* iters_done;     // out: lockstep iterations run by this launch
+  int nshift;
+  int nchunk;
+  int64_t rows;        // rows per chunk (multiple of kAT)
+  int max_iters;
+  int prof;
+};
+
+__device__ __forceinline__ unsigned ld_acquire(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(unsigned* p, unsigned v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
+
+// sense-reversing grid barrier; all CTAs are co-resident (cooperative launch)
+__device__ __forceinline__ void grid_sync(unsigned* bar, unsigned& gen) {
+  asm volatile("fence.proxy.async.global;\n" ::: "memory");   // generic writes -> later TMA reads
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned arrived = atomicAdd(bar, 1u) + 1u;
+    if (arrived == gridDim.x) {
+      bar[0] = 0u;
+      __threadfence();
+      st_release(bar + 1, gen + 1u);
+    } else {
+      while (ld_acquire(bar + 1) == gen) {
+      }
+    }
+    __threadfence();
+    asm volatile("fence.proxy.async.global;\n" ::: "memory");
+  }
+  gen += 1u;
+  __syncthreads();
+}
+
+__device__ __forceinline__ void chol_solve_p(int m, const double* L, double* x) {
+  for (int i = 0; i < m; ++i) {
+    double t = x[i];
+    for (int j = 0; j < i; ++j) t -= L[i + j * kMaxM] * x[j];
+    x[i] = t / L[i + i * kMaxM];
+  }
+  for (int i = m - 1; i >= 0; --i) {
+    double t = x[i];
+    for (int j = i + 1; j < m; ++j) t -= L[j + i * kMaxM] * x[j];
+    x[i] = t / L[i + i * kMaxM];
+  }
+}
+
+// per-iteration snapshot of the active list (shared memory)
+struct PList {
+  int n;
+  int sid[kPMaxShift];
+  int mode[kPMaxShift];     // status at the start of the iteration: ST_ACTIVE or ST_RCONV
+  int grp[kPMaxShift];      // shift group, local dimension m, carried column present
+  int m[kPMaxShift];
+  int hg[kPMaxShift];
+};
+
+// list of ACTIVE / RCONV shifts, sorted by group (phase B/C reuse the group blocks);
+// warp 0 compacts with ballots
+__device__ void build_list(const CgDev* cg, int ns, PList& L, int* tmp) {
+  for (int s = threadIdx.x; s < ns; s += blockDim.x) tmp[s] = cg->status[s] | (cg->group[s] << 8);
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int n = 0;
+    for (int g = 0; g < RSK_MAX_GROUPS; ++g)
+      for (int s0 = 0; s0 < ns; s0 += 32) {
+        const int s = s0 + lane;
+        const int v = s < ns ? tmp[s] : -1;
+        const int st = v & 0xff;
+        const bool in = s < ns && (v >> 8) == g && (st == ST_ACTIVE || st == ST_RCONV);
+        const unsigned bal = __ballot_sync(0xffffffffu, in);
+        if (in) {
+          const int pos = n + __popc(bal & ((1u << lane) - 1u));
+          L.sid[pos] = s;
+          L.mode[pos] = st;
+        }
+        n += __popc(bal);
+      }
+    if (lane == 0) L.n = n;
+  }
+  __syncthreads();
+  for (int li = threadIdx.x; li < L.n; li += blockDim.x) {
+    const int s = L.sid[li];
+    L.grp[li] = cg->group[s];
+    L.m[li] = cg->mloc[s];
+    L.hg[li] = cg->hasg[s];
+  }
+  __syncthreads();
+}
+
+// ---- phase B: r update and the per-chunk partial sums of rho' and z = Z^T r.
+// Thread <-> row; the loads of a batch of kBB shifts are issued before any is used.
+constexpr int kBB = 4;
+__device__ __noinline__ void phase_b(const PersistParams& P, const PList& L, double* smem, double* s_alpha,
+                                     const double* s_gam) {
+  CgDev* cg = P.cg;
+  const int n = L.n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t N = cg->N;
+  for (int li = tid; li < n; li += kAT) s_alpha[li] = (L.mode[li] == ST_ACTIVE) ? cg->alpha[L.sid[li]] : 0.0;
+  __syncthreads();
+  double* acc = smem;   // [kPW][kPT][kPV] (the apply stage buffers are free now)
+  for (int c = blockIdx.x; c < P.nchunk; c += gridDim.x) {
+    const int64_t cbeg = (int64_t)c * P.rows;
+    const int64_t cend = min(N, cbeg + P.rows);
+    for (int t0 = 0; t0 < n; t0 += kPT) {
+      const int nt = min(kPT, n - t0);
+      for (int e = tid; e < kPW * kPT * kPV; e += kAT) acc[e] = 0.0;
+      __syncthreads();
+      for (int64_t r0 = cbeg; r0 < cend; r0 += kAT) {
+        const int64_t i = r0 + tid;
+        const bool valid = i < cend;
+        const double bi = valid ? __ldg(cg->b + i) : 0.0;
+        int curg = -1;
+        double aw[16], ew[16];
+#pragma unroll 1
+        for (int k0 = 0; k0 < nt; k0 += kBB) {
+          double rv[kBB], wv[kBB], zg[kBB];
+#pragma unroll
+          for (int u = 0; u < kBB; ++u) {
+            rv[u] = 0.0; wv[u] = 0.0; zg[u] = 0.0;
+            const int li = t0 + k0 + u;
+            if (k0 + u < nt && valid) {
+              const int s = L.sid[li];
+              wv[u] = cg->Wv[(int64_t)s * N + i];
+              if (L.mode[li] == ST_ACTIVE) rv[u] = cg->R[(int64_t)s * N + i];
+              if (L.hg[li]) zg[u] = __ldg(cg->ZGhat + (int64_t)s * cg->ldgh + i);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kBB; ++u) {
+            const int k = k0 + u;
+            if (k >= nt) break;
+            const int li = t0 + k;
+            const int s = L.sid[li];
+            const int g = L.grp[li];
+            const int hg = L.hg[li];
+            const int nw = L.m[li] - hg;
+            if (g != curg) {
+              curg = g;
+              const int J = cg->grp.J[g];
+              const double* AWg = cg->grp.AW[g];
+              const double* EWg = cg->grp.EW[g];
+              const int64_t ldw = cg->grp.ldw;
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                aw[j] = (j < J && valid) ? __ldg(AWg + (int64_t)j * ldw + i) : 0.0;
+                ew[j] = (j < J && valid) ? __ldg(EWg + (int64_t)j * ldw + i) : 0.0;
+              }
+            }
+            double rn = 0.0;
+            if (valid) {
+              rn = (L.mode[li] == ST_ACTIVE) ? fma(-s_alpha[li], wv[u], rv[u]) : bi - wv[u];
+              cg->R[(int64_t)s * N + i] = rn;
+            }
+            const double gm = s_gam[s];
+            double* ak = acc + ((size_t)warp * kPT + k) * kPV;
+            // z_j = sum (AW_j + gamma EW_j) r  (j < nw), z_nw = ZGhat . r, rho = r . r
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+              if (j < nw) {
+                const double v = warp_sum(fma(gm, ew[j], aw[j]) * rn);
+                if (lane == 0) ak[j] += v;
+              }
+            }
+            if (hg) {
+              const double v = warp_sum(zg[u] * rn);
+              if (lane == 0) ak[nw] += v;
+            }
+            {
+              const double v = warp_sum(rn * rn);
+              if (lane == 0) ak[kMaxM] += v;
+            }
+          }
+        }
+      }
+      __syncthreads();
+      // cross-warp sums in fixed order -> partials of this chunk
+      for (int e = tid; e < nt * kPV; e += kAT) {
+        const int k = e / kPV, j = e - k * kPV;
+        double t = 0.0;
+#pragma unroll
+        for (int w = 0; w < kPW; ++w) t += acc[((size_t)w * kPT + k) * kPV + j];
+        P.partP[((size_t)L.sid[t0 + k] * kPV + j) * P.nchunk + c] = t;
+      }
+      __syncthreads();
+    }
+  }
+}
+
+// ---- phase B2: one CTA per shift. Warp w sums slots j = w, w + 8, ... over the chunks
+// (coalesced, fixed order); warp 0 then solves G mu = z with the Cholesky factor staged
+// in shared memory and updates the shift's scalars and status.
+__device__ __noinline__ void phase_b2(const PersistParams& P, const PList& L, double* smem) {
+  CgDev* cg = P.cg;
+  const int n = L.n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double* zs = smem;                  // [kPV]
+  double* Ls = smem + 32;             // [kMaxM][kMaxM] lower factor, row-major
+  for (int li = blockIdx.x; li < n; li += gridDim.x) {
+    const int s = L.sid[li];
+    const int mode0 = L.mode[li];
+    const int m = L.m[li];
+    const double* Lg = cg->Lf + (int64_t)s * kMaxM * kMaxM;
+    for (int e = tid; e < m * m; e += kAT) {
+      const int i = e / m, j = e - i * m;
+      if (j <= i) Ls[i * kMaxM + j] = Lg[i + j * kMaxM];
+    }
+    for (int j = warp; j < kPV; j += kPW) {
+      if (j < m || j == kMaxM) {
+        const double* pj = P.partP + ((size_t)s * kPV + j) * P.nchunk;
+        double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
+        int c = lane;
+        for (; c + 96 < P.nchunk; c += 128) {
+          t0 += pj[c]; t1 += pj[c + 32]; t2 += pj[c + 64]; t3 += pj[c + 96];
+        }
+        for (; c < P.nchunk; c += 32) t0 += pj[c];
+        const double t = warp_sum((t0 + t1) + (t2 + t3));
+        if (lane == 0) zs[j] = t;
+      }
+    }
+    __syncthreads();
+    if (tid == 0) {
+      const double rho_new = zs[kMaxM];
+      const int st = cg->status[s];
+      const double thr = cg->tol * cg->bnorm;
+      const bool conv = sqrt(rho_new) <= thr;
+      int nst = st;
+      bool newp = false;
+      if (mode0 == ST_ACTIVE) {
+        if (st == ST_ACTIVE) {   // not BREAKDOWN in phase A
+          const int itn = cg->iters[s] + 1;
+          cg->iters[s] = itn;
+          cg->beta[s] = rho_new / cg->rho[s];
+          cg->rho[s] = rho_new;
+          if (conv) nst = ST_RCONV;
+          else if (itn >= cg->maxit) nst = ST_MAXIT;
+          else newp = true;
+        }
+      } else {   // confirm on the true residual r = b - A_gamma x
+        cg->rho_true[s] = rho_new;
+        cg->nconf[s] += 1;
+        cg->alpha[s] = 0.0;
+        if (conv) nst = ST_DONE;
+        else if (cg->iters[s] >= cg->maxit) nst = ST_MAXIT;
+        else {
+          nst = ST_ACTIVE;   // restart from the true residual
+          cg->beta[s] = 0.0;
+          cg->rho[s] = rho_new;
+          newp = true;
+        }
+      }
+      if (newp) {
+        // mu = G^-1 z: forward / backward substitution with L L^T = G (m <= kMaxM)
+        double* cf = cg->coef + (int64_t)s * kMaxM;
+        double x[kMaxM];
+#pragma unroll
+        for (int i = 0; i < kMaxM; ++i) {
+          if (i < m) {
+            double t = zs[i];
+#pragma unroll
+            for (int j = 0; j < i; ++j) t -= Ls[i * kMaxM + j] * x[j];
+            x[i] = t / Ls[i * kMaxM + i];
+          }
+        }
+#pragma unroll
+        for (int i = kMaxM - 1; i >= 0; --i) {
+          if (i < m) {
+            double t = x[i];
+#pragma unroll
+            for (int j = i + 1; j < kMaxM; ++j)
+              if (j < m) t -= Ls[j * kMaxM + i] * x[j];
+            x[i] = t / Ls[i * kMaxM + i];
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < kMaxM; ++j) cf[j] = j < m ? x[j] : 0.0;
+        int slot = -1;
+        if (cg->store && cg->store_cnt[s] < cg->store_cap) {
+          slot = cg->store_cnt[s];
+          cg->store_cnt[s] = slot + 1;
+        }
+        cg->stslot[s] = slot;
+      }
+      cg->status[s] = nst;
+    }
+    __syncthreads();
+  }
+}
+
+// ---- phase C: x += alpha p; p = r + beta p - W mu_W - ghat mu_g; residual store
+__device__ __noinline__ void phase_c(const PersistParams& P, const PList& L, double* smem, const double* s_alpha,
+                                     int* s_new, double* s_beta, int* s_slot, double* s_rinv) {
+  CgDev* cg = P.cg;
+  const int n = L.n;
+  const int tid = threadIdx.x;
+  const int64_t N = cg->N;
+    double* scoef = smem;          // [n][kMaxM]
+    for (int li = tid; li < n; li += kAT) {
+      const int s = L.sid[li];
+      const int st = cg->status[s];
+      s_new[li] = st;
+      s_beta[li] = cg->beta[s];
+      s_slot[li] = (st == ST_ACTIVE) ? cg->stslot[s] : -1;
+      s_rinv[li] = (st == ST_ACTIVE && s_slot[li] >= 0) ? 1.0 / sqrt(cg->rho[s]) : 0.0;
+    }
+    for (int e = tid; e < n * kMaxM; e += kAT) {
+      const int li = e / kMaxM, j = e - li * kMaxM;
+      scoef[e] = cg->coef[(int64_t)L.sid[li] * kMaxM + j];
+    }
+    __syncthreads();
+    for (int c = blockIdx.x; c < P.nchunk; c += gridDim.x) {
+      const int64_t cbeg = (int64_t)c * P.rows;
+      const int64_t cend = min(N, cbeg + P.rows);
+      for (int64_t r0 = cbeg; r0 < cend; r0 += kAT) {
+        const int64_t i = r0 + tid;
+        if (i >= cend) break;
+        int curg = -1;
+        double* wv = smem + (size_t)kPMaxShift * kMaxM + tid;   // this thread's W row, stride kAT
+#pragma unroll 1
+        for (int k0 = 0; k0 < n; k0 += kBB) {
+          double pv[kBB], xv[kBB], rv[kBB], gv[kBB];
+#pragma unroll
+          for (int u = 0; u < kBB; ++u) {
+            pv[u] = 0.0; xv[u] = 0.0; rv[u] = 0.0; gv[u] = 0.0;
+            const int li = k0 + u;
+            if (li >= n) break;
+            const int s = L.sid[li];
+            const bool upd_x = (L.mode[li] == ST_ACTIVE) && (s_alpha[li] != 0.0);
+            const bool upd_p = (s_new[li] == ST_ACTIVE);
+            if (upd_x || upd_p) pv[u] = cg->P[(int64_t)s * N + i];
+            if (upd_x) xv[u] = cg->X[(int64_t)s * cg->ldx + i];
+            if (upd_p) {
+              rv[u] = cg->R[(int64_t)s * N + i];
+              if (L.hg[li]) gv[u] = __ldg(cg->Ghat + (int64_t)s * cg->ldgh + i);
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < kBB; ++u) {
+            const int li = k0 + u;
+            if (li >= n) break;
+            const int s = L.sid[li];
+            const bool upd_x = (L.mode[li] == ST_ACTIVE) && (s_alpha[li] != 0.0);
+            const bool upd_p = (s_new[li] == ST_ACTIVE);
+            if (upd_x) cg->X[(int64_t)s * cg->ldx + i] = fma(s_alpha[li], pv[u], xv[u]);
+            if (upd_p) {
+              const int g = L.grp[li];
+              if (g != curg) {
+                curg = g;
+                const int J = cg->grp.J[g];
+                const double* Wg = cg->grp.W[g];
+                const int64_t ldw = cg->grp.ldw;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) wv[j * kAT] = j < J ? __ldg(Wg + (int64_t)j * ldw + i) : 0.0;
+              }
+              const int hg = L.hg[li], nw = L.m[li] - hg;
+              const double* mu = scoef + li * kMaxM;
+              double pn = fma(s_beta[li], pv[u], rv[u]);
+#pragma unroll
+              for (int j = 0; j < 16; ++j)
+                if (j < nw) pn = fma(-mu[j], wv[j * kAT], pn);
+              if (hg) pn = fma(-mu[nw], gv[u], pn);
+              cg->P[(int64_t)s * N + i] = pn;
+              if (s_slot[li] >= 0)
+                cg->store[((int64_t)s * cg->store_cap + s_slot[li]) * cg->lds + i] = rv[u] * s_rinv[li];
+            }
+          }
+        }
+      }
+    }
+}
+
+// ---- phase A: the fused apply over the (tile, shift) items of the active list
+template <int R, bool kTma>
+__device__ __forceinline__ void phase_a(const PersistParams& P, const PList& L, double* smem, ApplyPipe& pp) {
+  const int n = L.n;
+  const int nitems = n * P.ap.ntiles;
+  const int per = (nitems + gridDim.x - 1) / gridDim.x;
+  const int ibeg = blockIdx.x * per;
+  const int iend = min(nitems, ibeg + per);
+  ApplyCore<R, kTma>::run(P.ap, smem, ibeg, iend, n, pp, L.sid, L.mode);
+}
+
+template <int R, bool kTma>
+__global__ void __launch_bounds__(kAT, kApplyCtasPerSm) cg_persist_kernel(const __grid_constant__ PersistParams P) {
+  extern __shared__ __align__(128) double smem[];
+  using Core = ApplyCore<R, kTma>;
+  __shared__ PList lists[2];
+  __shared__ int tmp[kPMaxShift];
+  __shared__ double s_alpha[kPMaxShift], s_beta[kPMaxShift], s_rinv[kPMaxShift], s_gam[kPMaxShift];
+  __shared__ int s_new[kPMaxShift], s_slot[kPMaxShift];
+
+  CgDev* cg = P.cg;
+  const int ns = P.nshift;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t N = cg->N;
+  Core::init_bars(smem, P.ap);
+  ApplyPipe pp{{0u, 0u}, 0};
+  unsigned gen = ld_acquire(P.bar + 1);
+  int cur = 0;
+  build_list(cg, ns, lists[0], tmp);
+  for (int s = tid; s < ns; s += kAT) s_gam[s] = cg->gam[s];
+  grid_sync(P.bar, gen);   // nobody changes a status before every CTA has read them
+
+  int it = 0;
+  unsigned long long t0 = 0;
+  auto mark = [&](int ph) {
+    if (P.prof && blockIdx.x == 0 && tid == 0) {
+      const unsigned long long t1 = gtimer();
+      if (t0) g_pprof[ph] += t1 - t0;
+      t0 = t1;
+    }
+  };
+  mark(7);
+  for (; it < P.max_iters; ++it) {
+    PList& L = lists[cur];
+    const int n = L.n;
+    if (n == 0) break;
+
+    // ================= A: w = A_gamma p (or A_gamma x for confirms)
+    phase_a<R, kTma>(P, L, smem, pp);
+    mark(0);
+    grid_sync(P.bar, gen);
+    mark(1);
+
+    phase_b(P, L, smem, s_alpha, s_gam);
+    mark(2);
+    grid_sync(P.bar, gen);
+    mark(1);
+
+    phase_b2(P, L, smem);
+    mark(3);
+    grid_sync(P.bar, gen);
+    mark(1);
+
+    PList& NL = lists[cur ^ 1];
+    build_list(cg, ns, NL, tmp);   // statuses are stable until the next phase A
+    phase_c(P, L, smem, s_alpha, s_new, s_beta, s_slot, s_rinv);
+    mark(4);
+    grid_sync(P.bar, gen);
+    mark(1);
+    if (P.prof && blockIdx.x == 0 && tid == 0) g_pprof[5] += 1;
+    cur ^= 1;
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    *P.nactive = lists[cur].n;
+    *P.iters_done = it;
+  }
+}
+
+// ------------------------------------------------------------------ host side
+bool fill_apply_params(Handle* h, const ApplyLaunch& a, ApplyParams& prm);
+
+template <int R>
+static cudaError_t launch_persist_r(PersistParams& prm, bool tma, int sm_count, cudaStream_t st, bool* ok) {
+  using C = TcCfg<R>;
+  // phases B / B2 / C reuse the apply's stage and T buffers below the correction table
+  static_assert(C::OFF_DC >= kPW * kPT * kPV && C::OFF_DC >= kPMaxShift * kMaxM + 16 * kAT &&
+                    C::OFF_DC >= 32 + kMaxM * kMaxM,
+                "persistent-loop scratch overlaps the apply's boundary-correction table");
+  auto kfn = tma ? cg_persist_kernel<R, true> : cg_persist_kernel<R, false>;
+  size_t smem = C::SMEM;
+  const size_t accb = sizeof(double) * (size_t)kPW * kPT * kPV;
+  const size_t coefb = sizeof(double) * ((size_t)kPMaxShift * kMaxM + 16 * kAT);
+  if (smem < accb) smem = accb;
+  if (smem < coefb) smem = coefb;
+  static int bps[2] = {0, 0};
+  int& b = bps[tma ? 1 : 0];
+  if (b == 0) {
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kfn, kAT, smem);
+    if (e != cudaSuccess) return e;
+    if (b < 1) b = -1;
+  }
+  if (b < 1) { *ok = false; return cudaSuccess; }
+  const int grid = b * sm_count;
+  if (prm.nchunk > grid) { *ok = false; return cudaSuccess; }
+  void* args[] = {&prm};
+  count_launch();
+  cudaError_t e = cudaLaunchCooperativeKernel((const void*)kfn, dim3(grid), dim3(kAT), args, smem, st);
+  if (e != cudaSuccess) {
+    static bool warned = false;
+    if (!warned) {
+      fprintf(stderr, "librsk: cooperative launch failed (%s); host-polled CG loop\n", cudaGetErrorString(e));
+      warned = true;
+    }
+    cudaGetLastError();
+    *ok = false;
+    return cudaSuccess;
+  }
+  *ok = true;
+  return cudaSuccess;
+}
+
+extern "C" int rsk_debug_persist_prof(double* out8, int reset) {
+  unsigned long long v[8];
+  if (cudaMemcpyFromSymbol(v, g_pprof, sizeof(v)) != cudaSuccess) return -1;
+  for (int i = 0; i < 8; ++i) out8[i] = (double)v[i];
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_pprof, z, sizeof(z));
+  }
+  return 0;
+}
+
+int persist_grid(const Handle* h) { return kApplyCtasPerSm * h->sm_count; }
+int persist_max_shift() { return kPMaxShift; }
+int persist_pv() { return kPV; }
+
+// Runs up to max_iters lockstep iterations; returns (through the device counters) the
+// number of shifts still in the loop. *ok = false if the cooperative launch is impossible
+// (caller falls back to the host-polled loop).
+cudaError_t launch_cg_persist(Handle* h, CgDev* dev, const CgDev& hc, double* partP, unsigned* bar,
+                              int* nactive, int* iters_done, int nchunk, int64_t rows, int max_iters,
+                              cudaStream_t st, bool* ok) {
+  PersistParams prm;
+  ApplyLaunch a{};
+  a.X = hc.P; a.ldx = hc.N;
+  a.X2 = hc.X; a.ldx2 = hc.ldx;
+  a.Y = hc.Wv; a.ldy = hc.N;
+  a.gamma = hc.gam;
+  a.nlist = hc.nshift;
+  a.nvec_total = hc.nshift;
+  a.mode = RSK_APPLY_SHIFTED;
+  a.cg = dev;
+  a.cg_alpha = true;
+  a.src2_rconv = true;
+  const bool tma = fill_apply_params(h, a, prm.ap);
+  prm.cg = dev;
+  prm.partP = partP;
+  prm.bar = bar;
+  prm.nactive = nactive;
+  prm.iters_done = iters_done;
+  prm.nshift = hc.nshift;
+  prm.nchunk = nchunk;
+  prm.rows = rows;
+  prm.max_iters = max_iters;
+  {
+    static int pf = -1;
+    if (pf < 0) pf = getenv("RSK_PERSIST_PROF") ? 1 : 0;
+    prm.prof = pf;
+  }
+  *ok = false;
+  if (hc.nshift > kPMaxShift) return cudaSuccess;
+  const int smc = h->sm_count;
+  switch (h->r) {
+    case 1: return launch_persist_r<1>(prm, tma, smc, st, ok);
+    case 2: return launch_persist_r<2>(prm, tma, smc, st, ok);
+    case 3: return launch_persist_r<3>(prm, tma, smc, st, ok);
+    case 4: return launch_persist_r<4>(prm, tma, smc, st, ok);
+    case 5: return launch_persist_r<5>(prm, tma, smc, st, ok);
+    case 6: return launch_persist_r<6>(prm, tma, smc, st, ok);
+    case 7: return launch_persist_r<7>(prm, tma, smc, st, ok);
+    case 8: return launch_persist_r<8>(prm, tma, smc, st, ok);
+    case 9: return launch_persist_r<9>(prm, tma, smc, st, ok);
+    case 10: return launch_persist_r<10>(prm, tma, smc, st, ok);
+    case 11: return launch_persist_r<11>(prm, tma, smc, st, ok);
+    case 12: return launch_persist_r<12>(prm, tma, smc, st, ok);
+    default: return cudaSuccess;
+  }
+}
+
+}  // namespace rsk

@@ -144,18 +144,28 @@ extern "C" rsk_status rsk_create(rsk_handle* out, int device, int64_t ny, int64_
             cudaStreamCreateWithFlags(&h->cg_stream, cudaStreamNonBlocking) == cudaSuccess;
   if (!ok) { rsk_destroy(h); return RSK_ENOMEM; }
   {
-    const int tyr = apply_tile_rows(r);
-    const int64_t nbx = (nx + kTX - 1) / kTX * (kTX / 8);
-    const int64_t nby = (ny + tyr - 1) / tyr * (tyr / 8);
-    std::vector<double> fx, fy;
-    build_frag_tables(r, nx, nbx, tx.data(), fx);
-    build_frag_tables(r, ny, nby, ty.data(), fy);
-    apply_interior_blocks(r, nx, &h->bx_lo, &h->bx_hi);
-    apply_interior_blocks(r, ny, &h->by_lo, &h->by_hi);
-    ok = cudaMalloc(&h->fragx, sizeof(double) * fx.size()) == cudaSuccess &&
-         cudaMalloc(&h->fragy, sizeof(double) * fy.size()) == cudaSuccess &&
-         cudaMemcpy(h->fragx, fx.data(), sizeof(double) * fx.size(), cudaMemcpyHostToDevice) == cudaSuccess &&
-         cudaMemcpy(h->fragy, fy.data(), sizeof(double) * fy.size(), cudaMemcpyHostToDevice) == cudaSuccess;
+    // B_trunc = Toeplitz(B) - D_lo - D_hi: D_lo(c, m) = sum_{j<0} f[j-c+r] f[j-m+r] for
+    // c, m < r; D_hi likewise with j >= n (the C-output rows outside the image)
+    std::vector<double> dc((size_t)4 * kMaxR * kMaxR, 0.0);
+    auto fill = [&](const double* f, int64_t n, int slot, int which) {
+      for (int a = 0; a < r; ++a)
+        for (int b = 0; b < r; ++b) {
+          double sacc = 0.0;
+          const int64_t c = which ? n - r + a : a, m = which ? n - r + b : b;
+          const int64_t jlo = which ? n : -r, jhi = which ? n + r : 0;
+          for (int64_t j = jlo; j < jhi; ++j) {
+            const int64_t ia = j - c + r, ib = j - m + r;
+            if (ia >= 0 && ia <= 2 * r && ib >= 0 && ib <= 2 * r) sacc += f[ia] * f[ib];
+          }
+          dc[((size_t)slot * kMaxR + a) * kMaxR + b] = sacc;
+        }
+    };
+    fill(v, nx, 0, 0);
+    fill(v, nx, 1, 1);
+    fill(u, ny, 2, 0);
+    fill(u, ny, 3, 1);
+    ok = cudaMalloc(&h->dcorr, sizeof(double) * dc.size()) == cudaSuccess &&
+         cudaMemcpy(h->dcorr, dc.data(), sizeof(double) * dc.size(), cudaMemcpyHostToDevice) == cudaSuccess;
     if (!ok) { rsk_destroy(h); return RSK_ENOMEM; }
   }
   std::vector<double> w((size_t)N);
@@ -178,8 +188,7 @@ extern "C" rsk_status rsk_destroy(rsk_handle h) {
   cudaSetDevice(h->device);
   cudaFree(h->tabBx);
   cudaFree(h->tabBy);
-  cudaFree(h->fragx);
-  cudaFree(h->fragy);
+  cudaFree(h->dcorr);
   cudaFree(h->wx);
   cudaFree(h->wy);
   cudaFree(h->scratch);
@@ -407,7 +416,9 @@ namespace {
 
 struct WsLayout {
   size_t off_R, off_P, off_W, off_dbl, off_int, off_cnt, off_pA, off_pB, off_list, off_dev, off_gb, total;
-  size_t off_glist, off_partG, off_cntG;
+  size_t off_glist, off_partG, off_cntG, off_partP, off_pbar;
+  int nchunkP;
+  int64_t rowsP;
   int nblkA, nblkB;
   int nchunkG, maxtilesG;
   int64_t rowsG;
@@ -436,13 +447,23 @@ WsLayout ws_layout(const Handle* h, int ns) {
   L.off_P = o; o = al(o + sizeof(double) * (size_t)N * ns);
   L.off_W = o; o = al(o + sizeof(double) * (size_t)N * ns);
   L.off_dbl = o; o = al(o + sizeof(double) * (size_t)ns * (5 + kMaxM + kMaxM * kMaxM));
-  L.off_int = o; o = al(o + sizeof(int) * (size_t)ns * 6);
+  L.off_int = o; o = al(o + sizeof(int) * (size_t)ns * 8);
   L.off_cnt = o; o = al(o + sizeof(unsigned) * (size_t)ns * 4);
   L.off_pA = o; o = al(o + sizeof(double) * (size_t)ns * L.nblkA);
   L.off_pB = o; o = al(o + sizeof(double) * (size_t)ns * L.nblkB * (kMaxM + 1));
   L.off_list = o; o = al(o + sizeof(int) * (size_t)ns * 2);
   L.off_dev = o; o = al(o + sizeof(CgDev));
   L.off_gb = o; o = al(o + sizeof(double) * (size_t)(RSK_MAX_GROUPS * (2 * 16 * 16 + 3 * 16 * ns) + ns));
+  // persistent loop: one row chunk (multiple of 256 rows) per CTA of the cooperative grid
+  {
+    const int pg = persist_grid(h);
+    int64_t rp = (N + pg - 1) / pg;
+    rp = (rp + 255) / 256 * 256;
+    L.rowsP = rp;
+    L.nchunkP = (int)((N + rp - 1) / rp);
+  }
+  L.off_partP = o; o = al(o + sizeof(double) * (size_t)ns * L.nchunkP * persist_pv());
+  L.off_pbar = o; o = al(o + sizeof(unsigned) * 8);
   L.total = o;
   return L;
 }
@@ -520,6 +541,8 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
   hc.hasg = in + 3 * ns;
   hc.group = in + 4 * ns;
   hc.store_cnt = in + 5 * ns;
+  hc.nconf = in + 6 * ns;
+  hc.stslot = in + 7 * ns;
   hc.cnt = reinterpret_cast<unsigned*>(base + L.off_cnt);
   hc.partA = reinterpret_cast<double*>(base + L.off_pA);
   hc.partB = reinterpret_cast<double*>(base + L.off_pB);
@@ -649,7 +672,7 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
     for (int s = 0; s < ns; ++s) dh[s] = d->gamma_h[s];
     std::memcpy(&dh[(size_t)5 * ns + (size_t)ns * kMaxM], Lf.data(), sizeof(double) * Lf.size());
     RSK_CUDA(cudaMemcpyAsync(dbl, dh.data(), sizeof(double) * dh.size(), cudaMemcpyHostToDevice, st));
-    std::vector<int> ih((size_t)ns * 6, 0);
+    std::vector<int> ih((size_t)ns * 8, 0);
     for (int s = 0; s < ns; ++s) {
       ih[s] = ST_ACTIVE;
       ih[2 * ns + s] = mloc[s];
@@ -710,6 +733,60 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
   }
   std::vector<int> stat_h(ns), it_h(ns);
   int64_t guard = 0;
+  // Persistent device loop (cg_persist.cu): one cooperative launch runs up to
+  // kChunkIters lockstep iterations incl. the true-residual confirmations; the host
+  // only polls the number of shifts left. Falls back to the host-polled loop below
+  // (also used by the per-kernel profiling mode) if the grid cannot be co-scheduled.
+  // Small images (working set in L2): one thread-block cluster per shift, no lockstep
+  // (cg_cluster.cu). The whole loop incl. confirmations runs in one launch.
+  const bool cluster_mode = !prof && getenv("RSK_CG_LEGACY") == nullptr && getenv("RSK_CG_NOCLUSTER") == nullptr &&
+                            N <= (int64_t)(getenv("RSK_CG_CLUSTER_MAXN") ? atoll(getenv("RSK_CG_CLUSTER_MAXN")) : 131072);
+  if (cluster_mode) {
+    unsigned* pbar = reinterpret_cast<unsigned*>(base + L.off_pbar);
+    RSK_CUDA(cudaMemsetAsync(pbar, 0, sizeof(unsigned) * 8, st));
+    bool ok = false;
+    RSK_CUDA(launch_cg_cluster(h, dev, hc, pbar + 6, st, &ok));
+    if (ok) {
+      std::vector<int> ncf(ns, 0);
+      RSK_CUDA(cudaMemcpyAsync(stat_h.data(), hc.status, sizeof(int) * ns, cudaMemcpyDeviceToHost, st));
+      RSK_CUDA(cudaMemcpyAsync(ncf.data(), hc.nconf, sizeof(int) * ns, cudaMemcpyDeviceToHost, st));
+      RSK_CUDA(cudaStreamSynchronize(st));
+      for (int s = 0; s < ns; ++s) { applies[s] += ncf[s]; confirms[s] += ncf[s]; }
+      active.clear();
+    }
+  }
+  if (!active.empty() && !prof && getenv("RSK_CG_LEGACY") == nullptr && ns <= persist_max_shift()) {
+    constexpr int kChunkIters = 512;
+    unsigned* pbar = reinterpret_cast<unsigned*>(base + L.off_pbar);
+    int* pna = reinterpret_cast<int*>(pbar + 4);
+    double* partP = reinterpret_cast<double*>(base + L.off_partP);
+    RSK_CUDA(cudaMemsetAsync(pbar, 0, sizeof(unsigned) * 8, st));
+    bool persisted = false;
+    int64_t pguard = 0;
+    for (;;) {
+      bool ok = false;
+      RSK_CUDA(launch_cg_persist(h, dev, hc, partP, pbar, pna, pna + 1, L.nchunkP, L.rowsP, kChunkIters, st, &ok));
+      if (!ok) break;
+      persisted = true;
+      int hv[2] = {0, 0};
+      RSK_CUDA(cudaMemcpyAsync(hv, pna, sizeof(int) * 2, cudaMemcpyDeviceToHost, st));
+      RSK_CUDA(cudaStreamSynchronize(st));
+      n_ka += hv[1];
+      if (hv[0] == 0) break;
+      if (++pguard > (2 * (int64_t)d->maxit + 64) / kChunkIters + 8) {
+        h->err = "rsk_cg_recycled_batch: persistent loop guard";
+        return RSK_ECUDA;
+      }
+    }
+    if (persisted) {
+      std::vector<int> ncf(ns, 0);
+      RSK_CUDA(cudaMemcpyAsync(stat_h.data(), hc.status, sizeof(int) * ns, cudaMemcpyDeviceToHost, st));
+      RSK_CUDA(cudaMemcpyAsync(ncf.data(), hc.nconf, sizeof(int) * ns, cudaMemcpyDeviceToHost, st));
+      RSK_CUDA(cudaStreamSynchronize(st));
+      for (int s = 0; s < ns; ++s) { applies[s] += ncf[s]; confirms[s] += ncf[s]; }
+      active.clear();
+    }
+  }
   const int ngrp = defl ? d->ngroups : 1;
   std::vector<int> gbuf(ns + 16);
   // The lockstep chunk (check_every x {apply, update, combine}) has a static launch

@@ -71,6 +71,8 @@ struct CgDev {
   int* hasg;        // carried column present (after drops)
   int* group;
   int* store_cnt;
+  int* nconf;       // true-residual confirmations done (persistent loop)
+  int* stslot;      // residual-store slot of the current iteration, or -1
   unsigned* cnt;    // [nshift][4] last-CTA counters
   double* partA;    // [nshift][nblkA]
   double* partB;    // [nshift][nblkB][kMaxM+1]
@@ -102,9 +104,7 @@ struct Handle {
   double cTx[kMaxTaps], cTy[kMaxTaps];      // taps of C^T (window form)
   double* tabBx = nullptr;    // [nx][4r+1]
   double* tabBy = nullptr;    // [ny][4r+1]
-  double* fragx = nullptr;    // fragment-ordered B_x rows per 8-column block (apply_core.cuh)
-  double* fragy = nullptr;    // fragment-ordered B_y rows per 8-row block
-  int bx_lo = 0, bx_hi = -1, by_lo = 0, by_hi = -1;  // interior block ranges
+  double* dcorr = nullptr;    // [4][kMaxR][kMaxR] zero-boundary corner corrections of Bx, By
   double* wx = nullptr;       // weights copy
   double* wy = nullptr;
   double* scratch = nullptr;  // reduction scratch
@@ -138,8 +138,7 @@ struct ApplyLaunch {
 cudaError_t launch_apply(Handle* h, const ApplyLaunch& a, cudaStream_t st);
 int apply_tiles(const Handle* h);
 int apply_tile_rows(int r);
-void build_frag_tables(int r, int64_t n, int64_t nblk, const double* tab, std::vector<double>& out);
-void apply_interior_blocks(int r, int64_t n, int* lo, int* hi);
+
 
 // ---- vector kernels (vec.cu)
 cudaError_t launch_gemm_tn(Handle* h, int64_t n, int k, const double* U, int64_t ldu, int nv,
@@ -171,6 +170,15 @@ cudaError_t launch_cg_combine(CgDev* dev, const CgDev& host, const int* list, in
 int cg_nblkB(int64_t N);
 cudaError_t launch_cg_update_grp(CgDev* dev, const CgDev& host, int ngroups, int maxtiles, cudaStream_t st);
 cudaError_t launch_cg_combine_grp(CgDev* dev, const CgDev& host, int ngroups, int maxtiles, cudaStream_t st);
+// cluster-per-shift loop (cg_cluster.cu)
+cudaError_t launch_cg_cluster(Handle* h, CgDev* dev, const CgDev& hc, unsigned* queue, cudaStream_t st, bool* ok);
+// persistent lockstep loop (cg_persist.cu)
+int persist_grid(const Handle* h);
+int persist_max_shift();
+int persist_pv();
+cudaError_t launch_cg_persist(Handle* h, CgDev* dev, const CgDev& hc, double* partP, unsigned* bar,
+                              int* nactive, int* iters_done, int nchunk, int64_t rows, int max_iters,
+                              cudaStream_t st, bool* ok);
 
 // kernel-launch accounting (rsk_launch_count): every librsk kernel launch bumps it
 void count_launch();
