@@ -225,17 +225,22 @@ def run_ours(args, cfg, inputs, rank, world):
     e2e = {"value": e_ap / (ems / 1e3), "unit": UNIT,
            "h2d_bytes_per_step": 2 * cfg.N * 8, "d2h_bytes_per_step": cfg.M * cfg.N * 8}
 
-    # ---- roofline of the dominant kernel: the fused apply inside the CG loop,
-    # measured live with CUDA events around each launch (one extra profiled step)
-    sol.profile = True
-    outs_p = step()
-    sol.profile = False
-    # ms_apply, ms_update, n_launch, px-vecs, ms_combine (summed over the outer steps)
-    prof = np.sum([o.prof for o in outs_p], axis=0)
-    ms_apply, ms_upd, n_ka, pxv, ms_cmb = [float(v) for v in prof]
-    alg_bytes = 16.0 * pxv + 16.0 * cfg.N * n_ka          # p read + w write per px-vec; W_k per launch
-    achieved = alg_bytes / (ms_apply / 1e3) / 1e9 if ms_apply > 0 else None
+    # ---- roofline of the dominant kernel: the device-side CG loop (cluster-per-shift
+    # kernel for L2-resident images, persistent lockstep kernel otherwise), timed live with
+    # CUDA events on its launching stream inside librsk over the timed steps (ms_loop[5..7]).
+    prof_all = [o.prof for o in last]
+    dl_ms = float(sum(p[5] for p in prof_all))
+    dl_its = float(sum(p[6] for p in prof_all))
+    kind = int(max(p[7] for p in prof_all)) if prof_all else 0
+    J = cfg.J
+    # algorithmic bytes per shift-iteration and pixel: apply p, w, W_k (32);
+    # update w, r, r', ZGhat, AW/EW (32 + 16 J); combine p, x, r, ghat, p', x', W (48 + 8 J);
+    # the group blocks are amortised over the shifts of a lockstep batch, not per cluster
+    per_px = (32 + 32 + 48 + 24 * J) if kind == 1 else (32 + 32 + 48 + 24 * J / max(1.0, cfg.M / 2))
+    alg_bytes = per_px * cfg.N * dl_its
+    achieved = alg_bytes / (dl_ms / 1e3) / 1e9 if dl_ms > 0 else None
     peak, peak_src = _peaks()
+    step_ms_last = ms / args.steps
     # standalone fused apply over the full batch (all M shifts): 20 back-to-back launches
     # between two events (no host gaps inside), best of 3
     X = torch.randn(cfg.M, cfg.N, dtype=torch.float64, device=dev)
@@ -275,14 +280,16 @@ def run_ours(args, cfg, inputs, rank, world):
             "iters_per_outer_step": [int(o.iters.sum()) for o in last],
             "e2e": e2e,
             "gpu_launches": int(launches),
-            "roofline": {"bound": "hbm", "kernel": "apply_kernel (fused A + gamma E, CG mode)",
+            "roofline": {"bound": "hbm",
+                         "kernel": {1: "cg_cluster_kernel (cluster-per-shift deflated CG loop)",
+                                    2: "cg_persist_kernel (persistent lockstep deflated CG loop)"}.get(kind, "host-polled loop"),
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": (achieved / peak) if achieved else None, "traffic": None,
                          "peak_source": peak_src,
-                         "kernel_ms_share": ms_apply / max(ms_apply + ms_upd + ms_cmb, 1e-9),
-                         "apply_launches": n_ka, "apply_px_vectors": pxv,
-                         "loop_ms": {"apply": ms_apply, "update": ms_upd, "combine": ms_cmb},
-                         "alg_bytes_per_px_vector": 16, "alg_bytes_per_launch_weights": 16 * cfg.N},
+                         "kernel_ms_per_step": dl_ms, "kernel_ms_share": dl_ms / max(step_ms_last, 1e-9),
+                         "shift_iterations_per_step": dl_its,
+                         "alg_bytes_per_shift_iteration_px": per_px,
+                         "working_set": "L2-resident (126 MB L2)" if cfg.N * cfg.M * 8 * 6 < 126e6 else "HBM"},
             "apply_standalone": standalone,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,

@@ -185,6 +185,10 @@ typedef struct {
   double* store;                /* RSK_CG_STORE_RES: device, shift s column c at */
   int64_t lds;                  /*   store + (s*store_cap + c)*lds               */
   int store_cap;
+  const int* order_h;           /* host [nshift] permutation or NULL: the order  */
+                                /* in which the device loop starts the shifts    */
+                                /* (longest first shortens the makespan; results */
+                                /* do not depend on it)                          */
 } rsk_cg_desc;
 
 typedef struct {                /* host arrays [nshift], filled on return        */
@@ -194,8 +198,13 @@ typedef struct {                /* host arrays [nshift], filled on return       
   int* status;                  /* RSK_CG_*                                      */
   int* m_used;                  /* recycle columns used                           */
   int* store_count;             /* residuals stored (RSK_CG_STORE_RES) or NULL   */
-  double* ms_loop;              /* RSK_CG_PROFILE: [5] = {apply ms, update ms,     */
-                                /*  apply launches, apply px-vectors, combine ms} */
+  double* ms_loop;              /* NULL or [8]: RSK_CG_PROFILE (host-polled loop) */
+                                /*  [0..4] = {apply ms, update ms, apply launches,*/
+                                /*  apply px-vectors, combine ms}; always: [5] ms */
+                                /*  of the device-loop kernel (CUDA events on the */
+                                /*  launching stream), [6] its shift-iterations  */
+                                /*  (loop applies incl. confirms), [7] loop kind  */
+                                /*  (1 cluster-per-shift, 2 persistent, 0 host)   */
 } rsk_cg_out;
 
 size_t rsk_cg_workspace_bytes(rsk_handle h, int nshift, int flags);

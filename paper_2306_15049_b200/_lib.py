@@ -52,6 +52,7 @@ class CgDesc(C.Structure):
         ("store", _dp),
         ("lds", _i64),
         ("store_cap", C.c_int),
+        ("order_h", C.POINTER(C.c_int)),
     ]
 
 

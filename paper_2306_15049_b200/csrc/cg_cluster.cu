@@ -34,6 +34,8 @@ struct alignas(64) ClusterParams {
   ApplyParams ap;      // X = P, X2 = caller x, Y = Wv, want_dot, cg = null
   CgDev* cg;
   unsigned* queue;     // next shift index (device counter, zeroed by the host)
+  const int* order;    // start order of the shifts (or null: 0..nshift-1)
+  double* zw;          // [cluster][16][N]: Z = AW + gamma EW of the cluster's shift
   int nshift;
   int64_t rows;        // rows per CTA of a cluster
   int prof;
@@ -57,6 +59,7 @@ __global__ void __launch_bounds__(kAT, 1) cg_cluster_kernel(const __grid_constan
   __shared__ double s_red[kCW][kCV];
   __shared__ double s_L[kMaxM * kMaxM];
   __shared__ double s_mu[kMaxM];
+  __shared__ double s_dinv[kMaxM];
   __shared__ double s_alpha, s_beta, s_rinv;
   __shared__ int s_mode, s_nst, s_slot, s_brk;
   __shared__ int s_list[1], s_lmode[1];
@@ -87,7 +90,7 @@ __global__ void __launch_bounds__(kAT, 1) cg_cluster_kernel(const __grid_constan
     const int idx = *cl.map_shared_rank(&s_next, 0);
     cl_sync();
     if (idx >= P.nshift) break;
-    const int s = idx;
+    const int s = P.order ? P.order[idx] : idx;
     // ---- per-shift state (replicated in every CTA of the cluster)
     int mode = cg->status[s];
     if (mode != ST_ACTIVE && mode != ST_RCONV) continue;
@@ -113,6 +116,16 @@ __global__ void __launch_bounds__(kAT, 1) cg_cluster_kernel(const __grid_constan
     const double* __restrict__ Gh = hg ? cg->Ghat + (int64_t)s * cg->ldgh : nullptr;
     const double* __restrict__ Zg = hg ? cg->ZGhat + (int64_t)s * cg->ldgh : nullptr;
     int status = mode;
+    // Z_j = AW_j + gamma EW_j over this CTA's rows, once per shift (same fma as before:
+    // the z partials are bitwise those of forming the column inside the loop)
+    double* Zs = P.zw + (size_t)(blockIdx.x / csz) * 16 * N;
+    for (int64_t i = rbeg + tid; i < rend; i += kAT) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < nw) Zs[(int64_t)j * N + i] = fma(gam, __ldg(EWg + (int64_t)j * ldw + i), __ldg(AWg + (int64_t)j * ldw + i));
+    }
+    // reciprocal pivots of the Cholesky factor (the solves multiply)
+    for (int i = tid; i < kMaxM; i += kAT) s_dinv[i] = (i < m) ? 1.0 / s_L[i + i * kMaxM] : 0.0;
     __syncthreads();
 
     for (;;) {
@@ -148,7 +161,7 @@ __global__ void __launch_bounds__(kAT, 1) cg_cluster_kernel(const __grid_constan
         Rv[i] = rn;
 #pragma unroll
         for (int j = 0; j < 16; ++j)
-          if (j < nw) acc[j] = fma(fma(gam, __ldg(EWg + (int64_t)j * ldw + i), __ldg(AWg + (int64_t)j * ldw + i)), rn, acc[j]);
+          if (j < nw) acc[j] = fma(Zs[(int64_t)j * N + i], rn, acc[j]);
         if (hg) accg = fma(__ldg(Zg + i), rn, accg);
         accr = fma(rn, rn, accr);
       }
@@ -213,7 +226,7 @@ __global__ void __launch_bounds__(kAT, 1) cg_cluster_kernel(const __grid_constan
               double t = s_z[i];
 #pragma unroll
               for (int j = 0; j < i; ++j) t -= s_L[i + j * kMaxM] * x[j];
-              x[i] = t / s_L[i + i * kMaxM];
+              x[i] = t * s_dinv[i];
             }
           }
 #pragma unroll
@@ -223,7 +236,7 @@ __global__ void __launch_bounds__(kAT, 1) cg_cluster_kernel(const __grid_constan
 #pragma unroll
               for (int j = i + 1; j < kMaxM; ++j)
                 if (j < m) t -= s_L[j + i * kMaxM] * x[j];
-              x[i] = t / s_L[i + i * kMaxM];
+              x[i] = t * s_dinv[i];
             }
           }
 #pragma unroll
@@ -295,7 +308,7 @@ __global__ void __launch_bounds__(kAT, 1) cg_cluster_kernel(const __grid_constan
 bool fill_apply_params(Handle* h, const ApplyLaunch& a, ApplyParams& prm);
 
 template <int R>
-static cudaError_t launch_cluster_r(ClusterParams& prm, bool tma, int csize, int nclusters, cudaStream_t st,
+static cudaError_t launch_cluster_r(ClusterParams& prm, bool tma, int csize, int nclusters, int slots, cudaStream_t st,
                                     bool* ok) {
   using C = TcCfg<R>;
   auto kfn = tma ? cg_cluster_kernel<R, true> : cg_cluster_kernel<R, false>;
@@ -320,7 +333,8 @@ static cudaError_t launch_cluster_r(ClusterParams& prm, bool tma, int csize, int
       maxcl[ti] = n;
     }
   }
-  const int ncl = nclusters < maxcl[ti] ? nclusters : maxcl[ti];
+  int ncl = nclusters < maxcl[ti] ? nclusters : maxcl[ti];
+  if (ncl > slots) ncl = slots;
   if (ncl < 1) { *ok = false; return cudaSuccess; }
   cudaLaunchConfig_t cfg = {};
   cudaLaunchAttribute at[1];
@@ -351,6 +365,14 @@ extern "C" int rsk_debug_cluster_prof(double* out8, int reset) {
   return 0;
 }
 
+int64_t cluster_max_n() {
+  const char* e = getenv("RSK_CG_CLUSTER_MAXN");
+  return e ? atoll(e) : 131072;
+}
+
+int cluster_size_for(const Handle* h);
+int cluster_slots(const Handle* h) { return h->sm_count / cluster_size_for(h) + 1; }
+
 int cluster_size_for(const Handle* h) {
   (void)h;
   const char* e = getenv("RSK_CG_CLUSTER");
@@ -360,7 +382,8 @@ int cluster_size_for(const Handle* h) {
 }
 
 // Runs every ACTIVE / RCONV shift to completion with one cluster per shift.
-cudaError_t launch_cg_cluster(Handle* h, CgDev* dev, const CgDev& hc, unsigned* queue, cudaStream_t st, bool* ok) {
+cudaError_t launch_cg_cluster(Handle* h, CgDev* dev, const CgDev& hc, unsigned* queue, const int* order,
+                              double* zw, cudaStream_t st, bool* ok) {
   ClusterParams prm;
   ApplyLaunch a{};
   a.X = hc.P; a.ldx = hc.N;
@@ -376,6 +399,8 @@ cudaError_t launch_cg_cluster(Handle* h, CgDev* dev, const CgDev& hc, unsigned* 
   prm.ap.cg = nullptr;
   prm.cg = dev;
   prm.queue = queue;
+  prm.order = order;
+  prm.zw = zw;
   prm.nshift = hc.nshift;
   int cs = cluster_size_for(h);
   int64_t rows = (hc.N + cs - 1) / cs;
@@ -384,20 +409,21 @@ cudaError_t launch_cg_cluster(Handle* h, CgDev* dev, const CgDev& hc, unsigned* 
   prm.prof = getenv("RSK_CLUSTER_PROF") ? 1 : 0;
   *ok = false;
   const int ncl = hc.nshift;
+  const int slots = cluster_slots(h);
   cudaError_t e = cudaSuccess;
   switch (h->r) {
-    case 1: e = launch_cluster_r<1>(prm, tma, cs, ncl, st, ok); break;
-    case 2: e = launch_cluster_r<2>(prm, tma, cs, ncl, st, ok); break;
-    case 3: e = launch_cluster_r<3>(prm, tma, cs, ncl, st, ok); break;
-    case 4: e = launch_cluster_r<4>(prm, tma, cs, ncl, st, ok); break;
-    case 5: e = launch_cluster_r<5>(prm, tma, cs, ncl, st, ok); break;
-    case 6: e = launch_cluster_r<6>(prm, tma, cs, ncl, st, ok); break;
-    case 7: e = launch_cluster_r<7>(prm, tma, cs, ncl, st, ok); break;
-    case 8: e = launch_cluster_r<8>(prm, tma, cs, ncl, st, ok); break;
-    case 9: e = launch_cluster_r<9>(prm, tma, cs, ncl, st, ok); break;
-    case 10: e = launch_cluster_r<10>(prm, tma, cs, ncl, st, ok); break;
-    case 11: e = launch_cluster_r<11>(prm, tma, cs, ncl, st, ok); break;
-    case 12: e = launch_cluster_r<12>(prm, tma, cs, ncl, st, ok); break;
+    case 1: e = launch_cluster_r<1>(prm, tma, cs, ncl, slots, st, ok); break;
+    case 2: e = launch_cluster_r<2>(prm, tma, cs, ncl, slots, st, ok); break;
+    case 3: e = launch_cluster_r<3>(prm, tma, cs, ncl, slots, st, ok); break;
+    case 4: e = launch_cluster_r<4>(prm, tma, cs, ncl, slots, st, ok); break;
+    case 5: e = launch_cluster_r<5>(prm, tma, cs, ncl, slots, st, ok); break;
+    case 6: e = launch_cluster_r<6>(prm, tma, cs, ncl, slots, st, ok); break;
+    case 7: e = launch_cluster_r<7>(prm, tma, cs, ncl, slots, st, ok); break;
+    case 8: e = launch_cluster_r<8>(prm, tma, cs, ncl, slots, st, ok); break;
+    case 9: e = launch_cluster_r<9>(prm, tma, cs, ncl, slots, st, ok); break;
+    case 10: e = launch_cluster_r<10>(prm, tma, cs, ncl, slots, st, ok); break;
+    case 11: e = launch_cluster_r<11>(prm, tma, cs, ncl, slots, st, ok); break;
+    case 12: e = launch_cluster_r<12>(prm, tma, cs, ncl, slots, st, ok); break;
     default: break;
   }
   return e;

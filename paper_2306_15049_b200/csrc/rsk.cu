@@ -416,7 +416,7 @@ namespace {
 
 struct WsLayout {
   size_t off_R, off_P, off_W, off_dbl, off_int, off_cnt, off_pA, off_pB, off_list, off_dev, off_gb, total;
-  size_t off_glist, off_partG, off_cntG, off_partP, off_pbar;
+  size_t off_glist, off_partG, off_cntG, off_partP, off_pbar, off_zw;
   int nchunkP;
   int64_t rowsP;
   int nblkA, nblkB;
@@ -451,7 +451,7 @@ WsLayout ws_layout(const Handle* h, int ns) {
   L.off_cnt = o; o = al(o + sizeof(unsigned) * (size_t)ns * 4);
   L.off_pA = o; o = al(o + sizeof(double) * (size_t)ns * L.nblkA);
   L.off_pB = o; o = al(o + sizeof(double) * (size_t)ns * L.nblkB * (kMaxM + 1));
-  L.off_list = o; o = al(o + sizeof(int) * (size_t)ns * 2);
+  L.off_list = o; o = al(o + sizeof(int) * (size_t)ns * 3);
   L.off_dev = o; o = al(o + sizeof(CgDev));
   L.off_gb = o; o = al(o + sizeof(double) * (size_t)(RSK_MAX_GROUPS * (2 * 16 * 16 + 3 * 16 * ns) + ns));
   // persistent loop: one row chunk (multiple of 256 rows) per CTA of the cooperative grid
@@ -464,6 +464,9 @@ WsLayout ws_layout(const Handle* h, int ns) {
   }
   L.off_partP = o; o = al(o + sizeof(double) * (size_t)ns * L.nchunkP * persist_pv());
   L.off_pbar = o; o = al(o + sizeof(unsigned) * 8);
+  // cluster-per-shift loop: per cluster, Z_s = AW + gamma_s EW of its current shift
+  L.off_zw = o;
+  if (N <= cluster_max_n()) o = al(o + sizeof(double) * (size_t)cluster_slots(h) * 16 * N);
   L.total = o;
   return L;
 }
@@ -740,12 +743,34 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
   // Small images (working set in L2): one thread-block cluster per shift, no lockstep
   // (cg_cluster.cu). The whole loop incl. confirmations runs in one launch.
   const bool cluster_mode = !prof && getenv("RSK_CG_LEGACY") == nullptr && getenv("RSK_CG_NOCLUSTER") == nullptr &&
-                            N <= (int64_t)(getenv("RSK_CG_CLUSTER_MAXN") ? atoll(getenv("RSK_CG_CLUSTER_MAXN")) : 131072);
+                            N <= cluster_max_n();
+  // device-loop kernel time (CUDA events on the launching stream) for the roofline
+  cudaEvent_t dl0 = nullptr, dl1 = nullptr;
+  double dl_kind = 0.0;
+  RSK_CUDA(cudaEventCreate(&dl0));
+  RSK_CUDA(cudaEventCreate(&dl1));
+  std::vector<int> it0(ns, 0);
+  RSK_CUDA(cudaMemcpyAsync(it0.data(), hc.iters, sizeof(int) * ns, cudaMemcpyDeviceToHost, st));
+  RSK_CUDA(cudaEventRecord(dl0, st));
   if (cluster_mode) {
     unsigned* pbar = reinterpret_cast<unsigned*>(base + L.off_pbar);
     RSK_CUDA(cudaMemsetAsync(pbar, 0, sizeof(unsigned) * 8, st));
     bool ok = false;
-    RSK_CUDA(launch_cg_cluster(h, dev, hc, pbar + 6, st, &ok));
+    int* dorder = nullptr;
+    if (d->order_h) {
+      std::vector<int> seen(ns, 0);
+      bool perm = true;
+      for (int s = 0; s < ns; ++s) {
+        const int v = d->order_h[s];
+        if (v < 0 || v >= ns || seen[v]) { perm = false; break; }
+        seen[v] = 1;
+      }
+      RSK_ARG(perm, "rsk_cg_recycled_batch: order_h is not a permutation");
+      dorder = dlist + 2 * ns;
+      RSK_CUDA(cudaMemcpyAsync(dorder, d->order_h, sizeof(int) * ns, cudaMemcpyHostToDevice, st));
+    }
+    RSK_CUDA(launch_cg_cluster(h, dev, hc, pbar + 6, dorder, reinterpret_cast<double*>(base + L.off_zw), st, &ok));
+    if (ok) dl_kind = 1.0;
     if (ok) {
       std::vector<int> ncf(ns, 0);
       RSK_CUDA(cudaMemcpyAsync(stat_h.data(), hc.status, sizeof(int) * ns, cudaMemcpyDeviceToHost, st));
@@ -779,6 +804,7 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
       }
     }
     if (persisted) {
+      dl_kind = 2.0;
       std::vector<int> ncf(ns, 0);
       RSK_CUDA(cudaMemcpyAsync(stat_h.data(), hc.status, sizeof(int) * ns, cudaMemcpyDeviceToHost, st));
       RSK_CUDA(cudaMemcpyAsync(ncf.data(), hc.nconf, sizeof(int) * ns, cudaMemcpyDeviceToHost, st));
@@ -815,6 +841,12 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
     }
     return cudaSuccess;
   };
+  RSK_CUDA(cudaEventRecord(dl1, st));
+  RSK_CUDA(cudaEventSynchronize(dl1));
+  float dl_ms = 0.0f;
+  cudaEventElapsedTime(&dl_ms, dl0, dl1);
+  cudaEventDestroy(dl0);
+  cudaEventDestroy(dl1);
   while (!active.empty()) {
     // active shifts grouped by shift group (group-shared kernels), with offsets/counts
     {
@@ -938,6 +970,16 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
   for (int s = 0; s < ns; ++s) { tot_it += it_h[s]; tot_ap += o->applies[s]; }
   h->nA += tot_ap;
   h->nE += tot_ap;
+  if (o->ms_loop && !prof) {
+    for (int i = 0; i < 5; ++i) o->ms_loop[i] = 0.0;
+  }
+  if (o->ms_loop) {
+    int64_t dits = 0;
+    for (int s = 0; s < ns; ++s) dits += (int64_t)(it_h[s] - it0[s]) + confirms[s];
+    o->ms_loop[5] = dl_kind > 0 ? dl_ms : 0.0;
+    o->ms_loop[6] = dl_kind > 0 ? (double)dits : 0.0;
+    o->ms_loop[7] = dl_kind;
+  }
   if (prof) {
     o->ms_loop[0] = ms_apply;
     o->ms_loop[1] = ms_upd;

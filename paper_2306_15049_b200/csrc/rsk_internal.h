@@ -171,7 +171,10 @@ int cg_nblkB(int64_t N);
 cudaError_t launch_cg_update_grp(CgDev* dev, const CgDev& host, int ngroups, int maxtiles, cudaStream_t st);
 cudaError_t launch_cg_combine_grp(CgDev* dev, const CgDev& host, int ngroups, int maxtiles, cudaStream_t st);
 // cluster-per-shift loop (cg_cluster.cu)
-cudaError_t launch_cg_cluster(Handle* h, CgDev* dev, const CgDev& hc, unsigned* queue, cudaStream_t st, bool* ok);
+cudaError_t launch_cg_cluster(Handle* h, CgDev* dev, const CgDev& hc, unsigned* queue, const int* order,
+                              double* zw, cudaStream_t st, bool* ok);
+int64_t cluster_max_n();          // largest N run cluster-per-shift (L2-resident working set)
+int cluster_slots(const Handle* h);   // upper bound on concurrently running clusters
 // persistent lockstep loop (cg_persist.cu)
 int persist_grid(const Handle* h);
 int persist_max_shift();

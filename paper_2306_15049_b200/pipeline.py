@@ -103,7 +103,7 @@ class GpuSolver:
 
     # ------------------------------------------------------------- building blocks
     def cg(self, gammas_idx, X, has_xp, Gout=None, groups=None, ghat=None, store=None,
-           flags=0):
+           flags=0, order=None):
         cfg = self.cfg
         ns = len(gammas_idx)
         gam = np.ascontiguousarray(self.gamma[gammas_idx])
@@ -115,6 +115,9 @@ class GpuSolver:
         hx = np.ascontiguousarray(has_xp, dtype=np.int32)
         d.has_xp_h = hx.ctypes.data_as(L.C.POINTER(L.C.c_int))
         d.Gout = Gout.data_ptr() if Gout is not None else None
+        if order is not None:   # device-loop start order (longest predicted first)
+            od = np.ascontiguousarray(order, dtype=np.int32)
+            d.order_h = od.ctypes.data_as(L.C.POINTER(L.C.c_int))
         d.ldg = self.N
         keep = []
         if groups is not None:
@@ -143,10 +146,12 @@ class GpuSolver:
         if self.profile:
             flags |= L.RSK_CG_PROFILE
         d.tol = cfg.tol; d.maxit = cfg.maxit; d.check_every = self.check_every; d.flags = flags
+        if order is not None:
+            keep.append(od)
         out = L.CgOut()
         iters = np.zeros(ns, dtype=np.int32); apl = np.zeros(ns, dtype=np.int64)
         rel = np.zeros(ns); stt = np.zeros(ns, dtype=np.int32); mu = np.zeros(ns, dtype=np.int32)
-        sc = np.zeros(ns, dtype=np.int32); ms = np.zeros(5)
+        sc = np.zeros(ns, dtype=np.int32); ms = np.zeros(8)
         P = L.C.POINTER
         out.iters = iters.ctypes.data_as(P(L.C.c_int)); out.applies = apl.ctypes.data_as(P(L.C.c_int64))
         out.relres_true = rel.ctypes.data_as(L._hp); out.status = stt.ctypes.data_as(P(L.C.c_int))
@@ -301,12 +306,16 @@ class GpuSolver:
         # ---- batched deflated CG on this rank's shifts
         G = torch.empty(ml, N, **self.f)
         if ml:
-            res = self.cg(mine, X, has_xp[mine], Gout=G, groups=groups, ghat=ghat)
+            prev = st.get("prev_iters")
+            order = None
+            if prev is not None and len(prev) == M:   # longest-processing-time first
+                order = np.argsort(-np.asarray(prev)[mine], kind="stable")
+            res = self.cg(mine, X, has_xp[mine], Gout=G, groups=groups, ghat=ghat, order=order)
             self.h.lcurve_norms(X, self.d, self.rho_dev, self.eta_dev, self.lc_scratch, stream=self.stream)
             rho_l, eta_l = _host(self.rho_dev)[:ml], _host(self.eta_dev)[:ml]
         else:
             res = dict(iters=np.zeros(0, np.int32), applies=np.zeros(0, np.int64), status=np.zeros(0, np.int32),
-                       relres=np.zeros(0), m_used=np.zeros(0, np.int32), prof=np.zeros(5))
+                       relres=np.zeros(0), m_used=np.zeros(0, np.int32), prof=np.zeros(8))
             rho_l = eta_l = np.zeros(0)
         # ---- exchange (allgather) and the L-curve
         if dist.enabled:
