@@ -303,6 +303,41 @@ rsk_status rsk_chol_solve_small(int n, const double* G_h, int nrhs, const double
  * (reading G25): centred differences on the uniform log-lambda grid,
  * endpoints excluded, ties to the smallest index. Returns the 0-based index in
  * *lstar; kappa_h (nullable, [M]) receives the curvatures (-inf at the ends). */
+/* ---- deflated-CG host steps (row-slab loop; also used by the
+ * single-domain setup). Loop states: */
+enum { RSK_LOOP_ACTIVE = 0, RSK_LOOP_RCONV = 1, RSK_LOOP_DONE = 2, RSK_LOOP_BREAKDOWN = 3, RSK_LOOP_MAXIT = 4 };
+
+/* Local Gram matrices G_l = sym(U_l^T (A + gamma_l E) U_l) of U_l = [W_g, ghat_l] (Alg. 3/4
+ * P:700-746, reading D1) assembled from reduced host pieces, and their Cholesky factors;
+ * on failure the carried column is dropped, then all of U (dropped_h[s] = 1). WA/WE:
+ * [g][256] J_g x J_g (ld J_g) = W^T A W, W^T E W; WZg/AWg/EWg: [g][16 ns] J_g x ns = W^T Zghat_s,
+ * (AW)^T ghat_s, (EW)^T ghat_s; gzg [ns] = ghat_s^T Zghat_s (NULL if no ghat). hasg_h in/out.
+ * L_h: [ns][RSK_MAX_LOCAL^2], lower, column-major, ld RSK_MAX_LOCAL. Host only. */
+rsk_status rsk_local_gram_factors(int ns, int ngroups, const int* J_h, const int* group_of_shift_h,
+                                  const double* gamma_h, const double* WA_h, const double* WE_h,
+                                  const double* WZg_h, const double* AWg_h, const double* EWg_h,
+                                  const double* gzg_h, double* L_h, int* m_h, int* hasg_h, int* dropped_h);
+
+/* mu_s = G_s^-1 [zA_s + gamma_s zE_s ; zG_s] with the factors of rsk_local_gram_factors
+ * (zA: J x ns, ld J; zE, zG nullable = 0; mu: [ns][RSK_MAX_LOCAL]). Host only. */
+rsk_status rsk_gram_solve(int ns, int J, const double* L_h, const int* m_h, const int* hasg_h,
+                          const double* gamma_h, const double* zA_h, const double* zE_h, const double* zG_h,
+                          double* mu_h);
+
+/* alpha_s = rho_s / (p_s . w_s) for shifts in RSK_LOOP_ACTIVE (O4 step 3); a non-positive
+ * or non-finite p.w sets RSK_LOOP_BREAKDOWN. Host arrays [ns]. */
+rsk_status rsk_cg_alpha(int ns, const double* rho_h, const double* pw_h, double* alpha_h, int* state_h);
+
+/* Scalar half of an iteration from the reduced sums of the new residual (O4 steps 3-4):
+ * rho' = r.r, zA = (AW)^T r, zE = (EW)^T r (J x ns, ld J), zG = ZGhat^T r. mode_h = state at
+ * the iteration start (ACTIVE: loop step, RCONV: r is the true residual). Updates rho, iters,
+ * rho_true, nconf, state; writes beta and mu = G^-1 z ([ns][RSK_MAX_LOCAL]). Host only. */
+rsk_status rsk_cg_scalars(int ns, int J, const int* mode_h, const double* gamma_h, const double* rho_new_h,
+                          const double* zA_h, const double* zE_h, const double* zG_h, const int* m_h,
+                          const int* hasg_h, const double* L_h, double thr, int maxit, double* rho_h,
+                          double* beta_h, double* mu_h, int* iters_h, double* rho_true_h, int* nconf_h,
+                          int* state_h);
+
 rsk_status rsk_lcurve_corner(int M, const double* rho_h, const double* eta_h, int* lstar,
                              double* kappa_h);
 

@@ -68,6 +68,8 @@ class CgOut(C.Structure):
     ]
 
 
+_ip = C.POINTER(C.c_int)
+
 _SIGS = {
     "rsk_version": (C.c_char_p, []),
     "rsk_launch_count": (C.c_int64, []),
@@ -100,6 +102,12 @@ _SIGS = {
     "rsk_svd_small": (C.c_int, [C.c_int, _hp, _hp, _hp, _hp]),
     "rsk_chol_solve_small": (C.c_int, [C.c_int, _hp, C.c_int, _hp, _hp]),
     "rsk_lcurve_corner": (C.c_int, [C.c_int, _hp, _hp, C.POINTER(C.c_int), _hp]),
+    "rsk_local_gram_factors": (C.c_int, [C.c_int, C.c_int, _ip, _ip, _hp, _hp, _hp, _hp, _hp, _hp, _hp, _hp,
+                                         _ip, _ip, _ip]),
+    "rsk_gram_solve": (C.c_int, [C.c_int, C.c_int, _hp, _ip, _ip, _hp, _hp, _hp, _hp, _hp]),
+    "rsk_cg_alpha": (C.c_int, [C.c_int, _hp, _hp, _hp, _ip]),
+    "rsk_cg_scalars": (C.c_int, [C.c_int, C.c_int, _ip, _hp, _hp, _hp, _hp, _hp, _ip, _ip, _hp, C.c_double,
+                                 C.c_int, _hp, _hp, _hp, _ip, _hp, _ip, _ip]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -322,3 +322,156 @@ extern "C" rsk_status rsk_lcurve_corner(int M, const double* rho_h, const double
     for (int l = 0; l < M; ++l) kappa_h[l] = kap[l];
   return RSK_OK;
 }
+
+// ---------------------------------------------------------------- deflated-CG host steps
+// Local Gram matrices G_l = sym(U_l^T Z_l), U_l = [W_g(l), ghat_l], Z_l = A_gamma U_l, from
+// their reduced pieces, and their Cholesky factors with the drop rule of O4 (first the
+// carried column, then all of U). Layout: WA/WE [g][16*16] (J_g x J_g, ld J_g),
+// WZg/AWg/EWg [g][16*ns] (J_g x ns, ld J_g), L [ns][RSK_MAX_LOCAL^2] (ld RSK_MAX_LOCAL).
+extern "C" rsk_status rsk_local_gram_factors(int ns, int ngroups, const int* J_h, const int* group_of_shift_h,
+                                             const double* gamma_h, const double* WA_h, const double* WE_h,
+                                             const double* WZg_h, const double* AWg_h, const double* EWg_h,
+                                             const double* gzg_h, double* L_h, int* m_h, int* hasg_h,
+                                             int* dropped_h) {
+  using rsk::kMaxM;
+  if (ns < 0 || ngroups < 1 || ngroups > RSK_MAX_GROUPS || !J_h || !group_of_shift_h || !gamma_h || !WA_h ||
+      !WE_h || !L_h || !m_h || !hasg_h || !dropped_h)
+    return RSK_EINVAL;
+  std::vector<double> Gm(kMaxM * kMaxM);
+  for (int s = 0; s < ns; ++s) {
+    const int g = group_of_shift_h[s];
+    if (g < 0 || g >= ngroups) return RSK_EINVAL;
+    const int J = J_h[g];
+    if (J < 0 || J > 16) return RSK_EINVAL;
+    if (hasg_h[s] && (!WZg_h || !AWg_h || !EWg_h || !gzg_h)) return RSK_EINVAL;
+    const double gm = gamma_h[s];
+    int nwk = J, hg = hasg_h[s] ? 1 : 0;
+    int m = nwk + hg;
+    dropped_h[s] = 0;
+    for (;;) {
+      if (m == 0) break;
+      for (int j = 0; j < m; ++j)
+        for (int i = 0; i < m; ++i) {
+          double v;
+          if (i < nwk && j < nwk) {
+            const double a = WA_h[g * 256 + i + j * J] + gm * WE_h[g * 256 + i + j * J];
+            const double b = WA_h[g * 256 + j + i * J] + gm * WE_h[g * 256 + j + i * J];
+            v = 0.5 * (a + b);
+          } else if (i < nwk && j == nwk) {   // W_i^T Zg  and  ghat^T Z_i
+            const double a = WZg_h[(size_t)g * 16 * ns + i + (size_t)s * J];
+            const double b = AWg_h[(size_t)g * 16 * ns + i + (size_t)s * J] + gm * EWg_h[(size_t)g * 16 * ns + i + (size_t)s * J];
+            v = 0.5 * (a + b);
+          } else if (i == nwk && j < nwk) {
+            const double a = WZg_h[(size_t)g * 16 * ns + j + (size_t)s * J];
+            const double b = AWg_h[(size_t)g * 16 * ns + j + (size_t)s * J] + gm * EWg_h[(size_t)g * 16 * ns + j + (size_t)s * J];
+            v = 0.5 * (a + b);
+          } else {
+            v = gzg_h[s];
+          }
+          Gm[i + j * m] = v;
+        }
+      if (rsk::chol_lower(m, Gm.data())) break;
+      dropped_h[s] = 1;
+      if (hg) { hg = 0; m = nwk; } else { nwk = 0; m = 0; }
+    }
+    for (int e = 0; e < kMaxM * kMaxM; ++e) L_h[(size_t)s * kMaxM * kMaxM + e] = 0.0;
+    for (int j = 0; j < m; ++j)
+      for (int i = 0; i < m; ++i) L_h[(size_t)s * kMaxM * kMaxM + i + j * kMaxM] = Gm[i + j * m];
+    m_h[s] = m;
+    hasg_h[s] = hg;
+  }
+  return RSK_OK;
+}
+
+// mu_s = G_s^-1 [zA_s + gamma_s zE_s ; zG_s] with the factors of rsk_local_gram_factors
+// (zE / zG nullable = 0). Forward then backward substitution, same order as the device loop.
+extern "C" rsk_status rsk_gram_solve(int ns, int J, const double* L_h, const int* m_h, const int* hasg_h,
+                                     const double* gamma_h, const double* zA_h, const double* zE_h,
+                                     const double* zG_h, double* mu_h) {
+  using rsk::kMaxM;
+  if (ns < 0 || J < 0 || J > 16 || !L_h || !m_h || !hasg_h || !gamma_h || !mu_h || (J > 0 && !zA_h))
+    return RSK_EINVAL;
+  for (int s = 0; s < ns; ++s) {
+    double* mu = mu_h + (size_t)s * kMaxM;
+    for (int j = 0; j < kMaxM; ++j) mu[j] = 0.0;
+    const int m = m_h[s], hg = hasg_h[s], nw = m - hg;
+    if (m < 0 || m > kMaxM || nw > J) return RSK_EINVAL;
+    for (int j = 0; j < nw; ++j)
+      mu[j] = zE_h ? zA_h[j + (size_t)s * J] + gamma_h[s] * zE_h[j + (size_t)s * J] : zA_h[j + (size_t)s * J];
+    if (hg) mu[nw] = zG_h ? zG_h[s] : 0.0;
+    const double* L = L_h + (size_t)s * kMaxM * kMaxM;
+    for (int i = 0; i < m; ++i) {
+      double t = mu[i];
+      for (int j = 0; j < i; ++j) t -= L[i + j * kMaxM] * mu[j];
+      mu[i] = t / L[i + i * kMaxM];
+    }
+    for (int i = m - 1; i >= 0; --i) {
+      double t = mu[i];
+      for (int j = i + 1; j < m; ++j) t -= L[j + i * kMaxM] * mu[j];
+      mu[i] = t / L[i + i * kMaxM];
+    }
+  }
+  return RSK_OK;
+}
+
+// alpha = rho / (p.w) for the shifts in state RSK_LOOP_ACTIVE (O4 step 3); p.w <= 0 or
+// non-finite -> RSK_LOOP_BREAKDOWN with alpha = 0.
+extern "C" rsk_status rsk_cg_alpha(int ns, const double* rho_h, const double* pw_h, double* alpha_h, int* state_h) {
+  if (ns < 0 || !rho_h || !pw_h || !alpha_h || !state_h) return RSK_EINVAL;
+  for (int s = 0; s < ns; ++s) {
+    alpha_h[s] = 0.0;
+    if (state_h[s] != RSK_LOOP_ACTIVE) continue;
+    const double pi = pw_h[s];
+    if (!(pi > 0.0) || !std::isfinite(pi)) state_h[s] = RSK_LOOP_BREAKDOWN;
+    else alpha_h[s] = rho_h[s] / pi;
+  }
+  return RSK_OK;
+}
+
+// The scalar half of a deflated-CG iteration (O4 steps 3-4) from the reduced sums of the
+// updated residual: rho' = r.r and z = [AW^T r + gamma EW^T r ; ZGhat^T r]. mode_h[s] is the
+// state at the start of the iteration (RSK_LOOP_ACTIVE: loop step; RSK_LOOP_RCONV: r was
+// the true residual b - A_gamma x). Writes beta, mu = G^-1 z (Cholesky factor L from
+// rsk_local_gram_factors; ld RSK_MAX_LOCAL per shift) and the new state.
+extern "C" rsk_status rsk_cg_scalars(int ns, int J, const int* mode_h, const double* gamma_h,
+                                     const double* rho_new_h, const double* zA_h, const double* zE_h,
+                                     const double* zG_h, const int* m_h, const int* hasg_h, const double* L_h,
+                                     double thr, int maxit, double* rho_h, double* beta_h, double* mu_h,
+                                     int* iters_h, double* rho_true_h, int* nconf_h, int* state_h) {
+  using rsk::kMaxM;
+  if (ns < 0 || J < 0 || J > 16 || !mode_h || !gamma_h || !rho_new_h || !m_h || !hasg_h || !L_h || !rho_h ||
+      !beta_h || !mu_h || !iters_h || !rho_true_h || !nconf_h || !state_h)
+    return RSK_EINVAL;
+  for (int s = 0; s < ns; ++s) {
+    const int mode = mode_h[s];
+    if (mode != RSK_LOOP_ACTIVE && mode != RSK_LOOP_RCONV) continue;
+    if (state_h[s] != mode) continue;   // BREAKDOWN in this iteration
+    const double rn = rho_new_h[s];
+    const bool conv = std::sqrt(rn) <= thr;
+    bool newp = false;
+    beta_h[s] = 0.0;
+    if (mode == RSK_LOOP_ACTIVE) {
+      iters_h[s] += 1;
+      beta_h[s] = rn / rho_h[s];
+      rho_h[s] = rn;
+      if (conv) state_h[s] = RSK_LOOP_RCONV;
+      else if (iters_h[s] >= maxit) state_h[s] = RSK_LOOP_MAXIT;
+      else newp = true;
+    } else {
+      rho_true_h[s] = rn;
+      nconf_h[s] += 1;
+      if (conv) state_h[s] = RSK_LOOP_DONE;
+      else if (iters_h[s] >= maxit) state_h[s] = RSK_LOOP_MAXIT;
+      else { state_h[s] = RSK_LOOP_ACTIVE; rho_h[s] = rn; newp = true; }
+    }
+    double* mu = mu_h + (size_t)s * kMaxM;
+    for (int j = 0; j < kMaxM; ++j) mu[j] = 0.0;
+    if (newp) {
+      rsk_status e = rsk_gram_solve(1, J, L_h + (size_t)s * kMaxM * kMaxM, m_h + s, hasg_h + s, gamma_h + s,
+                                    zA_h + (size_t)s * J, zE_h ? zE_h + (size_t)s * J : nullptr,
+                                    zG_h ? zG_h + s : nullptr, mu);
+      if (e != RSK_OK) return e;
+    }
+  }
+  return RSK_OK;
+}

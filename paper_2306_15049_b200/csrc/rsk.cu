@@ -629,44 +629,12 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
       RSK_CUDA(cudaMemcpyAsync(gzg.data(), o3, sizeof(double) * ns, cudaMemcpyDeviceToHost, st));
     }
     RSK_CUDA(cudaStreamSynchronize(st));
-    std::vector<double> Gm(kMaxM * kMaxM);
-    for (int s = 0; s < ns; ++s) {
-      const int g = grp[s], J = d->J[g];
-      const double gm = d->gamma_h[s];
-      int m = J + hasg[s];
-      int nwk = J, hg = hasg[s];
-      for (;;) {
-        if (m == 0) break;
-        for (int j = 0; j < m; ++j)
-          for (int i = 0; i < m; ++i) {
-            double v;
-            if (i < nwk && j < nwk) {
-              const double a = WA[g * 256 + i + j * J] + gm * WE[g * 256 + i + j * J];
-              const double b = WA[g * 256 + j + i * J] + gm * WE[g * 256 + j + i * J];
-              v = 0.5 * (a + b);
-            } else if (i < nwk && j == nwk) {   // W_i^T Zg  and  ghat^T Z_i
-              const double a = WZg[(size_t)g * 16 * ns + i + (size_t)s * J];
-              const double b = AWg[(size_t)g * 16 * ns + i + (size_t)s * J] + gm * EWg[(size_t)g * 16 * ns + i + (size_t)s * J];
-              v = 0.5 * (a + b);
-            } else if (i == nwk && j < nwk) {
-              const double a = WZg[(size_t)g * 16 * ns + j + (size_t)s * J];
-              const double b = AWg[(size_t)g * 16 * ns + j + (size_t)s * J] + gm * EWg[(size_t)g * 16 * ns + j + (size_t)s * J];
-              v = 0.5 * (a + b);
-            } else {
-              v = gzg[s];
-            }
-            Gm[i + j * m] = v;
-          }
-        if (chol_lower(m, Gm.data())) break;
-        dropped[s] = 1;
-        if (hg) { hg = 0; m = nwk; } else { nwk = 0; m = 0; }
-      }
-      // store L with leading dimension kMaxM
-      for (int j = 0; j < m; ++j)
-        for (int i = 0; i < m; ++i) Lf[(size_t)s * kMaxM * kMaxM + i + j * kMaxM] = Gm[i + j * m];
-      mloc[s] = m;
-      hasg[s] = hg;
-    }
+    std::vector<int> Jh(G);
+    for (int g = 0; g < G; ++g) Jh[g] = d->J[g];
+    rsk_status gs = rsk_local_gram_factors(ns, G, Jh.data(), grp.data(), d->gamma_h, WA.data(), WE.data(),
+                                           WZg.data(), AWg.data(), EWg.data(), gzg.data(), Lf.data(),
+                                           mloc.data(), hasg.data(), dropped.data());
+    if (gs != RSK_OK) { h->err = "rsk_cg_recycled_batch: local Gram factors"; return gs; }
   }
 
   // ---- upload per-shift state

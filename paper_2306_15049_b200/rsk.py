@@ -22,8 +22,8 @@ class RskError(RuntimeError):
 def _dptr(t):
     if t is None:
         return None
-    if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
-        raise RskError("librsk needs contiguous CUDA float64 tensors")
+    if not (t.is_cuda and t.dtype == torch.float64 and (t.is_contiguous() or (t.dim() == 2 and t.stride(-1) == 1))):
+        raise RskError("librsk needs CUDA float64 tensors with unit-stride rows")
     return t.data_ptr()
 
 
@@ -32,7 +32,13 @@ def _hp(a: np.ndarray):
 
 
 def _ld(t) -> int:
-    return t.shape[-1] if t.dim() > 1 else t.numel()
+    """Leading dimension (elements between consecutive vectors): row views of a wider
+    batch (e.g. the owned rows of row-slab vectors) keep their parent's stride."""
+    if t.dim() > 1:
+        if t.stride(-1) != 1:
+            raise ValueError("librsk vectors must be unit-stride")
+        return t.stride(0) if t.shape[0] > 1 else max(t.stride(0), t.shape[-1])
+    return t.numel()
 
 
 def _nv(t) -> int:
