@@ -1,0 +1,141 @@
+"""Parity at BASELINE.json's full sizes, in the launch configurations bench.py times.
+
+* The fused apply (rsk_apply_shifted, standalone launch) of configs C2..C5 -- 256^2 to
+  4096^2, PSF 9x9 to 21x21, IRN-shaped weights -- against the oracle evaluated pixel by
+  pixel on sampled outputs (corners, edge bands at 0, r, 2r, 2r+1 pixels, interior): the
+  oracle applies O1 literally to a (4r+1)^2 patch holding the pixel (moved inside the
+  image at the edges); the patch edges that are not image edges lie >= 2r+1 away,
+  outside the reach of their own truncation. Bar: 1e-13 relative to the largest |output|.
+* The nested solve of C2 (the bench workload; cluster-per-shift CG loop): every shift's
+  solution at outer steps 0 and 1 has an oracle-computed true residual
+  ||b - (A + gamma E_k) x|| <= tol ||b||, where E_1's weights are the oracle's IRN weights
+  of the GPU's x* (after checking the GPU weights equal them to 4 ulp).
+* The row-slab apply (C5, 2 and 4 slabs emulated on one GPU) against the single-domain
+  apply on every owned row (1e-13)."""
+import numpy as np
+import pytest
+
+import rsk_synth as S
+from oracle import operators as ops
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_dev():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA")
+    return torch, torch.device("cuda", 0)
+
+
+def _samples(n, r, seed, k=24):
+    g = np.random.Generator(np.random.PCG64(seed))
+    edge = sorted({0, 1, r, 2 * r, 2 * r + 1, n // 2, n - 1 - 2 * r, n - 1 - r, n - 2, n - 1})
+    pts = [(i, j) for i in edge[:3] + edge[-3:] for j in (edge[0], edge[3], edge[-1])]
+    pts += [tuple(v) for v in g.integers(0, n, size=(k, 2))]
+    return pts
+
+
+def _oracle_at(h, wx, wy, gam, x, i, j, r):
+    # square (4r+1)^2 patch holding the pixel, shifted inside the image at the edges:
+    # every patch edge is either an image edge or >= 2r + 1 pixels from (i, j)
+    n = x.shape[0]
+    P = min(n, 4 * r + 1)
+    i0 = min(max(i - 2 * r, 0), n - P)
+    j0 = min(max(j - 2 * r, 0), n - P)
+    i1, j1 = i0 + P, j0 + P
+    xp = x[i0:i1, j0:j1]
+    a = ops.apply_A(h, xp)[i - i0, j - j0]
+    e = ops.apply_E(wx[i0:i1, j0:j1], wy[i0:i1, j0:j1], xp)[i - i0, j - j0]
+    return a + gam * e
+
+
+@pytest.mark.parametrize("cfgname", ["C2", "C3", "C4", "C5"])
+def test_apply_full_size_sampled(torch_dev, cfgname):
+    torch, dev = torch_dev
+    from paper_2306_15049_b200.rsk import Handle
+    cfg = S.CONFIGS[cfgname]
+    n, r = cfg.n, cfg.r
+    psf = S.gaussian_psf(r, cfg.sigma)
+    wx, wy = S.random_weights(40 + cfg.index, n, lo=0.5, hi=1.0 / cfg.tau)
+    X = S.random_vectors(50 + cfg.index, (2, n * n))
+    gam = np.array([cfg.gamma_lo, cfg.gamma_hi])
+    h = Handle(n, n, psf, 0)
+    h.set_weights(torch.from_numpy(wx.ravel().copy()).to(dev), torch.from_numpy(wy.ravel().copy()).to(dev))
+    Xd = torch.from_numpy(X).to(dev)
+    Y = torch.empty_like(Xd)
+    h.apply_shifted(Xd, Y, gamma=torch.from_numpy(gam).to(dev))
+    Yh = Y.cpu().numpy()
+    for s in range(2):
+        img = X[s].reshape(n, n)
+        scale = np.max(np.abs(Yh[s]))
+        for (i, j) in _samples(n, r, 60 + s):
+            ref = _oracle_at(psf, wx, wy, gam[s], img, i, j, r)
+            assert abs(Yh[s, i * n + j] - ref) <= 1e-13 * scale, (cfgname, s, i, j)
+
+
+def test_c2_nested_solve_true_residuals(torch_dev):
+    torch, dev = torch_dev
+    from paper_2306_15049_b200.pipeline import GpuSolver
+    cfg = S.CONFIGS["C2"]
+    inp = S.make_inputs(cfg)
+    n = cfg.n
+    sol = GpuSolver(cfg, inp["psf"], inp["gamma"], device=0)
+    sol.set_data(torch.from_numpy(inp["x_true"]).to(dev), torch.from_numpy(inp["xi"]).to(dev))
+    d, b = ops.make_data(inp["psf"], inp["x_true"], inp["xi"], cfg.noise)
+    nb = np.linalg.norm(b)
+    wx, wy = ops.identity_weights(n)
+    outs = sol.run(K_out=1)
+    st = sol.final
+    for k in range(2):
+        X = st["X_prev"].cpu().numpy()
+        for l in range(cfg.M):
+            rt = b - ops.apply_shifted(inp["psf"], wx, wy, inp["gamma"][l], X[l].reshape(n, n))
+            assert np.linalg.norm(rt) <= cfg.tol * nb * (1 + 1e-6), (k, l, np.linalg.norm(rt) / nb)
+        if k == 0:
+            xs = st["xstar"].cpu().numpy().reshape(n, n)
+            wx, wy = ops.irn_weights(xs, cfg.tau)
+            sol.next_weights(st["xstar"])
+            gx, gy = sol.wx.cpu().numpy().reshape(n, n), sol.wy.cpu().numpy().reshape(n, n)
+            ulp = np.spacing(np.maximum(np.abs(wx), np.abs(wy)).max())
+            assert np.max(np.abs(gx - wx)) <= 4 * ulp and np.max(np.abs(gy - wy)) <= 4 * ulp
+            o1, st = sol.outer_step(1, st)
+            assert o1.iters.sum() > 0
+
+
+@pytest.mark.parametrize("nranks", [2, 4])
+def test_c5_slab_apply_matches_single_domain(torch_dev, nranks):
+    torch, dev = torch_dev
+    from paper_2306_15049_b200.rsk import Handle
+    from paper_2306_15049_b200.slab import SlabOps, SlabPlan, run_threads
+    cfg = S.CONFIGS["C5"]
+    n, r = cfg.n, cfg.r
+    psf = S.gaussian_psf(r, cfg.sigma)
+    wx, wy = S.random_weights(77, n, lo=0.5, hi=1.0 / cfg.tau)
+    wxd = torch.from_numpy(wx.ravel().copy()).to(dev)
+    wyd = torch.from_numpy(wy.ravel().copy()).to(dev)
+    X = torch.from_numpy(S.random_vectors(78, (2, n * n))).to(dev)
+    gam = torch.tensor([cfg.gamma_lo, cfg.gamma_hi], dtype=torch.float64, device=dev)
+    h = Handle(n, n, psf, 0)
+    h.set_weights(wxd, wyd)
+    Y = torch.empty_like(X)
+    h.apply_shifted(X, Y, gamma=gam)
+    torch.cuda.synchronize()
+    scale = float(Y.abs().max())
+    plan = SlabPlan(n, n, r, nranks)
+
+    def rank_fn(k, comm):
+        so = SlabOps(plan, k, comm, psf, 0)
+        so.set_weights(wxd, wyd)
+        Xe = torch.zeros(2, plan.slabs[k].ext_rows * n, dtype=torch.float64, device=dev)
+        so.own(Xe).copy_(plan.owned(X, k))
+        Ye = torch.empty_like(Xe)
+        so.apply(Xe, Ye, gam)
+        torch.cuda.synchronize()
+        err = float((so.own(Ye) - plan.owned(Y, k)).abs().max())
+        del Xe, Ye
+        return err
+
+    errs = run_threads(plan, rank_fn)
+    assert max(errs) <= 1e-13 * scale, errs
