@@ -234,9 +234,9 @@ def run_ours(args, cfg, inputs, rank, world):
     kind = int(max(p[7] for p in prof_all)) if prof_all else 0
     J = cfg.J
     # algorithmic bytes per shift-iteration and pixel: apply p, w, W_k (32);
-    # update w, r, r', ZGhat, AW/EW (32 + 16 J); combine p, x, r, ghat, p', x', W (48 + 8 J);
-    # the group blocks are amortised over the shifts of a lockstep batch, not per cluster
-    per_px = (32 + 32 + 48 + 24 * J) if kind == 1 else (32 + 32 + 48 + 24 * J / max(1.0, cfg.M / 2))
+    # update w, r, r', ZGhat, Z = AW + gamma EW (32 + 8 J); combine p, x, r, ghat, p', x',
+    # W (48 + 8 J). Lockstep batches share AW, EW, W (24 J) over a group's shifts.
+    per_px = (32 + 32 + 48 + 16 * J) if kind == 1 else (32 + 32 + 48 + 24 * J / max(1.0, cfg.M / 2))
     alg_bytes = per_px * cfg.N * dl_its
     achieved = alg_bytes / (dl_ms / 1e3) / 1e9 if dl_ms > 0 else None
     peak, peak_src = _peaks()
