@@ -134,7 +134,7 @@ static cudaError_t launch_r(const ApplyParams& prm, bool tma, int sm_count, cuda
   return cudaGetLastError();
 }
 
-bool fill_apply_params(Handle* h, const ApplyLaunch& a, ApplyParams& prm) {
+bool fill_apply_params(Handle* h, const ApplyLaunch& a, ApplyParams& prm, int ty_override) {
   std::memset(&prm, 0, sizeof(prm));
   prm.X = a.X; prm.ldx = a.ldx;
   prm.X2 = a.X2; prm.ldx2 = a.ldx2;
@@ -147,7 +147,8 @@ bool fill_apply_params(Handle* h, const ApplyLaunch& a, ApplyParams& prm) {
   prm.cg = a.cg;
   prm.ny = (int)h->ny; prm.nx = (int)h->nx;
   prm.tiles_x = (int)((h->nx + kTX - 1) / kTX);
-  prm.ntiles = apply_tiles(h);
+  const int tyg = ty_override > 0 ? ty_override : tc_tile_rows(h->r);
+  prm.ntiles = prm.tiles_x * (int)((h->ny + tyg - 1) / tyg);
   prm.nlist = a.nlist;
   prm.nlist_dev = a.nlist_dev;
   prm.mode = a.mode;
@@ -170,7 +171,7 @@ bool fill_apply_params(Handle* h, const ApplyLaunch& a, ApplyParams& prm) {
   }
   // TMA map (box = the staged halo tile); any failure -> cp.async path
   const int r = h->r;
-  const int ty = tc_tile_rows(r);
+  const int ty = tyg;
   const int hy = ((ty + 4 * r + 7) / 8) * 8;
   const int px = pad4mod8(kTX + 4 * r);
   bool tma = getenv("RSK_NO_TMA") == nullptr;
@@ -183,7 +184,7 @@ bool fill_apply_params(Handle* h, const ApplyLaunch& a, ApplyParams& prm) {
 cudaError_t launch_apply(Handle* h, const ApplyLaunch& a, cudaStream_t st) {
   if (a.nlist <= 0) return cudaSuccess;
   ApplyParams prm;
-  const bool tma = fill_apply_params(h, a, prm);
+  const bool tma = fill_apply_params(h, a, prm, 0);
   if (a.xdoty && !a.cg) {
     const size_t need = sizeof(double) * (size_t)prm.ntiles * (size_t)a.nlist;
     if (need > h->scratch_bytes) return cudaErrorMemoryAllocation;

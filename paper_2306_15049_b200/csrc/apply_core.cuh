@@ -73,12 +73,14 @@ constexpr int kAT = 256;   // threads per apply CTA (8 warps); 2 CTAs per SM
 constexpr int kApplyCtasPerSm = 1;   // one CTA per SM: 255 registers, double-buffered stage
 constexpr int kStages = 2;
 
-template <int R>
+// TY_ = 0: the default tile height tc_tile_rows(R) (64-row halo, 16 balanced x-pass
+// units); the cluster-per-shift loop uses taller tiles so one shift has <= 1 tile per CTA.
+template <int R, int TY_ = 0>
 struct TcCfg {
   static constexpr int H = 2 * R;            // halo of A (E needs 1 <= H)
   static constexpr int T = 4 * R + 1;        // taps of B
   static constexpr int KS = R + 2;           // DMMA k-steps per 8x8 block: (8 + 4r) / 4
-  static constexpr int TY = tc_tile_rows(R); // output rows per tile (multiple of 8)
+  static constexpr int TY = TY_ ? TY_ : tc_tile_rows(R); // output rows per tile (multiple of 8)
   static constexpr int HY = ((TY + 4 * R + 7) / 8) * 8;  // staged rows (64)
   static constexpr int RBX = HY / 8;         // x-pass row blocks
   static constexpr int RBY = TY / 8;         // y-pass row blocks (one warp: all of them)
@@ -97,8 +99,7 @@ struct TcCfg {
   static constexpr size_t SMEM = sizeof(double) * (size_t)DBL;
   static constexpr unsigned XBYTES = 8u * HY * PX;
   static_assert(TY >= 8 && TY % 8 == 0, "tile rows");
-  static_assert(HY <= 64, "staged rows");
-  static_assert(2 * RBX == 2 * (kAT / 32), "x-pass: two units per warp");
+  static_assert(HY <= 128, "staged rows");
   static_assert(PX <= 256, "TMA box width");
   static_assert(kApplyCtasPerSm * (SMEM + 1024) <= 227 * 1024, "shared memory");
 };
@@ -142,9 +143,9 @@ struct ApplyPipe {
   int stage;   // stage buffer of the next item
 };
 
-template <int R, bool kTma>
+template <int R, bool kTma, int TY_ = 0>
 struct ApplyCore {
-  using C = TcCfg<R>;
+  using C = TcCfg<R, TY_>;
 
   __device__ static void init_bars(double* smem, const ApplyParams& p) {
     // boundary corrections of B (tiny, read at every edge output)

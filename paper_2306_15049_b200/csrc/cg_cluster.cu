@@ -45,10 +45,81 @@ __device__ __forceinline__ void cl_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
+// r = r - alpha w (loop) or b - w (confirm) over this CTA's rows; per-warp sums of
+// z_j = Z_j . r (j < nw), ZGhat . r (slot nw) and r . r (slot kMaxM) into red[warp][slot].
+// Separate function: its own register allocation, not the apply's.
+__device__ __noinline__ void cluster_update_rows(double* __restrict__ Rv, const double* __restrict__ Wv,
+                                                 const double* __restrict__ b, const double* __restrict__ Zs,
+                                                 const double* __restrict__ Zg, int64_t N, int64_t rbeg,
+                                                 int64_t rend, bool loop, double alpha, int nw, int hg,
+                                                 double* red) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double acc[16], accg = 0.0, accr = 0.0;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+#pragma unroll 2
+  for (int64_t i = rbeg + tid; i < rend; i += kAT) {
+    const double wv = Wv[i];
+    const double rn = loop ? fma(-alpha, wv, Rv[i]) : __ldg(b + i) - wv;
+    Rv[i] = rn;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j < nw) acc[j] = fma(Zs[(int64_t)j * N + i], rn, acc[j]);
+    if (hg) accg = fma(__ldg(Zg + i), rn, accg);
+    accr = fma(rn, rn, accr);
+  }
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    if (j < nw) {
+      const double v = warp_sum(acc[j]);
+      if (lane == 0) red[warp * kCV + j] = v;
+    }
+  }
+  if (hg) {
+    const double v = warp_sum(accg);
+    if (lane == 0) red[warp * kCV + nw] = v;
+  }
+  const double v = warp_sum(accr);
+  if (lane == 0) red[warp * kCV + kMaxM] = v;
+}
+
+// x += alpha p (upd_x); p = r + beta p - W mu_W - ghat mu_g; residual store (upd_p)
+__device__ __noinline__ void cluster_combine_rows(double* __restrict__ Xv, double* __restrict__ Pv,
+                                                  const double* __restrict__ Rv, const double* __restrict__ Wg,
+                                                  int64_t ldw, const double* __restrict__ Gh, double* sto,
+                                                  int64_t rbeg, int64_t rend, bool upd_x, bool upd_p,
+                                                  double alpha, double beta, const double* smu, int nw, int hg,
+                                                  double rinv) {
+  const int tid = threadIdx.x;
+  double mu[16];
+#pragma unroll
+  for (int j = 0; j < 16; ++j) mu[j] = smu[j];
+  const double mug = hg ? smu[nw] : 0.0;
+#pragma unroll 2
+  for (int64_t i = rbeg + tid; i < rend; i += kAT) {
+    const double pv = Pv[i];
+    if (upd_x) Xv[i] = fma(alpha, pv, Xv[i]);
+    if (upd_p) {
+      const double rv = Rv[i];
+      double pn = fma(beta, pv, rv);
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < nw) pn = fma(-mu[j], __ldg(Wg + (int64_t)j * ldw + i), pn);
+      if (hg) pn = fma(-mug, __ldg(Gh + i), pn);
+      Pv[i] = pn;
+      if (sto) sto[i] = rv * rinv;
+    }
+  }
+}
+
+// taller tiles for the cluster loop: a 256-wide image (C2) is 16 tiles of 64 rows, one per
+// CTA of a 16-CTA cluster (the default 48-row tile gives 24 tiles = two rounds)
+__host__ __device__ constexpr int cluster_tile_rows(int r) { return r <= 6 ? 64 : (r <= 8 ? 56 : tc_tile_rows(r)); }
+
 template <int R, bool kTma>
 __global__ void __launch_bounds__(kAT, 1) cg_cluster_kernel(const __grid_constant__ ClusterParams P) {
   extern __shared__ __align__(128) double smem[];
-  using Core = ApplyCore<R, kTma>;
+  using Core = ApplyCore<R, kTma, cluster_tile_rows(R)>;
   cgx::cluster_group cl = cgx::this_cluster();
   const int crank = (int)cl.block_rank();
   const int csz = (int)cl.num_blocks();
@@ -151,35 +222,7 @@ __global__ void __launch_bounds__(kAT, 1) cg_cluster_kernel(const __grid_constan
       }
       mark(2);
       // ================= B: r update; partials of z = Z^T r and rho' = r.r
-      double acc[16], accg = 0.0, accr = 0.0;
-#pragma unroll
-      for (int j = 0; j < 16; ++j) acc[j] = 0.0;
-#pragma unroll 2
-      for (int64_t i = rbeg + tid; i < rend; i += kAT) {
-        const double wv = Wv[i];
-        const double rn = (mode == ST_ACTIVE) ? fma(-alpha, wv, Rv[i]) : __ldg(cg->b + i) - wv;
-        Rv[i] = rn;
-#pragma unroll
-        for (int j = 0; j < 16; ++j)
-          if (j < nw) acc[j] = fma(Zs[(int64_t)j * N + i], rn, acc[j]);
-        if (hg) accg = fma(__ldg(Zg + i), rn, accg);
-        accr = fma(rn, rn, accr);
-      }
-#pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        if (j < nw) {
-          const double v = warp_sum(acc[j]);
-          if (lane == 0) s_red[warp][j] = v;
-        }
-      }
-      if (hg) {
-        const double v = warp_sum(accg);
-        if (lane == 0) s_red[warp][nw] = v;
-      }
-      {
-        const double v = warp_sum(accr);
-        if (lane == 0) s_red[warp][kMaxM] = v;
-      }
+      cluster_update_rows(Rv, Wv, cg->b, Zs, Zg, N, rbeg, rend, mode == ST_ACTIVE, alpha, nw, hg, &s_red[0][0]);
       __syncthreads();
       mark(3);
       if (tid < kCV) {
@@ -259,27 +302,8 @@ __global__ void __launch_bounds__(kAT, 1) cg_cluster_kernel(const __grid_constan
         const int slot = s_slot;
         const double rinv = s_rinv;
         double* sto = (slot >= 0) ? cg->store + ((int64_t)s * cg->store_cap + slot) * cg->lds : nullptr;
-        double mu[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) mu[j] = s_mu[j];
-        const double mug = hg ? s_mu[nw] : 0.0;
-        if (upd_x || upd_p) {
-#pragma unroll 2
-          for (int64_t i = rbeg + tid; i < rend; i += kAT) {
-            const double pv = Pv[i];
-            if (upd_x) Xv[i] = fma(alpha, pv, Xv[i]);
-            if (upd_p) {
-              const double rv = Rv[i];
-              double pn = fma(beta, pv, rv);
-#pragma unroll
-              for (int j = 0; j < 16; ++j)
-                if (j < nw) pn = fma(-mu[j], __ldg(Wg + (int64_t)j * ldw + i), pn);
-              if (hg) pn = fma(-mug, __ldg(Gh + i), pn);
-              Pv[i] = pn;
-              if (sto) sto[i] = rv * rinv;
-            }
-          }
-        }
+        if (upd_x || upd_p)
+          cluster_combine_rows(Xv, Pv, Rv, Wg, ldw, Gh, sto, rbeg, rend, upd_x, upd_p, alpha, beta, s_mu, nw, hg, rinv);
       }
       asm volatile("fence.proxy.async.global;\n" ::: "memory");   // p / x stores -> next TMA reads
       mark(5);
@@ -305,12 +329,12 @@ __global__ void __launch_bounds__(kAT, 1) cg_cluster_kernel(const __grid_constan
 }
 
 // ------------------------------------------------------------------ host side
-bool fill_apply_params(Handle* h, const ApplyLaunch& a, ApplyParams& prm);
+bool fill_apply_params(Handle* h, const ApplyLaunch& a, ApplyParams& prm, int ty_override);
 
 template <int R>
 static cudaError_t launch_cluster_r(ClusterParams& prm, bool tma, int csize, int nclusters, int slots, cudaStream_t st,
                                     bool* ok) {
-  using C = TcCfg<R>;
+  using C = TcCfg<R, cluster_tile_rows(R)>;
   auto kfn = tma ? cg_cluster_kernel<R, true> : cg_cluster_kernel<R, false>;
   const size_t smem = C::SMEM;
   static int inited[2] = {0, 0};
@@ -395,7 +419,7 @@ cudaError_t launch_cg_cluster(Handle* h, CgDev* dev, const CgDev& hc, unsigned* 
   a.mode = RSK_APPLY_SHIFTED;
   a.src2_rconv = true;
   a.xdoty = reinterpret_cast<double*>(1);   // want_dot (accumulated through dot_acc)
-  const bool tma = fill_apply_params(h, a, prm.ap);
+  const bool tma = fill_apply_params(h, a, prm.ap, cluster_tile_rows(h->r));
   prm.ap.cg = nullptr;
   prm.cg = dev;
   prm.queue = queue;

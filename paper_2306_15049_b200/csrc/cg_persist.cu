@@ -504,7 +504,7 @@ __global__ void __launch_bounds__(kAT, kApplyCtasPerSm) cg_persist_kernel(const 
 }
 
 // ------------------------------------------------------------------ host side
-bool fill_apply_params(Handle* h, const ApplyLaunch& a, ApplyParams& prm);
+bool fill_apply_params(Handle* h, const ApplyLaunch& a, ApplyParams& prm, int ty_override);
 
 template <int R>
 static cudaError_t launch_persist_r(PersistParams& prm, bool tma, int sm_count, cudaStream_t st, bool* ok) {
@@ -581,7 +581,7 @@ cudaError_t launch_cg_persist(Handle* h, CgDev* dev, const CgDev& hc, double* pa
   a.cg = dev;
   a.cg_alpha = true;
   a.src2_rconv = true;
-  const bool tma = fill_apply_params(h, a, prm.ap);
+  const bool tma = fill_apply_params(h, a, prm.ap, 0);
   prm.cg = dev;
   prm.partP = partP;
   prm.bar = bar;
