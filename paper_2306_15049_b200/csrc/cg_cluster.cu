@@ -210,11 +210,13 @@ __global__ void __launch_bounds__(kAT, 1) cg_cluster_kernel(const __grid_constan
       mark(1);
       double alpha = 0.0;
       if (mode == ST_ACTIVE) {
-        if (tid == 0) {
-          double pi = 0.0;
-          for (int c = 0; c < csz; ++c) pi += *cl.map_shared_rank(&s_dot, c);
-          s_brk = !(pi > 0.0) || !isfinite(pi);
-          s_alpha = s_brk ? 0.0 : rho / pi;
+        if (warp == 0) {   // the 16 CTA partials through DSMEM, all in flight at once
+          const double v = (lane < csz) ? *cl.map_shared_rank(&s_dot, lane) : 0.0;
+          const double pi = warp_sum(v);
+          if (lane == 0) {
+            s_brk = !(pi > 0.0) || !isfinite(pi);
+            s_alpha = s_brk ? 0.0 : rho / pi;
+          }
         }
         __syncthreads();
         if (s_brk) { status = ST_BREAKDOWN; break; }
@@ -233,10 +235,14 @@ __global__ void __launch_bounds__(kAT, 1) cg_cluster_kernel(const __grid_constan
       }
       cl_sync();
       mark(1);
-      if (tid < kCV && (tid < m || tid == kMaxM)) {
-        double t = 0.0;
-        for (int c = 0; c < csz; ++c) t += *cl.map_shared_rank(&s_part[tid], c);
-        s_z[tid] = t;
+      for (int e = tid; e < 32 * 16; e += kAT) {   // slot j = e / 16 from rank c = e % 16
+        const int j = e >> 4, c = e & 15;
+        const int slot = (j < kCV) ? j : kMaxM;
+        const bool need = (j < m || j == kMaxM) && j < kCV;
+        double v = (need && c < csz) ? *cl.map_shared_rank(&s_part[slot], c) : 0.0;
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);   // within the 16-lane half
+        if (need && c == 0) s_z[j] = v;
       }
       __syncthreads();
       // ---- scalars and status (identical in every CTA)

@@ -45,8 +45,9 @@ if os.environ.get("RSK_APPLY_PROF"):
     a = (ctypes.c_double * 8)()
     lib.rsk_debug_apply_prof(a, 0)
     names = ["issue->wait", "TMA wait", "x-pass+sync", "y-pass+epilogue", "dot+ticket", "end sync"]
-    print("apply block %s per lockstep iteration (2 runs):" % os.environ["RSK_APPLY_PROF"],
-          ", ".join(f"{n} {a[i]/(2*its)/1e3:.2f} us" for i, n in enumerate(names)))
+    its2 = max(its, 300)
+    print("apply block %s per iteration (2 runs):" % os.environ["RSK_APPLY_PROF"],
+          ", ".join(f"{n} {a[i]/(2*its2)/1e3:.2f} us" for i, n in enumerate(names)))
 if os.environ.get("RSK_CLUSTER_PROF"):
     lib.rsk_debug_cluster_prof.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int]
     a = (ctypes.c_double * 8)()
