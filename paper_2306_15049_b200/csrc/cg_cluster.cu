@@ -57,8 +57,32 @@ __device__ __noinline__ void cluster_update_rows(double* __restrict__ Rv, const 
   double acc[16], accg = 0.0, accr = 0.0;
 #pragma unroll
   for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+  // pairs of rows through 16-byte loads (rows rbeg.. are even-aligned; an odd tail row
+  // takes the scalar path)
+  const int64_t npair = (rend - rbeg) >> 1;
 #pragma unroll 2
-  for (int64_t i = rbeg + tid; i < rend; i += kAT) {
+  for (int64_t q = tid; q < npair; q += kAT) {
+    const int64_t i = rbeg + 2 * q;
+    const double2 wv = *reinterpret_cast<const double2*>(Wv + i);
+    const double2 r0 = loop ? *reinterpret_cast<const double2*>(Rv + i) : __ldg(reinterpret_cast<const double2*>(b + i));
+    double2 rn;
+    rn.x = loop ? fma(-alpha, wv.x, r0.x) : r0.x - wv.x;
+    rn.y = loop ? fma(-alpha, wv.y, r0.y) : r0.y - wv.y;
+    *reinterpret_cast<double2*>(Rv + i) = rn;
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (j < nw) {
+        const double2 z = *reinterpret_cast<const double2*>(Zs + (int64_t)j * N + i);
+        acc[j] = fma(z.y, rn.y, fma(z.x, rn.x, acc[j]));
+      }
+    if (hg) {
+      const double2 z = __ldg(reinterpret_cast<const double2*>(Zg + i));
+      accg = fma(z.y, rn.y, fma(z.x, rn.x, accg));
+    }
+    accr = fma(rn.y, rn.y, fma(rn.x, rn.x, accr));
+  }
+  if (((rend - rbeg) & 1) && tid == 0) {
+    const int64_t i = rend - 1;
     const double wv = Wv[i];
     const double rn = loop ? fma(-alpha, wv, Rv[i]) : __ldg(b + i) - wv;
     Rv[i] = rn;
@@ -95,8 +119,7 @@ __device__ __noinline__ void cluster_combine_rows(double* __restrict__ Xv, doubl
 #pragma unroll
   for (int j = 0; j < 16; ++j) mu[j] = smu[j];
   const double mug = hg ? smu[nw] : 0.0;
-#pragma unroll 2
-  for (int64_t i = rbeg + tid; i < rend; i += kAT) {
+  auto row1 = [&](int64_t i) {
     const double pv = Pv[i];
     if (upd_x) Xv[i] = fma(alpha, pv, Xv[i]);
     if (upd_p) {
@@ -109,7 +132,36 @@ __device__ __noinline__ void cluster_combine_rows(double* __restrict__ Xv, doubl
       Pv[i] = pn;
       if (sto) sto[i] = rv * rinv;
     }
+  };
+  const int64_t npair = (rend - rbeg) >> 1;
+#pragma unroll 2
+  for (int64_t q = tid; q < npair; q += kAT) {
+    const int64_t i = rbeg + 2 * q;
+    const double2 pv = *reinterpret_cast<const double2*>(Pv + i);
+    if (upd_x) {
+      const double2 xv = *reinterpret_cast<const double2*>(Xv + i);
+      *reinterpret_cast<double2*>(Xv + i) = make_double2(fma(alpha, pv.x, xv.x), fma(alpha, pv.y, xv.y));
+    }
+    if (upd_p) {
+      const double2 rv = *reinterpret_cast<const double2*>(Rv + i);
+      double ax = fma(beta, pv.x, rv.x), ay = fma(beta, pv.y, rv.y);
+      double bx = 0.0, by = 0.0;   // two partial chains (even / odd j) halve the FMA latency chain
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (j < nw) {
+          const double2 w = __ldg(reinterpret_cast<const double2*>(Wg + (int64_t)j * ldw + i));
+          if (j & 1) { bx = fma(-mu[j], w.x, bx); by = fma(-mu[j], w.y, by); }
+          else { ax = fma(-mu[j], w.x, ax); ay = fma(-mu[j], w.y, ay); }
+        }
+      if (hg) {
+        const double2 g = __ldg(reinterpret_cast<const double2*>(Gh + i));
+        bx = fma(-mug, g.x, bx); by = fma(-mug, g.y, by);
+      }
+      *reinterpret_cast<double2*>(Pv + i) = make_double2(ax + bx, ay + by);
+      if (sto) *reinterpret_cast<double2*>(sto + i) = make_double2(rv.x * rinv, rv.y * rinv);
+    }
   }
+  if (((rend - rbeg) & 1) && tid == 0) row1(rend - 1);
 }
 
 // taller tiles for the cluster loop: a 256-wide image (C2) is 16 tiles of 64 rows, one per

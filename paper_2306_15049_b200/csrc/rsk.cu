@@ -711,7 +711,14 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
   // Small images (working set in L2): one thread-block cluster per shift, no lockstep
   // (cg_cluster.cu). The whole loop incl. confirmations runs in one launch.
   const bool cluster_mode = !prof && getenv("RSK_CG_LEGACY") == nullptr && getenv("RSK_CG_NOCLUSTER") == nullptr &&
-                            N <= cluster_max_n();
+                            N <= cluster_max_n() &&
+                            // 16-byte vector access to rows of every per-shift / group vector
+                            (N % 2 == 0) && (d->ldx % 2 == 0) && (!defl || d->ldw % 2 == 0) &&
+                            (!anyg || d->ldgh % 2 == 0) && (!store || d->lds % 2 == 0) &&
+                            ((reinterpret_cast<uintptr_t>(d->X) | reinterpret_cast<uintptr_t>(d->b) |
+                              reinterpret_cast<uintptr_t>(anyg ? d->Ghat : d->X) |
+                              reinterpret_cast<uintptr_t>(anyg ? d->ZGhat : d->X) |
+                              reinterpret_cast<uintptr_t>(store ? d->store : d->X)) & 15) == 0;
   // device-loop kernel time (CUDA events on the launching stream) for the roofline
   cudaEvent_t dl0 = nullptr, dl1 = nullptr;
   double dl_kind = 0.0;
