@@ -290,31 +290,6 @@ struct ApplyCore {
         for (int ks = 0; ks < C::KS; ++ks)
 #pragma unroll
           for (int c = 0; c < 4; ++c) dmma(d0[c], d1[c], a[2 * c + ks], bx[ks]);
-        if (p.edge_fix) {
-          const int cu = c0 + cl0;   // first global column of the unit
-          if (cu < R || cu + 32 > nx - R) {
-            const double* srow = S + (rb * 8 + g) * C::PX - (c0 - C::H);   // srow[m] = x(row, m)
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-#pragma unroll
-              for (int h2 = 0; h2 < 2; ++h2) {
-                const int col = cu + 8 * c + 2 * q + h2;
-                double corr = 0.0;
-                if (col < R) {
-                  const double* dl = smem + C::OFF_DC + col * R;
-#pragma unroll
-                  for (int m = 0; m < R; ++m) corr = fma(dl[m], srow[m], corr);
-                }
-                if (col >= nx - R && col < nx) {
-                  const double* dr = smem + C::OFF_DC + (R + col - (nx - R)) * R;
-#pragma unroll
-                  for (int m = 0; m < R; ++m) corr = fma(dr[m], srow[nx - R + m], corr);
-                }
-                if (h2 == 0) d0[c] -= corr; else d1[c] -= corr;
-              }
-            }
-          }
-        }
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           double2* tp = reinterpret_cast<double2*>(Tm + (rb * 8 + g) * C::PT + cl0 + 8 * c + 2 * q);
@@ -322,6 +297,32 @@ struct ApplyCore {
         }
       }
       __syncthreads();
+      // zero-boundary corrections of the x-pass on T (only tiles touching the left or right
+      // image edge): T[row][col] -= sum_m D(col, m) x(row, m) for the r columns nearest it
+      if (p.edge_fix && (c0 < R || c0 + kTX > nx - R)) {
+        for (int e = tid; e < C::HY * 2 * R; e += kAT) {
+          const int row = e / (2 * R), k = e - row * (2 * R);
+          const bool right = k >= R;
+          const int col = right ? nx - R + (k - R) : k;          // global column
+          const int lc = col - c0;
+          if (lc < 0 || lc >= kTX || col < 0 || col >= nx) continue;
+          if (right && col < R) continue;                          // tiny images: the left item does both
+          const double* srow = S + row * C::PX - (c0 - C::H);    // srow[m] = x(row, m)
+          double corr = 0.0;
+          if (!right) {
+            const double* dl = smem + C::OFF_DC + col * R;
+#pragma unroll
+            for (int m = 0; m < R; ++m) corr = fma(dl[m], srow[m], corr);
+          }
+          if (col >= nx - R) {
+            const double* dr = smem + C::OFF_DC + (R + col - (nx - R)) * R;
+#pragma unroll
+            for (int m = 0; m < R; ++m) corr = fma(dr[m], srow[nx - R + m], corr);
+          }
+          Tm[row * C::PT + lc] -= corr;
+        }
+        __syncthreads();
+      }
       amark(2);
 
       // ---- y-pass on the tensor cores + fused epilogue: warp = 8-column block, all RBY
