@@ -225,6 +225,8 @@ __global__ void __launch_bounds__(kAT, 1) cg_cluster_kernel(const __grid_constan
     double rho = cg->rho[s];
     int iters = cg->iters[s], nconf = cg->nconf[s], scnt = cg->store_cnt[s];
     double rho_true = cg->rho_true[s];
+    const int maxit = cg->maxit, store_cap = cg->store_cap;
+    const bool has_store = cg->store != nullptr;
     for (int e = tid; e < kMaxM * kMaxM; e += kAT) s_L[e] = cg->Lf[(int64_t)s * kMaxM * kMaxM + e];
     for (int j = tid; j < kMaxM; j += kAT) s_mu[j] = 0.0;
     if (tid == 0) { s_list[0] = s; }
@@ -297,8 +299,8 @@ __global__ void __launch_bounds__(kAT, 1) cg_cluster_kernel(const __grid_constan
         if (need && c == 0) s_z[j] = v;
       }
       __syncthreads();
-      // ---- scalars and status (identical in every CTA)
-      if (tid == 0) {
+      // ---- scalars and status (identical in every CTA; warp 0, lanes redundant)
+      if (warp == 0) {
         const double rho_new = s_z[kMaxM];
         const bool conv = sqrt(rho_new) <= thr;
         int nst = mode;
@@ -309,45 +311,38 @@ __global__ void __launch_bounds__(kAT, 1) cg_cluster_kernel(const __grid_constan
           beta = rho_new / rho;
           rho = rho_new;
           if (conv) nst = ST_RCONV;
-          else if (iters >= cg->maxit) nst = ST_MAXIT;
+          else if (iters >= maxit) nst = ST_MAXIT;
           else newp = true;
         } else {
           rho_true = rho_new;
           nconf += 1;
           if (conv) nst = ST_DONE;
-          else if (iters >= cg->maxit) nst = ST_MAXIT;
+          else if (iters >= maxit) nst = ST_MAXIT;
           else { nst = ST_ACTIVE; beta = 0.0; rho = rho_new; newp = true; }
         }
         int slot = -1;
         if (newp) {
-          double x[kMaxM];
-#pragma unroll
-          for (int i = 0; i < kMaxM; ++i) {
-            if (i < m) {
-              double t = s_z[i];
-#pragma unroll
-              for (int j = 0; j < i; ++j) t -= s_L[i + j * kMaxM] * x[j];
-              x[i] = t * s_dinv[i];
-            }
+          // mu = G^-1 z: L y = z then L^T mu = y, lane i holds component i
+          double x = (lane < m) ? s_z[lane] : 0.0;
+          for (int k = 0; k < m; ++k) {
+            if (lane == k) x *= s_dinv[k];
+            const double xk = __shfl_sync(0xffffffffu, x, k);
+            if (lane > k && lane < m) x = fma(-s_L[lane + k * kMaxM], xk, x);
           }
-#pragma unroll
-          for (int i = kMaxM - 1; i >= 0; --i) {
-            if (i < m) {
-              double t = x[i];
-#pragma unroll
-              for (int j = i + 1; j < kMaxM; ++j)
-                if (j < m) t -= s_L[j + i * kMaxM] * x[j];
-              x[i] = t * s_dinv[i];
-            }
+          for (int k = m - 1; k >= 0; --k) {
+            if (lane == k) x *= s_dinv[k];
+            const double xk = __shfl_sync(0xffffffffu, x, k);
+            if (lane < k) x = fma(-s_L[k + lane * kMaxM], xk, x);
           }
-#pragma unroll
-          for (int j = 0; j < kMaxM; ++j) s_mu[j] = j < m ? x[j] : 0.0;
-          if (cg->store && scnt < cg->store_cap) slot = scnt++;
+          if (lane < kMaxM) s_mu[lane] = (lane < m) ? x : 0.0;
+          if (has_store && scnt < store_cap) slot = scnt++;
         }
-        s_nst = nst;
-        s_beta = beta;
-        s_slot = slot;
-        s_rinv = (slot >= 0) ? 1.0 / sqrt(rho) : 0.0;
+        if (lane == 0) {
+          s_nst = nst;
+          s_beta = beta;
+          s_slot = slot;
+          s_rinv = (slot >= 0) ? 1.0 / sqrt(rho) : 0.0;
+        }
       }
       __syncthreads();
       const int nst = s_nst;
