@@ -94,7 +94,8 @@ struct TcCfg {
   static constexpr int OFF_T = kStages * SBUF;
   static constexpr int OFF_RED = OFF_T + TBUF;
   static constexpr int OFF_DC = OFF_RED + 16;         // 4 r x r boundary corrections
-  static constexpr int OFF_BAR = OFF_DC + al16(4 * R * R);   // kStages mbarriers (8 B each)
+  static constexpr int OFF_FR = OFF_DC + al16(4 * R * R);    // Toeplitz fragments [2][KS][32]
+  static constexpr int OFF_BAR = OFF_FR + al16(2 * KS * 32);  // kStages mbarriers (8 B each)
   static constexpr int DBL = OFF_BAR + kStages;
   static constexpr size_t SMEM = sizeof(double) * (size_t)DBL;
   static constexpr unsigned XBYTES = 8u * HY * PX;
@@ -149,6 +150,15 @@ struct ApplyCore {
 
   __device__ static void init_bars(double* smem, const ApplyParams& p) {
     // boundary corrections of B (tiny, read at every edge output)
+    // per-lane Toeplitz fragments, once per CTA: x-pass B[k][n] = cx[k - n], y-pass
+    // A[m][k] = cy[k - m] (k = 4 ks + q, n = m = g). Lane-indexed parameter reads diverge
+    // across the constant cache; the items read them back conflict-free from here.
+    for (int e = threadIdx.x; e < 2 * C::KS * 32; e += blockDim.x) {
+      const int which = e / (C::KS * 32), rem = e - which * C::KS * 32;
+      const int ks = rem >> 5, ln = rem & 31;
+      const int t = 4 * ks + (ln & 3) - (ln >> 2);
+      smem[C::OFF_FR + e] = (t >= 0 && t < C::T) ? (which ? p.cy[t] : p.cx[t]) : 0.0;
+    }
     for (int e = threadIdx.x; e < 4 * R * R; e += blockDim.x) {
       const int sl = e / (R * R), rem = e - sl * R * R, a = rem / R, b = rem - a * R;
       smem[C::OFF_DC + e] = p.dcorr ? p.dcorr[((size_t)sl * kMaxR + a) * kMaxR + b] : 0.0;
@@ -271,10 +281,7 @@ struct ApplyCore {
       // interior Toeplitz fragments: x-pass B[k][n] = cx[k - n] (from the parameter bank)
       double bx[C::KS];
 #pragma unroll
-      for (int ks = 0; ks < C::KS; ++ks) {
-        const int t = 4 * ks + q - g;
-        bx[ks] = (t >= 0 && t < C::T) ? p.cx[t] : 0.0;
-      }
+      for (int ks = 0; ks < C::KS; ++ks) bx[ks] = smem[C::OFF_FR + ks * 32 + lane];
 #pragma unroll 1
       for (int u = warp; u < 2 * C::RBX; u += kAT / 32) {
         const int rb = u >> 1, half = u & 1;
@@ -379,8 +386,7 @@ struct ApplyCore {
         for (int j = 0; j < C::RBY; ++j) { e0[j] = 0.0; e1[j] = 0.0; }
 #pragma unroll
         for (int ks = 0; ks < C::KS; ++ks) {
-          const int t = 4 * ks + q - g;   // y-pass A[m][k] = cy[k - m]
-          const double ay = (t >= 0 && t < C::T) ? p.cy[t] : 0.0;
+          const double ay = smem[C::OFF_FR + (C::KS + ks) * 32 + lane];   // y-pass A[m][k] = cy[k - m]
 #pragma unroll
           for (int j = 0; j < C::RBY; ++j) dmma(e0[j], e1[j], ay, bw[2 * j + ks]);
         }
