@@ -143,102 +143,141 @@ __device__ void build_list(const CgDev* cg, int ns, PList& L, int* tmp) {
   __syncthreads();
 }
 
+// Passes of up to 32 consecutive listed shifts of one group (the list is sorted by group).
+__device__ __forceinline__ int pass_end(const PList& L, int li0) {
+  const int g = L.grp[li0];
+  int li1 = li0;
+  while (li1 < L.n && li1 < li0 + 32 && L.grp[li1] == g) ++li1;
+  return li1;
+}
+
 // ---- phase B: r update and the per-chunk partial sums of rho' and z = Z^T r.
-// Thread <-> row; the loads of a batch of kBB shifts are issued before any is used.
-constexpr int kBB = 4;
+// The skinny products [AW; EW]^T R of a pass run on the FP64 tensor cores: a k-step is 4
+// rows; lane (g, q) updates r of (row q, shift 8 nb + g) -- exactly its B fragment -- and
+// loads the A fragment (column 8 mb + g, row q) of AW / EW, shared by the 4 N-blocks.
+// Each shift's column of D, its rho and zeta are summed in an order fixed by the chunk
+// geometry only (rows of a warp, then warps), independent of the other shifts in the pass.
+constexpr int kRW = 34;   // per (warp, shift) staging: za[16], ze[16], rho, zeta
 __device__ __noinline__ void phase_b(const PersistParams& P, const PList& L, double* smem, double* s_alpha,
                                      const double* s_gam) {
   CgDev* cg = P.cg;
   const int n = L.n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, q = lane & 3;
   const int64_t N = cg->N;
   for (int li = tid; li < n; li += kAT) s_alpha[li] = (L.mode[li] == ST_ACTIVE) ? cg->alpha[L.sid[li]] : 0.0;
   __syncthreads();
-  double* acc = smem;   // [kPW][kPT][kPV] (the apply stage buffers are free now)
+  double* red = smem;   // [kPW][32][kRW] (the apply stage buffers are free now)
+  const int64_t rpw = P.rows / kPW;   // rows per warp (multiple of 32)
   for (int c = blockIdx.x; c < P.nchunk; c += gridDim.x) {
     const int64_t cbeg = (int64_t)c * P.rows;
     const int64_t cend = min(N, cbeg + P.rows);
-    for (int t0 = 0; t0 < n; t0 += kPT) {
-      const int nt = min(kPT, n - t0);
-      for (int e = tid; e < kPW * kPT * kPV; e += kAT) acc[e] = 0.0;
-      __syncthreads();
-      for (int64_t r0 = cbeg; r0 < cend; r0 += kAT) {
-        const int64_t i = r0 + tid;
-        const bool valid = i < cend;
-        const double bi = valid ? __ldg(cg->b + i) : 0.0;
-        int curg = -1;
-        double aw[16], ew[16];
-#pragma unroll 1
-        for (int k0 = 0; k0 < nt; k0 += kBB) {
-          double rv[kBB], wv[kBB], zg[kBB];
+    const int64_t wbeg = cbeg + warp * rpw;
+    const int64_t wend = min(cend, wbeg + rpw);
+    for (int li0 = 0; li0 < n; ) {
+      const int li1 = pass_end(L, li0);
+      const int np = li1 - li0;
+      const int grp = L.grp[li0];
+      const int J = cg->grp.J[grp];
+      const double* AWg = cg->grp.AW[grp];
+      const double* EWg = cg->grp.EW[grp];
+      const int64_t ldw = cg->grp.ldw;
+      // this lane's shifts (one per N-block)
+      int sv[4], md[4], hgv[4];
+      double al[4];
+      bool ok[4];
 #pragma unroll
-          for (int u = 0; u < kBB; ++u) {
-            rv[u] = 0.0; wv[u] = 0.0; zg[u] = 0.0;
-            const int li = t0 + k0 + u;
-            if (k0 + u < nt && valid) {
-              const int s = L.sid[li];
-              wv[u] = cg->Wv[(int64_t)s * N + i];
-              if (L.mode[li] == ST_ACTIVE) rv[u] = cg->R[(int64_t)s * N + i];
-              if (L.hg[li]) zg[u] = __ldg(cg->ZGhat + (int64_t)s * cg->ldgh + i);
-            }
+      for (int nb = 0; nb < 4; ++nb) {
+        const int li = li0 + 8 * nb + g;
+        ok[nb] = li < li1;
+        sv[nb] = ok[nb] ? L.sid[li] : 0;
+        md[nb] = ok[nb] ? L.mode[li] : ST_ACTIVE;
+        hgv[nb] = ok[nb] ? L.hg[li] : 0;
+        al[nb] = ok[nb] ? s_alpha[li] : 0.0;
+      }
+      double dA[4][2][2], dE[4][2][2], rh[4], zt[4];
+#pragma unroll
+      for (int nb = 0; nb < 4; ++nb) {
+        rh[nb] = 0.0; zt[nb] = 0.0;
+#pragma unroll
+        for (int mb = 0; mb < 2; ++mb) { dA[nb][mb][0] = dA[nb][mb][1] = dE[nb][mb][0] = dE[nb][mb][1] = 0.0; }
+      }
+#pragma unroll 2
+      for (int64_t row0 = wbeg; row0 < wend; row0 += 4) {
+        const int64_t row = row0 + q;
+        const bool vr = row < wend;
+        double aA[2], aE[2];
+#pragma unroll
+        for (int mb = 0; mb < 2; ++mb) {
+          const int col = 8 * mb + g;
+          const bool va = vr && col < J;
+          aA[mb] = va ? __ldg(AWg + (int64_t)col * ldw + row) : 0.0;
+          aE[mb] = va ? __ldg(EWg + (int64_t)col * ldw + row) : 0.0;
+        }
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb) {
+          if (8 * nb >= np) break;                  // uniform across the warp
+          double rn = 0.0;
+          if (ok[nb] && vr) {
+            const int64_t o = (int64_t)sv[nb] * N + row;
+            const double wv = cg->Wv[o];
+            rn = (md[nb] == ST_ACTIVE) ? fma(-al[nb], wv, cg->R[o]) : __ldg(cg->b + row) - wv;
+            cg->R[o] = rn;
+            rh[nb] = fma(rn, rn, rh[nb]);
+            if (hgv[nb]) zt[nb] = fma(__ldg(cg->ZGhat + (int64_t)sv[nb] * cg->ldgh + row), rn, zt[nb]);
           }
+          dmma(dA[nb][0][0], dA[nb][0][1], aA[0], rn);
+          dmma(dE[nb][0][0], dE[nb][0][1], aE[0], rn);
+          if (J > 8) {
+            dmma(dA[nb][1][0], dA[nb][1][1], aA[1], rn);
+            dmma(dE[nb][1][0], dE[nb][1][1], aE[1], rn);
+          }
+        }
+      }
+      // stage: D[m = 8 mb + g][n = 2q, 2q+1] of N-block nb; rho / zeta summed over the q lanes
+      double* rw = red + (size_t)warp * 32 * kRW;
 #pragma unroll
-          for (int u = 0; u < kBB; ++u) {
-            const int k = k0 + u;
-            if (k >= nt) break;
-            const int li = t0 + k;
-            const int s = L.sid[li];
-            const int g = L.grp[li];
-            const int hg = L.hg[li];
-            const int nw = L.m[li] - hg;
-            if (g != curg) {
-              curg = g;
-              const int J = cg->grp.J[g];
-              const double* AWg = cg->grp.AW[g];
-              const double* EWg = cg->grp.EW[g];
-              const int64_t ldw = cg->grp.ldw;
+      for (int nb = 0; nb < 4; ++nb) {
+        if (8 * nb >= np) break;
+        double r1 = rh[nb], z1 = zt[nb];
+        r1 += __shfl_xor_sync(0xffffffffu, r1, 1);
+        r1 += __shfl_xor_sync(0xffffffffu, r1, 2);
+        z1 += __shfl_xor_sync(0xffffffffu, z1, 1);
+        z1 += __shfl_xor_sync(0xffffffffu, z1, 2);
+        if (q == 0) {
+          rw[(8 * nb + g) * kRW + 32] = r1;
+          rw[(8 * nb + g) * kRW + 33] = z1;
+        }
 #pragma unroll
-              for (int j = 0; j < 16; ++j) {
-                aw[j] = (j < J && valid) ? __ldg(AWg + (int64_t)j * ldw + i) : 0.0;
-                ew[j] = (j < J && valid) ? __ldg(EWg + (int64_t)j * ldw + i) : 0.0;
-              }
-            }
-            double rn = 0.0;
-            if (valid) {
-              rn = (L.mode[li] == ST_ACTIVE) ? fma(-s_alpha[li], wv[u], rv[u]) : bi - wv[u];
-              cg->R[(int64_t)s * N + i] = rn;
-            }
-            const double gm = s_gam[s];
-            double* ak = acc + ((size_t)warp * kPT + k) * kPV;
-            // z_j = sum (AW_j + gamma EW_j) r  (j < nw), z_nw = ZGhat . r, rho = r . r
+        for (int mb = 0; mb < 2; ++mb) {
+          const int m = 8 * mb + g;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-              if (j < nw) {
-                const double v = warp_sum(fma(gm, ew[j], aw[j]) * rn);
-                if (lane == 0) ak[j] += v;
-              }
-            }
-            if (hg) {
-              const double v = warp_sum(zg[u] * rn);
-              if (lane == 0) ak[nw] += v;
-            }
-            {
-              const double v = warp_sum(rn * rn);
-              if (lane == 0) ak[kMaxM] += v;
-            }
+          for (int h = 0; h < 2; ++h) {
+            const int sh = 8 * nb + 2 * q + h;
+            rw[sh * kRW + m] = dA[nb][mb][h];
+            rw[sh * kRW + 16 + m] = dE[nb][mb][h];
           }
         }
       }
       __syncthreads();
-      // cross-warp sums in fixed order -> partials of this chunk
-      for (int e = tid; e < nt * kPV; e += kAT) {
+      for (int e = tid; e < np * kPV; e += kAT) {
         const int k = e / kPV, j = e - k * kPV;
-        double t = 0.0;
+        const int li = li0 + k;
+        const int nw = L.m[li] - L.hg[li];
+        const bool isz = j < nw, isg = L.hg[li] && j == nw, isr = j == kMaxM;
+        if (!(isz || isg || isr)) continue;
+        double ta = 0.0, te = 0.0;
 #pragma unroll
-        for (int w = 0; w < kPW; ++w) t += acc[((size_t)w * kPT + k) * kPV + j];
-        P.partP[((size_t)L.sid[t0 + k] * kPV + j) * P.nchunk + c] = t;
+        for (int w = 0; w < kPW; ++w) {
+          const double* r = red + ((size_t)w * 32 + k) * kRW;
+          if (isz) { ta += r[j]; te += r[16 + j]; }
+          else ta += r[isr ? 32 : 33];
+        }
+        const double v = isz ? fma(s_gam[L.sid[li]], te, ta) : ta;
+        P.partP[((size_t)L.sid[li] * kPV + j) * P.nchunk + c] = v;
       }
       __syncthreads();
+      li0 = li1;
     }
   }
 }
@@ -343,86 +382,106 @@ __device__ __noinline__ void phase_b2(const PersistParams& P, const PList& L, do
   }
 }
 
-// ---- phase C: x += alpha p; p = r + beta p - W mu_W - ghat mu_g; residual store
+// ---- phase C: x += alpha p; p = r + beta p - W mu_W - ghat mu_g; residual store.
+// W mu of a pass on the tensor cores: an 8-row block x 8 shifts is D = W[8 x J] M[J x 8]
+// (A = W rows, B = the shifts' mu from shared memory); lane (g, q) then finishes the
+// elements (row g, shifts 2q, 2q+1) of each N-block.
 __device__ __noinline__ void phase_c(const PersistParams& P, const PList& L, double* smem, const double* s_alpha,
                                      int* s_new, double* s_beta, int* s_slot, double* s_rinv) {
   CgDev* cg = P.cg;
   const int n = L.n;
-  const int tid = threadIdx.x;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, q = lane & 3;
   const int64_t N = cg->N;
-    double* scoef = smem;          // [n][kMaxM]
-    for (int li = tid; li < n; li += kAT) {
-      const int s = L.sid[li];
-      const int st = cg->status[s];
-      s_new[li] = st;
-      s_beta[li] = cg->beta[s];
-      s_slot[li] = (st == ST_ACTIVE) ? cg->stslot[s] : -1;
-      s_rinv[li] = (st == ST_ACTIVE && s_slot[li] >= 0) ? 1.0 / sqrt(cg->rho[s]) : 0.0;
-    }
-    for (int e = tid; e < n * kMaxM; e += kAT) {
-      const int li = e / kMaxM, j = e - li * kMaxM;
-      scoef[e] = cg->coef[(int64_t)L.sid[li] * kMaxM + j];
-    }
-    __syncthreads();
-    for (int c = blockIdx.x; c < P.nchunk; c += gridDim.x) {
-      const int64_t cbeg = (int64_t)c * P.rows;
-      const int64_t cend = min(N, cbeg + P.rows);
-      for (int64_t r0 = cbeg; r0 < cend; r0 += kAT) {
-        const int64_t i = r0 + tid;
-        if (i >= cend) break;
-        int curg = -1;
-        double* wv = smem + (size_t)kPMaxShift * kMaxM + tid;   // this thread's W row, stride kAT
+  double* scoef = smem;          // [n][kMaxM]
+  for (int li = tid; li < n; li += kAT) {
+    const int s = L.sid[li];
+    const int st = cg->status[s];
+    s_new[li] = st;
+    s_beta[li] = cg->beta[s];
+    s_slot[li] = (st == ST_ACTIVE) ? cg->stslot[s] : -1;
+    s_rinv[li] = (st == ST_ACTIVE && s_slot[li] >= 0) ? 1.0 / sqrt(cg->rho[s]) : 0.0;
+  }
+  for (int e = tid; e < n * kMaxM; e += kAT) {
+    const int li = e / kMaxM, j = e - li * kMaxM;
+    scoef[e] = cg->coef[(int64_t)L.sid[li] * kMaxM + j];
+  }
+  __syncthreads();
+  const int64_t rpw = P.rows / kPW;
+  for (int c = blockIdx.x; c < P.nchunk; c += gridDim.x) {
+    const int64_t cbeg = (int64_t)c * P.rows;
+    const int64_t cend = min(N, cbeg + P.rows);
+    const int64_t wbeg = cbeg + warp * rpw;
+    const int64_t wend = min(cend, wbeg + rpw);
+    for (int li0 = 0; li0 < n; ) {
+      const int li1 = pass_end(L, li0);
+      const int np = li1 - li0;
+      const int grp = L.grp[li0];
+      const int J = cg->grp.J[grp];
+      const double* Wg = cg->grp.W[grp];
+      const int64_t ldw = cg->grp.ldw;
+      // B fragments: mu of shift 8 nb + g, component 4 kk + q (0 beyond its nw)
+      double bm[4][4];
+#pragma unroll
+      for (int nb = 0; nb < 4; ++nb) {
+        const int li = li0 + 8 * nb + g;
+        const int nw = (li < li1) ? L.m[li] - L.hg[li] : 0;
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk) {
+          const int j = 4 * kk + q;
+          bm[nb][kk] = (li < li1 && j < nw && s_new[li] == ST_ACTIVE) ? scoef[li * kMaxM + j] : 0.0;
+        }
+      }
+      const int nkk = (J + 3) >> 2;
 #pragma unroll 1
-        for (int k0 = 0; k0 < n; k0 += kBB) {
-          double pv[kBB], xv[kBB], rv[kBB], gv[kBB];
+      for (int64_t row0 = wbeg; row0 < wend; row0 += 8) {
+        const int64_t row = row0 + g;
+        const bool vr = row < wend;
+        double a[4];
 #pragma unroll
-          for (int u = 0; u < kBB; ++u) {
-            pv[u] = 0.0; xv[u] = 0.0; rv[u] = 0.0; gv[u] = 0.0;
-            const int li = k0 + u;
-            if (li >= n) break;
-            const int s = L.sid[li];
+        for (int kk = 0; kk < 4; ++kk) {
+          const int j = 4 * kk + q;
+          a[kk] = (vr && kk < nkk && j < J) ? __ldg(Wg + (int64_t)j * ldw + row) : 0.0;
+        }
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb) {
+          if (8 * nb >= np) break;
+          double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+          for (int kk = 0; kk < 4; ++kk)
+            if (kk < nkk) dmma(d0, d1, a[kk], bm[nb][kk]);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int li = li0 + 8 * nb + 2 * q + h;
+            if (li >= li1 || !vr) continue;
             const bool upd_x = (L.mode[li] == ST_ACTIVE) && (s_alpha[li] != 0.0);
             const bool upd_p = (s_new[li] == ST_ACTIVE);
-            if (upd_x || upd_p) pv[u] = cg->P[(int64_t)s * N + i];
-            if (upd_x) xv[u] = cg->X[(int64_t)s * cg->ldx + i];
-            if (upd_p) {
-              rv[u] = cg->R[(int64_t)s * N + i];
-              if (L.hg[li]) gv[u] = __ldg(cg->Ghat + (int64_t)s * cg->ldgh + i);
+            if (!upd_x && !upd_p) continue;
+            const int s = L.sid[li];
+            const int64_t o = (int64_t)s * N + row;
+            const double pv = cg->P[o];
+            if (upd_x) {
+              double* xp = cg->X + (int64_t)s * cg->ldx + row;
+              *xp = fma(s_alpha[li], pv, *xp);
             }
-          }
-#pragma unroll
-          for (int u = 0; u < kBB; ++u) {
-            const int li = k0 + u;
-            if (li >= n) break;
-            const int s = L.sid[li];
-            const bool upd_x = (L.mode[li] == ST_ACTIVE) && (s_alpha[li] != 0.0);
-            const bool upd_p = (s_new[li] == ST_ACTIVE);
-            if (upd_x) cg->X[(int64_t)s * cg->ldx + i] = fma(s_alpha[li], pv[u], xv[u]);
             if (upd_p) {
-              const int g = L.grp[li];
-              if (g != curg) {
-                curg = g;
-                const int J = cg->grp.J[g];
-                const double* Wg = cg->grp.W[g];
-                const int64_t ldw = cg->grp.ldw;
-#pragma unroll
-                for (int j = 0; j < 16; ++j) wv[j * kAT] = j < J ? __ldg(Wg + (int64_t)j * ldw + i) : 0.0;
+              const double rv = cg->R[o];
+              double pn = fma(s_beta[li], pv, rv) - (h ? d1 : d0);
+              const int hg = L.hg[li];
+              if (hg) {
+                const int nw = L.m[li] - hg;
+                pn = fma(-scoef[li * kMaxM + nw], __ldg(cg->Ghat + (int64_t)s * cg->ldgh + row), pn);
               }
-              const int hg = L.hg[li], nw = L.m[li] - hg;
-              const double* mu = scoef + li * kMaxM;
-              double pn = fma(s_beta[li], pv[u], rv[u]);
-#pragma unroll
-              for (int j = 0; j < 16; ++j)
-                if (j < nw) pn = fma(-mu[j], wv[j * kAT], pn);
-              if (hg) pn = fma(-mu[nw], gv[u], pn);
-              cg->P[(int64_t)s * N + i] = pn;
+              cg->P[o] = pn;
               if (s_slot[li] >= 0)
-                cg->store[((int64_t)s * cg->store_cap + s_slot[li]) * cg->lds + i] = rv[u] * s_rinv[li];
+                cg->store[((int64_t)s * cg->store_cap + s_slot[li]) * cg->lds + row] = rv * s_rinv[li];
             }
           }
         }
       }
+      li0 = li1;
     }
+  }
 }
 
 // ---- phase A: the fused apply over the (tile, shift) items of the active list
@@ -510,12 +569,12 @@ template <int R>
 static cudaError_t launch_persist_r(PersistParams& prm, bool tma, int sm_count, cudaStream_t st, bool* ok) {
   using C = TcCfg<R>;
   // phases B / B2 / C reuse the apply's stage and T buffers below the correction table
-  static_assert(C::OFF_DC >= kPW * kPT * kPV && C::OFF_DC >= kPMaxShift * kMaxM + 16 * kAT &&
+  static_assert(C::OFF_DC >= kPW * 32 * kRW && C::OFF_DC >= kPMaxShift * kMaxM + 16 * kAT &&
                     C::OFF_DC >= 32 + kMaxM * kMaxM,
                 "persistent-loop scratch overlaps the apply's boundary-correction table");
   auto kfn = tma ? cg_persist_kernel<R, true> : cg_persist_kernel<R, false>;
   size_t smem = C::SMEM;
-  const size_t accb = sizeof(double) * (size_t)kPW * kPT * kPV;
+  const size_t accb = sizeof(double) * (size_t)kPW * 32 * kRW;
   const size_t coefb = sizeof(double) * ((size_t)kPMaxShift * kMaxM + 16 * kAT);
   if (smem < accb) smem = accb;
   if (smem < coefb) smem = coefb;

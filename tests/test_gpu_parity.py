@@ -175,8 +175,16 @@ def _kappa_bound(cfg, iters):
     return 1e-8
 
 
+# the three implementations of the lockstep loop: cluster per shift (default at these
+# sizes), persistent cooperative grid, host-polled kernels
+LOOPS = {"cluster": {}, "persistent": {"RSK_CG_NOCLUSTER": "1"}, "hostpolled": {"RSK_CG_LEGACY": "1"}}
+
+
+@pytest.mark.parametrize("loop", list(LOOPS))
 @pytest.mark.parametrize("n", [40, 96])
-def test_cg_plain_batch_matches_oracle(torch_dev, n):
+def test_cg_plain_batch_matches_oracle(torch_dev, n, loop, monkeypatch):
+    for k, v in LOOPS[loop].items():
+        monkeypatch.setenv(k, v)
     torch, dev = torch_dev
     from paper_2306_15049_b200.pipeline import GpuSolver
     cfg = S.small_config(n=n, M=5, r=2, sigma=1.0, tol=1e-10)
@@ -201,7 +209,10 @@ def test_cg_plain_batch_matches_oracle(torch_dev, n):
         np.testing.assert_allclose(st, np.stack(o.store[:st.shape[0]]), atol=1e-9)
 
 
-def test_cg_deflated_with_guess_and_carried_column(torch_dev):
+@pytest.mark.parametrize("loop", list(LOOPS))
+def test_cg_deflated_with_guess_and_carried_column(torch_dev, loop, monkeypatch):
+    for k, v in LOOPS[loop].items():
+        monkeypatch.setenv(k, v)
     torch, dev = torch_dev
     from paper_2306_15049_b200.pipeline import GpuSolver
     cfg = S.small_config(n=64, M=4, r=3, sigma=1.3, tol=1e-10)
