@@ -433,6 +433,20 @@ __device__ __noinline__ void phase_c(const PersistParams& P, const PList& L, dou
         }
       }
       const int nkk = (J + 3) >> 2;
+      // per-element flags of this lane's 8 (N-block, h) pairs
+      int flg[4][2];
+#pragma unroll
+      for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int li = li0 + 8 * nb + 2 * q + h;
+          int f = 0;
+          if (li < li1) {
+            if ((L.mode[li] == ST_ACTIVE) && (s_alpha[li] != 0.0)) f |= 1;
+            if (s_new[li] == ST_ACTIVE) f |= 2;
+          }
+          flg[nb][h] = f;
+        }
 #pragma unroll 1
       for (int64_t row0 = wbeg; row0 < wend; row0 += 8) {
         const int64_t row = row0 + g;
@@ -443,38 +457,48 @@ __device__ __noinline__ void phase_c(const PersistParams& P, const PList& L, dou
           const int j = 4 * kk + q;
           a[kk] = (vr && kk < nkk && j < J) ? __ldg(Wg + (int64_t)j * ldw + row) : 0.0;
         }
+        // every element load of the row block first
+        double pv[4][2], rv[4][2], xv[4][2], gv[4][2];
+#pragma unroll
+        for (int nb = 0; nb < 4; ++nb)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            pv[nb][h] = rv[nb][h] = xv[nb][h] = gv[nb][h] = 0.0;
+            const int f = vr ? flg[nb][h] : 0;
+            if (f && 8 * nb < np) {
+              const int li = li0 + 8 * nb + 2 * q + h;
+              const int s = L.sid[li];
+              const int64_t o = (int64_t)s * N + row;
+              pv[nb][h] = cg->P[o];
+              if (f & 1) xv[nb][h] = cg->X[(int64_t)s * cg->ldx + row];
+              if (f & 2) {
+                rv[nb][h] = cg->R[o];
+                if (L.hg[li]) gv[nb][h] = __ldg(cg->Ghat + (int64_t)s * cg->ldgh + row);
+              }
+            }
+          }
 #pragma unroll
         for (int nb = 0; nb < 4; ++nb) {
           if (8 * nb >= np) break;
-          double d0 = 0.0, d1 = 0.0;
+          double d[2] = {0.0, 0.0};
 #pragma unroll
           for (int kk = 0; kk < 4; ++kk)
-            if (kk < nkk) dmma(d0, d1, a[kk], bm[nb][kk]);
+            if (kk < nkk) dmma(d[0], d[1], a[kk], bm[nb][kk]);
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
+            const int f = vr ? flg[nb][h] : 0;
+            if (!f) continue;
             const int li = li0 + 8 * nb + 2 * q + h;
-            if (li >= li1 || !vr) continue;
-            const bool upd_x = (L.mode[li] == ST_ACTIVE) && (s_alpha[li] != 0.0);
-            const bool upd_p = (s_new[li] == ST_ACTIVE);
-            if (!upd_x && !upd_p) continue;
             const int s = L.sid[li];
             const int64_t o = (int64_t)s * N + row;
-            const double pv = cg->P[o];
-            if (upd_x) {
-              double* xp = cg->X + (int64_t)s * cg->ldx + row;
-              *xp = fma(s_alpha[li], pv, *xp);
-            }
-            if (upd_p) {
-              const double rv = cg->R[o];
-              double pn = fma(s_beta[li], pv, rv) - (h ? d1 : d0);
+            if (f & 1) cg->X[(int64_t)s * cg->ldx + row] = fma(s_alpha[li], pv[nb][h], xv[nb][h]);
+            if (f & 2) {
+              double pn = fma(s_beta[li], pv[nb][h], rv[nb][h]) - d[h];
               const int hg = L.hg[li];
-              if (hg) {
-                const int nw = L.m[li] - hg;
-                pn = fma(-scoef[li * kMaxM + nw], __ldg(cg->Ghat + (int64_t)s * cg->ldgh + row), pn);
-              }
+              if (hg) pn = fma(-scoef[li * kMaxM + L.m[li] - hg], gv[nb][h], pn);
               cg->P[o] = pn;
               if (s_slot[li] >= 0)
-                cg->store[((int64_t)s * cg->store_cap + s_slot[li]) * cg->lds + row] = rv * s_rinv[li];
+                cg->store[((int64_t)s * cg->store_cap + s_slot[li]) * cg->lds + row] = rv[nb][h] * s_rinv[li];
             }
           }
         }
