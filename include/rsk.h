@@ -246,6 +246,13 @@ rsk_status rsk_lcurve_norms(rsk_handle h, int nvec, const double* X, int64_t ldx
                             void* stream);
 
 /* rsk_get_counters: cumulative apply counts (matvec accounting, §6). */
+/* eta2[s] = sum over image rows [row0, row1) of wx (Dx x_s)^2 + wy (Dy x_s)^2 under the
+ * handle's weights (the L-curve seminorm^2 of P:149 / P:161 restricted to a row range; Dy of
+ * the range's last row reads the next image row when there is one). Row slabs (§8(e2)) sum
+ * their owned rows and all-reduce. eta2: device [nvec]. */
+rsk_status rsk_seminorm_rows(rsk_handle h, int nvec, const double* X, int64_t ldx, int64_t row0, int64_t row1,
+                             double* eta2, void* stream);
+
 rsk_status rsk_get_counters(rsk_handle h, int64_t* applies_A_h, int64_t* applies_E_h,
                             int64_t* applies_C_h, int reset);
 

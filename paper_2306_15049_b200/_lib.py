@@ -91,6 +91,7 @@ _SIGS = {
                                   C.c_void_p]),
     "rsk_qr_tall": (C.c_int, [C.c_void_p, _i64, C.c_int, _dp, _i64, _dp, _i64, _hp, C.c_void_p]),
     "rsk_lcurve_norms": (C.c_int, [C.c_void_p, C.c_int, _dp, _i64, _dp, _dp, _dp, _dp, C.c_void_p]),
+    "rsk_seminorm_rows": (C.c_int, [C.c_void_p, C.c_int, _dp, _i64, _i64, _i64, _dp, C.c_void_p]),
     "rsk_get_counters": (C.c_int, [C.c_void_p, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64),
                                    C.c_int]),
     "rsk_orth_guess": (C.c_int, [C.c_int, _hp, _hp, _hp, _hp, _hp, C.c_double, C.c_int, _hp, _hp,

@@ -402,6 +402,16 @@ extern "C" rsk_status rsk_lcurve_norms(rsk_handle h, int nvec, const double* X, 
   return RSK_OK;
 }
 
+extern "C" rsk_status rsk_seminorm_rows(rsk_handle h, int nvec, const double* X, int64_t ldx, int64_t row0,
+                                        int64_t row1, double* eta2, void* stream) {
+  if (!h) return RSK_EINVAL;
+  const int64_t N = h->ny * h->nx;
+  RSK_ARG(nvec >= 1 && X && eta2 && ldx >= N && row0 >= 0 && row0 < row1 && row1 <= h->ny,
+          "rsk_seminorm_rows: bad arguments");
+  RSK_CUDA(launch_seminorm_rows(h, nvec, X, ldx, (int)row0, (int)row1, eta2, S(stream)));
+  return RSK_OK;
+}
+
 extern "C" rsk_status rsk_get_counters(rsk_handle h, int64_t* a, int64_t* e, int64_t* c, int reset) {
   if (!h) return RSK_EINVAL;
   if (a) *a = h->nA;

@@ -155,6 +155,8 @@ cudaError_t launch_irn(Handle* h, const double* x, double tau, double* wx, doubl
                        double* eta2, cudaStream_t st);
 cudaError_t launch_seminorm_batch(Handle* h, int nvec, const double* X, int64_t ldx,
                                   double* eta2, cudaStream_t st, int do_sqrt = 0);
+cudaError_t launch_seminorm_rows(Handle* h, int nvec, const double* X, int64_t ldx, int row0, int row1,
+                                 double* eta2, cudaStream_t st);
 cudaError_t launch_diffnorm_batch(Handle* h, int nvec, const double* Y, int64_t ldy,
                                   const double* d, double* out, cudaStream_t st);
 cudaError_t launch_scale_noise(int64_t n, const double* cx, const double* xi, const double* s2,

@@ -261,15 +261,18 @@ cudaError_t launch_irn(Handle* h, const double* x, double tau, double* wx, doubl
   return cudaGetLastError();
 }
 
+// sum over rows [row0, row1) of the image of wx (Dx x)^2 + wy (Dy x)^2 (Dy of the last
+// row of the range reads the next image row, when there is one)
 __global__ void __launch_bounds__(256) seminorm_part(int ny, int nx, const double* __restrict__ X,
                                                      int64_t ldx, const double* __restrict__ hwx,
                                                      const double* __restrict__ hwy,
-                                                     double* __restrict__ part, int nchunk) {
+                                                     double* __restrict__ part, int nchunk, int row0,
+                                                     int row1) {
   __shared__ double red[8];
   const int s = blockIdx.y;
   const double* x = X + (int64_t)s * ldx;
-  const int64_t N = (int64_t)ny * nx;
-  const int64_t base = (int64_t)blockIdx.x * kChunk;
+  const int64_t N = (int64_t)row1 * nx;
+  const int64_t base = (int64_t)row0 * nx + (int64_t)blockIdx.x * kChunk;
   double acc = 0.0;
   for (int e = 0; e < kChunk / 256; ++e) {
     const int64_t p = base + e * 256 + threadIdx.x;
@@ -289,8 +292,20 @@ cudaError_t launch_seminorm_batch(Handle* h, int nvec, const double* X, int64_t 
   const int nchunk = (int)((N + kChunk - 1) / kChunk);
   if (sizeof(double) * (size_t)nchunk * nvec > h->scratch_bytes) return cudaErrorMemoryAllocation;
   count_launch(); seminorm_part<<<dim3(nchunk, nvec), 256, 0, st>>>((int)h->ny, (int)h->nx, X, ldx, h->wx, h->wy,
-                                                    h->scratch, nchunk);
+                                                    h->scratch, nchunk, 0, (int)h->ny);
   count_launch(); reduce_partials<<<nvec, 32, 0, st>>>(h->scratch, nchunk, eta2, do_sqrt);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_seminorm_rows(Handle* h, int nvec, const double* X, int64_t ldx, int row0, int row1,
+                                 double* eta2, cudaStream_t st) {
+  const int64_t n = (int64_t)(row1 - row0) * h->nx;
+  const int nchunk = (int)((n + kChunk - 1) / kChunk);
+  if (nchunk < 1) return cudaErrorInvalidValue;
+  if (sizeof(double) * (size_t)nchunk * nvec > h->scratch_bytes) return cudaErrorMemoryAllocation;
+  count_launch(); seminorm_part<<<dim3(nchunk, nvec), 256, 0, st>>>((int)h->ny, (int)h->nx, X, ldx, h->wx, h->wy,
+                                                    h->scratch, nchunk, row0, row1);
+  count_launch(); reduce_partials<<<nvec, 32, 0, st>>>(h->scratch, nchunk, eta2, 0);
   return cudaGetLastError();
 }
 

@@ -151,6 +151,10 @@ class Handle:
         self._check(self.lib.rsk_lcurve_norms(self.h, _nv(X), _dptr(X), _ld(X), _dptr(d), _dptr(rho), _dptr(eta2),
                                               _dptr(scratch), _stream(stream)), "rsk_lcurve_norms")
 
+    def seminorm_rows(self, X, row0, row1, eta2, stream=None):
+        self._check(self.lib.rsk_seminorm_rows(self.h, _nv(X), _dptr(X), _ld(X), int(row0), int(row1), _dptr(eta2),
+                                               _stream(stream)), "rsk_seminorm_rows")
+
     def get_counters(self, reset=False):
         a, e, c = C.c_int64(), C.c_int64(), C.c_int64()
         self._check(self.lib.rsk_get_counters(self.h, C.byref(a), C.byref(e), C.byref(c), int(reset)),

@@ -261,6 +261,36 @@ class SlabOps:
         self.h.batch_axpby(np.ascontiguousarray(a, dtype=np.float64), Xo,
                            None if b is None else np.ascontiguousarray(b, dtype=np.float64), Yo)
 
+    def irn_weights(self, x: torch.Tensor, tau: float, adopt: bool = True):
+        """IRN weights of x (extended, halo refreshed here) for every stored row: owned rows
+        and halo rows get the global values (each needs x one row below, present in the
+        halo); only the last stored row of an interior slab is wrong (no row below) and no
+        owned output reads it. adopt: make them the handle's W_k."""
+        self.comm.halo(x[None] if x.dim() == 1 else x)
+        wx = torch.empty(self.ext_n, **self.f)
+        wy = torch.empty(self.ext_n, **self.f)
+        self.h.irn_weights(x, tau, wx, wy)
+        if adopt:
+            self.h.set_weights(wx, wy)
+        return wx, wy
+
+    def seminorm2(self, X: torch.Tensor) -> torch.Tensor:
+        """sum wx (Dx x)^2 + wy (Dy x)^2 over the whole image (L-curve eta^2) of each
+        extended vector: owned-row partials (halo refreshed for Dy), all-reduced."""
+        self.comm.halo(X)
+        out = torch.empty(X.shape[0], **self.f)
+        self.h.seminorm_rows(X, self.s.top, self.s.top + self.s.own_rows, out)
+        self.comm.allreduce(out)
+        return out
+
+    def resnorm2(self, X: torch.Tensor, d: torch.Tensor) -> torch.Tensor:
+        """||C x - d||^2 over the whole image (L-curve rho^2) of each extended vector."""
+        Y = torch.empty_like(X)
+        self.apply(X, Y, mode=L.RSK_APPLY_C_ONLY)
+        D = self.own(d).expand(X.shape[0], -1).contiguous()
+        self.axpby(np.full(X.shape[0], -1.0), D, np.ones(X.shape[0]), Y)
+        return self.dot(Y, Y)
+
     def add_uc(self, op, U, V, Cm):
         """V (+/-)= U Cm on the owned rows (U owned rows, V extended or owned)."""
         self.h.recycle_project(op, self.own(U), self.own(V), Cm)

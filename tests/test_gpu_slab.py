@@ -121,3 +121,50 @@ def test_slab_cg_matches_single_domain(torch_dev, nranks, J):
         rel = np.linalg.norm(Xs[l] - X1h[l]) / np.linalg.norm(X1h[l])
         assert rel <= 1e-8, (l, rel)
         assert res["relres_true"][l] <= cfg.tol * 1.0000001
+
+
+@pytest.mark.parametrize("n,r,nranks", [(64, 2, 2), (96, 3, 3)])
+def test_slab_irn_and_lcurve_norms_match_single_domain(torch_dev, n, r, nranks):
+    """IRN weights (halo of x*), the L-curve seminorm eta^2 and residual rho^2 in slab mode
+    against the single domain: weights bitwise on owned rows, norms <= 1e-13 relative."""
+    torch, dev = torch_dev
+    from paper_2306_15049_b200 import _lib as L
+    from paper_2306_15049_b200.rsk import Handle
+    from paper_2306_15049_b200.slab import SlabOps, SlabPlan, run_threads
+    psf = S.gaussian_psf(r, 1.0 + 0.3 * r)
+    x = torch.from_numpy(S.random_vectors(3 + n, (n * n,))).to(dev)
+    X = torch.from_numpy(S.random_vectors(4 + n, (2, n * n))).to(dev)
+    d = torch.from_numpy(S.random_vectors(5 + n, (n * n,))).to(dev)
+    tau = 1e-3
+    h = Handle(n, n, psf, 0)
+    wx = torch.empty(n * n, dtype=torch.float64, device=dev)
+    wy = torch.empty_like(wx)
+    h.irn_weights(x, tau, wx, wy)
+    h.set_weights(wx, wy)
+    eta = torch.empty(2, dtype=torch.float64, device=dev)
+    h.seminorm_rows(X, 0, n, eta)
+    Y = torch.empty_like(X)
+    h.apply_shifted(X, Y, mode=L.RSK_APPLY_C_ONLY)
+    rho2 = ((Y - d) ** 2).sum(1)
+    torch.cuda.synchronize()
+    plan = SlabPlan(n, n, r, nranks)
+
+    def rank_fn(k, comm):
+        so = SlabOps(plan, k, comm, psf, 0)
+        xe = torch.zeros(plan.slabs[k].ext_rows * n, dtype=torch.float64, device=dev)
+        so.own(xe).copy_(plan.owned(x, k))
+        swx, swy = so.irn_weights(xe, tau)
+        Xe = torch.zeros(2, plan.slabs[k].ext_rows * n, dtype=torch.float64, device=dev)
+        so.own(Xe).copy_(plan.owned(X, k))
+        de = plan.extend(d, k)
+        e2 = so.seminorm2(Xe)
+        r2 = so.resnorm2(Xe, de)
+        torch.cuda.synchronize()
+        return (so.own(swx).cpu().numpy(), so.own(swy).cpu().numpy(), e2.cpu().numpy(), r2.cpu().numpy())
+
+    outs = run_threads(plan, rank_fn)
+    for k, (a, b2, e2, r2) in enumerate(outs):
+        np.testing.assert_array_equal(a, plan.owned(wx, k).cpu().numpy())
+        np.testing.assert_array_equal(b2, plan.owned(wy, k).cpu().numpy())
+        np.testing.assert_allclose(e2, eta.cpu().numpy(), rtol=1e-13)
+        np.testing.assert_allclose(r2, rho2.cpu().numpy(), rtol=1e-13)
