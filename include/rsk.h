@@ -310,6 +310,12 @@ rsk_status rsk_chol_solve_small(int n, const double* G_h, int nrhs, const double
  * (reading G25): centred differences on the uniform log-lambda grid,
  * endpoints excluded, ties to the smallest index. Returns the 0-based index in
  * *lstar; kappa_h (nullable, [M]) receives the curvatures (-inf at the ends). */
+/* Host step of one shifted-Cholesky-QR pass (rsk_qr_tall runs three): from G = V^T V of
+ * the pass input (k x k column-major; n = global rows) returns T = R_pass^-1 (upper) with
+ * V T the pass output, and updates Racc <- R_pass Racc (pass 0: Racc = R_pass). Row slabs
+ * all-reduce G and apply T to their own rows. RSK_EPARTIAL if Cholesky fails. Host only. */
+rsk_status rsk_cholqr_pass(int k, int64_t n, int pass, const double* G_h, double* T_h, double* Racc_h);
+
 /* ---- deflated-CG host steps (row-slab loop; also used by the
  * single-domain setup). Loop states: */
 enum { RSK_LOOP_ACTIVE = 0, RSK_LOOP_RCONV = 1, RSK_LOOP_DONE = 2, RSK_LOOP_BREAKDOWN = 3, RSK_LOOP_MAXIT = 4 };

@@ -105,6 +105,7 @@ _SIGS = {
     "rsk_lcurve_corner": (C.c_int, [C.c_int, _hp, _hp, C.POINTER(C.c_int), _hp]),
     "rsk_local_gram_factors": (C.c_int, [C.c_int, C.c_int, _ip, _ip, _hp, _hp, _hp, _hp, _hp, _hp, _hp, _hp,
                                          _ip, _ip, _ip]),
+    "rsk_cholqr_pass": (C.c_int, [C.c_int, _i64, C.c_int, _hp, _hp, _hp]),
     "rsk_gram_solve": (C.c_int, [C.c_int, C.c_int, _hp, _ip, _ip, _hp, _hp, _hp, _hp, _hp]),
     "rsk_cg_alpha": (C.c_int, [C.c_int, _hp, _hp, _hp, _ip]),
     "rsk_cg_scalars": (C.c_int, [C.c_int, C.c_int, _ip, _hp, _hp, _hp, _hp, _hp, _ip, _ip, _hp, C.c_double,

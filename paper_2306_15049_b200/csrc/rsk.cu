@@ -314,75 +314,86 @@ extern "C" rsk_status rsk_batch_axpby(rsk_handle h, int64_t n, int nv, const dou
 // Shifted Cholesky QR3 (Fukaya, Kannan, Nakatsukasa, Yamamoto, Yanagisawa 2020):
 // backward-stable thin QR of an ill-conditioned tall-skinny block in three
 // Gram passes. V (n x k) is overwritten; Q (n x k) receives the orthonormal factor.
+// Host step of one shifted-Cholesky-QR pass (Fukaya et al. 2020) from the Gram matrix G =
+// V^T V of the pass's input (k x k, column-major): T = R_pass^-1 (upper, column-major) so
+// that V T is the pass's output, and Racc <- R_pass Racc. Pass 0 equilibrates with the Gram
+// diagonal and adds the shift 11 (n k + k (k+1)) u ||G||; later passes are unshifted unless
+// Cholesky needs it. Shared by rsk_qr_tall (one domain) and the row-slab QR (Gram
+// all-reduced over slabs).
+extern "C" rsk_status rsk_cholqr_pass(int k, int64_t n, int pass, const double* G_h, double* T_h, double* Racc_h) {
+  if (k < 1 || k > 256 || n < k || pass < 0 || !G_h || !T_h || !Racc_h) return RSK_EINVAL;
+  std::vector<double> G(G_h, G_h + (size_t)k * k), Rn((size_t)k * k);
+  std::vector<double> dsc(k, 1.0);
+  if (pass == 0)
+    for (int j = 0; j < k; ++j) dsc[j] = G[j + j * k] > 0 ? 1.0 / std::sqrt(G[j + j * k]) : 1.0;
+  std::vector<double> L((size_t)k * k);
+  double shift = 0.0;
+  for (int j = 0; j < k; ++j)
+    for (int i = 0; i < k; ++i) L[i + j * k] = 0.5 * (G[i + j * k] + G[j + i * k]) * dsc[i] * dsc[j];
+  double nrm2 = 0.0;
+  for (int j = 0; j < k; ++j) nrm2 += L[j + j * k];
+  if (pass == 0) shift = 11.0 * ((double)n * k + (double)k * (k + 1)) * 1.1102230246251565e-16 * nrm2;
+  std::vector<double> L0 = L;
+  int tries = 0;
+  for (;;) {
+    L = L0;
+    for (int j = 0; j < k; ++j) L[j + j * k] += shift;
+    if (rsk::chol_lower(k, L.data())) break;
+    shift = shift > 0 ? shift * 10.0 : 1e-15 * std::max(nrm2, 1e-300);
+    if (++tries > 40) return RSK_EPARTIAL;
+  }
+  // R_pass = L^T D^-1 ; T = (R_pass)^-1 = D L^-T (upper)
+  for (int j = 0; j < k; ++j)
+    for (int i = 0; i < k; ++i) Rn[i + j * k] = (i <= j) ? L[j + i * k] / dsc[j] : 0.0;
+  for (size_t e = 0; e < (size_t)k * k; ++e) T_h[e] = 0.0;
+  for (int j = 0; j < k; ++j) {
+    T_h[j + j * k] = 1.0 / Rn[j + j * k];
+    for (int i = j - 1; i >= 0; --i) {
+      double t = 0.0;
+      for (int q = i + 1; q <= j; ++q) t += Rn[i + q * k] * T_h[q + j * k];
+      T_h[i + j * k] = -t / Rn[i + i * k];
+    }
+  }
+  if (pass == 0) {
+    for (size_t e = 0; e < (size_t)k * k; ++e) Racc_h[e] = Rn[e];
+  } else {
+    std::vector<double> tmp((size_t)k * k, 0.0);
+    for (int j = 0; j < k; ++j)
+      for (int i = 0; i <= j; ++i) {
+        double t = 0.0;
+        for (int q = i; q <= j; ++q) t += Rn[i + q * k] * Racc_h[q + j * k];
+        tmp[i + j * k] = t;
+      }
+    for (size_t e = 0; e < (size_t)k * k; ++e) Racc_h[e] = tmp[e];
+  }
+  return RSK_OK;
+}
+
 extern "C" rsk_status rsk_qr_tall(rsk_handle h, int64_t n, int k, double* V, int64_t ldv, double* Q,
                                   int64_t ldq, double* R_h, void* stream) {
   if (!h) return RSK_EINVAL;
   RSK_ARG(n >= 1 && k >= 1 && k <= 256 && n >= k && V && Q && R_h && ldv >= n && ldq >= n,
           "rsk_qr_tall: bad arguments");
   cudaStream_t st = S(stream);
-  std::vector<double> G((size_t)k * k), T((size_t)k * k), Racc((size_t)k * k, 0.0), Rn((size_t)k * k);
+  std::vector<double> G((size_t)k * k), T((size_t)k * k), Racc((size_t)k * k, 0.0);
   double* dG = h->aux;
   double* dT = h->aux + 256 * 256;
-  // D scaling from the Gram diagonal
-  for (int pass = 0; pass < 3; ++pass) {
+  for (int pass = 0; pass < 3; ++pass) {   // passes write Q, V, Q
     double* src = (pass % 2 == 0) ? V : Q;
     const int64_t lds = (pass % 2 == 0) ? ldv : ldq;
     double* dst = (pass % 2 == 0) ? Q : V;
     const int64_t ldd = (pass % 2 == 0) ? ldq : ldv;
-    // the Gram partials live at the head of scratch; keep dG in the tail
     RSK_CUDA(launch_gemm_tn(h, n, k, src, lds, k, src, lds, dG, k, st));
     RSK_CUDA(cudaMemcpyAsync(G.data(), dG, sizeof(double) * k * k, cudaMemcpyDeviceToHost, st));
     RSK_CUDA(cudaStreamSynchronize(st));
-    std::vector<double> dsc(k, 1.0);
-    if (pass == 0)
-      for (int j = 0; j < k; ++j) dsc[j] = G[j + j * k] > 0 ? 1.0 / std::sqrt(G[j + j * k]) : 1.0;
-    std::vector<double> L((size_t)k * k);
-    double shift = 0.0;
-    for (int j = 0; j < k; ++j)
-      for (int i = 0; i < k; ++i) L[i + j * k] = 0.5 * (G[i + j * k] + G[j + i * k]) * dsc[i] * dsc[j];
-    double nrm2 = 0.0;
-    for (int j = 0; j < k; ++j) nrm2 += L[j + j * k];
-    if (pass == 0) shift = 11.0 * ((double)n * k + (double)k * (k + 1)) * 1.1102230246251565e-16 * nrm2;
-    std::vector<double> L0 = L;
-    int tries = 0;
-    for (;;) {
-      L = L0;
-      for (int j = 0; j < k; ++j) L[j + j * k] += shift;
-      if (chol_lower(k, L.data())) break;
-      shift = shift > 0 ? shift * 10.0 : 1e-15 * std::max(nrm2, 1e-300);
-      if (++tries > 40) { h->err = "rsk_qr_tall: Cholesky failed"; return RSK_EPARTIAL; }
-    }
-    // R_pass = L^T D^-1 ; T = (R_pass)^-1 = D L^-T (upper)
-    for (int j = 0; j < k; ++j)
-      for (int i = 0; i < k; ++i) Rn[i + j * k] = (i <= j) ? L[j + i * k] / dsc[j] : 0.0;
-    // invert the upper triangular Rn -> T
-    std::fill(T.begin(), T.end(), 0.0);
-    for (int j = 0; j < k; ++j) {
-      T[j + j * k] = 1.0 / Rn[j + j * k];
-      for (int i = j - 1; i >= 0; --i) {
-        double t = 0.0;
-        for (int q = i + 1; q <= j; ++q) t += Rn[i + q * k] * T[q + j * k];
-        T[i + j * k] = -t / Rn[i + i * k];
-      }
-    }
-    // Racc <- Rn * Racc
-    if (pass == 0) {
-      Racc = Rn;
-    } else {
-      std::vector<double> tmp((size_t)k * k, 0.0);
-      for (int j = 0; j < k; ++j)
-        for (int i = 0; i <= j; ++i) {
-          double t = 0.0;
-          for (int q = i; q <= j; ++q) t += Rn[i + q * k] * Racc[q + j * k];
-          tmp[i + j * k] = t;
-        }
-      Racc = tmp;
+    if (rsk_cholqr_pass(k, n, pass, G.data(), T.data(), Racc.data()) != RSK_OK) {
+      h->err = "rsk_qr_tall: Cholesky failed";
+      return RSK_EPARTIAL;
     }
     RSK_CUDA(cudaMemcpyAsync(dT, T.data(), sizeof(double) * k * k, cudaMemcpyHostToDevice, st));
     RSK_CUDA(cudaMemset2DAsync(dst, sizeof(double) * ldd, 0, sizeof(double) * n, k, st));
     RSK_CUDA(launch_gemm_nn(h, n, k, src, lds, k, dst, ldd, dT, k, 1.0, st));
   }
-  // after 3 passes the result is in Q (passes write Q, V, Q)
   for (int j = 0; j < k; ++j)
     for (int i = 0; i < k; ++i) R_h[i + j * k] = Racc[i + j * k];
   RSK_CUDA(cudaStreamSynchronize(st));

@@ -247,6 +247,10 @@ class SlabOps:
 
     def utv(self, U, V) -> torch.Tensor:
         """U^T V over the whole image: U (k, ext or own), V (nv, ...) -> (nv, k)."""
+        if V.dim() == 1:
+            V = V[None]
+        if U.dim() == 1:
+            U = U[None]
         k, nv = U.shape[0], V.shape[0]
         Cm = torch.empty(nv, k, **self.f)
         Uo, Vo = self.own(U), self.own(V)
@@ -302,75 +306,149 @@ def _h(t: torch.Tensor) -> np.ndarray:
 
 
 def slab_cg(ops: SlabOps, gamma: np.ndarray, b: torch.Tensor, X: torch.Tensor,
-            W=None, AW=None, EW=None, tol: float = 1e-8, maxit: int = 20000):
-    """Deflated CG (O4) for nshift shifted systems on the rank's slab.
-    b: (ext_n,) right-hand side (owned rows used); X: (nshift, ext_n) in x_p, out x.
-    W, AW, EW: (J, own_n) owned rows of the deflation block (or None: plain CG).
-    Returns dict(iters, applies, relres_true, status) (host arrays, identical on all ranks)."""
+            W=None, AW=None, EW=None, tol: float = 1e-8, maxit: int = 20000, *, has_xp=None,
+            groups=None, ghat=None, store=None, store_cap: int = 100, Gout=None):
+    """Deflated CG (O4) for nshift shifted systems on the rank's slab, the slab counterpart of
+    rsk_cg_recycled_batch (same recurrences, sums all-reduced).
+    b: (ext_n,) right-hand side; X: (nshift, ext_n) in x_p (has_xp) / out x.
+    Deflation: groups = dict(W, AW, EW: lists of (J_g, n) blocks, of_shift) -- or one block
+    W, AW, EW -- plus optional carried columns ghat = (Gh, ZGh, has_g) ((nshift, n) each).
+    store: (nshift * store_cap, n) residual store (seed solves); Gout: g = x - x_p.
+    Blocks may be owned-row (n = own_n) or extended tensors. Returns the host arrays of
+    rsk_cg_out (identical on all ranks)."""
     lib = ops.lib
     f = ops.f
     S = len(gamma)
+    KM = L.RSK_MAX_LOCAL
     gam = np.ascontiguousarray(gamma, dtype=np.float64)
     gam_d = torch.from_numpy(gam).to(ops.dev)
-    J = 0 if W is None else W.shape[0]
-    KM = L.RSK_MAX_LOCAL
+    if groups is None and W is not None:
+        groups = dict(W=[W], AW=[AW], EW=[EW], of_shift=np.zeros(S, np.int32))
+    G = 0 if groups is None else len(groups["W"])
+    gos = np.zeros(S, np.int32) if G == 0 else np.ascontiguousarray(groups["of_shift"], dtype=np.int32)
+    Js = [0] * max(G, 1) if G == 0 else [int(w.shape[0]) for w in groups["W"]]
+    Jm = max(Js) if G else 0
+    Gh = ZGh = None
+    has_g = np.zeros(S, np.int32)
+    if G and ghat is not None:
+        Gh, ZGh, hg0 = ghat
+        has_g = np.ascontiguousarray(hg0, dtype=np.int32).copy()
+    hx = np.ones(S, np.int32) if has_xp is None else np.ascontiguousarray(has_xp, dtype=np.int32)
     ones, zeros = np.ones(S), np.zeros(S)
+    for s_ in range(S):
+        if not hx[s_]:
+            ops.own(X[s_:s_ + 1]).zero_()
+    X0 = ops.own(X).clone() if Gout is not None else None
     Bv = torch.empty(S, ops.own_n, **f)
     Bv.copy_(ops.own(b).expand(S, -1))
     nb = float(np.sqrt(_h(ops.dot(b[None], b[None]))[0]))
+    out = dict(iters=np.zeros(S, np.int32), applies=np.zeros(S, np.int64), relres=np.zeros(S),
+               status=np.zeros(S, np.int32), m_used=np.zeros(S, np.int32), store_count=np.zeros(S, np.int32),
+               prof=np.zeros(8))
     if nb == 0.0:
-        X.zero_()
-        return dict(iters=np.zeros(S, np.int32), applies=np.zeros(S, np.int64), relres_true=np.zeros(S),
-                    status=np.full(S, LOOP_DONE, np.int32))
+        ops.own(X).zero_()
+        if Gout is not None:
+            ops.own(Gout).zero_()
+        out["status"][:] = L.RSK_CG_ZERO_RHS
+        return out
     thr = tol * nb
-    # ---- local Gram factors G_s = W^T (A + gamma_s E) W
+    # ---- local Gram factors (rsk_local_gram_factors) from all-reduced pieces
     Lf = np.zeros(S * KM * KM)
     m = np.zeros(S, np.int32)
-    hasg = np.zeros(S, np.int32)
+    hasg = has_g.copy()
     dropped = np.zeros(S, np.int32)
-    if J:
-        WA = np.zeros(256); WE = np.zeros(256)
-        WA[:J * J] = _h(ops.utv(W, AW)).ravel()      # (J x J): row a = AW_a^T W -> column-major W^T AW
-        WE[:J * J] = _h(ops.utv(W, EW)).ravel()
-        Jh = np.array([J], np.int32)
-        gos = np.zeros(S, np.int32)
-        st = lib.rsk_local_gram_factors(S, 1, _iptr(Jh), _iptr(gos), _ptr(gam), _ptr(WA), _ptr(WE), None, None,
-                                        None, None, _ptr(Lf), _iptr(m), _iptr(hasg), _iptr(dropped))
+    if G:
+        WA = np.zeros(G * 256); WE = np.zeros(G * 256)
+        WZg = np.zeros(G * 16 * S); AWg = np.zeros(G * 16 * S); EWg = np.zeros(G * 16 * S)
+        gzg = np.zeros(S)
+        for g in range(G):
+            J = Js[g]
+            if J == 0:
+                continue
+            Wg, AWg_, EWg_ = groups["W"][g], groups["AW"][g], groups["EW"][g]
+            WA[g * 256:g * 256 + J * J] = _h(ops.utv(Wg, AWg_)).ravel()
+            WE[g * 256:g * 256 + J * J] = _h(ops.utv(Wg, EWg_)).ravel()
+            if Gh is not None:
+                WZg[g * 16 * S:g * 16 * S + J * S] = _h(ops.utv(Wg, ZGh)).ravel()
+                AWg[g * 16 * S:g * 16 * S + J * S] = _h(ops.utv(AWg_, Gh)).ravel()
+                EWg[g * 16 * S:g * 16 * S + J * S] = _h(ops.utv(EWg_, Gh)).ravel()
+        if Gh is not None:
+            gzg = _h(ops.dot(Gh, ZGh))
+        Jh = np.ascontiguousarray(Js, dtype=np.int32)
+        st = lib.rsk_local_gram_factors(S, G, _iptr(Jh), _iptr(gos), _ptr(gam), _ptr(WA), _ptr(WE), _ptr(WZg),
+                                        _ptr(AWg), _ptr(EWg), _ptr(gzg), _ptr(Lf), _iptr(m), _iptr(hasg),
+                                        _iptr(dropped))
         if st != L.RSK_OK:
             raise RskError(f"rsk_local_gram_factors failed ({st})")
 
-    def gram_solve(zA, zE):
+    def zcols(Ua, Ue, R_):
+        """per shift, its group's (Ua)^T r and (Ue)^T r (Jm x S column-major; Ue may be None)"""
+        za = np.zeros(Jm * S); ze = np.zeros(Jm * S) if Ue is not None else None
+        for g in range(G):
+            J = Js[g]
+            if J == 0:
+                continue
+            ca = _h(ops.utv(Ua[g], R_))                 # (S, J)
+            ce = _h(ops.utv(Ue[g], R_)) if Ue is not None else None
+            for s_ in np.nonzero(gos == g)[0]:
+                za[s_ * Jm:s_ * Jm + J] = ca[s_]
+                if ce is not None:
+                    ze[s_ * Jm:s_ * Jm + J] = ce[s_]
+        return za, ze
+
+    def gram_solve(za, ze, zg):
         mu = np.zeros(S * KM)
-        st2 = lib.rsk_gram_solve(S, J, _ptr(Lf), _iptr(m), _iptr(hasg), _ptr(gam), _ptr(zA),
-                                 None if zE is None else _ptr(zE), None, _ptr(mu))
+        st2 = lib.rsk_gram_solve(S, Jm, _ptr(Lf), _iptr(m), _iptr(hasg), _ptr(gam), _ptr(za),
+                                 None if ze is None else _ptr(ze), None if zg is None else _ptr(zg), _ptr(mu))
         if st2 != L.RSK_OK:
             raise RskError(f"rsk_gram_solve failed ({st2})")
         return mu.reshape(S, KM)
 
-    def zcols(R):
-        """(AW)^T r and (EW)^T r, J x S column-major (ld J)."""
-        return (np.ascontiguousarray(_h(ops.utv(AW, R)).ravel()),
-                np.ascontiguousarray(_h(ops.utv(EW, R)).ravel()))
+    def sub_u(mu, V, which, sign=-1.0):
+        """V -= U mu (U = W / AW / EW of each shift's group) over the shifts' own columns"""
+        op = L.RSK_SUB_UC if sign < 0 else L.RSK_ADD_UC
+        for g in range(G):
+            J = Js[g]
+            if J == 0:
+                continue
+            nwv = m - hasg
+            C = np.zeros((S, J))
+            for s_ in np.nonzero(gos == g)[0]:
+                k = min(J, int(nwv[s_]))
+                C[s_, :k] = mu[s_, :k]
+            if not C.any():
+                continue
+            ops.add_uc(op, groups[which][g], V, torch.from_numpy(np.ascontiguousarray(C)).to(ops.dev))
+
+    def mu_g(mu):
+        """coefficient of the carried column (0 where absent)"""
+        nwv = m - hasg
+        return np.array([mu[s_, nwv[s_]] if hasg[s_] else 0.0 for s_ in range(S)])
 
     R = torch.empty(S, ops.own_n, **f)
     P = torch.zeros(S, ops.ext_n, **f)
     Wv = torch.empty(S, ops.ext_n, **f)
     applies = np.zeros(S, np.int64)
-    # ---- r_p = b - A_gamma x_p (one fresh apply, G15)
+    scnt = np.zeros(S, np.int32)
+    # ---- r_p = b - A_gamma x_p (one fresh apply for the shifts with x_p, G15)
     ops.apply(X, Wv, gam_d)
-    applies += 1
+    applies += hx
     R.copy_(Bv)
-    ops.axpby(-ones, Wv, ones, R)
-    # ---- Galerkin start on Range(W): c = G^-1 W^T r_p; x += W c; r -= (AW + gamma EW) c
-    if J:
-        zW = np.ascontiguousarray(_h(ops.utv(W, R)).ravel())
-        c = gram_solve(zW, None)
-        Cm = torch.from_numpy(np.ascontiguousarray(c[:, :J])).to(ops.dev)
-        ops.add_uc(L.RSK_ADD_UC, W, X, Cm)
-        ops.add_uc(L.RSK_SUB_UC, AW, R, Cm)
+    ops.axpby(-hx.astype(np.float64), Wv, ones, R)
+    # ---- Galerkin start on Range(U): c = G^-1 U^T r_p; x += U c; r -= Z c
+    if G:
+        za, _ = zcols(groups["W"], None, R)
+        zg = _h(ops.dot(Gh, R)) if Gh is not None else None
+        c = gram_solve(za, None, zg)
+        sub_u(c, X, "W", +1.0)
+        sub_u(c, R, "AW", -1.0)
         T = torch.zeros(S, ops.own_n, **f)
-        ops.add_uc(L.RSK_ADD_UC, EW, T, Cm)
+        sub_u(c, T, "EW", +1.0)
         ops.axpby(-gam, T, ones, R)
+        if Gh is not None:
+            cg_ = mu_g(c)
+            ops.axpby(cg_, Gh, ones, X)
+            ops.axpby(-cg_, ZGh, ones, R)
     rho = _h(ops.dot(R, R))
     state = np.where(np.sqrt(rho) <= thr, LOOP_RCONV, LOOP_ACTIVE).astype(np.int32)
     iters = np.zeros(S, np.int32)
@@ -379,18 +457,31 @@ def slab_cg(ops: SlabOps, gamma: np.ndarray, b: torch.Tensor, X: torch.Tensor,
     beta = np.zeros(S)
     alpha = np.zeros(S)
 
-    def new_p(mask, mu):
-        """p = r + beta p - W mu_W for the masked shifts."""
+    def new_p(mask, mu, rho_now):
+        """p = r + beta p - W mu_W - ghat mu_g for the masked shifts; residual store"""
         a = np.where(mask, 1.0, 0.0)
         bb = np.where(mask, beta, 1.0)
         ops.axpby(a, R, bb, P)
-        if J:
-            Cm2 = torch.from_numpy(np.ascontiguousarray(np.where(mask[:, None], mu[:, :J], 0.0))).to(ops.dev)
-            ops.add_uc(L.RSK_SUB_UC, W, P, Cm2)
+        if G:
+            sub_u(np.where(mask[:, None], mu, 0.0), P, "W", -1.0)
+            if Gh is not None:
+                ops.axpby(-np.where(mask, mu_g(mu), 0.0), Gh, ones, P)
+        if store is not None:
+            for s_ in np.nonzero(mask)[0]:
+                if scnt[s_] < store_cap:
+                    row = int(s_) * store_cap + int(scnt[s_])
+                    dst = store[row:row + 1]
+                    sc = np.zeros(1)
+                    ops.axpby(np.array([1.0 / np.sqrt(rho_now[s_])]), R[s_:s_ + 1], sc, dst)
+                    scnt[s_] += 1
 
-    # p_0 = r_0 - W mu_0
-    mu0 = gram_solve(*zcols(R)) if J else np.zeros((S, KM))
-    new_p(state == LOOP_ACTIVE, mu0)
+    # p_0 = r_0 - U mu_0 with mu_0 = G^-1 Z^T r_0
+    if G:
+        za, ze = zcols(groups["AW"], groups["EW"], R)
+        mu0 = gram_solve(za, ze, _h(ops.dot(ZGh, R)) if Gh is not None else None)
+    else:
+        mu0 = np.zeros((S, KM))
+    new_p(state == LOOP_ACTIVE, mu0, rho)
     guard = 0
     while np.any((state == LOOP_ACTIVE) | (state == LOOP_RCONV)):
         guard += 1
@@ -417,14 +508,19 @@ def slab_cg(ops: SlabOps, gamma: np.ndarray, b: torch.Tensor, X: torch.Tensor,
             ops.axpby(np.where(conf, 1.0, 0.0), Bv, ones, R)
             applies += conf
         rho_new = _h(ops.dot(R, R))
-        zA, zE = zcols(R) if J else (np.zeros(1), np.zeros(1))
+        if G:
+            za, ze = zcols(groups["AW"], groups["EW"], R)
+            zg = _h(ops.dot(ZGh, R)) if Gh is not None else None
+        else:
+            za, ze, zg = np.zeros(1), np.zeros(1), None
         mu = np.zeros(S * KM)
-        st = lib.rsk_cg_scalars(S, J, _iptr(mode), _ptr(gam), _ptr(rho_new), _ptr(zA), _ptr(zE), None,
-                                _iptr(m), _iptr(hasg), _ptr(Lf), float(thr), int(maxit), _ptr(rho), _ptr(beta),
-                                _ptr(mu), _iptr(iters), _ptr(rho_true), _iptr(nconf), _iptr(state))
+        st = lib.rsk_cg_scalars(S, Jm, _iptr(mode), _ptr(gam), _ptr(rho_new), _ptr(za), _ptr(ze),
+                                None if zg is None else _ptr(zg), _iptr(m), _iptr(hasg), _ptr(Lf), float(thr),
+                                int(maxit), _ptr(rho), _ptr(beta), _ptr(mu), _iptr(iters), _ptr(rho_true),
+                                _iptr(nconf), _iptr(state))
         if st != L.RSK_OK:
             raise RskError(f"rsk_cg_scalars failed ({st})")
-        new_p(state == LOOP_ACTIVE, mu.reshape(S, KM))
+        new_p(state == LOOP_ACTIVE, mu.reshape(S, KM), rho)
     # final true residual for shifts that stopped without a confirmation
     unconf = state != LOOP_DONE
     if unconf.any():
@@ -435,5 +531,190 @@ def slab_cg(ops: SlabOps, gamma: np.ndarray, b: torch.Tensor, X: torch.Tensor,
         rt = _h(ops.dot(Rt, Rt))
         rho_true = np.where(unconf, rt, rho_true)
         applies += unconf
-    return dict(iters=iters, applies=applies, relres_true=np.sqrt(np.maximum(rho_true, 0.0)) / nb,
-                status=state, m_used=m, dropped=dropped)
+    if Gout is not None:
+        ops.own(Gout).copy_(ops.own(X))
+        ops.axpby(-ones, X0, ones, Gout)
+    stat = np.where(state == LOOP_DONE, np.where(dropped > 0, L.RSK_CG_DEFL_DROPPED, L.RSK_CG_CONVERGED),
+                    np.where(state == LOOP_BREAKDOWN, L.RSK_CG_BREAKDOWN, L.RSK_CG_MAXIT))
+    out.update(iters=iters, applies=applies, relres=np.sqrt(np.maximum(rho_true, 0.0)) / nb,
+               status=stat.astype(np.int32), m_used=m, store_count=scnt, relres_true=None)
+    out["relres_true"] = out["relres"]
+    out["dropped"] = dropped
+    return out
+
+
+# ------------------------------------------------------------------ the outer step in slab mode
+class SlabHandle:
+    """The librsk Handle interface GpuSolver uses, with row-slab semantics: vectors are
+    extended (ext_rows x nx) tensors, every reduction is over owned rows and all-reduced,
+    applies refresh the halo first, the thin QR is the shifted Cholesky-QR3 with all-reduced
+    Grams (rsk_cholqr_pass)."""
+
+    def __init__(self, ops: SlabOps):
+        self.o = ops
+        self.lib = ops.lib
+
+    def set_weights(self, wx, wy, stream=None):
+        self.o.h.set_weights(wx, wy)
+
+    def apply_shifted(self, X, Y, gamma=None, EY=None, xdoty=None, mode=L.RSK_APPLY_SHIFTED, stream=None, nvec=None):
+        self.o.apply(X, Y, gamma, mode=mode, EY=EY)
+        if xdoty is not None:
+            xdoty.copy_(self.o.dot(X, Y))
+
+    def recycle_project(self, op, U, V, Cm, k=None, nv=None, stream=None):
+        if op == L.RSK_PROJ_UTV:
+            Cm.copy_(self.o.utv(U, V).reshape(Cm.shape))
+        else:
+            self.o.add_uc(op, U, V, Cm)
+
+    def batch_dot(self, X, Y, out, stream=None):
+        out.copy_(self.o.dot(X, Y))
+
+    def batch_axpby(self, a, X, b, Y, stream=None):
+        self.o.axpby(a, X, b, Y)
+
+    def qr_tall(self, V, Q, stream=None) -> np.ndarray:
+        """V (k, n) -> Q with orthonormal rows over the whole image, R (k x k, Fortran):
+        three shifted-Cholesky-QR passes (V -> Q -> V -> Q) with all-reduced Grams."""
+        o = self.o
+        k = V.shape[0]
+        nglob = o.plan.ny * o.plan.nx
+        Racc = np.zeros(k * k)
+        T = np.zeros(k * k)
+        src, dst = V, Q
+        for pss in range(3):
+            G = _h(o.utv(src, src)).ravel()                 # (k x k) row a = src^T src_a: symmetric
+            st = self.lib.rsk_cholqr_pass(k, nglob, pss, _ptr(np.ascontiguousarray(G)), _ptr(T), _ptr(Racc))
+            if st != L.RSK_OK:
+                raise RskError(f"rsk_cholqr_pass failed ({st})")
+            o.own(dst).zero_()
+            # dst_j = sum_i src_i T[i, j]  ->  Cm[j, i] = T[i + j k]
+            Cm = torch.from_numpy(np.ascontiguousarray(T.reshape(k, k))).to(o.dev)
+            o.add_uc(L.RSK_ADD_UC, src, dst, Cm)
+            src, dst = dst, src
+        return np.asfortranarray(Racc.reshape((k, k), order="F"))   # R[i, j] = Racc[i + j k]
+
+    def lcurve_norms(self, X, d, rho, eta2, scratch, stream=None):
+        rho.copy_(torch.sqrt(self.o.resnorm2(X, d)))
+        eta2.copy_(torch.sqrt(self.o.seminorm2(X)))
+
+    def irn_weights(self, x, tau, wx=None, wy=None, eta2=None, stream=None):
+        self.o.comm.halo(x[None])
+        self.o.h.irn_weights(x, tau, wx, wy)
+
+    def make_rhs(self, x_true, xi, nu, d, b, stream=None):
+        """d = C x_true + nu ||C x_true|| xi / ||xi||, b = C^T d (norms over the image)"""
+        o = self.o
+        Xt = x_true.reshape(1, -1).clone()
+        Cx = torch.empty_like(Xt)
+        o.apply(Xt, Cx, mode=L.RSK_APPLY_C_ONLY)
+        ncx = float(np.sqrt(_h(o.dot(Cx, Cx))[0]))
+        xv = xi.reshape(1, -1).clone()
+        nxi = float(np.sqrt(_h(o.dot(xv, xv))[0]))
+        D = d.reshape(1, -1)
+        o.own(D).copy_(o.own(Cx))
+        o.axpby(np.array([nu * ncx / nxi]), xv, np.ones(1), D)
+        Bm = b.reshape(1, -1)
+        o.apply(D, Bm, mode=L.RSK_APPLY_CT_ONLY)
+
+    def cg_workspace_bytes(self, nshift, flags=0) -> int:
+        return 8
+
+
+class SlabGpuSolver:
+    """GpuSolver's nested solve (pipeline.py) on one row slab: the same outer step, run
+    SPMD on every rank with SlabHandle for the vector work and slab_cg for the batched
+    deflated CG. Vectors are extended slab vectors (ext_rows x nx)."""
+
+    def __init__(self, cfg, psf: np.ndarray, gamma: np.ndarray, plan: SlabPlan, rank: int, comm, device: int = 0):
+        from . import pipeline as pl
+        from . import shard
+        self._pl = pl
+        torch.cuda.set_device(device)
+        self.dev = torch.device("cuda", device)
+        self.cfg = cfg
+        self.plan, self.rank = plan, rank
+        self.o = SlabOps(plan, rank, comm, psf, device)
+        self.n, self.M = cfg.n, cfg.M
+        self.N = self.o.ext_n
+        self.gamma = np.ascontiguousarray(gamma, dtype=np.float64)
+        self.h = SlabHandle(self.o)
+        self.check_every = 8
+        self.profile = False
+        self.stream = None
+        self.dist = shard.Dist(False)
+        f = dict(dtype=torch.float64, device=self.dev)
+        self.f = f
+        N, M = self.N, self.M
+        self.gam_dev = torch.from_numpy(self.gamma).to(self.dev)
+        self.b = torch.empty(N, **f)
+        self.d = torch.empty(N, **f)
+        w0 = torch.ones(self.n, self.n, **f)
+        w0[:, -1] = 0.0
+        self.w0x = plan.extend(w0.reshape(-1), rank).contiguous()
+        self.w0y = plan.extend(w0.t().contiguous().reshape(-1), rank).contiguous()
+        self.wx = torch.empty(N, **f)
+        self.wy = torch.empty(N, **f)
+        self.ws = torch.empty(8, dtype=torch.uint8, device=self.dev)
+        self.lc_scratch = torch.empty(M, N, **f)
+        self.rho_dev = torch.empty(M, **f)
+        self.eta_dev = torch.empty(M, **f)
+        self.grp = np.array([0 if (l + 1) <= cfg.I_split else 1 for l in range(M)], dtype=np.int32)
+
+    def set_data(self, x_true_full: torch.Tensor, xi_full: torch.Tensor):
+        """the global seeded images, cut to this slab (each rank holds its rows + halo)"""
+        xt = self.plan.extend(x_true_full.reshape(-1), self.rank)
+        xi = self.plan.extend(xi_full.reshape(-1), self.rank)
+        self.h.make_rhs(xt, xi, self.cfg.noise, self.d, self.b)
+
+    def cg(self, gammas_idx, X, has_xp, Gout=None, groups=None, ghat=None, store=None, flags=0, order=None):
+        from .pipeline import STORE_CAP
+        return slab_cg(self.o, self.gamma[list(gammas_idx)], self.b, X, tol=self.cfg.tol, maxit=self.cfg.maxit,
+                       has_xp=has_xp, groups=groups, ghat=ghat, store=store, store_cap=STORE_CAP, Gout=Gout)
+
+    def __getattr__(self, name):
+        # the outer-step logic is GpuSolver's, bound to this object
+        attr = getattr(self._pl.GpuSolver, name)
+        if callable(attr):
+            return attr.__get__(self, type(self))
+        return attr
+
+
+def main(argv=None):
+    """Row-slab nested solve across GPUs (one rank per GPU, NCCL):
+    python -m torch.distributed.run --nproc-per-node G -m paper_2306_15049_b200.slab --config C5 --outer 1"""
+    import argparse
+    import os
+    import time
+
+    import torch.distributed as dist
+
+    import rsk_synth as S
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--outer", type=int, default=1)
+    a = ap.parse_args(argv)
+    rank, world = int(os.environ.get("RANK", "0")), int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl")
+    cfg = S.CONFIGS[a.config]
+    inp = S.make_inputs(cfg)
+    plan = SlabPlan(cfg.n, cfg.n, cfg.r, world)
+    dev = torch.device("cuda", local)
+    sol = SlabGpuSolver(cfg, inp["psf"], inp["gamma"], plan, rank, DistComm(plan, rank), device=local)
+    t0 = time.perf_counter()
+    sol.set_data(torch.from_numpy(inp["x_true"]).to(dev), torch.from_numpy(inp["xi"]).to(dev))
+    outs = sol.run(K_out=a.outer)
+    torch.cuda.synchronize(dev)
+    dt = time.perf_counter() - t0
+    if rank == 0:
+        for o in outs:
+            print(f"outer {o.k}: iters {o.iters.tolist()} l* {o.lstar} status {o.status.tolist()}", flush=True)
+        print(f"{cfg.name} on {world} row slabs: {dt:.1f} s", flush=True)
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -168,3 +168,40 @@ def test_slab_irn_and_lcurve_norms_match_single_domain(torch_dev, n, r, nranks):
         np.testing.assert_array_equal(b2, plan.owned(wy, k).cpu().numpy())
         np.testing.assert_allclose(e2, eta.cpu().numpy(), rtol=1e-13)
         np.testing.assert_allclose(r2, rho2.cpu().numpy(), rtol=1e-13)
+
+
+@pytest.mark.parametrize("nranks", [2, 3])
+def test_slab_nested_outer_step_matches_single_domain(torch_dev, nranks):
+    """The whole outer step (seeds, Ritz, stabilize, anchoring, guesses, groups, deflated CG,
+    L-curve) in slab mode (SlabGpuSolver, ranks as threads) against the single-domain
+    GpuSolver: same corner l*, iteration counts +-max(2, 2%), solutions <= 1e-7 relative."""
+    torch, dev = torch_dev
+    from paper_2306_15049_b200.pipeline import GpuSolver
+    from paper_2306_15049_b200.slab import SlabGpuSolver, SlabPlan, run_threads
+    cfg = S.small_config(n=48, M=6, r=3, sigma=1.2, n_c=10, J=3, K_out=1, tol=1e-10)
+    inp = S.make_inputs(cfg)
+    xt = torch.from_numpy(inp["x_true"]).to(dev)
+    xi = torch.from_numpy(inp["xi"]).to(dev)
+    ref = GpuSolver(cfg, inp["psf"], inp["gamma"], device=0)
+    ref.set_data(xt, xi)
+    o_ref = ref.run(K_out=1)[0]
+    X_ref = ref.final["X_prev"].cpu().numpy()
+    torch.cuda.synchronize()
+    plan = SlabPlan(cfg.n, cfg.n, cfg.r, nranks)
+
+    def rank_fn(k, comm):
+        sol = SlabGpuSolver(cfg, inp["psf"], inp["gamma"], plan, k, comm, device=0)
+        sol.set_data(xt, xi)
+        o = sol.run(K_out=1)[0]
+        torch.cuda.synchronize()
+        return o, sol.o.own(sol.final["X_prev"]).cpu().numpy()
+
+    outs = run_threads(plan, rank_fn)
+    o = outs[0][0]
+    Xs = np.concatenate([r[1] for r in outs], axis=1)
+    assert o.lstar == o_ref.lstar
+    tolit = np.maximum(2, np.ceil(0.02 * o_ref.iters))
+    assert np.all(np.abs(o.iters - o_ref.iters) <= tolit), (o.iters, o_ref.iters)
+    for l in range(cfg.M):
+        rel = np.linalg.norm(Xs[l] - X_ref[l]) / np.linalg.norm(X_ref[l])
+        assert rel <= 1e-7, (l, rel)
