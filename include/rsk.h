@@ -143,6 +143,43 @@ rsk_status rsk_recycle_project(rsk_handle h, int op, int64_t n, int k, const dou
 rsk_status rsk_irn_weights(rsk_handle h, const double* x, double tau, double* wx, double* wy,
                            double* eta2, void* stream);
 
+/* rsk_irn_weights_iso -- isotropic IRN weights (the isotropic TV
+ * term of P:117, beta = tau^2; reading G32): one weight per pixel
+ *   w[i][j] = (gx^2 + gy^2 + tau^2)^(-1/2),  gx = x[i][j+1]-x[i][j] (0 at j = nx-1),
+ *                                            gy = x[i+1][j]-x[i][j] (0 at i = ny-1)
+ * written to wx[i][j] (j <= nx-2; 0 at j = nx-1) and wy[i][j] (i <= ny-2; 0 at
+ * i = ny-1), computed unfused in that order. Arguments, eta2, ownership and errors
+ * as rsk_irn_weights. */
+rsk_status rsk_irn_weights_iso(rsk_handle h, const double* x, double tau, double* wx, double* wy,
+                               double* eta2, void* stream);
+
+/* rsk_gazzola_weights -- the paper's own edge-preserving weight update
+ * (reading G31):
+ *   q = L x,  w = |D_k q| / ||D_k q||_inf,  w <- 1 - w.^p,  D_{k+1} = diag(w) D_k,
+ *   E_{k+1} = L^T D_{k+1}^2 L.
+ * D_k is diagonal over the rows of L and held in the weights' padded layout:
+ * dx[i][j] on the Dx row (i, j) (j <= nx-2), dy[i][j] on the Dy row (i <= ny-2),
+ * pads 0 (D_0 = I = the identity weights). x: device image (ny x nx).
+ * dx, dy: device, IN/OUT (D_k in, D_{k+1} out, pads written 0).
+ * wx, wy: device outputs, W_{k+1} = D_{k+1}^2 (adopt with rsk_set_weights).
+ * ||D_k q||_inf = 0 leaves D unchanged. p: finite, > 0 (the paper gives no value;
+ * p = 2 and 1 are exact squares/copies, 0.5 a sqrt, other p use pow). Uses the
+ * handle's scratch; deterministic (max is order-independent). Errors: EINVAL on NULL
+ * or misaligned pointers, aliased outputs, bad p. */
+rsk_status rsk_gazzola_weights(rsk_handle h, const double* x, double p, double* dx, double* dy,
+                               double* wx, double* wy, void* stream);
+
+/* rsk_gazzola_max / rsk_gazzola_update -- the two halves of rsk_gazzola_weights,
+ * for a decomposed image (row slabs): m (device scalar) = ||D_k L x||_inf over the
+ * handle's grid (a missing Dy row of the grid's last row does not count); the
+ * caller may combine the m of several sub-grids (max) before the update, which
+ * applies w = |D_k q| / m, w <- 1 - w.^p, D_{k+1} = diag(w) D_k, W = D^2 with that m.
+ * Arguments, ownership and errors as rsk_gazzola_weights. */
+rsk_status rsk_gazzola_max(rsk_handle h, const double* x, const double* dx, const double* dy,
+                           double* m, void* stream);
+rsk_status rsk_gazzola_update(rsk_handle h, const double* x, double p, const double* m, double* dx,
+                              double* dy, double* wx, double* wy, void* stream);
+
 /* rsk_cg_recycled_batch -- batched deflated CG (the paper's recycled inner
  * solve in CG form; eq:corr_g P:462-468, local spaces eq:localU P:473, Alg. 3/4;
  * readings D1/D3): for every shift l, in lockstep,

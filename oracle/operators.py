@@ -12,6 +12,8 @@ PAPER.md:
   * C: symmetric Gaussian blur, zero boundary
 North-star (BASELINE.json): E_k = L^T W_k L with the IRN weights
   w_i = ((L x)_i^2 + tau^2)^(-1/2), W_0 = I            (reading G2/G3)
+SURVEY §8(f) f1 (the paper's own outer step): Gazzola's rule P:144-152, isotropic
+  IRN, the 3-consecutive-lambda* stopping rule P:1042.
 """
 from __future__ import annotations
 
@@ -114,6 +116,61 @@ def irn_weights(x: np.ndarray, tau: float):
     wx[:, :-1] = 1.0 / np.sqrt(qx * qx + tau * tau)
     wy[:-1, :] = 1.0 / np.sqrt(qy * qy + tau * tau)
     return wx, wy
+
+
+def irn_weights_iso(x: np.ndarray, tau: float):
+    """Isotropic IRN weights (the isotropic TV term of P:117 with
+    beta = tau^2): one weight per PIXEL p,
+        w_p = ((Dx x)_p^2 + (Dy x)_p^2 + tau^2)^(-1/2),
+    a difference that does not exist at p (last column / last row) counting 0
+    (reading G32), placed on both rows of L at p; pads = 0."""
+    n = x.shape[0]
+    qx, qy = grad(x)
+    gx = np.zeros((n, n))
+    gy = np.zeros((n, n))
+    gx[:, :-1] = qx
+    gy[:-1, :] = qy
+    w = 1.0 / np.sqrt(gx * gx + gy * gy + tau * tau)
+    wx = w.copy()
+    wy = w.copy()
+    wx[:, n - 1] = 0.0
+    wy[n - 1, :] = 0.0
+    return wx, wy
+
+
+def gazzola_step(dx: np.ndarray, dy: np.ndarray, x: np.ndarray, p: float):
+    """Gazzola's edge-preserving update of the paper's own outer loop:
+        q = L x,   w = |D_k q| / ||D_k q||_inf,   w <- 1 - w.^p,   D_{k+1} = diag(w) D_k,
+    E_{k+1} = L^T D_{k+1}^2 L. D_k is diagonal over the 2 n(n-1) rows of L and is
+    held in the padded layout of the weights (dx on the Dx rows, dy on the Dy rows,
+    pads 0); D_0 = I (E_0 = L^T L). p is never given by the paper (default 2,
+    SPEC S:421). ||D_k q||_inf = 0 (x constant along every row with D_k > 0): w = 0,
+    so D_{k+1} = D_k (reading G31).
+    Returns (dx', dy') = D_{k+1} and (wx', wy') = D_{k+1}^2, the weights E uses."""
+    qx, qy = grad(x)
+    tx = np.abs(dx[:, :-1] * qx)
+    ty = np.abs(dy[:-1, :] * qy)
+    m = max(float(tx.max(initial=0.0)), float(ty.max(initial=0.0)))
+    if m > 0.0:
+        wxr = tx / m
+        wyr = ty / m
+    else:
+        wxr = np.zeros_like(tx)
+        wyr = np.zeros_like(ty)
+    wxr = 1.0 - wxr ** p
+    wyr = 1.0 - wyr ** p
+    ndx = np.zeros_like(dx)
+    ndy = np.zeros_like(dy)
+    ndx[:, :-1] = wxr * dx[:, :-1]
+    ndy[:-1, :] = wyr * dy[:-1, :]
+    return (ndx, ndy), (ndx * ndx, ndy * ndy)
+
+
+def lstar_settled(history, count: int = 3) -> bool:
+    """The paper's outer stopping rule: stop 'once the selected lambda is the
+    same for three consecutive iterations' -- the last `count` L-curve choices are one
+    shift index (the shift grid is fixed, so equal lambda = equal index)."""
+    return len(history) >= count and len(set(history[-count:])) == 1
 
 
 def seminorm2(wx, wy, x) -> float:

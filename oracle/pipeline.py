@@ -10,7 +10,8 @@ One outer step k (reading D3: all shifts of a step are independent):
   5. groups L = {l <= I}, R = {l > I}; W from gamma_{J_L}, gamma_{J_R} (Alg. 4)
   6. per shift: U_l = [W_g(l), g-hat^(k-1,l)] and deflated CG (O4)
   7. L-curve corner l* (P:138-140), x* = x^(k,l*)
-  8. W_{k+1} = IRN weights of x* (north_star; reading G2)
+  8. W_{k+1} = IRN weights of x* (north_star; reading G2), or the f1 rules:
+     isotropic IRN / Gazzola's D_{k+1} = diag(1 - w.^p) D_k
 """
 from __future__ import annotations
 
@@ -149,21 +150,42 @@ def outer_step(cfg, h, b, d, gamma, st: StepState, shifts=None) -> StepResult:
                       rho, eta, overhead, V_i1, Ut, an)
 
 
+def next_weights(cfg, st_w, xstar):
+    """W_{k+1} from x* by cfg.weight_rule: "irn" (north_star, reading G2), "irn_iso"
+    (isotropic IRN) or "gazzola" (st_w carries D_k). Returns
+    ((wx, wy), D_{k+1} or None)."""
+    rule = getattr(cfg, "weight_rule", "irn")
+    if rule == "irn":
+        return ops.irn_weights(xstar, cfg.tau), None
+    if rule == "irn_iso":
+        return ops.irn_weights_iso(xstar, cfg.tau), None
+    if rule == "gazzola":
+        D, W = ops.gazzola_step(st_w[0], st_w[1], xstar, getattr(cfg, "p", 2.0))
+        return W, D
+    raise ValueError(f"unknown weight rule {rule!r}")
+
+
 def run(cfg, inputs, K_out=None, keep_steps=False):
-    """The outer IRN loop: K_out outer steps (configs fix the count, reading of A28)."""
+    """The outer loop: up to K_out outer steps (configs fix the count, reading of A28);
+    cfg.stop == "lstar3" also stops once l* is the same for 3 consecutive steps."""
     n = cfg.n
     h = inputs["psf"]
     d, b2 = ops.make_data(h, inputs["x_true"], inputs["xi"], cfg.noise)
     b = b2.ravel(); dd = d
     gamma = inputs["gamma"]
     wx, wy = ops.identity_weights(n)
+    D = ops.identity_weights(n)            # D_0 = I (Gazzola's rule only)
     st = StepState(0, wx, wy, None, None, None)
     steps = []
+    hist = []
     for k in range(K_out or cfg.K_out):
         st.k = k
         res = outer_step(cfg, h, b, dd, gamma, st)
         steps.append(res if keep_steps else dataclasses.replace(res, Ut=None, anchor=None))
+        hist.append(res.lstar)
         xstar = res.X[:, res.lstar].reshape(n, n)
-        wx, wy = ops.irn_weights(xstar, cfg.tau)
+        (wx, wy), D = next_weights(cfg, D, xstar)
         st = StepState(k + 1, wx, wy, res.X, res.G, res.V_i1)
-    return {"b": b, "d": dd, "steps": steps, "final_weights": (wx, wy)}
+        if getattr(cfg, "stop", "fixed") == "lstar3" and ops.lstar_settled(hist):
+            break
+    return {"b": b, "d": dd, "steps": steps, "final_weights": (wx, wy), "lstar": hist}

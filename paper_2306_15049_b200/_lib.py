@@ -82,6 +82,10 @@ _SIGS = {
     "rsk_recycle_project": (C.c_int, [C.c_void_p, C.c_int, _i64, C.c_int, _dp, _i64, C.c_int, _dp,
                                       _i64, _dp, _i64, C.c_void_p]),
     "rsk_irn_weights": (C.c_int, [C.c_void_p, _dp, C.c_double, _dp, _dp, _dp, C.c_void_p]),
+    "rsk_irn_weights_iso": (C.c_int, [C.c_void_p, _dp, C.c_double, _dp, _dp, _dp, C.c_void_p]),
+    "rsk_gazzola_weights": (C.c_int, [C.c_void_p, _dp, C.c_double, _dp, _dp, _dp, _dp, C.c_void_p]),
+    "rsk_gazzola_max": (C.c_int, [C.c_void_p, _dp, _dp, _dp, _dp, C.c_void_p]),
+    "rsk_gazzola_update": (C.c_int, [C.c_void_p, _dp, C.c_double, _dp, _dp, _dp, _dp, _dp, C.c_void_p]),
     "rsk_cg_workspace_bytes": (C.c_size_t, [C.c_void_p, C.c_int, C.c_int]),
     "rsk_cg_recycled_batch": (C.c_int, [C.c_void_p, C.POINTER(CgDesc), C.POINTER(CgOut), _dp,
                                         C.c_size_t, C.c_void_p]),

@@ -274,8 +274,53 @@ extern "C" rsk_status rsk_irn_weights(rsk_handle h, const double* x, double tau,
   RSK_ARG(std::isfinite(tau) && tau > 0.0, "rsk_irn_weights: tau must be finite and > 0");
   RSK_ARG((wx == nullptr) == (wy == nullptr), "rsk_irn_weights: wx and wy must both be given or both NULL");
   RSK_ARG(wx || eta2, "rsk_irn_weights: nothing to compute");
-  RSK_CUDA(launch_irn(h, x, tau, wx, wy, eta2, S(stream)));
+  RSK_CUDA(launch_irn(h, x, tau, 0, wx, wy, eta2, S(stream)));
   return RSK_OK;
+}
+
+extern "C" rsk_status rsk_irn_weights_iso(rsk_handle h, const double* x, double tau, double* wx, double* wy,
+                                          double* eta2, void* stream) {
+  if (!h) return RSK_EINVAL;
+  RSK_ARG(x && aligned8(x), "rsk_irn_weights_iso: null x");
+  RSK_ARG(std::isfinite(tau) && tau > 0.0, "rsk_irn_weights_iso: tau must be finite and > 0");
+  RSK_ARG((wx == nullptr) == (wy == nullptr), "rsk_irn_weights_iso: wx and wy must both be given or both NULL");
+  RSK_ARG(wx || eta2, "rsk_irn_weights_iso: nothing to compute");
+  RSK_CUDA(launch_irn(h, x, tau, 1, wx, wy, eta2, S(stream)));
+  return RSK_OK;
+}
+
+extern "C" rsk_status rsk_gazzola_max(rsk_handle h, const double* x, const double* dx, const double* dy,
+                                      double* m, void* stream) {
+  if (!h) return RSK_EINVAL;
+  RSK_ARG(x && dx && dy && m, "rsk_gazzola_max: null pointer");
+  RSK_ARG(aligned8(x) && aligned8(dx) && aligned8(dy) && aligned8(m), "rsk_gazzola_max: misaligned pointer");
+  RSK_CUDA(launch_gazzola_max(h, x, dx, dy, m, S(stream)));
+  return RSK_OK;
+}
+
+extern "C" rsk_status rsk_gazzola_update(rsk_handle h, const double* x, double p, const double* m, double* dx,
+                                         double* dy, double* wx, double* wy, void* stream) {
+  if (!h) return RSK_EINVAL;
+  RSK_ARG(x && m && dx && dy && wx && wy, "rsk_gazzola_update: null pointer");
+  RSK_ARG(aligned8(x) && aligned8(m) && aligned8(dx) && aligned8(dy) && aligned8(wx) && aligned8(wy),
+          "rsk_gazzola_update: misaligned pointer");
+  RSK_ARG(std::isfinite(p) && p > 0.0, "rsk_gazzola_update: p must be finite and > 0");
+  RSK_ARG(dx != dy && wx != wy && wx != dx && wx != dy && wy != dx && wy != dy,
+          "rsk_gazzola_update: dx, dy, wx, wy must be four distinct arrays");
+  RSK_CUDA(launch_gazzola_update(h, x, p, m, dx, dy, wx, wy, S(stream)));
+  return RSK_OK;
+}
+
+extern "C" rsk_status rsk_gazzola_weights(rsk_handle h, const double* x, double p, double* dx, double* dy,
+                                          double* wx, double* wy, void* stream) {
+  if (!h) return RSK_EINVAL;
+  RSK_ARG(x && dx && dy && wx && wy, "rsk_gazzola_weights: null pointer");
+  RSK_ARG(std::isfinite(p) && p > 0.0, "rsk_gazzola_weights: p must be finite and > 0");
+  // the max goes to the last scratch slot (the per-chunk partials fill it from the front)
+  double* m = h->scratch + (h->scratch_bytes / sizeof(double) - 1);
+  rsk_status s = rsk_gazzola_max(h, x, dx, dy, m, stream);
+  if (s != RSK_OK) return s;
+  return rsk_gazzola_update(h, x, p, m, dx, dy, wx, wy, stream);
 }
 
 extern "C" rsk_status rsk_make_rhs(rsk_handle h, const double* x_true, const double* xi, double nu,

@@ -151,8 +151,12 @@ cudaError_t launch_batch_dot(Handle* h, int64_t n, int nv, const double* X, int6
 cudaError_t launch_batch_axpby(int64_t n, int nv, const double* a, const double* X,
                                int64_t ldx, const double* b, double* Y, int64_t ldy,
                                cudaStream_t st);  // a, b DEVICE arrays (b nullable)
-cudaError_t launch_irn(Handle* h, const double* x, double tau, double* wx, double* wy,
+cudaError_t launch_irn(Handle* h, const double* x, double tau, int iso, double* wx, double* wy,
                        double* eta2, cudaStream_t st);
+cudaError_t launch_gazzola_max(Handle* h, const double* x, const double* dx, const double* dy, double* m,
+                               cudaStream_t st);
+cudaError_t launch_gazzola_update(Handle* h, const double* x, double pw, const double* m, double* dx,
+                                  double* dy, double* wx, double* wy, cudaStream_t st);
 cudaError_t launch_seminorm_batch(Handle* h, int nvec, const double* X, int64_t ldx,
                                   double* eta2, cudaStream_t st, int do_sqrt = 0);
 cudaError_t launch_seminorm_rows(Handle* h, int nvec, const double* X, int64_t ldx, int row0, int row1,

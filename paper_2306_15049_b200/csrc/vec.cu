@@ -223,7 +223,7 @@ cudaError_t launch_batch_axpby(int64_t n, int nv, const double* a, const double*
 // ============================================================== IRN weights
 // wx = ((Dx x)^2 + tau^2)^(-1/2), wy likewise; eta2 partials under the handle weights.
 __global__ void __launch_bounds__(256) irn_kernel(int ny, int nx, const double* __restrict__ x,
-                                                  double tau, double* __restrict__ wx,
+                                                  double tau, int iso, double* __restrict__ wx,
                                                   double* __restrict__ wy,
                                                   const double* __restrict__ hwx,
                                                   const double* __restrict__ hwy,
@@ -231,7 +231,7 @@ __global__ void __launch_bounds__(256) irn_kernel(int ny, int nx, const double* 
   __shared__ double red[8];
   const int64_t N = (int64_t)ny * nx;
   const int64_t base = (int64_t)blockIdx.x * kChunk;
-  const double t2 = tau * tau;
+  const double t2 = __dmul_rn(tau, tau);
   double acc = 0.0;
   for (int e = 0; e < kChunk / 256; ++e) {
     const int64_t p = base + e * 256 + threadIdx.x;
@@ -242,7 +242,14 @@ __global__ void __launch_bounds__(256) irn_kernel(int ny, int nx, const double* 
     const bool hx = j < nx - 1, hy = i < ny - 1;
     if (hx) dx = x[p + 1] - xc;
     if (hy) dy = x[p + nx] - xc;
-    if (wx) {
+    if (wx && iso) {
+      // isotropic (reading G32): one weight per pixel, a missing difference is 0;
+      // unfused, in the order ((dx dx + dy dy) + tau tau)
+      const double g2 = __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), t2);
+      const double w = 1.0 / sqrt(g2);
+      wx[p] = hx ? w : 0.0;
+      wy[p] = hy ? w : 0.0;
+    } else if (wx) {
       wx[p] = hx ? 1.0 / sqrt(fma(dx, dx, t2)) : 0.0;
       wy[p] = hy ? 1.0 / sqrt(fma(dy, dy, t2)) : 0.0;
     }
@@ -251,13 +258,114 @@ __global__ void __launch_bounds__(256) irn_kernel(int ny, int nx, const double* 
   if (part) block_partial(acc, red, part + blockIdx.x);
 }
 
-cudaError_t launch_irn(Handle* h, const double* x, double tau, double* wx, double* wy,
+cudaError_t launch_irn(Handle* h, const double* x, double tau, int iso, double* wx, double* wy,
                        double* eta2, cudaStream_t st) {
   const int64_t N = h->ny * h->nx;
   const int nchunk = (int)((N + kChunk - 1) / kChunk);
-  count_launch(); irn_kernel<<<nchunk, 256, 0, st>>>((int)h->ny, (int)h->nx, x, tau, wx, wy, h->wx, h->wy,
-                                     eta2 ? h->scratch : nullptr);
+  count_launch(); irn_kernel<<<nchunk, 256, 0, st>>>((int)h->ny, (int)h->nx, x, tau, iso, wx, wy, h->wx,
+                                                     h->wy, eta2 ? h->scratch : nullptr);
   if (eta2) { count_launch(); reduce_partials<<<1, 32, 0, st>>>(h->scratch, nchunk, eta2, 0); }
+  return cudaGetLastError();
+}
+
+// ============================================================== Gazzola's weight update
+// q = L x, w = |D_k q| / ||D_k q||_inf, w <- 1 - w^p, D_{k+1} = diag(w) D_k,
+// W_{k+1} = D_{k+1}^2. Three launches: per-chunk max, final max, elementwise update.
+// max is order-independent, so the whole update is deterministic; every other step is
+// one correctly rounded operation in the oracle's order.
+__device__ __forceinline__ double block_max(double v, double* red) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  double t = lane < (int)(blockDim.x >> 5) ? red[lane] : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t = fmax(t, __shfl_xor_sync(0xffffffffu, t, o));
+  return t;
+}
+
+__global__ void __launch_bounds__(256) gz_max_part(int ny, int nx, const double* __restrict__ x,
+                                                   const double* __restrict__ dx,
+                                                   const double* __restrict__ dy,
+                                                   double* __restrict__ part) {
+  __shared__ double red[8];
+  const int64_t N = (int64_t)ny * nx;
+  const int64_t base = (int64_t)blockIdx.x * kChunk;
+  double m = 0.0;
+  for (int e = 0; e < kChunk / 256; ++e) {
+    const int64_t p = base + e * 256 + threadIdx.x;
+    if (p >= N) break;
+    const int i = (int)(p / nx), j = (int)(p - (int64_t)i * nx);
+    const double xc = x[p];
+    if (j < nx - 1) m = fmax(m, fabs(__dmul_rn(dx[p], x[p + 1] - xc)));
+    if (i < ny - 1) m = fmax(m, fabs(__dmul_rn(dy[p], x[p + nx] - xc)));
+  }
+  m = block_max(m, red);
+  if (threadIdx.x == 0) part[blockIdx.x] = m;
+}
+
+__global__ void __launch_bounds__(256) gz_max_final(const double* __restrict__ part, int nchunk,
+                                                    double* __restrict__ out) {
+  __shared__ double red[8];
+  double m = 0.0;
+  for (int j = threadIdx.x; j < nchunk; j += 256) m = fmax(m, part[j]);
+  m = block_max(m, red);
+  if (threadIdx.x == 0) *out = m;
+}
+
+__device__ __forceinline__ double gz_factor(double t, double m, double pw) {
+  const double w = m > 0.0 ? t / m : 0.0;
+  double wp;
+  if (pw == 2.0) wp = __dmul_rn(w, w);
+  else if (pw == 1.0) wp = w;
+  else if (pw == 0.5) wp = sqrt(w);
+  else wp = pow(w, pw);
+  return 1.0 - wp;
+}
+
+__global__ void __launch_bounds__(256) gz_update(int ny, int nx, const double* __restrict__ x, double pw,
+                                                 const double* __restrict__ mptr, double* __restrict__ dx,
+                                                 double* __restrict__ dy, double* __restrict__ wx,
+                                                 double* __restrict__ wy) {
+  const int64_t N = (int64_t)ny * nx;
+  const double m = *mptr;
+  for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < N;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(p / nx), j = (int)(p - (int64_t)i * nx);
+    const double xc = x[p];
+    double ndx = 0.0, ndy = 0.0;
+    if (j < nx - 1) {
+      const double d = dx[p];
+      ndx = __dmul_rn(gz_factor(fabs(__dmul_rn(d, x[p + 1] - xc)), m, pw), d);
+    }
+    if (i < ny - 1) {
+      const double d = dy[p];
+      ndy = __dmul_rn(gz_factor(fabs(__dmul_rn(d, x[p + nx] - xc)), m, pw), d);
+    }
+    dx[p] = ndx;
+    dy[p] = ndy;
+    wx[p] = __dmul_rn(ndx, ndx);
+    wy[p] = __dmul_rn(ndy, ndy);
+  }
+}
+
+cudaError_t launch_gazzola_max(Handle* h, const double* x, const double* dx, const double* dy, double* m,
+                               cudaStream_t st) {
+  const int64_t N = h->ny * h->nx;
+  const int nchunk = (int)((N + kChunk - 1) / kChunk);
+  if (sizeof(double) * (size_t)nchunk > h->scratch_bytes) return cudaErrorMemoryAllocation;
+  count_launch(); gz_max_part<<<nchunk, 256, 0, st>>>((int)h->ny, (int)h->nx, x, dx, dy, h->scratch);
+  count_launch(); gz_max_final<<<1, 256, 0, st>>>(h->scratch, nchunk, m);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gazzola_update(Handle* h, const double* x, double pw, const double* m, double* dx,
+                                  double* dy, double* wx, double* wy, cudaStream_t st) {
+  const int64_t N = h->ny * h->nx;
+  int64_t blocks = (N + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  count_launch(); gz_update<<<(unsigned)blocks, 256, 0, st>>>((int)h->ny, (int)h->nx, x, pw, m, dx, dy, wx, wy);
   return cudaGetLastError();
 }
 

@@ -100,6 +100,10 @@ class GpuSolver:
 
     def reset_weights(self):
         self.h.set_weights(self.w0x, self.w0y, stream=self.stream)
+        if getattr(self.cfg, "weight_rule", "irn") == "gazzola":
+            # D_0 = I, held in the weights' padded layout
+            self.Dx = self.w0x.clone()
+            self.Dy = self.w0y.clone()
 
     # ------------------------------------------------------------- building blocks
     def cg(self, gammas_idx, X, has_xp, Gout=None, groups=None, ghat=None, store=None,
@@ -340,19 +344,35 @@ class GpuSolver:
         return out, nst
 
     def next_weights(self, xstar: torch.Tensor):
-        """W_{k+1} from x* (north_star IRN rule, reading G2), adopted by the handle."""
-        self.h.irn_weights(xstar, self.cfg.tau, self.wx, self.wy, stream=self.stream)
+        """W_{k+1} from x*, adopted by the handle. cfg.weight_rule: "irn" (north_star,
+        reading G2), "irn_iso" (isotropic IRN) or "gazzola" (D_{k+1} =
+        diag(1 - w.^p) D_k)."""
+        rule = getattr(self.cfg, "weight_rule", "irn")
+        if rule == "irn":
+            self.h.irn_weights(xstar, self.cfg.tau, self.wx, self.wy, stream=self.stream)
+        elif rule == "irn_iso":
+            self.h.irn_weights_iso(xstar, self.cfg.tau, self.wx, self.wy, stream=self.stream)
+        elif rule == "gazzola":
+            self.h.gazzola_weights(xstar, self.cfg.p, self.Dx, self.Dy, self.wx, self.wy,
+                                   stream=self.stream)
+        else:
+            raise ValueError(f"unknown weight rule {rule!r}")
         self.h.set_weights(self.wx, self.wy, stream=self.stream)
 
     def run(self, K_out: int | None = None):
-        """The whole nested solve: K_out outer steps from W_0 = I."""
+        """The whole nested solve: up to K_out outer steps from W_0 = I; with
+        cfg.stop == "lstar3" it also stops once l* is the same for three consecutive
+        steps (P:1042)."""
         self.reset_weights()
         st: dict = {}
         outs = []
         K = K_out or self.cfg.K_out
+        settle = getattr(self.cfg, "stop", "fixed") == "lstar3"
         for k in range(K):
             o, st = self.outer_step(k, st)
             outs.append(o)
+            if settle and len(outs) >= 3 and len({x.lstar for x in outs[-3:]}) == 1:
+                break
             if k + 1 < K:
                 self.next_weights(st["xstar"])
         self.final = st

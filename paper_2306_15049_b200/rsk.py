@@ -114,6 +114,25 @@ class Handle:
                                       _stream(stream))
         self._check(st, "rsk_irn_weights")
 
+    def irn_weights_iso(self, x, tau, wx=None, wy=None, eta2=None, stream=None):
+        st = self.lib.rsk_irn_weights_iso(self.h, _dptr(x), float(tau), _dptr(wx), _dptr(wy), _dptr(eta2),
+                                          _stream(stream))
+        self._check(st, "rsk_irn_weights_iso")
+
+    def gazzola_weights(self, x, p, dx, dy, wx, wy, stream=None):
+        st = self.lib.rsk_gazzola_weights(self.h, _dptr(x), float(p), _dptr(dx), _dptr(dy), _dptr(wx),
+                                          _dptr(wy), _stream(stream))
+        self._check(st, "rsk_gazzola_weights")
+
+    def gazzola_max(self, x, dx, dy, m, stream=None):
+        st = self.lib.rsk_gazzola_max(self.h, _dptr(x), _dptr(dx), _dptr(dy), _dptr(m), _stream(stream))
+        self._check(st, "rsk_gazzola_max")
+
+    def gazzola_update(self, x, p, m, dx, dy, wx, wy, stream=None):
+        st = self.lib.rsk_gazzola_update(self.h, _dptr(x), float(p), _dptr(m), _dptr(dx), _dptr(dy),
+                                         _dptr(wx), _dptr(wy), _stream(stream))
+        self._check(st, "rsk_gazzola_update")
+
     def cg_workspace_bytes(self, nshift, flags=0) -> int:
         return int(self.lib.rsk_cg_workspace_bytes(self.h, nshift, flags))
 

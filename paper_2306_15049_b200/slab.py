@@ -88,9 +88,9 @@ class DistComm:
     def __init__(self, plan: SlabPlan, rank: int):
         self.plan, self.rank = plan, rank
 
-    def allreduce(self, t: torch.Tensor):
+    def allreduce(self, t: torch.Tensor, op: str = "sum"):
         import torch.distributed as dist
-        dist.all_reduce(t)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
 
     def halo(self, T: torch.Tensor):
         """T: (nv, ext_rows*nx). Fill the halo rows from the neighbours' owned rows."""
@@ -138,14 +138,17 @@ class ThreadComm:
         if t.is_cuda:
             torch.cuda.synchronize(t.device)
 
-    def allreduce(self, t: torch.Tensor):
+    def allreduce(self, t: torch.Tensor, op: str = "sum"):
         g = self.g
         self._sync(t)
         g.buf[self.rank] = t.clone()
         g.bar.wait()
         tot = g.buf[0].clone()
         for k in range(1, self.plan.nranks):     # fixed rank order
-            tot += g.buf[k]
+            if op == "max":
+                torch.maximum(tot, g.buf[k], out=tot)
+            else:
+                tot += g.buf[k]
         self._sync(tot)
         g.bar.wait()
         t.copy_(tot)
@@ -277,6 +280,28 @@ class SlabOps:
         if adopt:
             self.h.set_weights(wx, wy)
         return wx, wy
+
+    def irn_weights_iso(self, x: torch.Tensor, tau: float, adopt: bool = True):
+        """isotropic IRN weights, halo semantics as irn_weights"""
+        self.comm.halo(x[None] if x.dim() == 1 else x)
+        wx = torch.empty(self.ext_n, **self.f)
+        wy = torch.empty(self.ext_n, **self.f)
+        self.h.irn_weights_iso(x, tau, wx, wy)
+        if adopt:
+            self.h.set_weights(wx, wy)
+        return wx, wy
+
+    def gazzola_weights(self, x: torch.Tensor, p: float, dx, dy, wx, wy):
+        """Gazzola's update on the slab: the slab's ||D_k L x||_inf (every row
+        it stores is a true row of L except the missing Dy row of its last stored row,
+        which is not counted), max-reduced over ranks, then the elementwise update of
+        D (dx, dy in/out) and W = D^2 on every stored row (halo rows stay consistent with
+        their owners; the last stored row's Dy entry is not, and no owned output reads it)."""
+        self.comm.halo(x[None] if x.dim() == 1 else x)
+        m = torch.empty(1, **self.f)
+        self.h.gazzola_max(x, dx, dy, m)
+        self.comm.allreduce(m, op="max")
+        self.h.gazzola_update(x, p, m, dx, dy, wx, wy)
 
     def seminorm2(self, X: torch.Tensor) -> torch.Tensor:
         """sum wx (Dx x)^2 + wy (Dy x)^2 over the whole image (L-curve eta^2) of each
@@ -602,6 +627,13 @@ class SlabHandle:
     def irn_weights(self, x, tau, wx=None, wy=None, eta2=None, stream=None):
         self.o.comm.halo(x[None])
         self.o.h.irn_weights(x, tau, wx, wy)
+
+    def irn_weights_iso(self, x, tau, wx=None, wy=None, eta2=None, stream=None):
+        self.o.comm.halo(x[None])
+        self.o.h.irn_weights_iso(x, tau, wx, wy)
+
+    def gazzola_weights(self, x, p, dx, dy, wx, wy, stream=None):
+        self.o.gazzola_weights(x, p, dx, dy, wx, wy)
 
     def make_rhs(self, x_true, xi, nu, d, b, stream=None):
         """d = C x_true + nu ||C x_true|| xi / ||xi||, b = C^T d (norms over the image)"""

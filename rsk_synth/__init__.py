@@ -46,6 +46,9 @@ class Config:
     shapes: str           # phantom recipe key
     n_shapes: int
     maxit: int = 20000
+    weight_rule: str = "irn"   # outer weight update: "irn" (north_star), "irn_iso", "gazzola" (f1)
+    p: float = 2.0             # Gazzola exponent (never given by the paper; SPEC S:421 default)
+    stop: str = "fixed"        # outer stopping: "fixed" (K_out steps) or "lstar3"
 
     @property
     def N(self) -> int:

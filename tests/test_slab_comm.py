@@ -50,7 +50,9 @@ def _worker(rank, world, port, ny, nx, r, q):
         ok_halo = bool(torch.equal(T, plan.extend(full, rank)))
         t = torch.tensor([float(rank + 1), 2.0 * rank], dtype=torch.float64)
         comm.allreduce(t)
-        q.put((rank, ok_halo, t.tolist()))
+        m = torch.tensor([float((rank * 7) % 5), -float(rank)], dtype=torch.float64)
+        comm.allreduce(m, op="max")
+        q.put((rank, ok_halo, t.tolist() + m.tolist()))
     finally:
         dist.destroy_process_group()
 
@@ -67,7 +69,8 @@ def test_dist_halo_and_allreduce_gloo(world):
     res = dict((r, (h, t)) for r, h, t in (q.get(timeout=120) for _ in ps))
     for p in ps:
         p.join(timeout=60)
-    want = [sum(k + 1 for k in range(world)), sum(2.0 * k for k in range(world))]
+    want = [sum(k + 1 for k in range(world)), sum(2.0 * k for k in range(world)),
+            max(float((k * 7) % 5) for k in range(world)), 0.0]
     for k in range(world):
         assert res[k][0], f"rank {k}: halo rows differ from the neighbours' owned rows"
         assert res[k][1] == want
