@@ -71,7 +71,8 @@ enum {
   RSK_CG_BREAKDOWN = 2,    /* p.A_g p <= 0 or not finite; x = last iterate       */
   RSK_CG_DEFL_DROPPED = 3, /* converged, but G_l was not SPD and U_l was reduced */
   RSK_CG_ZERO_RHS = 4,     /* ||b|| = 0: x = 0, no iterations                    */
-  RSK_NOT_SPD = 5          /* rsk_orth_guess: Cholesky of G(delta) failed        */
+  RSK_NOT_SPD = 5,         /* rsk_orth_guess: Cholesky of G(delta) failed        */
+  RSK_SINGULAR = 6         /* rsk_oblique_guess: I + delta K^T E U singular      */
 };
 
 /* rsk_cg_desc.flags */
@@ -309,6 +310,20 @@ rsk_status rsk_get_counters(rsk_handle h, int64_t* applies_A_h, int64_t* applies
 rsk_status rsk_orth_guess(int nc, const double* R_h, const double* KtZE_h, const double* ZEtZE_h,
                           const double* ZEtb_h, const double* Ktb_h, double gamma_star, int m,
                           const double* gamma_h, double* C_h, int* status_h);
+
+/* rsk_oblique_guess -- the oblique-projection initial guesses of §sec:oblique
+ * (eq:obliqueupdate P:877-882): with (A + gamma_a E) U~ = K R at
+ * an anchor shift gamma_a and U = U~ R^-1 (never formed), x_0 = U q with K^T r_0 = 0:
+ *   (I + delta_l K^T E U) q = K^T b,   K^T E U = KtZE R^-1,   delta_l = gamma_l - gamma_a
+ *   C[:,l] = R^-1 q     (x_0 = U~ C[:,l])
+ * Dense LU with partial pivoting per shift. Two anchors (eq:updates P:1000-1005) are
+ * two calls, one per shift group, each with its own R, KtZE, Ktb, gamma_a.
+ * All host arrays, column-major: R_h, KtZE_h nc x nc; Ktb_h nc; gamma_h m; C_h nc x m.
+ * An exactly singular (or non-finite) system sets status_h[l] = RSK_SINGULAR and
+ * C[:,l] = 0. EINVAL on NULL, nc <= 0, m < 0, a zero diagonal of R, non-finite gamma_a. */
+rsk_status rsk_oblique_guess(int nc, const double* R_h, const double* KtZE_h, const double* Ktb_h,
+                             double gamma_anchor, int m, const double* gamma_h, double* C_h,
+                             int* status_h);
 
 /* rsk_pencil_ritz: Alg. 2 on the projected pencil (eq:hq P:677):
  * H = sym(Ahat) + gamma sym(Ehat) (nc x nc); cyclic-Jacobi eigenvectors, ascending;

@@ -7,6 +7,7 @@ One outer step k (reading D3: all shifts of a step are independent):
   2. U~ <- stabilize(U~, cap n_c)                         (Alg. 1)
   3. anchor at gamma_* = gamma_{i*}                       (eq:establishU)
   4. x_0^(k,l) = U q_l from eq:orthupdate
+     [f2(iii): oblique eq:obliqueupdate P:877-882 / two anchors eq:updates P:1000-1005]
   5. groups L = {l <= I}, R = {l > I}; W from gamma_{J_L}, gamma_{J_R} (Alg. 4)
   6. per shift: U_l = [W_g(l), g-hat^(k-1,l)] and deflated CG (O4)
   7. L-curve corner l* (P:138-140), x* = x^(k,l*)
@@ -106,6 +107,23 @@ def outer_step(cfg, h, b, d, gamma, st: StepState, shifts=None) -> StepResult:
     gstar = gamma[cfg.istar - 1]
     an = rc.anchor(h, wx, wy, Ut, b, gstar, n)
     overhead += Ut.shape[1]
+    mode = getattr(cfg, "guess", "orth")
+    if mode == "orth":
+        def guess(l):
+            return rc.principal_guess(an, gamma[l])
+    elif mode == "oblique":
+        def guess(l):
+            return rc.oblique_guess(an, gamma[l])
+    elif mode == "oblique2":
+        # eq:updates: anchors gamma_{I_L} (left group) and gamma_{I_R} (right group); the
+        # images Z_A, Z_E are shared (no extra applies), only K, R differ (reading G34)
+        anL = an if cfg.I_L == cfg.istar else rc.anchor(h, wx, wy, Ut, b, gamma[cfg.I_L - 1], n)
+        anR = rc.anchor(h, wx, wy, Ut, b, gamma[cfg.I_R - 1], n)
+
+        def guess(l):
+            return rc.oblique_guess(anL if (l + 1) <= cfg.I_split else anR, gamma[l])
+    else:
+        raise ValueError(f"unknown guess mode {mode!r}")
 
     groups = {}
     for gname, jidx in (("L", cfg.J_L - 1), ("R", cfg.J_R - 1)):
@@ -119,7 +137,7 @@ def outer_step(cfg, h, b, d, gamma, st: StepState, shifts=None) -> StepResult:
     todo = range(M) if shifts is None else shifts
     for l in todo:
         W, AW, EW = groups["L" if (l + 1) <= cfg.I_split else "R"]
-        xp = rc.principal_guess(an, gamma[l])
+        xp = guess(l)
         cols_U = [W]
         cols_Z = [AW + gamma[l] * EW]
         n_carry = 0

@@ -7,6 +7,7 @@ PAPER.md passages followed, in the order Alg. 5 uses them:
   stabilize (Alg. 1)                        P:581-587
   anchor (A + gamma_* E) U = K, K^T K = I   eq:establishU P:386-391, implicit R^-1 P:851-853
   initial guess per shift                   eq:orthupdate P:410-430
+    (or oblique: eq:obliqueupdate P:877-882, two anchors eq:updates P:1000-1005)
   projected pencil A^, E^                   eq:hq P:677
   group Ritz block W (Alg. 2, Alg. 4)       P:681-687, groups §5.4
   local space [W, g^(k-1,l)]                Alg. 3 P:700-704 without g^(k,l-1) (reading D3),
@@ -108,6 +109,28 @@ def guess_coeffs(an: Anchor, gamma: float):
         return None
     q = dense.chol_solve(L, an.v + d * an.u)
     return dense.tri_inv_apply(an.R, q)
+
+
+def oblique_coeffs(an: Anchor, gamma: float):
+    """eq:obliqueupdate: x_0 = U q with the oblique condition K^T r_0 = 0,
+    r_0 = b - (A + gamma E) U q = b - K q - delta E U q (since (A + gamma_a E) U = K):
+        (I + delta K^T E U) q = K^T b,   delta = gamma - gamma_a,
+    with K^T E U = K^T Z_E R^-1 = an.P. Solved by LU (numpy); returns c = R^-1 q, or
+    None when the system is singular (x_0 = 0)."""
+    nc = an.P.shape[0]
+    d = gamma - an.gamma_star
+    try:
+        q = np.linalg.solve(np.eye(nc) + d * an.P, an.v)
+    except np.linalg.LinAlgError:
+        return None
+    if not np.all(np.isfinite(q)):
+        return None
+    return dense.tri_inv_apply(an.R, q)
+
+
+def oblique_guess(an: Anchor, gamma: float):
+    c = oblique_coeffs(an, gamma)
+    return None if c is None else an.Ut @ c
 
 
 def principal_guess(an: Anchor, gamma: float):

@@ -14,7 +14,7 @@ RSK_OK, RSK_EINVAL, RSK_ECUDA, RSK_EUNSUPPORTED, RSK_EPARTIAL, RSK_ENOMEM = rang
 RSK_APPLY_SHIFTED, RSK_APPLY_SPLIT, RSK_APPLY_C_ONLY, RSK_APPLY_CT_ONLY = range(4)
 RSK_PROJ_UTV, RSK_ADD_UC, RSK_SUB_UC = range(3)
 (RSK_CG_CONVERGED, RSK_CG_MAXIT, RSK_CG_BREAKDOWN, RSK_CG_DEFL_DROPPED, RSK_CG_ZERO_RHS,
- RSK_NOT_SPD) = range(6)
+ RSK_NOT_SPD, RSK_SINGULAR) = range(7)
 RSK_CG_NO_DEFLATION, RSK_CG_STORE_RES, RSK_CG_PROFILE = 1, 2, 4
 RSK_MAX_GROUPS = 4
 RSK_MAX_LOCAL = 17
@@ -98,6 +98,7 @@ _SIGS = {
     "rsk_seminorm_rows": (C.c_int, [C.c_void_p, C.c_int, _dp, _i64, _i64, _i64, _dp, C.c_void_p]),
     "rsk_get_counters": (C.c_int, [C.c_void_p, C.POINTER(_i64), C.POINTER(_i64), C.POINTER(_i64),
                                    C.c_int]),
+    "rsk_oblique_guess": (C.c_int, [C.c_int, _hp, _hp, _hp, C.c_double, C.c_int, _hp, _hp, _ip]),
     "rsk_orth_guess": (C.c_int, [C.c_int, _hp, _hp, _hp, _hp, _hp, C.c_double, C.c_int, _hp, _hp,
                                  C.POINTER(C.c_int)]),
     "rsk_pencil_ritz": (C.c_int, [C.c_int, _hp, _hp, C.c_double, C.c_int, _hp, _hp]),

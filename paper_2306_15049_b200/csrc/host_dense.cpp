@@ -224,6 +224,71 @@ extern "C" rsk_status rsk_orth_guess(int nc, const double* R_h, const double* Kt
   return RSK_OK;
 }
 
+// Gaussian elimination with partial pivoting on a column-major n x n A (overwritten),
+// solving A q = b in place; false when a pivot is exactly zero or not finite.
+static bool lu_solve(int n, double* A, double* b) {
+  for (int k = 0; k < n; ++k) {
+    int piv = k;
+    double best = std::fabs(A[k + (size_t)k * n]);
+    for (int i = k + 1; i < n; ++i) {
+      const double v = std::fabs(A[i + (size_t)k * n]);
+      if (v > best) { best = v; piv = i; }
+    }
+    if (!(best > 0.0) || !std::isfinite(best)) return false;
+    if (piv != k) {
+      for (int j = 0; j < n; ++j) std::swap(A[k + (size_t)j * n], A[piv + (size_t)j * n]);
+      std::swap(b[k], b[piv]);
+    }
+    const double akk = A[k + (size_t)k * n];
+    for (int i = k + 1; i < n; ++i) {
+      const double f = A[i + (size_t)k * n] / akk;
+      A[i + (size_t)k * n] = f;
+      for (int j = k + 1; j < n; ++j) A[i + (size_t)j * n] -= f * A[k + (size_t)j * n];
+      b[i] -= f * b[k];
+    }
+  }
+  for (int i = n - 1; i >= 0; --i) {
+    double t = b[i];
+    for (int j = i + 1; j < n; ++j) t -= A[i + (size_t)j * n] * b[j];
+    b[i] = t / A[i + (size_t)i * n];
+  }
+  for (int i = 0; i < n; ++i)
+    if (!std::isfinite(b[i])) return false;
+  return true;
+}
+
+extern "C" rsk_status rsk_oblique_guess(int nc, const double* R_h, const double* KtZE_h, const double* Ktb_h,
+                                        double gamma_anchor, int m, const double* gamma_h, double* C_h,
+                                        int* status_h) {
+  if (nc <= 0 || m < 0 || !R_h || !KtZE_h || !Ktb_h || (m > 0 && (!gamma_h || !C_h || !status_h)) ||
+      !std::isfinite(gamma_anchor))
+    return RSK_EINVAL;
+  for (int i = 0; i < nc; ++i)
+    if (!(R_h[i + i * nc] != 0.0)) return RSK_EINVAL;
+  std::vector<double> P_(KtZE_h, KtZE_h + (size_t)nc * nc);   // K^T E U = KtZE R^-1
+  right_trsm_upper(nc, nc, R_h, P_.data());
+  std::vector<double> G((size_t)nc * nc), q(nc);
+  for (int l = 0; l < m; ++l) {
+    const double d = gamma_h[l] - gamma_anchor;
+    for (int j = 0; j < nc; ++j)
+      for (int i = 0; i < nc; ++i) G[i + (size_t)j * nc] = (i == j ? 1.0 : 0.0) + d * P_[i + (size_t)j * nc];
+    for (int i = 0; i < nc; ++i) q[i] = Ktb_h[i];
+    double* c = C_h + (size_t)l * nc;
+    if (!lu_solve(nc, G.data(), q.data())) {
+      status_h[l] = RSK_SINGULAR;
+      for (int i = 0; i < nc; ++i) c[i] = 0.0;
+      continue;
+    }
+    for (int i = nc - 1; i >= 0; --i) {   // c = R^-1 q
+      double t = q[i];
+      for (int j = i + 1; j < nc; ++j) t -= R_h[i + (size_t)j * nc] * c[j];
+      c[i] = t / R_h[i + (size_t)i * nc];
+    }
+    status_h[l] = 0;
+  }
+  return RSK_OK;
+}
+
 extern "C" rsk_status rsk_pencil_ritz(int nc, const double* Ahat_h, const double* Ehat_h, double gamma,
                                       int J, double* Wt_h, double* theta_h) {
   if (nc <= 0 || J < 0 || J > nc || !Ahat_h || !Ehat_h || (J > 0 && (!Wt_h || !theta_h)) ||

@@ -28,7 +28,7 @@ import torch
 
 from . import _lib as L
 from . import shard
-from .rsk import (Handle, carried_select, lcurve_corner, orth_guess, pencil_ritz,
+from .rsk import (Handle, carried_select, lcurve_corner, oblique_guess, orth_guess, pencil_ritz,
                   stabilize_small, sym_eig)
 
 COND_CAP = 1e10
@@ -267,16 +267,27 @@ class GpuSolver:
         R = self.h.qr_tall(Y, K, stream=self.stream)
         del Y
         KtZE = _host(self.utv(K, ZE)).T
-        ZEtZE = _host(self.utv(ZE, ZE)).T
-        ZEtb = _host(self.utv(ZE, self.b)).ravel()
         Ktb = _host(self.utv(K, self.b)).ravel()
         Ahat = _host(self.utv(Ut, ZA)).T
         Ehat = _host(self.utv(Ut, ZE)).T
         del K
-        # ---- principal guesses (eq:orthupdate) for this rank's shifts
-        Cg, gst = orth_guess(R, KtZE, ZEtZE, ZEtb, Ktb, gstar, self.gamma)
+        # ---- principal guesses for this rank's shifts: eq:orthupdate, or the oblique
+        # projections of §sec:oblique (f2(iii), Config.guess)
+        mode = getattr(cfg, "guess", "orth")
+        if mode == "orth":
+            ZEtZE = _host(self.utv(ZE, ZE)).T
+            ZEtb = _host(self.utv(ZE, self.b)).ravel()
+            Cg, gst = orth_guess(R, KtZE, ZEtZE, ZEtb, Ktb, gstar, self.gamma)
+        elif mode == "oblique":
+            Cg, gst = oblique_guess(R, KtZE, Ktb, gstar, self.gamma)
+        elif mode == "oblique2":
+            Cg, gst = self._two_anchor_guesses(ZA, ZE, R, KtZE, Ktb, gstar)
+        else:
+            raise ValueError(f"unknown guess mode {mode!r}")
         has_xp = (gst == 0).astype(np.int32)
         X = self.combine(Ut, Cg[:, mine]) if ml else torch.zeros(0, N, **self.f)
+        if getattr(self, "guess_hook", None) is not None:     # diagnostics (tools/probe_guess.py)
+            self.guess_hook(k, mine, X, has_xp[mine])
         # ---- group Ritz blocks (Alg. 2 / Alg. 4)
         Wg, AWg, EWg = [], [], []
         for jidx in (cfg.J_L - 1, cfg.J_R - 1):
@@ -342,6 +353,30 @@ class GpuSolver:
                       has_xp, keep, time.perf_counter() - t0, res["prof"])
         nst = dict(X_prev=Xf, G_prev=Gf, V_i1=V_i1, xstar=Xf[lstar], prev_iters=np.asarray(iters))
         return out, nst
+
+    def _two_anchor_guesses(self, ZA, ZE, R, KtZE, Ktb, gstar):
+        """eq:updates (reading G34): oblique guesses of the left group from
+        the anchor gamma_{I_L}, of the right group from gamma_{I_R}; the images Z_A, Z_E
+        are shared, each extra anchor costs one shifted CholQR3 and two projections."""
+        cfg = self.cfg
+        nI = cfg.I_split
+        parts = []
+        for (ia, sl) in ((cfg.I_L, slice(0, nI)), (cfg.I_R, slice(nI, self.M))):
+            ga = float(self.gamma[ia - 1])
+            if ga == gstar:
+                Ra, KtZEa, Ktba = R, KtZE, Ktb
+            else:
+                Y = ZA.clone()
+                self.h.batch_axpby(np.full(ZA.shape[0], ga), ZE, None, Y, stream=self.stream)
+                Ka = torch.empty_like(Y)
+                Ra = self.h.qr_tall(Y, Ka, stream=self.stream)
+                del Y
+                KtZEa = _host(self.utv(Ka, ZE)).T
+                Ktba = _host(self.utv(Ka, self.b)).ravel()
+                del Ka
+            parts.append(oblique_guess(Ra, KtZEa, Ktba, ga, self.gamma[sl]))
+        return (np.asfortranarray(np.concatenate([parts[0][0], parts[1][0]], axis=1)),
+                np.concatenate([parts[0][1], parts[1][1]]))
 
     def next_weights(self, xstar: torch.Tensor):
         """W_{k+1} from x*, adopted by the handle. cfg.weight_rule: "irn" (north_star,

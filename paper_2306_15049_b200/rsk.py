@@ -208,6 +208,23 @@ def orth_guess(R, KtZE, ZEtZE, ZEtb, Ktb, gamma_star, gammas):
     return Cm, stt
 
 
+def oblique_guess(R, KtZE, Ktb, gamma_anchor, gammas):
+    """eq:obliqueupdate per shift (host C++). Returns (C (nc x m, Fortran order), status[m])."""
+    lib = L.load()
+    nc = R.shape[0]
+    m = len(gammas)
+    R, KtZE = _f(R), _f(KtZE)
+    Ktb = np.ascontiguousarray(Ktb, dtype=np.float64).ravel()
+    g = np.ascontiguousarray(gammas, dtype=np.float64)
+    Cm = np.zeros((nc, m), order="F")
+    stt = np.zeros(m, dtype=np.int32)
+    st = lib.rsk_oblique_guess(nc, _hp(R), _hp(KtZE), _hp(Ktb), float(gamma_anchor), m, _hp(g), _hp(Cm),
+                               _ip(stt))
+    if st != L.RSK_OK:
+        raise RskError(f"rsk_oblique_guess failed ({st})")
+    return Cm, stt
+
+
 def pencil_ritz(Ahat, Ehat, gamma, J):
     lib = L.load()
     nc = Ahat.shape[0]

@@ -49,6 +49,8 @@ class Config:
     weight_rule: str = "irn"   # outer weight update: "irn" (north_star), "irn_iso", "gazzola" (f1)
     p: float = 2.0             # Gazzola exponent (never given by the paper; SPEC S:421 default)
     stop: str = "fixed"        # outer stopping: "fixed" (K_out steps) or "lstar3"
+    guess: str = "orth"        # principal guesses: "orth" (eq:orthupdate), "oblique" (one anchor,
+                               # eq:obliqueupdate) or "oblique2" (two anchors, eq:updates) -- f2(iii)
 
     @property
     def N(self) -> int:
@@ -78,6 +80,17 @@ class Config:
     @property
     def J_R(self) -> int:
         return self.M - 1
+
+    # anchors of the two-anchor oblique guesses (eq:updates P:1000-1005; reading G34):
+    # I_L = i* (already the principal anchor, inside the left group), I_R = the middle
+    # of the right group
+    @property
+    def I_L(self) -> int:
+        return self.istar
+
+    @property
+    def I_R(self) -> int:
+        return (self.I_split + 1 + self.M + 1) // 2
 
 
 CONFIGS = {

@@ -77,6 +77,33 @@ def test_host_orth_guess_matches_normal_equations():
         np.testing.assert_allclose(C[:, l], coef, rtol=1e-8, atol=1e-10)
 
 
+def test_host_oblique_guess_matches_petrov_galerkin():
+    """rsk_oblique_guess vs eq:obliqueupdate in the independent form
+    (K^T (A + gamma E) U~) c = K^T b (K^T r_0 = 0), solved densely."""
+    from paper_2306_15049_b200 import rsk
+    rng = np.random.default_rng(5)
+    N, nc = 60, 6
+    Ut, _ = np.linalg.qr(rng.standard_normal((N, nc)))
+    Ad = rng.standard_normal((N, N)); Ad = Ad @ Ad.T / N + np.eye(N)
+    Ed = rng.standard_normal((N, N)); Ed = Ed @ Ed.T / N
+    b = rng.standard_normal(N)
+    ga = 0.3
+    ZA, ZE = Ad @ Ut, Ed @ Ut
+    K, R = np.linalg.qr(ZA + ga * ZE)
+    sg = np.sign(np.diag(R)); K = K * sg; R = R * sg[:, None]
+    gammas = np.array([0.0, 0.01, 0.3, 5.0])
+    C, st = rsk.oblique_guess(R, K.T @ ZE, K.T @ b, ga, gammas)
+    assert np.all(st == 0)
+    for l, g in enumerate(gammas):
+        coef = np.linalg.solve(K.T @ (Ad + g * Ed) @ Ut, K.T @ b)
+        np.testing.assert_allclose(C[:, l], coef, rtol=1e-9, atol=1e-11)
+    # a singular system: K^T E U = -I / delta at delta = 1 -> I + P = 0
+    Rs = np.eye(3)
+    C, st = rsk.oblique_guess(Rs, -np.eye(3), np.ones(3), 0.0, np.array([1.0, 0.0]))
+    assert st[0] == 6 and np.all(C[:, 0] == 0) and st[1] == 0
+    np.testing.assert_array_equal(C[:, 1], np.ones(3))
+
+
 def test_host_lcurve_corner_matches_oracle():
     from oracle import pipeline
     from paper_2306_15049_b200 import rsk

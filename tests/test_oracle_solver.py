@@ -256,6 +256,55 @@ def test_orthogonal_beats_oblique_and_cs_identity():
     assert np.linalg.norm(b - Ag @ x0) == pytest.approx(np.linalg.norm(r1), rel=1e-9)
 
 
+@pytest.mark.parametrize("gamma", [1e-4, 0.05, 0.3, 2.0, 100.0])
+def test_oblique_guess_petrov_galerkin_and_analysis(gamma):
+    """eq:obliqueupdate: the oracle's oblique x_0 satisfies K^T r_0 = 0 with
+    r_0 from the dense operator, and its residual is the r_2 of §7.1's analysis
+    (q_2 = (K^T Y)^-1 K^T b with Y S = qr(K + delta E U))."""
+    n, h, wx, wy, b, Ut, an = _anchor_problem()
+    Ag = dense.assemble_shifted(h, wx, wy, gamma, n)
+    x0 = rc.oblique_guess(an, gamma)
+    r0 = b - Ag @ x0
+    assert np.linalg.norm(an.K.T @ r0) <= 1e-11 * np.linalg.norm(b)
+    d = gamma - an.gamma_star
+    EU = dense.tri_inv_t_apply(an.R, an.ZE.T).T
+    Y, _ = np.linalg.qr(an.K + d * EU)
+    r2 = b - Y @ np.linalg.solve(an.K.T @ Y, an.K.T @ b)
+    assert np.linalg.norm(r0) == pytest.approx(np.linalg.norm(r2), rel=1e-8)
+    assert np.linalg.norm(r0) >= np.linalg.norm(b - Ag @ rc.principal_guess(an, gamma)) * (1 - 1e-12)
+
+
+def test_oblique_guess_delta_zero_and_exact_range():
+    """delta = 0: oblique == orthogonal == eq:initX. b in Range((A + gamma E) U~):
+    both projections reproduce the exact solution (r_2 = r_1 = 0)."""
+    n, h, wx, wy, b, Ut, an = _anchor_problem()
+    c_o = rc.oblique_coeffs(an, an.gamma_star)
+    np.testing.assert_allclose(c_o, rc.guess_coeffs(an, an.gamma_star), rtol=1e-12, atol=1e-14)
+    gamma = 0.7
+    Ag = dense.assemble_shifted(h, wx, wy, gamma, n)
+    z = S.random_vectors(61, (Ut.shape[1],))
+    bb = Ag @ (Ut @ z)
+    an2 = rc.anchor(h, wx, wy, Ut, bb, an.gamma_star, n)
+    for x0 in (rc.oblique_guess(an2, gamma), rc.principal_guess(an2, gamma)):
+        np.testing.assert_allclose(x0, Ut @ z, rtol=0, atol=1e-9 * np.linalg.norm(Ut @ z))
+
+
+def test_two_anchor_oblique_groups():
+    """eq:updates: each group's guess is the oblique guess of its own anchor
+    (K_L or K_R), so K_g^T r_0 = 0 per group; at the right anchor's own shift it is
+    eq:initX for K_R."""
+    n, h, wx, wy, b, Ut, an = _anchor_problem(gamma_star=0.01)
+    gR = 3.0
+    anR = rc.anchor(h, wx, wy, Ut, b, gR, n)
+    for gamma, a in ((0.003, an), (0.02, an), (1.5, anR), (10.0, anR)):
+        Ag = dense.assemble_shifted(h, wx, wy, gamma, n)
+        r0 = b - Ag @ rc.oblique_guess(a, gamma)
+        assert np.linalg.norm(a.K.T @ r0) <= 1e-11 * np.linalg.norm(b)
+    AgR = dense.assemble_shifted(h, wx, wy, gR, n)
+    r0 = b - AgR @ rc.oblique_guess(anR, gR)
+    np.testing.assert_allclose(r0, b - anR.K @ (anR.K.T @ b), atol=1e-11 * np.linalg.norm(b))
+
+
 def test_group_ritz_smallest_eigenpairs():
     n, h, wx, wy, b, Ut, an = _anchor_problem(nc=9)
     gJ = 0.7
