@@ -249,6 +249,31 @@ size_t rsk_cg_workspace_bytes(rsk_handle h, int nshift, int flags);
 rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, rsk_cg_out* o, void* ws,
                                  size_t ws_bytes, void* stream);
 
+/* rsk_minres_recycled_batch -- recycling MINRES batched over shifts: the paper's
+ * OWN inner solver (PAPER.md §"Shift Specific Recycling" P:454-534; SURVEY §8(f)
+ * f2(ii)), an alternative to the deflated CG above on the same descriptor. Per
+ * shift l, with U~_l = [W_g, ghat_l] and Z_l = (A + gamma_l E) U~_l =
+ * [AW_g + gamma_l EW_g, ZGhat_l] (no applies):
+ *   eq:localU    Z_l = K_l R_l, K_l^T K_l = I (shifted Cholesky QR3; R_l singular
+ *                to 1e-14 relative -> drop ghat, then U~: DEFL_DROPPED)
+ *   eq:corr_g    r = b - A_g x_p (one apply when has_xp), solve for g = x - x_p
+ *   eq:minShift  Lanczos on (I - K K^T) A_g from (I - K K^T) r, the y-block
+ *                least squares by Givens rotations (MINRES), the z-block exactly
+ *   eq:xFinal    x = x_p + y_m + U~ R^-1 K^T (r - A_g y_m)
+ *   stop when the least-squares residual <= tol ||b||, confirmed on the true
+ *   residual b - A_g x (restart from x otherwise; reading G14).
+ * Same ownership, stream and error conventions as rsk_cg_recycled_batch: the call
+ * is host-blocking, `X` holds x_p in and x out, `Gout` (nullable) receives
+ * g = x - x_p; RSK_CG_STORE_RES is rejected (EINVAL). iters = Lanczos applies;
+ * applies = iters + the r_p apply + one per true-residual confirmation. ms_loop is
+ * not written. `ws`: at least rsk_minres_workspace_bytes(h, nshift, kmax) bytes,
+ * kmax = max_l (J_g(l) + has_ghat_l) <= RSK_MAX_LOCAL (7 N-vectors + kmax
+ * N-vectors (K_l) per shift). Returns RSK_OK, or RSK_EPARTIAL if a shift did not
+ * converge (status MAXIT / BREAKDOWN). */
+size_t rsk_minres_workspace_bytes(rsk_handle h, int nshift, int max_local_dim);
+rsk_status rsk_minres_recycled_batch(rsk_handle h, const rsk_cg_desc* d, rsk_cg_out* o, void* ws,
+                                     size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------------------ support calls */
 
 /* rsk_make_rhs: d = C x_true + nu ||C x_true|| xi/||xi|| (eq:forward P:107,

@@ -22,6 +22,7 @@ import math
 import numpy as np
 
 from . import defcg as dcg
+from . import minres as mr
 from . import operators as ops
 from . import recycle as rc
 
@@ -149,8 +150,12 @@ def outer_step(cfg, h, b, d, gamma, st: StepState, shifts=None) -> StepResult:
                 overhead += 1
                 cols_U.append(gh[:, None]); cols_Z.append(zg[:, None]); n_carry = 1
         U = np.column_stack(cols_U); Z = np.column_stack(cols_Z)
-        res = dcg.defcg(A_g(gamma[l]), b, x_p=xp, U=U, Z=Z, tol=cfg.tol,
-                        maxit=cfg.maxit, n_carry=n_carry)
+        if getattr(cfg, "inner", "cg") == "minres":    # the paper's inner solver (f2(ii))
+            res = mr.recycled_minres(A_g(gamma[l]), b, x0=xp, Ut=U, Z=Z, tol=cfg.tol,
+                                     maxit=cfg.maxit, n_carry=n_carry)
+        else:
+            res = dcg.defcg(A_g(gamma[l]), b, x_p=xp, U=U, Z=Z, tol=cfg.tol,
+                            maxit=cfg.maxit, n_carry=n_carry)
         X[:, l] = res.x
         Xp[:, l] = 0.0 if xp is None else xp
         G[:, l] = res.x - Xp[:, l]

@@ -89,6 +89,9 @@ _SIGS = {
     "rsk_cg_workspace_bytes": (C.c_size_t, [C.c_void_p, C.c_int, C.c_int]),
     "rsk_cg_recycled_batch": (C.c_int, [C.c_void_p, C.POINTER(CgDesc), C.POINTER(CgOut), _dp,
                                         C.c_size_t, C.c_void_p]),
+    "rsk_minres_workspace_bytes": (C.c_size_t, [C.c_void_p, C.c_int, C.c_int]),
+    "rsk_minres_recycled_batch": (C.c_int, [C.c_void_p, C.POINTER(CgDesc), C.POINTER(CgOut), _dp,
+                                            C.c_size_t, C.c_void_p]),
     "rsk_make_rhs": (C.c_int, [C.c_void_p, _dp, _dp, C.c_double, _dp, _dp, C.c_void_p]),
     "rsk_batch_dot": (C.c_int, [C.c_void_p, _i64, C.c_int, _dp, _i64, _dp, _i64, _dp, C.c_void_p]),
     "rsk_batch_axpby": (C.c_int, [C.c_void_p, _i64, C.c_int, _hp, _dp, _i64, _hp, _dp, _i64,

@@ -1,0 +1,747 @@
+// Recycling MINRES batched over shifts: the paper's own inner solver (SURVEY §8(f)
+// f2(ii); PAPER.md §"Shift Specific Recycling" P:454-534). See include/rsk.h
+// (rsk_minres_recycled_batch) for the contract.
+//
+// Per shift l, with U~_l = [W_g, g-hat_l] and Z_l = (A + gamma_l E) U~_l =
+// [AW_g + gamma_l EW_g, ZGhat_l] (no applies):
+//   eq:localU   Z_l = K_l R_l (shifted Cholesky QR3, K_l^T K_l = I, R_l upper)
+//   start       r = b - A_g x_0 ; c0 = K^T r ; v_1 = (I - K K^T) r / xi
+//   Lanczos     w = A_g v_j (fused apply, alpha_j = v_j . w from its epilogue);
+//               c_j = K^T w ; w <- w - K c_j - alpha_j v_j - beta_j v_{j-1};
+//               beta_{j+1} = ||w|| ; v_{j+1} = w / beta_{j+1}
+//   eq:minShift the y-block min || xi e_1 - T_m y || by Givens rotations (Paige-Saunders
+//               MINRES), the Krylov part y_m = V_m y by short recurrences of the
+//               directions d_j; K^T A_g y_m is carried with the same recurrence from
+//               the c_j, so the first block row needs no extra apply
+//   eq:xFinal   x = x_0 + y_m + U~ R^-1 (c0 - K^T A_g y_m)
+//   confirm     true residual b - A_g x (restart from x if it fails; reading G14)
+// The iteration count is the number of Lanczos applies, as in the oracle
+// (oracle/minres.py). All reductions are fixed-order (CTA partials summed in chunk
+// order by the last CTA of a ticket), so a shift's arithmetic depends only on N.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "rsk_internal.h"
+
+namespace rsk {
+namespace {
+
+constexpr int kMrK = RSK_MAX_LOCAL;   // local columns per shift (|J| + 1 <= 17)
+constexpr int kMrRows = 2048;         // rows per CTA chunk (independent of the batch)
+constexpr int kMrT = 256;
+
+struct MrDev {
+  int64_t N;
+  int ns;
+  double* V;    // v_j          N x ns
+  double* Vp;   // v_{j-1}
+  double* Wv;   // A_g v_j, projected in place
+  double* D1;   // d_{j-1}
+  double* D2;   // d_{j-2}
+  double* Y;    // y_m = V_m y
+  double* R0;   // residual of the (re)start point x_0
+  double* Kb;   // K_s at Kb + s * kMrK * N (ld N)
+  const double* gam;
+  const double* alpha;   // v_j . A_g v_j (apply epilogue), per shift
+  double* c;     // [ns][kMrK]  K^T A_g v_j
+  double* c0;    // [ns][kMrK]  K^T r at the (re)start
+  double* kd1;   // [ns][kMrK]  K^T A_g d_{j-1}
+  double* kd2;   // [ns][kMrK]
+  double* kay;   // [ns][kMrK]  K^T A_g y_m
+  double* tt;    // [ns][kMrK]  R^-1 (c0 - kay) for eq:xFinal
+  double* sc;    // [ns][16] MINRES scalars
+  double* part;  // [ns][nchunk][kMrK + 1]
+  double* rt2;   // [ns] ||b - A_g x||^2 after a confirm
+  int* m;        // [ns] local dimension
+  int* status;
+  int* iters;
+  int* tag;      // iteration tag of the last processed Lanczos step
+  unsigned* cnt; // [ns][4] tickets
+  const double* b;
+  double* X; int64_t ldx;
+  const double* W[RSK_MAX_GROUPS];
+  int J[RSK_MAX_GROUPS];
+  int64_t ldw;
+  const double* Ghat; int64_t ldgh;
+  int* group;
+  int* hasg;
+  int nchunk;
+  double tolb;   // tol * ||b||
+  int maxit;
+};
+
+// MINRES scalars (index into sc[s*16 + .])
+enum { S_BETA = 0, S_EPS, S_DBAR, S_CS, S_SN, S_PHIBAR, S_OLDEPS, S_DELTA, S_DENOM, S_PHI, S_INVB, S_XI };
+
+__device__ __forceinline__ double wsum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Sum v over the CTA (fixed tree); result valid in thread 0.
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  v = wsum(v);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[wid] = v;
+  __syncthreads();
+  double t = 0.0;
+  if (threadIdx.x == 0)
+    for (int w = 0; w < kMrT / 32; ++w) t += sh[w];
+  return t;
+}
+
+__device__ __forceinline__ bool last_cta(unsigned* c, int nchunk) {
+  __shared__ unsigned ticket;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    ticket = atomicAdd(c, 1u);
+  }
+  __syncthreads();
+  const bool last = ticket == (unsigned)(nchunk - 1);
+  if (last) {
+    __threadfence();
+    if (threadIdx.x == 0) *c = 0u;
+  }
+  return last;
+}
+
+// c[s] = K_s^T src_s (src = Wv in the loop, R0 at a start), fixed-order reduction.
+__global__ void __launch_bounds__(kMrT) mr_kdots(MrDev* __restrict__ g, const int* __restrict__ list, int start) {
+  const int s = list[blockIdx.y];
+  if (!start && g->status[s] != ST_ACTIVE) return;
+  const int m = g->m[s];
+  if (m == 0) return;
+  const int64_t N = g->N;
+  const int chunk = blockIdx.x;
+  const int64_t r0 = (int64_t)chunk * kMrRows, r1 = min(N, r0 + kMrRows);
+  const double* src = (start ? g->R0 : g->Wv) + (int64_t)s * N;
+  const double* K = g->Kb + (int64_t)s * kMrK * N;
+  double acc[kMrK];
+#pragma unroll
+  for (int j = 0; j < kMrK; ++j) acc[j] = 0.0;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += kMrT) {
+    const double w = src[i];
+#pragma unroll
+    for (int j = 0; j < kMrK; ++j)
+      if (j < m) acc[j] = fma(K[(int64_t)j * N + i], w, acc[j]);
+  }
+  __shared__ double sh[kMrT / 32];
+  double* part = g->part + ((int64_t)s * g->nchunk + chunk) * (kMrK + 1);
+#pragma unroll
+  for (int j = 0; j < kMrK; ++j) {
+    if (j < m) {
+      const double t = block_sum(acc[j], sh);
+      if (threadIdx.x == 0) part[j] = t;
+    }
+  }
+  if (!last_cta(&g->cnt[s * 4 + 0], g->nchunk)) return;
+  if (threadIdx.x < m) {
+    double t = 0.0;
+    for (int c = 0; c < g->nchunk; ++c) t += g->part[((int64_t)s * g->nchunk + c) * (kMrK + 1) + threadIdx.x];
+    (start ? g->c0 : g->c)[s * kMrK + threadIdx.x] = t;
+  }
+}
+
+// Lanczos step: w <- w - K c - alpha v - beta v_prev ; beta' = ||w||; the last CTA of a
+// shift updates the Givens QR of T_m (Paige-Saunders) and the status.
+__global__ void __launch_bounds__(kMrT) mr_project(MrDev* __restrict__ g, const int* __restrict__ list, int tag) {
+  const int s = list[blockIdx.y];
+  if (g->status[s] != ST_ACTIVE) return;
+  const int m = g->m[s];
+  const int64_t N = g->N;
+  const int chunk = blockIdx.x;
+  const int64_t r0 = (int64_t)chunk * kMrRows, r1 = min(N, r0 + kMrRows);
+  __shared__ double cs_[kMrK];
+  if (threadIdx.x < kMrK) cs_[threadIdx.x] = threadIdx.x < m ? g->c[s * kMrK + threadIdx.x] : 0.0;
+  __syncthreads();
+  const double alpha = g->alpha[s];
+  const double beta = g->sc[s * 16 + S_BETA];
+  const double* K = g->Kb + (int64_t)s * kMrK * N;
+  double* w = g->Wv + (int64_t)s * N;
+  const double* v = g->V + (int64_t)s * N;
+  const double* vp = g->Vp + (int64_t)s * N;
+  double nrm = 0.0;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += kMrT) {
+    double t = w[i];
+#pragma unroll
+    for (int j = 0; j < kMrK; ++j)
+      if (j < m) t = fma(-cs_[j], K[(int64_t)j * N + i], t);
+    t = fma(-alpha, v[i], t);
+    t = fma(-beta, vp[i], t);
+    w[i] = t;
+    nrm = fma(t, t, nrm);
+  }
+  __shared__ double sh[kMrT / 32];
+  const double tot = block_sum(nrm, sh);
+  double* part = g->part + ((int64_t)s * g->nchunk + chunk) * (kMrK + 1);
+  if (threadIdx.x == 0) part[kMrK] = tot;
+  if (!last_cta(&g->cnt[s * 4 + 1], g->nchunk)) return;
+  if (threadIdx.x != 0) return;
+  double n2 = 0.0;
+  for (int c = 0; c < g->nchunk; ++c) n2 += g->part[((int64_t)s * g->nchunk + c) * (kMrK + 1) + kMrK];
+  double* sc = g->sc + s * 16;
+  const double bn = sqrt(n2);
+  const double oldeps = sc[S_EPS];
+  const double cs = sc[S_CS], sn = sc[S_SN], dbar = sc[S_DBAR];
+  const double delta = cs * dbar + sn * alpha;
+  const double gbar = sn * dbar - cs * alpha;
+  const double epsln = sn * bn;
+  const double dbar2 = -cs * bn;
+  double gm = sqrt(gbar * gbar + bn * bn);
+  if (gm < 2.2250738585072014e-308) gm = 2.2250738585072014e-308;
+  const double cs2 = gbar / gm, sn2 = bn / gm;
+  const double phi = cs2 * sc[S_PHIBAR];
+  const double phibar = sn2 * sc[S_PHIBAR];
+  const double denom = 1.0 / gm;
+  // K^T A_g d_j = (c_j - oldeps K^T A_g d_{j-2} - delta K^T A_g d_{j-1}) / gamma_j
+  for (int j = 0; j < m; ++j) {
+    const int q = s * kMrK + j;
+    const double kd = (g->c[q] - oldeps * g->kd2[q] - delta * g->kd1[q]) * denom;
+    g->kay[q] = fma(phi, kd, g->kay[q]);
+    g->kd2[q] = g->kd1[q];
+    g->kd1[q] = kd;
+  }
+  sc[S_OLDEPS] = oldeps;
+  sc[S_DELTA] = delta;
+  sc[S_DENOM] = denom;
+  sc[S_PHI] = phi;
+  sc[S_INVB] = bn > 0.0 ? 1.0 / bn : 0.0;
+  sc[S_EPS] = epsln;
+  sc[S_DBAR] = dbar2;
+  sc[S_CS] = cs2;
+  sc[S_SN] = sn2;
+  sc[S_PHIBAR] = phibar;
+  sc[S_BETA] = bn;
+  const int it = g->iters[s] + 1;
+  g->iters[s] = it;
+  g->tag[s] = tag;
+  if (!isfinite(bn) || !isfinite(phibar) || !isfinite(alpha)) g->status[s] = ST_BREAKDOWN;
+  else if (fabs(phibar) <= g->tolb || bn == 0.0) g->status[s] = ST_RCONV;
+  else if (it >= g->maxit) g->status[s] = ST_MAXIT;
+}
+
+// d_j = (v_j - oldeps d_{j-2} - delta d_{j-1}) / gamma_j ; y += phi d_j ;
+// v_{j-1} <- v_j ; v_{j+1} = w / beta_{j+1}
+__global__ void __launch_bounds__(kMrT) mr_vec(MrDev* __restrict__ g, const int* __restrict__ list, int tag) {
+  const int s = list[blockIdx.y];
+  if (g->tag[s] != tag) return;
+  const int64_t N = g->N;
+  const int64_t r0 = (int64_t)blockIdx.x * kMrRows, r1 = min(N, r0 + kMrRows);
+  const double* sc = g->sc + s * 16;
+  const double oldeps = sc[S_OLDEPS], delta = sc[S_DELTA], denom = sc[S_DENOM], phi = sc[S_PHI],
+               invb = sc[S_INVB];
+  const int64_t o = (int64_t)s * N;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += kMrT) {
+    const double v = g->V[o + i];
+    const double d1 = g->D1[o + i], d2 = g->D2[o + i];
+    const double dn = (v - oldeps * d2 - delta * d1) * denom;
+    g->Y[o + i] = fma(phi, dn, g->Y[o + i]);
+    g->D2[o + i] = d1;
+    g->D1[o + i] = dn;
+    g->Vp[o + i] = v;
+    g->V[o + i] = g->Wv[o + i] * invb;
+  }
+}
+
+// start: V = R0 - K c0, xi^2 = ||V||^2; the last CTA initialises the MINRES scalars.
+__global__ void __launch_bounds__(kMrT) mr_start_proj(MrDev* __restrict__ g, const int* __restrict__ list) {
+  const int s = list[blockIdx.y];
+  const int m = g->m[s];
+  const int64_t N = g->N;
+  const int chunk = blockIdx.x;
+  const int64_t r0 = (int64_t)chunk * kMrRows, r1 = min(N, r0 + kMrRows);
+  __shared__ double cs_[kMrK];
+  if (threadIdx.x < kMrK) cs_[threadIdx.x] = threadIdx.x < m ? g->c0[s * kMrK + threadIdx.x] : 0.0;
+  __syncthreads();
+  const double* K = g->Kb + (int64_t)s * kMrK * N;
+  const double* r = g->R0 + (int64_t)s * N;
+  double* v = g->V + (int64_t)s * N;
+  double nrm = 0.0;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += kMrT) {
+    double t = r[i];
+#pragma unroll
+    for (int j = 0; j < kMrK; ++j)
+      if (j < m) t = fma(-cs_[j], K[(int64_t)j * N + i], t);
+    v[i] = t;
+    nrm = fma(t, t, nrm);
+  }
+  __shared__ double sh[kMrT / 32];
+  const double tot = block_sum(nrm, sh);
+  double* part = g->part + ((int64_t)s * g->nchunk + chunk) * (kMrK + 1);
+  if (threadIdx.x == 0) part[kMrK] = tot;
+  if (!last_cta(&g->cnt[s * 4 + 1], g->nchunk)) return;
+  if (threadIdx.x == 0) {
+    double n2 = 0.0;
+    for (int c = 0; c < g->nchunk; ++c) n2 += g->part[((int64_t)s * g->nchunk + c) * (kMrK + 1) + kMrK];
+    const double xi = sqrt(n2);
+    double* sc = g->sc + s * 16;
+    sc[S_BETA] = 0.0;       // beta_1 multiplies v_0 = 0
+    sc[S_EPS] = 0.0;
+    sc[S_DBAR] = 0.0;
+    sc[S_CS] = -1.0;
+    sc[S_SN] = 0.0;
+    sc[S_PHIBAR] = xi;
+    sc[S_XI] = xi;
+    sc[S_INVB] = xi > 0.0 ? 1.0 / xi : 0.0;
+    g->status[s] = (xi > 0.0 && isfinite(xi)) ? ST_ACTIVE : (isfinite(xi) ? ST_RCONV : ST_BREAKDOWN);
+    if (xi <= g->tolb && xi > 0.0) g->status[s] = ST_RCONV;   // x_0 + U K^T r already converged
+  }
+  if (threadIdx.x < kMrK) {
+    const int q = s * kMrK + threadIdx.x;
+    g->kd1[q] = 0.0; g->kd2[q] = 0.0; g->kay[q] = 0.0;
+  }
+}
+
+// start (after mr_start_proj): v_1 = V / xi ; v_0 = d = y = 0
+__global__ void __launch_bounds__(kMrT) mr_start_vec(MrDev* __restrict__ g, const int* __restrict__ list) {
+  const int s = list[blockIdx.y];
+  const int64_t N = g->N;
+  const int64_t r0 = (int64_t)blockIdx.x * kMrRows, r1 = min(N, r0 + kMrRows);
+  const double invb = g->sc[s * 16 + S_INVB];
+  const int64_t o = (int64_t)s * N;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += kMrT) {
+    g->V[o + i] *= invb;
+    g->Vp[o + i] = 0.0; g->D1[o + i] = 0.0; g->D2[o + i] = 0.0; g->Y[o + i] = 0.0;
+  }
+}
+
+// eq:xFinal: x += y_m + U~ t, t = R^-1 (c0 - K^T A y_m) (host triangular solve)
+__global__ void __launch_bounds__(kMrT) mr_final(MrDev* __restrict__ g, const int* __restrict__ list) {
+  const int s = list[blockIdx.y];
+  const int m = g->m[s];
+  const int64_t N = g->N;
+  const int64_t r0 = (int64_t)blockIdx.x * kMrRows, r1 = min(N, r0 + kMrRows);
+  const int gi = g->group[s];
+  const int J = m > 0 ? min(g->J[gi], m) : 0;
+  const bool hg = m > J;
+  const double* W = J > 0 ? g->W[gi] : nullptr;
+  const double* gh = hg ? g->Ghat + (int64_t)s * g->ldgh : nullptr;
+  __shared__ double t[kMrK];
+  if (threadIdx.x < kMrK) t[threadIdx.x] = threadIdx.x < m ? g->tt[s * kMrK + threadIdx.x] : 0.0;
+  __syncthreads();
+  double* x = g->X + (int64_t)s * g->ldx;
+  const double* y = g->Y + (int64_t)s * N;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += kMrT) {
+    double a = x[i] + y[i];
+    for (int j = 0; j < J; ++j) a = fma(t[j], W[(int64_t)j * g->ldw + i], a);
+    if (hg) a = fma(t[J], gh[i], a);
+    x[i] = a;
+  }
+}
+
+// R0 = b - R0 (R0 held A_g x) and ||R0||^2 -> rt2[s]
+__global__ void __launch_bounds__(kMrT) mr_resid(MrDev* __restrict__ g, const int* __restrict__ list) {
+  const int s = list[blockIdx.y];
+  const int64_t N = g->N;
+  const int chunk = blockIdx.x;
+  const int64_t r0 = (int64_t)chunk * kMrRows, r1 = min(N, r0 + kMrRows);
+  double* r = g->R0 + (int64_t)s * N;
+  double nrm = 0.0;
+  for (int64_t i = r0 + threadIdx.x; i < r1; i += kMrT) {
+    const double t = g->b[i] - r[i];
+    r[i] = t;
+    nrm = fma(t, t, nrm);
+  }
+  __shared__ double sh[kMrT / 32];
+  const double tot = block_sum(nrm, sh);
+  if (threadIdx.x == 0) g->part[((int64_t)s * g->nchunk + chunk) * (kMrK + 1) + kMrK] = tot;
+  if (!last_cta(&g->cnt[s * 4 + 2], g->nchunk)) return;
+  if (threadIdx.x == 0) {
+    double n2 = 0.0;
+    for (int c = 0; c < g->nchunk; ++c) n2 += g->part[((int64_t)s * g->nchunk + c) * (kMrK + 1) + kMrK];
+    g->rt2[s] = n2;
+  }
+}
+
+// Z_s = [AW_g + gamma_s EW_g, ZGhat_s] (m columns, ld N)
+__global__ void mr_formz(int64_t N, const double* __restrict__ AW, const double* __restrict__ EW, int64_t ldw,
+                         int J, double gam, const double* __restrict__ zg, double* __restrict__ Z) {
+  const int j = blockIdx.y;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+    Z[(int64_t)j * N + i] = j < J ? fma(gam, EW[(int64_t)j * ldw + i], AW[(int64_t)j * ldw + i]) : zg[i];
+}
+
+__global__ void mr_gout(int64_t N, int ns, const double* __restrict__ X, int64_t ldx, double* __restrict__ G,
+                        int64_t ldg) {
+  const int s = blockIdx.y;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
+    G[(int64_t)s * ldg + i] = X[(int64_t)s * ldx + i] - G[(int64_t)s * ldg + i];
+}
+
+struct MrLayout {
+  size_t vec, kb, zs, dbl, in, cnt, part, list, dev, total;
+  int nchunk;
+};
+
+size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
+
+MrLayout mr_layout(const Handle* h, int ns, int kmax) {
+  MrLayout L{};
+  const int64_t N = h->ny * h->nx;
+  L.nchunk = (int)((N + kMrRows - 1) / kMrRows);
+  size_t o = 0;
+  L.vec = o; o = al(o + sizeof(double) * (size_t)N * ns * 7);
+  L.kb = o; o = al(o + sizeof(double) * (size_t)N * ns * (kmax > 0 ? kMrK : 0));
+  L.zs = o; o = al(o + sizeof(double) * (size_t)N * (kmax > 0 ? kmax : 0));
+  L.dbl = o; o = al(o + sizeof(double) * (size_t)ns * (7 * kMrK + 16 + 2));
+  L.in = o; o = al(o + sizeof(int) * (size_t)ns * 8);
+  L.cnt = o; o = al(o + sizeof(unsigned) * (size_t)ns * 4);
+  L.part = o; o = al(o + sizeof(double) * (size_t)ns * L.nchunk * (kMrK + 1));
+  L.list = o; o = al(o + sizeof(int) * (size_t)ns * 2);
+  L.dev = o; o = al(o + sizeof(MrDev));
+  L.total = o;
+  return L;
+}
+
+inline cudaStream_t S(void* p) { return reinterpret_cast<cudaStream_t>(p); }
+
+}  // namespace
+}  // namespace rsk
+
+using namespace rsk;
+
+struct rsk_handle_s : public Handle {};   // as in rsk.cu
+
+#define MR_ARG(c, msg)            \
+  do {                            \
+    if (!(c)) {                   \
+      h->err = (msg);             \
+      return RSK_EINVAL;          \
+    }                             \
+  } while (0)
+#define MR_CUDA(x)                                                              \
+  do {                                                                          \
+    cudaError_t e_ = (x);                                                       \
+    if (e_ != cudaSuccess) {                                                    \
+      h->err = std::string("rsk_minres_recycled_batch: ") + cudaGetErrorString(e_); \
+      h->sticky = true;                                                         \
+      return RSK_ECUDA;                                                         \
+    }                                                                           \
+  } while (0)
+
+extern "C" size_t rsk_minres_workspace_bytes(rsk_handle h, int nshift, int max_local_dim) {
+  if (!h || nshift <= 0 || max_local_dim < 0 || max_local_dim > RSK_MAX_LOCAL) return 0;
+  return mr_layout(h, nshift, max_local_dim).total;
+}
+
+extern "C" rsk_status rsk_minres_recycled_batch(rsk_handle h, const rsk_cg_desc* d, rsk_cg_out* o, void* ws,
+                                                size_t ws_bytes, void* stream) {
+  if (!h) return RSK_EINVAL;
+  if (h->sticky) return RSK_ECUDA;
+  MR_ARG(d && o, "rsk_minres_recycled_batch: null desc/out");
+  const int ns = d->nshift;
+  const int64_t N = h->ny * h->nx;
+  MR_ARG(ns >= 1, "rsk_minres_recycled_batch: nshift < 1");
+  MR_ARG(d->gamma_h && d->b && d->X && d->ldx >= N, "rsk_minres_recycled_batch: gamma/b/X");
+  MR_ARG(o->iters && o->applies && o->relres_true && o->status && o->m_used, "rsk_minres_recycled_batch: outputs");
+  MR_ARG(d->tol > 0 && std::isfinite(d->tol) && d->maxit >= 1 && d->check_every >= 1,
+         "rsk_minres_recycled_batch: tol/maxit/check_every");
+  MR_ARG(!(d->flags & RSK_CG_STORE_RES), "rsk_minres_recycled_batch: residual store is a CG option");
+  const bool defl = !(d->flags & RSK_CG_NO_DEFLATION) && d->ngroups > 0;
+  MR_ARG(d->ngroups >= 0 && d->ngroups <= RSK_MAX_GROUPS, "rsk_minres_recycled_batch: ngroups");
+  std::vector<int> grp(ns, 0), hasg(ns, 0), m(ns, 0), hasxp(ns, 0);
+  int kmax = 0;
+  const bool anyg = defl && d->has_ghat_h != nullptr;
+  if (defl) {
+    MR_ARG(d->group_of_shift_h && d->ldw >= N, "rsk_minres_recycled_batch: groups");
+    for (int g = 0; g < d->ngroups; ++g)
+      MR_ARG(d->J[g] >= 0 && d->J[g] <= 16 && (d->J[g] == 0 || (d->W[g] && d->AW[g] && d->EW[g])),
+             "rsk_minres_recycled_batch: group block");
+    if (anyg) MR_ARG(d->Ghat && d->ZGhat && d->ldgh >= N, "rsk_minres_recycled_batch: Ghat/ZGhat");
+    for (int s = 0; s < ns; ++s) {
+      MR_ARG(d->group_of_shift_h[s] >= 0 && d->group_of_shift_h[s] < d->ngroups,
+             "rsk_minres_recycled_batch: group index");
+      grp[s] = d->group_of_shift_h[s];
+      hasg[s] = anyg ? (d->has_ghat_h[s] != 0) : 0;
+      m[s] = d->J[grp[s]] + hasg[s];
+      kmax = std::max(kmax, m[s]);
+    }
+  }
+  for (int s = 0; s < ns; ++s) {
+    MR_ARG(std::isfinite(d->gamma_h[s]) && d->gamma_h[s] >= 0, "rsk_minres_recycled_batch: gamma");
+    hasxp[s] = d->has_xp_h ? (d->has_xp_h[s] != 0) : 0;
+  }
+  const MrLayout L = mr_layout(h, ns, kmax);
+  MR_ARG(ws && ws_bytes >= L.total, "rsk_minres_recycled_batch: workspace too small");
+  MR_CUDA(cudaStreamSynchronize(S(stream)));
+  cudaStream_t st = h->cg_stream;
+
+  char* base = static_cast<char*>(ws);
+  MrDev hc{};
+  hc.N = N;
+  hc.ns = ns;
+  double* vec = reinterpret_cast<double*>(base + L.vec);
+  hc.V = vec; hc.Vp = vec + (size_t)N * ns; hc.Wv = vec + 2 * (size_t)N * ns;
+  hc.D1 = vec + 3 * (size_t)N * ns; hc.D2 = vec + 4 * (size_t)N * ns; hc.Y = vec + 5 * (size_t)N * ns;
+  hc.R0 = vec + 6 * (size_t)N * ns;
+  hc.Kb = reinterpret_cast<double*>(base + L.kb);
+  double* Zs = reinterpret_cast<double*>(base + L.zs);
+  double* dbl = reinterpret_cast<double*>(base + L.dbl);
+  double* gam = dbl;
+  double* alpha = dbl + ns;
+  hc.gam = gam; hc.alpha = alpha;
+  hc.c = dbl + 2 * ns;
+  hc.c0 = hc.c + (size_t)ns * kMrK;
+  hc.kd1 = hc.c0 + (size_t)ns * kMrK;
+  hc.kd2 = hc.kd1 + (size_t)ns * kMrK;
+  hc.kay = hc.kd2 + (size_t)ns * kMrK;
+  hc.tt = hc.kay + (size_t)ns * kMrK;
+  hc.sc = hc.tt + (size_t)ns * kMrK;
+  hc.rt2 = hc.sc + (size_t)ns * 16;
+  int* in = reinterpret_cast<int*>(base + L.in);
+  hc.m = in; hc.status = in + ns; hc.iters = in + 2 * ns; hc.tag = in + 3 * ns; hc.group = in + 4 * ns;
+  hc.hasg = in + 5 * ns;
+  hc.cnt = reinterpret_cast<unsigned*>(base + L.cnt);
+  hc.part = reinterpret_cast<double*>(base + L.part);
+  int* dlist = reinterpret_cast<int*>(base + L.list);
+  MrDev* dev = reinterpret_cast<MrDev*>(base + L.dev);
+  hc.b = d->b;
+  hc.X = d->X; hc.ldx = d->ldx;
+  for (int g = 0; g < RSK_MAX_GROUPS; ++g) {
+    hc.W[g] = (defl && g < d->ngroups) ? d->W[g] : nullptr;
+    hc.J[g] = (defl && g < d->ngroups) ? d->J[g] : 0;
+  }
+  hc.ldw = defl ? d->ldw : N;
+  hc.Ghat = anyg ? d->Ghat : nullptr;
+  hc.ldgh = anyg ? d->ldgh : N;
+  hc.nchunk = L.nchunk;
+  hc.maxit = d->maxit;
+
+  // ---- ||b||
+  MR_CUDA(launch_batch_dot(h, N, 1, d->b, N, d->b, N, h->scal + 8, st));
+  double nb2 = 0.0;
+  MR_CUDA(cudaMemcpyAsync(&nb2, h->scal + 8, sizeof(double), cudaMemcpyDeviceToHost, st));
+  MR_CUDA(cudaStreamSynchronize(st));
+  const double nb = std::sqrt(nb2);
+  if (nb == 0.0) {
+    for (int s = 0; s < ns; ++s) {
+      MR_CUDA(cudaMemsetAsync(d->X + (size_t)s * d->ldx, 0, sizeof(double) * N, st));
+      if (d->Gout) MR_CUDA(cudaMemsetAsync(d->Gout + (size_t)s * d->ldg, 0, sizeof(double) * N, st));
+      o->iters[s] = 0; o->applies[s] = 0; o->relres_true[s] = 0.0; o->status[s] = RSK_CG_ZERO_RHS;
+      o->m_used[s] = 0;
+      if (o->store_count) o->store_count[s] = 0;
+    }
+    MR_CUDA(cudaStreamSynchronize(st));
+    return RSK_OK;
+  }
+  hc.tolb = d->tol * nb;
+
+  // ---- eq:localU: Z_s = K_s R_s per shift (no applies), rank-deficient -> drop g-hat, then U~
+  std::vector<std::vector<double>> Rs(ns);
+  std::vector<int> dropped(ns, 0);
+  for (int s = 0; s < ns; ++s) {
+    while (m[s] > 0) {
+      const int g = grp[s];
+      const int J = std::min(d->J[g], m[s]);
+      dim3 gz((unsigned)std::min<int64_t>((N + 255) / 256, 1184), m[s]);
+      count_launch();
+      mr_formz<<<gz, 256, 0, st>>>(N, d->AW[g], d->EW[g], d->ldw, J, d->gamma_h[s],
+                                   (m[s] > J) ? d->ZGhat + (size_t)s * d->ldgh : nullptr, Zs);
+      MR_CUDA(cudaGetLastError());
+      std::vector<double> R((size_t)m[s] * m[s]);
+      double* Ks = hc.Kb + (size_t)s * kMrK * N;
+      rsk_status qs = rsk_qr_tall(h, N, m[s], Zs, N, Ks, N, R.data(), st);
+      if (qs == RSK_ECUDA) return qs;
+      bool ok = qs == RSK_OK;
+      if (ok) {
+        double dmin = 1e300, dmax = 0.0;
+        for (int j = 0; j < m[s]; ++j) {
+          const double a = std::fabs(R[j + (size_t)j * m[s]]);
+          dmin = std::min(dmin, a);
+          dmax = std::max(dmax, a);
+        }
+        ok = std::isfinite(dmax) && dmin > 1e-14 * dmax;
+      }
+      if (ok) { Rs[s] = R; break; }
+      dropped[s] = 1;
+      if (hasg[s] && m[s] == d->J[g] + 1) { hasg[s] = 0; m[s] -= 1; }
+      else m[s] = 0;
+    }
+  }
+
+  // ---- upload per-shift state
+  {
+    std::vector<double> dh((size_t)ns * (7 * kMrK + 16 + 2), 0.0);
+    for (int s = 0; s < ns; ++s) dh[s] = d->gamma_h[s];
+    MR_CUDA(cudaMemcpyAsync(dbl, dh.data(), sizeof(double) * dh.size(), cudaMemcpyHostToDevice, st));
+    std::vector<int> ih((size_t)ns * 8, 0);
+    for (int s = 0; s < ns; ++s) {
+      ih[s] = m[s];
+      ih[ns + s] = ST_IDLE;
+      ih[3 * ns + s] = -1;
+      ih[4 * ns + s] = grp[s];
+      ih[5 * ns + s] = hasg[s];
+    }
+    MR_CUDA(cudaMemcpyAsync(in, ih.data(), sizeof(int) * ih.size(), cudaMemcpyHostToDevice, st));
+    MR_CUDA(cudaMemsetAsync(hc.cnt, 0, sizeof(unsigned) * ns * 4, st));
+    MR_CUDA(cudaMemcpyAsync(dev, &hc, sizeof(MrDev), cudaMemcpyHostToDevice, st));
+  }
+  std::vector<int64_t> applies(ns, 0);
+  std::vector<int> all(ns), withxp;
+  for (int s = 0; s < ns; ++s) {
+    all[s] = s;
+    if (hasxp[s]) withxp.push_back(s);
+  }
+  auto upload = [&](const std::vector<int>& v) -> cudaError_t {
+    return cudaMemcpyAsync(dlist, v.data(), sizeof(int) * v.size(), cudaMemcpyHostToDevice, st);
+  };
+  auto grid = [&](size_t nl) { return dim3((unsigned)L.nchunk, (unsigned)nl); };
+  // apply A_g to the vectors `src` (ld ldsrc) of the shifts in dlist into R0 (or Wv)
+  auto apply_list = [&](const double* src, int64_t ldsrc, double* dst, int nl, double* xdoty) -> cudaError_t {
+    ApplyLaunch a{};
+    a.X = src; a.ldx = ldsrc; a.Y = dst; a.ldy = N; a.gamma = gam; a.list = dlist; a.nlist = nl;
+    a.mode = RSK_APPLY_SHIFTED; a.nvec_total = ns; a.xdoty = xdoty;
+    return launch_apply(h, a, st);
+  };
+
+  // ---- x_0 and r = b - A_g x_0
+  for (int s = 0; s < ns; ++s)
+    if (!hasxp[s]) MR_CUDA(cudaMemsetAsync(d->X + (size_t)s * d->ldx, 0, sizeof(double) * N, st));
+  if (d->Gout)
+    MR_CUDA(cudaMemcpy2DAsync(d->Gout, sizeof(double) * d->ldg, d->X, sizeof(double) * d->ldx,
+                              sizeof(double) * N, ns, cudaMemcpyDeviceToDevice, st));
+  MR_CUDA(cudaMemsetAsync(hc.R0, 0, sizeof(double) * (size_t)N * ns, st));
+  if (!withxp.empty()) {
+    MR_CUDA(upload(withxp));
+    MR_CUDA(apply_list(d->X, d->ldx, hc.R0, (int)withxp.size(), nullptr));
+    for (int s : withxp) applies[s] += 1;
+  }
+  MR_CUDA(upload(all));
+  count_launch();
+  mr_resid<<<grid(ns), kMrT, 0, st>>>(dev, dlist);
+  MR_CUDA(cudaGetLastError());
+
+  auto restart = [&](const std::vector<int>& lst) -> cudaError_t {
+    cudaError_t e = upload(lst);
+    if (e != cudaSuccess) return e;
+    count_launches(3);
+    mr_kdots<<<grid(lst.size()), kMrT, 0, st>>>(dev, dlist, 1);
+    mr_start_proj<<<grid(lst.size()), kMrT, 0, st>>>(dev, dlist);
+    mr_start_vec<<<grid(lst.size()), kMrT, 0, st>>>(dev, dlist);
+    return cudaGetLastError();
+  };
+  MR_CUDA(restart(all));
+
+  std::vector<int> status(ns, ST_ACTIVE), iters(ns, 0), done(ns, 0), final_status(ns, RSK_CG_CONVERGED);
+  std::vector<double> relres(ns, 0.0);
+  std::vector<int> it_restart(ns, -1);   // iterations at the last restart (stagnation guard)
+  int tag = 0;
+  int64_t guard = 0;
+  for (;;) {
+    MR_CUDA(cudaMemcpyAsync(status.data(), hc.status, sizeof(int) * ns, cudaMemcpyDeviceToHost, st));
+    MR_CUDA(cudaMemcpyAsync(iters.data(), hc.iters, sizeof(int) * ns, cudaMemcpyDeviceToHost, st));
+    MR_CUDA(cudaStreamSynchronize(st));
+    std::vector<int> active, fin;
+    for (int s = 0; s < ns; ++s) {
+      if (done[s]) continue;
+      if (status[s] == ST_ACTIVE) active.push_back(s);
+      else fin.push_back(s);
+    }
+    if (!fin.empty()) {
+      // ---- eq:xFinal for the finished shifts, then the true-residual confirmation
+      std::vector<double> c0((size_t)ns * kMrK), kay((size_t)ns * kMrK), tt((size_t)ns * kMrK, 0.0);
+      MR_CUDA(cudaMemcpyAsync(c0.data(), hc.c0, sizeof(double) * c0.size(), cudaMemcpyDeviceToHost, st));
+      MR_CUDA(cudaMemcpyAsync(kay.data(), hc.kay, sizeof(double) * kay.size(), cudaMemcpyDeviceToHost, st));
+      MR_CUDA(cudaStreamSynchronize(st));
+      for (int s : fin) {
+        const int k = m[s];
+        if (k == 0) continue;
+        const std::vector<double>& R = Rs[s];
+        double* t = &tt[(size_t)s * kMrK];
+        for (int j = 0; j < k; ++j) t[j] = c0[(size_t)s * kMrK + j] - kay[(size_t)s * kMrK + j];
+        for (int i = k - 1; i >= 0; --i) {      // R t = c0 - K^T A y_m (upper triangular)
+          double a = t[i];
+          for (int q = i + 1; q < k; ++q) a -= R[i + (size_t)q * k] * t[q];
+          t[i] = a / R[i + (size_t)i * k];
+        }
+      }
+      MR_CUDA(cudaMemcpyAsync(hc.tt, tt.data(), sizeof(double) * tt.size(), cudaMemcpyHostToDevice, st));
+      MR_CUDA(upload(fin));
+      count_launch();
+      mr_final<<<grid(fin.size()), kMrT, 0, st>>>(dev, dlist);
+      MR_CUDA(cudaGetLastError());
+      MR_CUDA(apply_list(d->X, d->ldx, hc.R0, (int)fin.size(), nullptr));
+      count_launch();
+      mr_resid<<<grid(fin.size()), kMrT, 0, st>>>(dev, dlist);
+      MR_CUDA(cudaGetLastError());
+      std::vector<double> rt2(ns);
+      MR_CUDA(cudaMemcpyAsync(rt2.data(), hc.rt2, sizeof(double) * ns, cudaMemcpyDeviceToHost, st));
+      MR_CUDA(cudaStreamSynchronize(st));
+      std::vector<int> again;
+      for (int s : fin) {
+        applies[s] += 1;
+        const double rr = std::sqrt(rt2[s]) / nb;
+        relres[s] = rr;
+        if (rr <= d->tol) {
+          done[s] = 1;
+          final_status[s] = dropped[s] ? RSK_CG_DEFL_DROPPED : RSK_CG_CONVERGED;
+        } else if (status[s] == ST_BREAKDOWN || !std::isfinite(rr)) {
+          done[s] = 1;
+          final_status[s] = RSK_CG_BREAKDOWN;
+        } else if (iters[s] >= d->maxit || it_restart[s] == iters[s]) {
+          done[s] = 1;              // maxit, or a restart that made no Lanczos step
+          final_status[s] = RSK_CG_MAXIT;
+        } else {
+          it_restart[s] = iters[s];
+          again.push_back(s);      // restart from x (x_0 <- x, r = b - A_g x)
+        }
+      }
+      if (!again.empty()) {
+        MR_CUDA(restart(again));
+        for (int s : again) active.push_back(s);
+      }
+    }
+    if (active.empty()) {
+      bool all_done = true;
+      for (int s = 0; s < ns; ++s) all_done = all_done && done[s];
+      if (all_done) break;
+      continue;    // restarted shifts whose x_0 + U K^T r is already converged
+    }
+    // ---- check_every lockstep Lanczos steps over the active shifts
+    MR_CUDA(upload(active));
+    const unsigned nl = (unsigned)active.size();
+    for (int it = 0; it < d->check_every; ++it) {
+      ++tag;
+      MR_CUDA(apply_list(hc.V, N, hc.Wv, (int)nl, alpha));
+      count_launches(3);
+      mr_kdots<<<grid(nl), kMrT, 0, st>>>(dev, dlist, 0);
+      mr_project<<<grid(nl), kMrT, 0, st>>>(dev, dlist, tag);
+      mr_vec<<<grid(nl), kMrT, 0, st>>>(dev, dlist, tag);
+      MR_CUDA(cudaGetLastError());
+    }
+    if (++guard > (int64_t)d->maxit * 4 + 100) {
+      h->err = "rsk_minres_recycled_batch: loop guard";
+      return RSK_ECUDA;
+    }
+  }
+  if (d->Gout) {
+    count_launch();
+    mr_gout<<<dim3((unsigned)std::min<int64_t>((N + 255) / 256, 1184), ns), 256, 0, st>>>(N, ns, d->X, d->ldx,
+                                                                                         d->Gout, d->ldg);
+    MR_CUDA(cudaGetLastError());
+  }
+  MR_CUDA(cudaMemcpyAsync(iters.data(), hc.iters, sizeof(int) * ns, cudaMemcpyDeviceToHost, st));
+  MR_CUDA(cudaStreamSynchronize(st));
+  bool partial = false;
+  for (int s = 0; s < ns; ++s) {
+    o->iters[s] = iters[s];
+    o->applies[s] = applies[s] + iters[s];
+    o->relres_true[s] = relres[s];
+    o->status[s] = final_status[s];
+    o->m_used[s] = m[s];
+    if (o->store_count) o->store_count[s] = 0;
+    partial = partial || (final_status[s] != RSK_CG_CONVERGED && final_status[s] != RSK_CG_DEFL_DROPPED);
+  }
+  int64_t tot = 0;
+  for (int s = 0; s < ns; ++s) tot += o->applies[s];
+  h->nA += tot;   // matvec accounting: each A_g apply = 1 A + 1 E
+  h->nE += tot;
+  return partial ? RSK_EPARTIAL : RSK_OK;
+}

@@ -107,7 +107,10 @@ class GpuSolver:
 
     # ------------------------------------------------------------- building blocks
     def cg(self, gammas_idx, X, has_xp, Gout=None, groups=None, ghat=None, store=None,
-           flags=0, order=None):
+           flags=0, order=None, inner="cg"):
+        """One batched inner solve over the shifts gammas_idx: recycled CG
+        (rsk_cg_recycled_batch) or, with inner="minres", the paper's recycling MINRES
+        (rsk_minres_recycled_batch) on the same descriptor."""
         cfg = self.cfg
         ns = len(gammas_idx)
         gam = np.ascontiguousarray(self.gamma[gammas_idx])
@@ -161,7 +164,14 @@ class GpuSolver:
         out.relres_true = rel.ctypes.data_as(L._hp); out.status = stt.ctypes.data_as(P(L.C.c_int))
         out.m_used = mu.ctypes.data_as(P(L.C.c_int)); out.store_count = sc.ctypes.data_as(P(L.C.c_int))
         out.ms_loop = ms.ctypes.data_as(L._hp)
-        self.h.cg_recycled_batch(d, out, self.ws, stream=self.stream)
+        if inner == "minres":
+            kmax = (max(d.J[g] for g in range(d.ngroups)) + (1 if ghat is not None else 0)) if d.ngroups else 0
+            need = self.h.minres_workspace_bytes(ns, kmax)
+            if getattr(self, "ws_mr", None) is None or self.ws_mr.numel() < need:
+                self.ws_mr = torch.empty(need, dtype=torch.uint8, device=self.dev)
+            self.h.minres_recycled_batch(d, out, self.ws_mr, stream=self.stream)
+        else:
+            self.h.cg_recycled_batch(d, out, self.ws, stream=self.stream)
         return dict(iters=iters, applies=apl, relres=rel, status=stt, m_used=mu, store_count=sc, prof=ms)
 
     def stabilize(self, raw: torch.Tensor, cap: int | None) -> torch.Tensor:
@@ -325,7 +335,8 @@ class GpuSolver:
             order = None
             if prev is not None and len(prev) == M:   # longest-processing-time first
                 order = np.argsort(-np.asarray(prev)[mine], kind="stable")
-            res = self.cg(mine, X, has_xp[mine], Gout=G, groups=groups, ghat=ghat, order=order)
+            res = self.cg(mine, X, has_xp[mine], Gout=G, groups=groups, ghat=ghat, order=order,
+                          inner=getattr(cfg, "inner", "cg"))
             self.h.lcurve_norms(X, self.d, self.rho_dev, self.eta_dev, self.lc_scratch, stream=self.stream)
             rho_l, eta_l = _host(self.rho_dev)[:ml], _host(self.eta_dev)[:ml]
         else:

@@ -141,6 +141,14 @@ class Handle:
                                             ws.numel() * ws.element_size(), _stream(stream))
         return self._check(st, "rsk_cg_recycled_batch", allow=(L.RSK_OK, L.RSK_EPARTIAL))
 
+    def minres_workspace_bytes(self, nshift, max_local_dim) -> int:
+        return int(self.lib.rsk_minres_workspace_bytes(self.h, nshift, max_local_dim))
+
+    def minres_recycled_batch(self, desc: L.CgDesc, out: L.CgOut, ws, stream=None) -> int:
+        st = self.lib.rsk_minres_recycled_batch(self.h, C.byref(desc), C.byref(out), ws.data_ptr(),
+                                                ws.numel() * ws.element_size(), _stream(stream))
+        return self._check(st, "rsk_minres_recycled_batch", allow=(L.RSK_OK, L.RSK_EPARTIAL))
+
     # ------------------------------------------------------------ support calls
     def make_rhs(self, x_true, xi, nu, d, b, stream=None):
         self._check(self.lib.rsk_make_rhs(self.h, _dptr(x_true), _dptr(xi), float(nu), _dptr(d), _dptr(b),

@@ -51,6 +51,8 @@ class Config:
     stop: str = "fixed"        # outer stopping: "fixed" (K_out steps) or "lstar3"
     guess: str = "orth"        # principal guesses: "orth" (eq:orthupdate), "oblique" (one anchor,
                                # eq:obliqueupdate) or "oblique2" (two anchors, eq:updates) -- f2(iii)
+    inner: str = "cg"          # inner solver: "cg" (north_star's recycled CG, reading G1) or
+                               # "minres" (the paper's recycling MINRES, eq:minShift) -- f2(ii)
 
     @property
     def N(self) -> int:

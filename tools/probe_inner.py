@@ -1,0 +1,61 @@
+"""Recycled CG (north_star) vs the paper's recycling MINRES (SURVEY §8(f) f2(ii),
+eq:minShift P:511-534) as the inner solver of the same nested solve: per outer step the
+iterations (Lanczos / CG applies), all A_g applies, wall time of the step, and for the
+MINRES batch the per-shift-iteration cost. One JSON line per (solver, outer step) and a
+summary line per solver.
+
+  python tools/probe_inner.py --config C2 --outer 5 [--rule irn|gazzola]"""
+import argparse
+import dataclasses
+import json
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import rsk_synth as S  # noqa: E402
+from paper_2306_15049_b200.pipeline import GpuSolver  # noqa: E402
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--outer", type=int, default=5)
+    ap.add_argument("--rule", default="irn")
+    ap.add_argument("--inners", default="cg,minres")
+    ap.add_argument("--repeat", type=int, default=2)
+    a = ap.parse_args()
+    dev = torch.device("cuda", 0)
+    for inner in a.inners.split(","):
+        cfg = dataclasses.replace(S.CONFIGS[a.config], inner=inner, weight_rule=a.rule)
+        inp = S.make_inputs(cfg)
+        sol = GpuSolver(cfg, inp["psf"], inp["gamma"])
+        sol.set_data(torch.from_numpy(inp["x_true"]).to(dev), torch.from_numpy(inp["xi"]).to(dev))
+        best = None
+        for rep in range(a.repeat):             # first pass warms up (module load, workspaces)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            outs = sol.run(K_out=a.outer)
+            torch.cuda.synchronize()
+            dt = time.perf_counter() - t0
+            if best is None or dt < best[0]:
+                best = (dt, outs)
+        dt, outs = best
+        for o in outs:
+            print(json.dumps(dict(config=a.config, rule=a.rule, inner=inner, k=o.k,
+                                  iters_total=int(o.iters.sum()), iters_max=int(o.iters.max()),
+                                  applies_total=int(o.applies.sum()) + int(o.overhead_applies),
+                                  status=sorted(set(int(s) for s in o.status)), lstar=int(o.lstar),
+                                  ms=round(o.ms * 1e3, 2))), flush=True)
+        its = sum(int(o.iters.sum()) for o in outs)
+        print(json.dumps(dict(config=a.config, rule=a.rule, inner=inner, summary=True,
+                              nested_solve_ms=round(dt * 1e3, 1), iterations=its,
+                              lstar=[int(o.lstar) for o in outs],
+                              us_per_shift_iteration=round(dt * 1e6 / its, 3))), flush=True)
+
+
+if __name__ == "__main__":
+    main()
