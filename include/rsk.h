@@ -227,6 +227,9 @@ typedef struct {
                                 /* in which the device loop starts the shifts    */
                                 /* (longest first shortens the makespan; results */
                                 /* do not depend on it)                          */
+  const double* Ghat2;          /* second carried column per shift (Alg. 3's     */
+  const double* ZGhat2;         /*   g^(k,l-1); ld ldgh) and its image;   */
+  const int* has_ghat2_h;       /*   rsk_minres_recycled_batch only (NULL here)  */
 } rsk_cg_desc;
 
 typedef struct {                /* host arrays [nshift], filled on return        */
@@ -253,9 +256,11 @@ rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, rsk_cg_out*
  * OWN inner solver (PAPER.md §"Shift Specific Recycling" P:454-534; SURVEY §8(f)
  * f2(ii)), an alternative to the deflated CG above on the same descriptor. Per
  * shift l, with U~_l = [W_g, ghat_l] and Z_l = (A + gamma_l E) U~_l =
- * [AW_g + gamma_l EW_g, ZGhat_l] (no applies):
+ * [AW_g + gamma_l EW_g, ZGhat_l] (no applies) -- with has_ghat2_h also
+ * the second carried column of Alg. 3 / Alg. 4 (U~_l = [W, g^(k-1,l), g^(k,l-1)],
+ * Ghat2 / ZGhat2):
  *   eq:localU    Z_l = K_l R_l, K_l^T K_l = I (shifted Cholesky QR3; R_l singular
- *                to 1e-14 relative -> drop ghat, then U~: DEFL_DROPPED)
+ *                to 1e-14 relative -> drop the carried columns, then U~: DEFL_DROPPED)
  *   eq:corr_g    r = b - A_g x_p (one apply when has_xp), solve for g = x - x_p
  *   eq:minShift  Lanczos on (I - K K^T) A_g from (I - K K^T) r, the y-block
  *                least squares by Givens rotations (MINRES), the z-block exactly

@@ -136,6 +136,7 @@ def outer_step(cfg, h, b, d, gamma, st: StepState, shifts=None) -> StepResult:
     status = np.zeros(M, dtype=np.int64); relres = np.zeros(M); grel = np.zeros(M)
     nb = np.linalg.norm(b)
     todo = range(M) if shifts is None else shifts
+    seq = getattr(cfg, "local", "d3") == "seq"
     for l in todo:
         W, AW, EW = groups["L" if (l + 1) <= cfg.I_split else "R"]
         xp = guess(l)
@@ -149,6 +150,16 @@ def outer_step(cfg, h, b, d, gamma, st: StepState, shifts=None) -> StepResult:
                 zg = (ops.apply_A(h, img) + gamma[l] * ops.apply_E(wx, wy, img)).ravel()
                 overhead += 1
                 cols_U.append(gh[:, None]); cols_Z.append(zg[:, None]); n_carry = 1
+        if seq and l >= 1 and _same_group(cfg, l - 1, l) and (shifts is None or (l - 1) in todo):
+            # Alg. 3 / Alg. 4: U~_l = [W, g^(k-1,l), g^(k,l-1)], the second
+            # correction orthogonalised against [W, g-hat] and dropped when nearly
+            # redundant (footnote P:691; reading G35)
+            gh2 = rc.carried_direction(np.column_stack(cols_U), G[:, l - 1])
+            if gh2 is not None:
+                img = gh2.reshape(n, n)
+                zg = (ops.apply_A(h, img) + gamma[l] * ops.apply_E(wx, wy, img)).ravel()
+                overhead += 1
+                cols_U.append(gh2[:, None]); cols_Z.append(zg[:, None]); n_carry += 1
         U = np.column_stack(cols_U); Z = np.column_stack(cols_Z)
         if getattr(cfg, "inner", "cg") == "minres":    # the paper's inner solver (f2(ii))
             res = mr.recycled_minres(A_g(gamma[l]), b, x0=xp, Ut=U, Z=Z, tol=cfg.tol,
@@ -171,6 +182,11 @@ def outer_step(cfg, h, b, d, gamma, st: StepState, shifts=None) -> StepResult:
     lstar = lcurve_corner(rho, eta)[0] if shifts is None else -1
     return StepResult(X, G, Xp, iters, applies, status, relres, grel, Ut.shape[1], lstar,
                       rho, eta, overhead, V_i1, Ut, an)
+
+
+def _same_group(cfg, a, b):
+    """Shifts a, b (0-based) in the same group (left: l <= I, right: l > I; Alg. 4)."""
+    return ((a + 1) <= cfg.I_split) == ((b + 1) <= cfg.I_split)
 
 
 def next_weights(cfg, st_w, xstar):

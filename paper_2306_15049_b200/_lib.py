@@ -53,6 +53,9 @@ class CgDesc(C.Structure):
         ("lds", _i64),
         ("store_cap", C.c_int),
         ("order_h", C.POINTER(C.c_int)),
+        ("Ghat2", _dp),
+        ("ZGhat2", _dp),
+        ("has_ghat2_h", C.POINTER(C.c_int)),
     ]
 
 

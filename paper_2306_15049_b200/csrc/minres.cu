@@ -20,6 +20,7 @@
 // order by the last CTA of a ticket), so a shift's arithmetic depends only on N.
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <vector>
 
@@ -31,7 +32,7 @@ namespace rsk {
 namespace {
 
 constexpr int kMrK = RSK_MAX_LOCAL;   // local columns per shift (|J| + 1 <= 17)
-constexpr int kMrRows = 2048;         // rows per CTA chunk (independent of the batch)
+constexpr int kMrRows = 512;          // rows per CTA chunk (independent of the batch)
 constexpr int kMrT = 256;
 
 struct MrDev {
@@ -59,7 +60,7 @@ struct MrDev {
   int* m;        // [ns] local dimension
   int* status;
   int* iters;
-  int* tag;      // iteration tag of the last processed Lanczos step
+  int* go;       // 1: mr_project took this iteration's Lanczos step (reset by mr_kdots)
   unsigned* cnt; // [ns][4] tickets
   const double* b;
   double* X; int64_t ldx;
@@ -67,8 +68,10 @@ struct MrDev {
   int J[RSK_MAX_GROUPS];
   int64_t ldw;
   const double* Ghat; int64_t ldgh;
+  const double* Ghat2;
   int* group;
   int* hasg;
+  int* hasg2;
   int nchunk;
   double tolb;   // tol * ||b||
   int maxit;
@@ -112,9 +115,18 @@ __device__ __forceinline__ bool last_cta(unsigned* c, int nchunk) {
   return last;
 }
 
+// Fixed-order sum of the chunk partials of column j of shift s (thread t takes chunks
+// t, t + kMrT, ... in order, then the fixed CTA tree); valid in thread 0.
+__device__ __forceinline__ double chunk_sum(const MrDev* g, int s, int j, double* sh) {
+  double t = 0.0;
+  for (int c = threadIdx.x; c < g->nchunk; c += kMrT) t += g->part[((int64_t)s * g->nchunk + c) * (kMrK + 1) + j];
+  return block_sum(t, sh);
+}
+
 // c[s] = K_s^T src_s (src = Wv in the loop, R0 at a start), fixed-order reduction.
 __global__ void __launch_bounds__(kMrT) mr_kdots(MrDev* __restrict__ g, const int* __restrict__ list, int start) {
   const int s = list[blockIdx.y];
+  if (blockIdx.x == 0 && threadIdx.x == 0) g->go[s] = 0;   // mr_project sets it when it steps s
   if (!start && g->status[s] != ST_ACTIVE) return;
   const int m = g->m[s];
   if (m == 0) return;
@@ -142,16 +154,15 @@ __global__ void __launch_bounds__(kMrT) mr_kdots(MrDev* __restrict__ g, const in
     }
   }
   if (!last_cta(&g->cnt[s * 4 + 0], g->nchunk)) return;
-  if (threadIdx.x < m) {
-    double t = 0.0;
-    for (int c = 0; c < g->nchunk; ++c) t += g->part[((int64_t)s * g->nchunk + c) * (kMrK + 1) + threadIdx.x];
-    (start ? g->c0 : g->c)[s * kMrK + threadIdx.x] = t;
+  for (int j = 0; j < m; ++j) {
+    const double t = chunk_sum(g, s, j, sh);
+    if (threadIdx.x == 0) (start ? g->c0 : g->c)[s * kMrK + j] = t;
   }
 }
 
 // Lanczos step: w <- w - K c - alpha v - beta v_prev ; beta' = ||w||; the last CTA of a
 // shift updates the Givens QR of T_m (Paige-Saunders) and the status.
-__global__ void __launch_bounds__(kMrT) mr_project(MrDev* __restrict__ g, const int* __restrict__ list, int tag) {
+__global__ void __launch_bounds__(kMrT) mr_project(MrDev* __restrict__ g, const int* __restrict__ list) {
   const int s = list[blockIdx.y];
   if (g->status[s] != ST_ACTIVE) return;
   const int m = g->m[s];
@@ -183,9 +194,8 @@ __global__ void __launch_bounds__(kMrT) mr_project(MrDev* __restrict__ g, const 
   double* part = g->part + ((int64_t)s * g->nchunk + chunk) * (kMrK + 1);
   if (threadIdx.x == 0) part[kMrK] = tot;
   if (!last_cta(&g->cnt[s * 4 + 1], g->nchunk)) return;
+  const double n2 = chunk_sum(g, s, kMrK, sh);
   if (threadIdx.x != 0) return;
-  double n2 = 0.0;
-  for (int c = 0; c < g->nchunk; ++c) n2 += g->part[((int64_t)s * g->nchunk + c) * (kMrK + 1) + kMrK];
   double* sc = g->sc + s * 16;
   const double bn = sqrt(n2);
   const double oldeps = sc[S_EPS];
@@ -221,7 +231,7 @@ __global__ void __launch_bounds__(kMrT) mr_project(MrDev* __restrict__ g, const 
   sc[S_BETA] = bn;
   const int it = g->iters[s] + 1;
   g->iters[s] = it;
-  g->tag[s] = tag;
+  g->go[s] = 1;
   if (!isfinite(bn) || !isfinite(phibar) || !isfinite(alpha)) g->status[s] = ST_BREAKDOWN;
   else if (fabs(phibar) <= g->tolb || bn == 0.0) g->status[s] = ST_RCONV;
   else if (it >= g->maxit) g->status[s] = ST_MAXIT;
@@ -229,9 +239,9 @@ __global__ void __launch_bounds__(kMrT) mr_project(MrDev* __restrict__ g, const 
 
 // d_j = (v_j - oldeps d_{j-2} - delta d_{j-1}) / gamma_j ; y += phi d_j ;
 // v_{j-1} <- v_j ; v_{j+1} = w / beta_{j+1}
-__global__ void __launch_bounds__(kMrT) mr_vec(MrDev* __restrict__ g, const int* __restrict__ list, int tag) {
+__global__ void __launch_bounds__(kMrT) mr_vec(MrDev* __restrict__ g, const int* __restrict__ list) {
   const int s = list[blockIdx.y];
-  if (g->tag[s] != tag) return;
+  if (!g->go[s]) return;
   const int64_t N = g->N;
   const int64_t r0 = (int64_t)blockIdx.x * kMrRows, r1 = min(N, r0 + kMrRows);
   const double* sc = g->sc + s * 16;
@@ -277,9 +287,8 @@ __global__ void __launch_bounds__(kMrT) mr_start_proj(MrDev* __restrict__ g, con
   double* part = g->part + ((int64_t)s * g->nchunk + chunk) * (kMrK + 1);
   if (threadIdx.x == 0) part[kMrK] = tot;
   if (!last_cta(&g->cnt[s * 4 + 1], g->nchunk)) return;
+  const double n2 = chunk_sum(g, s, kMrK, sh);
   if (threadIdx.x == 0) {
-    double n2 = 0.0;
-    for (int c = 0; c < g->nchunk; ++c) n2 += g->part[((int64_t)s * g->nchunk + c) * (kMrK + 1) + kMrK];
     const double xi = sqrt(n2);
     double* sc = g->sc + s * 16;
     sc[S_BETA] = 0.0;       // beta_1 multiplies v_0 = 0
@@ -320,9 +329,12 @@ __global__ void __launch_bounds__(kMrT) mr_final(MrDev* __restrict__ g, const in
   const int64_t r0 = (int64_t)blockIdx.x * kMrRows, r1 = min(N, r0 + kMrRows);
   const int gi = g->group[s];
   const int J = m > 0 ? min(g->J[gi], m) : 0;
-  const bool hg = m > J;
+  const bool hg = m > J && g->hasg[s];
+  const bool hg2 = m > J && g->hasg2[s];
   const double* W = J > 0 ? g->W[gi] : nullptr;
   const double* gh = hg ? g->Ghat + (int64_t)s * g->ldgh : nullptr;
+  const double* gh2 = hg2 ? g->Ghat2 + (int64_t)s * g->ldgh : nullptr;
+  const int j2 = J + (hg ? 1 : 0);
   __shared__ double t[kMrK];
   if (threadIdx.x < kMrK) t[threadIdx.x] = threadIdx.x < m ? g->tt[s * kMrK + threadIdx.x] : 0.0;
   __syncthreads();
@@ -332,6 +344,7 @@ __global__ void __launch_bounds__(kMrT) mr_final(MrDev* __restrict__ g, const in
     double a = x[i] + y[i];
     for (int j = 0; j < J; ++j) a = fma(t[j], W[(int64_t)j * g->ldw + i], a);
     if (hg) a = fma(t[J], gh[i], a);
+    if (hg2) a = fma(t[j2], gh2[i], a);
     x[i] = a;
   }
 }
@@ -353,19 +366,18 @@ __global__ void __launch_bounds__(kMrT) mr_resid(MrDev* __restrict__ g, const in
   const double tot = block_sum(nrm, sh);
   if (threadIdx.x == 0) g->part[((int64_t)s * g->nchunk + chunk) * (kMrK + 1) + kMrK] = tot;
   if (!last_cta(&g->cnt[s * 4 + 2], g->nchunk)) return;
-  if (threadIdx.x == 0) {
-    double n2 = 0.0;
-    for (int c = 0; c < g->nchunk; ++c) n2 += g->part[((int64_t)s * g->nchunk + c) * (kMrK + 1) + kMrK];
-    g->rt2[s] = n2;
-  }
+  const double n2 = chunk_sum(g, s, kMrK, sh);
+  if (threadIdx.x == 0) g->rt2[s] = n2;
 }
 
-// Z_s = [AW_g + gamma_s EW_g, ZGhat_s] (m columns, ld N)
+// Z_s = [AW_g + gamma_s EW_g, ZGhat_s, ZGhat2_s] (m columns, ld N; zg / zg2 nullable)
 __global__ void mr_formz(int64_t N, const double* __restrict__ AW, const double* __restrict__ EW, int64_t ldw,
-                         int J, double gam, const double* __restrict__ zg, double* __restrict__ Z) {
+                         int J, double gam, const double* __restrict__ zg, const double* __restrict__ zg2,
+                         double* __restrict__ Z) {
   const int j = blockIdx.y;
+  const double* zc = (j == J && zg) ? zg : zg2;
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x)
-    Z[(int64_t)j * N + i] = j < J ? fma(gam, EW[(int64_t)j * ldw + i], AW[(int64_t)j * ldw + i]) : zg[i];
+    Z[(int64_t)j * N + i] = j < J ? fma(gam, EW[(int64_t)j * ldw + i], AW[(int64_t)j * ldw + i]) : zc[i];
 }
 
 __global__ void mr_gout(int64_t N, int ns, const double* __restrict__ X, int64_t ldx, double* __restrict__ G,
@@ -446,21 +458,25 @@ extern "C" rsk_status rsk_minres_recycled_batch(rsk_handle h, const rsk_cg_desc*
   MR_ARG(!(d->flags & RSK_CG_STORE_RES), "rsk_minres_recycled_batch: residual store is a CG option");
   const bool defl = !(d->flags & RSK_CG_NO_DEFLATION) && d->ngroups > 0;
   MR_ARG(d->ngroups >= 0 && d->ngroups <= RSK_MAX_GROUPS, "rsk_minres_recycled_batch: ngroups");
-  std::vector<int> grp(ns, 0), hasg(ns, 0), m(ns, 0), hasxp(ns, 0);
+  std::vector<int> grp(ns, 0), hasg(ns, 0), hasg2(ns, 0), m(ns, 0), hasxp(ns, 0);
   int kmax = 0;
   const bool anyg = defl && d->has_ghat_h != nullptr;
+  const bool anyg2 = defl && d->has_ghat2_h != nullptr;
   if (defl) {
     MR_ARG(d->group_of_shift_h && d->ldw >= N, "rsk_minres_recycled_batch: groups");
     for (int g = 0; g < d->ngroups; ++g)
       MR_ARG(d->J[g] >= 0 && d->J[g] <= 16 && (d->J[g] == 0 || (d->W[g] && d->AW[g] && d->EW[g])),
              "rsk_minres_recycled_batch: group block");
     if (anyg) MR_ARG(d->Ghat && d->ZGhat && d->ldgh >= N, "rsk_minres_recycled_batch: Ghat/ZGhat");
+    if (anyg2) MR_ARG(d->Ghat2 && d->ZGhat2 && d->ldgh >= N, "rsk_minres_recycled_batch: Ghat2/ZGhat2");
     for (int s = 0; s < ns; ++s) {
       MR_ARG(d->group_of_shift_h[s] >= 0 && d->group_of_shift_h[s] < d->ngroups,
              "rsk_minres_recycled_batch: group index");
       grp[s] = d->group_of_shift_h[s];
       hasg[s] = anyg ? (d->has_ghat_h[s] != 0) : 0;
-      m[s] = d->J[grp[s]] + hasg[s];
+      hasg2[s] = anyg2 ? (d->has_ghat2_h[s] != 0) : 0;
+      m[s] = d->J[grp[s]] + hasg[s] + hasg2[s];
+      MR_ARG(m[s] <= kMrK, "rsk_minres_recycled_batch: local dimension > RSK_MAX_LOCAL");
       kmax = std::max(kmax, m[s]);
     }
   }
@@ -496,8 +512,9 @@ extern "C" rsk_status rsk_minres_recycled_batch(rsk_handle h, const rsk_cg_desc*
   hc.sc = hc.tt + (size_t)ns * kMrK;
   hc.rt2 = hc.sc + (size_t)ns * 16;
   int* in = reinterpret_cast<int*>(base + L.in);
-  hc.m = in; hc.status = in + ns; hc.iters = in + 2 * ns; hc.tag = in + 3 * ns; hc.group = in + 4 * ns;
+  hc.m = in; hc.status = in + ns; hc.iters = in + 2 * ns; hc.go = in + 3 * ns; hc.group = in + 4 * ns;
   hc.hasg = in + 5 * ns;
+  hc.hasg2 = in + 6 * ns;
   hc.cnt = reinterpret_cast<unsigned*>(base + L.cnt);
   hc.part = reinterpret_cast<double*>(base + L.part);
   int* dlist = reinterpret_cast<int*>(base + L.list);
@@ -510,7 +527,8 @@ extern "C" rsk_status rsk_minres_recycled_batch(rsk_handle h, const rsk_cg_desc*
   }
   hc.ldw = defl ? d->ldw : N;
   hc.Ghat = anyg ? d->Ghat : nullptr;
-  hc.ldgh = anyg ? d->ldgh : N;
+  hc.ldgh = (anyg || anyg2) ? d->ldgh : N;
+  hc.Ghat2 = anyg2 ? d->Ghat2 : nullptr;
   hc.nchunk = L.nchunk;
   hc.maxit = d->maxit;
 
@@ -543,7 +561,8 @@ extern "C" rsk_status rsk_minres_recycled_batch(rsk_handle h, const rsk_cg_desc*
       dim3 gz((unsigned)std::min<int64_t>((N + 255) / 256, 1184), m[s]);
       count_launch();
       mr_formz<<<gz, 256, 0, st>>>(N, d->AW[g], d->EW[g], d->ldw, J, d->gamma_h[s],
-                                   (m[s] > J) ? d->ZGhat + (size_t)s * d->ldgh : nullptr, Zs);
+                                   hasg[s] ? d->ZGhat + (size_t)s * d->ldgh : nullptr,
+                                   hasg2[s] ? d->ZGhat2 + (size_t)s * d->ldgh : nullptr, Zs);
       MR_CUDA(cudaGetLastError());
       std::vector<double> R((size_t)m[s] * m[s]);
       double* Ks = hc.Kb + (size_t)s * kMrK * N;
@@ -561,8 +580,8 @@ extern "C" rsk_status rsk_minres_recycled_batch(rsk_handle h, const rsk_cg_desc*
       }
       if (ok) { Rs[s] = R; break; }
       dropped[s] = 1;
-      if (hasg[s] && m[s] == d->J[g] + 1) { hasg[s] = 0; m[s] -= 1; }
-      else m[s] = 0;
+      if ((hasg[s] || hasg2[s]) && m[s] > d->J[g]) { hasg[s] = 0; hasg2[s] = 0; m[s] = d->J[g]; }
+      else m[s] = 0;   // the carried columns go first (as one block), then all of U~
     }
   }
 
@@ -575,9 +594,10 @@ extern "C" rsk_status rsk_minres_recycled_batch(rsk_handle h, const rsk_cg_desc*
     for (int s = 0; s < ns; ++s) {
       ih[s] = m[s];
       ih[ns + s] = ST_IDLE;
-      ih[3 * ns + s] = -1;
+      ih[3 * ns + s] = 0;
       ih[4 * ns + s] = grp[s];
       ih[5 * ns + s] = hasg[s];
+      ih[6 * ns + s] = hasg2[s];
     }
     MR_CUDA(cudaMemcpyAsync(in, ih.data(), sizeof(int) * ih.size(), cudaMemcpyHostToDevice, st));
     MR_CUDA(cudaMemsetAsync(hc.cnt, 0, sizeof(unsigned) * ns * 4, st));
@@ -589,14 +609,17 @@ extern "C" rsk_status rsk_minres_recycled_batch(rsk_handle h, const rsk_cg_desc*
     all[s] = s;
     if (hasxp[s]) withxp.push_back(s);
   }
-  auto upload = [&](const std::vector<int>& v) -> cudaError_t {
-    return cudaMemcpyAsync(dlist, v.data(), sizeof(int) * v.size(), cudaMemcpyHostToDevice, st);
+  int* dloop = dlist + ns;   // active list of the lockstep chunk (kept while its graph lives)
+  auto upload_to = [&](int* dst, const std::vector<int>& v) -> cudaError_t {
+    return cudaMemcpyAsync(dst, v.data(), sizeof(int) * v.size(), cudaMemcpyHostToDevice, st);
   };
+  auto upload = [&](const std::vector<int>& v) -> cudaError_t { return upload_to(dlist, v); };
   auto grid = [&](size_t nl) { return dim3((unsigned)L.nchunk, (unsigned)nl); };
   // apply A_g to the vectors `src` (ld ldsrc) of the shifts in dlist into R0 (or Wv)
-  auto apply_list = [&](const double* src, int64_t ldsrc, double* dst, int nl, double* xdoty) -> cudaError_t {
+  auto apply_list = [&](const double* src, int64_t ldsrc, double* dst, int nl, double* xdoty,
+                        const int* lst) -> cudaError_t {
     ApplyLaunch a{};
-    a.X = src; a.ldx = ldsrc; a.Y = dst; a.ldy = N; a.gamma = gam; a.list = dlist; a.nlist = nl;
+    a.X = src; a.ldx = ldsrc; a.Y = dst; a.ldy = N; a.gamma = gam; a.list = lst; a.nlist = nl;
     a.mode = RSK_APPLY_SHIFTED; a.nvec_total = ns; a.xdoty = xdoty;
     return launch_apply(h, a, st);
   };
@@ -610,7 +633,7 @@ extern "C" rsk_status rsk_minres_recycled_batch(rsk_handle h, const rsk_cg_desc*
   MR_CUDA(cudaMemsetAsync(hc.R0, 0, sizeof(double) * (size_t)N * ns, st));
   if (!withxp.empty()) {
     MR_CUDA(upload(withxp));
-    MR_CUDA(apply_list(d->X, d->ldx, hc.R0, (int)withxp.size(), nullptr));
+    MR_CUDA(apply_list(d->X, d->ldx, hc.R0, (int)withxp.size(), nullptr, dlist));
     for (int s : withxp) applies[s] += 1;
   }
   MR_CUDA(upload(all));
@@ -632,7 +655,13 @@ extern "C" rsk_status rsk_minres_recycled_batch(rsk_handle h, const rsk_cg_desc*
   std::vector<int> status(ns, ST_ACTIVE), iters(ns, 0), done(ns, 0), final_status(ns, RSK_CG_CONVERGED);
   std::vector<double> relres(ns, 0.0);
   std::vector<int> it_restart(ns, -1);   // iterations at the last restart (stagnation guard)
-  int tag = 0;
+  std::vector<int> glist;                // active set of the captured chunk graph
+  cudaGraphExec_t gexec = nullptr;
+  const bool use_graph = getenv("RSK_MR_NOGRAPH") == nullptr;
+  struct GraphGuard {
+    cudaGraphExec_t* g;
+    ~GraphGuard() { if (*g) cudaGraphExecDestroy(*g); }
+  } gguard{&gexec};
   int64_t guard = 0;
   for (;;) {
     MR_CUDA(cudaMemcpyAsync(status.data(), hc.status, sizeof(int) * ns, cudaMemcpyDeviceToHost, st));
@@ -667,7 +696,7 @@ extern "C" rsk_status rsk_minres_recycled_batch(rsk_handle h, const rsk_cg_desc*
       count_launch();
       mr_final<<<grid(fin.size()), kMrT, 0, st>>>(dev, dlist);
       MR_CUDA(cudaGetLastError());
-      MR_CUDA(apply_list(d->X, d->ldx, hc.R0, (int)fin.size(), nullptr));
+      MR_CUDA(apply_list(d->X, d->ldx, hc.R0, (int)fin.size(), nullptr, dlist));
       count_launch();
       mr_resid<<<grid(fin.size()), kMrT, 0, st>>>(dev, dlist);
       MR_CUDA(cudaGetLastError());
@@ -704,17 +733,45 @@ extern "C" rsk_status rsk_minres_recycled_batch(rsk_handle h, const rsk_cg_desc*
       if (all_done) break;
       continue;    // restarted shifts whose x_0 + U K^T r is already converged
     }
-    // ---- check_every lockstep Lanczos steps over the active shifts
-    MR_CUDA(upload(active));
+    // ---- check_every lockstep Lanczos steps over the active shifts: the first chunk
+    // of an active set runs eagerly, later ones replay it as a CUDA graph (the
+    // per-iteration kernels are short; launch overhead would dominate small batches)
     const unsigned nl = (unsigned)active.size();
-    for (int it = 0; it < d->check_every; ++it) {
-      ++tag;
-      MR_CUDA(apply_list(hc.V, N, hc.Wv, (int)nl, alpha));
-      count_launches(3);
-      mr_kdots<<<grid(nl), kMrT, 0, st>>>(dev, dlist, 0);
-      mr_project<<<grid(nl), kMrT, 0, st>>>(dev, dlist, tag);
-      mr_vec<<<grid(nl), kMrT, 0, st>>>(dev, dlist, tag);
-      MR_CUDA(cudaGetLastError());
+    const bool same = (active == glist);
+    if (!same) {
+      MR_CUDA(upload_to(dloop, active));
+      if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
+      glist = active;
+    }
+    auto chunk = [&]() -> cudaError_t {
+      for (int it = 0; it < d->check_every; ++it) {
+        cudaError_t e = apply_list(hc.V, N, hc.Wv, (int)nl, alpha, dloop);
+        if (e != cudaSuccess) return e;
+        count_launches(3);
+        mr_kdots<<<grid(nl), kMrT, 0, st>>>(dev, dloop, 0);
+        mr_project<<<grid(nl), kMrT, 0, st>>>(dev, dloop);
+        mr_vec<<<grid(nl), kMrT, 0, st>>>(dev, dloop);
+        e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+      }
+      return cudaSuccess;
+    };
+    if (!same || !use_graph) {
+      MR_CUDA(chunk());
+    } else {
+      if (!gexec) {
+        cudaGraph_t graph = nullptr;
+        MR_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        cudaError_t ce = chunk();
+        cudaError_t ee = cudaStreamEndCapture(st, &graph);
+        MR_CUDA(ce);
+        MR_CUDA(ee);
+        MR_CUDA(cudaGraphInstantiate(&gexec, graph, 0));
+        cudaGraphDestroy(graph);
+      } else {
+        count_launches((long long)d->check_every * 5);
+      }
+      MR_CUDA(cudaGraphLaunch(gexec, st));
     }
     if (++guard > (int64_t)d->maxit * 4 + 100) {
       h->err = "rsk_minres_recycled_batch: loop guard";

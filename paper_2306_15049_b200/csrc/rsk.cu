@@ -567,6 +567,9 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
   }
   const bool anyg = defl && d->has_ghat_h != nullptr;
   if (anyg) RSK_ARG(d->Ghat && d->ZGhat && d->ldgh >= N, "rsk_cg_recycled_batch: Ghat/ZGhat");
+  if (d->has_ghat2_h)
+    for (int s = 0; s < ns; ++s)
+      RSK_ARG(d->has_ghat2_h[s] == 0, "rsk_cg_recycled_batch: a second carried column (Alg. 3) needs rsk_minres_recycled_batch");
   const bool store = (d->flags & RSK_CG_STORE_RES) != 0;
   if (store) RSK_ARG(d->store && d->store_cap >= 1 && d->lds >= N, "rsk_cg_recycled_batch: store");
   for (int s = 0; s < ns; ++s) RSK_ARG(std::isfinite(d->gamma_h[s]) && d->gamma_h[s] >= 0, "rsk_cg_recycled_batch: gamma");

@@ -107,7 +107,7 @@ class GpuSolver:
 
     # ------------------------------------------------------------- building blocks
     def cg(self, gammas_idx, X, has_xp, Gout=None, groups=None, ghat=None, store=None,
-           flags=0, order=None, inner="cg"):
+           flags=0, order=None, inner="cg", ghat2=None):
         """One batched inner solve over the shifts gammas_idx: recycled CG
         (rsk_cg_recycled_batch) or, with inner="minres", the paper's recycling MINRES
         (rsk_minres_recycled_batch) on the same descriptor."""
@@ -147,6 +147,12 @@ class GpuSolver:
             keep.append(hg)
             d.Ghat = Gh.data_ptr(); d.ZGhat = ZGh.data_ptr(); d.ldgh = self.N
             d.has_ghat_h = hg.ctypes.data_as(L.C.POINTER(L.C.c_int))
+        if ghat2 is not None:
+            Gh2, ZGh2, hg2 = ghat2
+            hg2 = np.ascontiguousarray(hg2, dtype=np.int32)
+            keep.append(hg2)
+            d.Ghat2 = Gh2.data_ptr(); d.ZGhat2 = ZGh2.data_ptr(); d.ldgh = self.N
+            d.has_ghat2_h = hg2.ctypes.data_as(L.C.POINTER(L.C.c_int))
         if store is not None:
             d.store = store.data_ptr(); d.lds = self.N; d.store_cap = STORE_CAP
             flags |= L.RSK_CG_STORE_RES
@@ -165,7 +171,8 @@ class GpuSolver:
         out.m_used = mu.ctypes.data_as(P(L.C.c_int)); out.store_count = sc.ctypes.data_as(P(L.C.c_int))
         out.ms_loop = ms.ctypes.data_as(L._hp)
         if inner == "minres":
-            kmax = (max(d.J[g] for g in range(d.ngroups)) + (1 if ghat is not None else 0)) if d.ngroups else 0
+            kmax = (max(d.J[g] for g in range(d.ngroups)) + (1 if ghat is not None else 0)
+                    + (1 if ghat2 is not None else 0)) if d.ngroups else 0
             need = self.h.minres_workspace_bytes(ns, kmax)
             if getattr(self, "ws_mr", None) is None or self.ws_mr.numel() < need:
                 self.ws_mr = torch.empty(need, dtype=torch.uint8, device=self.dev)
@@ -330,7 +337,12 @@ class GpuSolver:
             ghat = (Gh, ZGh, keep)
         # ---- batched deflated CG on this rank's shifts
         G = torch.empty(ml, N, **self.f)
-        if ml:
+        if ml and getattr(cfg, "local", "d3") == "seq":
+            res = self._wavefront(mine, X, has_xp[mine], G, groups, ghat)
+            overhead += res.pop("overhead")
+            self.h.lcurve_norms(X, self.d, self.rho_dev, self.eta_dev, self.lc_scratch, stream=self.stream)
+            rho_l, eta_l = _host(self.rho_dev)[:ml], _host(self.eta_dev)[:ml]
+        elif ml:
             prev = st.get("prev_iters")
             order = None
             if prev is not None and len(prev) == M:   # longest-processing-time first
@@ -364,6 +376,77 @@ class GpuSolver:
                       has_xp, keep, time.perf_counter() - t0, res["prof"])
         nst = dict(X_prev=Xf, G_prev=Gf, V_i1=V_i1, xstar=Xf[lstar], prev_iters=np.asarray(iters))
         return out, nst
+
+    def _wavefront(self, mine, X, has_xp, G, groups, ghat):
+        """Alg. 3 / Alg. 4 local spaces U~_l = [W_g, g^(k-1,l), g^(k,l-1)] (P:703, P:745;
+        SURVEY §8(f) f2(i), reading G35): shift l needs the correction g^(k,l-1) of its
+        predecessor in the same group, so each group is a chain solved in order and the
+        two chains run side by side (a batch of <= 2 shifts per wavefront step), with the
+        paper's recycling MINRES as the inner solver."""
+        cfg = self.cfg
+        if getattr(cfg, "inner", "cg") != "minres":
+            raise ValueError("local='seq' needs inner='minres' (two carried columns per shift)")
+        if self.dist.enabled and self.dist.world > 1:
+            raise NotImplementedError("local='seq' chains are solved on one rank")
+        ml = len(mine)
+        chains = [[i for i in range(ml) if (mine[i] + 1) <= cfg.I_split],
+                  [i for i in range(ml) if (mine[i] + 1) > cfg.I_split]]
+        out = dict(iters=np.zeros(ml, np.int32), applies=np.zeros(ml, np.int64), relres=np.zeros(ml),
+                   status=np.zeros(ml, np.int32), m_used=np.zeros(ml, np.int32), prof=np.zeros(8),
+                   overhead=0)
+        gos = groups["of_shift"]
+        for t in range(max(len(c) for c in chains)):
+            batch = [c[t] for c in chains if t < len(c)]
+            idx = torch.tensor(batch, dtype=torch.long, device=self.dev)
+            nb = len(batch)
+            Xb = X[idx].contiguous()
+            Gb = torch.empty(nb, self.N, **self.f)
+            gh_b = None
+            if ghat is not None:
+                gh_b = (ghat[0][idx].contiguous(), ghat[1][idx].contiguous(), np.asarray(ghat[2])[batch])
+            # second carried column g^(k,l-1): CGS2 against [W_g, g-hat_l], footnote P:691 test
+            Gh2 = torch.zeros(nb, self.N, **self.f)
+            has2 = np.zeros(nb, np.int32)
+            for j, i in enumerate(batch):
+                if t == 0:
+                    continue
+                prev = [c for c in chains if i in c][0][t - 1]
+                Wg = groups["W"][gos[i]]
+                gp = G[prev:prev + 1]
+                gh = gp.clone()
+                for _ in range(2):
+                    cf = self.utv(Wg, gh)
+                    self.h.recycle_project(L.RSK_SUB_UC, Wg, gh, cf, stream=self.stream)
+                    if gh_b is not None and gh_b[2][j]:
+                        g1 = gh_b[0][j:j + 1]
+                        c1 = self.utv(g1, gh)
+                        self.h.recycle_project(L.RSK_SUB_UC, g1, gh, c1, stream=self.stream)
+                n0 = torch.empty(1, **self.f); n1 = torch.empty(1, **self.f)
+                self.h.batch_dot(gp, gp, n0, stream=self.stream)
+                self.h.batch_dot(gh, gh, n1, stream=self.stream)
+                scale, keep = carried_select(_host(n0), _host(n1), DUP_SIN)
+                if keep[0]:
+                    self.h.batch_axpby(np.zeros(1), None, scale, gh, stream=self.stream)
+                    Gh2[j] = gh[0]
+                    has2[j] = 1
+            ZGh2 = torch.zeros_like(Gh2)
+            if has2.any():
+                sel = [j for j in range(nb) if has2[j]]
+                sidx = torch.tensor(sel, dtype=torch.long, device=self.dev)
+                gsel = self.gam_dev[torch.tensor([mine[batch[j]] for j in sel], device=self.dev)].contiguous()
+                src = Gh2[sidx].contiguous()
+                img = torch.empty_like(src)
+                self.h.apply_shifted(src, img, gamma=gsel, stream=self.stream)
+                ZGh2[sidx] = img
+                out["overhead"] += len(sel)
+            grp_b = dict(W=groups["W"], AW=groups["AW"], EW=groups["EW"], of_shift=np.asarray(gos)[batch])
+            r = self.cg([mine[i] for i in batch], Xb, np.asarray(has_xp)[batch], Gout=Gb, groups=grp_b,
+                        ghat=gh_b, inner="minres", ghat2=(Gh2, ZGh2, has2))
+            X[idx] = Xb
+            G[idx] = Gb
+            for key in ("iters", "applies", "relres", "status", "m_used"):
+                out[key][batch] = r[key]
+        return out
 
     def _two_anchor_guesses(self, ZA, ZE, R, KtZE, Ktb, gstar):
         """eq:updates (reading G34): oblique guesses of the left group from

@@ -53,6 +53,9 @@ class Config:
                                # eq:obliqueupdate) or "oblique2" (two anchors, eq:updates) -- f2(iii)
     inner: str = "cg"          # inner solver: "cg" (north_star's recycled CG, reading G1) or
                                # "minres" (the paper's recycling MINRES, eq:minShift) -- f2(ii)
+    local: str = "d3"          # local spaces: "d3" ([W, g^(k-1,l)], shift-independent, reading D3)
+                               # or "seq" ([W, g^(k-1,l), g^(k,l-1)], Alg. 3/4; needs inner
+                               # "minres", solved as a wavefront down each group) -- f2(i)
 
     @property
     def N(self) -> int:

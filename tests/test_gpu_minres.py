@@ -154,11 +154,13 @@ def test_minres_zero_rhs_and_independence_of_batch(torch_dev):
     assert np.all(z["status"] == 4) and np.all(z["iters"] == 0) and np.all(z["X"] == 0)
 
 
-def test_nested_solve_minres_stepwise(torch_dev):
-    """inner="minres" in the whole outer step (C1, tol 1e-10), stepwise handoff."""
+@pytest.mark.parametrize("local", ["d3", "seq"])
+def test_nested_solve_minres_stepwise(torch_dev, local):
+    """inner="minres" in the whole outer step (C1, tol 1e-10), stepwise handoff; with
+    local="seq" the local spaces carry g^(k,l-1) too (Alg. 3/4, wavefront per group)."""
     torch, dev = torch_dev
     from paper_2306_15049_b200.pipeline import GpuSolver
-    cfg = dataclasses.replace(S.CONFIGS["C1"], tol=1e-10, inner="minres")
+    cfg = dataclasses.replace(S.CONFIGS["C1"], tol=1e-10, inner="minres", local=local)
     inp = S.make_inputs(cfg)
     ref = opipe.run(cfg, inp, keep_steps=True)
     sol = GpuSolver(cfg, inp["psf"], inp["gamma"], check_every=4)

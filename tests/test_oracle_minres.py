@@ -168,3 +168,42 @@ def test_zero_rhs_and_carried_column_drop():
     Z = np.stack([A(Ut[:, i]) for i in range(3)], 1)
     res = mr.recycled_minres(A, b, Ut=Ut, Z=Z, n_carry=1, tol=1e-10)
     assert res.status == mr.DEFL_DROPPED and res.m_used == 2 and res.relres_true <= 1e-10
+
+
+@pytest.mark.parametrize("local", ["d3", "seq"])
+def test_pipeline_minres_tiny_matches_dense_every_step(local):
+    """The nested solve with the paper's inner solver (inner="minres") and with its
+    sequential local spaces [W, g^(k-1,l), g^(k,l-1)] (Alg. 3/4, local="seq"): every
+    (k, l) solution within 2 kappa tol of the dense solve of eq:seqsys."""
+    import dataclasses
+    from oracle import pipeline
+    cfg = dataclasses.replace(S.small_config(n=10, M=6, r=2, sigma=1.0, n_c=8, J=2, K_out=3, tol=1e-10),
+                              inner="minres", local=local)
+    inp = S.make_inputs(cfg)
+    out = pipeline.run(cfg, inp, keep_steps=True)
+    h = inp["psf"]; b = out["b"]; n = cfg.n
+    wx, wy = ops.identity_weights(n)
+    for k, st in enumerate(out["steps"]):
+        assert np.all((st.status == mr.CONVERGED) | (st.status == mr.DEFL_DROPPED))
+        for l in range(cfg.M):
+            Ad = dense.assemble_shifted(h, wx, wy, inp["gamma"][l], n)
+            xs = np.linalg.solve(Ad, b)
+            kap = np.linalg.cond(Ad)
+            assert np.linalg.norm(st.X[:, l] - xs) <= max(2 * kap * cfg.tol, 1e-12) * np.linalg.norm(xs)
+        xstar = st.X[:, st.lstar].reshape(n, n)
+        wx, wy = ops.irn_weights(xstar, cfg.tau)
+
+
+def test_sequential_local_space_columns():
+    """Alg. 3's second correction: orthogonal to [W, g-hat] and of unit norm; a
+    duplicate of g-hat's direction is dropped (footnote P:691)."""
+    from oracle import recycle as rc
+    rng = np.random.Generator(np.random.PCG64(12))
+    W, _ = np.linalg.qr(rng.standard_normal((200, 4)))
+    g1 = rng.standard_normal(200)
+    gh1 = rc.carried_direction(W, g1)
+    B = np.column_stack([W, gh1])
+    g2 = rng.standard_normal(200)
+    gh2 = rc.carried_direction(B, g2)
+    assert np.linalg.norm(B.T @ gh2) <= 1e-14 and abs(np.linalg.norm(gh2) - 1) <= 1e-14
+    assert rc.carried_direction(B, 3.0 * g1 + 1e-6 * g2) is None

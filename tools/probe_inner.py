@@ -25,12 +25,13 @@ def main():
     ap.add_argument("--config", default="C2")
     ap.add_argument("--outer", type=int, default=5)
     ap.add_argument("--rule", default="irn")
-    ap.add_argument("--inners", default="cg,minres")
+    ap.add_argument("--inners", default="cg,minres", help="cg, minres, minres_seq (Alg. 3 local spaces)")
     ap.add_argument("--repeat", type=int, default=2)
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     for inner in a.inners.split(","):
-        cfg = dataclasses.replace(S.CONFIGS[a.config], inner=inner, weight_rule=a.rule)
+        cfg = dataclasses.replace(S.CONFIGS[a.config], inner=inner.split("_")[0], weight_rule=a.rule,
+                                  local="seq" if inner.endswith("_seq") else "d3")
         inp = S.make_inputs(cfg)
         sol = GpuSolver(cfg, inp["psf"], inp["gamma"])
         sol.set_data(torch.from_numpy(inp["x_true"]).to(dev), torch.from_numpy(inp["xi"]).to(dev))
