@@ -58,6 +58,8 @@ class StepState:
     X_prev: np.ndarray | None      # N x M solutions of step k-1
     G_prev: np.ndarray | None      # N x M corrections g^(k-1,l)
     V_i1: np.ndarray | None        # Ritz block kept from k = 0
+    wx_prev: np.ndarray | None = None   # W_{k-1} (only for cfg.principal == "vnew", eq:delta)
+    wy_prev: np.ndarray | None = None
 
 
 @dataclasses.dataclass
@@ -102,6 +104,10 @@ def outer_step(cfg, h, b, d, gamma, st: StepState, shifts=None) -> StepResult:
         V_i2, _, a2 = rc.ritz_space(A_g(gamma[i2]), s2.store, n2)
         overhead += s1.applies + s2.applies + a1 + a2
         raw = np.column_stack([s1.x, s2.x, V_i1, V_i2])
+    elif getattr(cfg, "principal", "g10") == "vnew" and st.wx_prev is not None:
+        V_new, a_new = principal_update(cfg, h, b, gamma, st)
+        overhead += a_new
+        raw = np.column_stack([V_i1, V_new, st.X_prev])
     else:
         raw = np.column_stack([V_i1, st.X_prev])
     Ut = rc.stabilize(raw, cfg.n_c)
@@ -184,6 +190,23 @@ def outer_step(cfg, h, b, d, gamma, st: StepState, shifts=None) -> StepResult:
                       rho, eta, overhead, V_i1, Ut, an)
 
 
+def principal_update(cfg, h, b, gamma, st):
+    """eq:delta (reading G36): for l_c = round(0.9 M) solve
+    (A + gamma_c E_k) dx = gamma_c (E_k - E_{k-1}) x^(k-1,l_c) (eq:delta times gamma_c)
+    by at most 100 CG steps from 0, storing the normalised residuals (the Krylov vectors,
+    the same span as MINRES's Lanczos vectors); V^(new) = [dx, stored residuals]
+    (<= 101 columns). Returns (V_new, applies: the two E images + CG)."""
+    n = cfg.n
+    lc = cfg.l_c - 1
+    gc = gamma[lc]
+    x = st.X_prev[:, lc].reshape(n, n)
+    q = gc * (ops.apply_E(st.wx, st.wy, x) - ops.apply_E(st.wx_prev, st.wy_prev, x)).ravel()
+    A = lambda v: ops.apply_shifted(h, st.wx, st.wy, gc, v.reshape(n, n)).ravel()
+    res = dcg.defcg(A, q, tol=cfg.tol, maxit=100, store_cap=100)
+    cols = [res.x] + list(res.store)
+    return np.column_stack(cols), res.applies + 2
+
+
 def _same_group(cfg, a, b):
     """Shifts a, b (0-based) in the same group (left: l <= I, right: l > I; Alg. 4)."""
     return ((a + 1) <= cfg.I_split) == ((b + 1) <= cfg.I_split)
@@ -224,7 +247,7 @@ def run(cfg, inputs, K_out=None, keep_steps=False):
         hist.append(res.lstar)
         xstar = res.X[:, res.lstar].reshape(n, n)
         (wx, wy), D = next_weights(cfg, D, xstar)
-        st = StepState(k + 1, wx, wy, res.X, res.G, res.V_i1)
+        st = StepState(k + 1, wx, wy, res.X, res.G, res.V_i1, st.wx, st.wy)
         if getattr(cfg, "stop", "fixed") == "lstar3" and ops.lstar_settled(hist):
             break
     return {"b": b, "d": dd, "steps": steps, "final_weights": (wx, wy), "lstar": hist}

@@ -100,6 +100,8 @@ class GpuSolver:
 
     def reset_weights(self):
         self.h.set_weights(self.w0x, self.w0y, stream=self.stream)
+        self.cur_w = (self.w0x, self.w0y)       # the handle's W_k (eq:delta needs W_{k-1})
+        self.w_prev = None
         if getattr(self.cfg, "weight_rule", "irn") == "gazzola":
             # D_0 = I, held in the weights' padded layout
             self.Dx = self.w0x.clone()
@@ -107,7 +109,7 @@ class GpuSolver:
 
     # ------------------------------------------------------------- building blocks
     def cg(self, gammas_idx, X, has_xp, Gout=None, groups=None, ghat=None, store=None,
-           flags=0, order=None, inner="cg", ghat2=None):
+           flags=0, order=None, inner="cg", ghat2=None, rhs=None, maxit=None):
         """One batched inner solve over the shifts gammas_idx: recycled CG
         (rsk_cg_recycled_batch) or, with inner="minres", the paper's recycling MINRES
         (rsk_minres_recycled_batch) on the same descriptor."""
@@ -117,7 +119,7 @@ class GpuSolver:
         d = L.CgDesc()
         d.nshift = ns
         d.gamma_h = gam.ctypes.data_as(L._hp)
-        d.b = self.b.data_ptr()
+        d.b = (self.b if rhs is None else rhs).data_ptr()
         d.X = X.data_ptr(); d.ldx = self.N
         hx = np.ascontiguousarray(has_xp, dtype=np.int32)
         d.has_xp_h = hx.ctypes.data_as(L.C.POINTER(L.C.c_int))
@@ -158,7 +160,7 @@ class GpuSolver:
             flags |= L.RSK_CG_STORE_RES
         if self.profile:
             flags |= L.RSK_CG_PROFILE
-        d.tol = cfg.tol; d.maxit = cfg.maxit; d.check_every = self.check_every; d.flags = flags
+        d.tol = cfg.tol; d.maxit = cfg.maxit if maxit is None else maxit; d.check_every = self.check_every; d.flags = flags
         if order is not None:
             keep.append(od)
         out = L.CgOut()
@@ -243,6 +245,10 @@ class GpuSolver:
             overhead += q1 + q2
             raw = torch.cat([Xs, V_i1, V_i2], 0)
             del store
+        elif getattr(cfg, "principal", "g10") == "vnew" and st.get("W_prev") is not None:
+            V_new, a_new = self.principal_update(st)
+            overhead += a_new
+            raw = torch.cat([V_i1, V_new, st["X_prev"]], 0)
         else:
             raw = torch.cat([V_i1, st["X_prev"]], 0)
         Ut = self.stabilize(raw, nc_cap)
@@ -253,6 +259,29 @@ class GpuSolver:
         self.h.apply_shifted(Ut, ZA, EY=ZE, mode=L.RSK_APPLY_SPLIT, stream=self.stream)
         overhead += nc
         return Ut, ZA, ZE, V_i1, overhead
+
+    def principal_update(self, st: dict):
+        """eq:delta (reading G36): at l_c solve
+        (A + gamma_c E_k) dx = gamma_c (E_k - E_{k-1}) x^(k-1,l_c) by <= 100 CG steps from 0
+        with the residual store; V^(new) = [dx, stored Krylov vectors]. The two E images
+        are split applies under W_k and W_{k-1} (the handle's weights are swapped and
+        restored). Returns (V_new, applies)."""
+        cfg = self.cfg
+        lc = cfg.l_c - 1
+        x = st["X_prev"][lc:lc + 1].contiguous()
+        Ax = torch.empty_like(x); Ek = torch.empty_like(x); Ep = torch.empty_like(x)
+        self.h.apply_shifted(x, Ax, EY=Ek, mode=L.RSK_APPLY_SPLIT, stream=self.stream)
+        wpx, wpy = st["W_prev"]
+        self.h.set_weights(wpx, wpy, stream=self.stream)
+        self.h.apply_shifted(x, Ax, EY=Ep, mode=L.RSK_APPLY_SPLIT, stream=self.stream)
+        self.h.set_weights(self.cur_w[0], self.cur_w[1], stream=self.stream)
+        gc = float(self.gamma[lc])
+        self.h.batch_axpby(np.array([-gc]), Ep, np.array([gc]), Ek, stream=self.stream)   # q
+        dx = torch.zeros(1, self.N, **self.f)
+        store = torch.empty(STORE_CAP, self.N, **self.f)
+        r = self.cg([lc], dx, [0], store=store, rhs=Ek, maxit=100)
+        cnt = int(r["store_count"][0])
+        return torch.cat([dx, store[:cnt]], 0), int(r["applies"][0]) + 2
 
     def outer_step(self, k: int, st: dict) -> tuple[StepOut, dict]:
         cfg = self.cfg
@@ -486,7 +515,9 @@ class GpuSolver:
                                    stream=self.stream)
         else:
             raise ValueError(f"unknown weight rule {rule!r}")
+        self.w_prev = (self.cur_w[0].clone(), self.cur_w[1].clone())
         self.h.set_weights(self.wx, self.wy, stream=self.stream)
+        self.cur_w = (self.wx, self.wy)
 
     def run(self, K_out: int | None = None):
         """The whole nested solve: up to K_out outer steps from W_0 = I; with
@@ -504,5 +535,6 @@ class GpuSolver:
                 break
             if k + 1 < K:
                 self.next_weights(st["xstar"])
+                st["W_prev"] = self.w_prev
         self.final = st
         return outs

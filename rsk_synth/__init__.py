@@ -56,6 +56,8 @@ class Config:
     local: str = "d3"          # local spaces: "d3" ([W, g^(k-1,l)], shift-independent, reading D3)
                                # or "seq" ([W, g^(k-1,l), g^(k,l-1)], Alg. 3/4; needs inner
                                # "minres", solved as a wavefront down each group) -- f2(i)
+    principal: str = "g10"     # k >= 1 principal block: "g10" ([V_i1, X^(k-1)], reading G10) or
+                               # "vnew" ([V_i1, V^(new), X^(k-1)], eq:delta / eq:tildeUupdate) -- f3
 
     @property
     def N(self) -> int:
@@ -85,6 +87,12 @@ class Config:
     @property
     def J_R(self) -> int:
         return self.M - 1
+
+    @property
+    def l_c(self) -> int:
+        """Shift of the eq:delta correction solve (P:648 "one of the large gamma_l";
+        Example 1 takes 18 of 20): round(0.9 M), 1-based (reading G36)."""
+        return max(1, min(self.M, int(round(0.9 * self.M))))
 
     # anchors of the two-anchor oblique guesses (eq:updates P:1000-1005; reading G34):
     # I_L = i* (already the principal anchor, inside the left group), I_R = the middle

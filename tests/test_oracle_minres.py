@@ -207,3 +207,46 @@ def test_sequential_local_space_columns():
     gh2 = rc.carried_direction(B, g2)
     assert np.linalg.norm(B.T @ gh2) <= 1e-14 and abs(np.linalg.norm(gh2) - 1) <= 1e-14
     assert rc.carried_direction(B, 3.0 * g1 + 1e-6 * g2) is None
+
+
+def test_principal_update_vnew_solves_eq_delta():
+    """eq:delta: the first column of V^(new) approximates
+    dx = x^(k-1,l_c) - x^(k,l_c), i.e. it solves (A + g E_k) dx = g (E_k - E_{k-1}) x^(k-1,l_c)
+    (checked against a dense solve); the rest are orthonormal Krylov vectors whose span
+    holds the rhs; the k >= 1 nested solve with principal="vnew" still matches dense
+    solves at every (k, l)."""
+    import dataclasses
+    from oracle import pipeline
+    cfg = dataclasses.replace(S.small_config(n=10, M=6, r=2, sigma=1.0, n_c=12, J=2, K_out=3, tol=1e-10),
+                              principal="vnew")
+    inp = S.make_inputs(cfg)
+    out = pipeline.run(cfg, inp, keep_steps=True)
+    h = inp["psf"]; b = out["b"]; n = cfg.n
+    wx0, wy0 = ops.identity_weights(n)
+    st0 = out["steps"][0]
+    wx1, wy1 = ops.irn_weights(st0.X[:, st0.lstar].reshape(n, n), cfg.tau)
+    st = pipeline.StepState(1, wx1, wy1, st0.X, st0.G, st0.V_i1, wx0, wy0)
+    V, _ = pipeline.principal_update(cfg, h, b, inp["gamma"], st)
+    lc = cfg.l_c - 1
+    g = inp["gamma"][lc]
+    Ak = dense.assemble_shifted(h, wx1, wy1, g, n)
+    E1 = dense.assemble_shifted(h, wx1, wy1, 1.0, n) - dense.assemble_shifted(h, wx1, wy1, 0.0, n)
+    E0 = dense.assemble_shifted(h, wx0, wy0, 1.0, n) - dense.assemble_shifted(h, wx0, wy0, 0.0, n)
+    q = g * (E1 - E0) @ st0.X[:, lc]
+    K = V[:, 1:]
+    assert np.allclose(np.linalg.norm(K, axis=0), 1.0)
+    # the first column is the 100-step CG iterate on eq:delta from 0 (scipy's CG as the
+    # independent reference), the first Krylov vector is the normalised rhs
+    op = spla.LinearOperator(Ak.shape, matvec=lambda v: Ak @ v, dtype=np.float64)
+    xs, _ = spla.cg(op, q, rtol=cfg.tol, atol=0.0, maxiter=100)
+    assert np.linalg.norm(V[:, 0] - xs) <= 1e-6 * np.linalg.norm(xs)
+    assert np.allclose(K[:, 0], q / np.linalg.norm(q), atol=1e-14)
+    dx = np.linalg.solve(Ak, q)
+    assert np.linalg.norm(V[:, 0] - dx) <= 1e-3 * np.linalg.norm(dx)
+    wx, wy = wx0, wy0
+    for k, sk in enumerate(out["steps"]):
+        for l in range(cfg.M):
+            Ad = dense.assemble_shifted(h, wx, wy, inp["gamma"][l], n)
+            xs = np.linalg.solve(Ad, b)
+            assert np.linalg.norm(sk.X[:, l] - xs) <= max(2 * np.linalg.cond(Ad) * cfg.tol, 1e-12) * np.linalg.norm(xs)
+        wx, wy = ops.irn_weights(sk.X[:, sk.lstar].reshape(n, n), cfg.tau)

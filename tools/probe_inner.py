@@ -27,11 +27,15 @@ def main():
     ap.add_argument("--rule", default="irn")
     ap.add_argument("--inners", default="cg,minres", help="cg, minres, minres_seq (Alg. 3 local spaces)")
     ap.add_argument("--repeat", type=int, default=2)
+    ap.add_argument("--principal", default="g10", help="g10 or vnew (eq:delta, f3)")
+    ap.add_argument("--nc", type=int, default=0, help="override the principal cap n_c")
     a = ap.parse_args()
     dev = torch.device("cuda", 0)
     for inner in a.inners.split(","):
         cfg = dataclasses.replace(S.CONFIGS[a.config], inner=inner.split("_")[0], weight_rule=a.rule,
-                                  local="seq" if inner.endswith("_seq") else "d3")
+                                  local="seq" if inner.endswith("_seq") else "d3", principal=a.principal)
+        if a.nc:
+            cfg = dataclasses.replace(cfg, n_c=a.nc)
         inp = S.make_inputs(cfg)
         sol = GpuSolver(cfg, inp["psf"], inp["gamma"])
         sol.set_data(torch.from_numpy(inp["x_true"]).to(dev), torch.from_numpy(inp["xi"]).to(dev))
@@ -46,13 +50,15 @@ def main():
                 best = (dt, outs)
         dt, outs = best
         for o in outs:
-            print(json.dumps(dict(config=a.config, rule=a.rule, inner=inner, k=o.k,
+            print(json.dumps(dict(config=a.config, rule=a.rule, inner=inner, k=o.k, principal=a.principal,
+                                  nc=int(o.nc),
                                   iters_total=int(o.iters.sum()), iters_max=int(o.iters.max()),
                                   applies_total=int(o.applies.sum()) + int(o.overhead_applies),
                                   status=sorted(set(int(s) for s in o.status)), lstar=int(o.lstar),
                                   ms=round(o.ms * 1e3, 2))), flush=True)
         its = sum(int(o.iters.sum()) for o in outs)
         print(json.dumps(dict(config=a.config, rule=a.rule, inner=inner, summary=True,
+                              principal=a.principal, n_c=cfg.n_c,
                               nested_solve_ms=round(dt * 1e3, 1), iterations=its,
                               lstar=[int(o.lstar) for o in outs],
                               us_per_shift_iteration=round(dt * 1e6 / its, 3))), flush=True)
