@@ -241,6 +241,15 @@ def run_ours(args, cfg, inputs, rank, world):
     achieved = alg_bytes / (dl_ms / 1e3) / 1e9 if dl_ms > 0 else None
     peak, peak_src = _peaks()
     step_ms_last = ms / args.steps
+    # DRAM traffic of the dominant kernel per launch: bytes per shift-iteration from the
+    # committed ncu --set full capture (profiles/r1/cg_cluster_traffic.json) times this
+    # step's shift-iterations per launch (one launch per outer step)
+    traffic = None
+    nl = sum(1 for p in prof_all if p[6] > 0)
+    tf = os.path.join(os.path.dirname(os.path.abspath(__file__)), "profiles", "r1", "cg_cluster_traffic.json")
+    if kind == 1 and nl and os.path.exists(tf) and cfg.name == "C2":
+        with open(tf) as f:
+            traffic = json.load(f)["dram_bytes_per_shift_iteration"] * dl_its / nl
     # standalone fused apply over the full batch (all M shifts): 20 back-to-back launches
     # between two events (no host gaps inside), best of 3
     X = torch.randn(cfg.M, cfg.N, dtype=torch.float64, device=dev)
@@ -284,7 +293,10 @@ def run_ours(args, cfg, inputs, rank, world):
                          "kernel": {1: "cg_cluster_kernel (cluster-per-shift deflated CG loop)",
                                     2: "cg_persist_kernel (persistent lockstep deflated CG loop)"}.get(kind, "host-polled loop"),
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": (achieved / peak) if achieved else None, "traffic": None,
+                         "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                         "traffic_unit": "B per launch (ncu dram__bytes_read+write, L2-resident: far below"
+                                         " the algorithmic bytes)",
+                         "alg_bytes_per_launch": (alg_bytes / nl) if nl else None,
                          "peak_source": peak_src,
                          "kernel_ms_per_step": dl_ms, "kernel_ms_share": dl_ms / max(step_ms_last, 1e-9),
                          "shift_iterations_per_step": dl_its,

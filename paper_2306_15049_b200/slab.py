@@ -700,9 +700,13 @@ class SlabGpuSolver:
         xi = self.plan.extend(xi_full.reshape(-1), self.rank)
         self.h.make_rhs(xt, xi, self.cfg.noise, self.d, self.b)
 
-    def cg(self, gammas_idx, X, has_xp, Gout=None, groups=None, ghat=None, store=None, flags=0, order=None):
+    def cg(self, gammas_idx, X, has_xp, Gout=None, groups=None, ghat=None, store=None, flags=0, order=None,
+           inner="cg", ghat2=None, rhs=None, maxit=None):
         from .pipeline import STORE_CAP
-        return slab_cg(self.o, self.gamma[list(gammas_idx)], self.b, X, tol=self.cfg.tol, maxit=self.cfg.maxit,
+        if inner != "cg" or ghat2 is not None or rhs is not None:
+            raise NotImplementedError("row slabs run the recycled CG inner solve (north_star) only")
+        return slab_cg(self.o, self.gamma[list(gammas_idx)], self.b, X, tol=self.cfg.tol,
+                       maxit=self.cfg.maxit if maxit is None else maxit,
                        has_xp=has_xp, groups=groups, ghat=ghat, store=store, store_cap=STORE_CAP, Gout=Gout)
 
     def __getattr__(self, name):
