@@ -89,6 +89,7 @@ def recycled_minres(apply_gamma, b, x0=None, Ut=None, Z=None, tol=1e-8, maxit=20
 
     applies = 0
     iters = 0
+    it_restart = -1
     hist = []
     if x0 is None:
         r = b.copy()
@@ -167,9 +168,10 @@ def recycled_minres(apply_gamma, b, x0=None, Ut=None, Z=None, tol=1e-8, maxit=20
         if rt <= tol * nb:
             status = CONVERGED
             break
-        if iters >= maxit:
-            status = MAXIT
+        if iters >= maxit or iters == it_restart:
+            status = MAXIT            # maxit, or a restart that made no Lanczos step (G37)
             break
+        it_restart = iters
     if status == CONVERGED and status_setup == DEFL_DROPPED:
         status = DEFL_DROPPED
     ktr = 0.0 if K is None else float(np.linalg.norm(K.T @ r)) / nb

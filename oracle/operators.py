@@ -33,6 +33,8 @@ def conv(h: np.ndarray, x: np.ndarray) -> np.ndarray:
     y[i, j] = sum_{a, b = -r..r} h[a+r, b+r] * x[i-a, j-b], summed over the
     in-range pixels (i-a, j-b) only.
     """
+    if hasattr(h, "forward"):          # an explicit operator (CT, oracle/ct.py)
+        return h.forward(x)
     r = _psf_r(h)
     n0, n1 = x.shape
     xp = np.zeros((n0 + 2 * r, n1 + 2 * r))
@@ -51,6 +53,8 @@ def conv_t(h: np.ndarray, y: np.ndarray) -> np.ndarray:
     For every (i, j) and (a, b) with (i-a, j-b) in range:
         out[i-a, j-b] += h[a+r, b+r] * y[i, j].
     """
+    if hasattr(h, "adjoint"):          # an explicit operator (CT, oracle/ct.py)
+        return h.adjoint(y)
     r = _psf_r(h)
     n0, n1 = y.shape
     op = np.zeros((n0 + 2 * r, n1 + 2 * r))

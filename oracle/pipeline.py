@@ -207,6 +207,14 @@ def principal_update(cfg, h, b, gamma, st):
     return np.column_stack(cols), res.applies + 2
 
 
+def operator_of(cfg, inputs):
+    """C of the configuration: the PSF array (blur, O1) or the explicit CT matrix (f4)."""
+    if getattr(cfg, "operator", "blur") == "ct":
+        from .ct import CTOperator
+        return CTOperator(cfg.n, inputs["angles"], cfg.ndet)
+    return inputs["psf"]
+
+
 def _same_group(cfg, a, b):
     """Shifts a, b (0-based) in the same group (left: l <= I, right: l > I; Alg. 4)."""
     return ((a + 1) <= cfg.I_split) == ((b + 1) <= cfg.I_split)
@@ -231,7 +239,7 @@ def run(cfg, inputs, K_out=None, keep_steps=False):
     """The outer loop: up to K_out outer steps (configs fix the count, reading of A28);
     cfg.stop == "lstar3" also stops once l* is the same for 3 consecutive steps."""
     n = cfg.n
-    h = inputs["psf"]
+    h = operator_of(cfg, inputs)
     d, b2 = ops.make_data(h, inputs["x_true"], inputs["xi"], cfg.noise)
     b = b2.ravel(); dd = d
     gamma = inputs["gamma"]

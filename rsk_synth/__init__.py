@@ -58,6 +58,10 @@ class Config:
                                # "minres", solved as a wavefront down each group) -- f2(i)
     principal: str = "g10"     # k >= 1 principal block: "g10" ([V_i1, X^(k-1)], reading G10) or
                                # "vnew" ([V_i1, V^(new), X^(k-1)], eq:delta / eq:tildeUupdate) -- f3
+    operator: str = "blur"     # C: "blur" (Gaussian PSF, Example 1) or "ct" (parallel-beam Radon
+                               # matrix, Example 2 P:1083-1098) -- SURVEY §8(f) f4
+    n_angles: int = 0          # CT: projection angles 1, 2, ..., n_angles degrees
+    idx: tuple = ()            # index overrides (i2, i*, I, J_L, J_R, l_c), 1-based; () = rules G11/G36
 
     @property
     def N(self) -> int:
@@ -70,29 +74,44 @@ class Config:
 
     @property
     def i2(self) -> int:
-        return self.M // 2
+        return self.idx[0] if self.idx else self.M // 2
 
     @property
     def istar(self) -> int:
-        return self.M // 2
+        return self.idx[1] if self.idx else self.M // 2
 
     @property
     def I_split(self) -> int:
-        return int(round(0.75 * self.M))
+        return self.idx[2] if self.idx else int(round(0.75 * self.M))
 
     @property
     def J_L(self) -> int:
-        return self.I_split
+        return self.idx[3] if self.idx else self.I_split
 
     @property
     def J_R(self) -> int:
-        return self.M - 1
+        return self.idx[4] if self.idx else self.M - 1
 
     @property
     def l_c(self) -> int:
         """Shift of the eq:delta correction solve (P:648 "one of the large gamma_l";
         Example 1 takes 18 of 20): round(0.9 M), 1-based (reading G36)."""
+        if self.idx:
+            return self.idx[5]
         return max(1, min(self.M, int(round(0.9 * self.M))))
+
+    @property
+    def ndet(self) -> int:
+        """CT detector bins (reading G38): 2 ceil(n / sqrt 2) + 2 bins of unit width
+        centred on the rotation axis (every ray of every angle through the image is
+        sampled; an even count puts the bins at half-integer offsets, off the pixel
+        grid lines of the axis-parallel angles)."""
+        return 2 * math.ceil(self.n / math.sqrt(2.0)) + 2
+
+    @property
+    def ndata(self) -> int:
+        """Length of the data vector d: N for the blur, n_angles * ndet for CT."""
+        return self.n_angles * self.ndet if self.operator == "ct" else self.N
 
     # anchors of the two-anchor oblique guesses (eq:updates P:1000-1005; reading G34):
     # I_L = i* (already the principal anchor, inside the left group), I_R = the middle
@@ -112,6 +131,12 @@ CONFIGS = {
     "C3": Config("C3", 3, 512, 64, 1e-6, 10.0, 7, 3.0, 0.02, 60, 10, 6, 1e-3, 1e-8, "rects+discs", 60),
     "C4": Config("C4", 4, 1024, 128, 1e-6, 100.0, 7, 4.0, 0.01, 80, 12, 8, 1e-4, 1e-8, "alternate", 200),
     "C5": Config("C5", 5, 4096, 16, 1e-5, 10.0, 10, 5.0, 0.01, 40, 8, 4, 1e-3, 1e-8, "alternate", 2000),
+    # Example 2: n = 82, angles 1..135 degrees, C with unit
+    # Frobenius norm, 1 % noise, 20 lambda log-spaced in [1e-4, 1e1] (gamma = lambda^2),
+    # i1 = 1, i2 = 10, gamma_* = 12th, I = 16, l_c = 19, J_L = 15, J_R = 19;
+    # 9 outer steps; n_c, |J|, tau, tol as C2 (readings G38)
+    "C6": Config("C6", 6, 82, 20, 1e-8, 1e2, 0, 0.0, 0.01, 40, 8, 9, 1e-3, 1e-8, "alternate", 16,
+                 operator="ct", n_angles=135, idx=(10, 12, 16, 15, 19, 19)),
 }
 
 
@@ -194,6 +219,11 @@ def make_inputs(cfg: Config) -> dict:
     """All seeded raw inputs of one configuration (fp64, C-contiguous)."""
     rng = rng_for(cfg)
     x_true = phantom(cfg, rng)
+    if cfg.operator == "ct":
+        xi = rng.standard_normal(cfg.ndata)       # noise in the sinogram (data) space
+        return {"x_true": np.ascontiguousarray(x_true), "psf": None, "xi": xi,
+                "gamma": gamma_ladder(cfg),
+                "angles": np.arange(1, cfg.n_angles + 1, dtype=np.float64)}
     xi = rng.standard_normal((cfg.n, cfg.n))
     return {
         "x_true": np.ascontiguousarray(x_true),
