@@ -105,7 +105,9 @@ def recycled_minres(apply_gamma, b, x0=None, Ut=None, Z=None, tol=1e-8, maxit=20
         alphas, betas = [], []       # T_m: diag alpha_j, sub-diagonal beta_{j+1}
         status = MAXIT
         y = np.zeros(0)
-        while xi > 0 and iters < maxit:
+        # an initial residual already small enough needs no update beyond the
+        # z-block (m = 0 in eq:minShift, whose least-squares residual is xi)
+        while xi > tol * nb and iters < maxit:
             j = len(V) - 1
             w = apply_gamma(V[j])
             iters += 1
