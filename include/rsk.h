@@ -93,6 +93,26 @@ enum { RSK_CG_NO_DEFLATION = 1, RSK_CG_STORE_RES = 2, RSK_CG_PROFILE = 4 };
  * flags: reserved, pass 0. Returns RSK_EINVAL on bad sizes / non-finite PSF. */
 rsk_status rsk_create(rsk_handle* h, int device, int64_t ny, int64_t nx,
                       const double* psf_h, int pny, int pnx, int flags);
+/* rsk_create_ct: a handle whose C is Example 2's parallel-beam CT matrix (
+ * SURVEY §8(f) f4; reading G38) on n x n images: the line-integral model, entry
+ * (ray, pixel) = length of the ray inside the pixel square, pixel (i, j) = the unit square
+ * x in [j - n/2, j + 1 - n/2], y in [n/2 - i - 1, n/2 - i]; ray (a, d) is the line
+ * x cos(t_a) + y sin(t_a) = d - (ndet - 1)/2 with t_a = angles_deg_h[a] degrees (host
+ * [nangles]); rows ordered angle-major; a ray lying on a pixel face counts for the
+ * pixel on its high side; C is scaled to unit Frobenius norm. The data length
+ * is ndata = nangles * ndet. Built once on the host (CSR of C and of C^T, device
+ * resident). On such a handle: rsk_apply_shifted (RSK_APPLY_C_ONLY maps an image to a
+ * data vector (ldy >= ndata), RSK_APPLY_CT_ONLY a data vector (ldx >= ndata) to an
+ * image; no shift lists for C_ONLY), rsk_make_rhs (xi and d of length ndata),
+ * rsk_lcurve_norms (scratch nvec x ndata), the weight / IRN calls and
+ * rsk_minres_recycled_batch work; rsk_cg_recycled_batch returns RSK_EUNSUPPORTED (its
+ * device loops embed the stencil apply). n in [2, 4096], nangles, ndet >= 1, finite
+ * angles, else RSK_EINVAL. */
+rsk_status rsk_create_ct(rsk_handle* h, int device, int64_t n, int nangles, const double* angles_deg_h,
+                         int ndet, int flags);
+/* rsk_ct_info: ndata, the number of stored entries of C, and the Frobenius norm of C
+ * before scaling (host outputs, each nullable). RSK_EINVAL for a non-CT handle. */
+rsk_status rsk_ct_info(rsk_handle h, int64_t* ndata, int64_t* nnz, double* fro_unscaled);
 rsk_status rsk_destroy(rsk_handle h);
 const char* rsk_last_error(rsk_handle h);
 /* Library build information (static host string). */
@@ -269,7 +289,9 @@ rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, rsk_cg_out*
  *   residual b - A_g x (restart from x otherwise; reading G14).
  * Same ownership, stream and error conventions as rsk_cg_recycled_batch: the call
  * is host-blocking, `X` holds x_p in and x out, `Gout` (nullable) receives
- * g = x - x_p; RSK_CG_STORE_RES is rejected (EINVAL). iters = Lanczos applies;
+ * g = x - x_p; with RSK_CG_STORE_RES the first store_cap normalised Lanczos vectors
+ * v_1, v_2, ... (the span of CG's normalised residuals) go to `store` exactly as the
+ * CG's residuals do (store_count filled). iters = Lanczos applies;
  * applies = iters + the r_p apply + one per true-residual confirmation. ms_loop is
  * not written. `ws`: at least rsk_minres_workspace_bytes(h, nshift, kmax) bytes,
  * kmax = max_l (J_g(l) + has_ghat_l) <= RSK_MAX_LOCAL (7 N-vectors + kmax

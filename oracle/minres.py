@@ -19,10 +19,11 @@ confirmed on the true residual b - A_g x; if the confirmation fails, the solve
 restarts from x (x_0 <- x). The iteration count is the number of Lanczos
 applies A_g v_j.
 
-Literal and slow: K from numpy's Householder QR (diag(R) > 0, reading G16), the
-basis V_m and the images A_g V_m stored, the LS residual min ||xi e_1 - T_m y||
-solved by numpy.linalg.lstsq at every iteration, and the full block LS of
-eq:minShift solved once at the end.  Pinned in tests/test_oracle_minres.py
+Plain and slow: K from numpy's Householder QR (diag(R) > 0, reading G16), the
+basis V_m and the images A_g V_m stored; the y-block min ||xi e_1 - T_m y|| by the
+textbook Givens QR of T_m (Paige-Saunders), its residual |phibar| checked after every
+step; at the end y from the triangular factor and the first block row of eq:minShift
+solved exactly (z = K^T r - K^T A_g V_m y).  Pinned in tests/test_oracle_minres.py
 (dense minimum-residual problems over explicit bases, scipy MINRES, K^T r = 0,
 monotone residuals, tiny SPD systems vs dense solves).
 """
@@ -45,6 +46,7 @@ class MinresResult:
     m_used: int           # columns of U~_l used
     res_hist: list = dataclasses.field(default_factory=list)   # LS residual per iteration
     ktr_max: float = 0.0  # ||K^T (b - A_g x)|| / ||b|| at exit (eq:xFinal makes it 0)
+    store: list = dataclasses.field(default_factory=list)    # normalised Lanczos vectors
 
 
 def local_factor(Z):
@@ -56,7 +58,7 @@ def local_factor(Z):
 
 
 def recycled_minres(apply_gamma, b, x0=None, Ut=None, Z=None, tol=1e-8, maxit=20000,
-                    n_carry=0) -> MinresResult:
+                    n_carry=0, store_cap=0) -> MinresResult:
     """Recycling MINRES on (A + gamma E) x = b from x0 over Range([U_l, V_m]).
 
     apply_gamma: flat vector -> (A + gamma E) times it.
@@ -64,6 +66,8 @@ def recycled_minres(apply_gamma, b, x0=None, Ut=None, Z=None, tol=1e-8, maxit=20
     Z:  N x m, (A + gamma E) U~_l (reused, no applies).
     n_carry: trailing carried columns of U~, dropped first if Z is rank deficient
     (R_l singular), then all of U~ (DEFL_DROPPED) -- the same fallback as O4.
+    store_cap > 0 keeps the first Lanczos vectors v_1, v_2, ... of the solve (the seed
+    solves' Krylov basis, S1; the span of CG's normalised residuals).
     """
     N = b.shape[0]
     nb = float(np.linalg.norm(b))
@@ -91,6 +95,7 @@ def recycled_minres(apply_gamma, b, x0=None, Ut=None, Z=None, tol=1e-8, maxit=20
     iters = 0
     it_restart = -1
     hist = []
+    store = []
     if x0 is None:
         r = b.copy()
     else:
@@ -102,9 +107,14 @@ def recycled_minres(apply_gamma, b, x0=None, Ut=None, Z=None, tol=1e-8, maxit=20
         xi = float(np.linalg.norm(rh))
         V = [rh / xi] if xi > 0 else []
         AV = []
-        alphas, betas = [], []       # T_m: diag alpha_j, sub-diagonal beta_{j+1}
+        betas = []                   # beta_{j+1} (sub-diagonal of T_m)
+        # QR of T_m by Givens rotations (Paige-Saunders): R_m has three diagonals
+        # (rd = diagonal, r1 = first, r2 = second super-diagonal), Q_m^T (xi e_1) = (t, phibar)
+        rd, r1, r2, tvec = [], [], [], []
+        cs_prev, sn_prev = 1.0, 0.0      # rotation j-1
+        cs_pp, sn_pp = 1.0, 0.0          # rotation j-2
+        phibar = xi
         status = MAXIT
-        y = np.zeros(0)
         # an initial residual already small enough needs no update beyond the
         # z-block (m = 0 in eq:minShift, whose least-squares residual is xi)
         while xi > tol * nb and iters < maxit:
@@ -115,50 +125,45 @@ def recycled_minres(apply_gamma, b, x0=None, Ut=None, Z=None, tol=1e-8, maxit=20
             AV.append(w)
             p = proj(w)                                   # (I - K K^T) A_g v_j
             a = float(V[j] @ p)
-            p = p - a * V[j] - (betas[-1] * V[j - 1] if j > 0 else 0.0)
+            bprev = betas[-1] if j > 0 else 0.0
+            p = p - a * V[j] - (bprev * V[j - 1] if j > 0 else 0.0)
             bn = float(np.linalg.norm(p))
-            alphas.append(a)
             betas.append(bn)
-            mm = len(alphas)
-            T = np.zeros((mm + 1, mm))
-            for i in range(mm):
-                T[i, i] = alphas[i]
-                T[i + 1, i] = betas[i]
-                if i + 1 < mm:
-                    T[i, i + 1] = betas[i]
-            e1 = np.zeros(mm + 1)
-            e1[0] = xi
-            y = np.linalg.lstsq(T, e1, rcond=None)[0]
-            res = float(np.linalg.norm(e1 - T @ y))
+            # new column of T_m: (.., bprev, a, bn) in rows j-1, j, j+1
+            e2 = sn_pp * bprev                     # row j-2 after rotation j-2
+            tmp = cs_pp * bprev
+            e1 = cs_prev * tmp + sn_prev * a       # row j-1 after rotation j-1
+            dj = -sn_prev * tmp + cs_prev * a      # row j before the new rotation
+            gm = float(np.hypot(dj, bn))
+            c_new, s_new = (dj / gm, bn / gm) if gm > 0 else (1.0, 0.0)
+            rd.append(gm); r1.append(e1); r2.append(e2)
+            tvec.append(c_new * phibar)
+            phibar = -s_new * phibar
+            cs_pp, sn_pp, cs_prev, sn_prev = cs_prev, sn_prev, c_new, s_new
+            res = abs(phibar)
             hist.append(res)
             if res <= tol * nb or bn == 0.0:
                 status = CONVERGED
                 break
             V.append(p / bn)
-        # ---- eq:minShift (full block least squares) and eq:xFinal
+        store.extend(V[:max(0, store_cap - len(store))][:max(len(AV), 0)])
+        # ---- eq:minShift: y from R_m y = t (back substitution), the first block row solved
+        # exactly, z = K^T r - K^T A_g V_m y; eq:xFinal
         mm = len(AV)
         if mm > 0:
-            Vm = np.stack(V[:mm], 1)
-            AVm = np.stack(AV, 1)
-            T = np.zeros((mm + 1, mm))
-            for i in range(mm):
-                T[i, i] = alphas[i]
-                T[i + 1, i] = betas[i]
+            y = np.zeros(mm)
+            for i in range(mm - 1, -1, -1):
+                v = tvec[i]
                 if i + 1 < mm:
-                    T[i, i + 1] = betas[i]
-            k = m_used
-            Mb = np.zeros((k + mm + 1, k + mm))
-            rhs = np.zeros(k + mm + 1)
-            if k:
-                Mb[:k, :k] = np.eye(k)
-                Mb[:k, k:] = K.T @ AVm
-                rhs[:k] = K.T @ r
-            Mb[k:, k:] = T
-            rhs[k] = xi
-            sol = np.linalg.lstsq(Mb, rhs, rcond=None)[0]
-            z, y = sol[:k], sol[k:]
+                    v -= r1[i + 1] * y[i + 1]
+                if i + 2 < mm:
+                    v -= r2[i + 2] * y[i + 2]
+                y[i] = v / rd[i]
+            Vm = np.stack(V[:mm], 1)
             g = Vm @ y
-            if k:
+            if m_used:
+                AVm = np.stack(AV, 1)
+                z = K.T @ r - K.T @ (AVm @ y)
                 g = g + Ut @ np.linalg.solve(R, z)      # U_l z = U~_l R_l^-1 z
             x = x + g
         elif m_used:
@@ -177,4 +182,4 @@ def recycled_minres(apply_gamma, b, x0=None, Ut=None, Z=None, tol=1e-8, maxit=20
     if status == CONVERGED and status_setup == DEFL_DROPPED:
         status = DEFL_DROPPED
     ktr = 0.0 if K is None else float(np.linalg.norm(K.T @ r)) / nb
-    return MinresResult(x, iters, applies, rt / nb, status, m_used, hist, ktr)
+    return MinresResult(x, iters, applies, rt / nb, status, m_used, hist, ktr, store)

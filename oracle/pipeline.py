@@ -98,8 +98,8 @@ def outer_step(cfg, h, b, d, gamma, st: StepState, shifts=None) -> StepResult:
     if st.k == 0:
         n1 = math.ceil(2 * (cfg.n_c - 2) / 3)
         n2 = cfg.n_c - 2 - n1
-        s1 = dcg.defcg(A_g(gamma[i1]), b, tol=cfg.tol, maxit=cfg.maxit, store_cap=100)
-        s2 = dcg.defcg(A_g(gamma[i2]), b, tol=cfg.tol, maxit=cfg.maxit, store_cap=100)
+        s1 = _seed_solver(cfg)(A_g(gamma[i1]), b, tol=cfg.tol, maxit=cfg.maxit, store_cap=100)
+        s2 = _seed_solver(cfg)(A_g(gamma[i2]), b, tol=cfg.tol, maxit=cfg.maxit, store_cap=100)
         V_i1, _, a1 = rc.ritz_space(A_g(gamma[i1]), s1.store, n1)
         V_i2, _, a2 = rc.ritz_space(A_g(gamma[i2]), s2.store, n2)
         overhead += s1.applies + s2.applies + a1 + a2
@@ -202,9 +202,17 @@ def principal_update(cfg, h, b, gamma, st):
     x = st.X_prev[:, lc].reshape(n, n)
     q = gc * (ops.apply_E(st.wx, st.wy, x) - ops.apply_E(st.wx_prev, st.wy_prev, x)).ravel()
     A = lambda v: ops.apply_shifted(h, st.wx, st.wy, gc, v.reshape(n, n)).ravel()
-    res = dcg.defcg(A, q, tol=cfg.tol, maxit=100, store_cap=100)
+    res = _seed_solver(cfg)(A, q, tol=cfg.tol, maxit=100, store_cap=100)
     cols = [res.x] + list(res.store)
     return np.column_stack(cols), res.applies + 2
+
+
+def _seed_solver(cfg):
+    """Plain solves with a Krylov store (seeds S1, eq:delta): the configured inner solver
+    (CG residuals or MINRES Lanczos vectors: the same Krylov space)."""
+    if getattr(cfg, "inner", "cg") == "minres":
+        return mr.recycled_minres
+    return dcg.defcg
 
 
 def operator_of(cfg, inputs):

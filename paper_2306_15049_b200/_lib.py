@@ -78,6 +78,8 @@ _SIGS = {
     "rsk_launch_count": (C.c_int64, []),
     "rsk_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, _i64, _i64, _hp, C.c_int, C.c_int, C.c_int]),
     "rsk_destroy": (C.c_int, [C.c_void_p]),
+    "rsk_create_ct": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, _i64, C.c_int, _hp, C.c_int, C.c_int]),
+    "rsk_ct_info": (C.c_int, [C.c_void_p, C.POINTER(_i64), C.POINTER(_i64), _hp]),
     "rsk_last_error": (C.c_char_p, [C.c_void_p]),
     "rsk_set_weights": (C.c_int, [C.c_void_p, _dp, _dp, C.c_void_p]),
     "rsk_apply_shifted": (C.c_int, [C.c_void_p, C.c_int, _dp, _i64, _dp, _dp, _i64, _dp, _i64, _dp,

@@ -182,6 +182,7 @@ bool fill_apply_params(Handle* h, const ApplyLaunch& a, ApplyParams& prm, int ty
 }
 
 cudaError_t launch_apply(Handle* h, const ApplyLaunch& a, cudaStream_t st) {
+  if (h->ct) return launch_ct_apply(h, a, st);   // CT: sparse C, C^T (ct.cu)
   if (a.nlist <= 0) return cudaSuccess;
   ApplyParams prm;
   const bool tma = fill_apply_params(h, a, prm, 0);

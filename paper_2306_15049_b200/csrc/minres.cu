@@ -34,6 +34,7 @@ namespace {
 constexpr int kMrK = RSK_MAX_LOCAL;   // local columns per shift (|J| + 1 <= 17)
 constexpr int kMrRows = 512;          // rows per CTA chunk (independent of the batch)
 constexpr int kMrT = 256;
+constexpr int kMrP = 2 * kMrK + 1;    // partial slots: K^T w (0..), K^T v (kMrK..), norm^2 (2 kMrK)
 
 struct MrDev {
   int64_t N;
@@ -55,7 +56,8 @@ struct MrDev {
   double* kay;   // [ns][kMrK]  K^T A_g y_m
   double* tt;    // [ns][kMrK]  R^-1 (c0 - kay) for eq:xFinal
   double* sc;    // [ns][16] MINRES scalars
-  double* part;  // [ns][nchunk][kMrK + 1]
+  double* part;  // [ns][nchunk][kMrP]
+  double* kv;    // [ns][kMrK]  K^T v_j (the Lanczos vector's drift out of K-perp)
   double* rt2;   // [ns] ||b - A_g x||^2 after a confirm
   int* m;        // [ns] local dimension
   int* status;
@@ -75,6 +77,11 @@ struct MrDev {
   int nchunk;
   double tolb;   // tol * ||b||
   int maxit;
+  double* store; // RSK_CG_STORE_RES: normalised Lanczos vectors, shift s slot c at
+  int64_t lds;   //   store + (s * store_cap + c) * lds
+  int store_cap;
+  int* slot;     // [ns] store slot of the vector v being formed, or -1
+  int* scnt;     // [ns] vectors stored
 };
 
 // MINRES scalars (index into sc[s*16 + .])
@@ -119,7 +126,7 @@ __device__ __forceinline__ bool last_cta(unsigned* c, int nchunk) {
 // t, t + kMrT, ... in order, then the fixed CTA tree); valid in thread 0.
 __device__ __forceinline__ double chunk_sum(const MrDev* g, int s, int j, double* sh) {
   double t = 0.0;
-  for (int c = threadIdx.x; c < g->nchunk; c += kMrT) t += g->part[((int64_t)s * g->nchunk + c) * (kMrK + 1) + j];
+  for (int c = threadIdx.x; c < g->nchunk; c += kMrT) t += g->part[((int64_t)s * g->nchunk + c) * kMrP + j];
   return block_sum(t, sh);
 }
 
@@ -134,29 +141,43 @@ __global__ void __launch_bounds__(kMrT) mr_kdots(MrDev* __restrict__ g, const in
   const int chunk = blockIdx.x;
   const int64_t r0 = (int64_t)chunk * kMrRows, r1 = min(N, r0 + kMrRows);
   const double* src = (start ? g->R0 : g->Wv) + (int64_t)s * N;
+  const double* vv = g->V + (int64_t)s * N;
   const double* K = g->Kb + (int64_t)s * kMrK * N;
-  double acc[kMrK];
+  double acc[kMrK], acv[kMrK];
 #pragma unroll
-  for (int j = 0; j < kMrK; ++j) acc[j] = 0.0;
+  for (int j = 0; j < kMrK; ++j) { acc[j] = 0.0; acv[j] = 0.0; }
   for (int64_t i = r0 + threadIdx.x; i < r1; i += kMrT) {
     const double w = src[i];
+    const double v = start ? 0.0 : vv[i];
 #pragma unroll
     for (int j = 0; j < kMrK; ++j)
-      if (j < m) acc[j] = fma(K[(int64_t)j * N + i], w, acc[j]);
+      if (j < m) {
+        const double k = K[(int64_t)j * N + i];
+        acc[j] = fma(k, w, acc[j]);
+        acv[j] = fma(k, v, acv[j]);
+      }
   }
   __shared__ double sh[kMrT / 32];
-  double* part = g->part + ((int64_t)s * g->nchunk + chunk) * (kMrK + 1);
+  double* part = g->part + ((int64_t)s * g->nchunk + chunk) * kMrP;
 #pragma unroll
   for (int j = 0; j < kMrK; ++j) {
     if (j < m) {
       const double t = block_sum(acc[j], sh);
       if (threadIdx.x == 0) part[j] = t;
+      if (!start) {
+        const double u = block_sum(acv[j], sh);
+        if (threadIdx.x == 0) part[kMrK + j] = u;
+      }
     }
   }
   if (!last_cta(&g->cnt[s * 4 + 0], g->nchunk)) return;
   for (int j = 0; j < m; ++j) {
     const double t = chunk_sum(g, s, j, sh);
     if (threadIdx.x == 0) (start ? g->c0 : g->c)[s * kMrK + j] = t;
+    if (!start) {
+      const double u = chunk_sum(g, s, kMrK + j, sh);
+      if (threadIdx.x == 0) g->kv[s * kMrK + j] = u;
+    }
   }
 }
 
@@ -172,7 +193,10 @@ __global__ void __launch_bounds__(kMrT) mr_project(MrDev* __restrict__ g, const 
   __shared__ double cs_[kMrK];
   if (threadIdx.x < kMrK) cs_[threadIdx.x] = threadIdx.x < m ? g->c[s * kMrK + threadIdx.x] : 0.0;
   __syncthreads();
-  const double alpha = g->alpha[s];
+  // alpha_j = v_j . (I - K K^T) A_g v_j = v_j . A_g v_j - (K^T v_j) . c_j (as the oracle:
+  // the projection before the inner product; the second term is v_j's drift out of K-perp)
+  double alpha = g->alpha[s];
+  for (int j = 0; j < m; ++j) alpha = fma(-g->kv[s * kMrK + j], cs_[j], alpha);
   const double beta = g->sc[s * 16 + S_BETA];
   const double* K = g->Kb + (int64_t)s * kMrK * N;
   double* w = g->Wv + (int64_t)s * N;
@@ -191,7 +215,7 @@ __global__ void __launch_bounds__(kMrT) mr_project(MrDev* __restrict__ g, const 
   }
   __shared__ double sh[kMrT / 32];
   const double tot = block_sum(nrm, sh);
-  double* part = g->part + ((int64_t)s * g->nchunk + chunk) * (kMrK + 1);
+  double* part = g->part + ((int64_t)s * g->nchunk + chunk) * kMrP;
   if (threadIdx.x == 0) part[kMrK] = tot;
   if (!last_cta(&g->cnt[s * 4 + 1], g->nchunk)) return;
   const double n2 = chunk_sum(g, s, kMrK, sh);
@@ -235,6 +259,9 @@ __global__ void __launch_bounds__(kMrT) mr_project(MrDev* __restrict__ g, const 
   if (!isfinite(bn) || !isfinite(phibar) || !isfinite(alpha)) g->status[s] = ST_BREAKDOWN;
   else if (fabs(phibar) <= g->tolb || bn == 0.0) g->status[s] = ST_RCONV;
   else if (it >= g->maxit) g->status[s] = ST_MAXIT;
+  int sl = -1;   // v_{j+1} is stored while the solve goes on (as CG stores r_j)
+  if (g->store && g->status[s] == ST_ACTIVE && g->scnt[s] < g->store_cap) sl = g->scnt[s]++;
+  g->slot[s] = sl;
 }
 
 // d_j = (v_j - oldeps d_{j-2} - delta d_{j-1}) / gamma_j ; y += phi d_j ;
@@ -248,6 +275,8 @@ __global__ void __launch_bounds__(kMrT) mr_vec(MrDev* __restrict__ g, const int*
   const double oldeps = sc[S_OLDEPS], delta = sc[S_DELTA], denom = sc[S_DENOM], phi = sc[S_PHI],
                invb = sc[S_INVB];
   const int64_t o = (int64_t)s * N;
+  const int sl = g->slot[s];
+  double* sto = (sl >= 0) ? g->store + ((int64_t)s * g->store_cap + sl) * g->lds : nullptr;
   for (int64_t i = r0 + threadIdx.x; i < r1; i += kMrT) {
     const double v = g->V[o + i];
     const double d1 = g->D1[o + i], d2 = g->D2[o + i];
@@ -256,7 +285,9 @@ __global__ void __launch_bounds__(kMrT) mr_vec(MrDev* __restrict__ g, const int*
     g->D2[o + i] = d1;
     g->D1[o + i] = dn;
     g->Vp[o + i] = v;
-    g->V[o + i] = g->Wv[o + i] * invb;
+    const double vn = g->Wv[o + i] * invb;
+    g->V[o + i] = vn;
+    if (sto) sto[i] = vn;
   }
 }
 
@@ -284,7 +315,7 @@ __global__ void __launch_bounds__(kMrT) mr_start_proj(MrDev* __restrict__ g, con
   }
   __shared__ double sh[kMrT / 32];
   const double tot = block_sum(nrm, sh);
-  double* part = g->part + ((int64_t)s * g->nchunk + chunk) * (kMrK + 1);
+  double* part = g->part + ((int64_t)s * g->nchunk + chunk) * kMrP;
   if (threadIdx.x == 0) part[kMrK] = tot;
   if (!last_cta(&g->cnt[s * 4 + 1], g->nchunk)) return;
   const double n2 = chunk_sum(g, s, kMrK, sh);
@@ -301,6 +332,9 @@ __global__ void __launch_bounds__(kMrT) mr_start_proj(MrDev* __restrict__ g, con
     sc[S_INVB] = xi > 0.0 ? 1.0 / xi : 0.0;
     g->status[s] = (xi > 0.0 && isfinite(xi)) ? ST_ACTIVE : (isfinite(xi) ? ST_RCONV : ST_BREAKDOWN);
     if (xi <= g->tolb && xi > 0.0) g->status[s] = ST_RCONV;   // x_0 + U K^T r already converged
+    int sl = -1;
+    if (g->store && g->status[s] == ST_ACTIVE && g->scnt[s] < g->store_cap) sl = g->scnt[s]++;
+    g->slot[s] = sl;
   }
   if (threadIdx.x < kMrK) {
     const int q = s * kMrK + threadIdx.x;
@@ -315,9 +349,13 @@ __global__ void __launch_bounds__(kMrT) mr_start_vec(MrDev* __restrict__ g, cons
   const int64_t r0 = (int64_t)blockIdx.x * kMrRows, r1 = min(N, r0 + kMrRows);
   const double invb = g->sc[s * 16 + S_INVB];
   const int64_t o = (int64_t)s * N;
+  const int sl = g->slot[s];
+  double* sto = (sl >= 0) ? g->store + ((int64_t)s * g->store_cap + sl) * g->lds : nullptr;
   for (int64_t i = r0 + threadIdx.x; i < r1; i += kMrT) {
-    g->V[o + i] *= invb;
+    const double v = g->V[o + i] * invb;
+    g->V[o + i] = v;
     g->Vp[o + i] = 0.0; g->D1[o + i] = 0.0; g->D2[o + i] = 0.0; g->Y[o + i] = 0.0;
+    if (sto) sto[i] = v;
   }
 }
 
@@ -364,7 +402,7 @@ __global__ void __launch_bounds__(kMrT) mr_resid(MrDev* __restrict__ g, const in
   }
   __shared__ double sh[kMrT / 32];
   const double tot = block_sum(nrm, sh);
-  if (threadIdx.x == 0) g->part[((int64_t)s * g->nchunk + chunk) * (kMrK + 1) + kMrK] = tot;
+  if (threadIdx.x == 0) g->part[((int64_t)s * g->nchunk + chunk) * kMrP + kMrK] = tot;
   if (!last_cta(&g->cnt[s * 4 + 2], g->nchunk)) return;
   const double n2 = chunk_sum(g, s, kMrK, sh);
   if (threadIdx.x == 0) g->rt2[s] = n2;
@@ -402,10 +440,10 @@ MrLayout mr_layout(const Handle* h, int ns, int kmax) {
   L.vec = o; o = al(o + sizeof(double) * (size_t)N * ns * 7);
   L.kb = o; o = al(o + sizeof(double) * (size_t)N * ns * (kmax > 0 ? kMrK : 0));
   L.zs = o; o = al(o + sizeof(double) * (size_t)N * (kmax > 0 ? kmax : 0));
-  L.dbl = o; o = al(o + sizeof(double) * (size_t)ns * (7 * kMrK + 16 + 2));
-  L.in = o; o = al(o + sizeof(int) * (size_t)ns * 8);
+  L.dbl = o; o = al(o + sizeof(double) * (size_t)ns * (8 * kMrK + 16 + 2));
+  L.in = o; o = al(o + sizeof(int) * (size_t)ns * 10);
   L.cnt = o; o = al(o + sizeof(unsigned) * (size_t)ns * 4);
-  L.part = o; o = al(o + sizeof(double) * (size_t)ns * L.nchunk * (kMrK + 1));
+  L.part = o; o = al(o + sizeof(double) * (size_t)ns * L.nchunk * kMrP);
   L.list = o; o = al(o + sizeof(int) * (size_t)ns * 2);
   L.dev = o; o = al(o + sizeof(MrDev));
   L.total = o;
@@ -455,7 +493,8 @@ extern "C" rsk_status rsk_minres_recycled_batch(rsk_handle h, const rsk_cg_desc*
   MR_ARG(o->iters && o->applies && o->relres_true && o->status && o->m_used, "rsk_minres_recycled_batch: outputs");
   MR_ARG(d->tol > 0 && std::isfinite(d->tol) && d->maxit >= 1 && d->check_every >= 1,
          "rsk_minres_recycled_batch: tol/maxit/check_every");
-  MR_ARG(!(d->flags & RSK_CG_STORE_RES), "rsk_minres_recycled_batch: residual store is a CG option");
+  const bool store = (d->flags & RSK_CG_STORE_RES) != 0;
+  if (store) MR_ARG(d->store && d->store_cap >= 1 && d->lds >= N, "rsk_minres_recycled_batch: store");
   const bool defl = !(d->flags & RSK_CG_NO_DEFLATION) && d->ngroups > 0;
   MR_ARG(d->ngroups >= 0 && d->ngroups <= RSK_MAX_GROUPS, "rsk_minres_recycled_batch: ngroups");
   std::vector<int> grp(ns, 0), hasg(ns, 0), hasg2(ns, 0), m(ns, 0), hasxp(ns, 0);
@@ -511,10 +550,16 @@ extern "C" rsk_status rsk_minres_recycled_batch(rsk_handle h, const rsk_cg_desc*
   hc.tt = hc.kay + (size_t)ns * kMrK;
   hc.sc = hc.tt + (size_t)ns * kMrK;
   hc.rt2 = hc.sc + (size_t)ns * 16;
+  hc.kv = hc.rt2 + (size_t)ns * 2;
   int* in = reinterpret_cast<int*>(base + L.in);
   hc.m = in; hc.status = in + ns; hc.iters = in + 2 * ns; hc.go = in + 3 * ns; hc.group = in + 4 * ns;
   hc.hasg = in + 5 * ns;
   hc.hasg2 = in + 6 * ns;
+  hc.slot = in + 8 * ns;
+  hc.scnt = in + 9 * ns;
+  hc.store = store ? d->store : nullptr;
+  hc.lds = d->lds;
+  hc.store_cap = store ? d->store_cap : 0;
   hc.cnt = reinterpret_cast<unsigned*>(base + L.cnt);
   hc.part = reinterpret_cast<double*>(base + L.part);
   int* dlist = reinterpret_cast<int*>(base + L.list);
@@ -587,10 +632,10 @@ extern "C" rsk_status rsk_minres_recycled_batch(rsk_handle h, const rsk_cg_desc*
 
   // ---- upload per-shift state
   {
-    std::vector<double> dh((size_t)ns * (7 * kMrK + 16 + 2), 0.0);
+    std::vector<double> dh((size_t)ns * (8 * kMrK + 16 + 2), 0.0);
     for (int s = 0; s < ns; ++s) dh[s] = d->gamma_h[s];
     MR_CUDA(cudaMemcpyAsync(dbl, dh.data(), sizeof(double) * dh.size(), cudaMemcpyHostToDevice, st));
-    std::vector<int> ih((size_t)ns * 8, 0);
+    std::vector<int> ih((size_t)ns * 10, 0);
     for (int s = 0; s < ns; ++s) {
       ih[s] = m[s];
       ih[ns + s] = ST_IDLE;
@@ -784,7 +829,9 @@ extern "C" rsk_status rsk_minres_recycled_batch(rsk_handle h, const rsk_cg_desc*
                                                                                          d->Gout, d->ldg);
     MR_CUDA(cudaGetLastError());
   }
+  std::vector<int> scnt_h(ns, 0);
   MR_CUDA(cudaMemcpyAsync(iters.data(), hc.iters, sizeof(int) * ns, cudaMemcpyDeviceToHost, st));
+  MR_CUDA(cudaMemcpyAsync(scnt_h.data(), hc.scnt, sizeof(int) * ns, cudaMemcpyDeviceToHost, st));
   MR_CUDA(cudaStreamSynchronize(st));
   bool partial = false;
   for (int s = 0; s < ns; ++s) {
@@ -793,7 +840,7 @@ extern "C" rsk_status rsk_minres_recycled_batch(rsk_handle h, const rsk_cg_desc*
     o->relres_true[s] = relres[s];
     o->status[s] = final_status[s];
     o->m_used[s] = m[s];
-    if (o->store_count) o->store_count[s] = 0;
+    if (o->store_count) o->store_count[s] = scnt_h[s];
     partial = partial || (final_status[s] != RSK_CG_CONVERGED && final_status[s] != RSK_CG_DEFL_DROPPED);
   }
   int64_t tot = 0;

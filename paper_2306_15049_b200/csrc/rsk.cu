@@ -104,6 +104,7 @@ extern "C" rsk_status rsk_create(rsk_handle* out, int device, int64_t ny, int64_
   h->device = device;
   h->ny = ny;
   h->nx = nx;
+  h->ndata = ny * nx;
   h->r = r;
   for (int i = 0; i < P; ++i) { h->u[i] = u[i]; h->v[i] = v[i]; }
   const int T = 4 * r + 1;
@@ -194,6 +195,13 @@ extern "C" rsk_status rsk_destroy(rsk_handle h) {
   cudaFree(h->scratch);
   cudaFree(h->scal);
   cudaFree(h->aux);
+  cudaFree(h->ct_rp);
+  cudaFree(h->ct_col);
+  cudaFree(h->ct_val);
+  cudaFree(h->ctT_rp);
+  cudaFree(h->ctT_col);
+  cudaFree(h->ctT_val);
+  cudaFree(h->ct_tmp);
   if (h->cg_stream) cudaStreamDestroy(h->cg_stream);
   delete h;
   return RSK_OK;
@@ -217,14 +225,17 @@ extern "C" rsk_status rsk_apply_shifted(rsk_handle h, int nvec, const double* X,
   if (nvec == 0) return RSK_OK;
   RSK_ARG(mode >= RSK_APPLY_SHIFTED && mode <= RSK_APPLY_CT_ONLY, "rsk_apply_shifted: bad mode");
   RSK_ARG(X && Y && aligned8(X) && aligned8(Y), "rsk_apply_shifted: null/misaligned X or Y");
-  RSK_ARG(ldx >= N && ldy >= N, "rsk_apply_shifted: ld < N");
+  // lengths: images N; data vectors (C X output, C^T X input) ndata (= N for the blur)
+  const int64_t nin = (mode == RSK_APPLY_CT_ONLY) ? h->ndata : N;
+  const int64_t nout = (mode == RSK_APPLY_C_ONLY) ? h->ndata : N;
+  RSK_ARG(ldx >= nin && ldy >= nout, "rsk_apply_shifted: ld < vector length");
   RSK_ARG(mode != RSK_APPLY_SHIFTED || gamma, "rsk_apply_shifted: gamma required");
   RSK_ARG(mode != RSK_APPLY_SPLIT || (EY && ldey >= N), "rsk_apply_shifted: EY required for SPLIT");
   {  // X and Y (and EY) must not overlap
     const char* xb = (const char*)X;
-    const char* xe = (const char*)(X + (nvec - 1) * ldx + N);
+    const char* xe = (const char*)(X + (nvec - 1) * ldx + nin);
     const char* yb = (const char*)Y;
-    const char* ye = (const char*)(Y + (nvec - 1) * ldy + N);
+    const char* ye = (const char*)(Y + (nvec - 1) * ldy + nout);
     RSK_ARG(ye <= xb || yb >= xe, "rsk_apply_shifted: X and Y overlap");
     if (mode == RSK_APPLY_SPLIT) {
       const char* eb = (const char*)EY;
@@ -328,13 +339,13 @@ extern "C" rsk_status rsk_make_rhs(rsk_handle h, const double* x_true, const dou
   if (!h) return RSK_EINVAL;
   RSK_ARG(x_true && xi && d && b, "rsk_make_rhs: null pointer");
   RSK_ARG(std::isfinite(nu) && nu >= 0.0, "rsk_make_rhs: bad noise level");
-  const int64_t N = h->ny * h->nx;
-  rsk_status s = rsk_apply_shifted(h, 1, x_true, N, nullptr, d, N, nullptr, N, nullptr, RSK_APPLY_C_ONLY, stream);
+  const int64_t N = h->ny * h->nx, M = h->ndata;   // image and data lengths
+  rsk_status s = rsk_apply_shifted(h, 1, x_true, N, nullptr, d, M, nullptr, N, nullptr, RSK_APPLY_C_ONLY, stream);
   if (s != RSK_OK) return s;
-  RSK_CUDA(launch_batch_dot(h, N, 1, d, N, d, N, h->scal + 0, S(stream)));
-  RSK_CUDA(launch_batch_dot(h, N, 1, xi, N, xi, N, h->scal + 1, S(stream)));
-  RSK_CUDA(launch_scale_noise(N, d, xi, h->scal, nu, d, S(stream)));
-  return rsk_apply_shifted(h, 1, d, N, nullptr, b, N, nullptr, N, nullptr, RSK_APPLY_CT_ONLY, stream);
+  RSK_CUDA(launch_batch_dot(h, M, 1, d, M, d, M, h->scal + 0, S(stream)));
+  RSK_CUDA(launch_batch_dot(h, M, 1, xi, M, xi, M, h->scal + 1, S(stream)));
+  RSK_CUDA(launch_scale_noise(M, d, xi, h->scal, nu, d, S(stream)));
+  return rsk_apply_shifted(h, 1, d, M, nullptr, b, N, nullptr, N, nullptr, RSK_APPLY_CT_ONLY, stream);
 }
 
 extern "C" rsk_status rsk_batch_dot(rsk_handle h, int64_t n, int nv, const double* X, int64_t ldx,
@@ -451,9 +462,10 @@ extern "C" rsk_status rsk_lcurve_norms(rsk_handle h, int nvec, const double* X, 
   const int64_t N = h->ny * h->nx;
   RSK_ARG(nvec >= 1 && X && d && rho && eta2 && scratch && ldx >= N, "rsk_lcurve_norms: bad arguments");
   double* Y = static_cast<double*>(scratch);
-  rsk_status s = rsk_apply_shifted(h, nvec, X, ldx, nullptr, Y, N, nullptr, N, nullptr, RSK_APPLY_C_ONLY, stream);
+  const int64_t M = h->ndata;   // data length (scratch: nvec x ndata)
+  rsk_status s = rsk_apply_shifted(h, nvec, X, ldx, nullptr, Y, M, nullptr, N, nullptr, RSK_APPLY_C_ONLY, stream);
   if (s != RSK_OK) return s;
-  RSK_CUDA(launch_diffnorm_batch(h, nvec, Y, N, d, rho, S(stream)));
+  RSK_CUDA(launch_diffnorm_batch(h, nvec, Y, M, d, rho, S(stream)));
   RSK_CUDA(launch_seminorm_batch(h, nvec, X, ldx, eta2, S(stream), /*do_sqrt=*/1));
   return RSK_OK;
 }
@@ -542,6 +554,7 @@ WsLayout ws_layout(const Handle* h, int ns) {
 extern "C" size_t rsk_cg_workspace_bytes(rsk_handle h, int nshift, int flags) {
   (void)flags;
   if (!h || nshift <= 0) return 0;
+  if (h->ct) return 256;   // CT handles: rsk_minres_recycled_batch only
   return ws_layout(h, nshift).total;
 }
 
@@ -549,6 +562,11 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
                                             size_t ws_bytes, void* stream) {
   if (!h) return RSK_EINVAL;
   RSK_ARG(d && o, "rsk_cg_recycled_batch: null desc/out");
+  if (h->ct) {
+    h->err = "rsk_cg_recycled_batch: the CG device loops embed the stencil apply; CT handles use "
+             "rsk_minres_recycled_batch";
+    return RSK_EUNSUPPORTED;
+  }
   const int ns = d->nshift;
   const int64_t N = h->ny * h->nx;
   RSK_ARG(ns >= 1, "rsk_cg_recycled_batch: nshift < 1");

@@ -116,6 +116,19 @@ struct Handle {
   int sm_count = 148;
   bool sticky = false;
   cudaStream_t cg_stream = nullptr;  // private capture-capable stream of rsk_cg_recycled_batch
+  // CT operator (rsk_create_ct, ct.cu): C as CSR over rays and C^T as CSR over pixels
+  bool ct = false;
+  int64_t ndata = 0;          // length of a data vector d: ny*nx (blur) or rays (CT)
+  double ct_fro = 0.0;        // Frobenius norm of the unscaled matrix
+  int64_t ct_nnz = 0;
+  int ct_tmp_vecs = 0;        // capacity of ct_tmp in data vectors
+  int64_t* ct_rp = nullptr;
+  int* ct_col = nullptr;
+  double* ct_val = nullptr;
+  int64_t* ctT_rp = nullptr;
+  int* ctT_col = nullptr;
+  double* ctT_val = nullptr;
+  double* ct_tmp = nullptr;   // C x of an apply batch
 };
 
 // ---- launchers (apply.cu)
@@ -136,6 +149,7 @@ struct ApplyLaunch {
   int nvec_total;              // vectors addressable in X (and X2): TMA map extent
 };
 cudaError_t launch_apply(Handle* h, const ApplyLaunch& a, cudaStream_t st);
+cudaError_t launch_ct_apply(Handle* h, const ApplyLaunch& a, cudaStream_t st);   // ct.cu
 int apply_tiles(const Handle* h);
 int apply_tile_rows(int r);
 

@@ -437,7 +437,7 @@ __global__ void __launch_bounds__(256) diffnorm_part(int64_t n, const double* __
 
 cudaError_t launch_diffnorm_batch(Handle* h, int nvec, const double* Y, int64_t ldy, const double* d,
                                   double* out, cudaStream_t st) {
-  const int64_t N = h->ny * h->nx;
+  const int64_t N = h->ndata;   // data vectors (= ny * nx for the blur)
   const int nchunk = (int)((N + kChunk - 1) / kChunk);
   if (sizeof(double) * (size_t)nchunk * nvec > h->scratch_bytes) return cudaErrorMemoryAllocation;
   count_launch(); diffnorm_part<<<dim3(nchunk, nvec), 256, 0, st>>>(N, Y, ldy, d, h->scratch, nchunk);

