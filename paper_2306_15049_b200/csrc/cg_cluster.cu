@@ -68,17 +68,19 @@ __device__ __noinline__ void cluster_update_rows(double* __restrict__ Rv, const 
     double2 rn;
     rn.x = loop ? fma(-alpha, wv.x, r0.x) : r0.x - wv.x;
     rn.y = loop ? fma(-alpha, wv.y, r0.y) : r0.y - wv.y;
+    // every load of the row pair is issued before the first FMA that consumes one (the
+    // scheduler otherwise serialises them through one register quad: 11 L2 round trips
+    // per row pair instead of one)
+    double2 zv[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      zv[j] = (j < nw) ? __ldcg(reinterpret_cast<const double2*>(Zs + (int64_t)j * N + i)) : make_double2(0.0, 0.0);
+    const double2 zgv = hg ? __ldg(reinterpret_cast<const double2*>(Zg + i)) : make_double2(0.0, 0.0);
     *reinterpret_cast<double2*>(Rv + i) = rn;
 #pragma unroll
     for (int j = 0; j < 16; ++j)
-      if (j < nw) {
-        const double2 z = *reinterpret_cast<const double2*>(Zs + (int64_t)j * N + i);
-        acc[j] = fma(z.y, rn.y, fma(z.x, rn.x, acc[j]));
-      }
-    if (hg) {
-      const double2 z = __ldg(reinterpret_cast<const double2*>(Zg + i));
-      accg = fma(z.y, rn.y, fma(z.x, rn.x, accg));
-    }
+      if (j < nw) acc[j] = fma(zv[j].y, rn.y, fma(zv[j].x, rn.x, acc[j]));
+    if (hg) accg = fma(zgv.y, rn.y, fma(zgv.x, rn.x, accg));
     accr = fma(rn.y, rn.y, fma(rn.x, rn.x, accr));
   }
   if (((rend - rbeg) & 1) && tid == 0) {
@@ -115,9 +117,7 @@ __device__ __noinline__ void cluster_combine_rows(double* __restrict__ Xv, doubl
                                                   double alpha, double beta, const double* smu, int nw, int hg,
                                                   double rinv) {
   const int tid = threadIdx.x;
-  double mu[16];
-#pragma unroll
-  for (int j = 0; j < 16; ++j) mu[j] = smu[j];
+  const double* mu = smu;   // shared-memory broadcast reads: registers stay free for the loads
   const double mug = hg ? smu[nw] : 0.0;
   auto row1 = [&](int64_t i) {
     const double pv = Pv[i];
@@ -144,19 +144,20 @@ __device__ __noinline__ void cluster_combine_rows(double* __restrict__ Xv, doubl
     }
     if (upd_p) {
       const double2 rv = *reinterpret_cast<const double2*>(Rv + i);
+      double2 wv[16];   // all loads first (see cluster_update_rows)
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        wv[j] = (j < nw) ? __ldcg(reinterpret_cast<const double2*>(Wg + (int64_t)j * ldw + i)) : make_double2(0.0, 0.0);
+      const double2 g = hg ? __ldcg(reinterpret_cast<const double2*>(Gh + i)) : make_double2(0.0, 0.0);
       double ax = fma(beta, pv.x, rv.x), ay = fma(beta, pv.y, rv.y);
       double bx = 0.0, by = 0.0;   // two partial chains (even / odd j) halve the FMA latency chain
 #pragma unroll
       for (int j = 0; j < 16; ++j)
         if (j < nw) {
-          const double2 w = __ldg(reinterpret_cast<const double2*>(Wg + (int64_t)j * ldw + i));
-          if (j & 1) { bx = fma(-mu[j], w.x, bx); by = fma(-mu[j], w.y, by); }
-          else { ax = fma(-mu[j], w.x, ax); ay = fma(-mu[j], w.y, ay); }
+          if (j & 1) { bx = fma(-mu[j], wv[j].x, bx); by = fma(-mu[j], wv[j].y, by); }
+          else { ax = fma(-mu[j], wv[j].x, ax); ay = fma(-mu[j], wv[j].y, ay); }
         }
-      if (hg) {
-        const double2 g = __ldg(reinterpret_cast<const double2*>(Gh + i));
-        bx = fma(-mug, g.x, bx); by = fma(-mug, g.y, by);
-      }
+      if (hg) { bx = fma(-mug, g.x, bx); by = fma(-mug, g.y, by); }
       *reinterpret_cast<double2*>(Pv + i) = make_double2(ax + bx, ay + by);
       if (sto) *reinterpret_cast<double2*>(sto + i) = make_double2(rv.x * rinv, rv.y * rinv);
     }
