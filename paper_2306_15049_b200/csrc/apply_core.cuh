@@ -344,7 +344,7 @@ struct ApplyCore {
         const bool vec = ((nx & 1) == 0);
         const int lc = cbl + 2 * q;
         const int gj = c0 + lc;
-        constexpr int EJ = C::RBY;   // all weight loads issued before the y-pass DMMAs
+        constexpr int EJ = C::RBY > 4 ? 4 : C::RBY;   // weight loads of the first EJ row blocks go out before the y-pass DMMAs
         double wl[EJ], wm[EJ], wr[EJ], yu0[EJ], yu1[EJ], yd0[EJ], yd1[EJ];
         auto load_w = [&](int j, int jj) {
           const int gi = r0 + j * 8 + g;

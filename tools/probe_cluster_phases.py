@@ -33,3 +33,11 @@ names = ["A apply", "cluster barriers", "alpha", "B rows+reduce", "z+status", "C
 tot = sum(a[i] for i in range(6)) / n / 1e3
 print(f"{cfg.name} K_out={K}: cluster 0 rank 0, {int(n)} iterations, {tot:.2f} us per iteration:",
       ", ".join(f"{nm} {a[i] / n / 1e3:.2f} us" for i, nm in enumerate(names)), flush=True)
+if os.environ.get("RSK_APPLY_PROF"):
+    lib.rsk_debug_apply_prof.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int]
+    b = (ctypes.c_double * 8)()
+    lib.rsk_debug_apply_prof(b, 0)
+    names = ["issue->wait", "TMA wait", "x-pass+sync", "y-pass+epilogue", "dot+ticket", "end sync", "", "entry"]
+    print("apply item phases, block %s, summed over both runs (us):" % os.environ["RSK_APPLY_PROF"],
+          ", ".join(f"{nm} {b[i] / 1e3:.1f}" for i, nm in enumerate(names) if nm), flush=True)
+    print("per iteration (2 x %d iterations): " % int(n), ", ".join(f"{nm} {b[i] / 1e3 / (2 * n):.2f}" for i, nm in enumerate(names) if nm))
