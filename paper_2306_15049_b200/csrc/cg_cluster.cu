@@ -176,8 +176,12 @@ __global__ void __launch_bounds__(kAT, 1) cg_cluster_kernel(const __grid_constan
   cgx::cluster_group cl = cgx::this_cluster();
   const int crank = (int)cl.block_rank();
   const int csz = (int)cl.num_blocks();
-  __shared__ double s_part[kCV];       // this CTA's partial sums (read by the whole cluster)
+  __shared__ double s_part[kCV];       // this CTA's partial sums (pushed to the whole cluster)
   __shared__ double s_dot;
+  // every CTA's partials, PUSHED here by their owners before the cluster barrier (remote
+  // stores are fire-and-forget; after the barrier the reads are local shared memory)
+  __shared__ double s_dots[16];
+  __shared__ double s_parts[16][kCV];
   __shared__ int s_next;
   __shared__ double s_z[kCV];
   __shared__ double s_red[kCW][kCV];
@@ -260,13 +264,14 @@ __global__ void __launch_bounds__(kAT, 1) cg_cluster_kernel(const __grid_constan
       __syncthreads();
       mark(-1);
       Core::run(P.ap, smem, ibeg, iend, 1, pp, s_list, s_lmode, &s_dot);
+      if (tid < csz) *cl.map_shared_rank(&s_dots[crank], tid) = s_dot;   // push p.w partial
       mark(0);
       cl_sync();
       mark(1);
       double alpha = 0.0;
       if (mode == ST_ACTIVE) {
-        if (warp == 0) {   // the 16 CTA partials through DSMEM, all in flight at once
-          const double v = (lane < csz) ? *cl.map_shared_rank(&s_dot, lane) : 0.0;
+        if (warp == 0) {   // the 16 CTA partials (pushed), fixed shuffle tree in rank order
+          const double v = (lane < csz) ? s_dots[lane] : 0.0;
           const double pi = warp_sum(v);
           if (lane == 0) {
             s_brk = !(pi > 0.0) || !isfinite(pi);
@@ -288,13 +293,18 @@ __global__ void __launch_bounds__(kAT, 1) cg_cluster_kernel(const __grid_constan
         for (int w = 0; w < kCW; ++w) t += s_red[w][tid];
         s_part[tid] = t;
       }
+      __syncthreads();
+      for (int e = tid; e < csz * kCV; e += kAT) {   // push slot e % kCV to rank e / kCV
+        const int c = e / kCV, slot = e - c * kCV;
+        if (slot < m || slot == kMaxM) *cl.map_shared_rank(&s_parts[crank][slot], c) = s_part[slot];
+      }
       cl_sync();
       mark(1);
       for (int e = tid; e < 32 * 16; e += kAT) {   // slot j = e / 16 from rank c = e % 16
         const int j = e >> 4, c = e & 15;
         const int slot = (j < kCV) ? j : kMaxM;
         const bool need = (j < m || j == kMaxM) && j < kCV;
-        double v = (need && c < csz) ? *cl.map_shared_rank(&s_part[slot], c) : 0.0;
+        double v = (need && c < csz) ? s_parts[c][slot] : 0.0;
 #pragma unroll
         for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);   // within the 16-lane half
         if (need && c == 0) s_z[j] = v;
