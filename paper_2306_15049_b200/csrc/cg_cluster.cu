@@ -48,19 +48,20 @@ __device__ __forceinline__ void cl_sync() {
 // r = r - alpha w (loop) or b - w (confirm) over this CTA's rows; per-warp sums of
 // z_j = Z_j . r (j < nw), ZGhat . r (slot nw) and r . r (slot kMaxM) into red[warp][slot].
 // Separate function: its own register allocation, not the apply's.
-__device__ __noinline__ void cluster_update_rows(double* __restrict__ Rv, const double* __restrict__ Wv,
+template <int MW, int UNR>
+__device__ __noinline__ void cluster_update_rows_t(double* __restrict__ Rv, const double* __restrict__ Wv,
                                                  const double* __restrict__ b, const double* __restrict__ Zs,
                                                  const double* __restrict__ Zg, int64_t N, int64_t rbeg,
                                                  int64_t rend, bool loop, double alpha, int nw, int hg,
                                                  double* red) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  double acc[16], accg = 0.0, accr = 0.0;
+  double acc[MW], accg = 0.0, accr = 0.0;
 #pragma unroll
-  for (int j = 0; j < 16; ++j) acc[j] = 0.0;
+  for (int j = 0; j < MW; ++j) acc[j] = 0.0;
   // pairs of rows through 16-byte loads (rows rbeg.. are even-aligned; an odd tail row
   // takes the scalar path)
   const int64_t npair = (rend - rbeg) >> 1;
-#pragma unroll 2
+#pragma unroll UNR
   for (int64_t q = tid; q < npair; q += kAT) {
     const int64_t i = rbeg + 2 * q;
     const double2 wv = *reinterpret_cast<const double2*>(Wv + i);
@@ -71,14 +72,14 @@ __device__ __noinline__ void cluster_update_rows(double* __restrict__ Rv, const 
     // every load of the row pair is issued before the first FMA that consumes one (the
     // scheduler otherwise serialises them through one register quad: 11 L2 round trips
     // per row pair instead of one)
-    double2 zv[16];
+    double2 zv[MW];
 #pragma unroll
-    for (int j = 0; j < 16; ++j)
+    for (int j = 0; j < MW; ++j)
       zv[j] = (j < nw) ? __ldcg(reinterpret_cast<const double2*>(Zs + (int64_t)j * N + i)) : make_double2(0.0, 0.0);
     const double2 zgv = hg ? __ldg(reinterpret_cast<const double2*>(Zg + i)) : make_double2(0.0, 0.0);
     *reinterpret_cast<double2*>(Rv + i) = rn;
 #pragma unroll
-    for (int j = 0; j < 16; ++j)
+    for (int j = 0; j < MW; ++j)
       if (j < nw) acc[j] = fma(zv[j].y, rn.y, fma(zv[j].x, rn.x, acc[j]));
     if (hg) accg = fma(zgv.y, rn.y, fma(zgv.x, rn.x, accg));
     accr = fma(rn.y, rn.y, fma(rn.x, rn.x, accr));
@@ -89,13 +90,13 @@ __device__ __noinline__ void cluster_update_rows(double* __restrict__ Rv, const 
     const double rn = loop ? fma(-alpha, wv, Rv[i]) : __ldg(b + i) - wv;
     Rv[i] = rn;
 #pragma unroll
-    for (int j = 0; j < 16; ++j)
+    for (int j = 0; j < MW; ++j)
       if (j < nw) acc[j] = fma(Zs[(int64_t)j * N + i], rn, acc[j]);
     if (hg) accg = fma(__ldg(Zg + i), rn, accg);
     accr = fma(rn, rn, accr);
   }
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
+  for (int j = 0; j < MW; ++j) {
     if (j < nw) {
       const double v = warp_sum(acc[j]);
       if (lane == 0) red[warp * kCV + j] = v;
@@ -109,8 +110,17 @@ __device__ __noinline__ void cluster_update_rows(double* __restrict__ Rv, const 
   if (lane == 0) red[warp * kCV + kMaxM] = v;
 }
 
+// nw <= 8 (the configs' |J|): half the registers per row pair, four row pairs in flight
+__device__ __forceinline__ void cluster_update_rows(double* Rv, const double* Wv, const double* b, const double* Zs,
+                                                    const double* Zg, int64_t N, int64_t rbeg, int64_t rend,
+                                                    bool loop, double alpha, int nw, int hg, double* red) {
+  if (nw <= 8) cluster_update_rows_t<8, 4>(Rv, Wv, b, Zs, Zg, N, rbeg, rend, loop, alpha, nw, hg, red);
+  else cluster_update_rows_t<16, 2>(Rv, Wv, b, Zs, Zg, N, rbeg, rend, loop, alpha, nw, hg, red);
+}
+
 // x += alpha p (upd_x); p = r + beta p - W mu_W - ghat mu_g; residual store (upd_p)
-__device__ __noinline__ void cluster_combine_rows(double* __restrict__ Xv, double* __restrict__ Pv,
+template <int MW, int UNR>
+__device__ __noinline__ void cluster_combine_rows_t(double* __restrict__ Xv, double* __restrict__ Pv,
                                                   const double* __restrict__ Rv, const double* __restrict__ Wg,
                                                   int64_t ldw, const double* __restrict__ Gh, double* sto,
                                                   int64_t rbeg, int64_t rend, bool upd_x, bool upd_p,
@@ -126,7 +136,7 @@ __device__ __noinline__ void cluster_combine_rows(double* __restrict__ Xv, doubl
       const double rv = Rv[i];
       double pn = fma(beta, pv, rv);
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
+      for (int j = 0; j < MW; ++j)
         if (j < nw) pn = fma(-mu[j], __ldg(Wg + (int64_t)j * ldw + i), pn);
       if (hg) pn = fma(-mug, __ldg(Gh + i), pn);
       Pv[i] = pn;
@@ -134,7 +144,7 @@ __device__ __noinline__ void cluster_combine_rows(double* __restrict__ Xv, doubl
     }
   };
   const int64_t npair = (rend - rbeg) >> 1;
-#pragma unroll 2
+#pragma unroll UNR
   for (int64_t q = tid; q < npair; q += kAT) {
     const int64_t i = rbeg + 2 * q;
     const double2 pv = *reinterpret_cast<const double2*>(Pv + i);
@@ -144,15 +154,15 @@ __device__ __noinline__ void cluster_combine_rows(double* __restrict__ Xv, doubl
     }
     if (upd_p) {
       const double2 rv = *reinterpret_cast<const double2*>(Rv + i);
-      double2 wv[16];   // all loads first (see cluster_update_rows)
+      double2 wv[MW];   // all loads first (see cluster_update_rows)
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
+      for (int j = 0; j < MW; ++j)
         wv[j] = (j < nw) ? __ldcg(reinterpret_cast<const double2*>(Wg + (int64_t)j * ldw + i)) : make_double2(0.0, 0.0);
       const double2 g = hg ? __ldcg(reinterpret_cast<const double2*>(Gh + i)) : make_double2(0.0, 0.0);
       double ax = fma(beta, pv.x, rv.x), ay = fma(beta, pv.y, rv.y);
       double bx = 0.0, by = 0.0;   // two partial chains (even / odd j) halve the FMA latency chain
 #pragma unroll
-      for (int j = 0; j < 16; ++j)
+      for (int j = 0; j < MW; ++j)
         if (j < nw) {
           if (j & 1) { bx = fma(-mu[j], wv[j].x, bx); by = fma(-mu[j], wv[j].y, by); }
           else { ax = fma(-mu[j], wv[j].x, ax); ay = fma(-mu[j], wv[j].y, ay); }
@@ -163,6 +173,16 @@ __device__ __noinline__ void cluster_combine_rows(double* __restrict__ Xv, doubl
     }
   }
   if (((rend - rbeg) & 1) && tid == 0) row1(rend - 1);
+}
+
+__device__ __forceinline__ void cluster_combine_rows(double* Xv, double* Pv, const double* Rv, const double* Wg,
+                                                     int64_t ldw, const double* Gh, double* sto, int64_t rbeg,
+                                                     int64_t rend, bool upd_x, bool upd_p, double alpha, double beta,
+                                                     const double* smu, int nw, int hg, double rinv) {
+  if (nw <= 8)
+    cluster_combine_rows_t<8, 4>(Xv, Pv, Rv, Wg, ldw, Gh, sto, rbeg, rend, upd_x, upd_p, alpha, beta, smu, nw, hg, rinv);
+  else
+    cluster_combine_rows_t<16, 2>(Xv, Pv, Rv, Wg, ldw, Gh, sto, rbeg, rend, upd_x, upd_p, alpha, beta, smu, nw, hg, rinv);
 }
 
 // taller tiles for the cluster loop: a 256-wide image (C2) is 16 tiles of 64 rows, one per
