@@ -12,6 +12,9 @@
 //   ct_adj   y = C^T t + gamma E_k x (or the SPLIT / C^T-only forms), one thread per pixel,
 //            its transpose row in ray order, the weighted 5-point E stencil fused, and the
 //            x . y partial per CTA (fixed-order reduction by apply_dot_reduce's rule)
+// Both serve up to 8 vectors of a batch per pass over the matrix entries (the CSR pair is
+// read once per 8 shifts, not once per shift); each vector's sums keep the one-vector
+// order, so results do not depend on the batch.
 // Every librsk call that goes through launch_apply (rsk_apply_shifted, the recycling
 // MINRES batch, the L-curve norms, make_rhs) works on a CT handle; the CG device loops
 // embed the stencil apply and reject it.
@@ -34,43 +37,93 @@ namespace {
 
 constexpr int kCtT = 256;
 
-// t[li][ray] = sum_k val[k] x[li][col[k]]  (warp per ray)
+constexpr int kVB = 8;   // vectors per CTA: one pass over a matrix row serves all of them
+
+// t[li][ray] = sum_k val[k] x[li][col[k]] for the kVB vectors li0 + b of this CTA (warp per
+// ray; each vector's sum in the same lane-strided order and shuffle tree as for one vector)
 __global__ void __launch_bounds__(kCtT) ct_fwd(int64_t m, const int64_t* __restrict__ rp, const int* __restrict__ col,
                                                const double* __restrict__ val, const double* __restrict__ X,
-                                               int64_t ldx, const int* __restrict__ list, double* __restrict__ T,
-                                               int64_t ldt) {
-  const int li = blockIdx.y;
-  const int s = list ? list[li] : li;
-  const double* x = X + (int64_t)s * ldx;
+                                               int64_t ldx, const int* __restrict__ list, int nl,
+                                               double* __restrict__ T, int64_t ldt) {
+  const int li0 = blockIdx.y * kVB;
+  const int nvb = min(kVB, nl - li0);
+  const double* x[kVB];
+#pragma unroll
+  for (int b = 0; b < kVB; ++b) {
+    const int li = li0 + (b < nvb ? b : 0);
+    x[b] = X + (int64_t)(list ? list[li] : li) * ldx;
+  }
   const int lane = threadIdx.x & 31;
   const int64_t ray = (int64_t)blockIdx.x * (kCtT / 32) + (threadIdx.x >> 5);
   if (ray >= m) return;
-  double acc = 0.0;
-  for (int64_t k = rp[ray] + lane; k < rp[ray + 1]; k += 32) acc = fma(val[k], __ldg(x + col[k]), acc);
+  double acc[kVB];
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
-  if (lane == 0) T[(int64_t)li * ldt + ray] = acc;
+  for (int b = 0; b < kVB; ++b) acc[b] = 0.0;
+  for (int64_t k = rp[ray] + lane; k < rp[ray + 1]; k += 32) {
+    const double v = val[k];
+    const int c = col[k];
+#pragma unroll
+    for (int b = 0; b < kVB; ++b)
+      if (b < nvb) acc[b] = fma(v, __ldg(x[b] + c), acc[b]);
+  }
+#pragma unroll
+  for (int b = 0; b < kVB; ++b) {
+    if (b >= nvb) break;
+    double t = acc[b];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if (lane == 0) T[(int64_t)(li0 + b) * ldt + ray] = t;
+  }
 }
 
-// y = C^T t (+ gamma E x | EY = E x), x . y partials (mode as RSK_APPLY_*)
+// y = C^T t (+ gamma E x | EY = E x), x . y partials (mode as RSK_APPLY_*): warp per pixel
+// (lane-strided transpose row, fixed shuffle tree), kVB vectors per pass over the row; lane b
+// finishes vector b (E stencil, gamma combine, store)
 __global__ void __launch_bounds__(kCtT) ct_adj(int n, const int64_t* __restrict__ rp, const int* __restrict__ col,
                                                const double* __restrict__ val, const double* __restrict__ T,
-                                               int64_t ldt, const int* __restrict__ list, int t_by_sid,
+                                               int64_t ldt, const int* __restrict__ list, int nl, int t_by_sid,
                                                const double* __restrict__ X, int64_t ldx, double* __restrict__ Y,
                                                int64_t ldy, double* __restrict__ EY, int64_t ldey,
                                                const double* __restrict__ gamma, const double* __restrict__ wx,
                                                const double* __restrict__ wy, int mode, double* __restrict__ part) {
-  const int li = blockIdx.y;
-  const int s = list ? list[li] : li;
+  const int li0 = blockIdx.y * kVB;
+  const int nvb = min(kVB, nl - li0);
   const int64_t N = (int64_t)n * n;
-  const int64_t p = (int64_t)blockIdx.x * kCtT + threadIdx.x;
-  const double* t = T + (int64_t)(t_by_sid ? s : li) * ldt;
-  double yv = 0.0;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t p = (int64_t)blockIdx.x * (kCtT / 32) + warp;
+  const double* t[kVB];
+#pragma unroll
+  for (int b = 0; b < kVB; ++b) {
+    const int li = li0 + (b < nvb ? b : 0);
+    t[b] = T + (int64_t)(t_by_sid ? (list ? list[li] : li) : li) * ldt;
+  }
+  double a[kVB];
+#pragma unroll
+  for (int b = 0; b < kVB; ++b) a[b] = 0.0;
   if (p < N) {
-    double a = 0.0;
-    for (int64_t k = rp[p]; k < rp[p + 1]; ++k) a = fma(val[k], t[col[k]], a);
-    yv = a;
-    if (mode == RSK_APPLY_SHIFTED || mode == RSK_APPLY_SPLIT) {
+    for (int64_t k = rp[p] + lane; k < rp[p + 1]; k += 32) {
+      const double v = val[k];
+      const int c = col[k];
+#pragma unroll
+      for (int b = 0; b < kVB; ++b)
+        if (b < nvb) a[b] = fma(v, t[b][c], a[b]);
+    }
+  }
+  double mine = 0.0;   // lane b keeps vector b's row sum
+#pragma unroll
+  for (int b = 0; b < kVB; ++b) {
+    double v = a[b];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == b) mine = v;
+  }
+  const bool withE = (mode == RSK_APPLY_SHIFTED || mode == RSK_APPLY_SPLIT);
+  double dotv = 0.0;
+  if (p < N && lane < nvb) {
+    const int li = li0 + lane;
+    const int s = list ? list[li] : li;
+    double yv = mine;
+    if (withE) {
       const double* x = X + (int64_t)s * ldx;
       const int i = (int)(p / n), j = (int)(p - (int64_t)i * n);
       const double xc = x[p];
@@ -81,20 +134,18 @@ __global__ void __launch_bounds__(kCtT) ct_adj(int n, const int64_t* __restrict_
       if (i > 0) e += wy[p - n] * (xc - x[p - n]);
       if (mode == RSK_APPLY_SHIFTED) yv = fma(gamma[s], e, yv);
       else EY[(int64_t)s * ldey + p] = e;
+      dotv = xc * yv;
     }
     Y[(int64_t)s * ldy + p] = yv;
   }
-  if (part) {   // x . y partial of this CTA (SHIFTED / SPLIT: X is the image the apply acts on)
-    double v = (p < N && (mode == RSK_APPLY_SHIFTED || mode == RSK_APPLY_SPLIT)) ? X[(int64_t)s * ldx + p] * yv : 0.0;
-    __shared__ double red[kCtT / 32];
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  if (part) {   // x . y partial of this CTA per vector: its 8 pixels (warps) in order
+    __shared__ double red[kCtT / 32][kVB];
+    if (lane < kVB) red[warp][lane] = dotv;
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < nvb) {
       double tot = 0.0;
-      for (int w = 0; w < kCtT / 32; ++w) tot += red[w];
-      part[(int64_t)li * gridDim.x + blockIdx.x] = tot;
+      for (int w = 0; w < kCtT / 32; ++w) tot += red[w][threadIdx.x];
+      part[(int64_t)(li0 + threadIdx.x) * gridDim.x + blockIdx.x] = tot;
     }
   }
 }
@@ -172,7 +223,7 @@ cudaError_t launch_ct_apply(Handle* h, const ApplyLaunch& a, cudaStream_t st) {
   const int n = (int)h->nx;
   const int64_t N = (int64_t)n * n, m = h->ndata;
   const int mode = a.mode;
-  const int nb = (int)((N + kCtT - 1) / kCtT);
+  const int nb = (int)((N + kCtT / 32 - 1) / (kCtT / 32));   // ct_adj: a warp per pixel
   for (int l0 = 0; l0 < a.nlist; l0 += h->ct_tmp_vecs) {
     const int nl = std::min(h->ct_tmp_vecs, a.nlist - l0);
     const int* lst = a.list ? a.list + l0 : nullptr;
@@ -184,8 +235,8 @@ cudaError_t launch_ct_apply(Handle* h, const ApplyLaunch& a, cudaStream_t st) {
     double* xd = (a.xdoty && !a.list) ? a.xdoty + l0 : a.xdoty;
     if (mode == RSK_APPLY_C_ONLY) {   // (C_ONLY writes by position: no list, checked above)
       count_launch();
-      ct_fwd<<<dim3((unsigned)((m + 7) / 8), nl), kCtT, 0, st>>>(m, h->ct_rp, h->ct_col, h->ct_val, X, a.ldx, lst,
-                                                                  Y, a.ldy);
+      ct_fwd<<<dim3((unsigned)((m + 7) / 8), (nl + kVB - 1) / kVB), kCtT, 0, st>>>(m, h->ct_rp, h->ct_col, h->ct_val, X,
+                                                                                  a.ldx, lst, nl, Y, a.ldy);
       continue;
     }
     const double* T = X;
@@ -193,8 +244,8 @@ cudaError_t launch_ct_apply(Handle* h, const ApplyLaunch& a, cudaStream_t st) {
     int t_by_sid = 1;
     if (mode != RSK_APPLY_CT_ONLY) {
       count_launch();
-      ct_fwd<<<dim3((unsigned)((m + 7) / 8), nl), kCtT, 0, st>>>(m, h->ct_rp, h->ct_col, h->ct_val, X, a.ldx, lst,
-                                                                  h->ct_tmp, m);
+      ct_fwd<<<dim3((unsigned)((m + 7) / 8), (nl + kVB - 1) / kVB), kCtT, 0, st>>>(m, h->ct_rp, h->ct_col, h->ct_val, X,
+                                                                                  a.ldx, lst, nl, h->ct_tmp, m);
       T = h->ct_tmp;
       ldt = m;
       t_by_sid = 0;
@@ -205,8 +256,9 @@ cudaError_t launch_ct_apply(Handle* h, const ApplyLaunch& a, cudaStream_t st) {
       part = h->scratch;
     }
     count_launch();
-    ct_adj<<<dim3((unsigned)nb, nl), kCtT, 0, st>>>(n, h->ctT_rp, h->ctT_col, h->ctT_val, T, ldt, lst, t_by_sid, X,
-                                                    a.ldx, Y, a.ldy, EY, a.ldey, gam, h->wx, h->wy, mode, part);
+    ct_adj<<<dim3((unsigned)nb, (nl + kVB - 1) / kVB), kCtT, 0, st>>>(n, h->ctT_rp, h->ctT_col, h->ctT_val, T, ldt, lst,
+                                                                      nl, t_by_sid, X, a.ldx, Y, a.ldy, EY, a.ldey, gam,
+                                                                      h->wx, h->wy, mode, part);
     if (xd) {
       count_launch();
       ct_dot_reduce<<<nl, 32, 0, st>>>(part, nb, lst, xd);
