@@ -123,3 +123,19 @@ def test_host_stabilize_small_cut():
     assert nk == int(np.sum(1.0 / np.logspace(0, -16, 10) < 1e10))
     Zs3, nk3 = rsk.stabilize_small(R, np.ones(10), 1e10, 3)
     assert nk3 == 3
+
+
+def test_create_ct_argument_errors_need_no_device(lib):
+    """rsk_create_ct rejects bad geometry before touching the device (EINVAL = 1)."""
+    import ctypes as C
+    from paper_2306_15049_b200 import _lib as L
+    h = C.c_void_p()
+    ang = np.arange(1, 11, dtype=np.float64)
+    hp = ang.ctypes.data_as(C.POINTER(C.c_double))
+    assert lib.rsk_create_ct(C.byref(h), 0, 1, 10, hp, 8, 0) == L.RSK_EINVAL         # n < 2
+    assert lib.rsk_create_ct(C.byref(h), 0, 16, 0, hp, 8, 0) == L.RSK_EINVAL         # no angles
+    assert lib.rsk_create_ct(C.byref(h), 0, 16, 10, hp, 0, 0) == L.RSK_EINVAL        # no bins
+    bad = ang.copy(); bad[3] = np.nan
+    assert lib.rsk_create_ct(C.byref(h), 0, 16, 10, bad.ctypes.data_as(C.POINTER(C.c_double)), 8, 0) == L.RSK_EINVAL
+    assert lib.rsk_ct_info(None, None, None, None) == L.RSK_EINVAL
+    assert lib.rsk_minres_workspace_bytes(None, 4, 9) == 0

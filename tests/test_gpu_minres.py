@@ -197,3 +197,52 @@ def test_nested_solve_minres_stepwise(torch_dev, local):
         wx, wy = ops.irn_weights(xstar, cfg.tau)
         st = opipe.StepState(k + 1, wx, wy, rs.X, rs.G, rs.V_i1)
     assert np.mean(np.concatenate(all_d) <= 2) >= 0.95, all_d
+
+
+def test_minres_store_spans_the_cg_residual_space_and_error_paths(torch_dev):
+    """RSK_CG_STORE_RES with MINRES: the stored normalised Lanczos vectors equal the
+    oracle's (up to rounding), span the same Krylov space as the CG's stored residuals,
+    and the count is min(cap, iterations); a second carried column is rejected by the CG
+    and a CT handle by rsk_cg_recycled_batch."""
+    torch, dev = torch_dev
+    from paper_2306_15049_b200 import _lib as L
+    from paper_2306_15049_b200.pipeline import GpuSolver, STORE_CAP
+    from paper_2306_15049_b200.rsk import RskError
+    cfg = dataclasses.replace(S.CONFIGS["C1"], tol=1e-10)
+    inp = S.make_inputs(cfg)
+    sol = GpuSolver(cfg, inp["psf"], inp["gamma"])
+    sol.set_data(_t(torch, dev, inp["x_true"].ravel()), _t(torch, dev, inp["xi"].ravel()))
+    sol.reset_weights()
+    N = cfg.N
+    st_m = torch.empty(STORE_CAP, N, dtype=torch.float64, device=dev)
+    st_c = torch.empty(STORE_CAP, N, dtype=torch.float64, device=dev)
+    Xm = torch.zeros(1, N, dtype=torch.float64, device=dev)
+    Xc = torch.zeros(1, N, dtype=torch.float64, device=dev)
+    rm = sol.cg([0], Xm, [0], store=st_m, inner="minres")
+    rc_ = sol.cg([0], Xc, [0], store=st_c)
+    km, kc = int(rm["store_count"][0]), int(rc_["store_count"][0])
+    assert km == min(STORE_CAP, int(rm["iters"][0])) and kc == min(STORE_CAP, int(rc_["iters"][0]))
+    b = sol.b.cpu().numpy()
+    wx, wy = ops.identity_weights(cfg.n)
+    A = lambda v: ops.apply_shifted(inp["psf"], wx, wy, inp["gamma"][0], v.reshape(cfg.n, cfg.n)).ravel()
+    ref = omr.recycled_minres(A, b, tol=cfg.tol, store_cap=STORE_CAP)
+    Vm = st_m[:km].cpu().numpy()
+    assert len(ref.store) == km
+    for j in range(min(km, 10)):       # early Lanczos vectors: rounding has not grown yet
+        assert np.linalg.norm(Vm[j] - ref.store[j]) <= 1e-9, j
+    k = min(km, kc, 20)
+    Qm, _ = np.linalg.qr(Vm[:k].T)
+    Qc, _ = np.linalg.qr(st_c[:k].cpu().numpy().T)
+    s = np.linalg.svd(Qm.T @ Qc, compute_uv=False)
+    assert s.min() >= 1 - 1e-6            # the same Krylov space K_k(A_g, b)
+    # a second carried column is MINRES-only
+    G2 = torch.zeros(1, N, dtype=torch.float64, device=dev)
+    with pytest.raises(RskError):
+        sol.cg([0], Xc, [0], ghat2=(G2, G2, np.ones(1, np.int32)),
+               groups=dict(W=[G2], AW=[G2], EW=[G2], of_shift=np.zeros(1, np.int32)))
+    # CT handles: the CG device loops embed the stencil apply
+    ctcfg = dataclasses.replace(S.CONFIGS["C6"], n=16, n_angles=20, M=2, inner="minres")
+    ct = GpuSolver(ctcfg, None, S.gamma_ladder(ctcfg))
+    X2 = torch.zeros(1, ctcfg.N, dtype=torch.float64, device=dev)
+    with pytest.raises(RskError):
+        ct.cg([0], X2, [0])
