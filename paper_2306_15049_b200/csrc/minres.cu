@@ -26,9 +26,11 @@
 
 #include <cuda_runtime.h>
 
+#include "apply_core.cuh"
 #include "rsk_internal.h"
 
 namespace rsk {
+bool fill_apply_params(Handle* h, const ApplyLaunch& a, ApplyParams& prm, int ty_override);   // apply.cu
 namespace {
 
 constexpr int kMrK = RSK_MAX_LOCAL;   // local columns per shift (|J| + 1 <= 17)
@@ -87,15 +89,15 @@ struct MrDev {
 // MINRES scalars (index into sc[s*16 + .])
 enum { S_BETA = 0, S_EPS, S_DBAR, S_CS, S_SN, S_PHIBAR, S_OLDEPS, S_DELTA, S_DENOM, S_PHI, S_INVB, S_XI };
 
-__device__ __forceinline__ double wsum(double v) {
+__device__ __forceinline__ double mr_wsum(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   return v;
 }
 
 // Sum v over the CTA (fixed tree); result valid in thread 0.
-__device__ __forceinline__ double block_sum(double v, double* sh) {
-  v = wsum(v);
+__device__ __forceinline__ double mr_block_sum(double v, double* sh) {
+  v = mr_wsum(v);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   __syncthreads();
   if (lane == 0) sh[wid] = v;
@@ -127,7 +129,7 @@ __device__ __forceinline__ bool last_cta(unsigned* c, int nchunk) {
 __device__ __forceinline__ double chunk_sum(const MrDev* g, int s, int j, double* sh) {
   double t = 0.0;
   for (int c = threadIdx.x; c < g->nchunk; c += kMrT) t += g->part[((int64_t)s * g->nchunk + c) * kMrP + j];
-  return block_sum(t, sh);
+  return mr_block_sum(t, sh);
 }
 
 // c[s] = K_s^T src_s (src = Wv in the loop, R0 at a start), fixed-order reduction.
@@ -162,10 +164,10 @@ __global__ void __launch_bounds__(kMrT) mr_kdots(MrDev* __restrict__ g, const in
 #pragma unroll
   for (int j = 0; j < kMrK; ++j) {
     if (j < m) {
-      const double t = block_sum(acc[j], sh);
+      const double t = mr_block_sum(acc[j], sh);
       if (threadIdx.x == 0) part[j] = t;
       if (!start) {
-        const double u = block_sum(acv[j], sh);
+        const double u = mr_block_sum(acv[j], sh);
         if (threadIdx.x == 0) part[kMrK + j] = u;
       }
     }
@@ -214,7 +216,7 @@ __global__ void __launch_bounds__(kMrT) mr_project(MrDev* __restrict__ g, const 
     nrm = fma(t, t, nrm);
   }
   __shared__ double sh[kMrT / 32];
-  const double tot = block_sum(nrm, sh);
+  const double tot = mr_block_sum(nrm, sh);
   double* part = g->part + ((int64_t)s * g->nchunk + chunk) * kMrP;
   if (threadIdx.x == 0) part[kMrK] = tot;
   if (!last_cta(&g->cnt[s * 4 + 1], g->nchunk)) return;
@@ -314,7 +316,7 @@ __global__ void __launch_bounds__(kMrT) mr_start_proj(MrDev* __restrict__ g, con
     nrm = fma(t, t, nrm);
   }
   __shared__ double sh[kMrT / 32];
-  const double tot = block_sum(nrm, sh);
+  const double tot = mr_block_sum(nrm, sh);
   double* part = g->part + ((int64_t)s * g->nchunk + chunk) * kMrP;
   if (threadIdx.x == 0) part[kMrK] = tot;
   if (!last_cta(&g->cnt[s * 4 + 1], g->nchunk)) return;
@@ -401,7 +403,7 @@ __global__ void __launch_bounds__(kMrT) mr_resid(MrDev* __restrict__ g, const in
     nrm = fma(t, t, nrm);
   }
   __shared__ double sh[kMrT / 32];
-  const double tot = block_sum(nrm, sh);
+  const double tot = mr_block_sum(nrm, sh);
   if (threadIdx.x == 0) g->part[((int64_t)s * g->nchunk + chunk) * kMrP + kMrK] = tot;
   if (!last_cta(&g->cnt[s * 4 + 2], g->nchunk)) return;
   const double n2 = chunk_sum(g, s, kMrK, sh);
@@ -425,8 +427,330 @@ __global__ void mr_gout(int64_t N, int ns, const double* __restrict__ X, int64_t
     G[(int64_t)s * ldg + i] = X[(int64_t)s * ldx + i] - G[(int64_t)s * ldg + i];
 }
 
+// ============================================================ cluster-per-shift loop
+// For images whose working set sits in L2 (as the CG's cg_cluster.cu): a 16-CTA thread-
+// block cluster owns one shift and runs its Lanczos / Givens recurrences to the stopping
+// point in one launch; partial sums are pushed into every CTA's shared memory before
+// the hardware cluster barrier and summed there in rank order (deterministic). Per
+// iteration (4 cluster barriers):
+//   A  w = A_g v (fused apply, v . w partial)                  -> alpha0
+//   B  c = K^T w, kv = K^T v over the CTA's rows               -> alpha = alpha0 - kv . c
+//   C  w <- w - K c - alpha v - beta v_prev; ||w||^2           -> beta', Givens (every CTA)
+//   D  d, y, v_prev, v updates (and the Lanczos-vector store)
+// The recurrences and stopping rule are those of the lockstep kernels above; finalisation
+// (eq:xFinal), confirmation and restarts stay on the host path.
+constexpr int kMrCS = 16;     // CTAs per cluster
+constexpr int kMrSl = 2 * kMrK + 2;   // pushed slots: c (kMrK), kv (kMrK), norm^2, p.w
+
+struct alignas(64) MrClusterParams {
+  ApplyParams ap;     // X = V, Y = Wv, want_dot
+  MrDev* g;
+  unsigned* queue;
+  const int* list;    // shifts to run (device), nl of them
+  int nl;
+  int64_t rows;       // rows per CTA
+};
+
+__host__ __device__ constexpr int mr_tile_rows(int r) { return r <= 6 ? 64 : (r <= 8 ? 56 : tc_tile_rows(r)); }
+
+__device__ __forceinline__ void mr_cl_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+
+template <int R, bool kTma>
+__global__ void __launch_bounds__(kAT, 1) mr_cluster_kernel(const __grid_constant__ MrClusterParams P) {
+  extern __shared__ __align__(128) double smem[];
+  using Core = ApplyCore<R, kTma, mr_tile_rows(R)>;
+  unsigned crank_u;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(crank_u));
+  const int crank = (int)crank_u;
+  const int csz = kMrCS;
+  __shared__ double s_dot;
+  __shared__ double s_dots[kMrCS];
+  __shared__ double s_part[kMrSl];
+  __shared__ double s_parts[kMrCS][kMrSl];
+  __shared__ double s_red[kAT / 32][kMrSl];
+  __shared__ double s_c[kMrK], s_kv[kMrK], s_kd1[kMrK], s_kd2[kMrK], s_kay[kMrK];
+  __shared__ double s_co[8];     // alpha, oldeps, delta, denom, phi, invb
+  __shared__ double s_beta;      // beta_j of the current Lanczos step
+  __shared__ int s_next, s_st, s_slot;
+  __shared__ int s_list[1], s_lmode[1];
+  MrDev* g = P.g;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t N = g->N;
+  Core::init_bars(smem, P.ap);
+  ApplyPipe pp{{0u, 0u}, 0};
+  const int64_t rbeg = (int64_t)crank * P.rows;
+  const int64_t rend = min(N, rbeg + P.rows);
+  const int ntiles = P.ap.ntiles;
+  const int tper = (ntiles + csz - 1) / csz;
+  const int ibeg = min(ntiles, crank * tper), iend = min(ntiles, ibeg + tper);
+  auto remote = [&](double* p, int rank) -> double* {
+    unsigned long long a;
+    asm volatile("mapa.u64 %0, %1, %2;" : "=l"(a) : "l"(p), "r"(rank));
+    return reinterpret_cast<double*>(a);
+  };
+  auto remote_i = [&](int* p, int rank) -> int* {
+    unsigned long long a;
+    asm volatile("mapa.u64 %0, %1, %2;" : "=l"(a) : "l"(p), "r"(rank));
+    return reinterpret_cast<int*>(a);
+  };
+  for (;;) {
+    if (crank == 0 && tid == 0) s_next = (int)atomicAdd(P.queue, 1u);
+    mr_cl_sync();
+    const int idx = *remote_i(&s_next, 0);
+    mr_cl_sync();
+    if (idx >= P.nl) break;
+    const int s = P.list[idx];
+    if (g->status[s] != ST_ACTIVE) continue;
+    const int m = g->m[s];
+    const double* K = g->Kb + (int64_t)s * kMrK * N;
+    double* V = g->V + (int64_t)s * N;
+    double* Vp = g->Vp + (int64_t)s * N;
+    double* W = g->Wv + (int64_t)s * N;
+    double* D1 = g->D1 + (int64_t)s * N;
+    double* D2 = g->D2 + (int64_t)s * N;
+    double* Yv = g->Y + (int64_t)s * N;
+    double* sc = g->sc + s * 16;
+    double beta = sc[S_BETA], eps = sc[S_EPS], dbar = sc[S_DBAR], cs = sc[S_CS], sn = sc[S_SN], phibar = sc[S_PHIBAR];
+    int iters = g->iters[s], scnt = g->scnt[s];
+    int slot = g->slot[s];      // store slot of the current v (set at the start)
+    const double tolb = g->tolb;
+    const int maxit = g->maxit;
+    if (tid < kMrK) {
+      const int q = s * kMrK + tid;
+      s_kd1[tid] = g->kd1[q]; s_kd2[tid] = g->kd2[q]; s_kay[tid] = g->kay[q];
+    }
+    if (tid == 0) { s_list[0] = s; s_lmode[0] = ST_ACTIVE; s_beta = beta; }
+    __syncthreads();
+    int status = ST_ACTIVE;
+    for (;;) {
+      // ================= A: w = A_g v, v . w
+      if (tid == 0) s_dot = 0.0;
+      __syncthreads();
+      Core::run(P.ap, smem, ibeg, iend, 1, pp, s_list, s_lmode, &s_dot);
+      if (tid < csz) *remote(&s_dots[crank], tid) = s_dot;
+      asm volatile("fence.proxy.async.global;\n" ::: "memory");
+      mr_cl_sync();
+      // ================= B: c = K^T w, kv = K^T v (row partials)
+      {
+        double ac[kMrK], av[kMrK];
+#pragma unroll
+        for (int j = 0; j < kMrK; ++j) { ac[j] = 0.0; av[j] = 0.0; }
+        for (int64_t i = rbeg + tid; i < rend; i += kAT) {
+          const double w = W[i], v = V[i];
+          double kk[kMrK];
+#pragma unroll
+          for (int j = 0; j < kMrK; ++j) kk[j] = (j < m) ? __ldcg(K + (int64_t)j * N + i) : 0.0;
+#pragma unroll
+          for (int j = 0; j < kMrK; ++j)
+            if (j < m) { ac[j] = fma(kk[j], w, ac[j]); av[j] = fma(kk[j], v, av[j]); }
+        }
+#pragma unroll
+        for (int j = 0; j < kMrK; ++j) {
+          if (j < m) {
+            const double x = mr_wsum(ac[j]), y = mr_wsum(av[j]);
+            if (lane == 0) { s_red[warp][j] = x; s_red[warp][kMrK + j] = y; }
+          }
+        }
+        __syncthreads();
+        if (tid < 2 * kMrK) {
+          const int j = tid < kMrK ? tid : tid - kMrK;
+          double t = 0.0;
+          if (j < m)
+            for (int w = 0; w < kAT / 32; ++w) t += s_red[w][tid];
+          s_part[tid] = t;
+        }
+        __syncthreads();
+        for (int e = tid; e < csz * 2 * kMrK; e += kAT) {
+          const int c = e / (2 * kMrK), sl = e - c * 2 * kMrK;
+          *remote(&s_parts[crank][sl], c) = s_part[sl];
+        }
+      }
+      mr_cl_sync();
+      if (tid < 2 * kMrK) {
+        double t = 0.0;
+        for (int c = 0; c < csz; ++c) t += s_parts[c][tid];
+        if (tid < kMrK) s_c[tid] = t; else s_kv[tid - kMrK] = t;
+      }
+      __syncthreads();
+      if (tid == 0) {
+        double a0 = 0.0;
+        for (int c = 0; c < csz; ++c) a0 += s_dots[c];
+        for (int j = 0; j < m; ++j) a0 = fma(-s_kv[j], s_c[j], a0);
+        s_co[0] = a0;
+      }
+      __syncthreads();
+      const double alpha = s_co[0];
+      // ================= C: w <- w - K c - alpha v - beta v_prev, ||w||^2
+      {
+        double cc[kMrK];
+#pragma unroll
+        for (int j = 0; j < kMrK; ++j) cc[j] = (j < m) ? s_c[j] : 0.0;
+        const double bprev = s_beta;
+        double nrm = 0.0;
+        for (int64_t i = rbeg + tid; i < rend; i += kAT) {
+          double kk[kMrK];
+#pragma unroll
+          for (int j = 0; j < kMrK; ++j) kk[j] = (j < m) ? __ldcg(K + (int64_t)j * N + i) : 0.0;
+          double t = W[i];
+          const double v = V[i], vp = Vp[i];
+#pragma unroll
+          for (int j = 0; j < kMrK; ++j)
+            if (j < m) t = fma(-cc[j], kk[j], t);
+          t = fma(-alpha, v, t);
+          t = fma(-bprev, vp, t);
+          W[i] = t;
+          nrm = fma(t, t, nrm);
+        }
+        nrm = mr_wsum(nrm);
+        if (lane == 0) s_red[warp][0] = nrm;
+        __syncthreads();
+        if (tid == 0) {
+          double t = 0.0;
+          for (int w = 0; w < kAT / 32; ++w) t += s_red[w][0];
+          s_part[2 * kMrK] = t;
+        }
+        __syncthreads();
+        if (tid < csz) *remote(&s_parts[crank][2 * kMrK], tid) = s_part[2 * kMrK];
+      }
+      mr_cl_sync();
+      // ---- Givens (identical in every CTA)
+      if (tid == 0) {
+        double n2 = 0.0;
+        for (int c = 0; c < csz; ++c) n2 += s_parts[c][2 * kMrK];
+        const double bn = sqrt(n2);
+        const double oldeps = eps;
+        const double delta = cs * dbar + sn * alpha;
+        const double gbar = sn * dbar - cs * alpha;
+        eps = sn * bn;
+        dbar = -cs * bn;
+        double gm = sqrt(gbar * gbar + bn * bn);
+        if (gm < 2.2250738585072014e-308) gm = 2.2250738585072014e-308;
+        cs = gbar / gm; sn = bn / gm;
+        const double phi = cs * phibar;
+        phibar = sn * phibar;
+        s_co[1] = oldeps; s_co[2] = delta; s_co[3] = 1.0 / gm; s_co[4] = phi; s_co[5] = bn > 0.0 ? 1.0 / bn : 0.0;
+        beta = bn;
+        s_beta = bn;
+        iters += 1;
+        int st = ST_ACTIVE;
+        if (!isfinite(bn) || !isfinite(phibar) || !isfinite(alpha)) st = ST_BREAKDOWN;
+        else if (fabs(phibar) <= tolb || bn == 0.0) st = ST_RCONV;
+        else if (iters >= maxit) st = ST_MAXIT;
+        int sl = -1;
+        if (g->store && st == ST_ACTIVE && scnt < g->store_cap) sl = scnt++;
+        s_st = st;
+        s_slot = sl;
+      }
+      __syncthreads();
+      // every thread keeps the scalars in registers (same values as thread 0)
+      {
+        const double oldeps = s_co[1], delta = s_co[2], denom = s_co[3], phi = s_co[4], invb = s_co[5];
+        if (tid < m) {   // K^T A_g d_j recurrence
+          const double kd = (s_c[tid] - oldeps * s_kd2[tid] - delta * s_kd1[tid]) * denom;
+          s_kay[tid] = fma(phi, kd, s_kay[tid]);
+          s_kd2[tid] = s_kd1[tid];
+          s_kd1[tid] = kd;
+        }
+        const int st = s_st;
+        const int sl = s_slot;
+        double* sto = (sl >= 0) ? g->store + ((int64_t)s * g->store_cap + sl) * g->lds : nullptr;
+        // ================= D: d, y, v_prev, v
+        for (int64_t i = rbeg + tid; i < rend; i += kAT) {
+          const double v = V[i];
+          const double d1 = D1[i], d2 = D2[i];
+          const double dn = (v - oldeps * d2 - delta * d1) * denom;
+          Yv[i] = fma(phi, dn, Yv[i]);
+          D2[i] = d1;
+          D1[i] = dn;
+          Vp[i] = v;
+          const double vn = W[i] * invb;
+          V[i] = vn;
+          if (sto) sto[i] = vn;
+        }
+        asm volatile("fence.proxy.async.global;\n" ::: "memory");   // v stores -> next TMA reads
+        mr_cl_sync();
+        status = st;
+        slot = sl;
+      }
+      if (status != ST_ACTIVE) break;
+    }
+    if (crank == 0 && tid == 0) {
+      sc[S_BETA] = beta; sc[S_EPS] = eps; sc[S_DBAR] = dbar; sc[S_CS] = cs; sc[S_SN] = sn; sc[S_PHIBAR] = phibar;
+      g->iters[s] = iters;
+      g->scnt[s] = scnt;
+      g->slot[s] = slot;
+      g->status[s] = status;
+    }
+    if (crank == 0 && tid < kMrK) {
+      const int q = s * kMrK + tid;
+      g->kd1[q] = s_kd1[tid]; g->kd2[q] = s_kd2[tid]; g->kay[q] = s_kay[tid];
+    }
+    __syncthreads();
+  }
+}
+
+template <int R>
+cudaError_t mr_launch_r(const MrClusterParams& prm, bool tma, int ncl_req, cudaStream_t st, bool* ok) {
+  using C = TcCfg<R, mr_tile_rows(R)>;
+  auto kfn = tma ? mr_cluster_kernel<R, true> : mr_cluster_kernel<R, false>;
+  const size_t smem = C::SMEM;
+  static int inited[2] = {0, 0};
+  static int maxcl[2] = {0, 0};
+  const int ti = tma ? 1 : 0;
+  if (!inited[ti]) {
+    inited[ti] = 1;
+    cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) { cudaGetLastError(); maxcl[ti] = 0; }
+    else {
+      cudaLaunchConfig_t cfg = {};
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = kMrCS; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+      cfg.gridDim = dim3(kMrCS * 64); cfg.blockDim = dim3(kAT); cfg.dynamicSmemBytes = smem;
+      cfg.attrs = at; cfg.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, (void*)kfn, &cfg) != cudaSuccess) { cudaGetLastError(); n = 0; }
+      maxcl[ti] = n;
+    }
+  }
+  int ncl = ncl_req < maxcl[ti] ? ncl_req : maxcl[ti];
+  if (ncl < 1) { *ok = false; return cudaSuccess; }
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = kMrCS; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.gridDim = dim3(kMrCS * ncl); cfg.blockDim = dim3(kAT); cfg.dynamicSmemBytes = smem; cfg.stream = st;
+  cfg.attrs = at; cfg.numAttrs = 1;
+  count_launch();
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kfn, prm);
+  if (e != cudaSuccess) { cudaGetLastError(); *ok = false; return cudaSuccess; }
+  *ok = true;
+  return cudaSuccess;
+}
+
+cudaError_t mr_launch_cluster(Handle* h, const MrClusterParams& prm, bool tma, int ncl, cudaStream_t st, bool* ok) {
+  switch (h->r) {
+    case 1: return mr_launch_r<1>(prm, tma, ncl, st, ok);
+    case 2: return mr_launch_r<2>(prm, tma, ncl, st, ok);
+    case 3: return mr_launch_r<3>(prm, tma, ncl, st, ok);
+    case 4: return mr_launch_r<4>(prm, tma, ncl, st, ok);
+    case 5: return mr_launch_r<5>(prm, tma, ncl, st, ok);
+    case 6: return mr_launch_r<6>(prm, tma, ncl, st, ok);
+    case 7: return mr_launch_r<7>(prm, tma, ncl, st, ok);
+    case 8: return mr_launch_r<8>(prm, tma, ncl, st, ok);
+    case 9: return mr_launch_r<9>(prm, tma, ncl, st, ok);
+    case 10: return mr_launch_r<10>(prm, tma, ncl, st, ok);
+    case 11: return mr_launch_r<11>(prm, tma, ncl, st, ok);
+    case 12: return mr_launch_r<12>(prm, tma, ncl, st, ok);
+    default: *ok = false; return cudaSuccess;
+  }
+}
+
 struct MrLayout {
-  size_t vec, kb, zs, dbl, in, cnt, part, list, dev, total;
+  size_t vec, kb, zs, dbl, in, cnt, part, list, q, dev, total;
   int nchunk;
 };
 
@@ -445,6 +769,7 @@ MrLayout mr_layout(const Handle* h, int ns, int kmax) {
   L.cnt = o; o = al(o + sizeof(unsigned) * (size_t)ns * 4);
   L.part = o; o = al(o + sizeof(double) * (size_t)ns * L.nchunk * kMrP);
   L.list = o; o = al(o + sizeof(int) * (size_t)ns * 2);
+  L.q = o; o = al(o + 64);
   L.dev = o; o = al(o + sizeof(MrDev));
   L.total = o;
   return L;
@@ -699,6 +1024,18 @@ extern "C" rsk_status rsk_minres_recycled_batch(rsk_handle h, const rsk_cg_desc*
 
   std::vector<int> status(ns, ST_ACTIVE), iters(ns, 0), done(ns, 0), final_status(ns, RSK_CG_CONVERGED);
   std::vector<double> relres(ns, 0.0);
+  // cluster-per-shift device loop for L2-resident images (as the CG, cg_cluster.cu)
+  bool use_cluster = getenv("RSK_MR_NOCLUSTER") == nullptr && N <= 131072 && h->r >= 1 && !h->ct;
+  ApplyParams capx;
+  bool cl_tma = false;
+  if (use_cluster) {
+    ApplyLaunch a{};
+    a.X = hc.V; a.ldx = N; a.Y = hc.Wv; a.ldy = N; a.gamma = gam; a.nlist = 1; a.nvec_total = ns;
+    a.mode = RSK_APPLY_SHIFTED;
+    a.xdoty = reinterpret_cast<double*>(1);   // want_dot (accumulated through dot_acc)
+    cl_tma = fill_apply_params(h, a, capx, mr_tile_rows(h->r));
+    capx.cg = nullptr;
+  }
   std::vector<int> it_restart(ns, -1);   // iterations at the last restart (stagnation guard)
   std::vector<int> glist;                // active set of the captured chunk graph
   cudaGraphExec_t gexec = nullptr;
@@ -782,6 +1119,31 @@ extern "C" rsk_status rsk_minres_recycled_batch(rsk_handle h, const rsk_cg_desc*
     // of an active set runs eagerly, later ones replay it as a CUDA graph (the
     // per-iteration kernels are short; launch overhead would dominate small batches)
     const unsigned nl = (unsigned)active.size();
+    if (use_cluster) {
+      // one launch runs every active shift to its stopping point (cluster per shift)
+      MR_CUDA(upload_to(dloop, active));
+      glist.clear();
+      if (gexec) { cudaGraphExecDestroy(gexec); gexec = nullptr; }
+      unsigned* dq = reinterpret_cast<unsigned*>(base + L.q);
+      MR_CUDA(cudaMemsetAsync(dq, 0, sizeof(unsigned), st));
+      MrClusterParams cp;
+      cp.ap = capx;
+      cp.g = dev;
+      cp.queue = dq;
+      cp.list = dloop;
+      cp.nl = (int)nl;
+      cp.rows = (N + kMrCS - 1) / kMrCS;
+      bool ok = false;
+      MR_CUDA(mr_launch_cluster(h, cp, cl_tma, (int)nl, st, &ok));
+      if (ok) {
+        if (++guard > (int64_t)d->maxit * 4 + 100) {
+          h->err = "rsk_minres_recycled_batch: loop guard";
+          return RSK_ECUDA;
+        }
+        continue;
+      }
+      use_cluster = false;   // could not co-schedule the clusters: lockstep kernels
+    }
     const bool same = (active == glist);
     if (!same) {
       MR_CUDA(upload_to(dloop, active));
