@@ -457,6 +457,108 @@ __device__ __forceinline__ void mr_cl_sync() {
   asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
 }
 
+// phase B rows: per-warp sums of c_j = K_j . w and kv_j = K_j . v into red[warp][j],
+// red[warp][kMrK + j] (MK >= m: register arrays sized for the local dimension)
+template <int MK>
+__device__ __noinline__ void mr_rows_b_t(const double* __restrict__ K, const double* __restrict__ W,
+                                         const double* __restrict__ V, int64_t N, int64_t rbeg, int64_t rend, int m,
+                                         double (*red)[kMrSl]) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double ac[MK], av[MK];
+#pragma unroll
+  for (int j = 0; j < MK; ++j) { ac[j] = 0.0; av[j] = 0.0; }
+  const int64_t np2 = (rend - rbeg) >> 1;   // row pairs (rbeg even): 16-byte loads
+#pragma unroll 2
+  for (int64_t q = tid; q < np2; q += kAT) {
+    const int64_t i = rbeg + 2 * q;
+    double2 kk[MK];
+#pragma unroll
+    for (int j = 0; j < MK; ++j)
+      kk[j] = (j < m) ? __ldcg(reinterpret_cast<const double2*>(K + (int64_t)j * N + i)) : make_double2(0.0, 0.0);
+    const double2 w = *reinterpret_cast<const double2*>(W + i), v = *reinterpret_cast<const double2*>(V + i);
+#pragma unroll
+    for (int j = 0; j < MK; ++j)
+      if (j < m) {
+        ac[j] = fma(kk[j].y, w.y, fma(kk[j].x, w.x, ac[j]));
+        av[j] = fma(kk[j].y, v.y, fma(kk[j].x, v.x, av[j]));
+      }
+  }
+  if (((rend - rbeg) & 1) && tid == 0) {
+    const int64_t i = rend - 1;
+    const double w = W[i], v = V[i];
+#pragma unroll
+    for (int j = 0; j < MK; ++j)
+      if (j < m) {
+        const double k = K[(int64_t)j * N + i];
+        ac[j] = fma(k, w, ac[j]);
+        av[j] = fma(k, v, av[j]);
+      }
+  }
+#pragma unroll
+  for (int j = 0; j < MK; ++j) {
+    if (j < m) {
+      const double x = mr_wsum(ac[j]), y = mr_wsum(av[j]);
+      if (lane == 0) { red[warp][j] = x; red[warp][kMrK + j] = y; }
+    }
+  }
+}
+
+__device__ __forceinline__ void mr_rows_b(const double* K, const double* W, const double* V, int64_t N, int64_t rbeg,
+                                          int64_t rend, int m, double (*red)[kMrSl]) {
+  if (m <= 10) mr_rows_b_t<10>(K, W, V, N, rbeg, rend, m, red);
+  else mr_rows_b_t<kMrK>(K, W, V, N, rbeg, rend, m, red);
+}
+
+// phase C rows: w <- w - K c - alpha v - beta_prev v_prev over the CTA's rows; returns this
+// thread's part of ||w||^2
+template <int MK>
+__device__ __noinline__ double mr_rows_c_t(const double* __restrict__ K, double* __restrict__ W,
+                                           const double* __restrict__ V, const double* __restrict__ Vp, int64_t N,
+                                           int64_t rbeg, int64_t rend, int m, const double* sc, double alpha,
+                                           double bprev) {
+  const int tid = threadIdx.x;
+  double cc[MK];
+#pragma unroll
+  for (int j = 0; j < MK; ++j) cc[j] = (j < m) ? sc[j] : 0.0;
+  double nrm = 0.0;
+  const int64_t np2 = (rend - rbeg) >> 1;
+#pragma unroll 2
+  for (int64_t q = tid; q < np2; q += kAT) {
+    const int64_t i = rbeg + 2 * q;
+    double2 kk[MK];
+#pragma unroll
+    for (int j = 0; j < MK; ++j)
+      kk[j] = (j < m) ? __ldcg(reinterpret_cast<const double2*>(K + (int64_t)j * N + i)) : make_double2(0.0, 0.0);
+    double2 t = *reinterpret_cast<const double2*>(W + i);
+    const double2 v = *reinterpret_cast<const double2*>(V + i), vp = *reinterpret_cast<const double2*>(Vp + i);
+#pragma unroll
+    for (int j = 0; j < MK; ++j)
+      if (j < m) { t.x = fma(-cc[j], kk[j].x, t.x); t.y = fma(-cc[j], kk[j].y, t.y); }
+    t.x = fma(-bprev, vp.x, fma(-alpha, v.x, t.x));
+    t.y = fma(-bprev, vp.y, fma(-alpha, v.y, t.y));
+    *reinterpret_cast<double2*>(W + i) = t;
+    nrm = fma(t.y, t.y, fma(t.x, t.x, nrm));
+  }
+  if (((rend - rbeg) & 1) && tid == 0) {
+    const int64_t i = rend - 1;
+    double t = W[i];
+#pragma unroll
+    for (int j = 0; j < MK; ++j)
+      if (j < m) t = fma(-cc[j], K[(int64_t)j * N + i], t);
+    t = fma(-bprev, Vp[i], fma(-alpha, V[i], t));
+    W[i] = t;
+    nrm = fma(t, t, nrm);
+  }
+  return nrm;
+}
+
+__device__ __forceinline__ double mr_rows_c(const double* K, double* W, const double* V, const double* Vp, int64_t N,
+                                            int64_t rbeg, int64_t rend, int m, const double* sc, double alpha,
+                                            double bprev) {
+  if (m <= 10) return mr_rows_c_t<10>(K, W, V, Vp, N, rbeg, rend, m, sc, alpha, bprev);
+  return mr_rows_c_t<kMrK>(K, W, V, Vp, N, rbeg, rend, m, sc, alpha, bprev);
+}
+
 template <int R, bool kTma>
 __global__ void __launch_bounds__(kAT, 1) mr_cluster_kernel(const __grid_constant__ MrClusterParams P) {
   extern __shared__ __align__(128) double smem[];
@@ -534,25 +636,7 @@ __global__ void __launch_bounds__(kAT, 1) mr_cluster_kernel(const __grid_constan
       mr_cl_sync();
       // ================= B: c = K^T w, kv = K^T v (row partials)
       {
-        double ac[kMrK], av[kMrK];
-#pragma unroll
-        for (int j = 0; j < kMrK; ++j) { ac[j] = 0.0; av[j] = 0.0; }
-        for (int64_t i = rbeg + tid; i < rend; i += kAT) {
-          const double w = W[i], v = V[i];
-          double kk[kMrK];
-#pragma unroll
-          for (int j = 0; j < kMrK; ++j) kk[j] = (j < m) ? __ldcg(K + (int64_t)j * N + i) : 0.0;
-#pragma unroll
-          for (int j = 0; j < kMrK; ++j)
-            if (j < m) { ac[j] = fma(kk[j], w, ac[j]); av[j] = fma(kk[j], v, av[j]); }
-        }
-#pragma unroll
-        for (int j = 0; j < kMrK; ++j) {
-          if (j < m) {
-            const double x = mr_wsum(ac[j]), y = mr_wsum(av[j]);
-            if (lane == 0) { s_red[warp][j] = x; s_red[warp][kMrK + j] = y; }
-          }
-        }
+        mr_rows_b(K, W, V, N, rbeg, rend, m, s_red);
         __syncthreads();
         if (tid < 2 * kMrK) {
           const int j = tid < kMrK ? tid : tid - kMrK;
@@ -584,25 +668,8 @@ __global__ void __launch_bounds__(kAT, 1) mr_cluster_kernel(const __grid_constan
       const double alpha = s_co[0];
       // ================= C: w <- w - K c - alpha v - beta v_prev, ||w||^2
       {
-        double cc[kMrK];
-#pragma unroll
-        for (int j = 0; j < kMrK; ++j) cc[j] = (j < m) ? s_c[j] : 0.0;
         const double bprev = s_beta;
-        double nrm = 0.0;
-        for (int64_t i = rbeg + tid; i < rend; i += kAT) {
-          double kk[kMrK];
-#pragma unroll
-          for (int j = 0; j < kMrK; ++j) kk[j] = (j < m) ? __ldcg(K + (int64_t)j * N + i) : 0.0;
-          double t = W[i];
-          const double v = V[i], vp = Vp[i];
-#pragma unroll
-          for (int j = 0; j < kMrK; ++j)
-            if (j < m) t = fma(-cc[j], kk[j], t);
-          t = fma(-alpha, v, t);
-          t = fma(-bprev, vp, t);
-          W[i] = t;
-          nrm = fma(t, t, nrm);
-        }
+        double nrm = mr_rows_c(K, W, V, Vp, N, rbeg, rend, m, s_c, alpha, bprev);
         nrm = mr_wsum(nrm);
         if (lane == 0) s_red[warp][0] = nrm;
         __syncthreads();
@@ -657,7 +724,7 @@ __global__ void __launch_bounds__(kAT, 1) mr_cluster_kernel(const __grid_constan
         const int sl = s_slot;
         double* sto = (sl >= 0) ? g->store + ((int64_t)s * g->store_cap + sl) * g->lds : nullptr;
         // ================= D: d, y, v_prev, v
-        for (int64_t i = rbeg + tid; i < rend; i += kAT) {
+        auto upd1 = [&](int64_t i) {
           const double v = V[i];
           const double d1 = D1[i], d2 = D2[i];
           const double dn = (v - oldeps * d2 - delta * d1) * denom;
@@ -668,7 +735,25 @@ __global__ void __launch_bounds__(kAT, 1) mr_cluster_kernel(const __grid_constan
           const double vn = W[i] * invb;
           V[i] = vn;
           if (sto) sto[i] = vn;
+        };
+        const int64_t np2 = (rend - rbeg) >> 1;
+        for (int64_t q = tid; q < np2; q += kAT) {
+          const int64_t i = rbeg + 2 * q;
+          const double2 v = *reinterpret_cast<const double2*>(V + i);
+          const double2 d1 = *reinterpret_cast<const double2*>(D1 + i), d2 = *reinterpret_cast<const double2*>(D2 + i);
+          const double2 y = *reinterpret_cast<const double2*>(Yv + i), w = *reinterpret_cast<const double2*>(W + i);
+          double2 dn;
+          dn.x = (v.x - oldeps * d2.x - delta * d1.x) * denom;
+          dn.y = (v.y - oldeps * d2.y - delta * d1.y) * denom;
+          *reinterpret_cast<double2*>(Yv + i) = make_double2(fma(phi, dn.x, y.x), fma(phi, dn.y, y.y));
+          *reinterpret_cast<double2*>(D2 + i) = d1;
+          *reinterpret_cast<double2*>(D1 + i) = dn;
+          *reinterpret_cast<double2*>(Vp + i) = v;
+          const double2 vn = make_double2(w.x * invb, w.y * invb);
+          *reinterpret_cast<double2*>(V + i) = vn;
+          if (sto) *reinterpret_cast<double2*>(sto + i) = vn;
         }
+        if (((rend - rbeg) & 1) && tid == 0) upd1(rend - 1);
         asm volatile("fence.proxy.async.global;\n" ::: "memory");   // v stores -> next TMA reads
         mr_cl_sync();
         status = st;
@@ -1025,7 +1110,9 @@ extern "C" rsk_status rsk_minres_recycled_batch(rsk_handle h, const rsk_cg_desc*
   std::vector<int> status(ns, ST_ACTIVE), iters(ns, 0), done(ns, 0), final_status(ns, RSK_CG_CONVERGED);
   std::vector<double> relres(ns, 0.0);
   // cluster-per-shift device loop for L2-resident images (as the CG, cg_cluster.cu)
-  bool use_cluster = getenv("RSK_MR_NOCLUSTER") == nullptr && N <= 131072 && h->r >= 1 && !h->ct;
+  bool use_cluster = getenv("RSK_MR_NOCLUSTER") == nullptr && N <= 131072 && h->r >= 1 && !h->ct &&
+                     (N % 2 == 0) && (!store || d->lds % 2 == 0) &&
+                     ((reinterpret_cast<uintptr_t>(ws) | reinterpret_cast<uintptr_t>(store ? d->store : ws)) & 15) == 0;
   ApplyParams capx;
   bool cl_tma = false;
   if (use_cluster) {
@@ -1132,7 +1219,7 @@ extern "C" rsk_status rsk_minres_recycled_batch(rsk_handle h, const rsk_cg_desc*
       cp.queue = dq;
       cp.list = dloop;
       cp.nl = (int)nl;
-      cp.rows = (N + kMrCS - 1) / kMrCS;
+      cp.rows = ((N + kMrCS - 1) / kMrCS + 1) / 2 * 2;   // even: 16-byte row pairs
       bool ok = false;
       MR_CUDA(mr_launch_cluster(h, cp, cl_tma, (int)nl, st, &ok));
       if (ok) {
