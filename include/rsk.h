@@ -113,6 +113,22 @@ rsk_status rsk_create_ct(rsk_handle* h, int device, int64_t n, int nangles, cons
 /* rsk_ct_info: ndata, the number of stored entries of C, and the Frobenius norm of C
  * before scaling (host outputs, each nullable). RSK_EINVAL for a non-CT handle. */
 rsk_status rsk_ct_info(rsk_handle h, int64_t* ndata, int64_t* nnz, double* fro_unscaled);
+/* rsk_create_slab: the handle of one row slab of an ny_global x nx image (SURVEY §8(e2),
+ * configs[4] = C5): owned global rows [row0, row0 + nrows) plus up to `halo` >= 2r
+ * halo rows on each side, clipped at the image edges -- the handle's image is global rows
+ * [max(0, row0 - halo), min(ny_global, row0 + nrows + halo)) and every librsk call on it
+ * works on those extended rows (vectors of ext_rows * nx). With the halo rows refreshed
+ * from the neighbours, the fused apply is exact on every owned row: the zero-boundary
+ * truncation only acts within r rows of the extended array's edge, i.e. inside the halo
+ * or at a true image edge. Communication (the halo exchange, the all-reduce of dots) is
+ * the caller's, over torch.distributed / NCCL (paper_2306_15049_b200/slab.py) -- the
+ * library holds no communicator, so no kernel ever waits on another rank's kernel.
+ * EINVAL: bad geometry, halo < 2r, nrows < halo; otherwise as rsk_create. */
+rsk_status rsk_create_slab(rsk_handle* h, int device, int64_t ny_global, int64_t nx, int64_t row0,
+                           int64_t nrows, const double* psf_h, int pny, int pnx, int halo, int flags);
+/* rsk_slab_info: info6_h = {ny_global, ext0, ext1, row0, row1, halo} (host [6]);
+ * RSK_EINVAL for a handle not made by rsk_create_slab. */
+rsk_status rsk_slab_info(rsk_handle h, int64_t* info6_h);
 rsk_status rsk_destroy(rsk_handle h);
 const char* rsk_last_error(rsk_handle h);
 /* Library build information (static host string). */

@@ -78,6 +78,9 @@ _SIGS = {
     "rsk_launch_count": (C.c_int64, []),
     "rsk_create": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, _i64, _i64, _hp, C.c_int, C.c_int, C.c_int]),
     "rsk_destroy": (C.c_int, [C.c_void_p]),
+    "rsk_create_slab": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, _i64, _i64, _i64, _i64, _hp, C.c_int, C.c_int,
+                                  C.c_int, C.c_int]),
+    "rsk_slab_info": (C.c_int, [C.c_void_p, C.POINTER(_i64)]),
     "rsk_create_ct": (C.c_int, [C.POINTER(C.c_void_p), C.c_int, _i64, C.c_int, _hp, C.c_int, C.c_int]),
     "rsk_ct_info": (C.c_int, [C.c_void_p, C.POINTER(_i64), C.POINTER(_i64), _hp]),
     "rsk_last_error": (C.c_char_p, [C.c_void_p]),

@@ -184,6 +184,34 @@ extern "C" rsk_status rsk_create(rsk_handle* out, int device, int64_t ny, int64_
   return RSK_OK;
 }
 
+extern "C" rsk_status rsk_create_slab(rsk_handle* out, int device, int64_t ny_global, int64_t nx, int64_t row0,
+                                      int64_t nrows, const double* psf_h, int pny, int pnx, int halo, int flags) {
+  if (!out || ny_global < 2 || nx < 2 || row0 < 0 || nrows < 1 || row0 + nrows > ny_global) return RSK_EINVAL;
+  if (pny != pnx || pny % 2 != 1 || halo < 2 * (pny / 2) || nrows < halo) return RSK_EINVAL;
+  const int64_t e0 = std::max<int64_t>(0, row0 - halo), e1 = std::min<int64_t>(ny_global, row0 + nrows + halo);
+  rsk_status st = rsk_create(out, device, e1 - e0, nx, psf_h, pny, pnx, flags);
+  if (st != RSK_OK) return st;
+  rsk_handle h = *out;
+  h->ny_global = ny_global;
+  h->slab_ext0 = e0;
+  h->slab_ext1 = e1;
+  h->slab_row0 = row0;
+  h->slab_row1 = row0 + nrows;
+  h->slab_halo = halo;
+  return RSK_OK;
+}
+
+extern "C" rsk_status rsk_slab_info(rsk_handle h, int64_t* info6_h) {
+  if (!h || !info6_h || h->ny_global == 0) return RSK_EINVAL;
+  info6_h[0] = h->ny_global;
+  info6_h[1] = h->slab_ext0;
+  info6_h[2] = h->slab_ext1;
+  info6_h[3] = h->slab_row0;
+  info6_h[4] = h->slab_row1;
+  info6_h[5] = h->slab_halo;
+  return RSK_OK;
+}
+
 extern "C" rsk_status rsk_destroy(rsk_handle h) {
   if (!h) return RSK_EINVAL;
   cudaSetDevice(h->device);

@@ -116,6 +116,9 @@ struct Handle {
   int sm_count = 148;
   bool sticky = false;
   cudaStream_t cg_stream = nullptr;  // private capture-capable stream of rsk_cg_recycled_batch
+  // row slab (rsk_create_slab): this handle's rows are global rows [slab_ext0, slab_ext1),
+  // of which [slab_row0, slab_row1) are owned; ny_global = the whole image
+  int64_t ny_global = 0, slab_ext0 = 0, slab_ext1 = 0, slab_row0 = 0, slab_row1 = 0, slab_halo = 0;
   // CT operator (rsk_create_ct, ct.cu): C as CSR over rays and C^T as CSR over pixels
   bool ct = false;
   int64_t ndata = 0;          // length of a data vector d: ny*nx (blur) or rays (CT)

@@ -69,6 +69,30 @@ class Handle:
         self.ndata = self.N
 
     @classmethod
+    def slab(cls, ny_global: int, nx: int, row0: int, nrows: int, psf: np.ndarray, halo: int,
+             device: int = 0) -> "Handle":
+        """The handle of one row slab (rsk_create_slab): global rows [ext0, ext1) stored,
+        [row0, row0 + nrows) owned; self.slab_info = (ny_global, ext0, ext1, row0, row1, halo)."""
+        self = cls.__new__(cls)
+        self.lib = L.load()
+        psf = np.ascontiguousarray(psf, dtype=np.float64)
+        h = C.c_void_p()
+        st = self.lib.rsk_create_slab(C.byref(h), device, int(ny_global), int(nx), int(row0), int(nrows), _hp(psf),
+                                      psf.shape[0], psf.shape[1], int(halo), 0)
+        if st != L.RSK_OK:
+            raise RskError(f"rsk_create_slab failed with status {st}")
+        self.h = h
+        self._psf = psf
+        info = (C.c_int64 * 6)()
+        self.lib.rsk_slab_info(h, info)
+        self.slab_info = tuple(int(v) for v in info)
+        self.ny, self.nx = self.slab_info[2] - self.slab_info[1], int(nx)
+        self.N = self.ny * self.nx
+        self.ndata = self.N
+        self.device = device
+        return self
+
+    @classmethod
     def ct(cls, n: int, angles_deg, ndet: int, device: int = 0) -> "Handle":
         """A handle whose C is the parallel-beam CT matrix (rsk_create_ct; Example 2)."""
         self = cls.__new__(cls)

@@ -217,7 +217,8 @@ class SlabOps:
         self.own0 = self.s.top * plan.nx
         self.own_n = self.s.own_rows * plan.nx
         self.dev = torch.device("cuda", device)
-        self.h = Handle(self.s.ext_rows, plan.nx, psf, device)
+        self.h = Handle.slab(plan.ny, plan.nx, self.s.row0, self.s.own_rows, psf, plan.H, device)
+        assert self.h.slab_info[1:3] == (self.s.ext0, self.s.ext1), (self.h.slab_info, self.s)
         self.lib = L.load()
         self.f = dict(dtype=torch.float64, device=self.dev)
 

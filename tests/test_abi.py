@@ -139,3 +139,17 @@ def test_create_ct_argument_errors_need_no_device(lib):
     assert lib.rsk_create_ct(C.byref(h), 0, 16, 10, bad.ctypes.data_as(C.POINTER(C.c_double)), 8, 0) == L.RSK_EINVAL
     assert lib.rsk_ct_info(None, None, None, None) == L.RSK_EINVAL
     assert lib.rsk_minres_workspace_bytes(None, 4, 9) == 0
+
+
+def test_create_slab_argument_errors_need_no_device(lib):
+    """rsk_create_slab rejects bad slab geometry before touching the device."""
+    import ctypes as C
+    from paper_2306_15049_b200 import _lib as L
+    import rsk_synth as S
+    h = C.c_void_p()
+    psf = np.ascontiguousarray(S.gaussian_psf(4, 2.0))
+    hp = psf.ctypes.data_as(C.POINTER(C.c_double))
+    assert lib.rsk_create_slab(C.byref(h), 0, 256, 256, 0, 64, hp, 9, 9, 7, 0) == L.RSK_EINVAL     # halo < 2r
+    assert lib.rsk_create_slab(C.byref(h), 0, 256, 256, 250, 64, hp, 9, 9, 8, 0) == L.RSK_EINVAL   # past the image
+    assert lib.rsk_create_slab(C.byref(h), 0, 256, 256, 0, 4, hp, 9, 9, 8, 0) == L.RSK_EINVAL      # rows < halo
+    assert lib.rsk_slab_info(None, None) == L.RSK_EINVAL
