@@ -99,8 +99,9 @@ def oracle_sample(cfg, inputs, budget_s=12.0):
     Returns applies/s (same unit as the GPU metric)."""
     from oracle import defcg as dcg
     from oracle import operators as ops
+    from oracle import pipeline as opipe
     n = cfg.n
-    h = inputs["psf"]
+    h = opipe.operator_of(cfg, inputs)   # the PSF, or the CT matrix (C6)
     d, b = ops.make_data(h, inputs["x_true"], inputs["xi"], cfg.noise)
     wx, wy = ops.identity_weights(n)
     g = float(inputs["gamma"][cfg.i1 - 1])
@@ -280,6 +281,8 @@ def run_ours(args, cfg, inputs, rank, world):
             "scaling": "strong" if world > 1 else "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": cfg.name, "n": cfg.n, "N": cfg.N, "shifts": cfg.M,
+                       "inner": cfg.inner, "local": cfg.local, "weight_rule": cfg.weight_rule,
+                       "principal": cfg.principal, "operator": cfg.operator,
                        "outer_steps": cfg.K_out, "n_c": cfg.n_c, "J": cfg.J, "psf": f"{2*cfg.r+1}x{2*cfg.r+1}",
                        "tol": cfg.tol, "l2": "flushed between steps (256 MB write)",
                        "parallelism": f"shift-sharded x{world} (NCCL)" if world > 1 else "single"},
@@ -320,10 +323,22 @@ def main():
     ap.add_argument("--cpu-budget", type=float, default=12.0)
     ap.add_argument("--ref-budget", type=float, default=15.0)
     ap.add_argument("--no-cpu", action="store_true")
+    # options of the nested solve (defaults = north_star's path; see README / DESIGN)
+    ap.add_argument("--inner", default=None, choices=["cg", "minres"])
+    ap.add_argument("--local", default=None, choices=["d3", "seq"])
+    ap.add_argument("--rule", default=None, choices=["irn", "irn_iso", "gazzola"])
+    ap.add_argument("--principal", default=None, choices=["g10", "vnew"])
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     cfg = S.CONFIGS[args.config]
+    import dataclasses
+    over = {k: v for k, v in (("inner", args.inner), ("local", args.local), ("weight_rule", args.rule),
+                              ("principal", args.principal)) if v is not None}
+    if cfg.operator == "ct":
+        over.setdefault("inner", "minres")
+    if over:
+        cfg = dataclasses.replace(cfg, **over)
     inputs = S.make_inputs(cfg)
     if args.impl == "reference":
         run_reference(args, cfg, inputs, rank, world)
