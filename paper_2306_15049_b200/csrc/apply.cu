@@ -15,10 +15,14 @@
 
 namespace rsk {
 
+// standalone tiles: 64 output rows for r <= 6 (a 64 x (64 + 4r) halo box, fewer items:
+// C2 x 32 shifts is 512 items instead of 768 on 148 CTAs), else the default height
+__host__ __device__ constexpr int std_tile_rows(int r) { return r <= 6 ? 64 : (r <= 8 ? 56 : tc_tile_rows(r)); }
+
 template <int R, bool kTma>
 __global__ void __launch_bounds__(kAT, kApplyCtasPerSm) apply_kernel(const __grid_constant__ ApplyParams p) {
   extern __shared__ __align__(128) double smem[];
-  using Core = ApplyCore<R, kTma>;
+  using Core = ApplyCore<R, kTma, std_tile_rows(R)>;
   Core::init_bars(smem, p);
   const int nl = p.nlist_dev ? *p.nlist_dev : p.nlist;
   const int nitems = nl * p.ntiles;
@@ -114,7 +118,7 @@ bool make_map2(CUtensorMap* m, const double* base, int64_t nx, int64_t ny, int b
 // ---------------------------------------------------------------- launch
 template <int R>
 static cudaError_t launch_r(const ApplyParams& prm, bool tma, int sm_count, cudaStream_t st) {
-  using C = TcCfg<R>;
+  using C = TcCfg<R, std_tile_rows(R)>;
   static int bps[2] = {0, 0};
   int& blocks_per_sm = bps[tma ? 1 : 0];
   if (blocks_per_sm == 0) {
@@ -185,7 +189,7 @@ cudaError_t launch_apply(Handle* h, const ApplyLaunch& a, cudaStream_t st) {
   if (h->ct) return launch_ct_apply(h, a, st);   // CT: sparse C, C^T (ct.cu)
   if (a.nlist <= 0) return cudaSuccess;
   ApplyParams prm;
-  const bool tma = fill_apply_params(h, a, prm, 0);
+  const bool tma = fill_apply_params(h, a, prm, std_tile_rows(h->r));
   if (a.xdoty && !a.cg) {
     const size_t need = sizeof(double) * (size_t)prm.ntiles * (size_t)a.nlist;
     if (need > h->scratch_bytes) return cudaErrorMemoryAllocation;
