@@ -107,7 +107,7 @@ rsk_status rsk_create(rsk_handle* h, int device, int64_t ny, int64_t nx,
  * rsk_lcurve_norms (scratch nvec x ndata), the weight / IRN calls and
  * rsk_minres_recycled_batch work; rsk_cg_recycled_batch returns RSK_EUNSUPPORTED (its
  * device loops embed the stencil apply). n in [2, 4096], nangles, ndet >= 1, finite
- * angles, else RSK_EINVAL. */
+ * angles, else RSK_EINVAL; nangles * ndet * 2n > 1e9 stored entries -> RSK_ENOMEM. */
 rsk_status rsk_create_ct(rsk_handle* h, int device, int64_t n, int nangles, const double* angles_deg_h,
                          int ndet, int flags);
 /* rsk_ct_info: ndata, the number of stored entries of C, and the Frobenius norm of C

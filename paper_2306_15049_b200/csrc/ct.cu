@@ -276,6 +276,9 @@ extern "C" rsk_status rsk_create_ct(rsk_handle* out, int device, int64_t n, int 
   for (int a = 0; a < nangles; ++a)
     if (!std::isfinite(angles_deg_h[a])) return RSK_EINVAL;
   const int64_t N = n * n, m = (int64_t)nangles * ndet;
+  // every ray crosses at most 2n pixels: keep the stored entries addressable and the host
+  // build bounded (the explicit matrix is meant for Example 2's sizes, n = 82)
+  if ((double)m * 2.0 * (double)n > 1.0e9) return RSK_ENOMEM;
   // ---- C on the host: CSR over rays (angle-major, detector-minor)
   std::vector<int64_t> rp((size_t)m + 1, 0);
   std::vector<int> col;
