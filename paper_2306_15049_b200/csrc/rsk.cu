@@ -814,7 +814,7 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
   double ms_apply = 0.0, ms_upd = 0.0, ms_cmb = 0.0;
   int64_t n_ka = 0;
   if (prof) {
-    evs.resize(4 * ce);
+    evs.assign(4 * ce, nullptr);
     for (auto& e : evs) RSK_CUDA(cudaEventCreate(&e));
   }
   std::vector<int> stat_h(ns), it_h(ns);
@@ -836,6 +836,14 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
                               reinterpret_cast<uintptr_t>(store ? d->store : d->X)) & 15) == 0;
   // device-loop kernel time (CUDA events on the launching stream) for the roofline
   cudaEvent_t dl0 = nullptr, dl1 = nullptr;
+  struct EvGuard {   // the events (and the profiling ones) are released on every exit path
+    cudaEvent_t* a; cudaEvent_t* b; std::vector<cudaEvent_t>* v;
+    ~EvGuard() {
+      if (*a) cudaEventDestroy(*a);
+      if (*b) cudaEventDestroy(*b);
+      for (auto& e : *v) if (e) cudaEventDestroy(e);
+    }
+  } evguard{&dl0, &dl1, &evs};
   double dl_kind = 0.0;
   RSK_CUDA(cudaEventCreate(&dl0));
   RSK_CUDA(cudaEventCreate(&dl1));
@@ -935,8 +943,6 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
   RSK_CUDA(cudaEventSynchronize(dl1));
   float dl_ms = 0.0f;
   cudaEventElapsedTime(&dl_ms, dl0, dl1);
-  cudaEventDestroy(dl0);
-  cudaEventDestroy(dl1);
   while (!active.empty()) {
     // active shifts grouped by shift group (group-shared kernels), with offsets/counts
     {
@@ -1007,7 +1013,6 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
     active.swap(next);
     if (++guard > (int64_t)d->maxit * 4 + 100) { h->err = "rsk_cg_recycled_batch: loop guard"; return RSK_ECUDA; }
   }
-  if (prof) for (auto& e : evs) cudaEventDestroy(e);
   if (gexec) cudaGraphExecDestroy(gexec);
   if (graph) cudaGraphDestroy(graph);
 
