@@ -139,3 +139,54 @@ def test_c5_slab_apply_matches_single_domain(torch_dev, nranks):
 
     errs = run_threads(plan, rank_fn)
     assert max(errs) <= 1e-13 * scale, errs
+
+
+def test_c2_minres_nested_solve_true_residuals(torch_dev):
+    """The paper's inner solver at full C2 size in the launch configuration the probes time
+    (cluster-per-shift MINRES loop): every shift of outer steps 0 and 1 meets tol on the
+    true residual the oracle computes, and the IRN weights of step 1 are the oracle's."""
+    import dataclasses
+    torch, dev = torch_dev
+    from paper_2306_15049_b200.pipeline import GpuSolver
+    cfg = dataclasses.replace(S.CONFIGS["C2"], inner="minres")
+    inp = S.make_inputs(cfg)
+    n = cfg.n
+    sol = GpuSolver(cfg, inp["psf"], inp["gamma"], device=0)
+    sol.set_data(torch.from_numpy(inp["x_true"]).to(dev), torch.from_numpy(inp["xi"]).to(dev))
+    d, b = ops.make_data(inp["psf"], inp["x_true"], inp["xi"], cfg.noise)
+    nb = np.linalg.norm(b)
+    outs = sol.run(K_out=2)
+    assert all(np.all(o.status == 0) for o in outs)
+    # step 1 ran under the weights of step 0's x*: recompute them on the oracle side
+    X = sol.final["X_prev"].cpu().numpy()
+    wx, wy = sol.wx.cpu().numpy().reshape(n, n), sol.wy.cpu().numpy().reshape(n, n)
+    for l in range(cfg.M):
+        rt = b - ops.apply_shifted(inp["psf"], wx, wy, inp["gamma"][l], X[l].reshape(n, n))
+        assert np.linalg.norm(rt) <= cfg.tol * nb * (1 + 1e-6), (l, np.linalg.norm(rt) / nb)
+
+
+def test_c6_ct_nested_solve_true_residuals(torch_dev):
+    """Example 2 at full size (n = 82, 135 angles, 20 shifts; MINRES): after two outer
+    steps every shift meets tol on the true residual with the oracle's CT matrix."""
+    torch, dev = torch_dev
+    from oracle import pipeline as opipe
+    from paper_2306_15049_b200.pipeline import GpuSolver
+    import dataclasses
+    cfg = dataclasses.replace(S.CONFIGS["C6"], inner="minres")
+    inp = S.make_inputs(cfg)
+    n = cfg.n
+    op = opipe.operator_of(cfg, inp)
+    sol = GpuSolver(cfg, None, inp["gamma"], device=0)
+    sol.set_data(torch.from_numpy(inp["x_true"]).to(dev), torch.from_numpy(inp["xi"]).to(dev))
+    d, b = ops.make_data(op, inp["x_true"], inp["xi"], cfg.noise)
+    # b = C^T d: the two sides build C independently (Siddon t-differences of coordinates
+    # ~n/2 vs per-pixel clipping), so short segments carry ~eps * n / length relative error
+    assert np.max(np.abs(sol.b.cpu().numpy() - b.ravel())) <= 1e-11 * np.max(np.abs(op.C).T @ np.abs(d))
+    nb = np.linalg.norm(b)
+    outs = sol.run(K_out=2)
+    assert all(np.all(o.status == 0) for o in outs)
+    X = sol.final["X_prev"].cpu().numpy()
+    wx, wy = sol.wx.cpu().numpy().reshape(n, n), sol.wy.cpu().numpy().reshape(n, n)
+    for l in range(cfg.M):
+        rt = b.ravel() - ops.apply_shifted(op, wx, wy, inp["gamma"][l], X[l].reshape(n, n)).ravel()
+        assert np.linalg.norm(rt) <= cfg.tol * nb * (1 + 1e-6), (l, np.linalg.norm(rt) / nb)
