@@ -98,7 +98,7 @@ def _run_gpu(torch, dev, P, tol, maxit=20000, check_every=4, defl=True):
     out.iters = iters.ctypes.data_as(P_(L.C.c_int)); out.applies = apl.ctypes.data_as(P_(L.C.c_int64))
     out.relres_true = rel.ctypes.data_as(L._hp); out.status = stt.ctypes.data_as(P_(L.C.c_int))
     out.m_used = mu.ctypes.data_as(P_(L.C.c_int))
-    kmax = (J + 1) if defl else 0
+    kmax = (J + 1) if defl else 0   # (J of the call)
     ws = torch.empty(hd.minres_workspace_bytes(M, kmax), dtype=torch.uint8, device=dev)
     hd.get_counters(reset=True)
     hd.minres_recycled_batch(d, out, ws)
@@ -109,12 +109,15 @@ def _run_gpu(torch, dev, P, tol, maxit=20000, check_every=4, defl=True):
                 status=stt, m_used=mu)
 
 
-@pytest.mark.parametrize("n,r,sigma,defl", [(24, 2, 1.0, True), (37, 3, 1.3, True), (64, 4, 1.5, True),
-                                            (40, 3, 1.2, False)])
-def test_minres_batch_matches_oracle(torch_dev, n, r, sigma, defl):
+@pytest.mark.parametrize("n,r,sigma,defl,J", [(24, 2, 1.0, True, 4), (37, 3, 1.3, True, 4), (64, 4, 1.5, True, 4),
+                                              (40, 3, 1.2, False, 4), (64, 3, 1.2, True, 16), (48, 2, 1.0, True, 10)])
+def test_minres_batch_matches_oracle(torch_dev, n, r, sigma, defl, J):
+    """Odd sizes (37: host-polled lockstep kernels), even ones (cluster loop), the local
+    dimension at its maximum |J| + 1 = 17 and at the 10 / 11 boundary of the register
+    arrays."""
     torch, dev = torch_dev
     tol = 1e-10
-    P = _setup(n, r, sigma, M=6, J=4, seed=100 + n)
+    P = _setup(n, r, sigma, M=6, J=J, seed=100 + n)
     res = _run_gpu(torch, dev, P, tol, defl=defl)
     for l in range(P["M"]):
         A = lambda v, g=P["gam"][l]: ops.apply_shifted(P["h"], P["wx"], P["wy"], g, v.reshape(n, n)).ravel()
@@ -246,3 +249,19 @@ def test_minres_store_spans_the_cg_residual_space_and_error_paths(torch_dev):
     X2 = torch.zeros(1, ctcfg.N, dtype=torch.float64, device=dev)
     with pytest.raises(RskError):
         ct.cg([0], X2, [0])
+
+
+def test_minres_rank_deficient_local_space_drops_carried(torch_dev):
+    """g-hat equal to a W column makes Z_l rank deficient: the carried column is dropped
+    (status DEFL_DROPPED, m_used = J) and the solve still converges (as the oracle)."""
+    torch, dev = torch_dev
+    P = _setup(32, 2, 1.0, M=4, J=3, seed=5)
+    for l in range(P["M"]):
+        g = P["grp"][l]
+        P["Gh"][:, l] = P["W"][g][:, 0]
+        P["ZGh"][:, l] = P["AW"][g][:, 0] + P["gam"][l] * P["EW"][g][:, 0]
+    P["has_g"][:] = 1
+    res = _run_gpu(torch, dev, P, 1e-10)
+    assert np.all(res["status"] == 3), res["status"]
+    assert np.all(res["m_used"] == 3)
+    assert np.all(res["relres"] <= 1e-10)
