@@ -209,8 +209,11 @@ def test_cg_plain_batch_matches_oracle(torch_dev, n, loop, monkeypatch):
         np.testing.assert_allclose(st, np.stack(o.store[:st.shape[0]]), atol=1e-9)
 
 
-@pytest.mark.parametrize("loop", list(LOOPS))
-def test_cg_deflated_with_guess_and_carried_column(torch_dev, loop, monkeypatch):
+@pytest.mark.parametrize("loop,J", [(lp, 5) for lp in LOOPS] + [("cluster", 12), ("cluster", 16),
+                                                                  ("persistent", 16)])
+def test_cg_deflated_with_guess_and_carried_column(torch_dev, loop, J, monkeypatch):
+    """All three loops at |J| = 5; the cluster loop's wide register path (|J| > 8) and the
+    maximum local dimension |J| + 1 = 17."""
     for k, v in LOOPS[loop].items():
         monkeypatch.setenv(k, v)
     torch, dev = torch_dev
@@ -225,7 +228,6 @@ def test_cg_deflated_with_guess_and_carried_column(torch_dev, loop, monkeypatch)
     sol.set_data(_t(torch, dev, inp["x_true"]), _t(torch, dev, inp["xi"]))
     b = sol.b.cpu().numpy()
     rng = np.random.default_rng(12)
-    J = 5
     W, _ = np.linalg.qr(rng.standard_normal((N, J)))
     AW = np.stack([ops.apply_A(psf, W[:, j].reshape(n, n)).ravel() for j in range(J)], 1)
     EW = np.stack([ops.apply_E(wx, wy, W[:, j].reshape(n, n)).ravel() for j in range(J)], 1)
