@@ -45,7 +45,132 @@ void chol_solve_lower(int n, const double* L, double* x) {
 }
 
 // Cyclic Jacobi on sym(H); eigenvalues ascending, eigenvectors in columns of V.
+// Symmetric eigendecomposition by Householder tridiagonalisation + implicit-shift QL
+// (the EISPACK tred2 / tql2 pair; O(n^3) once instead of Jacobi's O(n^3) per sweep).
+// a (n x n, row-major z[i][j] = a[i*n+j]) is overwritten by the eigenvectors (columns),
+// d receives the eigenvalues (unsorted). Returns false if QL did not converge.
+static bool tred2_tql2(int n, std::vector<double>& z, std::vector<double>& d) {
+  std::vector<double> e(n, 0.0);
+  d.assign(n, 0.0);
+  auto Z = [&](int i, int j) -> double& { return z[(size_t)i * n + j]; };
+  for (int i = n - 1; i > 0; --i) {
+    const int l = i - 1;
+    double h = 0.0, scale = 0.0;
+    if (l > 0) {
+      for (int k = 0; k <= l; ++k) scale += std::fabs(Z(i, k));
+      if (scale == 0.0) {
+        e[i] = Z(i, l);
+      } else {
+        for (int k = 0; k <= l; ++k) {
+          Z(i, k) /= scale;
+          h += Z(i, k) * Z(i, k);
+        }
+        double f = Z(i, l);
+        double g = (f >= 0.0) ? -std::sqrt(h) : std::sqrt(h);
+        e[i] = scale * g;
+        h -= f * g;
+        Z(i, l) = f - g;
+        f = 0.0;
+        for (int j = 0; j <= l; ++j) {
+          Z(j, i) = Z(i, j) / h;
+          g = 0.0;
+          for (int k = 0; k <= j; ++k) g += Z(j, k) * Z(i, k);
+          for (int k = j + 1; k <= l; ++k) g += Z(k, j) * Z(i, k);
+          e[j] = g / h;
+          f += e[j] * Z(i, j);
+        }
+        const double hh = f / (h + h);
+        for (int j = 0; j <= l; ++j) {
+          f = Z(i, j);
+          e[j] = g = e[j] - hh * f;
+          for (int k = 0; k <= j; ++k) Z(j, k) -= (f * e[k] + g * Z(i, k));
+        }
+      }
+    } else {
+      e[i] = Z(i, l);
+    }
+    d[i] = h;
+  }
+  d[0] = 0.0;
+  e[0] = 0.0;
+  for (int i = 0; i < n; ++i) {
+    const int l = i - 1;
+    if (d[i] != 0.0) {
+      for (int j = 0; j <= l; ++j) {
+        double g = 0.0;
+        for (int k = 0; k <= l; ++k) g += Z(i, k) * Z(k, j);
+        for (int k = 0; k <= l; ++k) Z(k, j) -= g * Z(k, i);
+      }
+    }
+    d[i] = Z(i, i);
+    Z(i, i) = 1.0;
+    for (int j = 0; j <= l; ++j) Z(j, i) = Z(i, j) = 0.0;
+  }
+  // QL with implicit shifts on (d, e)
+  for (int i = 1; i < n; ++i) e[i - 1] = e[i];
+  e[n - 1] = 0.0;
+  for (int l = 0; l < n; ++l) {
+    int iter = 0, m;
+    do {
+      for (m = l; m < n - 1; ++m) {
+        const double dd = std::fabs(d[m]) + std::fabs(d[m + 1]);
+        if (std::fabs(e[m]) <= 1e-16 * dd) break;
+      }
+      if (m != l) {
+        if (iter++ == 60) return false;
+        double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
+        double r = std::hypot(g, 1.0);
+        g = d[m] - d[l] + e[l] / (g + (g >= 0.0 ? std::fabs(r) : -std::fabs(r)));
+        double s = 1.0, c = 1.0, p = 0.0;
+        int i;
+        for (i = m - 1; i >= l; --i) {
+          double f = s * e[i];
+          const double b = c * e[i];
+          e[i + 1] = (r = std::hypot(f, g));
+          if (r == 0.0) {
+            d[i + 1] -= p;
+            e[m] = 0.0;
+            break;
+          }
+          s = f / r;
+          c = g / r;
+          g = d[i + 1] - p;
+          r = (d[i] - g) * s + 2.0 * c * b;
+          d[i + 1] = g + (p = s * r);
+          g = c * r - b;
+          for (int k = 0; k < n; ++k) {
+            f = Z(k, i + 1);
+            Z(k, i + 1) = s * Z(k, i) + c * f;
+            Z(k, i) = c * Z(k, i) - s * f;
+          }
+        }
+        if (r == 0.0 && i >= l) continue;
+        d[l] -= p;
+        e[l] = g;
+        e[m] = 0.0;
+      }
+    } while (m != l);
+  }
+  return true;
+}
+
 void jacobi_eig(int n, const double* H, double* theta, double* V) {
+  // fast path: Householder + QL; cyclic Jacobi below only if QL does not converge
+  {
+    std::vector<double> z((size_t)n * n), d;
+    for (int i = 0; i < n; ++i)
+      for (int j = 0; j < n; ++j) z[(size_t)i * n + j] = 0.5 * (H[i + j * n] + H[j + i * n]);
+    if (n >= 2 && tred2_tql2(n, z, d)) {
+      std::vector<int> idx(n);
+      std::iota(idx.begin(), idx.end(), 0);
+      std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return d[a] < d[b]; });
+      for (int j = 0; j < n; ++j) {
+        theta[j] = d[idx[j]];
+        for (int i = 0; i < n; ++i) V[i + j * n] = z[(size_t)i * n + idx[j]];
+      }
+      return;
+    }
+  }
   std::vector<double> A(n * n);
   for (int j = 0; j < n; ++j)
     for (int i = 0; i < n; ++i) A[i + j * n] = 0.5 * (H[i + j * n] + H[j + i * n]);
@@ -67,17 +192,22 @@ void jacobi_eig(int n, const double* H, double* theta, double* V) {
         const double tau = (aqq - app) / (2.0 * apq);
         const double t = (tau >= 0 ? 1.0 : -1.0) / (std::fabs(tau) + std::sqrt(1.0 + tau * tau));
         const double c = 1.0 / std::sqrt(1.0 + t * t), s = t * c;
-        for (int k = 0; k < n; ++k) {  // A <- J^T A J (columns)
-          const double akp = A[k + p * n], akq = A[k + q * n];
-          A[k + p * n] = c * akp - s * akq;
-          A[k + q * n] = s * akp + c * akq;
+        // A <- J^T A J using the symmetry: columns p, q rotated (contiguous), rows mirrored,
+        // the 2 x 2 block in closed form (a_pp - t a_pq, a_qq + t a_pq, 0)
+        double* cp = &A[(size_t)p * n];
+        double* cq = &A[(size_t)q * n];
+        for (int k = 0; k < n; ++k) {
+          if (k == p || k == q) continue;
+          const double akp = cp[k], akq = cq[k];
+          const double np_ = c * akp - s * akq, nq_ = s * akp + c * akq;
+          cp[k] = np_;
+          cq[k] = nq_;
+          A[p + (size_t)k * n] = np_;
+          A[q + (size_t)k * n] = nq_;
         }
-        for (int k = 0; k < n; ++k) {  // rows
-          const double apk = A[p + k * n], aqk = A[q + k * n];
-          A[p + k * n] = c * apk - s * aqk;
-          A[q + k * n] = s * apk + c * aqk;
-        }
-        A[p + q * n] = A[q + p * n] = 0.0;
+        cp[p] = app - t * apq;
+        cq[q] = aqq + t * apq;
+        cp[q] = cq[p] = 0.0;
         for (int k = 0; k < n; ++k) {
           const double qkp = Q[k + p * n], qkq = Q[k + q * n];
           Q[k + p * n] = c * qkp - s * qkq;
@@ -100,16 +230,21 @@ void jacobi_svd(int k, const double* R, double* Ur, double* s, double* Vr) {
   std::vector<double> A(R, R + (size_t)k * k);
   std::vector<double> V((size_t)k * k, 0.0);
   for (int i = 0; i < k; ++i) V[i + i * k] = 1.0;
+  std::vector<double> cn(k);   // squared column norms, recomputed each sweep, updated per rotation
   for (int sweep = 0; sweep < 80; ++sweep) {
     bool rotated = false;
+    for (int j = 0; j < k; ++j) {
+      double t = 0.0;
+      for (int i = 0; i < k; ++i) t += A[i + j * k] * A[i + j * k];
+      cn[j] = t;
+    }
     for (int p = 0; p < k - 1; ++p) {
       for (int q = p + 1; q < k; ++q) {
-        double alpha = 0, beta = 0, gamma = 0;
-        for (int i = 0; i < k; ++i) {
-          alpha += A[i + p * k] * A[i + p * k];
-          beta += A[i + q * k] * A[i + q * k];
-          gamma += A[i + p * k] * A[i + q * k];
-        }
+        const double alpha = cn[p], beta = cn[q];
+        double gamma = 0;
+        const double* ap_ = &A[(size_t)p * k];
+        const double* aq_ = &A[(size_t)q * k];
+        for (int i = 0; i < k; ++i) gamma += ap_[i] * aq_[i];
         if (gamma == 0.0 || std::fabs(gamma) <= 1e-15 * std::sqrt(alpha * beta)) continue;
         rotated = true;
         const double zeta = (beta - alpha) / (2.0 * gamma);
@@ -123,6 +258,8 @@ void jacobi_svd(int k, const double* R, double* Ur, double* s, double* Vr) {
           V[i + p * k] = c * vp - sn * vq;
           V[i + q * k] = sn * vp + c * vq;
         }
+        cn[p] = alpha - t * gamma;   // the rotation moves t gamma between the two norms
+        cn[q] = beta + t * gamma;
       }
     }
     if (!rotated) break;
