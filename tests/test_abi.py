@@ -153,3 +153,16 @@ def test_create_slab_argument_errors_need_no_device(lib):
     assert lib.rsk_create_slab(C.byref(h), 0, 256, 256, 250, 64, hp, 9, 9, 8, 0) == L.RSK_EINVAL   # past the image
     assert lib.rsk_create_slab(C.byref(h), 0, 256, 256, 0, 4, hp, 9, 9, 8, 0) == L.RSK_EINVAL      # rows < halo
     assert lib.rsk_slab_info(None, None) == L.RSK_EINVAL
+
+
+def test_product_path_fails_loudly_without_the_library(tmp_path):
+    """No CPU fallback: loading a missing librsk raises (the product path never routes
+    through the oracle), and the package has no import of oracle/."""
+    from paper_2306_15049_b200 import _lib as L
+    with pytest.raises(RuntimeError, match="no CPU fallback"):
+        L.load(str(tmp_path / "librsk.so"))
+    pkg = os.path.join(ROOT, "paper_2306_15049_b200")
+    for f in os.listdir(pkg):
+        if f.endswith(".py"):
+            src = open(os.path.join(pkg, f)).read()
+            assert "import oracle" not in src and "from oracle" not in src, f
