@@ -7,6 +7,7 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <chrono>
 #include <cstring>
 #include <vector>
 
@@ -624,7 +625,9 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
   // The call is host-blocking: drain the caller's stream, then run on the handle's
   // private non-blocking stream (CUDA-graph capture is not allowed on the legacy
   // default stream), and drain that before returning.
+  const auto t_enter = std::chrono::steady_clock::now();
   RSK_CUDA(cudaStreamSynchronize(S(stream)));
+  const auto t_drained = std::chrono::steady_clock::now();
   cudaStream_t st = h->cg_stream;
   const bool prof = (d->flags & RSK_CG_PROFILE) != 0 && o->ms_loop;
 
@@ -849,6 +852,8 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
   RSK_CUDA(cudaEventCreate(&dl1));
   std::vector<int> it0(ns, 0);
   RSK_CUDA(cudaMemcpyAsync(it0.data(), hc.iters, sizeof(int) * ns, cudaMemcpyDeviceToHost, st));
+  RSK_CUDA(cudaStreamSynchronize(st));
+  const auto t_setup = std::chrono::steady_clock::now();
   RSK_CUDA(cudaEventRecord(dl0, st));
   if (cluster_mode) {
     unsigned* pbar = reinterpret_cast<unsigned*>(base + L.off_pbar);
@@ -943,6 +948,7 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
   RSK_CUDA(cudaEventSynchronize(dl1));
   float dl_ms = 0.0f;
   cudaEventElapsedTime(&dl_ms, dl0, dl1);
+  const auto t_loop = std::chrono::steady_clock::now();
   while (!active.empty()) {
     // active shifts grouped by shift group (group-shared kernels), with offsets/counts
     {
@@ -1063,6 +1069,14 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
   }
   int64_t tot_it = 0, tot_ap = 0;
   for (int s = 0; s < ns; ++s) { tot_it += it_h[s]; tot_ap += o->applies[s]; }
+  if (getenv("RSK_CG_TIMING")) {
+    auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+      return std::chrono::duration<double, std::milli>(b - a).count();
+    };
+    const auto t_end = std::chrono::steady_clock::now();
+    fprintf(stderr, "[rsk_cg] ns=%d drain %.2f setup %.2f loop %.2f (device %.2f) finish %.2f ms\n", ns,
+            ms(t_enter, t_drained), ms(t_drained, t_setup), ms(t_setup, t_loop), dl_ms, ms(t_loop, t_end));
+  }
   h->nA += tot_ap;
   h->nE += tot_ap;
   if (o->ms_loop && !prof) {
