@@ -2,6 +2,8 @@
 // batched dots / axpby, the IRN weight update, L-curve norms, and the two CG
 // vector kernels (update + dots, combine). All fp64, all reductions deterministic
 // (fixed per-thread order, fixed shuffle tree, fixed-order sum of CTA partials).
+#include <cstdlib>
+
 #include <cuda_runtime.h>
 
 #include "rsk_internal.h"
@@ -70,8 +72,104 @@ __global__ void gemm_tn_reduce(int k, int nv, int nchunk, const double* __restri
   C[i + (int64_t)j * ldc] = t;
 }
 
+// U^T V partials on the FP64 tensor cores (mma.sync.m8n8k4.f64 -> DMMA): CTA (chunk,
+// k-tile, nv-tile) computes a 32 x 32 block; warp w takes the 4-row groups w, w + 8, ... of
+// the chunk and holds 4 x 4 accumulator fragments (A = U^T: a = U[row q][col g], B = V:
+// b = V[row q][col g], D[g][2q..2q+1]); the 8 warp partials are summed in warp order
+// through shared memory. Same part[chunk][k][nv] layout as gemm_tn_part.
+__device__ __forceinline__ void dmma_tn(double& d0, double& d1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(d0), "+d"(d1)
+               : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(256) gemm_tn_part_tc(int64_t n, int k, const double* __restrict__ U, int64_t ldu,
+                                                       int nv, const double* __restrict__ V, int64_t ldv,
+                                                       double* __restrict__ part, int64_t rows_per_chunk) {
+  extern __shared__ double red[];   // [8 warps][32][33]
+  const int chunk = blockIdx.x;
+  const int kt = blockIdx.y * 32, vt = blockIdx.z * 32;
+  const int64_t rbeg = (int64_t)chunk * rows_per_chunk;
+  const int64_t rend = min(n, rbeg + rows_per_chunk);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  const double* up[4];
+  const double* vp[4];
+  bool uk[4], vk[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int cu = kt + 8 * i + g, cv = vt + 8 * i + g;
+    uk[i] = cu < k;
+    vk[i] = cv < nv;
+    up[i] = U + (int64_t)(uk[i] ? cu : 0) * ldu;
+    vp[i] = V + (int64_t)(vk[i] ? cv : 0) * ldv;
+  }
+#pragma unroll 2
+  for (int64_t r0 = rbeg + 4 * warp; r0 < rend; r0 += 32) {
+    const int64_t row = r0 + q;
+    const bool vr = row < rend;
+    double a[4], b[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      a[i] = (vr && uk[i]) ? __ldg(up[i] + row) : 0.0;
+      b[i] = (vr && vk[i]) ? __ldg(vp[i] + row) : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma_tn(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+  }
+  double* rw = red + (size_t)warp * 32 * 33;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      rw[(8 * i + g) * 33 + 8 * j + 2 * q] = acc[i][j][0];
+      rw[(8 * i + g) * 33 + 8 * j + 2 * q + 1] = acc[i][j][1];
+    }
+  __syncthreads();
+  double* pc = part + (int64_t)chunk * k * nv;
+  for (int e = threadIdx.x; e < 32 * 32; e += 256) {
+    const int m = e >> 5, c = e & 31;
+    const int gi = kt + m, gj = vt + c;
+    if (gi >= k || gj >= nv) continue;
+    double t = 0.0;
+    for (int w = 0; w < 8; ++w) t += red[(size_t)w * 32 * 33 + m * 33 + c];
+    pc[gi + (int64_t)gj * k] = t;
+  }
+}
+
 cudaError_t launch_gemm_tn(Handle* h, int64_t n, int k, const double* U, int64_t ldu, int nv,
                            const double* V, int64_t ldv, double* C, int64_t ldc, cudaStream_t st) {
+  if (k >= 16 && nv >= 16 && getenv("RSK_GEMM_NOTC") == nullptr) {   // tensor-core path for the wide Grams
+    const int tk = (k + 31) / 32, tv = (nv + 31) / 32;
+    int64_t nchunk = (2 * h->sm_count + tk * tv - 1) / (tk * tv);
+    const int64_t maxchunk = (n + 255) / 256;
+    if (nchunk > maxchunk) nchunk = maxchunk;
+    if (nchunk < 1) nchunk = 1;
+    const size_t cap = h->scratch_bytes / (sizeof(double) * (size_t)k * nv);
+    if ((size_t)nchunk > cap) nchunk = (int64_t)cap;
+    if (nchunk < 1) return cudaErrorMemoryAllocation;
+    int64_t rpc = (n + nchunk - 1) / nchunk;
+    rpc = (rpc + 31) / 32 * 32;
+    nchunk = (n + rpc - 1) / rpc;
+    const size_t smem = sizeof(double) * 8 * 32 * 33;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(gemm_tn_part_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = true;
+    }
+    dim3 grid((unsigned)nchunk, tk, tv);
+    count_launch(); gemm_tn_part_tc<<<grid, 256, smem, st>>>(n, k, U, ldu, nv, V, ldv, h->scratch, rpc);
+    const int64_t tot = (int64_t)k * nv;
+    count_launch(); gemm_tn_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(k, nv, (int)nchunk, h->scratch, C, ldc);
+    return cudaGetLastError();
+  }
   const int tk = (k + 31) / 32, tv = (nv + 31) / 32;
   int64_t nchunk = (2 * h->sm_count + tk * tv - 1) / (tk * tv);
   const int64_t maxchunk = (n + 255) / 256;
