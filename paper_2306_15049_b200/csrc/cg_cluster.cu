@@ -39,6 +39,7 @@ struct alignas(64) ClusterParams {
   int nshift;
   int64_t rows;        // rows per CTA of a cluster
   int prof;
+  int smem_r;          // 1: the CTA's rows of r live in shared memory for the whole shift
 };
 
 __device__ __forceinline__ void cl_sync() {
@@ -259,7 +260,15 @@ __global__ void __launch_bounds__(kAT, 1) cg_cluster_kernel(const __grid_constan
     const double* EWg = cg->grp.EW[grp];
     const double* Wg = cg->grp.W[grp];
     const int64_t ldw = cg->grp.ldw;
-    double* __restrict__ Rv = cg->R + (int64_t)s * N;
+    double* Rg = cg->R + (int64_t)s * N;
+    // r is touched only by its owning CTA (update, combine, store): keep the CTA's rows in
+    // shared memory behind the apply's buffers for the whole shift (-24 B/px per iteration)
+    double* sR = smem + ((Core::C::DBL + 1) & ~1);
+    double* Rv = Rg;
+    if (P.smem_r) {
+      for (int64_t i = rbeg + tid; i < rend; i += kAT) sR[i - rbeg] = Rg[i];
+      Rv = sR - rbeg;
+    }
     double* __restrict__ Pv = cg->P + (int64_t)s * N;
     double* __restrict__ Wv = cg->Wv + (int64_t)s * N;
     double* __restrict__ Xv = cg->X + (int64_t)s * cg->ldx;
@@ -398,6 +407,10 @@ __global__ void __launch_bounds__(kAT, 1) cg_cluster_kernel(const __grid_constan
       status = nst;
       if (nst != ST_ACTIVE && nst != ST_RCONV) break;
     }
+    if (P.smem_r) {   // r back to global memory (the host's confirmation norms read it)
+      __syncthreads();
+      for (int64_t i = rbeg + tid; i < rend; i += kAT) Rg[i] = sR[i - rbeg];
+    }
     // ---- per-shift outputs (leader CTA)
     if (crank == 0 && tid == 0) {
       cg->status[s] = status;
@@ -420,12 +433,18 @@ static cudaError_t launch_cluster_r(ClusterParams& prm, bool tma, int csize, int
                                     bool* ok) {
   using C = TcCfg<R, cluster_tile_rows(R)>;
   auto kfn = tma ? cg_cluster_kernel<R, true> : cg_cluster_kernel<R, false>;
-  const size_t smem = C::SMEM;
+  // r in shared memory if it fits next to the apply's buffers and the static arrays
+  const size_t rbytes = sizeof(double) * (size_t)prm.rows;
+  const size_t base = sizeof(double) * (size_t)((C::DBL + 1) & ~1);
+  prm.smem_r = (getenv("RSK_CLUSTER_RGLOBAL") == nullptr && base + rbytes + 12 * 1024 <= 227 * 1024) ? 1 : 0;
+  const size_t smem = prm.smem_r ? base + rbytes : C::SMEM;
   static int inited[2] = {0, 0};
   static int maxcl[2] = {0, 0};
   const int ti = tma ? 1 : 0;
-  if (!inited[ti]) {
+  static size_t attr_smem[2] = {0, 0};
+  if (!inited[ti] || smem > attr_smem[ti]) {
     inited[ti] = 1;
+    attr_smem[ti] = smem;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess && csize > 8) e = cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) { cudaGetLastError(); maxcl[ti] = 0; }
