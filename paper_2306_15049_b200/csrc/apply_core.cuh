@@ -471,8 +471,8 @@ struct ApplyCore {
       amark(3);
       if (p.want_dot) {
         const double bs = block_sum(dot, red);
-        if (dot_acc) {
-          if (tid == 0) *dot_acc += bs;
+        if (dot_acc) {          // per list index (the cluster loops pass one shift: [0])
+          if (tid == 0) dot_acc[li] += bs;
         } else if (!p.cg) {
           if (tid == 0) p.part[(int64_t)li * p.ntiles + tile] = bs;
         } else {

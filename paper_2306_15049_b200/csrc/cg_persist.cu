@@ -45,6 +45,7 @@ struct alignas(64) PersistParams {
   ApplyParams ap;      // CG-mode apply: X = P, X2 = caller x, Y = Wv
   CgDev* cg;
   double* partP;       // [shift][kPV][chunk]
+  double* partA;       // [shift][grid]: each CTA's p.w partial of phase A (its items, in order)
   unsigned* bar;       // grid barrier {count, generation}
   int* nactive;        // out: shifts still ACTIVE / RCONV when the launch returns
   int* iters_done;     // out: lockstep iterations run by this launch
@@ -165,7 +166,25 @@ __device__ __noinline__ void phase_b(const PersistParams& P, const PList& L, dou
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, q = lane & 3;
   const int64_t N = cg->N;
-  for (int li = tid; li < n; li += kAT) s_alpha[li] = (L.mode[li] == ST_ACTIVE) ? cg->alpha[L.sid[li]] : 0.0;
+  // alpha = rho / pi from the grid's phase-A partials (every CTA, same fixed order); CTA 0
+  // records it and flags breakdowns for B2 / C
+  for (int li = warp; li < n; li += kAT / 32) {   // a warp per shift: strided lanes, fixed tree
+    double a = 0.0;
+    if (L.mode[li] == ST_ACTIVE) {
+      const int s = L.sid[li];
+      const double* pa = P.partA + (size_t)s * gridDim.x;
+      double pi = 0.0;
+      for (int c = lane; c < (int)gridDim.x; c += 32) pi += __ldcg(pa + c);
+      pi = warp_sum(pi);
+      if (!(pi > 0.0) || !isfinite(pi)) {
+        if (blockIdx.x == 0 && lane == 0) { cg->status[s] = ST_BREAKDOWN; cg->alpha[s] = 0.0; }
+      } else {
+        a = cg->rho[s] / pi;
+        if (blockIdx.x == 0 && lane == 0) cg->alpha[s] = a;
+      }
+    }
+    if (lane == 0) s_alpha[li] = a;
+  }
   __syncthreads();
   double* red = smem;   // [kPW][32][kRW] (the apply stage buffers are free now)
   const int64_t rpw = P.rows / kPW;   // rows per warp (multiple of 32)
@@ -510,13 +529,20 @@ __device__ __noinline__ void phase_c(const PersistParams& P, const PList& L, dou
 
 // ---- phase A: the fused apply over the (tile, shift) items of the active list
 template <int R, bool kTma>
-__device__ __forceinline__ void phase_a(const PersistParams& P, const PList& L, double* smem, ApplyPipe& pp) {
+__device__ __forceinline__ void phase_a(const PersistParams& P, const PList& L, double* smem, ApplyPipe& pp,
+                                        double* s_pw) {
   const int n = L.n;
   const int nitems = n * P.ap.ntiles;
   const int per = (nitems + gridDim.x - 1) / gridDim.x;
   const int ibeg = blockIdx.x * per;
   const int iend = min(nitems, ibeg + per);
-  ApplyCore<R, kTma>::run(P.ap, smem, ibeg, iend, n, pp, L.sid, L.mode);
+  // p.w: per-CTA partials accumulated in shared memory over its items (fixed order), one
+  // store per shift; alpha is formed from them at the start of phase B (no per-item ticket)
+  for (int li = threadIdx.x; li < n; li += kAT) s_pw[li] = 0.0;
+  __syncthreads();
+  ApplyCore<R, kTma>::run(P.ap, smem, ibeg, iend, n, pp, L.sid, L.mode, s_pw);
+  __syncthreads();
+  for (int li = threadIdx.x; li < n; li += kAT) P.partA[(size_t)L.sid[li] * gridDim.x + blockIdx.x] = s_pw[li];
 }
 
 template <int R, bool kTma>
@@ -527,6 +553,7 @@ __global__ void __launch_bounds__(kAT, kApplyCtasPerSm) cg_persist_kernel(const 
   __shared__ int tmp[kPMaxShift];
   __shared__ double s_alpha[kPMaxShift], s_beta[kPMaxShift], s_rinv[kPMaxShift], s_gam[kPMaxShift];
   __shared__ int s_new[kPMaxShift], s_slot[kPMaxShift];
+  __shared__ double s_pw[kPMaxShift];
 
   CgDev* cg = P.cg;
   const int ns = P.nshift;
@@ -556,7 +583,7 @@ __global__ void __launch_bounds__(kAT, kApplyCtasPerSm) cg_persist_kernel(const 
     if (n == 0) break;
 
     // ================= A: w = A_gamma p (or A_gamma x for confirms)
-    phase_a<R, kTma>(P, L, smem, pp);
+    phase_a<R, kTma>(P, L, smem, pp, s_pw);
     mark(0);
     grid_sync(P.bar, gen);
     mark(1);
@@ -667,6 +694,7 @@ cudaError_t launch_cg_persist(Handle* h, CgDev* dev, const CgDev& hc, double* pa
   const bool tma = fill_apply_params(h, a, prm.ap, 0);
   prm.cg = dev;
   prm.partP = partP;
+  prm.partA = partP + (size_t)hc.nshift * nchunk * kPV;
   prm.bar = bar;
   prm.nactive = nactive;
   prm.iters_done = iters_done;

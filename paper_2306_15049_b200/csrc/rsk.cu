@@ -569,7 +569,7 @@ WsLayout ws_layout(const Handle* h, int ns) {
     L.rowsP = rp;
     L.nchunkP = (int)((N + rp - 1) / rp);
   }
-  L.off_partP = o; o = al(o + sizeof(double) * (size_t)ns * L.nchunkP * persist_pv());
+  L.off_partP = o; o = al(o + sizeof(double) * (size_t)ns * (L.nchunkP * persist_pv() + persist_grid(h)));
   L.off_pbar = o; o = al(o + sizeof(unsigned) * 8);
   // cluster-per-shift loop: per cluster, Z_s = AW + gamma_s EW of its current shift
   L.off_zw = o;
