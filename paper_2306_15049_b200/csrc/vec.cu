@@ -62,14 +62,32 @@ __global__ void __launch_bounds__(256) gemm_tn_part(int64_t n, int k, const doub
   if (gi + 1 < k && gj + 1 < nv) pc[gi + 1 + (int64_t)(gj + 1) * k] = acc11;
 }
 
+// C = sum over the chunk partials: a warp per output element when there are many chunks
+// (lanes stride the chunks, fixed shuffle tree), a thread per element otherwise
 __global__ void gemm_tn_reduce(int k, int nv, int nchunk, const double* __restrict__ part,
                                double* __restrict__ C, int64_t ldc) {
+  const int64_t tot = (int64_t)k * nv;
+  if (nchunk >= 32) {
+    const int64_t idx = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (idx >= tot) return;
+    double t = 0.0;
+    for (int c = lane; c < nchunk; c += 32) t += part[(int64_t)c * tot + idx];
+    t = wsum(t);
+    if (lane == 0) C[(idx % k) + (int64_t)(idx / k) * ldc] = t;
+    return;
+  }
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= (int64_t)k * nv) return;
+  if (idx >= tot) return;
   double t = 0.0;
-  for (int c = 0; c < nchunk; ++c) t += part[(int64_t)c * k * nv + idx];
+  for (int c = 0; c < nchunk; ++c) t += part[(int64_t)c * tot + idx];
   const int i = (int)(idx % k), j = (int)(idx / k);
   C[i + (int64_t)j * ldc] = t;
+}
+
+static inline unsigned reduce_blocks(int64_t tot, int nchunk) {
+  const int64_t threads = nchunk >= 32 ? tot * 32 : tot;
+  return (unsigned)((threads + 255) / 256);
 }
 
 // U^T V partials on the FP64 tensor cores (mma.sync.m8n8k4.f64 -> DMMA): CTA (chunk,
@@ -167,7 +185,7 @@ cudaError_t launch_gemm_tn(Handle* h, int64_t n, int k, const double* U, int64_t
     dim3 grid((unsigned)nchunk, tk, tv);
     count_launch(); gemm_tn_part_tc<<<grid, 256, smem, st>>>(n, k, U, ldu, nv, V, ldv, h->scratch, rpc);
     const int64_t tot = (int64_t)k * nv;
-    count_launch(); gemm_tn_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(k, nv, (int)nchunk, h->scratch, C, ldc);
+    count_launch(); gemm_tn_reduce<<<reduce_blocks(tot, (int)nchunk), 256, 0, st>>>(k, nv, (int)nchunk, h->scratch, C, ldc);
     return cudaGetLastError();
   }
   const int tk = (k + 31) / 32, tv = (nv + 31) / 32;
@@ -184,7 +202,7 @@ cudaError_t launch_gemm_tn(Handle* h, int64_t n, int k, const double* U, int64_t
   dim3 grid((unsigned)nchunk, tk, tv);
   count_launch(); gemm_tn_part<<<grid, 256, 0, st>>>(n, k, U, ldu, nv, V, ldv, h->scratch, rpc);
   const int64_t tot = (int64_t)k * nv;
-  count_launch(); gemm_tn_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(k, nv, (int)nchunk, h->scratch, C, ldc);
+  count_launch(); gemm_tn_reduce<<<reduce_blocks(tot, (int)nchunk), 256, 0, st>>>(k, nv, (int)nchunk, h->scratch, C, ldc);
   return cudaGetLastError();
 }
 
