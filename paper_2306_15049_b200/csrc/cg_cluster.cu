@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(kAT, 1) cg_cluster_kernel(const __grid_constan
   __shared__ double s_mu[kMaxM];
   __shared__ double s_dinv[kMaxM];
   __shared__ double s_alpha, s_beta, s_rinv;
-  __shared__ int s_mode, s_nst, s_slot, s_brk;
+  __shared__ int s_nst, s_slot, s_brk;
   __shared__ int s_list[1], s_lmode[1];
 
   CgDev* cg = P.cg;
@@ -245,7 +245,6 @@ __global__ void __launch_bounds__(kAT, 1) cg_cluster_kernel(const __grid_constan
     if (mode != ST_ACTIVE && mode != ST_RCONV) continue;
     const int m = cg->mloc[s], hg = cg->hasg[s], nw = m - hg;
     const int grp = cg->group[s];
-    const int J = cg->grp.J[grp];
     const double gam = cg->gam[s];
     const double thr = cg->tol * cg->bnorm;
     double rho = cg->rho[s];
