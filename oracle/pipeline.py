@@ -107,9 +107,9 @@ def outer_step(cfg, h, b, d, gamma, st: StepState, shifts=None) -> StepResult:
     elif getattr(cfg, "principal", "g10") == "vnew" and st.wx_prev is not None:
         V_new, a_new = principal_update(cfg, h, b, gamma, st)
         overhead += a_new
-        raw = np.column_stack([V_i1, V_new, st.X_prev])
+        raw = np.column_stack([V_i1, V_new, _raw_solutions(cfg, st.X_prev)])
     else:
-        raw = np.column_stack([V_i1, st.X_prev])
+        raw = np.column_stack([V_i1, _raw_solutions(cfg, st.X_prev)])
     Ut = rc.stabilize(raw, cfg.n_c)
     gstar = gamma[cfg.istar - 1]
     an = rc.anchor(h, wx, wy, Ut, b, gstar, n)
@@ -205,6 +205,15 @@ def principal_update(cfg, h, b, gamma, st):
     res = _seed_solver(cfg)(A, q, tol=cfg.tol, maxit=100, store_cap=100)
     cols = [res.x] + list(res.store)
     return np.column_stack(cols), res.applies + 2
+
+
+def _raw_solutions(cfg, X_prev):
+    """Reading G39 (weak scaling by shift): with cfg.ladder_base the k >= 1 raw block keeps
+    every (M / ladder_base)-th previous solution; otherwise all of them (eq:tildeUupdate)."""
+    base = getattr(cfg, "ladder_base", 0)
+    if base and cfg.M > base:
+        return X_prev[:, ::cfg.M // base][:, :base]
+    return X_prev
 
 
 def _seed_solver(cfg):

@@ -255,9 +255,9 @@ class GpuSolver:
         elif getattr(cfg, "principal", "g10") == "vnew" and st.get("W_prev") is not None:
             V_new, a_new = self.principal_update(st)
             overhead += a_new
-            raw = torch.cat([V_i1, V_new, st["X_prev"]], 0)
+            raw = torch.cat([V_i1, V_new, self._raw_solutions(st["X_prev"])], 0)
         else:
-            raw = torch.cat([V_i1, st["X_prev"]], 0)
+            raw = torch.cat([V_i1, self._raw_solutions(st["X_prev"])], 0)
         Ut = self.stabilize(raw, nc_cap)
         nc = Ut.shape[0]
         del raw
@@ -266,6 +266,14 @@ class GpuSolver:
         self.h.apply_shifted(Ut, ZA, EY=ZE, mode=L.RSK_APPLY_SPLIT, stream=self.stream)
         overhead += nc
         return Ut, ZA, ZE, V_i1, overhead
+
+    def _raw_solutions(self, Xp: torch.Tensor) -> torch.Tensor:
+        """X^(k-1) columns of the k >= 1 raw block: all of them, or with cfg.ladder_base
+        (weak scaling by shift, reading G39) every (M / ladder_base)-th one."""
+        base = getattr(self.cfg, "ladder_base", 0)
+        if base and self.M > base:
+            return Xp[::self.M // base][:base].contiguous()
+        return Xp
 
     def principal_update(self, st: dict):
         """eq:delta (reading G36): at l_c solve

@@ -62,6 +62,8 @@ class Config:
                                # matrix, Example 2 P:1083-1098) -- SURVEY §8(f) f4
     n_angles: int = 0          # CT: projection angles 1, 2, ..., n_angles degrees
     idx: tuple = ()            # index overrides (i2, i*, I, J_L, J_R, l_c), 1-based; () = rules G11/G36
+    ladder_base: int = 0       # weak scaling by shift (G39): M = ladder_base * G; the k >= 1 raw block
+                               # keeps every (M / ladder_base)-th previous solution (0 = all)
 
     @property
     def N(self) -> int:
