@@ -449,6 +449,7 @@ struct alignas(64) MrClusterParams {
   const int* list;    // shifts to run (device), nl of them
   int nl;
   int64_t rows;       // rows per CTA
+  int smem_vp;        // 1: the CTA's rows of v_{j-1} live in shared memory for the whole shift
 };
 
 __host__ __device__ constexpr int mr_tile_rows(int r) { return r <= 6 ? 64 : (r <= 8 ? 56 : tc_tile_rows(r)); }
@@ -608,7 +609,15 @@ __global__ void __launch_bounds__(kAT, 1) mr_cluster_kernel(const __grid_constan
     const int m = g->m[s];
     const double* K = g->Kb + (int64_t)s * kMrK * N;
     double* V = g->V + (int64_t)s * N;
-    double* Vp = g->Vp + (int64_t)s * N;
+    double* Vpg = g->Vp + (int64_t)s * N;
+    // v_{j-1} is touched only by its owning CTA (phases C and D): its rows stay in shared
+    // memory behind the apply's buffers for the whole shift when they fit
+    double* sVp = smem + ((Core::C::DBL + 1) & ~1);
+    double* Vp = Vpg;
+    if (P.smem_vp) {
+      for (int64_t i = rbeg + tid; i < rend; i += kAT) sVp[i - rbeg] = Vpg[i];
+      Vp = sVp - rbeg;
+    }
     double* W = g->Wv + (int64_t)s * N;
     double* D1 = g->D1 + (int64_t)s * N;
     double* D2 = g->D2 + (int64_t)s * N;
@@ -761,6 +770,10 @@ __global__ void __launch_bounds__(kAT, 1) mr_cluster_kernel(const __grid_constan
       }
       if (status != ST_ACTIVE) break;
     }
+    if (P.smem_vp) {   // v_{j-1} back to global memory (a host restart reinitialises it there)
+      __syncthreads();
+      for (int64_t i = rbeg + tid; i < rend; i += kAT) Vpg[i] = sVp[i - rbeg];
+    }
     if (crank == 0 && tid == 0) {
       sc[S_BETA] = beta; sc[S_EPS] = eps; sc[S_DBAR] = dbar; sc[S_CS] = cs; sc[S_SN] = sn; sc[S_PHIBAR] = phibar;
       g->iters[s] = iters;
@@ -780,12 +793,17 @@ template <int R>
 cudaError_t mr_launch_r(const MrClusterParams& prm, bool tma, int ncl_req, cudaStream_t st, bool* ok) {
   using C = TcCfg<R, mr_tile_rows(R)>;
   auto kfn = tma ? mr_cluster_kernel<R, true> : mr_cluster_kernel<R, false>;
-  const size_t smem = C::SMEM;
+  const size_t base = sizeof(double) * (size_t)((C::DBL + 1) & ~1);
+  const size_t vpb = sizeof(double) * (size_t)prm.rows;
+  const int smem_vp = (getenv("RSK_MR_VPGLOBAL") == nullptr && base + vpb + 16 * 1024 <= 227 * 1024) ? 1 : 0;
+  const size_t smem = smem_vp ? base + vpb : C::SMEM;
   static int inited[2] = {0, 0};
   static int maxcl[2] = {0, 0};
+  static size_t attr_smem[2] = {0, 0};
   const int ti = tma ? 1 : 0;
-  if (!inited[ti]) {
+  if (!inited[ti] || smem > attr_smem[ti]) {
     inited[ti] = 1;
+    attr_smem[ti] = smem;
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e == cudaSuccess) e = cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     if (e != cudaSuccess) { cudaGetLastError(); maxcl[ti] = 0; }
@@ -810,7 +828,9 @@ cudaError_t mr_launch_r(const MrClusterParams& prm, bool tma, int ncl_req, cudaS
   cfg.gridDim = dim3(kMrCS * ncl); cfg.blockDim = dim3(kAT); cfg.dynamicSmemBytes = smem; cfg.stream = st;
   cfg.attrs = at; cfg.numAttrs = 1;
   count_launch();
-  cudaError_t e = cudaLaunchKernelEx(&cfg, kfn, prm);
+  MrClusterParams p2 = prm;
+  p2.smem_vp = smem_vp;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kfn, p2);
   if (e != cudaSuccess) { cudaGetLastError(); *ok = false; return cudaSuccess; }
   *ok = true;
   return cudaSuccess;
