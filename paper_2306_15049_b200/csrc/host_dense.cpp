@@ -225,8 +225,87 @@ void jacobi_eig(int n, const double* H, double* theta, double* V) {
   }
 }
 
+static void jacobi_svd_plain(int k, const double* R, double* Ur, double* s, double* Vr);
+
 // One-sided Jacobi SVD of a k x k matrix: R = Ur diag(s) Vr^T, s descending.
+// k >= 24: preconditioned by Householder QR with column pivoting (R P = Q1 R1), the Jacobi
+// sweeps then run on X = R1^T, whose columns are close to orthogonal (a few sweeps instead
+// of many): X V = Ux S, so R = (Q1 V) S (P Ux)^T.
 void jacobi_svd(int k, const double* R, double* Ur, double* s, double* Vr) {
+  if (k < 24) { jacobi_svd_plain(k, R, Ur, s, Vr); return; }
+  std::vector<double> A(R, R + (size_t)k * k);
+  std::vector<int> perm(k);
+  std::iota(perm.begin(), perm.end(), 0);
+  std::vector<double> tau(k, 0.0), cn(k);
+  for (int j = 0; j < k; ++j) {
+    double t = 0.0;
+    for (int i = 0; i < k; ++i) t += A[i + (size_t)j * k] * A[i + (size_t)j * k];
+    cn[j] = t;
+  }
+  for (int j = 0; j < k; ++j) {
+    // pivot: the remaining column of largest norm (recomputed: k is small)
+    int pj = j;
+    double best = -1.0;
+    for (int c = j; c < k; ++c) {
+      double t = 0.0;
+      for (int i = j; i < k; ++i) t += A[i + (size_t)c * k] * A[i + (size_t)c * k];
+      if (t > best) { best = t; pj = c; }
+    }
+    if (pj != j) {
+      for (int i = 0; i < k; ++i) std::swap(A[i + (size_t)j * k], A[i + (size_t)pj * k]);
+      std::swap(perm[j], perm[pj]);
+    }
+    // Householder reflector for A[j:, j]
+    double nrm = 0.0;
+    for (int i = j; i < k; ++i) nrm += A[i + (size_t)j * k] * A[i + (size_t)j * k];
+    nrm = std::sqrt(nrm);
+    if (nrm == 0.0) { tau[j] = 0.0; continue; }
+    const double a0 = A[j + (size_t)j * k];
+    const double beta = a0 >= 0 ? -nrm : nrm;
+    const double v0 = a0 - beta;
+    for (int i = j + 1; i < k; ++i) A[i + (size_t)j * k] /= v0;   // v = [1, A[j+1:, j]]
+    tau[j] = (beta - a0) / beta;
+    A[j + (size_t)j * k] = beta;
+    for (int c = j + 1; c < k; ++c) {
+      double w = A[j + (size_t)c * k];
+      for (int i = j + 1; i < k; ++i) w += A[i + (size_t)j * k] * A[i + (size_t)c * k];
+      w *= tau[j];
+      A[j + (size_t)c * k] -= w;
+      for (int i = j + 1; i < k; ++i) A[i + (size_t)c * k] -= w * A[i + (size_t)j * k];
+    }
+  }
+  // Q1 (explicit) from the reflectors, R1 = upper triangle of A
+  std::vector<double> Q((size_t)k * k, 0.0);
+  for (int i = 0; i < k; ++i) Q[i + (size_t)i * k] = 1.0;
+  for (int j = k - 1; j >= 0; --j) {
+    if (tau[j] == 0.0) continue;
+    for (int c = 0; c < k; ++c) {
+      double w = Q[j + (size_t)c * k];
+      for (int i = j + 1; i < k; ++i) w += A[i + (size_t)j * k] * Q[i + (size_t)c * k];
+      w *= tau[j];
+      Q[j + (size_t)c * k] -= w;
+      for (int i = j + 1; i < k; ++i) Q[i + (size_t)c * k] -= w * A[i + (size_t)j * k];
+    }
+  }
+  // X = R1^T (lower triangular)
+  std::vector<double> X((size_t)k * k, 0.0);
+  for (int j = 0; j < k; ++j)
+    for (int i = 0; i <= j; ++i) X[j + (size_t)i * k] = A[i + (size_t)j * k];
+  std::vector<double> Ux((size_t)k * k), sx(k), Vx((size_t)k * k);
+  jacobi_svd_plain(k, X.data(), Ux.data(), sx.data(), Vx.data());   // X = Ux S Vx^T
+  // R P = Q1 R1 = Q1 X^T = Q1 Vx S Ux^T  ->  Ur = Q1 Vx, Vr = P Ux
+  for (int j = 0; j < k; ++j) {
+    s[j] = sx[j];
+    for (int i = 0; i < k; ++i) {
+      double t = 0.0;
+      for (int q = 0; q < k; ++q) t += Q[i + (size_t)q * k] * Vx[q + (size_t)j * k];
+      Ur[i + (size_t)j * k] = t;
+      Vr[perm[i] + (size_t)j * k] = Ux[i + (size_t)j * k];
+    }
+  }
+}
+
+static void jacobi_svd_plain(int k, const double* R, double* Ur, double* s, double* Vr) {
   std::vector<double> A(R, R + (size_t)k * k);
   std::vector<double> V((size_t)k * k, 0.0);
   for (int i = 0; i < k; ++i) V[i + i * k] = 1.0;
