@@ -104,7 +104,7 @@ def oracle_sample(cfg, inputs, budget_s=12.0):
     h = opipe.operator_of(cfg, inputs)   # the PSF, or the CT matrix (C6)
     d, b = ops.make_data(h, inputs["x_true"], inputs["xi"], cfg.noise)
     wx, wy = ops.identity_weights(n)
-    g = float(inputs["gamma"][cfg.i1 - 1])
+    g = float(inputs["gamma"][0])   # gamma_i1, i1 = 1
     A = lambda v: ops.apply_shifted(h, wx, wy, g, v.reshape(n, n)).ravel()
     # time a few iterations to size the sample to the budget
     t0 = time.perf_counter()

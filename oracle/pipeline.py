@@ -22,6 +22,7 @@ import math
 import numpy as np
 
 from . import defcg as dcg
+from . import indices as _ix
 from . import minres as mr
 from . import operators as ops
 from . import recycle as rc
@@ -93,7 +94,7 @@ def outer_step(cfg, h, b, d, gamma, st: StepState, shifts=None) -> StepResult:
         return lambda v: ops.apply_shifted(h, wx, wy, g, v.reshape(n, n)).ravel()
 
     overhead = 0
-    i1, i2 = cfg.i1 - 1, cfg.i2 - 1
+    i1, i2 = _ix.of(cfg).i1 - 1, _ix.of(cfg).i2 - 1
     V_i1 = st.V_i1
     if st.k == 0:
         n1 = math.ceil(2 * (cfg.n_c - 2) / 3)
@@ -107,11 +108,11 @@ def outer_step(cfg, h, b, d, gamma, st: StepState, shifts=None) -> StepResult:
     elif getattr(cfg, "principal", "g10") == "vnew" and st.wx_prev is not None:
         V_new, a_new = principal_update(cfg, h, b, gamma, st)
         overhead += a_new
-        raw = np.column_stack([V_i1, V_new, _raw_solutions(cfg, st.X_prev)])
+        raw = np.column_stack([V_i1, V_new, st.X_prev])
     else:
-        raw = np.column_stack([V_i1, _raw_solutions(cfg, st.X_prev)])
+        raw = np.column_stack([V_i1, st.X_prev])
     Ut = rc.stabilize(raw, cfg.n_c)
-    gstar = gamma[cfg.istar - 1]
+    gstar = gamma[_ix.of(cfg).istar - 1]
     an = rc.anchor(h, wx, wy, Ut, b, gstar, n)
     overhead += Ut.shape[1]
     mode = getattr(cfg, "guess", "orth")
@@ -124,16 +125,16 @@ def outer_step(cfg, h, b, d, gamma, st: StepState, shifts=None) -> StepResult:
     elif mode == "oblique2":
         # eq:updates: anchors gamma_{I_L} (left group) and gamma_{I_R} (right group); the
         # images Z_A, Z_E are shared (no extra applies), only K, R differ (reading G34)
-        anL = an if cfg.I_L == cfg.istar else rc.anchor(h, wx, wy, Ut, b, gamma[cfg.I_L - 1], n)
-        anR = rc.anchor(h, wx, wy, Ut, b, gamma[cfg.I_R - 1], n)
+        anL = an if _ix.of(cfg).I_L == _ix.of(cfg).istar else rc.anchor(h, wx, wy, Ut, b, gamma[_ix.of(cfg).I_L - 1], n)
+        anR = rc.anchor(h, wx, wy, Ut, b, gamma[_ix.of(cfg).I_R - 1], n)
 
         def guess(l):
-            return rc.oblique_guess(anL if (l + 1) <= cfg.I_split else anR, gamma[l])
+            return rc.oblique_guess(anL if (l + 1) <= _ix.of(cfg).I else anR, gamma[l])
     else:
         raise ValueError(f"unknown guess mode {mode!r}")
 
     groups = {}
-    for gname, jidx in (("L", cfg.J_L - 1), ("R", cfg.J_R - 1)):
+    for gname, jidx in (("L", _ix.of(cfg).J_L - 1), ("R", _ix.of(cfg).J_R - 1)):
         W, AW, EW, _, _ = rc.group_ritz(an, gamma[jidx], cfg.J)
         groups[gname] = (W, AW, EW)
 
@@ -144,7 +145,7 @@ def outer_step(cfg, h, b, d, gamma, st: StepState, shifts=None) -> StepResult:
     todo = range(M) if shifts is None else shifts
     seq = getattr(cfg, "local", "d3") == "seq"
     for l in todo:
-        W, AW, EW = groups["L" if (l + 1) <= cfg.I_split else "R"]
+        W, AW, EW = groups["L" if (l + 1) <= _ix.of(cfg).I else "R"]
         xp = guess(l)
         cols_U = [W]
         cols_Z = [AW + gamma[l] * EW]
@@ -197,7 +198,7 @@ def principal_update(cfg, h, b, gamma, st):
     the same span as MINRES's Lanczos vectors); V^(new) = [dx, stored residuals]
     (<= 101 columns). Returns (V_new, applies: the two E images + CG)."""
     n = cfg.n
-    lc = cfg.l_c - 1
+    lc = _ix.of(cfg).l_c - 1
     gc = gamma[lc]
     x = st.X_prev[:, lc].reshape(n, n)
     q = gc * (ops.apply_E(st.wx, st.wy, x) - ops.apply_E(st.wx_prev, st.wy_prev, x)).ravel()
@@ -205,15 +206,6 @@ def principal_update(cfg, h, b, gamma, st):
     res = _seed_solver(cfg)(A, q, tol=cfg.tol, maxit=100, store_cap=100)
     cols = [res.x] + list(res.store)
     return np.column_stack(cols), res.applies + 2
-
-
-def _raw_solutions(cfg, X_prev):
-    """Reading G39 (weak scaling by shift): with cfg.ladder_base the k >= 1 raw block keeps
-    every (M / ladder_base)-th previous solution; otherwise all of them (eq:tildeUupdate)."""
-    base = getattr(cfg, "ladder_base", 0)
-    if base and cfg.M > base:
-        return X_prev[:, ::cfg.M // base][:, :base]
-    return X_prev
 
 
 def _seed_solver(cfg):
@@ -234,7 +226,7 @@ def operator_of(cfg, inputs):
 
 def _same_group(cfg, a, b):
     """Shifts a, b (0-based) in the same group (left: l <= I, right: l > I; Alg. 4)."""
-    return ((a + 1) <= cfg.I_split) == ((b + 1) <= cfg.I_split)
+    return ((a + 1) <= _ix.of(cfg).I) == ((b + 1) <= _ix.of(cfg).I)
 
 
 def next_weights(cfg, st_w, xstar):

@@ -28,6 +28,7 @@ import torch
 
 from . import _lib as L
 from . import shard
+from .indices import shift_indices
 from .rsk import (Handle, carried_select, lcurve_corner, oblique_guess, orth_guess, pencil_ritz,
                   stabilize_small, sym_eig)
 
@@ -97,7 +98,7 @@ class GpuSolver:
         self.lc_scratch = torch.empty(M, self.h.ndata, **f)
         self.rho_dev = torch.empty(M, **f)
         self.eta_dev = torch.empty(M, **f)
-        self.grp = np.array([0 if (l + 1) <= cfg.I_split else 1 for l in range(M)], dtype=np.int32)
+        self.grp = np.array([0 if (l + 1) <= shift_indices(cfg).I_split else 1 for l in range(M)], dtype=np.int32)
 
     # ------------------------------------------------------------------ data
     def set_data(self, x_true: torch.Tensor, xi: torch.Tensor):
@@ -237,7 +238,7 @@ class GpuSolver:
         cfg = self.cfg
         N, nc_cap = self.N, cfg.n_c
         overhead = 0
-        i1, i2 = cfg.i1 - 1, cfg.i2 - 1
+        i1, i2 = shift_indices(cfg).i1 - 1, shift_indices(cfg).i2 - 1
         V_i1 = st.get("V_i1")
         if k == 0:
             n1 = math.ceil(2 * (nc_cap - 2) / 3)
@@ -255,9 +256,9 @@ class GpuSolver:
         elif getattr(cfg, "principal", "g10") == "vnew" and st.get("W_prev") is not None:
             V_new, a_new = self.principal_update(st)
             overhead += a_new
-            raw = torch.cat([V_i1, V_new, self._raw_solutions(st["X_prev"])], 0)
+            raw = torch.cat([V_i1, V_new, st["X_prev"]], 0)
         else:
-            raw = torch.cat([V_i1, self._raw_solutions(st["X_prev"])], 0)
+            raw = torch.cat([V_i1, st["X_prev"]], 0)
         Ut = self.stabilize(raw, nc_cap)
         nc = Ut.shape[0]
         del raw
@@ -267,14 +268,6 @@ class GpuSolver:
         overhead += nc
         return Ut, ZA, ZE, V_i1, overhead
 
-    def _raw_solutions(self, Xp: torch.Tensor) -> torch.Tensor:
-        """X^(k-1) columns of the k >= 1 raw block: all of them, or with cfg.ladder_base
-        (weak scaling by shift, reading G39) every (M / ladder_base)-th one."""
-        base = getattr(self.cfg, "ladder_base", 0)
-        if base and self.M > base:
-            return Xp[::self.M // base][:base].contiguous()
-        return Xp
-
     def principal_update(self, st: dict):
         """eq:delta (reading G36): at l_c solve
         (A + gamma_c E_k) dx = gamma_c (E_k - E_{k-1}) x^(k-1,l_c) by <= 100 CG steps from 0
@@ -282,7 +275,7 @@ class GpuSolver:
         are split applies under W_k and W_{k-1} (the handle's weights are swapped and
         restored). Returns (V_new, applies)."""
         cfg = self.cfg
-        lc = cfg.l_c - 1
+        lc = shift_indices(cfg).l_c - 1
         x = st["X_prev"][lc:lc + 1].contiguous()
         Ax = torch.empty_like(x); Ek = torch.empty_like(x); Ep = torch.empty_like(x)
         self.h.apply_shifted(x, Ax, EY=Ek, mode=L.RSK_APPLY_SPLIT, stream=self.stream)
@@ -321,7 +314,7 @@ class GpuSolver:
             torch.cuda.synchronize(self.dev)
             dist.bcast(Ut); dist.bcast(ZA); dist.bcast(ZE)
         # ---- anchoring (eq:establishU) and Grams: identical on every rank
-        gstar = float(self.gamma[cfg.istar - 1])
+        gstar = float(self.gamma[shift_indices(cfg).istar - 1])
         Y = ZA.clone()
         self.h.batch_axpby(np.full(nc, gstar), ZE, None, Y, stream=self.stream)
         K = torch.empty_like(Y)
@@ -351,7 +344,7 @@ class GpuSolver:
             self.guess_hook(k, mine, X, has_xp[mine])
         # ---- group Ritz blocks (Alg. 2 / Alg. 4)
         Wg, AWg, EWg = [], [], []
-        for jidx in (cfg.J_L - 1, cfg.J_R - 1):
+        for jidx in (shift_indices(cfg).J_L - 1, shift_indices(cfg).J_R - 1):
             Wt, _ = pencil_ritz(Ahat, Ehat, float(self.gamma[jidx]), min(cfg.J, nc))
             Wg.append(self.combine(Ut, Wt)); AWg.append(self.combine(ZA, Wt)); EWg.append(self.combine(ZE, Wt))
         del ZA, ZE
@@ -359,7 +352,7 @@ class GpuSolver:
         # ---- carried corrections (Alg. 3, reading D3 / G12) for this rank's shifts
         ghat = None
         keep = None
-        nL = int(np.sum(np.asarray(mine) < cfg.I_split))
+        nL = int(np.sum(np.asarray(mine) < shift_indices(cfg).I_split))
         if k >= 1 and st.get("G_prev") is not None and ml:
             idx = torch.tensor(mine, dtype=torch.long, device=self.dev)
             Gp = st["G_prev"][idx].contiguous()
@@ -433,8 +426,8 @@ class GpuSolver:
         if self.dist.enabled and self.dist.world > 1:
             raise NotImplementedError("local='seq' chains are solved on one rank")
         ml = len(mine)
-        chains = [[i for i in range(ml) if (mine[i] + 1) <= cfg.I_split],
-                  [i for i in range(ml) if (mine[i] + 1) > cfg.I_split]]
+        chains = [[i for i in range(ml) if (mine[i] + 1) <= shift_indices(cfg).I_split],
+                  [i for i in range(ml) if (mine[i] + 1) > shift_indices(cfg).I_split]]
         out = dict(iters=np.zeros(ml, np.int32), applies=np.zeros(ml, np.int64), relres=np.zeros(ml),
                    status=np.zeros(ml, np.int32), m_used=np.zeros(ml, np.int32), prof=np.zeros(8),
                    overhead=0)
@@ -497,9 +490,9 @@ class GpuSolver:
         the anchor gamma_{I_L}, of the right group from gamma_{I_R}; the images Z_A, Z_E
         are shared, each extra anchor costs one shifted CholQR3 and two projections."""
         cfg = self.cfg
-        nI = cfg.I_split
+        nI = shift_indices(cfg).I_split
         parts = []
-        for (ia, sl) in ((cfg.I_L, slice(0, nI)), (cfg.I_R, slice(nI, self.M))):
+        for (ia, sl) in ((shift_indices(cfg).I_L, slice(0, nI)), (shift_indices(cfg).I_R, slice(nI, self.M))):
             ga = float(self.gamma[ia - 1])
             if ga == gstar:
                 Ra, KtZEa, Ktba = R, KtZE, Ktb

@@ -29,6 +29,7 @@ import numpy as np
 import torch
 
 from . import _lib as L
+from .indices import shift_indices
 from .rsk import Handle, RskError
 
 LOOP_ACTIVE, LOOP_RCONV, LOOP_DONE, LOOP_BREAKDOWN, LOOP_MAXIT = range(5)
@@ -693,7 +694,7 @@ class SlabGpuSolver:
         self.lc_scratch = torch.empty(M, N, **f)
         self.rho_dev = torch.empty(M, **f)
         self.eta_dev = torch.empty(M, **f)
-        self.grp = np.array([0 if (l + 1) <= cfg.I_split else 1 for l in range(M)], dtype=np.int32)
+        self.grp = np.array([0 if (l + 1) <= shift_indices(cfg).I_split else 1 for l in range(M)], dtype=np.int32)
 
     def set_data(self, x_true_full: torch.Tensor, xi_full: torch.Tensor):
         """the global seeded images, cut to this slab (each rank holds its rows + halo)"""

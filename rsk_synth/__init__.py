@@ -62,45 +62,10 @@ class Config:
                                # matrix, Example 2 P:1083-1098) -- SURVEY §8(f) f4
     n_angles: int = 0          # CT: projection angles 1, 2, ..., n_angles degrees
     idx: tuple = ()            # index overrides (i2, i*, I, J_L, J_R, l_c), 1-based; () = rules G11/G36
-    ladder_base: int = 0       # weak scaling by shift (G39): M = ladder_base * G; the k >= 1 raw block
-                               # keeps every (M / ladder_base)-th previous solution (0 = all)
 
     @property
     def N(self) -> int:
         return self.n * self.n
-
-    # Index readings of SURVEY G11 (1-based, as in the paper's Table)
-    @property
-    def i1(self) -> int:
-        return 1
-
-    @property
-    def i2(self) -> int:
-        return self.idx[0] if self.idx else self.M // 2
-
-    @property
-    def istar(self) -> int:
-        return self.idx[1] if self.idx else self.M // 2
-
-    @property
-    def I_split(self) -> int:
-        return self.idx[2] if self.idx else int(round(0.75 * self.M))
-
-    @property
-    def J_L(self) -> int:
-        return self.idx[3] if self.idx else self.I_split
-
-    @property
-    def J_R(self) -> int:
-        return self.idx[4] if self.idx else self.M - 1
-
-    @property
-    def l_c(self) -> int:
-        """Shift of the eq:delta correction solve (P:648 "one of the large gamma_l";
-        Example 1 takes 18 of 20): round(0.9 M), 1-based (reading G36)."""
-        if self.idx:
-            return self.idx[5]
-        return max(1, min(self.M, int(round(0.9 * self.M))))
 
     @property
     def ndet(self) -> int:
@@ -114,17 +79,6 @@ class Config:
     def ndata(self) -> int:
         """Length of the data vector d: N for the blur, n_angles * ndet for CT."""
         return self.n_angles * self.ndet if self.operator == "ct" else self.N
-
-    # anchors of the two-anchor oblique guesses (eq:updates P:1000-1005; reading G34):
-    # I_L = i* (already the principal anchor, inside the left group), I_R = the middle
-    # of the right group
-    @property
-    def I_L(self) -> int:
-        return self.istar
-
-    @property
-    def I_R(self) -> int:
-        return (self.I_split + 1 + self.M + 1) // 2
 
 
 CONFIGS = {

@@ -8,6 +8,7 @@ import numpy as np
 import pytest
 
 import rsk_synth as S
+from paper_2306_15049_b200.indices import shift_indices
 from oracle import dense
 from oracle import operators as ops
 from oracle import pipeline as opipe
@@ -67,7 +68,7 @@ def test_vnew_stepwise_handoff(torch_dev, inner):
             # so compare the iterates to 1e-4 and their residuals in eq:delta to 25 %
             # (MINRES: Lanczos loses orthogonality over the 100 steps, iterates agree to 1e-2)
             assert np.linalg.norm(dxg - dxo) <= (1e-4 if inner == "cg" else 1e-2) * np.linalg.norm(dxo)
-            lc = cfg.l_c - 1
+            lc = shift_indices(cfg).l_c - 1
             gc = inp["gamma"][lc]
             xp = st.X_prev[:, lc].reshape(n, n)
             q = gc * (ops.apply_E(st.wx, st.wy, xp) - ops.apply_E(st.wx_prev, st.wy_prev, xp)).ravel()

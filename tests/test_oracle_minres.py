@@ -5,6 +5,8 @@ construction implies (K^T r = 0 after eq:xFinal, monotone LS residuals)."""
 import numpy as np
 import pytest
 import scipy.linalg
+
+from oracle.indices import of as _ixof
 import scipy.sparse.linalg as spla
 
 import rsk_synth as S
@@ -227,7 +229,7 @@ def test_principal_update_vnew_solves_eq_delta():
     wx1, wy1 = ops.irn_weights(st0.X[:, st0.lstar].reshape(n, n), cfg.tau)
     st = pipeline.StepState(1, wx1, wy1, st0.X, st0.G, st0.V_i1, wx0, wy0)
     V, _ = pipeline.principal_update(cfg, h, b, inp["gamma"], st)
-    lc = cfg.l_c - 1
+    lc = _ixof(cfg).l_c - 1
     g = inp["gamma"][lc]
     Ak = dense.assemble_shifted(h, wx1, wy1, g, n)
     E1 = dense.assemble_shifted(h, wx1, wy1, 1.0, n) - dense.assemble_shifted(h, wx1, wy1, 0.0, n)

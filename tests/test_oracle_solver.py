@@ -364,23 +364,3 @@ def test_pipeline_tiny_matches_dense_every_step():
         xstar = st.X[:, st.lstar].reshape(n, n)
         wx, wy = ops.irn_weights(xstar, cfg.tau)
 
-
-def test_ladder_base_subsamples_raw_block_and_still_solves():
-    """Reading G39: with ladder_base the k >= 1 raw block keeps every (M / base)-th
-    previous solution; the nested solve still meets every dense solution."""
-    import dataclasses
-    cfg = dataclasses.replace(S.small_config(n=8, M=8, r=1, sigma=0.8, n_c=8, J=2, K_out=2, tol=1e-10),
-                              ladder_base=4)
-    X = np.arange(5 * 8, dtype=float).reshape(5, 8)
-    sub = pipeline._raw_solutions(cfg, X)
-    np.testing.assert_array_equal(sub, X[:, ::2][:, :4])
-    inp = S.make_inputs(cfg)
-    out = pipeline.run(cfg, inp, keep_steps=True)
-    h = inp["psf"]; b = out["b"]; n = cfg.n
-    wx, wy = ops.identity_weights(n)
-    for st in out["steps"]:
-        for l in range(cfg.M):
-            Ad = dense.assemble_shifted(h, wx, wy, inp["gamma"][l], n)
-            xs = np.linalg.solve(Ad, b)
-            assert np.linalg.norm(st.X[:, l] - xs) <= max(2 * np.linalg.cond(Ad) * cfg.tol, 1e-12) * np.linalg.norm(xs)
-        wx, wy = ops.irn_weights(st.X[:, st.lstar].reshape(n, n), cfg.tau)
