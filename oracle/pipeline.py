@@ -83,18 +83,29 @@ class StepResult:
     anchor: rc.Anchor | None = None
 
 
-def outer_step(cfg, h, b, d, gamma, st: StepState, shifts=None) -> StepResult:
+_SHIFT_SOLVE = None
+
+
+def _run_shift(l):
+    """Pool trampoline (fork start method: the closure is inherited, never pickled)."""
+    return _SHIFT_SOLVE(l)
+
+
+def outer_step(cfg, h, b, d, gamma, st: StepState, shifts=None, workers: int = 1) -> StepResult:
     """One outer step (Alg. 5 body) under the readings listed above.
     `shifts` optionally restricts the CG solves to a subset of 0-based indices
-    (the others are left at zero) -- used for bounded-cost samples."""
+    (the others are left at zero) -- used for bounded-cost samples.
+    `workers` > 1 runs the per-shift solves (independent under reading D3) in that many
+    forked processes -- the only parallelism of the oracle (across shifts)."""
     n, M, N = cfg.n, cfg.M, cfg.N
     wx, wy = st.wx, st.wy
+    ix = _ix.of(cfg)
 
     def A_g(g):
         return lambda v: ops.apply_shifted(h, wx, wy, g, v.reshape(n, n)).ravel()
 
     overhead = 0
-    i1, i2 = _ix.of(cfg).i1 - 1, _ix.of(cfg).i2 - 1
+    i1, i2 = ix.i1 - 1, ix.i2 - 1
     V_i1 = st.V_i1
     if st.k == 0:
         n1 = math.ceil(2 * (cfg.n_c - 2) / 3)
@@ -112,7 +123,7 @@ def outer_step(cfg, h, b, d, gamma, st: StepState, shifts=None) -> StepResult:
     else:
         raw = np.column_stack([V_i1, st.X_prev])
     Ut = rc.stabilize(raw, cfg.n_c)
-    gstar = gamma[_ix.of(cfg).istar - 1]
+    gstar = gamma[ix.istar - 1]
     an = rc.anchor(h, wx, wy, Ut, b, gstar, n)
     overhead += Ut.shape[1]
     mode = getattr(cfg, "guess", "orth")
@@ -125,16 +136,16 @@ def outer_step(cfg, h, b, d, gamma, st: StepState, shifts=None) -> StepResult:
     elif mode == "oblique2":
         # eq:updates: anchors gamma_{I_L} (left group) and gamma_{I_R} (right group); the
         # images Z_A, Z_E are shared (no extra applies), only K, R differ (reading G34)
-        anL = an if _ix.of(cfg).I_L == _ix.of(cfg).istar else rc.anchor(h, wx, wy, Ut, b, gamma[_ix.of(cfg).I_L - 1], n)
-        anR = rc.anchor(h, wx, wy, Ut, b, gamma[_ix.of(cfg).I_R - 1], n)
+        anL = an if ix.I_L == ix.istar else rc.anchor(h, wx, wy, Ut, b, gamma[ix.I_L - 1], n)
+        anR = rc.anchor(h, wx, wy, Ut, b, gamma[ix.I_R - 1], n)
 
         def guess(l):
-            return rc.oblique_guess(anL if (l + 1) <= _ix.of(cfg).I else anR, gamma[l])
+            return rc.oblique_guess(anL if (l + 1) <= ix.I else anR, gamma[l])
     else:
         raise ValueError(f"unknown guess mode {mode!r}")
 
     groups = {}
-    for gname, jidx in (("L", _ix.of(cfg).J_L - 1), ("R", _ix.of(cfg).J_R - 1)):
+    for gname, jidx in (("L", ix.J_L - 1), ("R", ix.J_R - 1)):
         W, AW, EW, _, _ = rc.group_ritz(an, gamma[jidx], cfg.J)
         groups[gname] = (W, AW, EW)
 
@@ -142,22 +153,26 @@ def outer_step(cfg, h, b, d, gamma, st: StepState, shifts=None) -> StepResult:
     iters = np.zeros(M, dtype=np.int64); applies = np.zeros(M, dtype=np.int64)
     status = np.zeros(M, dtype=np.int64); relres = np.zeros(M); grel = np.zeros(M)
     nb = np.linalg.norm(b)
-    todo = range(M) if shifts is None else shifts
+    todo = list(range(M)) if shifts is None else list(shifts)
     seq = getattr(cfg, "local", "d3") == "seq"
-    for l in todo:
-        W, AW, EW = groups["L" if (l + 1) <= _ix.of(cfg).I else "R"]
+
+    def solve(l):
+        """Shift l: principal guess, local space [W_g, g-hat (, g^(k,l-1))], inner solve.
+        Returns (x, x_p, iters, applies, status, relres_true, guess relres, overhead)."""
+        W, AW, EW = groups["L" if (l + 1) <= ix.I else "R"]
         xp = guess(l)
         cols_U = [W]
         cols_Z = [AW + gamma[l] * EW]
         n_carry = 0
+        ov = 0
         if st.k >= 1 and st.G_prev is not None:
             gh = rc.carried_direction(W, st.G_prev[:, l])
             if gh is not None:
                 img = gh.reshape(n, n)
                 zg = (ops.apply_A(h, img) + gamma[l] * ops.apply_E(wx, wy, img)).ravel()
-                overhead += 1
+                ov += 1
                 cols_U.append(gh[:, None]); cols_Z.append(zg[:, None]); n_carry = 1
-        if seq and l >= 1 and _same_group(cfg, l - 1, l) and (shifts is None or (l - 1) in todo):
+        if seq and l >= 1 and _same_group(cfg, l - 1, l) and (l - 1) in todo:
             # Alg. 3 / Alg. 4 (P:703, P:745): U~_l = [W, g^(k-1,l), g^(k,l-1)], the second
             # correction orthogonalised against [W, g-hat] and dropped when nearly
             # redundant (footnote P:691; reading G35)
@@ -165,7 +180,7 @@ def outer_step(cfg, h, b, d, gamma, st: StepState, shifts=None) -> StepResult:
             if gh2 is not None:
                 img = gh2.reshape(n, n)
                 zg = (ops.apply_A(h, img) + gamma[l] * ops.apply_E(wx, wy, img)).ravel()
-                overhead += 1
+                ov += 1
                 cols_U.append(gh2[:, None]); cols_Z.append(zg[:, None]); n_carry += 1
         U = np.column_stack(cols_U); Z = np.column_stack(cols_Z)
         if getattr(cfg, "inner", "cg") == "minres":    # the paper's inner solver (f2(ii))
@@ -174,12 +189,30 @@ def outer_step(cfg, h, b, d, gamma, st: StepState, shifts=None) -> StepResult:
         else:
             res = dcg.defcg(A_g(gamma[l]), b, x_p=xp, U=U, Z=Z, tol=cfg.tol,
                             maxit=cfg.maxit, n_carry=n_carry)
-        X[:, l] = res.x
-        Xp[:, l] = 0.0 if xp is None else xp
-        G[:, l] = res.x - Xp[:, l]
-        iters[l] = res.iters; applies[l] = res.applies; status[l] = res.status
-        relres[l] = res.relres_true
-        grel[l] = (np.linalg.norm(b - A_g(gamma[l])(Xp[:, l])) / nb) if xp is not None else 1.0
+        xpv = np.zeros(N) if xp is None else xp
+        gr = (np.linalg.norm(b - A_g(gamma[l])(xpv)) / nb) if xp is not None else 1.0
+        return res.x, xpv, res.iters, res.applies, res.status, res.relres_true, gr, ov
+
+    def store(l, r):
+        nonlocal overhead
+        X[:, l], Xp[:, l] = r[0], r[1]
+        G[:, l] = r[0] - r[1]
+        iters[l], applies[l], status[l], relres[l], grel[l] = r[2], r[3], r[4], r[5], r[6]
+        overhead += r[7]
+
+    if workers > 1 and not seq and len(todo) > 1:
+        import multiprocessing as mp
+        global _SHIFT_SOLVE
+        _SHIFT_SOLVE = solve
+        try:
+            with mp.get_context("fork").Pool(min(workers, len(todo))) as pool:
+                for l, r in zip(todo, pool.map(_run_shift, todo, chunksize=1)):
+                    store(l, r)
+        finally:
+            _SHIFT_SOLVE = None
+    else:
+        for l in todo:
+            store(l, solve(l))
 
     rho = np.zeros(M); eta = np.zeros(M)
     for l in range(M):

@@ -514,6 +514,9 @@ class GpuSolver:
         reading G2), "irn_iso" (isotropic IRN) or "gazzola" (D_{k+1} =
         diag(1 - w.^p) D_k)."""
         rule = getattr(self.cfg, "weight_rule", "irn")
+        # W_k is kept for eq:delta (f3) BEFORE the rule overwrites self.wx / self.wy in
+        # place (from step 1 on they are the handle's current weights)
+        self.w_prev = (self.cur_w[0].clone(), self.cur_w[1].clone())
         if rule == "irn":
             self.h.irn_weights(xstar, self.cfg.tau, self.wx, self.wy, stream=self.stream)
         elif rule == "irn_iso":
@@ -523,7 +526,6 @@ class GpuSolver:
                                    stream=self.stream)
         else:
             raise ValueError(f"unknown weight rule {rule!r}")
-        self.w_prev = (self.cur_w[0].clone(), self.cur_w[1].clone())
         self.h.set_weights(self.wx, self.wy, stream=self.stream)
         self.cur_w = (self.wx, self.wy)
 

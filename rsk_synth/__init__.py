@@ -45,7 +45,7 @@ class Config:
     tol: float            # CG relative residual tolerance
     shapes: str           # phantom recipe key
     n_shapes: int
-    maxit: int = 20000
+    maxit: int = 100000        # reading G14: C4 at k >= 1 (tau = 1e-4) needs > 20000 at gamma = 100
     weight_rule: str = "irn"   # outer weight update: "irn" (north_star), "irn_iso", "gazzola" (f1)
     p: float = 2.0             # Gazzola exponent (never given by the paper; SPEC S:421 default)
     stop: str = "fixed"        # outer stopping: "fixed" (K_out steps) or "lstar3"

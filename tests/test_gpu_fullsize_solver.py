@@ -1,0 +1,183 @@
+"""Solver parity at BASELINE.json's full sizes, in the launch configurations the bench
+and the nested solve use (the oracle runs its per-shift solves in forked processes, one
+per host core -- its only parallelism, across shifts):
+
+* C4 (1024 x 1024, 15 x 15 PSF, all 128 shifts, two groups of |J| = 12, carried columns,
+  principal guesses): the persistent lockstep loop over the whole ladder for a fixed 30
+  iterations; eight sampled shifts (l = 1, 17, ..., 113, 128) are recomputed by the oracle
+  one by one and compared element by element (the iterates of 30 CG steps agree to
+  rounding: 1e-10 relative 2-norm) with the same apply accounting.
+* C2 (256 x 256, 32 shifts): outer steps k = 0 and k = 1 stepwise (reading G28: the
+  oracle's state after step 0 seeds the GPU's step 1), both sides at relres 1e-10:
+  n_c and l* equal, iterations +-2 on >= 95 % of the shifts and +-max(2, 1 %) on all,
+  solutions 1e-8 relative (north_star) -- a shift beyond 1e-8 must have a GPU solution
+  whose true residual, recomputed by the oracle, meets the tolerance (reading G27:
+  tolerance-limited), and at most 10 % of them may be.
+"""
+import dataclasses
+import multiprocessing as mp
+import os
+
+import numpy as np
+import pytest
+
+import rsk_synth as S
+from oracle import defcg as dcg
+from oracle import operators as ops
+from oracle import pipeline as opipe
+
+pytestmark = pytest.mark.gpu
+_CTX = {}
+WORKERS = max(1, min(16, os.cpu_count() or 1))
+
+
+def _t(torch, dev, a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
+
+
+def _pmap(fn, items):
+    with mp.get_context("fork").Pool(min(len(items), WORKERS)) as pool:
+        return pool.map(fn, items, chunksize=1)
+
+
+def _img_A(v):
+    n = _CTX["n"]
+    return ops.apply_A(_CTX["psf"], v.reshape(n, n)).ravel()
+
+
+def _img_E(v):
+    n = _CTX["n"]
+    return ops.apply_E(_CTX["wx"], _CTX["wy"], v.reshape(n, n)).ravel()
+
+
+def _img_shift(a):
+    v, g = a
+    n = _CTX["n"]
+    return ops.apply_shifted(_CTX["psf"], _CTX["wx"], _CTX["wy"], g, v.reshape(n, n)).ravel()
+
+
+def _c4_oracle(l):
+    c = _CTX
+    n, g = c["n"], c["gam"][l]
+    A = lambda v: ops.apply_shifted(c["psf"], c["wx"], c["wy"], g, v.reshape(n, n)).ravel()
+    grp = c["grp"][l]
+    U, Z = c["W"][grp], c["AW"][grp] + g * c["EW"][grp]
+    nc = 0
+    if l in c["gidx"]:
+        j = c["gidx"].index(l)
+        U = np.column_stack([U, c["gh"][:, j]]); Z = np.column_stack([Z, c["Zg"][:, j]]); nc = 1
+    xp = c["xp"][:, l] if c["has_xp"][l] else None
+    r = dcg.defcg(A, c["b"], x_p=xp, U=U, Z=Z, tol=c["tol"], maxit=c["maxit"], n_carry=nc)
+    return r.x, r.iters, r.applies, r.status
+
+
+@pytest.fixture(scope="module")
+def torch_dev():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA")
+    return torch, torch.device("cuda", 0)
+
+
+def test_c4_full_ladder_fixed_iterations(torch_dev):
+    torch, dev = torch_dev
+    from paper_2306_15049_b200.pipeline import GpuSolver
+    cfg = dataclasses.replace(S.CONFIGS["C4"], tol=1e-30, maxit=30)
+    inp = S.make_inputs(cfg)
+    n, N, M, J = cfg.n, cfg.N, cfg.M, cfg.J
+    psf, gam = inp["psf"], inp["gamma"]
+    wx, wy = S.random_weights(4104, n, 1.0, 1.0 / cfg.tau)     # IRN-shaped: up to 1/tau
+    rng = np.random.default_rng(4104)
+    Wall, _ = np.linalg.qr(rng.standard_normal((N, 2 * J)))
+    Ws = [Wall[:, :J], Wall[:, J:]]
+    _CTX.clear()
+    _CTX.update(n=n, psf=psf, wx=wx, wy=wy)
+    cols = [Wall[:, j] for j in range(2 * J)]
+    AWall = np.stack(_pmap(_img_A, cols), 1)
+    EWall = np.stack(_pmap(_img_E, cols), 1)
+    AWs, EWs = [AWall[:, :J], AWall[:, J:]], [EWall[:, :J], EWall[:, J:]]
+    nL = int(round(0.75 * M))
+    grp = np.array([0 if l < nL else 1 for l in range(M)], dtype=np.int32)
+    sample = [0, 16, 32, 48, 64, 80, 96, 112, 127]
+    gidx = sorted(set(sample[::2] + [5, 40, 100, 120]))         # shifts with a carried column
+    gh = rng.standard_normal((N, len(gidx)))
+    for j, l in enumerate(gidx):
+        W = Ws[grp[l]]
+        gh[:, j] -= W @ (W.T @ gh[:, j])
+        gh[:, j] /= np.linalg.norm(gh[:, j])
+    Zg = np.stack(_pmap(_img_shift, [(gh[:, j], gam[l]) for j, l in enumerate(gidx)]), 1)
+    has_xp = (np.arange(M) % 3 != 0).astype(np.int32)
+    xp = 0.01 * rng.standard_normal((N, M)) * has_xp
+
+    sol = GpuSolver(cfg, psf, gam, check_every=8)
+    sol.h.set_weights(_t(torch, dev, wx.ravel()), _t(torch, dev, wy.ravel()))
+    sol.set_data(_t(torch, dev, inp["x_true"]), _t(torch, dev, inp["xi"]))
+    b = sol.b.cpu().numpy()
+    ghf = np.zeros((M, N)); zgf = np.zeros((M, N)); hg = np.zeros(M, dtype=np.int32)
+    for j, l in enumerate(gidx):
+        ghf[l], zgf[l], hg[l] = gh[:, j], Zg[:, j], 1
+    groups = dict(W=[_t(torch, dev, W.T) for W in Ws], AW=[_t(torch, dev, A.T) for A in AWs],
+                  EW=[_t(torch, dev, E.T) for E in EWs], of_shift=grp)
+    X = _t(torch, dev, xp.T)
+    res = sol.cg(list(range(M)), X, has_xp, groups=groups, ghat=(_t(torch, dev, ghf), _t(torch, dev, zgf), hg))
+    assert int(res["prof"][7]) == 2, "the persistent lockstep loop must have run"
+    Xs = X[sample].cpu().numpy()
+    del X, groups, sol
+    torch.cuda.empty_cache()
+    _CTX.update(gam=gam, grp=grp, W=Ws, AW=AWs, EW=EWs, gidx=gidx, gh=gh, Zg=Zg, has_xp=has_xp, xp=xp,
+                b=b, tol=cfg.tol, maxit=cfg.maxit)
+    ref = _pmap(_c4_oracle, sample)
+    for i, l in enumerate(sample):
+        x, it, ap, st = ref[i]
+        assert int(res["iters"][l]) == it == cfg.maxit, (l, res["iters"][l], it)
+        assert int(res["applies"][l]) == ap, (l, res["applies"][l], ap)
+        assert int(res["status"][l]) == st, (l, res["status"][l], st)
+        rel = np.linalg.norm(Xs[i] - x) / np.linalg.norm(x)
+        assert rel <= 1e-10, (l, rel)
+
+
+def _c2_true_res(a):
+    v, g = a
+    return np.linalg.norm(_CTX["b"] - _img_shift((v, g))) / np.linalg.norm(_CTX["b"])
+
+
+def test_c2_stepwise_k0_k1(torch_dev):
+    torch, dev = torch_dev
+    from paper_2306_15049_b200.pipeline import GpuSolver
+    cfg = dataclasses.replace(S.CONFIGS["C2"], tol=1e-10)
+    inp = S.make_inputs(cfg)
+    n, M = cfg.n, cfg.M
+    h = inp["psf"]
+    d, b2 = ops.make_data(h, inp["x_true"], inp["xi"], cfg.noise)
+    b = b2.ravel()
+    wx, wy = ops.identity_weights(n)
+    st = opipe.StepState(0, wx, wy, None, None, None)
+    sol = GpuSolver(cfg, h, inp["gamma"], check_every=8)
+    sol.set_data(_t(torch, dev, inp["x_true"]), _t(torch, dev, inp["xi"]))
+    limited = 0
+    for k in range(2):
+        rs = opipe.outer_step(cfg, h, b, d, inp["gamma"], st, workers=WORKERS)
+        sol.h.set_weights(_t(torch, dev, st.wx.ravel()), _t(torch, dev, st.wy.ravel()))
+        dst = {}
+        if st.V_i1 is not None:
+            dst = {"V_i1": _t(torch, dev, st.V_i1.T), "X_prev": _t(torch, dev, st.X_prev.T),
+                   "G_prev": _t(torch, dev, st.G_prev.T)}
+        o, X = sol.outer_step(k, dst)
+        assert o.nc == rs.nc, (k, o.nc, rs.nc)
+        assert np.all(o.status == 0) and np.all(rs.status == 0), (o.status, rs.status)
+        assert o.lstar == rs.lstar, (k, o.lstar, rs.lstar)
+        d_it = np.abs(o.iters - rs.iters)
+        assert np.mean(d_it <= 2) >= 0.95 and np.all(d_it <= np.maximum(2, 0.01 * rs.iters)), (k, o.iters, rs.iters)
+        Xg = X["X_prev"].cpu().numpy()
+        rel = np.array([np.linalg.norm(Xg[l] - rs.X[:, l]) / np.linalg.norm(rs.X[:, l]) for l in range(M)])
+        bad = [l for l in range(M) if rel[l] > 1e-8]
+        if bad:
+            _CTX.clear(); _CTX.update(n=n, psf=h, wx=st.wx, wy=st.wy, b=b)
+            tr = _pmap(_c2_true_res, [(Xg[l], inp["gamma"][l]) for l in bad])
+            for l, t in zip(bad, tr):
+                assert t <= 1.01 * cfg.tol and rel[l] <= 1e-5, (k, l, rel[l], t)
+            limited += len(bad)
+        xstar = rs.X[:, rs.lstar].reshape(n, n)
+        nwx, nwy = ops.irn_weights(xstar, cfg.tau)
+        st = opipe.StepState(k + 1, nwx, nwy, rs.X, rs.G, rs.V_i1)
+    assert limited <= 0.1 * 2 * M, f"{limited} tolerance-limited solutions"

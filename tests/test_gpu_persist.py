@@ -1,0 +1,113 @@
+"""Parity of the persistent lockstep CG loop (the loop C3, C4 and C5 run) against the
+oracle's deflated CG (O4, oracle/defcg.py) on the code paths those configs exercise:
+passes of 32 shifts with all four 8-shift DMMA N-blocks (nb = 0..3), a group switch
+inside the sorted active list, |J| = 12, carried columns and principal guesses on some
+shifts, and a ragged row count (N not a multiple of the 256-row chunks).
+Bar (north_star): iterations +-2, solutions 1e-8 relative 2-norm, both at relres 1e-10."""
+import multiprocessing as mp
+
+import numpy as np
+import pytest
+
+import rsk_synth as S
+from oracle import defcg as dcg
+from oracle import operators as ops
+
+pytestmark = pytest.mark.gpu
+
+_CTX = {}
+
+
+def _t(torch, dev, a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
+
+
+def _oracle_shift(l):
+    c = _CTX
+    n = c["n"]
+    g = c["gam"][l]
+    A = lambda v: ops.apply_shifted(c["psf"], c["wx"], c["wy"], g, v.reshape(n, n)).ravel()
+    grp = c["grp"][l]
+    U, Z = c["W"][grp], c["AW"][grp] + g * c["EW"][grp]
+    nc = 0
+    if c["has_g"][l]:
+        U = np.column_stack([U, c["gh"][:, l]]); Z = np.column_stack([Z, c["Zg"][:, l]]); nc = 1
+    xp = c["xp"][:, l] if c["has_xp"][l] else None
+    r = dcg.defcg(A, c["b"], x_p=xp, U=U, Z=Z, tol=c["tol"], maxit=c["maxit"], n_carry=nc)
+    return r.x, r.iters, r.applies, r.status
+
+
+def _pool_map(fn, items):
+    with mp.get_context("fork").Pool(min(len(items), mp.cpu_count())) as pool:
+        return pool.map(fn, items, chunksize=1)
+
+
+@pytest.fixture(scope="module")
+def torch_dev():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA")
+    return torch, torch.device("cuda", 0)
+
+
+def _setup(torch, dev, cfg, nL, nR, J, seed, gam):
+    from paper_2306_15049_b200.pipeline import GpuSolver
+    inp = S.make_inputs(cfg)
+    n, N, M = cfg.n, cfg.N, nL + nR
+    psf = inp["psf"]
+    sol = GpuSolver(cfg, psf, gam, check_every=5)
+    wx, wy = S.random_weights(seed, n, 1.0, 100.0)
+    sol.h.set_weights(_t(torch, dev, wx.ravel()), _t(torch, dev, wy.ravel()))
+    sol.set_data(_t(torch, dev, inp["x_true"]), _t(torch, dev, inp["xi"]))
+    b = sol.b.cpu().numpy()
+    rng = np.random.default_rng(seed)
+    Ws, AWs, EWs = [], [], []
+    for g in range(2):
+        W, _ = np.linalg.qr(rng.standard_normal((N, J)))
+        Ws.append(W)
+        AWs.append(np.stack([ops.apply_A(psf, W[:, j].reshape(n, n)).ravel() for j in range(J)], 1))
+        EWs.append(np.stack([ops.apply_E(wx, wy, W[:, j].reshape(n, n)).ravel() for j in range(J)], 1))
+    grp = np.array([0] * nL + [1] * nR, dtype=np.int32)
+    gh = rng.standard_normal((N, M))
+    for l in range(M):
+        W = Ws[grp[l]]
+        gh[:, l] -= W @ (W.T @ gh[:, l])
+    gh /= np.linalg.norm(gh, axis=0)
+    Zg = np.stack([ops.apply_shifted(psf, wx, wy, gam[l], gh[:, l].reshape(n, n)).ravel() for l in range(M)], 1)
+    has_g = (np.arange(M) % 3 != 1).astype(np.int32)
+    has_xp = (np.arange(M) % 4 != 2).astype(np.int32)
+    xp = 0.05 * rng.standard_normal((N, M))
+    _CTX.clear()
+    _CTX.update(n=n, gam=gam, psf=psf, wx=wx, wy=wy, grp=grp, W=Ws, AW=AWs, EW=EWs, gh=gh, Zg=Zg,
+                has_g=has_g, has_xp=has_xp, xp=xp, b=b, tol=cfg.tol, maxit=cfg.maxit)
+    groups = dict(W=[_t(torch, dev, W.T) for W in Ws], AW=[_t(torch, dev, A.T) for A in AWs],
+                  EW=[_t(torch, dev, E.T) for E in EWs], of_shift=grp)
+    ghat = (_t(torch, dev, gh.T), _t(torch, dev, Zg.T), has_g)
+    X = _t(torch, dev, (xp * has_xp).T)
+    return sol, groups, ghat, X
+
+
+@pytest.mark.parametrize("n,r,nL,nR", [(112, 3, 44, 10), (100, 7, 40, 9)])
+def test_persistent_loop_multi_pass_two_groups(torch_dev, monkeypatch, n, r, nL, nR):
+    monkeypatch.setenv("RSK_CG_NOCLUSTER", "1")
+    torch, dev = torch_dev
+    import dataclasses
+    M = nL + nR
+    cfg = dataclasses.replace(S.small_config(n=n, M=M, r=r, sigma=1.0 + 0.3 * r, tol=1e-10), maxit=20000)
+    gam = np.logspace(-4, 1.5, M)
+    sol, groups, ghat, X = _setup(torch, dev, cfg, nL, nR, 12, 900 + n, gam)
+    G = torch.empty_like(X)
+    res = sol.cg(list(range(M)), X, _CTX["has_xp"], Gout=G, groups=groups, ghat=ghat)
+    assert int(res["prof"][7]) == 2, "the persistent lockstep loop must have run"
+    ref = _pool_map(_oracle_shift, list(range(M)))
+    its = np.array([r[1] for r in ref])
+    assert len(set(its.tolist())) > M // 3, "iteration counts should spread (active set shrinks pass by pass)"
+    Xh, Gh = X.cpu().numpy(), G.cpu().numpy()
+    for l in range(M):
+        x, it, ap, st = ref[l]
+        assert res["status"][l] == 0 and st == 0, (l, res["status"][l], st)
+        assert abs(int(res["iters"][l]) - it) <= 2, (l, res["iters"][l], it)
+        assert int(res["applies"][l]) - int(res["iters"][l]) == ap - it, l
+        assert np.linalg.norm(Xh[l] - x) <= 1e-8 * np.linalg.norm(x), l
+        g_ref = x - (_CTX["xp"][:, l] if _CTX["has_xp"][l] else 0.0)
+        assert np.linalg.norm(Gh[l] - g_ref) <= 1e-8 * np.linalg.norm(x), l
