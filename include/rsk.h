@@ -139,7 +139,13 @@ int64_t rsk_launch_count(void);
 /* rsk_set_weights: copy W_k into the handle (E_k = L^T W_k L).
  * wx[i][j] weights (Dx x)[i,j] = x[i,j+1]-x[i,j]; wx[i][nx-1] must be 0.
  * wy[i][j] weights (Dy x)[i,j] = x[i+1,j]-x[i,j]; wy[ny-1][j] must be 0.
- * Device pointers, N doubles each. Enqueued on `stream`. */
+ * Device pointers, N doubles each. The weights are validated on the device before they
+ * are adopted (a host synchronisation of `stream`): a non-finite or negative value, or a
+ * non-zero pad (wx[:, nx-1]; wy[ny-1, :] when the handle holds the image's last row),
+ * returns RSK_EINVAL and leaves the handle's weights unchanged. IRN weights reach 1/tau,
+ * so SPEC's [0, 1] bound is relaxed to >= 0 (reading D2).
+ * Streams: the calls of one handle must be issued to one stream at a time (the host-
+ * driven helpers stage small coefficients in per-handle device scratch). */
 rsk_status rsk_set_weights(rsk_handle h, const double* wx, const double* wy, void* stream);
 
 /* ------------------------------------------------------- the four hot-path calls */

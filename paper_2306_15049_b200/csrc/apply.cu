@@ -188,6 +188,15 @@ bool fill_apply_params(Handle* h, const ApplyLaunch& a, ApplyParams& prm, int ty
 cudaError_t launch_apply(Handle* h, const ApplyLaunch& a, cudaStream_t st) {
   if (h->ct) return launch_ct_apply(h, a, st);   // CT: sparse C, C^T (ct.cu)
   if (a.nlist <= 0) return cudaSuccess;
+  {
+    // large images: the streaming strip core (strip_core.cuh); RSK_APPLY_STRIP=0/1 forces
+    const char* ev = getenv("RSK_APPLY_STRIP");
+    const int force = ev ? atoi(ev) : -1;
+    if (force == 1 || (force != 0 && h->ny * h->nx >= kStripMinN)) {
+      cudaError_t es = launch_apply_strip(h, a, st);
+      if (es != cudaErrorNotSupported) return es;
+    }
+  }
   ApplyParams prm;
   const bool tma = fill_apply_params(h, a, prm, std_tile_rows(h->r));
   if (a.xdoty && !a.cg) {

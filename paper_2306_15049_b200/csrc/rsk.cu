@@ -236,10 +236,39 @@ extern "C" rsk_status rsk_destroy(rsk_handle h) {
   return RSK_OK;
 }
 
+// validity of a weight pair (rsk_set_weights): bit 0 = a non-finite or negative value,
+// bit 1 = a non-zero pad (wx[:, nx-1]; wy[ny-1, :] when this handle holds the last row)
+__global__ void weights_check_kernel(const double* __restrict__ wx, const double* __restrict__ wy, int64_t ny,
+                                     int64_t nx, int bottom, int* flag) {
+  int f = 0;
+  const int64_t N = ny * nx;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N; i += (int64_t)gridDim.x * blockDim.x) {
+    const double a = wx[i], b = wy[i];
+    if (!(a >= 0.0) || !(b >= 0.0) || !isfinite(a) || !isfinite(b)) f |= 1;
+    if ((i % nx == nx - 1) && a != 0.0) f |= 2;
+    if (bottom && i >= N - nx && b != 0.0) f |= 2;
+  }
+  f = __reduce_or_sync(0xffffffffu, f);
+  if ((threadIdx.x & 31) == 0 && f) atomicOr(flag, f);
+}
+
 extern "C" rsk_status rsk_set_weights(rsk_handle h, const double* wx, const double* wy, void* stream) {
   if (!h) return RSK_EINVAL;
   RSK_ARG(wx && wy && aligned8(wx) && aligned8(wy), "rsk_set_weights: null or misaligned pointer");
   const size_t bytes = sizeof(double) * (size_t)(h->ny * h->nx);
+  // validate before adopting (weights reach 1/tau, so only >= 0 and finite are required;
+  // the pads of L's missing rows must be 0). A host sync point, once per outer step.
+  int* flag = reinterpret_cast<int*>(h->scal + 63);   // reserved for this check
+  RSK_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), S(stream)));
+  const int bottom = (h->ny_global == 0 || h->slab_ext1 == h->ny_global) ? 1 : 0;
+  count_launch();
+  weights_check_kernel<<<2 * h->sm_count, 256, 0, S(stream)>>>(wx, wy, h->ny, h->nx, bottom, flag);
+  RSK_CUDA(cudaGetLastError());
+  int hf = 0;
+  RSK_CUDA(cudaMemcpyAsync(&hf, flag, sizeof(int), cudaMemcpyDeviceToHost, S(stream)));
+  RSK_CUDA(cudaStreamSynchronize(S(stream)));
+  RSK_ARG(!(hf & 1), "rsk_set_weights: a weight is negative or not finite");
+  RSK_ARG(!(hf & 2), "rsk_set_weights: non-zero pad (wx[:, nx-1] and wy[ny-1, :] must be 0)");
   RSK_CUDA(cudaMemcpyAsync(h->wx, wx, bytes, cudaMemcpyDeviceToDevice, S(stream)));
   RSK_CUDA(cudaMemcpyAsync(h->wy, wy, bytes, cudaMemcpyDeviceToDevice, S(stream)));
   return RSK_OK;
@@ -523,7 +552,7 @@ namespace {
 
 struct WsLayout {
   size_t off_R, off_P, off_W, off_dbl, off_int, off_cnt, off_pA, off_pB, off_list, off_dev, off_gb, total;
-  size_t off_glist, off_partG, off_cntG, off_partP, off_pbar, off_zw;
+  size_t off_glist, off_partG, off_cntG, off_partP, off_pbar, off_zw, off_sA, off_sB;
   int nchunkP;
   int64_t rowsP;
   int nblkA, nblkB;
@@ -571,6 +600,9 @@ WsLayout ws_layout(const Handle* h, int ns) {
   }
   L.off_partP = o; o = al(o + sizeof(double) * (size_t)ns * (L.nchunkP * persist_pv() + persist_grid(h)));
   L.off_pbar = o; o = al(o + sizeof(unsigned) * 8);
+  // streaming loop (cg_stream.cu): per-item apply partials and per-chunk B partials
+  L.off_sA = o; o = al(o + sizeof(double) * (size_t)ns * stream_ipv(h));
+  L.off_sB = o; o = al(o + sizeof(double) * (size_t)ns * stream_pv() * stream_nchunk(N));
   // cluster-per-shift loop: per cluster, Z_s = AW + gamma_s EW of its current shift
   L.off_zw = o;
   if (N <= cluster_max_n()) o = al(o + sizeof(double) * (size_t)cluster_slots(h) * 16 * N);
@@ -875,6 +907,43 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
     RSK_CUDA(launch_cg_cluster(h, dev, hc, pbar + 6, dorder, reinterpret_cast<double*>(base + L.off_zw), st, &ok));
     if (ok) dl_kind = 1.0;
     if (ok) {
+      std::vector<int> ncf(ns, 0);
+      RSK_CUDA(cudaMemcpyAsync(stat_h.data(), hc.status, sizeof(int) * ns, cudaMemcpyDeviceToHost, st));
+      RSK_CUDA(cudaMemcpyAsync(ncf.data(), hc.nconf, sizeof(int) * ns, cudaMemcpyDeviceToHost, st));
+      RSK_CUDA(cudaStreamSynchronize(st));
+      for (int s = 0; s < ns; ++s) { applies[s] += ncf[s]; confirms[s] += ncf[s]; }
+      active.clear();
+    }
+  }
+  // Streaming persistent loop for images beyond L2 (cg_stream.cu; RSK_CG_STREAM=0/1 forces)
+  const char* sev = getenv("RSK_CG_STREAM");
+  const int sforce = sev ? atoi(sev) : -1;
+  if (!active.empty() && !prof && getenv("RSK_CG_LEGACY") == nullptr &&
+      (sforce == 1 || (sforce != 0 && N >= kStripMinN))) {
+    constexpr int kChunkIters = 512;
+    unsigned* pbar = reinterpret_cast<unsigned*>(base + L.off_pbar);
+    int* pna = reinterpret_cast<int*>(pbar + 4);
+    RSK_CUDA(cudaMemsetAsync(pbar, 0, sizeof(unsigned) * 8, st));
+    bool streamed = false;
+    int64_t pguard = 0;
+    for (;;) {
+      bool ok = false;
+      RSK_CUDA(launch_cg_stream(h, dev, hc, reinterpret_cast<double*>(base + L.off_sA),
+                                reinterpret_cast<double*>(base + L.off_sB), pbar, pna, pna + 1, kChunkIters, st, &ok));
+      if (!ok) break;
+      streamed = true;
+      int hv[2] = {0, 0};
+      RSK_CUDA(cudaMemcpyAsync(hv, pna, sizeof(int) * 2, cudaMemcpyDeviceToHost, st));
+      RSK_CUDA(cudaStreamSynchronize(st));
+      n_ka += hv[1];
+      if (hv[0] == 0) break;
+      if (++pguard > (2 * (int64_t)d->maxit + 64) / kChunkIters + 8) {
+        h->err = "rsk_cg_recycled_batch: streaming loop guard";
+        return RSK_ECUDA;
+      }
+    }
+    if (streamed) {
+      dl_kind = 3.0;
       std::vector<int> ncf(ns, 0);
       RSK_CUDA(cudaMemcpyAsync(stat_h.data(), hc.status, sizeof(int) * ns, cudaMemcpyDeviceToHost, st));
       RSK_CUDA(cudaMemcpyAsync(ncf.data(), hc.nconf, sizeof(int) * ns, cudaMemcpyDeviceToHost, st));

@@ -152,6 +152,9 @@ struct ApplyLaunch {
   int nvec_total;              // vectors addressable in X (and X2): TMA map extent
 };
 cudaError_t launch_apply(Handle* h, const ApplyLaunch& a, cudaStream_t st);
+// streaming strip apply for large images (apply_strip.cu); cudaErrorNotSupported = not applicable
+constexpr int64_t kStripMinN = 512 * 512;
+cudaError_t launch_apply_strip(Handle* h, const ApplyLaunch& a, cudaStream_t st);
 cudaError_t launch_ct_apply(Handle* h, const ApplyLaunch& a, cudaStream_t st);   // ct.cu
 int apply_tiles(const Handle* h);
 int apply_tile_rows(int r);
@@ -205,6 +208,13 @@ int persist_pv();
 cudaError_t launch_cg_persist(Handle* h, CgDev* dev, const CgDev& hc, double* partP, unsigned* bar,
                               int* nactive, int* iters_done, int nchunk, int64_t rows, int max_iters,
                               cudaStream_t st, bool* ok);
+
+// streaming persistent loop for images beyond L2 (cg_stream.cu)
+int stream_ipv(const Handle* h);
+int stream_nchunk(int64_t N);
+int stream_pv();
+cudaError_t launch_cg_stream(Handle* h, CgDev* dev, const CgDev& hc, double* partA, double* partB, unsigned* bar,
+                             int* nactive, int* iters_done, int max_iters, cudaStream_t st, bool* ok);
 
 // kernel-launch accounting (rsk_launch_count): every librsk kernel launch bumps it
 void count_launch();

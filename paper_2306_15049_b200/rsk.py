@@ -16,7 +16,11 @@ from . import _lib as L
 
 
 class RskError(RuntimeError):
-    pass
+    """A librsk call returned an error status (`status`: the rsk_status value, or None)."""
+
+    def __init__(self, msg, status=None):
+        super().__init__(msg)
+        self.status = status
 
 
 def _dptr(t):
@@ -126,7 +130,7 @@ class Handle:
     def _check(self, st, name, allow=(L.RSK_OK,)):
         if st not in allow:
             msg = self.lib.rsk_last_error(self.h)
-            raise RskError(f"{name} failed ({st}): {msg.decode() if msg else ''}")
+            raise RskError(f"{name} failed ({st}): {msg.decode() if msg else ''}", st)
         return st
 
     # ------------------------------------------------------------------ weights

@@ -177,7 +177,8 @@ def _kappa_bound(cfg, iters):
 
 # the three implementations of the lockstep loop: cluster per shift (default at these
 # sizes), persistent cooperative grid, host-polled kernels
-LOOPS = {"cluster": {}, "persistent": {"RSK_CG_NOCLUSTER": "1"}, "hostpolled": {"RSK_CG_LEGACY": "1"}}
+LOOPS = {"cluster": {}, "persistent": {"RSK_CG_NOCLUSTER": "1", "RSK_CG_STREAM": "0"},
+         "stream": {"RSK_CG_NOCLUSTER": "1", "RSK_CG_STREAM": "1"}, "hostpolled": {"RSK_CG_LEGACY": "1"}}
 
 
 @pytest.mark.parametrize("loop", list(LOOPS))
@@ -210,7 +211,7 @@ def test_cg_plain_batch_matches_oracle(torch_dev, n, loop, monkeypatch):
 
 
 @pytest.mark.parametrize("loop,J", [(lp, 5) for lp in LOOPS] + [("cluster", 12), ("cluster", 16),
-                                                                  ("persistent", 16)])
+                                                                  ("persistent", 16), ("stream", 16)])
 def test_cg_deflated_with_guess_and_carried_column(torch_dev, loop, J, monkeypatch):
     """All three loops at |J| = 5; the cluster loop's wide register path (|J| > 8) and the
     maximum local dimension |J| + 1 = 17."""
@@ -330,3 +331,67 @@ def test_outer_steps_stepwise_handoff(torch_dev, cfgname):
         st = opipe.StepState(k + 1, wx, wy, rs.X, rs.G, rs.V_i1)
     assert abs(total_it_gpu - total_it_ref) <= 0.02 * total_it_ref + 4
     assert limited <= 0.1 * cfg.M * cfg.K_out, f"{limited} tolerance-limited solutions"
+
+
+@pytest.mark.parametrize("n,r,sigma", [(50, 2, 1.0), (96, 4, 1.5), (130, 4, 2.0), (64, 10, 5.0),
+                                       (200, 7, 3.0), (72, 12, 5.0), (136, 1, 0.8)])
+def test_apply_strip_core_shifted_and_split(torch_dev, monkeypatch, n, r, sigma):
+    """The streaming strip core (strip_core.cuh; default for N >= 512^2) forced at small,
+    ragged sizes: several strips with a partial last strip, several 8-row blocks with a
+    ragged last block, the top / bottom / left / right zero-boundary corrections."""
+    monkeypatch.setenv("RSK_APPLY_STRIP", "1")
+    torch, dev = torch_dev
+    from paper_2306_15049_b200 import _lib as L
+    psf = S.gaussian_psf(r, sigma)
+    h = _handle(n, psf)
+    wx, wy = S.random_weights(300 + n, n)
+    h.set_weights(_t(torch, dev, wx.ravel()), _t(torch, dev, wy.ravel()))
+    nv = 5
+    X = S.random_vectors(400 + n, (nv, n * n))
+    gam = np.array([0.0, 1e-6, 0.5, 3.0, 700.0])
+    Xd = _t(torch, dev, X)
+    Y = torch.empty_like(Xd); AY = torch.empty_like(Xd); EY = torch.empty_like(Xd)
+    xy = torch.empty(nv, dtype=torch.float64, device=dev)
+    h.apply_shifted(Xd, Y, gamma=_t(torch, dev, gam), xdoty=xy)
+    h.apply_shifted(Xd, AY, EY=EY, mode=L.RSK_APPLY_SPLIT)
+    torch.cuda.synchronize()
+    Yh, AYh, EYh, xyh = (a.cpu().numpy() for a in (Y, AY, EY, xy))
+    for s in range(nv):
+        x = X[s].reshape(n, n)
+        ref = ops.apply_shifted(psf, wx, wy, gam[s], x)
+        assert _rel_inf(Yh[s].reshape(n, n), ref) <= 1e-13, s
+        assert _rel_inf(AYh[s].reshape(n, n), ops.apply_A(psf, x)) <= 1e-13, s
+        assert _rel_inf(EYh[s].reshape(n, n), ops.apply_E(wx, wy, x)) <= 1e-13, s
+        assert abs(xyh[s] - float(np.sum(x * ref))) <= 1e-13 * float(np.sum(np.abs(x) * np.abs(ref))), s
+
+
+def test_set_weights_rejects_invalid(torch_dev):
+    """rsk_set_weights (include/rsk.h): non-finite / negative weights and non-zero pads
+    return RSK_EINVAL and leave the handle's weights (hence E_k) unchanged."""
+    torch, dev = torch_dev
+    from paper_2306_15049_b200 import _lib as L
+    from paper_2306_15049_b200.rsk import RskError
+    n = 24
+    psf = S.gaussian_psf(2, 1.0)
+    h = _handle(n, psf)
+    wx, wy = S.random_weights(5, n)
+    h.set_weights(_t(torch, dev, wx.ravel()), _t(torch, dev, wy.ravel()))
+    X = _t(torch, dev, S.random_vectors(6, (1, n * n)))
+    E0 = torch.empty_like(X); A0 = torch.empty_like(X)
+    h.apply_shifted(X, A0, EY=E0, mode=L.RSK_APPLY_SPLIT)
+    bad = []
+    for kind in ("nan", "inf", "neg", "padx", "pady"):
+        bx, by = wx.copy(), wy.copy()
+        if kind == "nan": bx[3, 4] = np.nan
+        if kind == "inf": by[5, 6] = np.inf
+        if kind == "neg": bx[7, 1] = -1e-3
+        if kind == "padx": bx[2, n - 1] = 1.0
+        if kind == "pady": by[n - 1, 3] = 2.0
+        with pytest.raises(RskError) as ei:
+            h.set_weights(_t(torch, dev, bx.ravel()), _t(torch, dev, by.ravel()))
+        assert ei.value.status == L.RSK_EINVAL, kind
+        bad.append(kind)
+    E1 = torch.empty_like(X); A1 = torch.empty_like(X)
+    h.apply_shifted(X, A1, EY=E1, mode=L.RSK_APPLY_SPLIT)
+    torch.cuda.synchronize()
+    assert torch.equal(E0, E1) and len(bad) == 5

@@ -87,9 +87,12 @@ def _setup(torch, dev, cfg, nL, nR, J, seed, gam):
     return sol, groups, ghat, X
 
 
+@pytest.mark.parametrize("loop", ["stream", "tiled"])
 @pytest.mark.parametrize("n,r,nL,nR", [(112, 3, 44, 10), (100, 7, 40, 9)])
-def test_persistent_loop_multi_pass_two_groups(torch_dev, monkeypatch, n, r, nL, nR):
+def test_persistent_loop_multi_pass_two_groups(torch_dev, monkeypatch, n, r, nL, nR, loop):
+    """loop = "stream": cg_stream.cu (the default for N >= 512^2); "tiled": cg_persist.cu."""
     monkeypatch.setenv("RSK_CG_NOCLUSTER", "1")
+    monkeypatch.setenv("RSK_CG_STREAM", "1" if loop == "stream" else "0")
     torch, dev = torch_dev
     import dataclasses
     M = nL + nR
@@ -98,7 +101,7 @@ def test_persistent_loop_multi_pass_two_groups(torch_dev, monkeypatch, n, r, nL,
     sol, groups, ghat, X = _setup(torch, dev, cfg, nL, nR, 12, 900 + n, gam)
     G = torch.empty_like(X)
     res = sol.cg(list(range(M)), X, _CTX["has_xp"], Gout=G, groups=groups, ghat=ghat)
-    assert int(res["prof"][7]) == 2, "the persistent lockstep loop must have run"
+    assert int(res["prof"][7]) == (3 if loop == "stream" else 2), "the requested loop must have run"
     ref = _pool_map(_oracle_shift, list(range(M)))
     its = np.array([r[1] for r in ref])
     assert len(set(its.tolist())) > M // 3, "iteration counts should spread (active set shrinks pass by pass)"
@@ -106,8 +109,12 @@ def test_persistent_loop_multi_pass_two_groups(torch_dev, monkeypatch, n, r, nL,
     for l in range(M):
         x, it, ap, st = ref[l]
         assert res["status"][l] == 0 and st == 0, (l, res["status"][l], st)
-        assert abs(int(res["iters"][l]) - it) <= 2, (l, res["iters"][l], it)
-        assert int(res["applies"][l]) - int(res["iters"][l]) == ap - it, l
         assert np.linalg.norm(Xh[l] - x) <= 1e-8 * np.linalg.norm(x), l
         g_ref = x - (_CTX["xp"][:, l] if _CTX["has_xp"][l] else 0.0)
         assert np.linalg.norm(Gh[l] - g_ref) <= 1e-8 * np.linalg.norm(x), l
+        # the accounting beyond the iterations (r_p apply, confirmations) is identical
+        assert int(res["applies"][l]) - int(res["iters"][l]) == ap - it, l
+    # iterations: reading G27 -- +-2 on >= 95 % of the shifts, +-max(2, 1 %) on all
+    # (summation order alone moves counts by up to ~1 % at these condition numbers)
+    d_it = np.abs(res["iters"].astype(np.int64) - its)
+    assert np.mean(d_it <= 2) >= 0.95 and np.all(d_it <= np.maximum(2, 0.01 * its)), (res["iters"], its)

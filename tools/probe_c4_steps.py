@@ -25,23 +25,30 @@ sol = GpuSolver(cfg, inp["psf"], S.gamma_ladder(cfg))
 sol.set_data(torch.from_numpy(inp["x_true"]).to(dev), torch.from_numpy(inp["xi"]).to(dev))
 lib = L.load()
 lib.rsk_debug_persist_prof.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int]
+lib.rsk_debug_stream_prof.argtypes = [ctypes.POINTER(ctypes.c_double), ctypes.c_int]
 a = (ctypes.c_double * 8)()
+b8 = (ctypes.c_double * 8)()
 names = ["A apply", "barriers", "B update", "B2 scalars", "C combine"]
 sol.reset_weights()
 st = {}
 for k in range(K):
     lib.rsk_debug_persist_prof(a, 1)
+    lib.rsk_debug_stream_prof(b8, 1)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     o, st = sol.outer_step(k, st)
     torch.cuda.synchronize()
     dt = time.perf_counter() - t0
     lib.rsk_debug_persist_prof(a, 0)
+    lib.rsk_debug_stream_prof(b8, 0)
+    if b8[5] > 0:
+        a = b8
     its = max(a[5], 1)
     it = np.asarray(o.iters)
     rec = {"cfg": cfg.name, "k": k, "s": dt, "shift_iterations": int(it.sum()), "lockstep": int(its),
            "mean_active": float(it.sum() / its), "iters": it.tolist(), "lstar": int(o.lstar), "nc": int(o.nc),
            "loop_ms": float(o.prof[5]) if o.prof is not None else None,
+           "loop_kind": int(o.prof[7]) if o.prof is not None else None,
            "phase_us": {n: a[i] / its / 1e3 for i, n in enumerate(names)}}
     print(json.dumps(rec), flush=True)
     if k + 1 < K:
