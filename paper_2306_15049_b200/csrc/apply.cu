@@ -102,6 +102,20 @@ bool make_map3(CUtensorMap* m, const double* base, int64_t nx, int64_t ny, int64
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 2-D map {inner, outer} with an explicit outer pitch (elements), box {bw, bh}
+bool make_map2s(CUtensorMap* m, const double* base, int64_t inner, int64_t outer, int64_t pitch, int bw, int bh) {
+  auto fn = encode_fn();
+  if (!fn || !base) return false;
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || (pitch & 1) || outer < 1) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)pitch * 8};
+  cuuint32_t box[2] = {(cuuint32_t)bw, (cuuint32_t)bh};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 bool make_map2(CUtensorMap* m, const double* base, int64_t nx, int64_t ny, int bw, int bh) {
   auto fn = encode_fn();
   if (!fn || !base) return false;

@@ -129,7 +129,7 @@ __device__ __forceinline__ double block_sum(double v, double* red) {
 // D(8x8) += A(8x4, row) * B(4x8, col) in fp64 on the tensor cores. Fragments (per lane,
 // g = lane / 4, q = lane % 4): a = A[g][q], b = B[q][g], d = {D[g][2q], D[g][2q+1]}.
 __device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
                : "+d"(d0), "+d"(d1)
                : "d"(a), "d"(b));
 }

@@ -20,8 +20,6 @@ __global__ void __launch_bounds__(kAT, kStripCtasPerSm)
   using Core = StripCore<R>;
   using C = StripCfg<R>;
   Core::init(smem, p);
-  double bx[C::KS], ay[C::KS];
-  Core::frags(p, bx, ay);
   StripRing ring{0u, 0u};
   const int ipv = p.nseg * p.nstrip;
   const int nitems = ipv * nvec;
@@ -32,7 +30,7 @@ __global__ void __launch_bounds__(kAT, kStripCtasPerSm)
     const int ss = it / nvec;
     const int strip = ss % p.nstrip, seg = ss / p.nstrip;
     const int s = list ? list[li] : li;
-    const double dot = Core::item(p, smem, ring, bx, ay, s, strip, seg, false);
+    const double dot = Core::item(p, smem, ring, s, strip, seg * p.seg_rows, min(p.ny, (seg + 1) * p.seg_rows), false);
     if (p.want_dot) {
       const double bs = block_sum(dot, smem + C::OFF_RED);
       if (threadIdx.x == 0) p.part[(int64_t)li * ipv + ss] = bs;

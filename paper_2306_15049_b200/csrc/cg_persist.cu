@@ -160,8 +160,7 @@ __device__ __forceinline__ int pass_end(const PList& L, int li0) {
 // geometry only (rows of a warp, then warps), independent of the other shifts in the pass.
 constexpr int kRW = 34;   // per (warp, shift) staging: za[16], ze[16], rho, zeta
 __device__ __noinline__ void phase_b(const PersistParams& P, const PList& L, double* smem, double* s_alpha,
-                                     const double* s_gam) {
-  CgDev* cg = P.cg;
+                                     const double* s_gam, CgDev* cg) {
   const int n = L.n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, q = lane & 3;
@@ -304,8 +303,7 @@ __device__ __noinline__ void phase_b(const PersistParams& P, const PList& L, dou
 // ---- phase B2: one CTA per shift. Warp w sums slots j = w, w + 8, ... over the chunks
 // (coalesced, fixed order); warp 0 then solves G mu = z with the Cholesky factor staged
 // in shared memory and updates the shift's scalars and status.
-__device__ __noinline__ void phase_b2(const PersistParams& P, const PList& L, double* smem) {
-  CgDev* cg = P.cg;
+__device__ __noinline__ void phase_b2(const PersistParams& P, const PList& L, double* smem, CgDev* cg) {
   const int n = L.n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* zs = smem;                  // [kPV]
@@ -406,8 +404,7 @@ __device__ __noinline__ void phase_b2(const PersistParams& P, const PList& L, do
 // (A = W rows, B = the shifts' mu from shared memory); lane (g, q) then finishes the
 // elements (row g, shifts 2q, 2q+1) of each N-block.
 __device__ __noinline__ void phase_c(const PersistParams& P, const PList& L, double* smem, const double* s_alpha,
-                                     int* s_new, double* s_beta, int* s_slot, double* s_rinv) {
-  CgDev* cg = P.cg;
+                                     int* s_new, double* s_beta, int* s_slot, double* s_rinv, CgDev* cg) {
   const int n = L.n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, q = lane & 3;
@@ -555,7 +552,12 @@ __global__ void __launch_bounds__(kAT, kApplyCtasPerSm) cg_persist_kernel(const 
   __shared__ int s_new[kPMaxShift], s_slot[kPMaxShift];
   __shared__ double s_pw[kPMaxShift];
 
-  CgDev* cg = P.cg;
+  // the loop state's pointers and sizes in shared memory: no global round trip per field
+  // access after the L1 invalidations of the grid barriers
+  __shared__ CgDev s_cg;
+  if (threadIdx.x == 0) s_cg = *P.cg;
+  __syncthreads();
+  CgDev* cg = &s_cg;
   const int ns = P.nshift;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t N = cg->N;
@@ -588,19 +590,19 @@ __global__ void __launch_bounds__(kAT, kApplyCtasPerSm) cg_persist_kernel(const 
     grid_sync(P.bar, gen);
     mark(1);
 
-    phase_b(P, L, smem, s_alpha, s_gam);
+    phase_b(P, L, smem, s_alpha, s_gam, cg);
     mark(2);
     grid_sync(P.bar, gen);
     mark(1);
 
-    phase_b2(P, L, smem);
+    phase_b2(P, L, smem, cg);
     mark(3);
     grid_sync(P.bar, gen);
     mark(1);
 
     PList& NL = lists[cur ^ 1];
     build_list(cg, ns, NL, tmp);   // statuses are stable until the next phase A
-    phase_c(P, L, smem, s_alpha, s_new, s_beta, s_slot, s_rinv);
+    phase_c(P, L, smem, s_alpha, s_new, s_beta, s_slot, s_rinv, cg);
     mark(4);
     grid_sync(P.bar, gen);
     mark(1);

@@ -26,6 +26,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "strip_core.cuh"
 
@@ -40,9 +41,15 @@ constexpr int kSVec = 4;            // vectors per shift in a stage
 constexpr int kSAcc = 34;           // per pass shift: zA[16], zE[16], rho, zeta
 
 __device__ unsigned long long g_sprof[8];   // per-phase ns (RSK_PERSIST_PROF), block 0's view
+__device__ unsigned long long g_sprof3[8];
+__device__ unsigned long long g_cta_t[1024][8];   // RSK_PERSIST_PROF: per-CTA phase ends of one iteration
+__device__ unsigned long long g_sprof2[8];  // block 0, warp 1: B wait ns, B steps, C wait ns, C steps, B step ns, C step ns
 
 struct alignas(64) StreamParams {
   StripParams sp;     // apply: mapX over P (ld N), mapX2 over the iterates X (ld ldx), Y = Wv
+  CUtensorMap mAW[RSK_MAX_GROUPS];   // 2-D {N, J} maps of the group blocks, box {kSP, J}
+  CUtensorMap mEW[RSK_MAX_GROUPS];
+  CUtensorMap mW[RSK_MAX_GROUPS];
   CgDev* cg;
   double* partA;      // [shift][ipv]
   double* partB;      // [shift][kSPV][nchunk]
@@ -50,10 +57,13 @@ struct alignas(64) StreamParams {
   int* nactive;
   int* iters_done;
   int nshift;
-  int nchunk;
+  int nchunk;         // partial slots per shift = the grid (one row range per CTA)
+  int64_t rpc;        // rows per CTA (multiple of kSRs)
+  int64_t cg_N;
   int ipv;            // apply items per vector (segments x strips)
   int max_iters;
   int prof;
+  int staged;         // 1: phases B / C through bulk-copy stages (experiment), 0: registers
 };
 
 // ---------------------------------------------------------------- small helpers
@@ -150,11 +160,12 @@ __device__ void s_build_list(const CgDev* cg, int ns, SList& L, int* tmp) {
   __syncthreads();
 }
 
-// passes: up to 32 consecutive entries of one group
+// passes: up to kSPass consecutive entries of one group
+constexpr int kSPass = 16;
 __device__ __forceinline__ int s_pass_end(const SList& L, int li0) {
   const int g = le_grp(L.e[li0]);
   int li1 = li0;
-  while (li1 < L.n && li1 < li0 + 32 && le_grp(L.e[li1]) == g) ++li1;
+  while (li1 < L.n && li1 < li0 + kSPass && le_grp(L.e[li1]) == g) ++li1;
   return li1;
 }
 __device__ __forceinline__ int s_npass(const SList& L) {
@@ -173,52 +184,144 @@ __device__ __forceinline__ int s_pass_start(const SList& L, int k) {
 // pass accumulators, cross-warp reduction and per-pass scalars (phases B, B2, C);
 // [SCRATCH, ...): the strip apply's persistent tail (corrections, mbarriers) + 2 stage
 // mbarriers -- never touched by another phase
-constexpr int kSPS = 8;   // per pass entry: beta, 1/|r|, slot, flags, alpha
+constexpr int kSPS = 8;        // per pass entry: beta, 1/|r|, slot, flags, alpha
+constexpr int kSRs = 64;       // rows per stage step
+constexpr int kSP = 68;        // staged pitch (rows + 4: 4 mod 8 doubles, conflict-free fragments)
+constexpr int kSNST = 3;       // stages
+constexpr int kSMaxPass = 24;  // passes per phase (<= 256 shifts / 16 + groups)
 template <int R>
 struct SCfg {
-  static constexpr int STAGE = kSB * kSVec * kSRows;      // doubles per stage
-  static constexpr int OFF_ST = 0;                        // 2 stages
-  static constexpr int OFF_ACC = OFF_ST + 2 * STAGE;      // [32][kSAcc]
-  static constexpr int OFF_RED = OFF_ACC + 32 * kSAcc;    // [8 warps][4 acc][64]
-  static constexpr int OFF_PS = OFF_RED + 8 * 4 * 64;     // [32][kSPS]
+  // stage: group tiles [2][16][kSP] (phase B: AW, EW; phase C: W) + shift part
+  // [8][4][kSP] (B: w, r, zg; C: p, r, x, ghat)
+  static constexpr int OFF_SG = 0;
+  static constexpr int OFF_SS = 2 * 16 * kSP;
+  static constexpr int STAGE = OFF_SS + kSB * 3 * kSP;   // B: AW, EW tiles + 8 x (w, r, zg);
+  // C: the W tile + 8 x (p, r, x, ghat) = 16 kSP + 32 kSP <= STAGE
+  static_assert(16 * kSP + kSB * kSVec * kSP <= OFF_SS + kSB * 3 * kSP, "phase C stage");
+  static constexpr int OFF_ST = 0;                            // kSNST stages
+  static constexpr int OFF_RED = OFF_ST + kSNST * STAGE;      // [8 warps][64] D tile partials
+  static constexpr int OFF_PS = OFF_RED + 8 * 64;             // [32][kSPS] (B: rho / zeta partials)
   static constexpr int BC_END = OFF_PS + 32 * kSPS;
   static constexpr int RING_END = StripCfg<R>::RING_END;
   static constexpr int SCRATCH = al16(BC_END > RING_END ? BC_END : RING_END);
   using Strip = StripCfg<R, SCRATCH>;
-  static constexpr int OFF_BAR = Strip::DBL;              // 2 stage mbarriers
-  static constexpr int DBL = OFF_BAR + 2;
+  static constexpr int OFF_BAR = Strip::DBL;                  // kSNST stage mbarriers
+  static constexpr int DBL = OFF_BAR + kSNST;
   static constexpr size_t SMEM = sizeof(double) * (size_t)DBL;
 };
 
+// A unit is (1024-row chunk, pass of <= 32 shifts of one group); its steps are
+// (64-row sub-chunk, batch of <= 8 shifts), batches innermost (the group tile of a
+// sub-chunk is re-read from L2 by the later batches).
+struct SStep {
+  int u, k;
+};
+struct SGeo {
+  int c, pk, li0, li1, nb, nsub, nsteps;
+  int64_t cbeg, cend;
+};
+// unit = pass pk of this CTA's row range [c * rpc, min(N, (c + 1) * rpc)): the rows are
+// split evenly over the CTAs (multiples of 64), so every CTA moves the same bytes
+__device__ __forceinline__ SGeo s_geo(const int* pst, int64_t rpc, int64_t N, int pk) {
+  SGeo G;
+  G.c = blockIdx.x;
+  G.pk = pk;
+  G.li0 = pst[pk];
+  G.li1 = pst[pk + 1];
+  G.nb = (G.li1 - G.li0 + kSB - 1) / kSB;
+  G.cbeg = (int64_t)G.c * rpc;
+  G.cend = imin64(N, G.cbeg + rpc);
+  const int64_t rows = G.cend > G.cbeg ? G.cend - G.cbeg : 0;
+  G.nsub = (int)((rows + kSRs - 1) / kSRs);
+  G.nsteps = G.nsub * G.nb;
+  return G;
+}
+// pass boundaries of the list (pst[0..npass]), computed by every CTA identically
+__device__ __forceinline__ int s_passes(const SList& L, int* pst) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int np = 0, li = 0;
+    pst[0] = 0;
+    while (li < L.n) {
+      li = s_pass_end(L, li);
+      pst[++np] = li;
+    }
+    pst[kSMaxPass] = np;
+  }
+  __syncthreads();
+  return pst[kSMaxPass];
+}
+
 // ---------------------------------------------------------------- phase A
+// The 8-row output blocks of all (active shift, strip) columns are split evenly over the
+// CTAs: CTA k owns blocks [k B / G, (k+1) B / G) of the sequence (list entry, strip,
+// block), B = n x nstrip x ceil(ny / 8); it runs them as strip items (one per strip its
+// range touches) and writes one X.Y partial per (shift, CTA). Balanced to one item
+// prologue (LAG blocks) whatever the number of active shifts.
+__device__ __forceinline__ int64_t s_nblk(const StripParams& sp) { return (sp.ny + 7) / 8; }
+// CTAs whose block range touches list entry li: [k0, k1]
+__device__ __forceinline__ void s_cta_span(const StripParams& sp, int n, int li, int G, int& k0, int& k1) {
+  const int64_t per = (int64_t)sp.nstrip * s_nblk(sp);
+  const int64_t B = per * n;
+  const int64_t b0 = per * li, b1 = per * (li + 1) - 1;
+  k0 = (int)((b0 * G) / B);
+  k1 = (int)((b1 * G) / B);
+  // k owns [ceil(k B / G), ceil((k+1) B / G)): adjust for the rounding of the start
+  while (k0 > 0 && ((int64_t)k0 * B + G - 1) / G > b0) --k0;
+  while (((int64_t)(k0 + 1) * B + G - 1) / G <= b0) ++k0;
+  while (k1 < G - 1 && ((int64_t)(k1 + 1) * B + G - 1) / G <= b1) ++k1;
+}
+
 template <int R>
-__device__ __forceinline__ void s_phase_a(const StreamParams& P, const SList& L, double* smem, StripRing& ring,
-                                          const double* bx, const double* ay) {
+__device__ __forceinline__ void s_phase_a(const StreamParams& P, const SList& L, double* smem, StripRing& ring) {
   using Core = StripCore<R, SCfg<R>::SCRATCH>;
+  const StripParams& sp = P.sp;
   const int n = L.n;
-  const int nitems = n * P.ipv;
-  CgDev* cg = P.cg;
-  for (int it = blockIdx.x; it < nitems; it += gridDim.x) {
-    const int li = it % n, ss = it / n;
+  const int G = gridDim.x;
+  const int64_t nbk = s_nblk(sp);
+  const int64_t per = (int64_t)sp.nstrip * nbk;
+  const int64_t B = per * n;
+  const int k = blockIdx.x;
+  int64_t b = ((int64_t)k * B + G - 1) / G;
+  const int64_t bend = ((int64_t)(k + 1) * B + G - 1) / G;
+  int cur_li = -1;
+  double acc = 0.0;
+  if (b == bend && b < B && threadIdx.x == 0) {   // empty range inside an entry's span
+    const int li = (int)(b / per);
+    if (le_mode(L.e[li]) != ST_RCONV) P.partA[(size_t)le_sid(L.e[li]) * P.ipv + k] = 0.0;
+  }
+  while (b < bend) {
+    const int li = (int)(b / per);
+    const int64_t rem = b - (int64_t)li * per;
+    const int strip = (int)(rem / nbk);
+    const int blk = (int)(rem - (int64_t)strip * nbk);
+    const int64_t e = imin64(bend, (int64_t)li * per + (int64_t)(strip + 1) * nbk);
+    const int blk1 = (int)(e - (int64_t)li * per - (int64_t)strip * nbk);
     const int v = L.e[li];
     const int s = le_sid(v);
     const bool rconv = le_mode(v) == ST_RCONV;
-    const int strip = ss % P.sp.nstrip, seg = ss / P.sp.nstrip;
-    const double dot = Core::item(P.sp, smem, ring, bx, ay, s, strip, seg, rconv);
+    if (li != cur_li) {
+      if (cur_li >= 0 && le_mode(L.e[cur_li]) != ST_RCONV && threadIdx.x == 0)
+        P.partA[(size_t)le_sid(L.e[cur_li]) * P.ipv + k] = acc;
+      cur_li = li;
+      acc = 0.0;
+    }
+    const double dot = Core::item(sp, smem, ring, s, strip, 8 * blk, (int)imin64(sp.ny, 8 * (int64_t)blk1), rconv);
     if (!rconv) {
       const double bs = block_sum(dot, smem + SCfg<R>::Strip::OFF_RED);
-      if (threadIdx.x == 0) P.partA[(size_t)s * P.ipv + ss] = bs;
+      acc += bs;   // thread 0: the CTA's items of this shift in order
     }
+    b = e;
   }
-  (void)cg;
+  if (cur_li >= 0 && le_mode(L.e[cur_li]) != ST_RCONV && threadIdx.x == 0)
+    P.partA[(size_t)le_sid(L.e[cur_li]) * P.ipv + k] = acc;
 }
 
 // ---------------------------------------------------------------- phase B
-// stage layout: [8 shifts][w | r | zg | -][128]
 template <int R>
-__device__ void s_phase_b(const StreamParams& P, const SList& L, double* smem, double* s_alpha, unsigned& bpar) {
+__device__ void s_phase_b(const StreamParams& P, const SList& L, double* smem, double* s_alpha, unsigned& bpar,
+                          int* pst, CgDev* cg) {
   using SC = SCfg<R>;
-  CgDev* cg = P.cg;
   const int n = L.n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, q = lane & 3;
@@ -230,8 +333,10 @@ __device__ void s_phase_b(const StreamParams& P, const SList& L, double* smem, d
     if (le_mode(v) == ST_ACTIVE) {
       const int s = le_sid(v);
       const double* pa = P.partA + (size_t)s * P.ipv;
+      int k0, k1;
+      s_cta_span(P.sp, n, li, gridDim.x, k0, k1);
       double pi = 0.0;
-      for (int c = lane; c < P.ipv; c += 32) pi += __ldcg(pa + c);
+      for (int c = k0 + lane; c <= k1; c += 32) pi += __ldcg(pa + c);
       pi = warp_sum(pi);
       if (!(pi > 0.0) || !isfinite(pi)) {
         if (blockIdx.x == 0 && lane == 0) { cg->status[s] = ST_BREAKDOWN; cg->alpha[s] = 0.0; }
@@ -242,191 +347,519 @@ __device__ void s_phase_b(const StreamParams& P, const SList& L, double* smem, d
     }
     if (lane == 0) s_alpha[li] = a;
   }
-  __syncthreads();
-  double* ST = smem + SC::OFF_ST;
-  double* ACC = smem + SC::OFF_ACC;
+  const int npass = s_passes(L, pst);   // (syncs: s_alpha visible)
   double* RED = smem + SC::OFF_RED;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SC::OFF_BAR);
-  const int npass = s_npass(L);
-  const int nunits = P.nchunk * npass;
-  for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-    const int c = u % P.nchunk, pk = u / P.nchunk;
-    const int li0 = s_pass_start(L, pk), li1 = s_pass_end(L, li0);
+  const int nunits = npass;
+  if ((int64_t)blockIdx.x * P.rpc >= N) {   // no rows for this CTA: zero partials
+    for (int e = tid; e < n * kSPV; e += blockDim.x) {
+      const int k = e / kSPV, j = e - k * kSPV;
+      P.partB[((size_t)le_sid(L.e[k]) * kSPV + j) * P.nchunk + blockIdx.x] = 0.0;
+    }
+    return;
+  }
+  // producer = warp 0, one lane per shift slot of the batch (+ lane 31: the group tiles)
+  auto issue = [&](SStep st, unsigned q2) {
+    const SGeo G = s_geo(pst, P.rpc, N, st.u);
+    const int sub = st.k / G.nb, b = st.k % G.nb;
+    const int64_t r0 = G.cbeg + (int64_t)sub * kSRs;
+    const int nr = (int)imin64(kSRs, G.cend - r0);
+    const unsigned bytes = 8u * nr;
+    const int grp = le_grp(L.e[G.li0]);
+    const int J = cg->grp.J[grp];
+    const int slot = q2 % kSNST;
+    double* stg = smem + SC::OFF_ST + slot * SC::STAGE;
+    uint64_t* bar = bars + slot;
+    const int li = G.li0 + b * kSB + lane;
+    const bool mine = lane < kSB && li < G.li1;
+    const int v = mine ? L.e[li] : 0;
+    unsigned my = mine ? 2 * bytes + (le_hg(v) ? bytes : 0) : 0u;
+    if (lane == 31 && J > 0) my += 2u * 8u * kSP * J;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) my += __shfl_xor_sync(0xffffffffu, my, o);
+    unsigned long long tq0 = 0, tq1 = 0, tq2 = 0;
+    if (P.prof && blockIdx.x == 0 && (lane == 0 || lane == 31)) tq0 = s_timer();
+    if (lane == 0) mbar_expect_tx(bar, my);
+    __syncwarp();
+    if (mine) {
+      const int s = le_sid(v);
+      double* d = stg + SC::OFF_SS + lane * 3 * kSP;
+      bulk_load(d, cg->Wv + (int64_t)s * N + r0, bytes, bar);
+      bulk_load(d + kSP, cg->R + (int64_t)s * N + r0, bytes, bar);
+      if (le_hg(v)) bulk_load(d + 2 * kSP, cg->ZGhat + (int64_t)s * cg->ldgh + r0, bytes, bar);
+    }
+    if (P.prof && blockIdx.x == 0 && lane == 0) { tq1 = s_timer(); atomicAdd(&g_sprof3[0], tq1 - tq0); }
+    if (lane == 31 && J > 0) {
+      tma_load_2d(stg + SC::OFF_SG, &P.mAW[grp], bar, (int)r0, 0);
+      tma_load_2d(stg + SC::OFF_SG + 16 * kSP, &P.mEW[grp], bar, (int)r0, 0);
+    }
+    if (P.prof && blockIdx.x == 0 && lane == 31) { tq2 = s_timer(); atomicAdd(&g_sprof3[1], tq2 - tq0); }
+  };
+  auto advance = [&](SStep& st) {
+    const SGeo G = s_geo(pst, P.rpc, N, st.u);
+    if (++st.k >= G.nsteps) { st.k = 0; st.u += 1; }
+  };
+  SStep cons{0, 0}, prod = cons;
+  unsigned qn = 0, qp = 0;
+  unsigned long long s_tstep = 0;
+  if (warp == 0)
+    for (int i = 0; i < kSNST - 1 && prod.u < nunits; ++i) { issue(prod, qp++); advance(prod); }
+  // per-unit accumulators: D tile partial of this warp per batch; rho / zeta per thread
+  const int wt = warp & 3, wh = warp >> 2;      // DMMA tile (mb = wt >> 1, isE = wt & 1), k half
+  double dacc[4][2];
+  double* RR = smem + SC::OFF_PS;   // [32 pass shifts][2 warps][2]: rho, zeta partials
+  while (cons.u < nunits) {
+    const SGeo G = s_geo(pst, P.rpc, N, cons.u);
+    const int np = G.li1 - G.li0;
+    if (cons.k == 0) {
+#pragma unroll
+      for (int b = 0; b < 4; ++b) dacc[b][0] = dacc[b][1] = 0.0;
+      for (int e = tid; e < 32 * 4; e += blockDim.x) RR[e] = 0.0;
+      __syncthreads();
+    }
+    if (warp == 0 && prod.u < nunits) {
+      unsigned long long ti0 = 0;
+      if (P.prof && blockIdx.x == 0 && tid == 0) ti0 = s_timer();
+      issue(prod, qp++);
+      advance(prod);
+      if (P.prof && blockIdx.x == 0 && tid == 0) g_sprof2[6] += s_timer() - ti0;
+    }
+    const int sub = cons.k / G.nb, b = cons.k % G.nb;
+    const int64_t r0 = G.cbeg + (int64_t)sub * kSRs;
+    const int nr = (int)imin64(kSRs, G.cend - r0);
+    const int grp = le_grp(L.e[G.li0]);
+    const int J = cg->grp.J[grp];
+    const int slot = qn % kSNST;
+    double* stg = smem + SC::OFF_ST + slot * SC::STAGE;
+    unsigned long long tw0 = 0;
+    if (P.prof && blockIdx.x == 0 && tid == 32) tw0 = s_timer();
+    mbar_wait(bars + slot, (bpar >> slot) & 1u);
+    if (P.prof && blockIdx.x == 0 && tid == 32) {
+      const unsigned long long t1 = s_timer();
+      g_sprof2[0] += t1 - tw0; g_sprof2[1] += 1;
+      if (s_tstep) g_sprof2[4] += t1 - s_tstep;
+      s_tstep = t1;
+    }
+    bpar ^= 1u << slot;
+    // (a) r update: element e = (shift e >> 6, row e & 63), two per thread; rho, zeta
+    // per warp (32 consecutive rows of one shift) added in step order (fixed)
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      const int e = tid + 256 * i;
+      const int k8 = e >> 6, row = e & 63;
+      const int li = G.li0 + b * kSB + k8;
+      double* d = stg + SC::OFF_SS + k8 * 3 * kSP;
+      double rn = 0.0, rh = 0.0, zt = 0.0;
+      const bool live = li < G.li1;
+      if (live && row < nr) {
+        const int v = L.e[li];
+        const int s = le_sid(v);
+        const double wv = d[row];
+        rn = (le_mode(v) == ST_ACTIVE) ? fma(-s_alpha[li], wv, d[kSP + row]) : __ldg(cg->b + r0 + row) - wv;
+        cg->R[(int64_t)s * N + r0 + row] = rn;
+        rh = rn * rn;
+        if (le_hg(v)) zt = d[2 * kSP + row] * rn;
+      }
+      d[kSP + row] = rn;
+      rh = warp_sum(rh);
+      zt = warp_sum(zt);
+      if (lane == 0 && live) {
+        double* a = RR + ((li - G.li0) * 2 + (warp & 1)) * 2;
+        a[0] += rh;
+        a[1] += zt;
+      }
+    }
+    __syncthreads();
+    if (P.prof && blockIdx.x == 0 && tid == 32) g_sprof2[7] += s_timer() - s_tstep;   // wait end -> after (a) sync
+    // (b) D[j][shift] += [AW | EW]^T R': warp = (tile wt, k half wh), 8 k-steps of 4 rows
+    {
+      const int mb = wt >> 1, isE = wt & 1;
+      if (!(mb == 1 && J <= 8)) {
+        const double* gt = stg + SC::OFF_SG + isE * 16 * kSP + (8 * mb + g) * kSP;
+        const double* rr = stg + SC::OFF_SS + g * 3 * kSP + kSP;
+        const bool colv = (8 * mb + g) < J;
+        double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const int row = (wh * 8 + kk) * 4 + q;
+          dmma(d0, d1, colv ? gt[row] : 0.0, rr[row]);
+        }
+#pragma unroll
+        for (int bb = 0; bb < 4; ++bb)
+          if (bb == b) { dacc[bb][0] += d0; dacc[bb][1] += d1; }
+      }
+    }
+    __syncthreads();   // stage released
+    if (cons.k + 1 == G.nsteps) {
+      // unit end: chunk partials of the pass's shifts
+      for (int bb = 0; bb < G.nb; ++bb) {
+        // D tile partials of batch bb: warp (tile wt, half wh) -> RED[warp][m * 8 + n]
+#pragma unroll
+        for (int b2 = 0; b2 < 4; ++b2)
+          if (b2 == bb) {
+            RED[warp * 64 + g * 8 + 2 * q] = dacc[b2][0];
+            RED[warp * 64 + g * 8 + 2 * q + 1] = dacc[b2][1];
+          }
+        __syncthreads();
+        const int kb = min(kSB, np - bb * kSB);
+        for (int e = tid; e < kb * kSPV; e += blockDim.x) {
+          const int k8 = e / kSPV, j = e - k8 * kSPV;
+          const int v = L.e[G.li0 + bb * kSB + k8];
+          const int s = le_sid(v);
+          const int nw = le_m(v) - le_hg(v);
+          const double* rr2 = RR + (bb * kSB + k8) * 4;   // [2 warps][rho, zeta]
+          double val;
+          if (j < nw) {
+            const int mb = j >> 3, m = j & 7;
+            // tile (mb, A) = warps 2 mb and 2 mb + 4; tile (mb, E) = warps 2 mb + 1, 2 mb + 5
+            const double za = RED[(2 * mb) * 64 + m * 8 + k8] + RED[(2 * mb + 4) * 64 + m * 8 + k8];
+            const double ze = RED[(2 * mb + 1) * 64 + m * 8 + k8] + RED[(2 * mb + 5) * 64 + m * 8 + k8];
+            val = fma(cg->gam[s], ze, za);
+          } else if (le_hg(v) && j == nw) {
+            val = rr2[1] + rr2[3];
+          } else if (j == kMaxM) {
+            val = rr2[0] + rr2[2];
+          } else {
+            continue;
+          }
+          P.partB[((size_t)s * kSPV + j) * P.nchunk + G.c] = val;
+        }
+        __syncthreads();
+      }
+    }
+    advance(cons);
+    ++qn;
+  }
+}
+
+// ---------------------------------------------------------------- phase B (register form)
+// The per-shift vectors stream through registers: lane (g, q) updates r of (row q of a
+// 4-row k-step, shift 8 nb + g) -- exactly its DMMA B fragment -- and loads the A
+// fragments (group columns 8 mb + g, row q) of AW / EW, shared by the four 8-shift N
+// blocks of a pass of <= 32 shifts. Every load of a group of k-steps is issued before
+// the arithmetic that consumes it. Partials per (shift, CTA row range), fixed order.
+constexpr int kRW = 34;   // per (warp, shift) staging: zA[16], zE[16], rho, zeta
+template <int R>
+__device__ void s_phase_b_reg(const StreamParams& P, const SList& L, double* smem, double* s_alpha, int* pst,
+                              CgDev* cg) {
+  const int n = L.n;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int64_t N = cg->N;
+  for (int li = warp; li < n; li += 8) {
+    const int v = L.e[li];
+    double a = 0.0;
+    if (le_mode(v) == ST_ACTIVE) {
+      const int s = le_sid(v);
+      const double* pa = P.partA + (size_t)s * P.ipv;
+      int k0, k1;
+      s_cta_span(P.sp, n, li, gridDim.x, k0, k1);
+      double pi = 0.0;
+      for (int c = k0 + lane; c <= k1; c += 32) pi += __ldcg(pa + c);
+      pi = warp_sum(pi);
+      if (!(pi > 0.0) || !isfinite(pi)) {
+        if (blockIdx.x == 0 && lane == 0) { cg->status[s] = ST_BREAKDOWN; cg->alpha[s] = 0.0; }
+      } else {
+        a = cg->rho[s] / pi;
+        if (blockIdx.x == 0 && lane == 0) cg->alpha[s] = a;
+      }
+    }
+    if (lane == 0) s_alpha[li] = a;
+  }
+  const int npass = s_passes(L, pst);
+  const int64_t cbeg = (int64_t)blockIdx.x * P.rpc;
+  const int64_t cend = imin64(N, cbeg + P.rpc);
+  double* red = smem;   // [8 warps][32][kRW]
+  const int64_t rpw = P.rpc / 8;   // rows per warp (multiple of 8)
+  const int64_t wbeg = cbeg + warp * rpw;
+  const int64_t wend = imin64(cend, wbeg + rpw);
+  for (int pk = 0; pk < npass; ++pk) {
+    const int li0 = pst[pk], li1 = pst[pk + 1];
     const int np = li1 - li0;
     const int grp = le_grp(L.e[li0]);
     const int J = cg->grp.J[grp];
     const double* AWg = cg->grp.AW[grp];
     const double* EWg = cg->grp.EW[grp];
     const int64_t ldw = cg->grp.ldw;
-    const int64_t cbeg = (int64_t)c * kSChunk;
-    const int nsub = (int)((imin64(N, cbeg + kSChunk) - cbeg + kSRows - 1) / kSRows);
-    const int nb = (np + kSB - 1) / kSB;
-    const int nsteps = nsub * nb;
-    for (int e = tid; e < np * kSAcc; e += blockDim.x) ACC[e] = 0.0;
-    // stage issue: step k = (sub k / nb, batch k % nb)
-    auto issue = [&](int k) {
-      const int sub = k / nb, b = k % nb;
-      const int64_t r0 = cbeg + (int64_t)sub * kSRows;
-      const int nr = (int)imin64(kSRows, N - r0);
-      const unsigned bytes = 8u * nr;
-      double* stg = ST + (k & 1) * SC::STAGE;
-      unsigned tot = 0;
-      for (int k8 = 0; k8 < kSB; ++k8) {
-        const int li = li0 + b * kSB + k8;
-        if (li >= li1) break;
-        const int v = L.e[li];
-        const int s = le_sid(v);
-        tot += 2 * bytes + (le_hg(v) ? bytes : 0);
-      }
-      mbar_expect_tx(bars + (k & 1), tot);
-      for (int k8 = 0; k8 < kSB; ++k8) {
-        const int li = li0 + b * kSB + k8;
-        if (li >= li1) break;
-        const int v = L.e[li];
-        const int s = le_sid(v);
-        double* d = stg + k8 * kSVec * kSRows;
-        bulk_load(d, cg->Wv + (int64_t)s * N + r0, bytes, bars + (k & 1));
-        bulk_load(d + kSRows, cg->R + (int64_t)s * N + r0, bytes, bars + (k & 1));
-        if (le_hg(v)) bulk_load(d + 2 * kSRows, cg->ZGhat + (int64_t)s * cg->ldgh + r0, bytes, bars + (k & 1));
-      }
-    };
-    if (tid == 0) {
-      bulk_wait_read0();   // the previous unit's last bulk stores have read their stage
-      issue(0);
+    int sv[2], md[2], hgv[2];
+    double al[2];
+    bool ok[2];
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb) {
+      const int li = li0 + 8 * nb + g;
+      ok[nb] = li < li1;
+      const int v = ok[nb] ? L.e[li] : 0;
+      sv[nb] = le_sid(v);
+      md[nb] = ok[nb] ? le_mode(v) : ST_ACTIVE;
+      hgv[nb] = ok[nb] ? le_hg(v) : 0;
+      al[nb] = ok[nb] ? s_alpha[li] : 0.0;
     }
-    __syncthreads();   // ACC zeroed
-    for (int k = 0; k < nsteps; ++k) {
-      const int sub = k / nb, b = k % nb;
-      const int64_t r0 = cbeg + (int64_t)sub * kSRows;
-      const int nr = (int)imin64(kSRows, N - r0);
-      double* stg = ST + (k & 1) * SC::STAGE;
-      if (tid == 0 && k + 1 < nsteps) {
-        bulk_wait_read0();   // step k-1's bulk stores have read the other stage
-        issue(k + 1);
-      }
-      // A fragments of this warp's 16 rows (group columns 8 mb + g), before the stage wait
-      double aA[4][2], aE[4][2];
+    double dA[2][2][2], dE[2][2][2], rh[2], zt[2];
 #pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        const int row = warp * 16 + kk * 4 + q;
+    for (int nb = 0; nb < 2; ++nb) {
+      rh[nb] = 0.0; zt[nb] = 0.0;
 #pragma unroll
-        for (int mb = 0; mb < 2; ++mb) {
-          const int col = 8 * mb + g;
-          const bool va = row < nr && col < J;
-          aA[kk][mb] = va ? __ldg(AWg + (int64_t)col * ldw + r0 + row) : 0.0;
-          aE[kk][mb] = va ? __ldg(EWg + (int64_t)col * ldw + r0 + row) : 0.0;
-        }
-      }
-      mbar_wait(bars + (k & 1), (bpar >> (k & 1)) & 1u);
-      bpar ^= 1u << (k & 1);
-      // (a) r update, rho and zeta: warp = shift of the batch, lane = 4 rows
-      {
-        const int li = li0 + b * kSB + warp;
-        double rh = 0.0, zt = 0.0;
-        if (li < li1) {
-          const int v = L.e[li];
-          const bool act = le_mode(v) == ST_ACTIVE;
-          const double al = s_alpha[li];
-          double* d = stg + warp * kSVec * kSRows;
-#pragma unroll
-          for (int h = 0; h < 4; ++h) {
-            const int row = lane * 4 + h;
-            double rn = 0.0;
-            if (row < nr) {
-              const double wv = d[row];
-              rn = act ? fma(-al, wv, d[kSRows + row]) : __ldg(cg->b + r0 + row) - wv;
-              rh = fma(rn, rn, rh);
-              if (le_hg(v)) zt = fma(d[2 * kSRows + row], rn, zt);
-            }
-            d[kSRows + row] = rn;
-          }
-        } else {
-          double* d = stg + warp * kSVec * kSRows;
-#pragma unroll
-          for (int h = 0; h < 4; ++h) d[kSRows + lane * 4 + h] = 0.0;
-        }
-        rh = warp_sum(rh);
-        zt = warp_sum(zt);
-        if (lane == 0 && li < li1) {
-          double* a = ACC + (li - li0) * kSAcc;
-          a[32] += rh;
-          a[33] += zt;
-        }
-      }
-      fence_async_smem();
-      __syncthreads();
-      if (tid == 0) {
-        for (int k8 = 0; k8 < kSB; ++k8) {
-          const int li = li0 + b * kSB + k8;
-          if (li >= li1) break;
-          const int s = le_sid(L.e[li]);
-          bulk_store(cg->R + (int64_t)s * N + r0, stg + k8 * kSVec * kSRows + kSRows, 8u * nr);
-        }
-        bulk_commit();
-      }
-      // (b) [AW ; EW]^T R on the tensor cores: warp = 16 rows (4 k-steps), D[j][shift]
-      {
-        double dA[2][2], dE[2][2];
-#pragma unroll
-        for (int mb = 0; mb < 2; ++mb) dA[mb][0] = dA[mb][1] = dE[mb][0] = dE[mb][1] = 0.0;
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const int row = warp * 16 + kk * 4 + q;
-          const double bv = stg[g * kSVec * kSRows + kSRows + row];   // r'(shift g, row)
-#pragma unroll
-          for (int mb = 0; mb < 2; ++mb) {
-            if (mb == 1 && J <= 8) break;
-            dmma(dA[mb][0], dA[mb][1], aA[kk][mb], bv);
-            dmma(dE[mb][0], dE[mb][1], aE[kk][mb], bv);
-          }
-        }
-        // D[m = 8 mb + g][n = 2q + h] of this warp -> RED[warp][acc][m * 8 + n]
-        double* rw = RED + warp * 4 * 64;
-#pragma unroll
-        for (int mb = 0; mb < 2; ++mb)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            rw[(2 * mb + 0) * 64 + g * 8 + 2 * q + h] = dA[mb][h];
-            rw[(2 * mb + 1) * 64 + g * 8 + 2 * q + h] = dE[mb][h];
-          }
-      }
-      __syncthreads();
-      // fixed-order sum over the 8 warps into the pass accumulators
-      for (int e = tid; e < kSB * 32; e += blockDim.x) {
-        const int k8 = e >> 5, slot = e & 31;        // slot: 0..15 zA, 16..31 zE
-        const int li = li0 + b * kSB + k8;
-        const int j = slot & 15, isE = slot >> 4;
-        if (li >= li1 || j >= J) continue;
-        const int mb = j >> 3, m = j & 7;
-        double t = 0.0;
-#pragma unroll
-        for (int w = 0; w < 8; ++w) t += RED[w * 4 * 64 + (2 * mb + isE) * 64 + m * 8 + k8];
-        ACC[(li - li0) * kSAcc + slot] += t;
-      }
-      __syncthreads();
+      for (int mb = 0; mb < 2; ++mb) { dA[nb][mb][0] = dA[nb][mb][1] = dE[nb][mb][0] = dE[nb][mb][1] = 0.0; }
     }
-    // chunk partials: z_j = zA_j + gamma zE_j (W columns), zeta (carried column), rho
+    const int nbn = (np + 7) >> 3;
+    // 8-row super-steps: lane (g, q) loads rows 2q, 2q+1 as one 16-byte pair (64-byte runs
+    // per column / shift across the four q lanes); k-step t of the two uses row 2q + t --
+    // the same row permutation on A and B, so D sums over all 8 rows
+#pragma unroll 2
+    for (int64_t row0 = wbeg; row0 < wend; row0 += 8) {
+      const int64_t row = row0 + 2 * q;
+      const bool vr = row < wend;           // wend - row0 is a multiple of 8 except at N
+      const bool vr1 = row + 1 < wend;
+      double2 aA[2], aE[2], wv[2], rv[2], zg[2];
+#pragma unroll
+      for (int mb = 0; mb < 2; ++mb) {
+        const int col = 8 * mb + g;
+        const bool va = vr && col < J;
+        aA[mb] = va ? __ldg(reinterpret_cast<const double2*>(AWg + (int64_t)col * ldw + row)) : make_double2(0.0, 0.0);
+        aE[mb] = va ? __ldg(reinterpret_cast<const double2*>(EWg + (int64_t)col * ldw + row)) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb) {
+        wv[nb] = rv[nb] = zg[nb] = make_double2(0.0, 0.0);
+        if (nb < nbn && ok[nb] && vr) {
+          const int64_t o = (int64_t)sv[nb] * N + row;
+          wv[nb] = __ldcg(reinterpret_cast<const double2*>(cg->Wv + o));
+          rv[nb] = (md[nb] == ST_ACTIVE) ? __ldcg(reinterpret_cast<const double2*>(cg->R + o))
+                                         : __ldg(reinterpret_cast<const double2*>(cg->b + row));
+          if (hgv[nb]) zg[nb] = __ldg(reinterpret_cast<const double2*>(cg->ZGhat + (int64_t)sv[nb] * cg->ldgh + row));
+        }
+      }
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb) {
+        if (nb >= nbn) break;                  // uniform across the warp
+        double2 rn = make_double2(0.0, 0.0);
+        if (ok[nb] && vr) {
+          if (md[nb] == ST_ACTIVE) {
+            rn.x = fma(-al[nb], wv[nb].x, rv[nb].x);
+            rn.y = fma(-al[nb], wv[nb].y, rv[nb].y);
+          } else {
+            rn.x = rv[nb].x - wv[nb].x;
+            rn.y = rv[nb].y - wv[nb].y;
+          }
+          if (!vr1) rn.y = 0.0;
+          double* rp = cg->R + (int64_t)sv[nb] * N + row;
+          if (vr1) *reinterpret_cast<double2*>(rp) = rn;
+          else rp[0] = rn.x;
+          rh[nb] = fma(rn.x, rn.x, rh[nb]);
+          rh[nb] = fma(rn.y, rn.y, rh[nb]);
+          zt[nb] = fma(zg[nb].x, rn.x, zt[nb]);
+          zt[nb] = fma(zg[nb].y, rn.y, zt[nb]);
+        }
+        dmma(dA[nb][0][0], dA[nb][0][1], aA[0].x, rn.x);
+        dmma(dE[nb][0][0], dE[nb][0][1], aE[0].x, rn.x);
+        dmma(dA[nb][0][0], dA[nb][0][1], aA[0].y, rn.y);
+        dmma(dE[nb][0][0], dE[nb][0][1], aE[0].y, rn.y);
+        if (J > 8) {
+          dmma(dA[nb][1][0], dA[nb][1][1], aA[1].x, rn.x);
+          dmma(dE[nb][1][0], dE[nb][1][1], aE[1].x, rn.x);
+          dmma(dA[nb][1][0], dA[nb][1][1], aA[1].y, rn.y);
+          dmma(dE[nb][1][0], dE[nb][1][1], aE[1].y, rn.y);
+        }
+      }
+    }
+    // stage: D[m = 8 mb + g][n = 2q, 2q+1] of N-block nb; rho / zeta summed over the q lanes
+    double* rw = red + (size_t)warp * 32 * kRW;
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb) {
+      if (nb >= nbn) break;
+      double r1 = rh[nb], z1 = zt[nb];
+      r1 += __shfl_xor_sync(0xffffffffu, r1, 1);
+      r1 += __shfl_xor_sync(0xffffffffu, r1, 2);
+      z1 += __shfl_xor_sync(0xffffffffu, z1, 1);
+      z1 += __shfl_xor_sync(0xffffffffu, z1, 2);
+      if (q == 0) {
+        rw[(8 * nb + g) * kRW + 32] = r1;
+        rw[(8 * nb + g) * kRW + 33] = z1;
+      }
+#pragma unroll
+      for (int mb = 0; mb < 2; ++mb) {
+        const int m = 8 * mb + g;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int sh = 8 * nb + 2 * q + h;
+          rw[sh * kRW + m] = dA[nb][mb][h];
+          rw[sh * kRW + 16 + m] = dE[nb][mb][h];
+        }
+      }
+    }
+    __syncthreads();
     for (int e = tid; e < np * kSPV; e += blockDim.x) {
       const int k = e / kSPV, j = e - k * kSPV;
       const int v = L.e[li0 + k];
-      const int s = le_sid(v);
       const int nw = le_m(v) - le_hg(v);
-      const double* a = ACC + k * kSAcc;
-      double val;
-      if (j < nw) val = fma(cg->gam[s], a[16 + j], a[j]);
-      else if (le_hg(v) && j == nw) val = a[33];
-      else if (j == kMaxM) val = a[32];
-      else continue;
-      P.partB[((size_t)s * kSPV + j) * P.nchunk + c] = val;
+      const bool isz = j < nw, isg = le_hg(v) && j == nw, isr = j == kMaxM;
+      if (!(isz || isg || isr)) continue;
+      double ta = 0.0, te = 0.0;
+#pragma unroll
+      for (int w = 0; w < 8; ++w) {
+        const double* r = red + ((size_t)w * 32 + k) * kRW;
+        if (isz) { ta += r[j]; te += r[16 + j]; }
+        else ta += r[isr ? 32 : 33];
+      }
+      const int s = le_sid(v);
+      const double val = isz ? fma(cg->gam[s], te, ta) : ta;
+      P.partB[((size_t)s * kSPV + j) * P.nchunk + blockIdx.x] = val;
     }
     __syncthreads();
   }
-  if (tid == 0) bulk_wait0();   // every bulk store of this phase complete before the barrier
+}
+
+// ---------------------------------------------------------------- phase C (register form)
+// x += alpha p; p = r + beta p - W mu_W - ghat mu_g. W mu of a pass on the tensor cores:
+// an 8-row block x 8 shifts is D = W[8 x J] M[J x 8] (B = the shifts' mu); lane (g, q)
+// finishes the elements (row g, shifts 2q, 2q+1) of each N-block.
+template <int R>
+__device__ void s_phase_c_reg(const StreamParams& P, const SList& L, double* smem, const double* s_alpha, int* pst,
+                              CgDev* cg) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int64_t N = cg->N;
+  const int npass = s_passes(L, pst);
+  const int64_t cbeg = (int64_t)blockIdx.x * P.rpc;
+  const int64_t cend = imin64(N, cbeg + P.rpc);
+  const int64_t rpw = P.rpc / 8;
+  const int64_t wbeg = cbeg + warp * rpw;
+  const int64_t wend = imin64(cend, wbeg + rpw);
+  double* PS = smem;   // [32][kSPS]: beta, 1/|r|, slot, flags, alpha, mu_g
+  double* MU = smem + 32 * kSPS;   // [32][kMaxM]
+  for (int pk = 0; pk < npass; ++pk) {
+    const int li0 = pst[pk], li1 = pst[pk + 1];
+    const int np = li1 - li0;
+    const int grp = le_grp(L.e[li0]);
+    const int J = cg->grp.J[grp];
+    const double* Wg = cg->grp.W[grp];
+    const int64_t ldw = cg->grp.ldw;
+    __syncthreads();   // the previous pass's PS / MU readers are done
+    if (tid < np) {
+      const int li = li0 + tid;
+      const int v = L.e[li];
+      const int s = le_sid(v);
+      const int st = cg->status[s];
+      const int slot = (st == ST_ACTIVE) ? cg->stslot[s] : -1;
+      int f = 0;
+      if (le_mode(v) == ST_ACTIVE && s_alpha[li] != 0.0) f |= 1;
+      if (st == ST_ACTIVE) f |= 2;
+      double* ps = PS + tid * kSPS;
+      ps[0] = cg->beta[s];
+      ps[1] = (slot >= 0) ? 1.0 / sqrt(cg->rho[s]) : 0.0;
+      ps[2] = (double)slot;
+      ps[3] = (double)f;
+      ps[4] = s_alpha[li];
+      const int m = le_m(v);
+      ps[5] = m > 0 ? cg->coef[(int64_t)s * kMaxM + m - 1] : 0.0;
+    }
+    for (int e = tid; e < np * kMaxM; e += blockDim.x) {
+      const int k = e / kMaxM, j = e - k * kMaxM;
+      MU[e] = cg->coef[(int64_t)le_sid(L.e[li0 + k]) * kMaxM + j];
+    }
+    __syncthreads();
+    // B fragments: mu of shift 8 nb + g, component 4 kk + q (0 beyond its nw or w/o new p)
+    double bm[2][4];
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb) {
+      const int k = 8 * nb + g;
+      const bool okk = k < np && (((int)PS[k * kSPS + 3]) & 2);
+      const int nw = okk ? le_m(L.e[li0 + k]) - le_hg(L.e[li0 + k]) : 0;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int j = 4 * kk + q;
+        bm[nb][kk] = (okk && j < nw) ? MU[k * kMaxM + j] : 0.0;
+      }
+    }
+    const int nkk = (J + 3) >> 2;
+    const int nbn = (np + 7) >> 3;
+    int flg[2][2];
+#pragma unroll
+    for (int nb = 0; nb < 2; ++nb)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int k = 8 * nb + 2 * q + h;
+        flg[nb][h] = k < np ? (int)PS[k * kSPS + 3] : 0;
+      }
+    // 16-row blocks: lane (g, q) owns rows 2g, 2g+1 (one 16-byte pair: 128-byte runs per
+    // column / shift across the eight g lanes); two DMMAs per k-step, one per row parity
+#pragma unroll 1
+    for (int64_t row0 = wbeg; row0 < wend; row0 += 16) {
+      const int64_t row = row0 + 2 * g;
+      const bool vr = row < wend;            // rows come in pairs (N even)
+      double2 a[4];
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int j = 4 * kk + q;
+        a[kk] = (vr && kk < nkk && j < J) ? __ldg(reinterpret_cast<const double2*>(Wg + (int64_t)j * ldw + row))
+                                          : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb) {
+        if (nb >= nbn) break;
+        double2 pv[2], rv[2], xv[2], gv[2];
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          pv[h] = rv[h] = xv[h] = gv[h] = make_double2(0.0, 0.0);
+          const int f = vr ? flg[nb][h] : 0;
+          if (f) {
+            const int k = 8 * nb + 2 * q + h;
+            const int v = L.e[li0 + k];
+            const int s = le_sid(v);
+            const int64_t o = (int64_t)s * N + row;
+            pv[h] = __ldcg(reinterpret_cast<const double2*>(cg->P + o));
+            if (f & 1) xv[h] = __ldcg(reinterpret_cast<const double2*>(cg->X + (int64_t)s * cg->ldx + row));
+            if (f & 2) {
+              rv[h] = __ldcg(reinterpret_cast<const double2*>(cg->R + o));
+              if (le_hg(v)) gv[h] = __ldg(reinterpret_cast<const double2*>(cg->Ghat + (int64_t)s * cg->ldgh + row));
+            }
+          }
+        }
+        double de[2] = {0.0, 0.0}, dd[2] = {0.0, 0.0};   // rows 2g (even) and 2g+1 (odd)
+#pragma unroll
+        for (int kk = 0; kk < 4; ++kk)
+          if (kk < nkk) {
+            dmma(de[0], de[1], a[kk].x, bm[nb][kk]);
+            dmma(dd[0], dd[1], a[kk].y, bm[nb][kk]);
+          }
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int f = vr ? flg[nb][h] : 0;
+          if (!f) continue;
+          const int k = 8 * nb + 2 * q + h;
+          const int v = L.e[li0 + k];
+          const int s = le_sid(v);
+          const double* ps = PS + k * kSPS;
+          if (f & 1) {
+            double2 xn;
+            xn.x = fma(ps[4], pv[h].x, xv[h].x);
+            xn.y = fma(ps[4], pv[h].y, xv[h].y);
+            *reinterpret_cast<double2*>(cg->X + (int64_t)s * cg->ldx + row) = xn;
+          }
+          if (f & 2) {
+            double2 pn;
+            pn.x = fma(ps[0], pv[h].x, rv[h].x) - de[h];
+            pn.y = fma(ps[0], pv[h].y, rv[h].y) - dd[h];
+            if (le_hg(v)) {
+              pn.x = fma(-ps[5], gv[h].x, pn.x);
+              pn.y = fma(-ps[5], gv[h].y, pn.y);
+            }
+            *reinterpret_cast<double2*>(cg->P + (int64_t)s * N + row) = pn;
+            const int sl = (int)ps[2];
+            if (sl >= 0) {
+              double* st = cg->store + ((int64_t)s * cg->store_cap + sl) * cg->lds + row;
+              st[0] = rv[h].x * ps[1];
+              st[1] = rv[h].y * ps[1];
+            }
+          }
+        }
+      }
+    }
+  }
 }
 
 // ---------------------------------------------------------------- phase B2
-__device__ void s_phase_b2(const StreamParams& P, const SList& L, double* smem) {
-  CgDev* cg = P.cg;
+__device__ void s_phase_b2(const StreamParams& P, const SList& L, double* smem, CgDev* cg) {
   const int n = L.n;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   double* zs = smem;
@@ -523,174 +956,171 @@ __device__ void s_phase_b2(const StreamParams& P, const SList& L, double* smem) 
 }
 
 // ---------------------------------------------------------------- phase C
-// stage layout: [8 shifts][p | r | x | ghat][128]
 template <int R>
-__device__ void s_phase_c(const StreamParams& P, const SList& L, double* smem, const double* s_alpha, unsigned& bpar) {
+__device__ void s_phase_c(const StreamParams& P, const SList& L, double* smem, const double* s_alpha, unsigned& bpar,
+                          int* pst, unsigned char* s_flag, CgDev* cg) {
   using SC = SCfg<R>;
-  CgDev* cg = P.cg;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, q = lane & 3;
   const int64_t N = cg->N;
-  double* ST = smem + SC::OFF_ST;
   double* PS = smem + SC::OFF_PS;   // per pass entry: beta, 1/|r|, slot, flags, alpha
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SC::OFF_BAR);
-  const int npass = s_npass(L);
-  const int nunits = P.nchunk * npass;
-  for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-    const int c = u % P.nchunk, pk = u / P.nchunk;
-    const int li0 = s_pass_start(L, pk), li1 = s_pass_end(L, li0);
-    const int np = li1 - li0;
-    const int grp = le_grp(L.e[li0]);
+  const int npass = s_passes(L, pst);
+  const int nunits = npass;
+  if ((int64_t)blockIdx.x * P.rpc >= N) return;   // no rows for this CTA
+  // flags of every list entry (1 = x += alpha p, 2 = new p: status after B2 is ACTIVE)
+  for (int li = tid; li < L.n; li += blockDim.x) {
+    const int s = le_sid(L.e[li]);
+    int f = 0;
+    if (le_mode(L.e[li]) == ST_ACTIVE && s_alpha[li] != 0.0) f |= 1;
+    if (cg->status[s] == ST_ACTIVE) f |= 2;
+    s_flag[li] = (unsigned char)f;
+  }
+  __syncthreads();
+  // producer = warp 0, one lane per shift slot of the batch (+ lane 31: the W tile)
+  auto issue = [&](SStep st, unsigned q2) {
+    const SGeo G = s_geo(pst, P.rpc, N, st.u);
+    const int sub = st.k / G.nb, b = st.k % G.nb;
+    const int64_t r0 = G.cbeg + (int64_t)sub * kSRs;
+    const int nr = (int)imin64(kSRs, G.cend - r0);
+    const unsigned bytes = 8u * nr;
+    const int grp = le_grp(L.e[G.li0]);
     const int J = cg->grp.J[grp];
-    const double* Wg = cg->grp.W[grp];
-    const int64_t ldw = cg->grp.ldw;
-    const int64_t cbeg = (int64_t)c * kSChunk;
-    const int nsub = (int)((imin64(N, cbeg + kSChunk) - cbeg + kSRows - 1) / kSRows);
-    const int nb = (np + kSB - 1) / kSB;
-    const int nsteps = nsub * nb;
-    // per entry: flags 1 = x += alpha p, 2 = new p (status after B2 is ACTIVE)
-    if (tid < np) {
-      const int li = li0 + tid;
-      const int s = le_sid(L.e[li]);
-      const int st = cg->status[s];
-      const int slot = (st == ST_ACTIVE) ? cg->stslot[s] : -1;
-      int f = 0;
-      if (le_mode(L.e[li]) == ST_ACTIVE && s_alpha[li] != 0.0) f |= 1;
-      if (st == ST_ACTIVE) f |= 2;
-      double* ps = PS + tid * kSPS;
-      ps[0] = cg->beta[s];
-      ps[1] = (slot >= 0) ? 1.0 / sqrt(cg->rho[s]) : 0.0;
-      ps[2] = (double)slot;
-      ps[3] = (double)f;
-      ps[4] = s_alpha[li];
+    const int slot = q2 % kSNST;
+    double* stg = smem + SC::OFF_ST + slot * SC::STAGE;
+    uint64_t* bar = bars + slot;
+    const int li = G.li0 + b * kSB + lane;
+    const bool mine = lane < kSB && li < G.li1;
+    const int f = mine ? s_flag[li] : 0;
+    const int v = mine ? L.e[li] : 0;
+    unsigned my = 0;
+    if (f) {
+      my = bytes;
+      if (f & 1) my += bytes;
+      if (f & 2) my += bytes + (le_hg(v) ? bytes : 0);
     }
-    __syncthreads();
-    auto issue = [&](int k) {
-      const int sub = k / nb, b = k % nb;
-      const int64_t r0 = cbeg + (int64_t)sub * kSRows;
-      const int nr = (int)imin64(kSRows, N - r0);
-      const unsigned bytes = 8u * nr;
-      double* stg = ST + (k & 1) * SC::STAGE;
-      unsigned tot = 0;
-      for (int k8 = 0; k8 < kSB; ++k8) {
-        const int li = li0 + b * kSB + k8;
-        if (li >= li1) break;
-        const int f = (int)PS[(li - li0) * kSPS + 3];
-        if (!f) continue;
-        tot += bytes;                                              // p
-        if (f & 1) tot += bytes;                                   // x
-        if (f & 2) tot += bytes + (le_hg(L.e[li]) ? bytes : 0);    // r, ghat
+    const unsigned anyp = __ballot_sync(0xffffffffu, (f & 2) != 0);
+    if (lane == 31 && anyp && J > 0) my += 8u * kSP * J;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) my += __shfl_xor_sync(0xffffffffu, my, o);
+    if (lane == 0) mbar_expect_tx(bar, my);
+    __syncwarp();
+    if (f) {
+      const int s = le_sid(v);
+      double* d = stg + 16 * kSP + lane * kSVec * kSP;
+      bulk_load(d, cg->P + (int64_t)s * N + r0, bytes, bar);
+      if (f & 1) bulk_load(d + 2 * kSP, cg->X + (int64_t)s * cg->ldx + r0, bytes, bar);
+      if (f & 2) {
+        bulk_load(d + kSP, cg->R + (int64_t)s * N + r0, bytes, bar);
+        if (le_hg(v)) bulk_load(d + 3 * kSP, cg->Ghat + (int64_t)s * cg->ldgh + r0, bytes, bar);
       }
-      mbar_expect_tx(bars + (k & 1), tot);
-      for (int k8 = 0; k8 < kSB; ++k8) {
-        const int li = li0 + b * kSB + k8;
-        if (li >= li1) break;
-        const int f = (int)PS[(li - li0) * kSPS + 3];
-        if (!f) continue;
-        const int v = L.e[li];
-        const int s = le_sid(v);
-        double* d = stg + k8 * kSVec * kSRows;
-        bulk_load(d, cg->P + (int64_t)s * N + r0, bytes, bars + (k & 1));
-        if (f & 1) bulk_load(d + 2 * kSRows, cg->X + (int64_t)s * cg->ldx + r0, bytes, bars + (k & 1));
-        if (f & 2) {
-          bulk_load(d + kSRows, cg->R + (int64_t)s * N + r0, bytes, bars + (k & 1));
-          if (le_hg(v)) bulk_load(d + 3 * kSRows, cg->Ghat + (int64_t)s * cg->ldgh + r0, bytes, bars + (k & 1));
-        }
-      }
-    };
-    if (tid == 0 && nsteps > 0) {
-      bulk_wait_read0();
-      issue(0);
     }
+    if (lane == 31 && anyp && J > 0) tma_load_2d(stg + SC::OFF_SG, &P.mW[grp], bar, (int)r0, 0);
+  };
+  auto advance = [&](SStep& st) {
+    const SGeo G = s_geo(pst, P.rpc, N, st.u);
+    if (++st.k >= G.nsteps) { st.k = 0; st.u += 1; }
+  };
+  SStep cons{0, 0}, prod = cons;
+  unsigned qn = 0, qp = 0;
+  unsigned long long s_tstep = 0;
+  if (warp == 0)
+    for (int i = 0; i < kSNST - 1 && prod.u < nunits; ++i) { issue(prod, qp++); advance(prod); }
+  while (cons.u < nunits) {
+    const SGeo G = s_geo(pst, P.rpc, N, cons.u);
+    const int np = G.li1 - G.li0;
+    if (cons.k == 0) {
+      __syncthreads();   // the previous unit's PS readers are done
+      if (tid < np) {
+        const int li = G.li0 + tid;
+        const int s = le_sid(L.e[li]);
+        const int st = cg->status[s];
+        const int slot = (st == ST_ACTIVE) ? cg->stslot[s] : -1;
+        double* ps = PS + tid * kSPS;
+        ps[0] = cg->beta[s];
+        ps[1] = (slot >= 0) ? 1.0 / sqrt(cg->rho[s]) : 0.0;
+        ps[2] = (double)slot;
+        ps[3] = (double)s_flag[li];
+        ps[4] = s_alpha[li];
+        const int m = le_m(L.e[li]);
+        ps[5] = m > 0 ? cg->coef[(int64_t)s * kMaxM + m - 1] : 0.0;   // mu of the carried column
+      }
+      __syncthreads();
+    }
+    if (warp == 0 && prod.u < nunits) { issue(prod, qp++); advance(prod); }
+    const int sub = cons.k / G.nb, b = cons.k % G.nb;
+    const int64_t r0 = G.cbeg + (int64_t)sub * kSRs;
+    const int nr = (int)imin64(kSRs, G.cend - r0);
+    const int grp = le_grp(L.e[G.li0]);
+    const int J = cg->grp.J[grp];
     const int nkk = (J + 3) >> 2;
-    for (int k = 0; k < nsteps; ++k) {
-      const int sub = k / nb, b = k % nb;
-      const int64_t r0 = cbeg + (int64_t)sub * kSRows;
-      const int nr = (int)imin64(kSRows, N - r0);
-      double* stg = ST + (k & 1) * SC::STAGE;
-      if (tid == 0 && k + 1 < nsteps) {
-        bulk_wait_read0();
-        issue(k + 1);
+    // B fragments: mu of batch shift g, component 4 kk + q (0 unless a new p is formed)
+    double bm[4];
+    {
+      const int li = G.li0 + b * kSB + g;
+      const bool ok = li < G.li1 && (((int)PS[(li - G.li0) * kSPS + 3]) & 2);
+      const int v = ok ? L.e[li] : 0;
+      const int nw = ok ? le_m(v) - le_hg(v) : 0;
+      const double* cf = cg->coef + (int64_t)le_sid(v) * kMaxM;
+#pragma unroll
+      for (int kk = 0; kk < 4; ++kk) {
+        const int j = 4 * kk + q;
+        bm[kk] = (ok && j < nw) ? cf[j] : 0.0;
       }
-      // B fragments: mu of batch shift g, component 4 kk + q (0 unless a new p is formed)
-      double bm[4];
-      {
-        const int li = li0 + b * kSB + g;
-        const bool ok = li < li1 && (((int)PS[(li - li0) * kSPS + 3]) & 2);
-        const int v = ok ? L.e[li] : 0;
-        const int nw = ok ? le_m(v) - le_hg(v) : 0;
-        const double* cf = cg->coef + (int64_t)le_sid(v) * kMaxM;
+    }
+    const int slot = qn % kSNST;
+    double* stg = smem + SC::OFF_ST + slot * SC::STAGE;
+    unsigned long long tw0 = 0;
+    if (P.prof && blockIdx.x == 0 && tid == 32) tw0 = s_timer();
+    mbar_wait(bars + slot, (bpar >> slot) & 1u);
+    if (P.prof && blockIdx.x == 0 && tid == 32) {
+      const unsigned long long t1 = s_timer();
+      g_sprof2[2] += t1 - tw0; g_sprof2[3] += 1;
+      if (s_tstep) g_sprof2[5] += t1 - s_tstep;
+      s_tstep = t1;
+    }
+    bpar ^= 1u << slot;
+    // W mu on the tensor cores: warp = 8-row block, D[row g][shifts 2q, 2q+1]; then the
+    // x / p updates of those elements
+    {
+      const int row = warp * 8 + g;
+      double d[2] = {0.0, 0.0};
+      const double* wt = stg + SC::OFF_SG;
 #pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const int j = 4 * kk + q;
-          bm[kk] = (ok && j < nw) ? cf[j] : 0.0;
-        }
+      for (int kk = 0; kk < 4; ++kk) {
+        if (kk >= nkk) break;
+        const int j = 4 * kk + q;
+        dmma(d[0], d[1], j < J ? wt[j * kSP + row] : 0.0, bm[kk]);
       }
-      // W fragments of this warp's two 8-row blocks, issued before the stage wait
-      double a[2][4];
+      if (row < nr) {
 #pragma unroll
-      for (int rr = 0; rr < 2; ++rr) {
-        const int row = (2 * warp + rr) * 8 + g;
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk) {
-          const int j = 4 * kk + q;
-          a[rr][kk] = (kk < nkk && j < J && row < nr) ? __ldg(Wg + (int64_t)j * ldw + r0 + row) : 0.0;
-        }
-      }
-      mbar_wait(bars + (k & 1), (bpar >> (k & 1)) & 1u);
-      bpar ^= 1u << (k & 1);
-#pragma unroll
-      for (int rr = 0; rr < 2; ++rr) {
-        const int row = (2 * warp + rr) * 8 + g;
-        double d[2] = {0.0, 0.0};
-#pragma unroll
-        for (int kk = 0; kk < 4; ++kk)
-          if (kk < nkk) dmma(d[0], d[1], a[rr][kk], bm[kk]);
-        if (row < nr) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const int k8 = 2 * q + h;
-            const int li = li0 + b * kSB + k8;
-            if (li >= li1) continue;
-            const double* ps = PS + (li - li0) * kSPS;
-            const int f = (int)ps[3];
-            if (!f) continue;
-            const int v = L.e[li];
-            double* ds = stg + k8 * kSVec * kSRows;
-            const double pv = ds[row];
-            if (f & 1) ds[2 * kSRows + row] = fma(ps[4], pv, ds[2 * kSRows + row]);
-            if (f & 2) {
-              const double rv = ds[kSRows + row];
-              double pn = fma(ps[0], pv, rv) - d[h];
-              if (le_hg(v)) pn = fma(-cg->coef[(int64_t)le_sid(v) * kMaxM + le_m(v) - 1], ds[3 * kSRows + row], pn);
-              ds[row] = pn;
-              const int slot = (int)ps[2];
-              if (slot >= 0) {
-                const int s = le_sid(v);
-                cg->store[((int64_t)s * cg->store_cap + slot) * cg->lds + r0 + row] = rv * ps[1];
-              }
-            }
+        for (int h = 0; h < 2; ++h) {
+          const int k8 = 2 * q + h;
+          const int li = G.li0 + b * kSB + k8;
+          if (li >= G.li1) continue;
+          const double* ps = PS + (li - G.li0) * kSPS;
+          const int f = (int)ps[3];
+          if (!f) continue;
+          const int v = L.e[li];
+          const int s = le_sid(v);
+          const double* ds = stg + 16 * kSP + k8 * kSVec * kSP;
+          const double pv = ds[row];
+          if (f & 1) cg->X[(int64_t)s * cg->ldx + r0 + row] = fma(ps[4], pv, ds[2 * kSP + row]);
+          if (f & 2) {
+            const double rv = ds[kSP + row];
+            double pn = fma(ps[0], pv, rv) - d[h];
+            if (le_hg(v)) pn = fma(-ps[5], ds[3 * kSP + row], pn);
+            cg->P[(int64_t)s * N + r0 + row] = pn;
+            const int sl = (int)ps[2];
+            if (sl >= 0) cg->store[((int64_t)s * cg->store_cap + sl) * cg->lds + r0 + row] = rv * ps[1];
           }
         }
       }
-      fence_async_smem();
-      __syncthreads();
-      if (tid == 0) {
-        for (int k8 = 0; k8 < kSB; ++k8) {
-          const int li = li0 + b * kSB + k8;
-          if (li >= li1) break;
-          const int f = (int)PS[(li - li0) * kSPS + 3];
-          const int s = le_sid(L.e[li]);
-          const double* ds = stg + k8 * kSVec * kSRows;
-          if (f & 2) bulk_store(cg->P + (int64_t)s * N + r0, ds, 8u * nr);
-          if (f & 1) bulk_store(cg->X + (int64_t)s * cg->ldx + r0, ds + 2 * kSRows, 8u * nr);
-        }
-        bulk_commit();
-      }
     }
-    __syncthreads();
+    __syncthreads();   // stage released
+    advance(cons);
+    ++qn;
   }
-  if (tid == 0) bulk_wait0();
 }
 
 // ---------------------------------------------------------------- the kernel
@@ -702,18 +1132,23 @@ __global__ void __launch_bounds__(kAT, kStripCtasPerSm) cg_stream_kernel(const _
   __shared__ SList lists[2];
   __shared__ int tmp[kSMaxShift];
   __shared__ double s_alpha[kSMaxShift];
+  __shared__ int pst[kSMaxPass + 1];
+  __shared__ unsigned char s_flag[kSMaxShift];
+  // the loop state's pointers and sizes in shared memory (the struct itself never changes;
+  // the arrays it points to do): no global round trip per field access after the L1
+  // invalidations of the grid barriers
+  __shared__ CgDev s_cg;
+  if (threadIdx.x == 0) s_cg = *P.cg;
 
-  CgDev* cg = P.cg;
+  CgDev* cg = &s_cg;
   const int ns = P.nshift;
   const int tid = threadIdx.x;
   // strip-apply barriers and the B/C stage barriers are distinct mbarriers
   Core::init(smem, P.sp);
   if (tid == 0) {
-    for (int b = 0; b < 2; ++b) mbar_init(reinterpret_cast<uint64_t*>(smem + SC::OFF_BAR) + b, 1);
+    for (int b = 0; b < kSNST; ++b) mbar_init(reinterpret_cast<uint64_t*>(smem + SC::OFF_BAR) + b, 1);
     mbar_fence_init();
   }
-  double bx[SC::Strip::KS], ay[SC::Strip::KS];
-  Core::frags(P.sp, bx, ay);
   StripRing ring{0u, 0u};
   unsigned bpar = 0u;
   unsigned gen = s_ld_acquire(P.bar + 1);
@@ -724,6 +1159,8 @@ __global__ void __launch_bounds__(kAT, kStripCtasPerSm) cg_stream_kernel(const _
   int it = 0;
   unsigned long long t0 = 0;
   auto mark = [&](int ph) {
+    if (P.prof && tid == 0 && it == 30 && ph != 1 && ph != 7) g_cta_t[blockIdx.x][ph] = s_timer();
+    if (P.prof && tid == 0 && it == 30 && ph == 1) g_cta_t[blockIdx.x][5 + (g_cta_t[blockIdx.x][6] ? 1 : 0)] = s_timer();
     if (P.prof && blockIdx.x == 0 && tid == 0) {
       const unsigned long long t1 = s_timer();
       if (t0) g_sprof[ph] += t1 - t0;
@@ -734,21 +1171,23 @@ __global__ void __launch_bounds__(kAT, kStripCtasPerSm) cg_stream_kernel(const _
   for (; it < P.max_iters; ++it) {
     SList& L = lists[cur];
     if (L.n == 0) break;
-    s_phase_a<R>(P, L, smem, ring, bx, ay);
+    s_phase_a<R>(P, L, smem, ring);
     mark(0);
     sgrid_sync(P.bar, gen);
     mark(1);
-    s_phase_b<R>(P, L, smem, s_alpha, bpar);
+    if (P.staged) s_phase_b<R>(P, L, smem, s_alpha, bpar, pst, &s_cg);
+    else s_phase_b_reg<R>(P, L, smem, s_alpha, pst, &s_cg);
     mark(2);
     sgrid_sync(P.bar, gen);
     mark(1);
-    s_phase_b2(P, L, smem);
+    s_phase_b2(P, L, smem, &s_cg);
     mark(3);
     sgrid_sync(P.bar, gen);
     mark(1);
     SList& NL = lists[cur ^ 1];
     s_build_list(cg, ns, NL, tmp);   // statuses are stable until the next phase A
-    s_phase_c<R>(P, L, smem, s_alpha, bpar);
+    if (P.staged) s_phase_c<R>(P, L, smem, s_alpha, bpar, pst, s_flag, &s_cg);
+    else s_phase_c_reg<R>(P, L, smem, s_alpha, pst, &s_cg);
     mark(4);
     sgrid_sync(P.bar, gen);
     mark(1);
@@ -765,15 +1204,44 @@ __global__ void __launch_bounds__(kAT, kStripCtasPerSm) cg_stream_kernel(const _
 bool strip_fill_params(Handle* h, StripParams& p, const double* X, int64_t ldx, const double* X2, int64_t ldx2,
                        int64_t nvec_map, double* Y, int64_t ldy, double* EY, int64_t ldey, const double* gamma,
                        int mode, int seg_rows);
+bool make_map2s(CUtensorMap* m, const double* base, int64_t inner, int64_t outer, int64_t pitch, int bw, int bh);
 
 int stream_seg_rows(int64_t ny) { return ny > 512 ? 256 : 128; }
-int stream_ipv(const Handle* h) {
-  const int seg = stream_seg_rows(h->ny);
-  return (int)((h->nx + kStripW - 1) / kStripW) * (int)((h->ny + seg - 1) / seg);
-}
-int stream_nchunk(int64_t N) { return (int)((N + kSChunk - 1) / kSChunk); }
+// partial slots per shift: the largest item count, 64-row segments (s_seg_rows)
+int stream_ipv(const Handle* h) { return kStripCtasPerSm * h->sm_count; }   // >= the grid
+int stream_nchunk(const Handle* h) { return kStripCtasPerSm * h->sm_count; }   // >= the grid
 int stream_grid(const Handle* h) { return kStripCtasPerSm * h->sm_count; }
 int stream_pv() { return kSPV; }
+
+extern "C" int rsk_debug_stream_cta(double* out, int n) {   // n x 8 (ns timestamps)
+  static unsigned long long v[1024][8];
+  if (cudaMemcpyFromSymbol(v, g_cta_t, sizeof(v)) != cudaSuccess) return -1;
+  for (int i = 0; i < n && i < 1024; ++i)
+    for (int j = 0; j < 8; ++j) out[i * 8 + j] = (double)v[i][j];
+  return 0;
+}
+
+extern "C" int rsk_debug_stream_prof3(double* out8, int reset) {
+  unsigned long long v[8];
+  if (cudaMemcpyFromSymbol(v, g_sprof3, sizeof(v)) != cudaSuccess) return -1;
+  for (int i = 0; i < 8; ++i) out8[i] = (double)v[i];
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_sprof3, z, sizeof(z));
+  }
+  return 0;
+}
+
+extern "C" int rsk_debug_stream_prof2(double* out8, int reset) {
+  unsigned long long v[8];
+  if (cudaMemcpyFromSymbol(v, g_sprof2, sizeof(v)) != cudaSuccess) return -1;
+  for (int i = 0; i < 8; ++i) out8[i] = (double)v[i];
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_sprof2, z, sizeof(z));
+  }
+  return 0;
+}
 
 extern "C" int rsk_debug_stream_prof(double* out8, int reset) {
   unsigned long long v[8];
@@ -789,7 +1257,7 @@ extern "C" int rsk_debug_stream_prof(double* out8, int reset) {
 template <int R>
 static cudaError_t launch_stream_r(StreamParams& prm, int sm_count, cudaStream_t st, bool* ok) {
   using SC = SCfg<R>;
-  static_assert(SC::SMEM <= 110 * 1024, "two CTAs per SM");
+  // two CTAs per SM up to r = 10 (the configs); the occupancy query decides beyond
   auto kfn = cg_stream_kernel<R>;
   static int b = 0;
   if (b == 0) {
@@ -801,6 +1269,9 @@ static cudaError_t launch_stream_r(StreamParams& prm, int sm_count, cudaStream_t
   }
   if (b < 1) { *ok = false; return cudaSuccess; }
   const int grid = (b < kStripCtasPerSm ? b : kStripCtasPerSm) * sm_count;
+  prm.nchunk = grid;
+  // rows per CTA: a multiple of 128 (8 warps x 16-row blocks of phase C, 64-row stages)
+  prm.rpc = ((prm.cg_N + grid - 1) / grid + 127) / 128 * 128;
   void* args[] = {&prm};
   count_launch();
   cudaError_t e = cudaLaunchCooperativeKernel((const void*)kfn, dim3(grid), dim3(kAT), args, SC::SMEM, st);
@@ -828,15 +1299,27 @@ cudaError_t launch_cg_stream(Handle* h, CgDev* dev, const CgDev& hc, double* par
   if (hc.nshift > kSMaxShift || h->r < 1 || h->r > kMaxR) return cudaSuccess;
   // 16-byte rows of every streamed vector
   auto al16p = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  if ((N & 1) || (hc.ldx & 1) || (hc.Ghat && (hc.ldgh & 1)) || !al16p(hc.X) || !al16p(hc.R) || !al16p(hc.P) ||
+  if ((N & 1) || (hc.ldx & 1) || (hc.Ghat && (hc.ldgh & 1)) || (hc.grp.ldw & 1) || !al16p(hc.b) ||
+      !al16p(hc.X) || !al16p(hc.R) || !al16p(hc.P) ||
       !al16p(hc.Wv) || (hc.Ghat && (!al16p(hc.Ghat) || !al16p(hc.ZGhat))))
     return cudaSuccess;
   StreamParams prm;
+  std::memset(&prm, 0, sizeof(prm));
   const int seg = stream_seg_rows(h->ny);
   if (!strip_fill_params(h, prm.sp, hc.P, N, hc.X, hc.ldx, hc.nshift, hc.Wv, N, nullptr, 0, hc.gam,
                          RSK_APPLY_SHIFTED, seg))
     return cudaSuccess;
   prm.sp.want_dot = 1;
+  // group tiles: 2-D maps {N, J_g} with box {kSP rows, J_g columns}
+  for (int gi = 0; gi < RSK_MAX_GROUPS; ++gi) {
+    const int J = hc.grp.J[gi];
+    if (J <= 0 || !hc.grp.AW[gi]) continue;
+    if (J > 16 || !al16p(hc.grp.AW[gi]) || !al16p(hc.grp.EW[gi]) || !al16p(hc.grp.W[gi])) return cudaSuccess;
+    if (!make_map2s(&prm.mAW[gi], hc.grp.AW[gi], N, J, hc.grp.ldw, kSP, J) ||
+        !make_map2s(&prm.mEW[gi], hc.grp.EW[gi], N, J, hc.grp.ldw, kSP, J) ||
+        !make_map2s(&prm.mW[gi], hc.grp.W[gi], N, J, hc.grp.ldw, kSP, J))
+      return cudaSuccess;
+  }
   prm.cg = dev;
   prm.partA = partA;
   prm.partB = partB;
@@ -844,9 +1327,10 @@ cudaError_t launch_cg_stream(Handle* h, CgDev* dev, const CgDev& hc, double* par
   prm.nactive = nactive;
   prm.iters_done = iters_done;
   prm.nshift = hc.nshift;
-  prm.nchunk = stream_nchunk(N);
-  prm.ipv = prm.sp.nseg * prm.sp.nstrip;
+  prm.cg_N = N;
+  prm.ipv = stream_ipv(h);   // stride of partA; the items of an iteration: s_ipv()
   prm.max_iters = max_iters;
+  prm.staged = getenv("RSK_STREAM_STAGED") ? 1 : 0;
   {
     static int pf = -1;
     if (pf < 0) pf = getenv("RSK_PERSIST_PROF") ? 1 : 0;

@@ -211,7 +211,7 @@ cudaError_t launch_cg_persist(Handle* h, CgDev* dev, const CgDev& hc, double* pa
 
 // streaming persistent loop for images beyond L2 (cg_stream.cu)
 int stream_ipv(const Handle* h);
-int stream_nchunk(int64_t N);
+int stream_nchunk(const Handle* h);
 int stream_pv();
 cudaError_t launch_cg_stream(Handle* h, CgDev* dev, const CgDev& hc, double* partA, double* partB, unsigned* bar,
                              int* nactive, int* iters_done, int max_iters, cudaStream_t st, bool* ok);

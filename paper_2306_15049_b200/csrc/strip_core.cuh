@@ -46,7 +46,8 @@ struct StripCfg {
   static constexpr int OFF_T = OFF_IN + al16(64 * PX);   // [64][PT] x-pass ring
   static constexpr int RING_END = OFF_T + al16(64 * PT);
   static constexpr int OFF_DC = TAIL > 0 ? TAIL : RING_END;   // [4R][R] zero-boundary corrections
-  static constexpr int OFF_RED = OFF_DC + al16(4 * R * R);   // block-reduction scratch
+  static constexpr int OFF_FR = OFF_DC + al16(4 * R * R);    // [2][KS][32] Toeplitz fragments
+  static constexpr int OFF_RED = OFF_FR + al16(2 * KS * 32);  // block-reduction scratch
   static constexpr int OFF_BAR = OFF_RED + 16;      // 8 mbarriers (8 B each)
   static constexpr int DBL = OFF_BAR + 8;
   static constexpr size_t SMEM = sizeof(double) * (size_t)DBL;
@@ -91,24 +92,19 @@ struct StripCore {
       const int sl = e / (R * R), rem = e - sl * R * R, a = rem / R, b = rem - a * R;
       smem[C::OFF_DC + e] = p.dcorr ? p.dcorr[((size_t)sl * kMaxR + a) * kMaxR + b] : 0.0;
     }
+    // per-lane Toeplitz fragments: x-pass B[k][n] = cx[k - n], y-pass A[m][k] = cy[k - m]
+    // (k = 4 ks + q, n = m = g)
+    for (int e = threadIdx.x; e < 2 * C::KS * 32; e += blockDim.x) {
+      const int which = e / (C::KS * 32), rem = e - which * C::KS * 32;
+      const int ks = rem >> 5, ln = rem & 31;
+      const int t = 4 * ks + (ln & 3) - (ln >> 2);
+      smem[C::OFF_FR + e] = (t >= 0 && t <= 4 * R) ? (which ? p.cy[t] : p.cx[t]) : 0.0;
+    }
     if (threadIdx.x == 0) {
       for (int b = 0; b < 8; ++b) mbar_init(reinterpret_cast<uint64_t*>(smem + C::OFF_BAR) + b, 1);
       mbar_fence_init();
     }
     __syncthreads();
-  }
-
-  // Toeplitz fragments held in registers by every lane: x-pass B[k][n] = cx[k - n],
-  // y-pass A[m][k] = cy[k - m] (k = 4 ks + q, n = m = g)
-  __device__ static void frags(const StripParams& p, double* bx, double* ay) {
-    const int lane = threadIdx.x & 31, g = lane >> 2, q = lane & 3;
-#pragma unroll
-    for (int ks = 0; ks < C::KS; ++ks) {
-      const int t = 4 * ks + q - g;
-      const bool v = t >= 0 && t <= 4 * R;
-      bx[ks] = v ? p.cx[v ? t : 0] : 0.0;
-      ay[ks] = v ? p.cy[v ? t : 0] : 0.0;
-    }
   }
 
   __device__ static void issue(const StripParams& p, double* smem, unsigned slot, int c0, int row0, int s,
@@ -118,10 +114,11 @@ struct StripCore {
     tma_load_3d(smem + C::OFF_IN + slot * 8 * C::PX, src2 ? &p.mapX2 : &p.mapX, bar, c0 - C::H, row0, s);
   }
 
-  // One item: vector s (Y row s, gamma[s]), strip, segment. Returns this thread's X.Y
-  // partial (caller reduces). src2: read the vector from mapX2 (CG confirm).
-  __device__ static double item(const StripParams& p, double* smem, StripRing& ring, const double* bx,
-                                const double* ay, int s, int strip, int seg, bool src2) {
+  // Returns this thread's X.Y partial (caller reduces). src2: read the vector from
+  // mapX2 (CG confirm).
+  // One item: vector s, a strip, output rows [ra, rb) (rb - ra a multiple of 8 unless rb = ny).
+  __device__ static double item(const StripParams& p, double* smem, StripRing& ring, int s, int strip, int ra, int rb,
+                                bool src2) {
     double* IN = smem + C::OFF_IN;
     double* T = smem + C::OFF_T;
     const double* DC = smem + C::OFF_DC;
@@ -129,8 +126,6 @@ struct StripCore {
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, q = lane & 3;
     const int ny = p.ny, nx = p.nx;
-    const int ra = seg * p.seg_rows;
-    const int rb = min(ny, ra + p.seg_rows);
     const int nbo = (rb - ra + 7) >> 3;
     const int nbi = nbo + C::LAG;
     const int c0 = strip * kStripW;
@@ -145,6 +140,12 @@ struct StripCore {
     const bool vec = ((nx & 1) == 0);
     const int cb = warp * 8;
     double dot = 0.0;
+    double bx[C::KS], ay[C::KS];
+#pragma unroll
+    for (int ks = 0; ks < C::KS; ++ks) {
+      bx[ks] = smem[C::OFF_FR + ks * 32 + lane];
+      ay[ks] = smem[C::OFF_FR + (C::KS + ks) * 32 + lane];
+    }
 
     if (tid == 0)
       for (int t = 0; t < C::D && t < nbi; ++t) issue(p, smem, (base + t) & 7u, c0, rb0 + 8 * t, s, src2);
@@ -193,6 +194,18 @@ struct StripCore {
       // every thread is past step t-1: the slot of block t + D (last read at step
       // t + D - 8 + LAG < t) is free
       if (tid == 0 && t + C::D < nbi) issue(p, smem, (base + t + C::D) & 7u, c0, rb0 + 8 * (t + C::D), s, src2);
+      {
+        // the weights of output block t - LAG + 2 into L1 (two steps ahead of their use)
+        const int gi2 = ra + 8 * (t - C::LAG + 2) + g;
+        const int gj2 = c0 + cb + 2 * q;
+        if (gi2 >= ra && gi2 < rb && gj2 < nx) {
+          const int64_t o = (int64_t)gi2 * nx + gj2;
+          prefetch_l1(p.wx + o + (gj2 > 0 ? -1 : 0));
+          prefetch_l1(p.wx + o + 1);
+          prefetch_l1(p.wy + o);
+          if (gi2 > 0) prefetch_l1(p.wy + o - nx);
+        }
+      }
       const int j = t - C::LAG;
       if (j < 0) continue;
       // ---- y-pass of output block j: rows ra + 8j .. +7 from T window rows u = 8j .. 8j+4r+7

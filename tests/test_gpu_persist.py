@@ -117,4 +117,4 @@ def test_persistent_loop_multi_pass_two_groups(torch_dev, monkeypatch, n, r, nL,
     # iterations: reading G27 -- +-2 on >= 95 % of the shifts, +-max(2, 1 %) on all
     # (summation order alone moves counts by up to ~1 % at these condition numbers)
     d_it = np.abs(res["iters"].astype(np.int64) - its)
-    assert np.mean(d_it <= 2) >= 0.95 and np.all(d_it <= np.maximum(2, 0.01 * its)), (res["iters"], its)
+    assert np.mean(d_it <= 2) >= 0.95 and np.all(d_it <= np.maximum(2, np.ceil(0.01 * its))), (res["iters"], its)
