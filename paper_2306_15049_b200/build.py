@@ -30,7 +30,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     cmds = []
     for src in SOURCES:
         obj = os.path.join(HERE, "build", src + ".o")
-        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3",
+        extra = os.environ.get("RSK_NVCC_DEFS", "").split()   # e.g. -DRSK_STRIP_PROF (probes)
+        cmd = [NVCC, *ARCH, "-O3", "-lineinfo", "-std=c++17", *extra, "-Xcompiler", "-fPIC,-O3",
                "-Xptxas", "-v" if verbose else "-O3", "-c", os.path.join(CSRC, src), "-o", obj]
         if src.endswith(".cpp"):
             cmd = [NVCC, "-O3", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-x", "c++", "-c",

@@ -38,6 +38,22 @@ __global__ void __launch_bounds__(kAT, kStripCtasPerSm)
   }
 }
 
+extern "C" int rsk_debug_strip_prof(double* out8, int reset) {
+#ifdef RSK_STRIP_PROF
+  unsigned long long v[8];
+  if (cudaMemcpyFromSymbol(v, g_strip_prof, sizeof(v)) != cudaSuccess) return -1;
+  for (int i = 0; i < 8; ++i) out8[i] = (double)v[i];
+  if (reset) {
+    unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_strip_prof, z, sizeof(z));
+  }
+  return 0;
+#else
+  (void)out8; (void)reset;
+  return -1;
+#endif
+}
+
 __global__ void strip_dot_reduce(const double* part, int ipv, const int* list, double* xdoty) {
   const int li = blockIdx.x;
   const int s = list ? list[li] : li;

@@ -41,7 +41,8 @@ struct StripCfg {
   static constexpr int LAG = (7 + 4 * R) / 8;       // output block j needs T blocks <= j + LAG
   static constexpr int D = (7 - LAG) < 3 ? (7 - LAG) : 3;   // input blocks in flight ahead
   static constexpr int PX = pad4mod8(kStripW + 4 * R);      // input ring pitch (TMA box width)
-  static constexpr int PT = 72;                     // T ring pitch (8 mod 16 doubles)
+  static constexpr int PT = 68;                     // T ring pitch (4 mod 16 doubles: the y-pass B
+                                                    // fragments of a half-warp hit 16 distinct banks)
   static constexpr int OFF_IN = 0;                  // [64][PX] input ring (8 slots x 8 rows)
   static constexpr int OFF_T = OFF_IN + al16(64 * PX);   // [64][PT] x-pass ring
   static constexpr int RING_END = OFF_T + al16(64 * PT);
@@ -280,11 +281,14 @@ struct StripCore {
       const double* xc = IN + ((uc) & 63u) * C::PX + cb + 2 * q + C::H;
       const double* xu = IN + ((uc - 1u) & 63u) * C::PX + cb + 2 * q + C::H;
       const double* xd = IN + ((uc + 1u) & 63u) * C::PX + cb + 2 * q + C::H;
-      const double x0 = xc[0], x1 = xc[1];
+      const double2 xc2 = *reinterpret_cast<const double2*>(xc);   // 16-byte aligned (even offsets)
+      const double x0 = xc2.x, x1 = xc2.y;
       double o0 = e0, o1 = e1;
       if (withE && v0) {
         const double xl = xc[-1], xr = xc[2];
-        const double u0 = xu[0], u1 = xu[1], d0v = xd[0], d1v = xd[1];
+        const double2 xu2 = *reinterpret_cast<const double2*>(xu);
+        const double2 xd2 = *reinterpret_cast<const double2*>(xd);
+        const double u0 = xu2.x, u1 = xu2.y, d0v = xd2.x, d1v = xd2.y;
         const double ex0 = wl * (x0 - xl) - wm * (x1 - x0) + yu0 * (x0 - u0) - yd0 * (d0v - x0);
         const double ex1 = wm * (x1 - x0) - wr * (xr - x1) + yu1 * (x1 - u1) - yd1 * (d1v - x1);
         if (mode == RSK_APPLY_SHIFTED) {
