@@ -8,7 +8,7 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "librsk.so")
-SOURCES = ["apply.cu", "apply_strip.cu", "cg_persist.cu", "cg_stream.cu", "cg_cluster.cu", "vec.cu", "cg_group.cu", "rsk.cu", "minres.cu", "ct.cu", "host_dense.cpp"]
+SOURCES = ["apply.cu", "apply_strip.cu", "apply_rank2.cu", "cg_persist.cu", "cg_stream.cu", "cg_cluster.cu", "vec.cu", "cg_group.cu", "rsk.cu", "minres.cu", "ct.cu", "host_dense.cpp"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

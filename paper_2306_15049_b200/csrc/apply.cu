@@ -199,9 +199,38 @@ bool fill_apply_params(Handle* h, const ApplyLaunch& a, ApplyParams& prm, int ty
   return tma;
 }
 
+cudaError_t launch_apply_taps(Handle* h, const ApplyLaunch& a, const double* cx, const double* cy, int edge_fix,
+                              cudaStream_t st) {
+  if (a.nlist <= 0) return cudaSuccess;
+  if (a.cg || a.xdoty) return cudaErrorNotSupported;
+  ApplyParams prm;
+  const bool tma = fill_apply_params(h, a, prm, std_tile_rows(h->r));
+  const int T = 4 * h->r + 1;
+  for (int t = 0; t < T; ++t) { prm.cx[t] = cx ? cx[t] : 0.0; prm.cy[t] = cy ? cy[t] : 0.0; }
+  prm.edge_fix = edge_fix;
+  prm.want_dot = 0;
+  const int smc = h->sm_count;
+  switch (h->r) {
+    case 1: return launch_r<1>(prm, tma, smc, st);
+    case 2: return launch_r<2>(prm, tma, smc, st);
+    case 3: return launch_r<3>(prm, tma, smc, st);
+    case 4: return launch_r<4>(prm, tma, smc, st);
+    case 5: return launch_r<5>(prm, tma, smc, st);
+    case 6: return launch_r<6>(prm, tma, smc, st);
+    case 7: return launch_r<7>(prm, tma, smc, st);
+    case 8: return launch_r<8>(prm, tma, smc, st);
+    case 9: return launch_r<9>(prm, tma, smc, st);
+    case 10: return launch_r<10>(prm, tma, smc, st);
+    case 11: return launch_r<11>(prm, tma, smc, st);
+    case 12: return launch_r<12>(prm, tma, smc, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
 cudaError_t launch_apply(Handle* h, const ApplyLaunch& a, cudaStream_t st) {
   if (h->ct) return launch_ct_apply(h, a, st);   // CT: sparse C, C^T (ct.cu)
   if (a.nlist <= 0) return cudaSuccess;
+  if (h->rank == 2) return launch_apply_rank2(h, a, st);
   {
     // large images: the streaming strip core (strip_core.cuh); RSK_APPLY_STRIP=0/1 forces
     const char* ev = getenv("RSK_APPLY_STRIP");

@@ -1130,7 +1130,7 @@ extern "C" rsk_status rsk_minres_recycled_batch(rsk_handle h, const rsk_cg_desc*
   std::vector<int> status(ns, ST_ACTIVE), iters(ns, 0), done(ns, 0), final_status(ns, RSK_CG_CONVERGED);
   std::vector<double> relres(ns, 0.0);
   // cluster-per-shift device loop for L2-resident images (as the CG, cg_cluster.cu)
-  bool use_cluster = getenv("RSK_MR_NOCLUSTER") == nullptr && N <= 131072 && h->r >= 1 && !h->ct &&
+  bool use_cluster = getenv("RSK_MR_NOCLUSTER") == nullptr && N <= 131072 && h->r >= 1 && !h->ct && h->rank == 1 &&
                      (N % 2 == 0) && (!store || d->lds % 2 == 0) &&
                      ((reinterpret_cast<uintptr_t>(ws) | reinterpret_cast<uintptr_t>(store ? d->store : ws)) & 15) == 0;
   ApplyParams capx;

@@ -98,7 +98,28 @@ extern "C" rsk_status rsk_create(rsk_handle* out, int device, int64_t ny, int64_
   double res = 0.0;
   for (int i = 0; i < P; ++i)
     for (int j = 0; j < P; ++j) res = std::max(res, std::fabs(psf_h[i * P + j] - u[i] * v[j]));
-  if (res > 1e-13 * hmax) return RSK_EUNSUPPORTED;
+  // rank 2 (Example 1's C = sum_{i=1,2} C_i^(1) (x) C_i^(2)): the two leading
+  // singular triplets of the P x P PSF, h = s1 U1 V1^T + s2 U2 V2^T (one-sided Jacobi SVD)
+  int rank = 1;
+  double u2[2 * kMaxR + 1] = {0}, v2[2 * kMaxR + 1] = {0};
+  if (res > 1e-13 * hmax) {
+    std::vector<double> Hc((size_t)P * P), Us((size_t)P * P), Vs((size_t)P * P), sv(P);
+    for (int i = 0; i < P; ++i)
+      for (int j = 0; j < P; ++j) Hc[i + (size_t)j * P] = psf_h[i * P + j];
+    jacobi_svd(P, Hc.data(), Us.data(), sv.data(), Vs.data());
+    for (int i = 0; i < P; ++i) {
+      u[i] = sv[0] * Us[i];
+      v[i] = Vs[i];
+      u2[i] = sv[1] * Us[i + P];
+      v2[i] = Vs[i + P];
+    }
+    double res2 = 0.0;
+    for (int i = 0; i < P; ++i)
+      for (int j = 0; j < P; ++j)
+        res2 = std::max(res2, std::fabs(psf_h[i * P + j] - u[i] * v[j] - u2[i] * v2[j]));
+    if (res2 > 1e-13 * hmax) return RSK_EUNSUPPORTED;   // rank > 2: no general 2-D path
+    rank = 2;
+  }
 
   rsk_handle h = new (std::nothrow) rsk_handle_s();
   if (!h) return RSK_ENOMEM;
@@ -107,7 +128,8 @@ extern "C" rsk_status rsk_create(rsk_handle* out, int device, int64_t ny, int64_
   h->nx = nx;
   h->ndata = ny * nx;
   h->r = r;
-  for (int i = 0; i < P; ++i) { h->u[i] = u[i]; h->v[i] = v[i]; }
+  for (int i = 0; i < P; ++i) { h->u[i] = u[i]; h->v[i] = v[i]; h->u2[i] = u2[i]; h->v2[i] = v2[i]; }
+  h->rank = rank;
   const int T = 4 * r + 1;
   for (int t = 0; t < kMaxTaps; ++t) {
     h->cBx[t] = h->cBy[t] = h->cCx[t] = h->cCy[t] = h->cTx[t] = h->cTy[t] = 0.0;
@@ -120,11 +142,16 @@ extern "C" rsk_status rsk_create(rsk_handle* out, int device, int64_t ny, int64_
   }
   // C: out[j] = sum_b f[b+r] in[j-b]  ->  t = 2r - b, tap = f[3r - t]   (t in [r, 3r])
   // C^T: out[m] = sum_b f[b+r] in[m+b] ->  t = b + 2r, tap = f[t - r]
+  for (int t = 0; t < kMaxTaps; ++t) h->cCx2[t] = h->cCy2[t] = h->cTx2[t] = h->cTy2[t] = 0.0;
   for (int t = r; t <= 3 * r; ++t) {
     h->cCx[t] = v[3 * r - t];
     h->cCy[t] = u[3 * r - t];
     h->cTx[t] = v[t - r];
     h->cTy[t] = u[t - r];
+    h->cCx2[t] = v2[3 * r - t];
+    h->cCy2[t] = u2[3 * r - t];
+    h->cTx2[t] = v2[t - r];
+    h->cTy2[t] = u2[t - r];
   }
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) { delete h; return RSK_ECUDA; }
@@ -216,6 +243,7 @@ extern "C" rsk_status rsk_slab_info(rsk_handle h, int64_t* info6_h) {
 extern "C" rsk_status rsk_destroy(rsk_handle h) {
   if (!h) return RSK_EINVAL;
   cudaSetDevice(h->device);
+  cudaFree(h->r2buf);
   cudaFree(h->tabBx);
   cudaFree(h->tabBy);
   cudaFree(h->dcorr);
@@ -623,9 +651,9 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
                                             size_t ws_bytes, void* stream) {
   if (!h) return RSK_EINVAL;
   RSK_ARG(d && o, "rsk_cg_recycled_batch: null desc/out");
-  if (h->ct) {
-    h->err = "rsk_cg_recycled_batch: the CG device loops embed the stencil apply; CT handles use "
-             "rsk_minres_recycled_batch";
+  if (h->ct || h->rank != 1) {
+    h->err = "rsk_cg_recycled_batch: the CG device loops embed the rank-1 stencil apply; CT and rank-2 "
+             "handles use rsk_minres_recycled_batch";
     return RSK_EUNSUPPORTED;
   }
   const int ns = d->nshift;

@@ -102,6 +102,13 @@ struct Handle {
   double cBx[kMaxTaps], cBy[kMaxTaps];      // interior taps of B = G^T G
   double cCx[kMaxTaps], cCy[kMaxTaps];      // taps of C   (window form)
   double cTx[kMaxTaps], cTy[kMaxTaps];      // taps of C^T (window form)
+  // rank-2 PSF h = u v^T + u2 v2^T (Example 1's C = sum_i C_i^(1) (x) C_i^(2)):
+  // the second term's C / C^T taps; the fused-apply device loops are rank-1 only
+  int rank = 1;
+  double u2[2 * kMaxR + 1], v2[2 * kMaxR + 1];
+  double cCx2[kMaxTaps], cCy2[kMaxTaps], cTx2[kMaxTaps], cTy2[kMaxTaps];
+  double* r2buf = nullptr;     // rank-2 apply temporaries (3 x vectors x N), grown on demand
+  size_t r2bytes = 0;
   double* tabBx = nullptr;    // [nx][4r+1]
   double* tabBy = nullptr;    // [ny][4r+1]
   double* dcorr = nullptr;    // [4][kMaxR][kMaxR] zero-boundary corner corrections of Bx, By
@@ -152,6 +159,12 @@ struct ApplyLaunch {
   int nvec_total;              // vectors addressable in X (and X2): TMA map extent
 };
 cudaError_t launch_apply(Handle* h, const ApplyLaunch& a, cudaStream_t st);
+// the tiled apply kernel with explicit taps (C / C^T passes of one rank-1 term, or E alone
+// with zero taps); no dot products, no CG mode (apply.cu)
+cudaError_t launch_apply_taps(Handle* h, const ApplyLaunch& a, const double* cx, const double* cy, int edge_fix,
+                              cudaStream_t st);
+// rank-2 PSF handles: the apply as a composition of rank-1 C / C^T passes (apply_rank2.cu)
+cudaError_t launch_apply_rank2(Handle* h, const ApplyLaunch& a, cudaStream_t st);
 // streaming strip apply for large images (apply_strip.cu); cudaErrorNotSupported = not applicable
 constexpr int64_t kStripMinN = 512 * 512;
 cudaError_t launch_apply_strip(Handle* h, const ApplyLaunch& a, cudaStream_t st);

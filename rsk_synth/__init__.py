@@ -62,6 +62,8 @@ class Config:
                                # matrix, Example 2 P:1083-1098) -- SURVEY §8(f) f4
     n_angles: int = 0          # CT: projection angles 1, 2, ..., n_angles degrees
     idx: tuple = ()            # index overrides (i2, i*, I, J_L, J_R, l_c), 1-based; () = rules G11/G36
+    psf_terms: tuple = ()      # rank-2 PSF of Example 1: ((band_x, sigma_x, band_y,
+                               # sigma_y), ...) per Kronecker term; () = one Gaussian (r, sigma)
 
     @property
     def N(self) -> int:
@@ -93,7 +95,32 @@ CONFIGS = {
     # 9 outer steps; n_c, |J|, tau, tol as C2 (readings G38)
     "C6": Config("C6", 6, 82, 20, 1e-8, 1e2, 0, 0.0, 0.01, 40, 8, 9, 1e-3, 1e-8, "alternate", 16,
                  operator="ct", n_angles=135, idx=(10, 12, 16, 15, 19, 19)),
+    # Example 1 (§8.2, reading G40): 128 x 128, rank-2 blur
+    # C = sum_{i=1,2} C_i^(1) (x) C_i^(2), Toeplitz bandwidths 8, 7, 12, 4 and sigma 3, 5/2,
+    # 4, 2 (C_i^(1) along x, C_i^(2) along y; bandwidth b = half-width b - 1, Regtools'
+    # blur), 0.5 % noise, 20 lambda log-spaced in [1e-4, 10^2.5] (gamma = lambda^2), I = 15,
+    # i1 = 1, i2 = i* = 10, J_L = 15, J_R = 19, l_c = 18, 12 local Ritz vectors, principal
+    # space 100 + 50 Ritz vectors + 2 solutions (n_c = 152), inner relres 1e-6,
+    # the paper's own method: recycling MINRES, sequential local spaces, V^(new), Gazzola's
+    # weights, stop on 3 equal l* (at most 11 outer steps)
+    "C7": Config("C7", 7, 128, 20, 1e-8, 10.0 ** 5, 11, 0.0, 0.005, 152, 12, 11, 1e-3, 1e-6, "rects", 20,
+                 weight_rule="gazzola", stop="lstar3", inner="minres", local="seq", principal="vnew",
+                 idx=(10, 10, 15, 15, 19, 18), psf_terms=((8, 3.0, 7, 2.5), (12, 4.0, 4, 2.0))),
 }
+
+
+def kronecker_psf(terms) -> np.ndarray:
+    """h = sum_i u_i v_i^T / total for Toeplitz factors with Regtools' blur shape (band b:
+    entries exp(-k^2 / (2 sigma^2)) for |k| <= b - 1): v_i along x (columns, C_i^(1)),
+    u_i along y (rows, C_i^(2)); centred in the (2r+1)^2 window, r = max band - 1, sum 1."""
+    r = max(max(bx, by) for bx, _, by, _ in terms) - 1
+    a = np.arange(-r, r + 1, dtype=np.float64)
+    h = np.zeros((2 * r + 1, 2 * r + 1))
+    for bx, sx, by, sy in terms:
+        v = np.where(np.abs(a) <= bx - 1, np.exp(-a ** 2 / (2.0 * sx * sx)), 0.0)
+        u = np.where(np.abs(a) <= by - 1, np.exp(-a ** 2 / (2.0 * sy * sy)), 0.0)
+        h += np.outer(u, v)
+    return h / h.sum()
 
 
 def small_config(n: int = 16, M: int = 6, r: int = 2, sigma: float = 1.0, n_c: int = 8,
@@ -183,7 +210,7 @@ def make_inputs(cfg: Config) -> dict:
     xi = rng.standard_normal((cfg.n, cfg.n))
     return {
         "x_true": np.ascontiguousarray(x_true),
-        "psf": gaussian_psf(cfg.r, cfg.sigma),
+        "psf": kronecker_psf(cfg.psf_terms) if cfg.psf_terms else gaussian_psf(cfg.r, cfg.sigma),
         "xi": np.ascontiguousarray(xi),
         "gamma": gamma_ladder(cfg),
     }

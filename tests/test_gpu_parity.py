@@ -395,3 +395,57 @@ def test_set_weights_rejects_invalid(torch_dev):
     h.apply_shifted(X, A1, EY=E1, mode=L.RSK_APPLY_SPLIT)
     torch.cuda.synchronize()
     assert torch.equal(E0, E1) and len(bad) == 5
+
+
+@pytest.mark.parametrize("n", [128, 75])
+def test_apply_rank2_psf_all_modes(torch_dev, n):
+    """Rank-2 PSF (Example 1's C = sum_i C_i^(1) (x) C_i^(2), config C7): rsk_create finds
+    the two separable terms; every apply mode against the oracle's literal 2-D conv."""
+    torch, dev = torch_dev
+    from paper_2306_15049_b200 import _lib as L
+    psf = S.make_inputs(S.CONFIGS["C7"])["psf"]
+    h = _handle(n, psf)
+    wx, wy = S.random_weights(500 + n, n)
+    h.set_weights(_t(torch, dev, wx.ravel()), _t(torch, dev, wy.ravel()))
+    nv = 3
+    X = S.random_vectors(600 + n, (nv, n * n))
+    gam = np.array([0.0, 1e-3, 40.0])
+    Xd = _t(torch, dev, X)
+    Y = torch.empty_like(Xd); AY = torch.empty_like(Xd); EY = torch.empty_like(Xd)
+    Yc = torch.empty_like(Xd); Yt = torch.empty_like(Xd)
+    xy = torch.empty(nv, dtype=torch.float64, device=dev)
+    h.apply_shifted(Xd, Y, gamma=_t(torch, dev, gam), xdoty=xy)
+    h.apply_shifted(Xd, AY, EY=EY, mode=L.RSK_APPLY_SPLIT)
+    h.apply_shifted(Xd, Yc, mode=L.RSK_APPLY_C_ONLY)
+    h.apply_shifted(Xd, Yt, mode=L.RSK_APPLY_CT_ONLY)
+    torch.cuda.synchronize()
+    for s in range(nv):
+        x = X[s].reshape(n, n)
+        ref = ops.apply_shifted(psf, wx, wy, gam[s], x)
+        assert _rel_inf(Y[s].cpu().numpy().reshape(n, n), ref) <= 1e-13
+        assert _rel_inf(AY[s].cpu().numpy().reshape(n, n), ops.apply_A(psf, x)) <= 1e-13
+        assert _rel_inf(EY[s].cpu().numpy().reshape(n, n), ops.apply_E(wx, wy, x)) <= 1e-13
+        assert _rel_inf(Yc[s].cpu().numpy().reshape(n, n), ops.conv(psf, x)) <= 1e-13
+        assert _rel_inf(Yt[s].cpu().numpy().reshape(n, n), ops.conv_t(psf, x)) <= 1e-13
+        assert abs(float(xy[s]) - float(np.sum(x * ref))) <= 1e-13 * float(np.sum(np.abs(x) * np.abs(ref)))
+
+
+def test_rank3_psf_unsupported_and_rank2_cg_refused(torch_dev):
+    torch, dev = torch_dev
+    from paper_2306_15049_b200 import _lib as L
+    from paper_2306_15049_b200.rsk import RskError
+    rng = np.random.default_rng(3)
+    h3 = rng.random((7, 7))           # generic: rank 7
+    with pytest.raises(RskError):
+        _handle(40, h3)
+    cfg = S.CONFIGS["C7"]
+    import dataclasses
+    cfg = dataclasses.replace(cfg, n=48, M=4, inner="cg")
+    from paper_2306_15049_b200.pipeline import GpuSolver
+    inp = S.make_inputs(S.CONFIGS["C7"])
+    sol = GpuSolver(cfg, inp["psf"], np.logspace(-3, 0, 4))
+    sol.reset_weights()
+    X = torch.zeros(4, cfg.N, dtype=torch.float64, device=dev)
+    with pytest.raises(RskError) as ei:
+        sol.cg(list(range(4)), X, [0] * 4)
+    assert ei.value.status == L.RSK_EUNSUPPORTED

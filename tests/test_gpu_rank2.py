@@ -1,0 +1,53 @@
+"""The Example-1-shaped workload (config C7, rank-2 blur, reading G40) end to end on the
+GPU against the oracle, stepwise (reading G28): outer step k = 0 with the recycling MINRES
+batch (the rank-2 apply composition of apply_rank2.cu inside it), both sides at relres
+1e-10; the local spaces [W_g, g-hat] (D3) so the oracle's per-shift solves run in parallel.
+Bars as the C1 / C2 stepwise tests (reading G27)."""
+import dataclasses
+import os
+
+import numpy as np
+import pytest
+
+import rsk_synth as S
+from oracle import operators as ops
+from oracle import pipeline as opipe
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def torch_dev():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA")
+    return torch, torch.device("cuda", 0)
+
+
+def _t(torch, dev, a):
+    return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
+
+
+def test_c7_outer_step_k0(torch_dev):
+    torch, dev = torch_dev
+    from paper_2306_15049_b200.pipeline import GpuSolver
+    cfg = dataclasses.replace(S.CONFIGS["C7"], tol=1e-10, local="d3", principal="g10", n_c=60)
+    inp = S.make_inputs(cfg)
+    n, M = cfg.n, cfg.M
+    h = inp["psf"]
+    d, b2 = ops.make_data(h, inp["x_true"], inp["xi"], cfg.noise)
+    wx, wy = ops.identity_weights(n)
+    rs = opipe.outer_step(cfg, h, b2.ravel(), d, inp["gamma"], opipe.StepState(0, wx, wy, None, None, None),
+                          workers=max(1, min(16, os.cpu_count() or 1)))
+    sol = GpuSolver(cfg, h, inp["gamma"], check_every=8)
+    sol.set_data(_t(torch, dev, inp["x_true"]), _t(torch, dev, inp["xi"]))
+    assert np.max(np.abs(sol.b.cpu().numpy() - b2.ravel())) <= 1e-13 * np.max(np.abs(b2))
+    sol.reset_weights()
+    o, X = sol.outer_step(0, {})
+    assert o.nc == rs.nc and o.lstar == rs.lstar, (o.nc, rs.nc, o.lstar, rs.lstar)
+    assert np.all(o.status == 0) and np.all(rs.status == 0)
+    d_it = np.abs(o.iters - rs.iters)
+    assert np.mean(d_it <= 2) >= 0.95 and np.all(d_it <= np.maximum(2, np.ceil(0.01 * rs.iters))), (o.iters, rs.iters)
+    Xg = X["X_prev"].cpu().numpy()
+    rel = [np.linalg.norm(Xg[l] - rs.X[:, l]) / np.linalg.norm(rs.X[:, l]) for l in range(M)]
+    assert np.mean(np.array(rel) <= 1e-8) >= 0.9 and max(rel) <= 1e-6, rel
