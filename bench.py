@@ -427,7 +427,8 @@ def run_ours(args, cfg, rank, world):
             "gpu_launches": int(launches),
             "roofline": {"bound": "hbm",
                          "kernel": {1: "cg_cluster_kernel (cluster-per-shift deflated CG loop)",
-                                    2: "cg_persist_kernel (persistent lockstep deflated CG loop)"}.get(kind, "host-polled loop"),
+                                    2: "cg_persist_kernel (tiled persistent lockstep deflated CG loop)",
+                                    3: "cg_stream_kernel (streaming persistent lockstep deflated CG loop)"}.get(kind, "host-polled loop"),
                          "achieved": achieved, "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": (achieved / pk["hbm_gbs"]) if achieved else None, "traffic": traffic,
                          "peak_src": pk["hbm_src"],
@@ -441,6 +442,66 @@ def run_ours(args, cfg, rank, world):
             "cpu_baseline": cpu,
         }
         print(json.dumps(line), flush=True)
+
+
+def run_slab(args, cfg, rank, world):
+    """C5 across G GPUs as row slabs: every rank holds its rows (+ 2r halo)
+    of all 16 shifts; halo exchange and the all-reduced dot products over NCCL
+    (slab.DistComm). A step = outer step k = 0 of the nested solve (seed solves, Ritz,
+    stabilize, anchoring, guesses, group blocks, batched deflated CG, L-curve)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2306_15049_b200 import _lib as L
+    from paper_2306_15049_b200.slab import DistComm, SlabGpuSolver, SlabPlan
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    lib = L.load()
+    inputs = S.make_inputs(cfg)
+    plan = SlabPlan(cfg.n, cfg.n, cfg.r, world)
+    sol = SlabGpuSolver(cfg, inputs["psf"], inputs["gamma"], plan, rank, DistComm(plan, rank), device=local)
+    x_true = torch.from_numpy(inputs["x_true"]).to(dev)
+    xi = torch.from_numpy(inputs["xi"]).to(dev)
+
+    def step():
+        sol.set_data(x_true, xi)
+        sol.reset_weights()
+        o, _ = sol.outer_step(0, {})
+        return o
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    dist.barrier()
+    stream = torch.cuda.current_stream(dev)
+    ms = 0.0
+    ap = sv = conv = 0
+    l0 = lib.rsk_launch_count()
+    with ClockSampler(local) as clk:
+        for i in range(args.steps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            o = step()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            ms += e0.elapsed_time(e1)
+            ap += int(o.applies.sum()) + o.overhead_applies
+            sv += int(o.applies.size)
+            conv += int(np.isin(o.status, CONVERGED).sum())
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    if rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": ap / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": cfg.name, "n": cfg.n, "N": cfg.N, "shifts": cfg.M, "step": "outer step k=0",
+                       "parallelism": f"row slabs x{world} (NCCL halo exchange + all-reduced dots)",
+                       "l2": "working set > L2"},
+            "solves_per_s": sv / (ms / 1e3), "converged": f"{conv}/{sv}",
+            "gpu_launches": int(lib.rsk_launch_count() - l0), "clocks": clk.summary(),
+        }), flush=True)
 
 
 def main():
@@ -479,7 +540,10 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group(os.environ.get("RSK_BENCH_BACKEND", "nccl"))
-    run_ours(args, cfg, rank, world)
+    if world > 1 and cfg.name == "C5":
+        run_slab(args, cfg, rank, world)
+    else:
+        run_ours(args, cfg, rank, world)
     if world > 1:
         import torch.distributed as dist
         dist.destroy_process_group()

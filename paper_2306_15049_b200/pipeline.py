@@ -232,9 +232,11 @@ class GpuSolver:
         return self.combine(Q, Z[:, :kk]), q
 
     # ------------------------------------------------------------- one outer step
-    def _principal(self, k: int, st: dict):
-        """Rank-0 part of the outer step: raw block, stabilize (Alg. 1) and the anchor
-        images A U~, E U~ (n_c split applies). Returns (Ut, ZA, ZE, V_i1, overhead)."""
+    def _principal(self, k: int, st: dict, images: bool = True):
+        """Rank-0 part of the outer step: raw block, stabilize (Alg. 1) and (images=True)
+        the anchor images A U~, E U~ (n_c split applies; with several ranks they are
+        column-split across the ranks instead, see outer_step).
+        Returns (Ut, ZA, ZE, V_i1, overhead)."""
         cfg = self.cfg
         N, nc_cap = self.N, cfg.n_c
         overhead = 0
@@ -262,10 +264,12 @@ class GpuSolver:
         Ut = self.stabilize(raw, nc_cap)
         nc = Ut.shape[0]
         del raw
+        overhead += nc
+        if not images:
+            return Ut, None, None, V_i1, overhead
         ZA = torch.empty(nc, N, **self.f)
         ZE = torch.empty(nc, N, **self.f)
         self.h.apply_shifted(Ut, ZA, EY=ZE, mode=L.RSK_APPLY_SPLIT, stream=self.stream)
-        overhead += nc
         return Ut, ZA, ZE, V_i1, overhead
 
     def principal_update(self, st: dict):
@@ -296,23 +300,32 @@ class GpuSolver:
         N, M = self.N, self.M
         dist = self.dist
         t0 = time.perf_counter()
-        owners = shard.assignment(k, M, dist.world, st.get("prev_iters"))
+        owners = shard.assignment(k, M, dist.world, st.get("prev_iters"), groups=self.grp, J=cfg.J)
         mine = owners[dist.rank]
         ml = len(mine)
         # ---- principal space on rank 0, broadcast once per outer step (§8(e1))
         V_i1 = st.get("V_i1")
         overhead = 0
         if dist.rank == 0:
-            Ut, ZA, ZE, V_i1, overhead = self._principal(k, st)
+            Ut, ZA, ZE, V_i1, overhead = self._principal(k, st, images=not dist.enabled)
             nc = Ut.shape[0]
         nc = dist.bcast_int(nc if dist.rank == 0 else 0, self.dev)
         if dist.rank != 0:
             Ut = torch.empty(nc, N, **self.f)
-            ZA = torch.empty(nc, N, **self.f)
-            ZE = torch.empty(nc, N, **self.f)
         if dist.enabled:
+            # U~ from rank 0; the n_c anchoring applies A U~, E U~ column-split across the
+            # ranks (contiguous blocks), then all-gathered
             torch.cuda.synchronize(self.dev)
-            dist.bcast(Ut); dist.bcast(ZA); dist.bcast(ZE)
+            dist.bcast(Ut)
+            cols = [list(range(r * nc // dist.world, (r + 1) * nc // dist.world)) for r in range(dist.world)]
+            mc = cols[dist.rank]
+            za = torch.empty(len(mc), N, **self.f)
+            ze = torch.empty(len(mc), N, **self.f)
+            if mc:
+                self.h.apply_shifted(Ut[mc[0]:mc[-1] + 1], za, EY=ze, mode=L.RSK_APPLY_SPLIT, stream=self.stream)
+            torch.cuda.synchronize(self.dev)
+            ZA = dist.gather_rows(za, cols, nc)
+            ZE = dist.gather_rows(ze, cols, nc)
         # ---- anchoring (eq:establishU) and Grams: identical on every rank
         gstar = float(self.gamma[shift_indices(cfg).istar - 1])
         Y = ZA.clone()

@@ -11,14 +11,17 @@ step suffices and the CG loop has no per-iteration communication:
   allgather  X^(k), G^(k) (M x N each), iteration counts, L-curve norms
   all ranks  L-curve corner and IRN weights (identical)
 
-Assignment: outer step 0 deals the ladder round-robin; later steps use greedy LPT on
-the previous step's per-shift iteration counts (the cost model of SURVEY §8(e)),
-ties broken by shift index, so every rank computes the same assignment.
+Assignment: outer step 0 deals the ladder round-robin; later steps use the group-aware
+LPT of group_lpt_assign on the previous step's per-shift iteration counts (the cost
+model of SURVEY §8(e)), ties broken by shift index, so every rank computes the same
+assignment.
 
-Per-shift arithmetic does not depend on the batch a shift shares (fixed launch
-geometry, per-shift reductions), so a G-rank run reproduces the 1-rank solutions
-bit for bit. This module holds only host logic and collectives; it works on CPU
-tensors under gloo (tests) and on CUDA tensors under NCCL (bench).
+The cluster-per-shift loop (images in L2) computes each shift independently of the
+batch it shares, so a G-rank run reproduces the 1-rank solutions bit for bit there; the
+lockstep loops for larger images sum some partials per CTA range of the whole batch, so
+their solutions agree to rounding (iterations within the stepwise bars), not bitwise.
+This module holds only host logic and collectives; it works on CPU tensors under gloo
+(tests) and on CUDA tensors under NCCL (bench).
 """
 from __future__ import annotations
 
@@ -44,11 +47,46 @@ def lpt_assign(costs, world: int) -> list[list[int]]:
     return [sorted(x) for x in out]
 
 
-def assignment(k: int, M: int, world: int, prev_iters=None) -> list[list[int]]:
+def group_lpt_assign(iters, groups, world: int, J: int = 12, S_ref: float = 80.0) -> list[list[int]]:
+    """Group-aware assignment: a GPU holding shifts of a group re-reads that
+    group's W, AW, EW (24|J| B/px) every lockstep iteration while any of them is active, so
+    groups are kept apart. Cost model per shift-iteration: S_ref = 80 B/px of per-shift
+    vectors; per GPU and group touched: the longest of its shifts x 24|J| B/px. GPUs go to
+    the groups in proportion to the groups' predicted bytes (>= 1 each), shifts to the GPUs
+    of their group by LPT; with fewer GPUs than groups, plain LPT. Deterministic."""
+    iters = np.asarray(iters, dtype=np.float64)
+    groups = np.asarray(groups)
+    gids = sorted(set(groups.tolist()))
+    if world < len(gids) or len(gids) < 2:
+        return lpt_assign(iters, world)
+    cost = {g: S_ref * float(np.sum(iters[groups == g] + 1)) + 24.0 * J * float(np.max(iters[groups == g]) + 1)
+            for g in gids}
+    total = sum(cost.values())
+    # largest-remainder apportionment of the GPUs, at least one per group
+    share = {g: max(1, int(np.floor(world * cost[g] / total))) for g in gids}
+    while sum(share.values()) > world:
+        g = max(gids, key=lambda x: (share[x], -cost[x]))
+        share[g] -= 1
+    rem = sorted(gids, key=lambda g: (-(world * cost[g] / total - share[g]), g))
+    i = 0
+    while sum(share.values()) < world:
+        share[rem[i % len(rem)]] += 1
+        i += 1
+    out: list[list[int]] = []
+    for g in gids:
+        idx = [int(l) for l in np.nonzero(groups == g)[0]]
+        sub = lpt_assign(iters[idx], share[g])
+        out.extend([[idx[j] for j in o] for o in sub])
+    return [sorted(o) for o in out]
+
+
+def assignment(k: int, M: int, world: int, prev_iters=None, groups=None, J: int = 12) -> list[list[int]]:
     if world == 1:
         return [list(range(M))]
     if k == 0 or prev_iters is None:
         return round_robin(M, world)
+    if groups is not None:
+        return group_lpt_assign(prev_iters, groups, world, J)
     return lpt_assign(prev_iters, world)
 
 

@@ -83,3 +83,22 @@ def test_gloo_world2_gather_and_broadcast():
     for p in ps:
         p.join(timeout=60)
     assert all(all(r[1:]) for r in res), res
+
+
+def test_group_aware_assignment_keeps_groups_apart():
+    """prefer group-pure GPUs, GPUs to groups in proportion to their work."""
+    rng = np.random.default_rng(4)
+    M, W = 128, 8
+    groups = np.array([0 if l < 96 else 1 for l in range(M)])
+    its = np.where(groups == 0, rng.integers(300, 1100, M), rng.integers(700, 20000, M))
+    owners = shard.group_lpt_assign(its, groups, W)
+    assert sorted(l for o in owners for l in o) == list(range(M)) and len(owners) == W
+    assert all(len(set(groups[o].tolist())) == 1 for o in owners if o)       # group-pure
+    nR = sum(1 for o in owners if o and groups[o[0]] == 1)
+    costR = 80 * (its[groups == 1] + 1).sum()
+    costL = 80 * (its[groups == 0] + 1).sum()
+    assert nR >= round(W * costR / (costR + costL)) - 1 and nR >= 1
+    assert shard.group_lpt_assign(its, groups, W) == owners                   # deterministic
+    # fewer GPUs than groups: plain LPT
+    assert shard.group_lpt_assign(its, groups, 1) == [list(range(M))]
+    assert shard.assignment(1, M, W, its, groups=groups) == owners
