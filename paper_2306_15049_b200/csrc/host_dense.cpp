@@ -44,129 +44,111 @@ void chol_solve_lower(int n, const double* L, double* x) {
   }
 }
 
-// Cyclic Jacobi on sym(H); eigenvalues ascending, eigenvectors in columns of V.
-// Symmetric eigendecomposition by Householder tridiagonalisation + implicit-shift QL
-// (the EISPACK tred2 / tql2 pair; O(n^3) once instead of Jacobi's O(n^3) per sweep).
-// a (n x n, row-major z[i][j] = a[i*n+j]) is overwritten by the eigenvectors (columns),
-// d receives the eigenvalues (unsorted). Returns false if QL did not converge.
-static bool tred2_tql2(int n, std::vector<double>& z, std::vector<double>& d) {
-  std::vector<double> e(n, 0.0);
+// Symmetric eigendecomposition (Golub & Van Loan, Matrix Computations, 4th ed., §8.3):
+// Householder tridiagonalisation Q^T A Q = T, then implicit symmetric QR steps with the
+// Wilkinson shift on T (bulge chasing by Givens rotations, accumulated into Q); O(n^3)
+// once instead of cyclic Jacobi's O(n^3) per sweep. A: n x n column-major (symmetric).
+// On return d = eigenvalues (unsorted), Q = eigenvectors (columns, column-major).
+// Returns false if the QR iteration does not converge (the caller falls back to Jacobi).
+static bool sym_tridiag_qr(int n, std::vector<double>& A, std::vector<double>& Q, std::vector<double>& d) {
+  auto a = [&](int i, int j) -> double& { return A[(size_t)i + (size_t)j * n]; };
+  auto qq = [&](int i, int j) -> double& { return Q[(size_t)i + (size_t)j * n]; };
+  Q.assign((size_t)n * n, 0.0);
+  for (int i = 0; i < n; ++i) qq(i, i) = 1.0;
+  std::vector<double> v(n), p(n), w(n);
+  for (int k = 0; k + 2 < n; ++k) {
+    // reflector H = I - beta v v^T with H x = alpha e_1, x = A[k+1:, k]
+    double xn = 0.0;
+    for (int i = k + 1; i < n; ++i) xn += a(i, k) * a(i, k);
+    xn = std::sqrt(xn);
+    if (xn == 0.0) continue;
+    const double x0 = a(k + 1, k);
+    const double alpha = x0 >= 0.0 ? -xn : xn;
+    for (int i = k + 1; i < n; ++i) v[i] = a(i, k);
+    v[k + 1] -= alpha;
+    double vv = 0.0;
+    for (int i = k + 1; i < n; ++i) vv += v[i] * v[i];
+    if (vv == 0.0) continue;
+    const double beta = 2.0 / vv;
+    // trailing block: A <- H A H = A - v q^T - q v^T, p = beta A v, q = p - (beta v^T p / 2) v
+    double vp = 0.0;
+    for (int i = k + 1; i < n; ++i) {
+      double t = 0.0;
+      for (int j2 = k + 1; j2 < n; ++j2) t += a(i, j2) * v[j2];
+      p[i] = beta * t;
+      vp += v[i] * p[i];
+    }
+    const double kk = 0.5 * beta * vp;
+    for (int i = k + 1; i < n; ++i) w[i] = p[i] - kk * v[i];
+    for (int j2 = k + 1; j2 < n; ++j2)
+      for (int i = k + 1; i < n; ++i) a(i, j2) -= v[i] * w[j2] + w[i] * v[j2];
+    a(k + 1, k) = a(k, k + 1) = alpha;
+    for (int i = k + 2; i < n; ++i) a(i, k) = a(k, i) = 0.0;
+    // Q <- Q H
+    for (int i = 0; i < n; ++i) {
+      double t = 0.0;
+      for (int j2 = k + 1; j2 < n; ++j2) t += qq(i, j2) * v[j2];
+      t *= beta;
+      for (int j2 = k + 1; j2 < n; ++j2) qq(i, j2) -= t * v[j2];
+    }
+  }
   d.assign(n, 0.0);
-  auto Z = [&](int i, int j) -> double& { return z[(size_t)i * n + j]; };
-  for (int i = n - 1; i > 0; --i) {
-    const int l = i - 1;
-    double h = 0.0, scale = 0.0;
-    if (l > 0) {
-      for (int k = 0; k <= l; ++k) scale += std::fabs(Z(i, k));
-      if (scale == 0.0) {
-        e[i] = Z(i, l);
-      } else {
-        for (int k = 0; k <= l; ++k) {
-          Z(i, k) /= scale;
-          h += Z(i, k) * Z(i, k);
-        }
-        double f = Z(i, l);
-        double g = (f >= 0.0) ? -std::sqrt(h) : std::sqrt(h);
-        e[i] = scale * g;
-        h -= f * g;
-        Z(i, l) = f - g;
-        f = 0.0;
-        for (int j = 0; j <= l; ++j) {
-          Z(j, i) = Z(i, j) / h;
-          g = 0.0;
-          for (int k = 0; k <= j; ++k) g += Z(j, k) * Z(i, k);
-          for (int k = j + 1; k <= l; ++k) g += Z(k, j) * Z(i, k);
-          e[j] = g / h;
-          f += e[j] * Z(i, j);
-        }
-        const double hh = f / (h + h);
-        for (int j = 0; j <= l; ++j) {
-          f = Z(i, j);
-          e[j] = g = e[j] - hh * f;
-          for (int k = 0; k <= j; ++k) Z(j, k) -= (f * e[k] + g * Z(i, k));
-        }
-      }
-    } else {
-      e[i] = Z(i, l);
+  std::vector<double> e(n > 1 ? n - 1 : 1, 0.0);
+  for (int i = 0; i < n; ++i) d[i] = a(i, i);
+  for (int i = 0; i + 1 < n; ++i) e[i] = a(i + 1, i);
+  const double eps = 1e-16;
+  int m = n - 1, iter = 0;
+  while (m > 0) {
+    if (std::fabs(e[m - 1]) <= eps * (std::fabs(d[m - 1]) + std::fabs(d[m]))) {
+      e[m - 1] = 0.0;
+      --m;
+      continue;
     }
-    d[i] = h;
-  }
-  d[0] = 0.0;
-  e[0] = 0.0;
-  for (int i = 0; i < n; ++i) {
-    const int l = i - 1;
-    if (d[i] != 0.0) {
-      for (int j = 0; j <= l; ++j) {
-        double g = 0.0;
-        for (int k = 0; k <= l; ++k) g += Z(i, k) * Z(k, j);
-        for (int k = 0; k <= l; ++k) Z(k, j) -= g * Z(k, i);
+    int l = m - 1;
+    while (l > 0 && std::fabs(e[l - 1]) > eps * (std::fabs(d[l - 1]) + std::fabs(d[l]))) --l;
+    if (++iter > 60 * n) return false;
+    // Wilkinson shift from the trailing 2 x 2 block of T[l..m]
+    const double dd = 0.5 * (d[m - 1] - d[m]);
+    const double em = e[m - 1];
+    const double mu = d[m] - em * em / (dd + (dd >= 0.0 ? 1.0 : -1.0) * std::hypot(dd, em));
+    double x = d[l] - mu, z = e[l], bulge = 0.0;
+    for (int k = l; k < m; ++k) {
+      const double r = std::hypot(x, z);
+      const double c = r == 0.0 ? 1.0 : x / r, s2 = r == 0.0 ? 0.0 : z / r;
+      if (k > l) e[k - 1] = r;                       // the bulge at (k-1, k+1) is annihilated
+      const double dk = d[k], dk1 = d[k + 1], ek = e[k];
+      d[k] = c * c * dk + 2.0 * c * s2 * ek + s2 * s2 * dk1;
+      d[k + 1] = s2 * s2 * dk - 2.0 * c * s2 * ek + c * c * dk1;
+      e[k] = c * s2 * (dk1 - dk) + (c * c - s2 * s2) * ek;
+      if (k + 1 < m) {                               // new bulge at (k, k+2)
+        bulge = s2 * e[k + 1];
+        e[k + 1] *= c;
       }
+      for (int i = 0; i < n; ++i) {                  // Q <- Q G^T on columns k, k+1
+        const double qk = qq(i, k), qk1 = qq(i, k + 1);
+        qq(i, k) = c * qk + s2 * qk1;
+        qq(i, k + 1) = -s2 * qk + c * qk1;
+      }
+      x = e[k];
+      z = bulge;
     }
-    d[i] = Z(i, i);
-    Z(i, i) = 1.0;
-    for (int j = 0; j <= l; ++j) Z(j, i) = Z(i, j) = 0.0;
-  }
-  // QL with implicit shifts on (d, e)
-  for (int i = 1; i < n; ++i) e[i - 1] = e[i];
-  e[n - 1] = 0.0;
-  for (int l = 0; l < n; ++l) {
-    int iter = 0, m;
-    do {
-      for (m = l; m < n - 1; ++m) {
-        const double dd = std::fabs(d[m]) + std::fabs(d[m + 1]);
-        if (std::fabs(e[m]) <= 1e-16 * dd) break;
-      }
-      if (m != l) {
-        if (iter++ == 60) return false;
-        double g = (d[l + 1] - d[l]) / (2.0 * e[l]);
-        double r = std::hypot(g, 1.0);
-        g = d[m] - d[l] + e[l] / (g + (g >= 0.0 ? std::fabs(r) : -std::fabs(r)));
-        double s = 1.0, c = 1.0, p = 0.0;
-        int i;
-        for (i = m - 1; i >= l; --i) {
-          double f = s * e[i];
-          const double b = c * e[i];
-          e[i + 1] = (r = std::hypot(f, g));
-          if (r == 0.0) {
-            d[i + 1] -= p;
-            e[m] = 0.0;
-            break;
-          }
-          s = f / r;
-          c = g / r;
-          g = d[i + 1] - p;
-          r = (d[i] - g) * s + 2.0 * c * b;
-          d[i + 1] = g + (p = s * r);
-          g = c * r - b;
-          for (int k = 0; k < n; ++k) {
-            f = Z(k, i + 1);
-            Z(k, i + 1) = s * Z(k, i) + c * f;
-            Z(k, i) = c * Z(k, i) - s * f;
-          }
-        }
-        if (r == 0.0 && i >= l) continue;
-        d[l] -= p;
-        e[l] = g;
-        e[m] = 0.0;
-      }
-    } while (m != l);
   }
   return true;
 }
 
 void jacobi_eig(int n, const double* H, double* theta, double* V) {
-  // fast path: Householder + QL; cyclic Jacobi below only if QL does not converge
+  // fast path: Householder + implicit QR; cyclic Jacobi below only if QR does not converge
   {
-    std::vector<double> z((size_t)n * n), d;
-    for (int i = 0; i < n; ++i)
-      for (int j = 0; j < n; ++j) z[(size_t)i * n + j] = 0.5 * (H[i + j * n] + H[j + i * n]);
-    if (n >= 2 && tred2_tql2(n, z, d)) {
+    std::vector<double> Az((size_t)n * n), Qz, d;
+    for (int j = 0; j < n; ++j)
+      for (int i = 0; i < n; ++i) Az[(size_t)i + (size_t)j * n] = 0.5 * (H[i + j * n] + H[j + i * n]);
+    if (n >= 2 && sym_tridiag_qr(n, Az, Qz, d)) {
       std::vector<int> idx(n);
       std::iota(idx.begin(), idx.end(), 0);
       std::stable_sort(idx.begin(), idx.end(), [&](int a, int b) { return d[a] < d[b]; });
       for (int j = 0; j < n; ++j) {
         theta[j] = d[idx[j]];
-        for (int i = 0; i < n; ++i) V[i + j * n] = z[(size_t)i * n + idx[j]];
+        for (int i = 0; i < n; ++i) V[i + j * n] = Qz[(size_t)i + (size_t)idx[j] * n];
       }
       return;
     }
@@ -236,12 +218,7 @@ void jacobi_svd(int k, const double* R, double* Ur, double* s, double* Vr) {
   std::vector<double> A(R, R + (size_t)k * k);
   std::vector<int> perm(k);
   std::iota(perm.begin(), perm.end(), 0);
-  std::vector<double> tau(k, 0.0), cn(k);
-  for (int j = 0; j < k; ++j) {
-    double t = 0.0;
-    for (int i = 0; i < k; ++i) t += A[i + (size_t)j * k] * A[i + (size_t)j * k];
-    cn[j] = t;
-  }
+  std::vector<double> tau(k, 0.0);
   for (int j = 0; j < k; ++j) {
     // pivot: the remaining column of largest norm (recomputed: k is small)
     int pj = j;
@@ -293,6 +270,37 @@ void jacobi_svd(int k, const double* R, double* Ur, double* s, double* Vr) {
     for (int i = 0; i <= j; ++i) X[j + (size_t)i * k] = A[i + (size_t)j * k];
   std::vector<double> Ux((size_t)k * k), sx(k), Vx((size_t)k * k);
   jacobi_svd_plain(k, X.data(), Ux.data(), sx.data(), Vx.data());   // X = Ux S Vx^T
+  // left vectors of zero singular values are not defined by X V = U S: complete Ux to an
+  // orthonormal basis (Gram-Schmidt of unit vectors against the kept columns, twice) so
+  // that Vr = P Ux is orthogonal for rank-deficient R too
+  {
+    std::vector<int> good(k, 0);
+    for (int j = 0; j < k; ++j) good[j] = sx[j] > 0.0;
+    int cand = 0;
+    for (int j = 0; j < k; ++j) {
+      if (good[j]) continue;
+      std::vector<double> u((size_t)k);
+      for (; cand < k; ++cand) {
+        for (int i = 0; i < k; ++i) u[i] = (i == cand) ? 1.0 : 0.0;
+        for (int pass = 0; pass < 2; ++pass)
+          for (int c = 0; c < k; ++c) {
+            if (!good[c]) continue;
+            double t = 0.0;
+            for (int i = 0; i < k; ++i) t += Ux[i + (size_t)c * k] * u[i];
+            for (int i = 0; i < k; ++i) u[i] -= t * Ux[i + (size_t)c * k];
+          }
+        double nn = 0.0;
+        for (int i = 0; i < k; ++i) nn += u[i] * u[i];
+        if (nn > 0.25) {
+          nn = std::sqrt(nn);
+          for (int i = 0; i < k; ++i) Ux[i + (size_t)j * k] = u[i] / nn;
+          good[j] = 1;
+          ++cand;
+          break;
+        }
+      }
+    }
+  }
   // R P = Q1 R1 = Q1 X^T = Q1 Vx S Ux^T  ->  Ur = Q1 Vx, Vr = P Ux
   for (int j = 0; j < k; ++j) {
     s[j] = sx[j];

@@ -182,3 +182,35 @@ def test_host_svd_relative_accuracy_on_graded_triangle():
     sm = np.sort(np.array([float(x) for x in mpmath.svd_r(mpmath.matrix(R.tolist()), compute_uv=False)]))[::-1]
     assert np.max(np.abs(s - sm) / sm) <= 1e-8
     np.testing.assert_allclose(U @ np.diag(s) @ Vt.T, R, atol=1e-14)
+
+
+@pytest.mark.parametrize("n", [2, 5, 17, 40, 121])
+def test_host_sym_eig_against_lapack(n):
+    """rsk_sym_eig (Householder tridiagonalisation + implicit Wilkinson-shift QR, host C++)
+    against LAPACK's eigh: eigenvalues, eigenvector residuals and orthogonality, with a
+    cluster of equal eigenvalues and a wide dynamic range."""
+    from paper_2306_15049_b200 import rsk
+    rng = np.random.default_rng(n)
+    Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    lam = np.concatenate([np.logspace(-8, 4, n - n // 4), np.full(n // 4, 3.0)])
+    H = (Q * lam) @ Q.T
+    th, V = rsk.sym_eig(H)
+    ref = np.linalg.eigvalsh(H)
+    scale = np.max(np.abs(lam))
+    assert np.all(np.diff(th) >= 0)
+    assert np.max(np.abs(th - ref)) <= 1e-13 * scale
+    assert np.max(np.abs(H @ V - V * th)) <= 1e-12 * scale
+    assert np.max(np.abs(V.T @ V - np.eye(n))) <= 1e-13
+
+
+def test_host_svd_rank_deficient_right_vectors_orthogonal():
+    """k >= 24 path (QR with column pivoting + Jacobi): Vr orthogonal also when R is
+    rank-deficient (the null-space columns are completed)."""
+    from paper_2306_15049_b200 import rsk
+    rng = np.random.default_rng(9)
+    k = 30
+    B = rng.standard_normal((k, 20)) @ rng.standard_normal((20, k))    # rank 20
+    U, s, Vt = rsk.svd_small(B)
+    V = Vt   # rsk_svd_small returns Vr (columns = right singular vectors)
+    assert np.max(np.abs(V.T @ V - np.eye(k))) <= 1e-12
+    assert np.max(np.abs(U[:, :20] * s[:20] @ V[:, :20].T - B)) <= 1e-12 * np.max(np.abs(B))
