@@ -373,6 +373,7 @@ def run_ours(args, cfg, rank, world):
 
     # ---- one full nested solve of the config (K_out outer steps), if it fits the budget
     nested_s = None
+    outs_n = None
     if not nested and not args.no_nested and (ms / args.steps) * cfg.K_out / 1e3 < args.nested_budget:
         torch.cuda.synchronize(dev)
         D.barrier()
@@ -401,6 +402,14 @@ def run_ours(args, cfg, rank, world):
         v, cores, desc = oracle_sample(cfg, args.cpu_budget)
         cpu = {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": desc}
 
+    if rank == 0 and args.report:
+        from paper_2306_15049_b200.pipeline import report_rows
+        rows = report_rows(outs_n if nested_info else last, inputs["gamma"])
+        import csv
+        with open(args.report, "w", newline="") as fh:
+            wr = csv.DictWriter(fh, fieldnames=list(rows[0].keys()))
+            wr.writeheader()
+            wr.writerows(rows)
     if rank == 0:
         o = last[-1]
         line = {
@@ -518,6 +527,7 @@ def main():
     ap.add_argument("--nested-budget", type=float, default=300.0)
     ap.add_argument("--no-nested", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--report", default=None, help="CSV of the per-(k, l) accounting of the last step / nested solve")
     # options of the nested solve (defaults = north_star's path; see README / DESIGN)
     ap.add_argument("--inner", default=None, choices=["cg", "minres"])
     ap.add_argument("--local", default=None, choices=["d3", "seq"])

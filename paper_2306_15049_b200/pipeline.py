@@ -60,6 +60,57 @@ def _host(t: torch.Tensor) -> np.ndarray:
     return t.detach().cpu().numpy()
 
 
+class _Phases:
+    """NVTX ranges for the phases of one outer step: an outer range, one nested range per
+    phase (each call closes the previous phase)."""
+
+    def __init__(self, name: str):
+        torch.cuda.nvtx.range_push(name)
+        self.open = False
+
+    def __call__(self, phase: str):
+        if self.open:
+            torch.cuda.nvtx.range_pop()
+        torch.cuda.nvtx.range_push(phase)
+        self.open = True
+
+    def end(self):
+        if self.open:
+            torch.cuda.nvtx.range_pop()
+        torch.cuda.nvtx.range_pop()
+
+
+class _nvtx:
+    """NVTX range around a phase of the outer step (visible in Nsight Systems / ncu)."""
+
+    def __init__(self, name: str):
+        self.name = name
+
+    def __enter__(self):
+        torch.cuda.nvtx.range_push(self.name)
+
+    def __exit__(self, *a):
+        torch.cuda.nvtx.range_pop()
+
+
+def report_rows(outs, gamma) -> list[dict]:
+    """Per (outer step k, shift l) accounting -- the quantity of the paper's matvec figures
+    (P:1075-1081): gamma, inner iterations, A_gamma applies (each counts one
+    A and one E matvec: shifted applies), true relative residual, status, local dimension,
+    and the outer step's fixed applies (seeds, Ritz, anchoring, g-hat images) on l = -1."""
+    rows = []
+    for o in outs:
+        for l in range(len(o.iters)):
+            rows.append(dict(k=int(o.k), l=l + 1, gamma=float(gamma[l]), iters=int(o.iters[l]),
+                             applies_A=int(o.applies[l]), applies_E=int(o.applies[l]),
+                             relres=float(o.relres[l]), status=int(o.status[l]), m_used=int(o.m_used[l]),
+                             principal_guess=int(o.has_xp[l]), lstar=int(o.lstar) + 1, nc=int(o.nc)))
+        rows.append(dict(k=int(o.k), l=-1, gamma=float("nan"), iters=0, applies_A=int(o.overhead_applies),
+                         applies_E=int(o.overhead_applies), relres=float("nan"), status=-1, m_used=0,
+                         principal_guess=0, lstar=int(o.lstar) + 1, nc=int(o.nc)))
+    return rows
+
+
 class GpuSolver:
     """All device state of one configuration (one image grid, one PSF, M shifts)."""
 
@@ -300,6 +351,8 @@ class GpuSolver:
         N, M = self.N, self.M
         dist = self.dist
         t0 = time.perf_counter()
+        ph = _Phases(f"rsk outer step k={k}")
+        ph("principal space (seeds / Ritz / stabilize)")
         owners = shard.assignment(k, M, dist.world, st.get("prev_iters"), groups=self.grp, J=cfg.J)
         mine = owners[dist.rank]
         ml = len(mine)
@@ -326,6 +379,7 @@ class GpuSolver:
             torch.cuda.synchronize(self.dev)
             ZA = dist.gather_rows(za, cols, nc)
             ZE = dist.gather_rows(ze, cols, nc)
+        ph("anchoring + Grams")
         # ---- anchoring (eq:establishU) and Grams: identical on every rank
         gstar = float(self.gamma[shift_indices(cfg).istar - 1])
         Y = ZA.clone()
@@ -338,6 +392,7 @@ class GpuSolver:
         Ahat = _host(self.utv(Ut, ZA)).T
         Ehat = _host(self.utv(Ut, ZE)).T
         del K
+        ph("principal guesses")
         # ---- principal guesses for this rank's shifts: eq:orthupdate, or the oblique
         # projections of §sec:oblique (f2(iii), Config.guess)
         mode = getattr(cfg, "guess", "orth")
@@ -355,6 +410,7 @@ class GpuSolver:
         X = self.combine(Ut, Cg[:, mine]) if ml else torch.zeros(0, N, **self.f)
         if getattr(self, "guess_hook", None) is not None:     # diagnostics (tools/probe_guess.py)
             self.guess_hook(k, mine, X, has_xp[mine])
+        ph("group Ritz blocks")
         # ---- group Ritz blocks (Alg. 2 / Alg. 4)
         Wg, AWg, EWg = [], [], []
         for jidx in (shift_indices(cfg).J_L - 1, shift_indices(cfg).J_R - 1):
@@ -362,6 +418,7 @@ class GpuSolver:
             Wg.append(self.combine(Ut, Wt)); AWg.append(self.combine(ZA, Wt)); EWg.append(self.combine(ZE, Wt))
         del ZA, ZE
         groups = dict(W=Wg, AW=AWg, EW=EWg, of_shift=self.grp[mine])
+        ph("carried corrections")
         # ---- carried corrections (Alg. 3, reading D3 / G12) for this rank's shifts
         ghat = None
         keep = None
@@ -385,6 +442,7 @@ class GpuSolver:
             self.h.apply_shifted(Gh, ZGh, gamma=self.gam_dev[idx].contiguous(), stream=self.stream)
             overhead += int(keep.sum())
             ghat = (Gh, ZGh, keep)
+        ph("batched inner solve")
         # ---- batched deflated CG on this rank's shifts
         G = torch.empty(ml, N, **self.f)
         if ml and getattr(cfg, "local", "d3") == "seq":
@@ -405,6 +463,7 @@ class GpuSolver:
             res = dict(iters=np.zeros(0, np.int32), applies=np.zeros(0, np.int64), status=np.zeros(0, np.int32),
                        relres=np.zeros(0), m_used=np.zeros(0, np.int32), prof=np.zeros(8))
             rho_l = eta_l = np.zeros(0)
+        ph("exchange + L-curve")
         # ---- exchange (allgather) and the L-curve
         if dist.enabled:
             torch.cuda.synchronize(self.dev)
@@ -422,6 +481,7 @@ class GpuSolver:
             relres, m_used, rho, eta = res["relres"], res["m_used"], rho_l, eta_l
         lstar, _ = lcurve_corner(rho, eta)
         torch.cuda.synchronize(self.dev)
+        ph.end()
         out = StepOut(k, iters, applies, status, relres, m_used, nc, lstar, rho, eta, overhead,
                       has_xp, keep, time.perf_counter() - t0, res["prof"])
         nst = dict(X_prev=Xf, G_prev=Gf, V_i1=V_i1, xstar=Xf[lstar], prev_iters=np.asarray(iters))
