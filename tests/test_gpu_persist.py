@@ -87,8 +87,8 @@ def _setup(torch, dev, cfg, nL, nR, J, seed, gam):
     return sol, groups, ghat, X
 
 
-@pytest.mark.parametrize("loop", ["stream", "tiled"])
-@pytest.mark.parametrize("n,r,nL,nR", [(112, 3, 44, 10), (100, 7, 40, 9)])
+@pytest.mark.parametrize("n,r,nL,nR,loop", [(112, 3, 44, 10, "stream"), (100, 7, 40, 9, "stream"),
+                                            (100, 7, 40, 9, "tiled")])
 def test_persistent_loop_multi_pass_two_groups(torch_dev, monkeypatch, n, r, nL, nR, loop):
     """loop = "stream": cg_stream.cu (the default for N >= 512^2); "tiled": cg_persist.cu."""
     monkeypatch.setenv("RSK_CG_NOCLUSTER", "1")

@@ -31,7 +31,10 @@ def _t(torch, dev, a):
 def test_c7_outer_step_k0(torch_dev):
     torch, dev = torch_dev
     from paper_2306_15049_b200.pipeline import GpuSolver
-    cfg = dataclasses.replace(S.CONFIGS["C7"], tol=1e-10, local="d3", principal="g10", n_c=60)
+    # the C7 PSF (r = 11) and method on a 64^2 image, 8 shifts (the full C7 ladder reaches
+    # gamma = 1e-8, where plain MINRES seeds need many thousand oracle iterations)
+    cfg = dataclasses.replace(S.CONFIGS["C7"], n=64, M=8, gamma_lo=1e-4, gamma_hi=1e2, n_c=24, J=4, idx=(),
+                              tol=1e-10, local="d3", principal="g10")
     inp = S.make_inputs(cfg)
     n, M = cfg.n, cfg.M
     h = inp["psf"]
