@@ -87,8 +87,14 @@ _SHIFT_SOLVE = None
 
 
 def _run_shift(l):
-    """Pool trampoline (fork start method: the closure is inherited, never pickled)."""
-    return _SHIFT_SOLVE(l)
+    """Pool trampoline (fork start method: the closure is inherited, never pickled). One
+    BLAS thread per worker process: the workers are the parallelism."""
+    try:
+        from threadpoolctl import threadpool_limits
+    except ImportError:   # pragma: no cover
+        return _SHIFT_SOLVE(l)
+    with threadpool_limits(1):
+        return _SHIFT_SOLVE(l)
 
 
 def outer_step(cfg, h, b, d, gamma, st: StepState, shifts=None, workers: int = 1) -> StepResult:

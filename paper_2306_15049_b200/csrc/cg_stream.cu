@@ -603,38 +603,11 @@ __device__ void s_phase_b_reg(const StreamParams& P, const SList& L, double* sme
       for (int mb = 0; mb < 2; ++mb) { dA[nb][mb][0] = dA[nb][mb][1] = dE[nb][mb][0] = dE[nb][mb][1] = 0.0; }
     }
     const int nbn = (np + 7) >> 3;
-    // L2 prefetch 64 rows (one 128-byte line per stream every other super-step) ahead:
-    // lane v of the warp owns stream v (w, r or b, zg of the pass's shifts; AW, EW columns)
-    const double* pf0 = nullptr;
-    const double* pf1 = nullptr;
-    {
-      auto stream_ptr = [&](int v) -> const double* {
-        if (v < 3 * np) {
-          const int k = v / 3, w = v - 3 * k;
-          const int e = L.e[li0 + k];
-          const int s = le_sid(e);
-          if (w == 0) return cg->Wv + (int64_t)s * N;
-          if (w == 1) return le_mode(e) == ST_ACTIVE ? cg->R + (int64_t)s * N : cg->b;
-          return le_hg(e) ? cg->ZGhat + (int64_t)s * cg->ldgh : nullptr;
-        }
-        v -= 3 * np;
-        if (v < J) return AWg + (int64_t)v * ldw;
-        v -= J;
-        if (v < J) return EWg + (int64_t)v * ldw;
-        return nullptr;
-      };
-      pf0 = stream_ptr(lane);
-      pf1 = stream_ptr(lane + 32);
-    }
     // 8-row super-steps: lane (g, q) loads rows 2q, 2q+1 as one 16-byte pair (64-byte runs
     // per column / shift across the four q lanes); k-step t of the two uses row 2q + t --
     // the same row permutation on A and B, so D sums over all 8 rows
 #pragma unroll 2
     for (int64_t row0 = wbeg; row0 < wend; row0 += 8) {
-      if (((row0 - wbeg) & 15) == 0 && row0 + 64 < wend) {
-        if (pf0) prefetch_l2(pf0 + row0 + 64);
-        if (pf1) prefetch_l2(pf1 + row0 + 64);
-      }
       const int64_t row = row0 + 2 * q;
       const bool vr = row < wend;           // wend - row0 is a multiple of 8 except at N
       const bool vr1 = row + 1 < wend;
@@ -809,36 +782,10 @@ __device__ void s_phase_c_reg(const StreamParams& P, const SList& L, double* sme
         const int k = 8 * nb + 2 * q + h;
         flg[nb][h] = k < np ? (int)PS[k * kSPS + 3] : 0;
       }
-    // L2 prefetch 64 rows ahead (one 128-byte line per stream and 16-row block): lane v
-    // owns stream v (p, x, r, ghat of the pass's shifts as their flags need; W columns)
-    const double* pf0 = nullptr;
-    const double* pf1 = nullptr;
-    {
-      auto stream_ptr = [&](int v) -> const double* {
-        if (v < 4 * np) {
-          const int k = v >> 2, w = v & 3;
-          const int e = L.e[li0 + k];
-          const int s = le_sid(e);
-          const int f = (int)PS[k * kSPS + 3];
-          if (w == 0) return f ? cg->P + (int64_t)s * N : nullptr;
-          if (w == 1) return (f & 1) ? cg->X + (int64_t)s * cg->ldx : nullptr;
-          if (w == 2) return (f & 2) ? cg->R + (int64_t)s * N : nullptr;
-          return ((f & 2) && le_hg(e)) ? cg->Ghat + (int64_t)s * cg->ldgh : nullptr;
-        }
-        v -= 4 * np;
-        return v < J ? Wg + (int64_t)v * ldw : nullptr;
-      };
-      pf0 = stream_ptr(lane);
-      pf1 = stream_ptr(lane + 32);
-    }
     // 16-row blocks: lane (g, q) owns rows 2g, 2g+1 (one 16-byte pair: 128-byte runs per
     // column / shift across the eight g lanes); two DMMAs per k-step, one per row parity
 #pragma unroll 1
     for (int64_t row0 = wbeg; row0 < wend; row0 += 16) {
-      if (row0 + 64 < wend) {
-        if (pf0) prefetch_l2(pf0 + row0 + 64);
-        if (pf1) prefetch_l2(pf1 + row0 + 64);
-      }
       const int64_t row = row0 + 2 * g;
       const bool vr = row < wend;            // rows come in pairs (N even)
       double2 a[4];

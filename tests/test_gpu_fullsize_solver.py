@@ -35,9 +35,16 @@ def _t(torch, dev, a):
     return torch.from_numpy(np.ascontiguousarray(a, dtype=np.float64)).to(dev)
 
 
+def _one_thread(fn, x):
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1):   # one BLAS thread per worker: the workers are the parallelism
+        return fn(x)
+
+
 def _pmap(fn, items):
+    import functools
     with mp.get_context("fork").Pool(min(len(items), WORKERS)) as pool:
-        return pool.map(fn, items, chunksize=1)
+        return pool.map(functools.partial(_one_thread, fn), items, chunksize=1)
 
 
 def _img_A(v):

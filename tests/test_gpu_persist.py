@@ -37,9 +37,16 @@ def _oracle_shift(l):
     return r.x, r.iters, r.applies, r.status
 
 
+def _one_thread(fn, x):
+    from threadpoolctl import threadpool_limits
+    with threadpool_limits(1):   # one BLAS thread per worker: the workers are the parallelism
+        return fn(x)
+
+
 def _pool_map(fn, items):
+    import functools
     with mp.get_context("fork").Pool(min(len(items), mp.cpu_count())) as pool:
-        return pool.map(fn, items, chunksize=1)
+        return pool.map(functools.partial(_one_thread, fn), items, chunksize=1)
 
 
 @pytest.fixture(scope="module")

