@@ -500,6 +500,14 @@ def run_slab(args, cfg, rank, world):
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms = float(t.item())
+    if rank == 0 and args.report:
+        from paper_2306_15049_b200.pipeline import report_rows
+        import csv
+        rows = report_rows([o], inputs["gamma"])
+        with open(args.report, "w", newline="") as fh:
+            wr = csv.DictWriter(fh, fieldnames=list(rows[0].keys()))
+            wr.writeheader()
+            wr.writerows(rows)
     if rank == 0:
         print(json.dumps({
             "metric": METRIC, "value": ap / (ms / 1e3), "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -528,6 +536,7 @@ def main():
     ap.add_argument("--no-nested", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--report", default=None, help="CSV of the per-(k, l) accounting of the last step / nested solve")
+    ap.add_argument("--slab", action="store_true", help="row slabs across the ranks (default for C5 at N > 1)")
     # options of the nested solve (defaults = north_star's path; see README / DESIGN)
     ap.add_argument("--inner", default=None, choices=["cg", "minres"])
     ap.add_argument("--local", default=None, choices=["d3", "seq"])
@@ -550,7 +559,7 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group(os.environ.get("RSK_BENCH_BACKEND", "nccl"))
-    if world > 1 and cfg.name == "C5":
+    if world > 1 and (cfg.name == "C5" or args.slab):
         run_slab(args, cfg, rank, world)
     else:
         run_ours(args, cfg, rank, world)
