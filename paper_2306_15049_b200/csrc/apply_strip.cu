@@ -93,6 +93,7 @@ bool strip_fill_params(Handle* h, StripParams& p, const double* X, int64_t ldx, 
   p.seg_rows = seg_rows;
   p.nseg = (int)((h->ny + seg_rows - 1) / seg_rows);
   p.mode = mode;
+  p.prefetch_w = getenv("RSK_STRIP_NOPF") ? 0 : 1;
   const int T = 4 * r + 1;
   for (int t = 0; t < T; ++t) { p.cx[t] = h->cBx[t]; p.cy[t] = h->cBy[t]; }
   return true;

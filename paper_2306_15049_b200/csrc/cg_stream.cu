@@ -121,6 +121,12 @@ __device__ __forceinline__ void bulk_store(void* dst, const void* src, unsigned 
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+// group-block loads: read once per pass and CTA range -- L2 only (RSK_GRP_L1 kept them in L1)
+#ifdef RSK_GRP_L1
+__device__ __forceinline__ double2 ldgrp(const double2* p) { return __ldg(p); }
+#else
+__device__ __forceinline__ double2 ldgrp(const double2* p) { return __ldcg(p); }
+#endif
 __device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p)); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
@@ -616,8 +622,8 @@ __device__ void s_phase_b_reg(const StreamParams& P, const SList& L, double* sme
       for (int mb = 0; mb < 2; ++mb) {
         const int col = 8 * mb + g;
         const bool va = vr && col < J;
-        aA[mb] = va ? __ldg(reinterpret_cast<const double2*>(AWg + (int64_t)col * ldw + row)) : make_double2(0.0, 0.0);
-        aE[mb] = va ? __ldg(reinterpret_cast<const double2*>(EWg + (int64_t)col * ldw + row)) : make_double2(0.0, 0.0);
+        aA[mb] = va ? ldgrp(reinterpret_cast<const double2*>(AWg + (int64_t)col * ldw + row)) : make_double2(0.0, 0.0);
+        aE[mb] = va ? ldgrp(reinterpret_cast<const double2*>(EWg + (int64_t)col * ldw + row)) : make_double2(0.0, 0.0);
       }
 #pragma unroll
       for (int nb = 0; nb < 2; ++nb) {
@@ -792,7 +798,7 @@ __device__ void s_phase_c_reg(const StreamParams& P, const SList& L, double* sme
 #pragma unroll
       for (int kk = 0; kk < 4; ++kk) {
         const int j = 4 * kk + q;
-        a[kk] = (vr && kk < nkk && j < J) ? __ldg(reinterpret_cast<const double2*>(Wg + (int64_t)j * ldw + row))
+        a[kk] = (vr && kk < nkk && j < J) ? ldgrp(reinterpret_cast<const double2*>(Wg + (int64_t)j * ldw + row))
                                           : make_double2(0.0, 0.0);
       }
 #pragma unroll

@@ -74,6 +74,7 @@ struct alignas(64) StripParams {
   int nstrip, nseg, seg_rows;
   int mode;              // RSK_APPLY_SHIFTED or RSK_APPLY_SPLIT
   int want_dot;
+  int prefetch_w;        // L1 prefetch of the weights two blocks ahead (RSK_STRIP_NOPF=1: off)
   double cx[kMaxTaps];
   double cy[kMaxTaps];
 };
@@ -199,7 +200,7 @@ struct StripCore {
         // the weights of output block t - LAG + 2 into L1 (two steps ahead of their use)
         const int gi2 = ra + 8 * (t - C::LAG + 2) + g;
         const int gj2 = c0 + cb + 2 * q;
-        if (gi2 >= ra && gi2 < rb && gj2 < nx) {
+        if (p.prefetch_w && gi2 >= ra && gi2 < rb && gj2 < nx) {
           const int64_t o = (int64_t)gi2 * nx + gj2;
           prefetch_l1(p.wx + o + (gj2 > 0 ? -1 : 0));
           prefetch_l1(p.wx + o + 1);
