@@ -129,62 +129,97 @@ class ClockSampler:
 
 
 # ---------------------------------------------------------------- CPU oracle leg
-def _oracle_worker(args):
-    """One host core: the oracle as it stands (numpy fp64, one thread) running plain CG
-    (O4 with U = empty, x_0 = 0, W_0 = I -- the seed-solve form of the same operator) at
-    shift gamma_l for `budget_s` seconds. Returns the number of A_gamma applies."""
-    cfg_name, l, budget_s = args
+_OW = {}
+
+
+def _oracle_init(cfg_name):
+    """Worker set-up (once per process): the config's operator and right-hand side."""
     os.environ["OMP_NUM_THREADS"] = "1"
-    from oracle import defcg as dcg
+    try:
+        from threadpoolctl import threadpool_limits
+        threadpool_limits(1)
+    except Exception:
+        pass
     from oracle import operators as ops
     from oracle import pipeline as opipe
     cfg = S.CONFIGS[cfg_name]
     inputs = S.make_inputs(cfg)
-    n = cfg.n
     h = opipe.operator_of(cfg, inputs)
     d, b = ops.make_data(h, inputs["x_true"], inputs["xi"], cfg.noise)
-    wx, wy = ops.identity_weights(n)
-    g = float(inputs["gamma"][l])
+    _OW.update(cfg=cfg, h=h, b=b.ravel(), gamma=inputs["gamma"], w=ops.identity_weights(cfg.n))
+
+
+def _oracle_worker(args):
+    """One host core: the oracle as it stands (numpy fp64, one thread) running plain CG
+    (O4 with U = empty, x_0 = 0, W_0 = I -- the seed-solve form of the same operator) at
+    shift gamma_l for about `budget_s` seconds. Returns (applies, seconds)."""
+    l, budget_s = args
+    from oracle import defcg as dcg
+    from oracle import operators as ops
+    cfg, h, b = _OW["cfg"], _OW["h"], _OW["b"]
+    wx, wy = _OW["w"]
+    n = cfg.n
+    g = float(_OW["gamma"][l])
     A = lambda v: ops.apply_shifted(h, wx, wy, g, v.reshape(n, n)).ravel()
     t0 = time.perf_counter()
-    dcg.defcg(A, b.ravel(), tol=1e-300, maxit=1)
+    dcg.defcg(A, b, tol=1e-300, maxit=1)
     per = max(time.perf_counter() - t0, 1e-4) / 2.0
     its = max(1, int(budget_s / per))
     t0 = time.perf_counter()
-    r = dcg.defcg(A, b.ravel(), tol=1e-300, maxit=its)
+    r = dcg.defcg(A, b, tol=1e-300, maxit=its)
     return r.applies, time.perf_counter() - t0
 
 
+class OraclePool:
+    """The oracle, untuned, on ALL host cores: one process per core (spawned once), each a
+    plain CG of the config's operator at a different shift of the ladder."""
+
+    def __init__(self, cfg, cores=None):
+        self.model, ncpu = _cpu_desc()
+        self.cores = cores or ncpu
+        self.cfg = cfg
+        self.ls = [int(round(i * (cfg.M - 1) / max(self.cores - 1, 1))) for i in range(self.cores)]
+        self.pool = mp.get_context("spawn").Pool(self.cores, initializer=_oracle_init, initargs=(cfg.name,))
+
+    def sample(self, budget_s):
+        """Returns (applies/s, cores, description) of one bounded sample."""
+        t0 = time.perf_counter()
+        res = self.pool.map(_oracle_worker, [(l, budget_s) for l in self.ls], chunksize=1)
+        wall = time.perf_counter() - t0
+        ap = sum(a for a, _ in res)
+        busy = max(t for _, t in res)
+        cfg = self.cfg
+        return ap / busy, self.cores, (f"oracle (numpy fp64) plain CG on {cfg.name} (n={cfg.n}, {2*cfg.r+1}x{2*cfg.r+1} "
+                                       f"PSF), one shift per core over the ladder, {ap} applies in {busy:.1f} s on "
+                                       f"{self.cores} cores ({self.model}); wall {wall:.1f} s")
+
+    def close(self):
+        self.pool.close()
+        self.pool.join()
+
+
 def oracle_sample(cfg, budget_s, cores=None):
-    """The oracle, untuned, on ALL host cores: one process per core, each a plain CG of
-    the config's operator at a different shift of the ladder, for about budget_s s.
-    Returns (applies/s, cores, description)."""
-    model, ncpu = _cpu_desc()
-    cores = cores or ncpu
-    ls = [int(round(i * (cfg.M - 1) / max(cores - 1, 1))) for i in range(cores)]
-    t0 = time.perf_counter()
-    ctx = mp.get_context("spawn")
-    with ctx.Pool(cores) as pool:
-        res = pool.map(_oracle_worker, [(cfg.name, l, budget_s) for l in ls])
-    wall = time.perf_counter() - t0
-    ap = sum(a for a, _ in res)
-    busy = max(t for _, t in res)
-    return ap / busy, cores, (f"oracle (numpy fp64) plain CG on {cfg.name} (n={cfg.n}, {2*cfg.r+1}x{2*cfg.r+1} "
-                              f"PSF), one shift per core over the ladder, {ap} applies in {busy:.1f} s on "
-                              f"{cores} cores ({model}); wall incl. setup {wall:.1f} s")
+    p = OraclePool(cfg, cores)
+    try:
+        return p.sample(budget_s)
+    finally:
+        p.close()
 
 
 def run_reference(args, cfg, rank, world):
     if rank != 0:
         return
-    oracle_sample(cfg, 1.0)                     # warm-up (process start, imports)
+    pool = OraclePool(cfg)
+    for _ in range(max(1, args.warmup)):
+        pool.sample(1.0)                        # warm-up (process start, imports, set-up)
     vals = []
     desc = cores = None
     t_total = time.perf_counter()
     for _ in range(args.steps):
-        v, cores, desc = oracle_sample(cfg, args.ref_budget)
+        v, cores, desc = pool.sample(args.ref_budget)
         vals.append(v)
     t_total = time.perf_counter() - t_total
+    pool.close()
     v = float(np.mean(vals))
     print(json.dumps({
         "impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
