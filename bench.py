@@ -302,6 +302,7 @@ def run_ours(args, cfg, rank, world):
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     tot_ap = tot_sv = tot_it = tot_conv = 0
     loop_ms = loop_its = 0.0
+    loop_launches = 0
     kinds = set()
     l0 = lib.rsk_launch_count()
     with ClockSampler(local) as clk:
@@ -315,6 +316,7 @@ def run_ours(args, cfg, rank, world):
             for o in outs:
                 if o.prof is not None:
                     loop_ms += float(o.prof[5]); loop_its += float(o.prof[6]); kinds.add(int(o.prof[7]))
+                    loop_launches += int(np.ceil(float(o.prof[2]) / 512.0))   # 512 lockstep iterations per launch
         torch.cuda.synchronize(dev)
     launches = lib.rsk_launch_count() - l0
     ms = sum(a.elapsed_time(b) for a, b in ev)
@@ -374,13 +376,16 @@ def run_ours(args, cfg, rank, world):
     achieved = alg_bytes / (loop_ms / 1e3) / 1e9 if loop_ms > 0 else None
     kind = max(kinds) if kinds else 0
     n_launch_loop = 0
+    # DRAM traffic of the loop kernel per launch: the DRAM bytes per ms of the committed
+    # ncu --set full capture of one k = 1 launch (profiles/r2/cg_loop_traffic.json) x this
+    # run's mean launch duration
     traffic = None
     tf = os.path.join(ROOT, "profiles", "r2", "cg_loop_traffic.json")
-    if os.path.exists(tf):
+    if os.path.exists(tf) and loop_launches:
         with open(tf) as fh:
             tr = json.load(fh)
-        if tr.get("workload") == cfg.name:
-            traffic = tr["dram_bytes_per_shift_iteration"] * loop_its / max(args.steps, 1) / tr.get("launches_per_step", 1)
+        if tr.get("workload") == cfg.name and world == 1:
+            traffic = tr["dram_bytes_per_ms"] * loop_ms / loop_launches
     # standalone fused apply over the full batch (all M shifts): 10 back-to-back launches
     # between two events, best of 3; FP64 work (16 r + 20) flop/px
     X = torch.randn(cfg.M, cfg.N, **f)
@@ -479,6 +484,8 @@ def run_ours(args, cfg, rank, world):
                          "alg_bytes_per_shift_iteration_px": per_px,
                          "alg_formula": "80 + (n_grp*24*J + 16)/S, S = shifts per GPU, n_grp = 2 (SURVEY 8(d) d2)",
                          "shift_iterations": loop_its, "kernel_ms": loop_ms, "N": cfg.N,
+                         "launches": loop_launches,
+                         "alg_bytes_per_launch": (alg_bytes / loop_launches) if loop_launches else None,
                          "kernel_ms_share": loop_ms / max(ms, 1e-9)},
             "apply_roofline": apply_roof,
             "nested_solve": nested_info,

@@ -1178,6 +1178,7 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
   h->nE += tot_ap;
   if (o->ms_loop && !prof) {
     for (int i = 0; i < 5; ++i) o->ms_loop[i] = 0.0;
+    o->ms_loop[2] = (double)n_ka;   // lockstep iterations of the device loop (launches: ceil(/512))
   }
   if (o->ms_loop) {
     int64_t dits = 0;
