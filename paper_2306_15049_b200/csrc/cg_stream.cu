@@ -64,6 +64,7 @@ struct alignas(64) StreamParams {
   int max_iters;
   int prof;
   int staged;         // 1: phases B / C through bulk-copy stages (experiment), 0: registers
+  int wide;           // 1: phase B in the wide form (32-byte lanes, 128-byte runs)
 };
 
 // ---------------------------------------------------------------- small helpers
@@ -716,6 +717,187 @@ __device__ void s_phase_b_reg(const StreamParams& P, const SList& L, double* sme
   }
 }
 
+// ---------------------------------------------------------------- phase B (wide form)
+// Same sums as s_phase_b_reg with 16-row super-steps and 32-byte lane loads: lane (g, q)
+// loads rows 4q..4q+3 of shift 8 nb + g (w, r, zg) and of column 8 mt + g of the
+// concatenated group block [AW | EW] (2J columns, NMT = ceil(2J / 8) m-tiles); k-step t of
+// the four uses row 4q + t on both operands. Each shift / column then moves as one
+// 128-byte run per warp instruction -- the 64-byte runs of the 8-row form cap the phase
+// near 3 TB/s (tools/stream_bw.cu: 64-byte runs 2.6-3.1 TB/s, 128-byte 5.4-6.3 TB/s).
+// Needs N, ldw, ldgh multiples of 4 and 32-byte aligned vectors (launch_cg_stream).
+__device__ __forceinline__ void ld4cg(const double* p, double* v) {
+  asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+               : "l"(p));
+}
+__device__ __forceinline__ void ld4nc(const double* p, double* v) {
+  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+               : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
+               : "l"(p));
+}
+__device__ __forceinline__ void st4(double* p, const double* v) {
+  asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
+               : "memory");
+}
+// One warp = one 8-shift N block of the pass (nb) over its row range: a pass of <= 8 shifts
+// spreads the CTA's rows over all 8 warps; a pass of 9..16 gives each N block 4 warps, each
+// over a quarter of the rows (the group columns are then read by two warps; the second read
+// hits L2). Keeps the per-warp registers at one N block (no spills at NMT = 3).
+template <int NMT>
+__device__ void s_phase_b_wide_pass(const StreamParams& P, const SList& L, double* red, const double* s_alpha,
+                                    int li0, int li1, CgDev* cg, int64_t cbeg, int64_t cend) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int g = lane >> 2, q = lane & 3;
+  const int64_t N = cg->N;
+  const int np = li1 - li0;
+  const int nbn = (np + 7) >> 3;   // 1 or 2
+  const int nb = nbn == 2 ? warp >> 2 : 0;
+  const int wpb = nbn == 2 ? 4 : 8;   // warps per N block
+  const int64_t rpw = (cend - cbeg + 16 * wpb - 1) / (16 * wpb) * 16;
+  const int64_t wbeg = cbeg + (warp % wpb) * rpw;
+  const int64_t wend = imin64(cend, wbeg + rpw);
+  const int grp = le_grp(L.e[li0]);
+  const int J = cg->grp.J[grp];
+  const int64_t ldw = cg->grp.ldw;
+  // column 8 mt + g of [AW | EW]
+  const double* colp[NMT];
+  bool colv[NMT];
+#pragma unroll
+  for (int mt = 0; mt < NMT; ++mt) {
+    const int c = 8 * mt + g;
+    colv[mt] = c < 2 * J;
+    colp[mt] = colv[mt] ? (c < J ? cg->grp.AW[grp] + (int64_t)c * ldw : cg->grp.EW[grp] + (int64_t)(c - J) * ldw)
+                        : cg->grp.AW[grp];
+  }
+  const int li = li0 + 8 * nb + g;
+  const bool ok = li < li1;
+  const int v = ok ? L.e[li] : 0;
+  const bool act = !ok || le_mode(v) == ST_ACTIVE;
+  const bool hg = ok && le_hg(v);
+  const double al = ok ? s_alpha[li] : 0.0;
+  const double* wp = cg->Wv + (int64_t)le_sid(v) * N;
+  double* rp = cg->R + (int64_t)le_sid(v) * N;
+  const double* zp = cg->ZGhat + (int64_t)le_sid(v) * cg->ldgh;
+  double dz[NMT][2], rh = 0.0, zt = 0.0;
+#pragma unroll
+  for (int mt = 0; mt < NMT; ++mt) dz[mt][0] = dz[mt][1] = 0.0;
+#pragma unroll 1
+  for (int64_t row0 = wbeg; row0 < wend; row0 += 16) {
+    const int64_t row = row0 + 4 * q;
+    const bool vr = row < wend;   // N % 4 == 0: the 4 rows are all valid or all beyond
+    double a[NMT][4], wv[4], rv[4], zg[4];
+#pragma unroll
+    for (int mt = 0; mt < NMT; ++mt) {
+      if (vr && colv[mt]) ld4cg(colp[mt] + row, a[mt]);
+      else a[mt][0] = a[mt][1] = a[mt][2] = a[mt][3] = 0.0;
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) wv[t] = rv[t] = zg[t] = 0.0;
+    const bool lv = ok && vr;
+    if (lv) {
+      ld4cg(wp + row, wv);
+      if (act) ld4cg(rp + row, rv);
+      else ld4nc(cg->b + row, rv);
+      if (hg) ld4nc(zp + row, zg);
+    }
+    double rn[4] = {0.0, 0.0, 0.0, 0.0};
+    if (lv) {
+#pragma unroll
+      for (int t = 0; t < 4; ++t) rn[t] = act ? fma(-al, wv[t], rv[t]) : rv[t] - wv[t];
+      st4(rp + row, rn);
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        rh = fma(rn[t], rn[t], rh);
+        zt = fma(zg[t], rn[t], zt);
+      }
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t)
+#pragma unroll
+      for (int mt = 0; mt < NMT; ++mt) dmma(dz[mt][0], dz[mt][1], a[mt][t], rn[t]);
+  }
+  // stage: warp's D[c = 8 mt + g][n = 2q, 2q+1] of its N block (c < J: zA[c], else zE[c - J])
+  double* rw = red + (size_t)warp * 32 * kRW;
+  rh += __shfl_xor_sync(0xffffffffu, rh, 1);
+  rh += __shfl_xor_sync(0xffffffffu, rh, 2);
+  zt += __shfl_xor_sync(0xffffffffu, zt, 1);
+  zt += __shfl_xor_sync(0xffffffffu, zt, 2);
+  if (q == 0) {
+    rw[(8 * nb + g) * kRW + 32] = rh;
+    rw[(8 * nb + g) * kRW + 33] = zt;
+  }
+#pragma unroll
+  for (int mt = 0; mt < NMT; ++mt) {
+    const int c = 8 * mt + g;
+    if (c >= 2 * J) continue;
+    const int off = c < J ? c : 16 + (c - J);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) rw[(8 * nb + 2 * q + h) * kRW + off] = dz[mt][h];
+  }
+  __syncthreads();
+  for (int e = tid; e < np * kSPV; e += blockDim.x) {
+    const int k = e / kSPV, j = e - k * kSPV;
+    const int v2 = L.e[li0 + k];
+    const int nw = le_m(v2) - le_hg(v2);
+    const bool isz = j < nw, isg = le_hg(v2) && j == nw, isr = j == kMaxM;
+    if (!(isz || isg || isr)) continue;
+    // the warps of shift k's N block, in warp order
+    const int w0 = nbn == 2 ? 4 * (k >> 3) : 0;
+    double ta = 0.0, te = 0.0;
+#pragma unroll
+    for (int w = 0; w < 8; ++w) {
+      if (w >= wpb) break;
+      const double* r = red + ((size_t)(w0 + w) * 32 + k) * kRW;
+      if (isz) { ta += r[j]; te += r[16 + j]; }
+      else ta += r[isr ? 32 : 33];
+    }
+    const int s = le_sid(v2);
+    const double val = isz ? fma(cg->gam[s], te, ta) : ta;
+    P.partB[((size_t)s * kSPV + j) * P.nchunk + blockIdx.x] = val;
+  }
+  __syncthreads();
+}
+
+template <int R>
+__device__ void s_phase_b_wide(const StreamParams& P, const SList& L, double* smem, double* s_alpha, int* pst,
+                               CgDev* cg) {
+  const int n = L.n;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t N = cg->N;
+  for (int li = warp; li < n; li += 8) {
+    const int v = L.e[li];
+    double a = 0.0;
+    if (le_mode(v) == ST_ACTIVE) {
+      const int s = le_sid(v);
+      const double* pa = P.partA + (size_t)s * P.ipv;
+      int k0, k1;
+      s_cta_span(P.sp, n, li, gridDim.x, k0, k1);
+      double pi = 0.0;
+      for (int c = k0 + lane; c <= k1; c += 32) pi += __ldcg(pa + c);
+      pi = warp_sum(pi);
+      if (!(pi > 0.0) || !isfinite(pi)) {
+        if (blockIdx.x == 0 && lane == 0) { cg->status[s] = ST_BREAKDOWN; cg->alpha[s] = 0.0; }
+      } else {
+        a = cg->rho[s] / pi;
+        if (blockIdx.x == 0 && lane == 0) cg->alpha[s] = a;
+      }
+    }
+    if (lane == 0) s_alpha[li] = a;
+  }
+  const int npass = s_passes(L, pst);
+  const int64_t cbeg = (int64_t)blockIdx.x * P.rpc;
+  const int64_t cend = imin64(N, cbeg + P.rpc);
+  for (int pk = 0; pk < npass; ++pk) {
+    const int li0 = pst[pk], li1 = pst[pk + 1];
+    const int J = cg->grp.J[le_grp(L.e[li0])];
+    const int nmt = (2 * J + 7) >> 3;
+    if (nmt <= 1) s_phase_b_wide_pass<1>(P, L, smem, s_alpha, li0, li1, cg, cbeg, cend);
+    else if (nmt == 2) s_phase_b_wide_pass<2>(P, L, smem, s_alpha, li0, li1, cg, cbeg, cend);
+    else if (nmt == 3) s_phase_b_wide_pass<3>(P, L, smem, s_alpha, li0, li1, cg, cbeg, cend);
+    else s_phase_b_wide_pass<4>(P, L, smem, s_alpha, li0, li1, cg, cbeg, cend);
+  }
+}
+
 // ---------------------------------------------------------------- phase C (register form)
 // x += alpha p; p = r + beta p - W mu_W - ghat mu_g. W mu of a pass on the tensor cores:
 // an 8-row block x 8 shifts is D = W[8 x J] M[J x 8] (B = the shifts' mu); lane (g, q)
@@ -895,68 +1077,67 @@ __device__ void s_phase_b2(const StreamParams& P, const SList& L, double* smem, 
       }
     }
     __syncthreads();
-    if (tid == 0) {
-      const double rho_new = zs[kMaxM];
-      const int st = cg->status[s];
-      const double thr = cg->tol * cg->bnorm;
-      const bool conv = sqrt(rho_new) <= thr;
-      int nst = st;
-      bool newp = false;
-      if (mode0 == ST_ACTIVE) {
-        if (st == ST_ACTIVE) {
-          const int itn = cg->iters[s] + 1;
-          cg->iters[s] = itn;
-          cg->beta[s] = rho_new / cg->rho[s];
-          cg->rho[s] = rho_new;
-          if (conv) nst = ST_RCONV;
-          else if (itn >= cg->maxit) nst = ST_MAXIT;
-          else newp = true;
-        }
-      } else {
-        cg->rho_true[s] = rho_new;
-        cg->nconf[s] += 1;
-        cg->alpha[s] = 0.0;
-        if (conv) nst = ST_DONE;
-        else if (cg->iters[s] >= cg->maxit) nst = ST_MAXIT;
-        else {
-          nst = ST_ACTIVE;
-          cg->beta[s] = 0.0;
-          cg->rho[s] = rho_new;
-          newp = true;
+    if (warp == 0) {
+      // status by lane 0; the two triangular solves with G = L L^T by the warp (lane i =
+      // row i, column-oriented substitution: no local arrays, no spills)
+      int nst = 0, newp = 0;
+      if (lane == 0) {
+        const double rho_new = zs[kMaxM];
+        const int st = cg->status[s];
+        const double thr = cg->tol * cg->bnorm;
+        const bool conv = sqrt(rho_new) <= thr;
+        nst = st;
+        if (mode0 == ST_ACTIVE) {
+          if (st == ST_ACTIVE) {
+            const int itn = cg->iters[s] + 1;
+            cg->iters[s] = itn;
+            cg->beta[s] = rho_new / cg->rho[s];
+            cg->rho[s] = rho_new;
+            if (conv) nst = ST_RCONV;
+            else if (itn >= cg->maxit) nst = ST_MAXIT;
+            else newp = 1;
+          }
+        } else {
+          cg->rho_true[s] = rho_new;
+          cg->nconf[s] += 1;
+          cg->alpha[s] = 0.0;
+          if (conv) nst = ST_DONE;
+          else if (cg->iters[s] >= cg->maxit) nst = ST_MAXIT;
+          else {
+            nst = ST_ACTIVE;
+            cg->beta[s] = 0.0;
+            cg->rho[s] = rho_new;
+            newp = 1;
+          }
         }
       }
+      newp = __shfl_sync(0xffffffffu, newp, 0);
       if (newp) {
-        double* cf = cg->coef + (int64_t)s * kMaxM;
-        double x[kMaxM];
-#pragma unroll
-        for (int i = 0; i < kMaxM; ++i) {
-          if (i < m) {
-            double t = zs[i];
-#pragma unroll
-            for (int j = 0; j < i; ++j) t -= Ls[i * kMaxM + j] * x[j];
-            x[i] = t / Ls[i * kMaxM + i];
+        const int i = lane;
+        double t = (i < m) ? zs[i] : 0.0;
+        // forward: L y = z
+        for (int j = 0; j < m; ++j) {
+          const double xj = __shfl_sync(0xffffffffu, t, j) / Ls[j * kMaxM + j];
+          if (i == j) t = xj;
+          else if (i > j && i < m) t = fma(-Ls[i * kMaxM + j], xj, t);
+        }
+        // backward: L^T x = y
+        for (int j = m - 1; j >= 0; --j) {
+          const double xj = __shfl_sync(0xffffffffu, t, j) / Ls[j * kMaxM + j];
+          if (i == j) t = xj;
+          else if (i < j) t = fma(-Ls[j * kMaxM + i], xj, t);
+        }
+        if (i < kMaxM) cg->coef[(int64_t)s * kMaxM + i] = i < m ? t : 0.0;
+        if (lane == 0) {
+          int slot = -1;
+          if (cg->store && cg->store_cnt[s] < cg->store_cap) {
+            slot = cg->store_cnt[s];
+            cg->store_cnt[s] = slot + 1;
           }
+          cg->stslot[s] = slot;
         }
-#pragma unroll
-        for (int i = kMaxM - 1; i >= 0; --i) {
-          if (i < m) {
-            double t = x[i];
-#pragma unroll
-            for (int j = i + 1; j < kMaxM; ++j)
-              if (j < m) t -= Ls[j * kMaxM + i] * x[j];
-            x[i] = t / Ls[i * kMaxM + i];
-          }
-        }
-#pragma unroll
-        for (int j = 0; j < kMaxM; ++j) cf[j] = j < m ? x[j] : 0.0;
-        int slot = -1;
-        if (cg->store && cg->store_cnt[s] < cg->store_cap) {
-          slot = cg->store_cnt[s];
-          cg->store_cnt[s] = slot + 1;
-        }
-        cg->stslot[s] = slot;
       }
-      cg->status[s] = nst;
+      if (lane == 0) cg->status[s] = nst;
     }
     __syncthreads();
   }
@@ -1183,6 +1364,7 @@ __global__ void __launch_bounds__(kAT, kStripCtasPerSm) cg_stream_kernel(const _
     sgrid_sync(P.bar, gen);
     mark(1);
     if (P.staged) s_phase_b<R>(P, L, smem, s_alpha, bpar, pst, &s_cg);
+    else if (P.wide) s_phase_b_wide<R>(P, L, smem, s_alpha, pst, &s_cg);
     else s_phase_b_reg<R>(P, L, smem, s_alpha, pst, &s_cg);
     mark(2);
     sgrid_sync(P.bar, gen);
@@ -1338,6 +1520,15 @@ cudaError_t launch_cg_stream(Handle* h, CgDev* dev, const CgDev& hc, double* par
   prm.ipv = stream_ipv(h);   // stride of partA; the items of an iteration: s_ipv()
   prm.max_iters = max_iters;
   prm.staged = getenv("RSK_STREAM_STAGED") ? 1 : 0;
+  {
+    // wide phase B: 32-byte rows of every vector it streams
+    auto al32p = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31) == 0; };
+    bool w = (N % 4) == 0 && (hc.grp.ldw % 4) == 0 && al32p(hc.b) && al32p(hc.R) && al32p(hc.Wv) &&
+             (!hc.Ghat || ((hc.ldgh % 4) == 0 && al32p(hc.ZGhat)));
+    for (int gi = 0; gi < RSK_MAX_GROUPS; ++gi)
+      if (hc.grp.J[gi] > 0 && hc.grp.AW[gi]) w = w && al32p(hc.grp.AW[gi]) && al32p(hc.grp.EW[gi]);
+    prm.wide = (w && !getenv("RSK_STREAM_NARROW")) ? 1 : 0;
+  }
   {
     static int pf = -1;
     if (pf < 0) pf = getenv("RSK_PERSIST_PROF") ? 1 : 0;

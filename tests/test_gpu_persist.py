@@ -95,11 +95,15 @@ def _setup(torch, dev, cfg, nL, nR, J, seed, gam):
 
 
 @pytest.mark.parametrize("n,r,nL,nR,loop", [(112, 3, 44, 10, "stream"), (100, 7, 40, 9, "stream"),
-                                            (100, 7, 40, 9, "tiled")])
+                                            (100, 7, 40, 9, "stream-narrow"), (100, 7, 40, 9, "tiled")])
 def test_persistent_loop_multi_pass_two_groups(torch_dev, monkeypatch, n, r, nL, nR, loop):
-    """loop = "stream": cg_stream.cu (the default for N >= 512^2); "tiled": cg_persist.cu."""
+    """loop = "stream": cg_stream.cu (the default for N >= 512^2; phase B in its wide form,
+    N % 4 == 0); "stream-narrow": the same loop with the 16-byte-lane phase B (the form odd
+    leading dimensions take); "tiled": cg_persist.cu."""
     monkeypatch.setenv("RSK_CG_NOCLUSTER", "1")
-    monkeypatch.setenv("RSK_CG_STREAM", "1" if loop == "stream" else "0")
+    monkeypatch.setenv("RSK_CG_STREAM", "0" if loop == "tiled" else "1")
+    if loop == "stream-narrow":
+        monkeypatch.setenv("RSK_STREAM_NARROW", "1")
     torch, dev = torch_dev
     import dataclasses
     M = nL + nR
@@ -108,7 +112,7 @@ def test_persistent_loop_multi_pass_two_groups(torch_dev, monkeypatch, n, r, nL,
     sol, groups, ghat, X = _setup(torch, dev, cfg, nL, nR, 12, 900 + n, gam)
     G = torch.empty_like(X)
     res = sol.cg(list(range(M)), X, _CTX["has_xp"], Gout=G, groups=groups, ghat=ghat)
-    assert int(res["prof"][7]) == (3 if loop == "stream" else 2), "the requested loop must have run"
+    assert int(res["prof"][7]) == (2 if loop == "tiled" else 3), "the requested loop must have run"
     ref = _pool_map(_oracle_shift, list(range(M)))
     its = np.array([r[1] for r in ref])
     assert len(set(its.tolist())) > M // 3, "iteration counts should spread (active set shrinks pass by pass)"
