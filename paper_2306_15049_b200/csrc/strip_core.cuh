@@ -16,8 +16,16 @@
 //
 // Every x-pass result is used by 4r + 8 output rows (no recomputed halo rows: the tiled
 // core recomputes 4r of every 64 - 4r rows, 1.6x the DMMAs at r = 7), and consecutive
-// strips of one vector share their 2r-column halos through L2. One __syncthreads per
-// 8-row step; both rings are 8 blocks deep (input ring: LAG + D + 1 <= 8).
+// strips of one vector share their 2r-column halos through L2. Both rings are 8 blocks
+// deep (input ring: LAG + D + 1 <= 8).
+//
+// No CTA barrier per step: a warp's x-pass writes and its y-pass reads only its own 8
+// columns of the T ring (__syncwarp), and the input ring is a full / empty mbarrier
+// pipeline -- full[slot] completes with the TMA bytes, empty[slot] when all 8 warps have
+// made their last read of the block (x-pass at step b, E-stencil rows at steps up to
+// b + K, K = LAG - floor((H - 1) / 8)); thread 0 waits on empty before re-filling a slot.
+// The warps drift apart by up to 7 - D - K steps, so the DMMA, shared-load and
+// epilogue phases of different warps overlap instead of running in lockstep.
 #pragma once
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -49,8 +57,11 @@ struct StripCfg {
   static constexpr int OFF_DC = TAIL > 0 ? TAIL : RING_END;   // [4R][R] zero-boundary corrections
   static constexpr int OFF_FR = OFF_DC + al16(4 * R * R);    // [2][KS][32] Toeplitz fragments
   static constexpr int OFF_RED = OFF_FR + al16(2 * KS * 32);  // block-reduction scratch
-  static constexpr int OFF_BAR = OFF_RED + 16;      // 8 mbarriers (8 B each)
-  static constexpr int DBL = OFF_BAR + 8;
+  static constexpr int OFF_BAR = OFF_RED + 16;      // 8 full mbarriers (8 B each)
+  static constexpr int OFF_EBAR = OFF_BAR + 8;      // 8 empty mbarriers (8 warp arrivals)
+  static constexpr int DBL = OFF_EBAR + 8;
+  static constexpr int K = LAG - (H - 1) / 8;       // block b's last read: step b + K
+  static_assert(D + K <= 7, "input ring reuse: the issuer at step t needs block t + D - 8 released");
   static constexpr size_t SMEM = sizeof(double) * (size_t)DBL;
   static constexpr unsigned XBYTES = 8u * 8u * PX;
   static_assert(D >= 1, "input ring too shallow for this r");
@@ -104,13 +115,18 @@ struct StripCore {
     }
     if (threadIdx.x == 0) {
       for (int b = 0; b < 8; ++b) mbar_init(reinterpret_cast<uint64_t*>(smem + C::OFF_BAR) + b, 1);
+      for (int b = 0; b < 8; ++b) mbar_init(reinterpret_cast<uint64_t*>(smem + C::OFF_EBAR) + b, kAT / 32);
       mbar_fence_init();
     }
     __syncthreads();
   }
 
-  __device__ static void issue(const StripParams& p, double* smem, unsigned slot, int c0, int row0, int s,
+  // fill ring position P (slot P & 7) with the input block at image row row0; the slot's
+  // previous block (P - 8) must have been released by every warp
+  __device__ static void issue(const StripParams& p, double* smem, unsigned P, int c0, int row0, int s,
                                bool src2) {
+    const unsigned slot = P & 7u;
+    if (P >= 8u) mbar_wait(reinterpret_cast<uint64_t*>(smem + C::OFF_EBAR) + slot, ((P >> 3) - 1u) & 1u);
     uint64_t* bar = reinterpret_cast<uint64_t*>(smem + C::OFF_BAR) + slot;
     mbar_expect_tx(bar, C::XBYTES);
     tma_load_3d(smem + C::OFF_IN + slot * 8 * C::PX, src2 ? &p.mapX2 : &p.mapX, bar, c0 - C::H, row0, s);
@@ -149,12 +165,14 @@ struct StripCore {
       ay[ks] = smem[C::OFF_FR + (C::KS + ks) * 32 + lane];
     }
 
+    uint64_t* ebars = reinterpret_cast<uint64_t*>(smem + C::OFF_EBAR);
     if (tid == 0)
-      for (int t = 0; t < C::D && t < nbi; ++t) issue(p, smem, (base + t) & 7u, c0, rb0 + 8 * t, s, src2);
+      for (int t = 0; t < C::D && t < nbi; ++t) issue(p, smem, base + t, c0, rb0 + 8 * t, s, src2);
 
 #pragma unroll 1
     for (int t = 0; t < nbi; ++t) {
       const unsigned slot = (base + t) & 7u;
+      if (tid == 0 && t + C::D < nbi) issue(p, smem, base + t + C::D, c0, rb0 + 8 * (t + C::D), s, src2);
       mbar_wait(bars + slot, (ring.parity >> slot) & 1u);
       ring.parity ^= 1u << slot;
       // ---- x-pass of input block t: T[8 rows][cb .. cb+8) = IN[8 rows][cb .. cb+8+4r) x Bx
@@ -192,10 +210,7 @@ struct StripCore {
         }
         *reinterpret_cast<double2*>(T + (slot * 8 + g) * C::PT + cb + 2 * q) = make_double2(d0, d1);
       }
-      __syncthreads();
-      // every thread is past step t-1: the slot of block t + D (last read at step
-      // t + D - 8 + LAG < t) is free
-      if (tid == 0 && t + C::D < nbi) issue(p, smem, (base + t + C::D) & 7u, c0, rb0 + 8 * (t + C::D), s, src2);
+      __syncwarp();   // the warp's T columns: x-pass stores before its y-pass loads
       {
         // the weights of output block t - LAG + 2 into L1 (two steps ahead of their use)
         const int gi2 = ra + 8 * (t - C::LAG + 2) + g;
@@ -209,7 +224,10 @@ struct StripCore {
         }
       }
       const int j = t - C::LAG;
-      if (j < 0) continue;
+      if (j < 0) {
+        release(ebars, base, t - C::K, lane);
+        continue;
+      }
       // ---- y-pass of output block j: rows ra + 8j .. +7 from T window rows u = 8j .. 8j+4r+7
       const int i0 = ra + 8 * j;
       const int gi = i0 + g;                 // this lane's output row
@@ -313,10 +331,19 @@ struct StripCore {
         ys[(int64_t)gi * nx + gj] = o0;
         dot = fma(x0, o0, dot);
       }
+      release(ebars, base, t - C::K, lane);
     }
+    // the blocks whose last read was in this item's final steps
+    for (int b = nbi - C::K; b < nbi; ++b) release(ebars, base, b, lane);
     ring.pos = base + (unsigned)nbi;
-    __syncthreads();   // the next item's prologue refills slots this item's last steps read
     return dot;
+  }
+
+  // this warp is done with block b of the item (ring position base + b)
+  __device__ static void release(uint64_t* ebars, unsigned base, int b, int lane) {
+    if (b < 0) return;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(ebars + ((base + (unsigned)b) & 7u));
   }
 };
 
