@@ -138,7 +138,7 @@ def load(path: str | None = None):
     global _lib
     if _lib is not None and path is None:
         return _lib
-    p = path or LIB_PATH
+    p = path or os.environ.get("RSK_LIB_PATH") or LIB_PATH   # RSK_LIB_PATH: A/B builds (tools)
     if not os.path.exists(p):
         raise RuntimeError(f"librsk.so not found at {p}: build it with "
                            "`python -m paper_2306_15049_b200.build` (no CPU fallback exists)")

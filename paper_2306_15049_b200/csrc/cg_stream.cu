@@ -1065,14 +1065,19 @@ __device__ void s_phase_b2(const StreamParams& P, const SList& L, double* smem, 
     }
     for (int j = warp; j < kSPV; j += 8) {
       if (j < m || j == kMaxM) {
+        // all ten loads of a lane in flight at once (one L2 round trip per 320 chunks)
         const double* pj = P.partB + ((size_t)s * kSPV + j) * P.nchunk;
-        double t0 = 0.0, t1 = 0.0, t2 = 0.0, t3 = 0.0;
-        int c = lane;
-        for (; c + 96 < P.nchunk; c += 128) {
-          t0 += __ldcg(pj + c); t1 += __ldcg(pj + c + 32); t2 += __ldcg(pj + c + 64); t3 += __ldcg(pj + c + 96);
+        double t = 0.0;
+        for (int c0 = 0; c0 < P.nchunk; c0 += 320) {
+          double v[10];
+#pragma unroll
+          for (int i = 0; i < 10; ++i) {
+            const int c = c0 + lane + 32 * i;
+            v[i] = c < P.nchunk ? __ldcg(pj + c) : 0.0;
+          }
+          t += (((v[0] + v[1]) + (v[2] + v[3])) + ((v[4] + v[5]) + (v[6] + v[7]))) + (v[8] + v[9]);
         }
-        for (; c < P.nchunk; c += 32) t0 += __ldcg(pj + c);
-        const double t = warp_sum((t0 + t1) + (t2 + t3));
+        t = warp_sum(t);
         if (lane == 0) zs[j] = t;
       }
     }
