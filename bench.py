@@ -341,7 +341,8 @@ def run_ours(args, cfg, rank, world):
         h_in = [torch.from_numpy(inputs["x_true"]).pin_memory(), torch.from_numpy(inputs["xi"]).pin_memory()]
         d_in = [x_true, xi]
     else:
-        d_in = [snap["X_prev"], snap["G_prev"], snap["V_i1"], W1[0], W1[1]]
+        # (ranks other than 0 hold no V_i1: rank 0 builds the principal space, shard.py)
+        d_in = [t for t in (snap["X_prev"], snap["G_prev"], snap["V_i1"], W1[0], W1[1]) if t is not None]
         h_in = [t.cpu().pin_memory() for t in d_in]
     res_h = torch.empty(cfg.M, cfg.N, dtype=torch.float64).pin_memory()
     ee = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(e2e_steps)]
@@ -505,6 +506,8 @@ def run_slab(args, cfg, rank, world):
     from paper_2306_15049_b200 import _lib as L
     from paper_2306_15049_b200.slab import DistComm, SlabGpuSolver, SlabPlan
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if os.environ.get("RSK_BENCH_SAME_GPU"):   # test hook: every rank on cuda:0 (gloo)
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     lib = L.load()
@@ -598,14 +601,19 @@ def main():
     if args.impl == "reference":
         run_reference(args, cfg, rank, world)
         return
-    if world > 1:
+    # --slab at one rank runs the row-slab solver on a single slab (the N = 1 point of the
+    # slab scaling curve; a process group of one)
+    slab = (world > 1 and cfg.name == "C5") or args.slab
+    if world > 1 or slab:
         import torch.distributed as dist
-        dist.init_process_group(os.environ.get("RSK_BENCH_BACKEND", "nccl"))
-    if world > 1 and (cfg.name == "C5" or args.slab):
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group(os.environ.get("RSK_BENCH_BACKEND", "nccl"), rank=rank, world_size=world)
+    if slab:
         run_slab(args, cfg, rank, world)
     else:
         run_ours(args, cfg, rank, world)
-    if world > 1:
+    if world > 1 or slab:
         import torch.distributed as dist
         dist.destroy_process_group()
 

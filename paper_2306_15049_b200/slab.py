@@ -89,9 +89,20 @@ class DistComm:
     def __init__(self, plan: SlabPlan, rank: int):
         self.plan, self.rank = plan, rank
 
+    def _host(self) -> bool:
+        # gloo (several ranks on one device, CPU tests) moves CUDA tensors through host memory
+        import torch.distributed as dist
+        return dist.get_backend() == "gloo"
+
     def allreduce(self, t: torch.Tensor, op: str = "sum"):
         import torch.distributed as dist
-        dist.all_reduce(t, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+        rop = dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM
+        if self._host() and t.is_cuda:
+            h = t.cpu()
+            dist.all_reduce(h, op=rop)
+            t.copy_(h)
+        else:
+            dist.all_reduce(t, op=rop)
 
     def halo(self, T: torch.Tensor):
         """T: (nv, ext_rows*nx). Fill the halo rows from the neighbours' owned rows."""
@@ -100,16 +111,17 @@ class DistComm:
         s = p.slabs[k]
         off = s.top
         ops, recv = [], []
+        bdev = torch.device("cpu") if (self._host() and T.is_cuda) else T.device
         if k > 0:
             up = p.slabs[k - 1]
-            send = T[:, off * nx:(off + up.bot) * nx].contiguous()
-            buf = torch.empty(T.shape[0], s.top * nx, dtype=T.dtype, device=T.device)
+            send = T[:, off * nx:(off + up.bot) * nx].contiguous().to(bdev)
+            buf = torch.empty(T.shape[0], s.top * nx, dtype=T.dtype, device=bdev)
             ops += [dist.P2POp(dist.isend, send, k - 1), dist.P2POp(dist.irecv, buf, k - 1)]
             recv.append((buf, 0))
         if k < p.nranks - 1:
             dn = p.slabs[k + 1]
-            send = T[:, (off + s.own_rows - dn.top) * nx:(off + s.own_rows) * nx].contiguous()
-            buf = torch.empty(T.shape[0], s.bot * nx, dtype=T.dtype, device=T.device)
+            send = T[:, (off + s.own_rows - dn.top) * nx:(off + s.own_rows) * nx].contiguous().to(bdev)
+            buf = torch.empty(T.shape[0], s.bot * nx, dtype=T.dtype, device=bdev)
             ops += [dist.P2POp(dist.isend, send, k + 1), dist.P2POp(dist.irecv, buf, k + 1)]
             recv.append((buf, (off + s.own_rows) * nx))
         if ops:
