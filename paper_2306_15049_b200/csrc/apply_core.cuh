@@ -112,6 +112,39 @@ __device__ __forceinline__ double warp_sum(double v) {
 }
 
 // deterministic block sum (fixed tree), result valid in thread 0
+// Double-double accumulation (Knuth TwoSum, exact for any operand order): sums of many
+// terms kept to ~2^-104 relative, so the rounded total does not depend on how the terms were
+// grouped (the streaming CG loop's p.w: batch-composition-independent alpha).
+__device__ __forceinline__ void dd_add(double& h, double& l, double bh, double bl) {
+  const double s = h + bh;
+  const double bb = s - h;
+  double e = (h - (s - bb)) + (bh - bb);
+  e += l + bl;
+  h = s + e;
+  l = e - (h - s);
+}
+__device__ __forceinline__ void warp_sum_dd(double& h, double& l) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const double oh = __shfl_xor_sync(0xffffffffu, h, o), ol = __shfl_xor_sync(0xffffffffu, l, o);
+    dd_add(h, l, oh, ol);
+  }
+}
+// red: >= 2 x (warps) doubles; every thread of warp 0 returns the CTA's sum
+__device__ __forceinline__ void block_sum_dd(double& h, double& l, double* red) {
+  warp_sum_dd(h, l);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
+  if (lane == 0) { red[2 * wid] = h; red[2 * wid + 1] = l; }
+  __syncthreads();
+  if (wid == 0) {
+    const bool in = lane < (int)(blockDim.x >> 5);
+    h = in ? red[2 * lane] : 0.0;
+    l = in ? red[2 * lane + 1] : 0.0;
+    warp_sum_dd(h, l);
+  }
+}
+
 __device__ __forceinline__ double block_sum(double v, double* red) {
   v = warp_sum(v);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;

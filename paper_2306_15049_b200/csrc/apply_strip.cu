@@ -30,7 +30,9 @@ __global__ void __launch_bounds__(kAT, kStripCtasPerSm)
     const int ss = it / nvec;
     const int strip = ss % p.nstrip, seg = ss / p.nstrip;
     const int s = list ? list[li] : li;
-    const double dot = Core::item(p, smem, ring, s, strip, seg * p.seg_rows, min(p.ny, (seg + 1) * p.seg_rows), false);
+    double lo;
+    const double dot = Core::item(p, smem, ring, s, strip, seg * p.seg_rows, min(p.ny, (seg + 1) * p.seg_rows), false,
+                                  &lo) + lo;
     if (p.want_dot) {
       const double bs = block_sum(dot, smem + C::OFF_RED);
       if (threadIdx.x == 0) p.part[(int64_t)li * ipv + ss] = bs;

@@ -34,11 +34,8 @@ namespace rsk {
 
 constexpr int kSMaxShift = 256;
 constexpr int kSPV = kMaxM + 1;     // partial slots per (shift, chunk): z_0..z_{m-1}, rho at kMaxM
-constexpr int kSRows = 128;         // rows per stage
-constexpr int kSChunk = 1024;       // rows per partial chunk (8 stages)
 constexpr int kSB = 8;              // shifts per stage batch
 constexpr int kSVec = 4;            // vectors per shift in a stage
-constexpr int kSAcc = 34;           // per pass shift: zA[16], zE[16], rho, zeta
 
 __device__ unsigned long long g_sprof[8];   // per-phase ns (RSK_PERSIST_PROF), block 0's view
 __device__ unsigned long long g_sprof3[8];
@@ -63,7 +60,6 @@ struct alignas(64) StreamParams {
   int ipv;            // apply items per vector (segments x strips)
   int max_iters;
   int prof;
-  int staged;         // 1: phases B / C through bulk-copy stages (experiment), 0: registers
   int wide;           // 1: phase B in the wide form (32-byte lanes, 128-byte runs)
 };
 
@@ -293,10 +289,16 @@ __device__ __forceinline__ void s_phase_a(const StreamParams& P, const SList& L,
   int64_t b = ((int64_t)k * B + G - 1) / G;
   const int64_t bend = ((int64_t)(k + 1) * B + G - 1) / G;
   int cur_li = -1;
-  double acc = 0.0;
+  // the CTA's p.w partial of the current shift as a double-double (hi at partA[s][k], lo at
+  // partA[nshift + s][k]): the shift's total is then the same whatever the block ranges
+  double acc = 0.0, acl = 0.0;
+  double* partL = P.partA + (size_t)P.nshift * P.ipv;
   if (b == bend && b < B && threadIdx.x == 0) {   // empty range inside an entry's span
     const int li = (int)(b / per);
-    if (le_mode(L.e[li]) != ST_RCONV) P.partA[(size_t)le_sid(L.e[li]) * P.ipv + k] = 0.0;
+    if (le_mode(L.e[li]) != ST_RCONV) {
+      P.partA[(size_t)le_sid(L.e[li]) * P.ipv + k] = 0.0;
+      partL[(size_t)le_sid(L.e[li]) * P.ipv + k] = 0.0;
+    }
   }
   while (b < bend) {
     const int li = (int)(b / per);
@@ -309,237 +311,29 @@ __device__ __forceinline__ void s_phase_a(const StreamParams& P, const SList& L,
     const int s = le_sid(v);
     const bool rconv = le_mode(v) == ST_RCONV;
     if (li != cur_li) {
-      if (cur_li >= 0 && le_mode(L.e[cur_li]) != ST_RCONV && threadIdx.x == 0)
+      if (cur_li >= 0 && le_mode(L.e[cur_li]) != ST_RCONV && threadIdx.x == 0) {
         P.partA[(size_t)le_sid(L.e[cur_li]) * P.ipv + k] = acc;
+        partL[(size_t)le_sid(L.e[cur_li]) * P.ipv + k] = acl;
+      }
       cur_li = li;
       acc = 0.0;
+      acl = 0.0;
     }
-    const double dot = Core::item(sp, smem, ring, s, strip, 8 * blk, (int)imin64(sp.ny, 8 * (int64_t)blk1), rconv);
+    double lo;
+    double dot = Core::item(sp, smem, ring, s, strip, 8 * blk, (int)imin64(sp.ny, 8 * (int64_t)blk1), rconv, &lo);
     if (!rconv) {
-      const double bs = block_sum(dot, smem + SCfg<R>::Strip::OFF_RED);
-      acc += bs;   // thread 0: the CTA's items of this shift in order
+      block_sum_dd(dot, lo, smem + SCfg<R>::Strip::OFF_RED);
+      dd_add(acc, acl, dot, lo);   // thread 0: the CTA's items of this shift
     }
     b = e;
   }
-  if (cur_li >= 0 && le_mode(L.e[cur_li]) != ST_RCONV && threadIdx.x == 0)
+  if (cur_li >= 0 && le_mode(L.e[cur_li]) != ST_RCONV && threadIdx.x == 0) {
     P.partA[(size_t)le_sid(L.e[cur_li]) * P.ipv + k] = acc;
+    partL[(size_t)le_sid(L.e[cur_li]) * P.ipv + k] = acl;
+  }
 }
 
 // ---------------------------------------------------------------- phase B
-template <int R>
-__device__ void s_phase_b(const StreamParams& P, const SList& L, double* smem, double* s_alpha, unsigned& bpar,
-                          int* pst, CgDev* cg) {
-  using SC = SCfg<R>;
-  const int n = L.n;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, q = lane & 3;
-  const int64_t N = cg->N;
-  // alpha = rho / pi, pi = the shift's item partials in item order (every CTA, same tree)
-  for (int li = warp; li < n; li += 8) {
-    const int v = L.e[li];
-    double a = 0.0;
-    if (le_mode(v) == ST_ACTIVE) {
-      const int s = le_sid(v);
-      const double* pa = P.partA + (size_t)s * P.ipv;
-      int k0, k1;
-      s_cta_span(P.sp, n, li, gridDim.x, k0, k1);
-      double pi = 0.0;
-      for (int c = k0 + lane; c <= k1; c += 32) pi += __ldcg(pa + c);
-      pi = warp_sum(pi);
-      if (!(pi > 0.0) || !isfinite(pi)) {
-        if (blockIdx.x == 0 && lane == 0) { cg->status[s] = ST_BREAKDOWN; cg->alpha[s] = 0.0; }
-      } else {
-        a = cg->rho[s] / pi;
-        if (blockIdx.x == 0 && lane == 0) cg->alpha[s] = a;
-      }
-    }
-    if (lane == 0) s_alpha[li] = a;
-  }
-  const int npass = s_passes(L, pst);   // (syncs: s_alpha visible)
-  double* RED = smem + SC::OFF_RED;
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SC::OFF_BAR);
-  const int nunits = npass;
-  if ((int64_t)blockIdx.x * P.rpc >= N) {   // no rows for this CTA: zero partials
-    for (int e = tid; e < n * kSPV; e += blockDim.x) {
-      const int k = e / kSPV, j = e - k * kSPV;
-      P.partB[((size_t)le_sid(L.e[k]) * kSPV + j) * P.nchunk + blockIdx.x] = 0.0;
-    }
-    return;
-  }
-  // producer = warp 0, one lane per shift slot of the batch (+ lane 31: the group tiles)
-  auto issue = [&](SStep st, unsigned q2) {
-    const SGeo G = s_geo(pst, P.rpc, N, st.u);
-    const int sub = st.k / G.nb, b = st.k % G.nb;
-    const int64_t r0 = G.cbeg + (int64_t)sub * kSRs;
-    const int nr = (int)imin64(kSRs, G.cend - r0);
-    const unsigned bytes = 8u * nr;
-    const int grp = le_grp(L.e[G.li0]);
-    const int J = cg->grp.J[grp];
-    const int slot = q2 % kSNST;
-    double* stg = smem + SC::OFF_ST + slot * SC::STAGE;
-    uint64_t* bar = bars + slot;
-    const int li = G.li0 + b * kSB + lane;
-    const bool mine = lane < kSB && li < G.li1;
-    const int v = mine ? L.e[li] : 0;
-    unsigned my = mine ? 2 * bytes + (le_hg(v) ? bytes : 0) : 0u;
-    if (lane == 31 && J > 0) my += 2u * 8u * kSP * J;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) my += __shfl_xor_sync(0xffffffffu, my, o);
-    unsigned long long tq0 = 0, tq1 = 0, tq2 = 0;
-    if (P.prof && blockIdx.x == 0 && (lane == 0 || lane == 31)) tq0 = s_timer();
-    if (lane == 0) mbar_expect_tx(bar, my);
-    __syncwarp();
-    if (mine) {
-      const int s = le_sid(v);
-      double* d = stg + SC::OFF_SS + lane * 3 * kSP;
-      bulk_load(d, cg->Wv + (int64_t)s * N + r0, bytes, bar);
-      bulk_load(d + kSP, cg->R + (int64_t)s * N + r0, bytes, bar);
-      if (le_hg(v)) bulk_load(d + 2 * kSP, cg->ZGhat + (int64_t)s * cg->ldgh + r0, bytes, bar);
-    }
-    if (P.prof && blockIdx.x == 0 && lane == 0) { tq1 = s_timer(); atomicAdd(&g_sprof3[0], tq1 - tq0); }
-    if (lane == 31 && J > 0) {
-      tma_load_2d(stg + SC::OFF_SG, &P.mAW[grp], bar, (int)r0, 0);
-      tma_load_2d(stg + SC::OFF_SG + 16 * kSP, &P.mEW[grp], bar, (int)r0, 0);
-    }
-    if (P.prof && blockIdx.x == 0 && lane == 31) { tq2 = s_timer(); atomicAdd(&g_sprof3[1], tq2 - tq0); }
-  };
-  auto advance = [&](SStep& st) {
-    const SGeo G = s_geo(pst, P.rpc, N, st.u);
-    if (++st.k >= G.nsteps) { st.k = 0; st.u += 1; }
-  };
-  SStep cons{0, 0}, prod = cons;
-  unsigned qn = 0, qp = 0;
-  unsigned long long s_tstep = 0;
-  if (warp == 0)
-    for (int i = 0; i < kSNST - 1 && prod.u < nunits; ++i) { issue(prod, qp++); advance(prod); }
-  // per-unit accumulators: D tile partial of this warp per batch; rho / zeta per thread
-  const int wt = warp & 3, wh = warp >> 2;      // DMMA tile (mb = wt >> 1, isE = wt & 1), k half
-  double dacc[4][2];
-  double* RR = smem + SC::OFF_PS;   // [32 pass shifts][2 warps][2]: rho, zeta partials
-  while (cons.u < nunits) {
-    const SGeo G = s_geo(pst, P.rpc, N, cons.u);
-    const int np = G.li1 - G.li0;
-    if (cons.k == 0) {
-#pragma unroll
-      for (int b = 0; b < 4; ++b) dacc[b][0] = dacc[b][1] = 0.0;
-      for (int e = tid; e < 32 * 4; e += blockDim.x) RR[e] = 0.0;
-      __syncthreads();
-    }
-    if (warp == 0 && prod.u < nunits) {
-      unsigned long long ti0 = 0;
-      if (P.prof && blockIdx.x == 0 && tid == 0) ti0 = s_timer();
-      issue(prod, qp++);
-      advance(prod);
-      if (P.prof && blockIdx.x == 0 && tid == 0) g_sprof2[6] += s_timer() - ti0;
-    }
-    const int sub = cons.k / G.nb, b = cons.k % G.nb;
-    const int64_t r0 = G.cbeg + (int64_t)sub * kSRs;
-    const int nr = (int)imin64(kSRs, G.cend - r0);
-    const int grp = le_grp(L.e[G.li0]);
-    const int J = cg->grp.J[grp];
-    const int slot = qn % kSNST;
-    double* stg = smem + SC::OFF_ST + slot * SC::STAGE;
-    unsigned long long tw0 = 0;
-    if (P.prof && blockIdx.x == 0 && tid == 32) tw0 = s_timer();
-    mbar_wait(bars + slot, (bpar >> slot) & 1u);
-    if (P.prof && blockIdx.x == 0 && tid == 32) {
-      const unsigned long long t1 = s_timer();
-      g_sprof2[0] += t1 - tw0; g_sprof2[1] += 1;
-      if (s_tstep) g_sprof2[4] += t1 - s_tstep;
-      s_tstep = t1;
-    }
-    bpar ^= 1u << slot;
-    // (a) r update: element e = (shift e >> 6, row e & 63), two per thread; rho, zeta
-    // per warp (32 consecutive rows of one shift) added in step order (fixed)
-#pragma unroll
-    for (int i = 0; i < 2; ++i) {
-      const int e = tid + 256 * i;
-      const int k8 = e >> 6, row = e & 63;
-      const int li = G.li0 + b * kSB + k8;
-      double* d = stg + SC::OFF_SS + k8 * 3 * kSP;
-      double rn = 0.0, rh = 0.0, zt = 0.0;
-      const bool live = li < G.li1;
-      if (live && row < nr) {
-        const int v = L.e[li];
-        const int s = le_sid(v);
-        const double wv = d[row];
-        rn = (le_mode(v) == ST_ACTIVE) ? fma(-s_alpha[li], wv, d[kSP + row]) : __ldg(cg->b + r0 + row) - wv;
-        cg->R[(int64_t)s * N + r0 + row] = rn;
-        rh = rn * rn;
-        if (le_hg(v)) zt = d[2 * kSP + row] * rn;
-      }
-      d[kSP + row] = rn;
-      rh = warp_sum(rh);
-      zt = warp_sum(zt);
-      if (lane == 0 && live) {
-        double* a = RR + ((li - G.li0) * 2 + (warp & 1)) * 2;
-        a[0] += rh;
-        a[1] += zt;
-      }
-    }
-    __syncthreads();
-    if (P.prof && blockIdx.x == 0 && tid == 32) g_sprof2[7] += s_timer() - s_tstep;   // wait end -> after (a) sync
-    // (b) D[j][shift] += [AW | EW]^T R': warp = (tile wt, k half wh), 8 k-steps of 4 rows
-    {
-      const int mb = wt >> 1, isE = wt & 1;
-      if (!(mb == 1 && J <= 8)) {
-        const double* gt = stg + SC::OFF_SG + isE * 16 * kSP + (8 * mb + g) * kSP;
-        const double* rr = stg + SC::OFF_SS + g * 3 * kSP + kSP;
-        const bool colv = (8 * mb + g) < J;
-        double d0 = 0.0, d1 = 0.0;
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const int row = (wh * 8 + kk) * 4 + q;
-          dmma(d0, d1, colv ? gt[row] : 0.0, rr[row]);
-        }
-#pragma unroll
-        for (int bb = 0; bb < 4; ++bb)
-          if (bb == b) { dacc[bb][0] += d0; dacc[bb][1] += d1; }
-      }
-    }
-    __syncthreads();   // stage released
-    if (cons.k + 1 == G.nsteps) {
-      // unit end: chunk partials of the pass's shifts
-      for (int bb = 0; bb < G.nb; ++bb) {
-        // D tile partials of batch bb: warp (tile wt, half wh) -> RED[warp][m * 8 + n]
-#pragma unroll
-        for (int b2 = 0; b2 < 4; ++b2)
-          if (b2 == bb) {
-            RED[warp * 64 + g * 8 + 2 * q] = dacc[b2][0];
-            RED[warp * 64 + g * 8 + 2 * q + 1] = dacc[b2][1];
-          }
-        __syncthreads();
-        const int kb = min(kSB, np - bb * kSB);
-        for (int e = tid; e < kb * kSPV; e += blockDim.x) {
-          const int k8 = e / kSPV, j = e - k8 * kSPV;
-          const int v = L.e[G.li0 + bb * kSB + k8];
-          const int s = le_sid(v);
-          const int nw = le_m(v) - le_hg(v);
-          const double* rr2 = RR + (bb * kSB + k8) * 4;   // [2 warps][rho, zeta]
-          double val;
-          if (j < nw) {
-            const int mb = j >> 3, m = j & 7;
-            // tile (mb, A) = warps 2 mb and 2 mb + 4; tile (mb, E) = warps 2 mb + 1, 2 mb + 5
-            const double za = RED[(2 * mb) * 64 + m * 8 + k8] + RED[(2 * mb + 4) * 64 + m * 8 + k8];
-            const double ze = RED[(2 * mb + 1) * 64 + m * 8 + k8] + RED[(2 * mb + 5) * 64 + m * 8 + k8];
-            val = fma(cg->gam[s], ze, za);
-          } else if (le_hg(v) && j == nw) {
-            val = rr2[1] + rr2[3];
-          } else if (j == kMaxM) {
-            val = rr2[0] + rr2[2];
-          } else {
-            continue;
-          }
-          P.partB[((size_t)s * kSPV + j) * P.nchunk + G.c] = val;
-        }
-        __syncthreads();
-      }
-    }
-    advance(cons);
-    ++qn;
-  }
-}
-
 // ---------------------------------------------------------------- phase B (register form)
 // The per-shift vectors stream through registers: lane (g, q) updates r of (row q of a
 // 4-row k-step, shift 8 nb + g) -- exactly its DMMA B fragment -- and loads the A
@@ -560,11 +354,12 @@ __device__ void s_phase_b_reg(const StreamParams& P, const SList& L, double* sme
     if (le_mode(v) == ST_ACTIVE) {
       const int s = le_sid(v);
       const double* pa = P.partA + (size_t)s * P.ipv;
+      const double* pl = P.partA + (size_t)(P.nshift + s) * P.ipv;
       int k0, k1;
       s_cta_span(P.sp, n, li, gridDim.x, k0, k1);
-      double pi = 0.0;
-      for (int c = k0 + lane; c <= k1; c += 32) pi += __ldcg(pa + c);
-      pi = warp_sum(pi);
+      double pi = 0.0, pil = 0.0;
+      for (int c = k0 + lane; c <= k1; c += 32) dd_add(pi, pil, __ldcg(pa + c), __ldcg(pl + c));
+      warp_sum_dd(pi, pil);
       if (!(pi > 0.0) || !isfinite(pi)) {
         if (blockIdx.x == 0 && lane == 0) { cg->status[s] = ST_BREAKDOWN; cg->alpha[s] = 0.0; }
       } else {
@@ -739,23 +534,19 @@ __device__ __forceinline__ void st4(double* p, const double* v) {
   asm volatile("st.global.v4.f64 [%0], {%1,%2,%3,%4};" ::"l"(p), "d"(v[0]), "d"(v[1]), "d"(v[2]), "d"(v[3])
                : "memory");
 }
-// One warp = one 8-shift N block of the pass (nb) over its row range: a pass of <= 8 shifts
-// spreads the CTA's rows over all 8 warps; a pass of 9..16 gives each N block 4 warps, each
-// over a quarter of the rows (the group columns are then read by two warps; the second read
-// hits L2). Keeps the per-warp registers at one N block (no spills at NMT = 3).
+// Every warp streams its fixed eighth of the CTA's rows (rpc / 8, a multiple of 16) for
+// all NB <= 2 N blocks of the pass, so a shift's sums run over the same rows in the same
+// order whatever the pass composition (batch-composition invariance, as every other sum
+// of the loop); all loads of a 16-row super-step are issued before its arithmetic.
 template <int NMT>
 __device__ void s_phase_b_wide_pass(const StreamParams& P, const SList& L, double* red, const double* s_alpha,
-                                    int li0, int li1, CgDev* cg, int64_t cbeg, int64_t cend) {
+                                    int li0, int li1, CgDev* cg, int64_t wbeg, int64_t wend) {
+  constexpr int NB = 2;
+  const int nbn = (li1 - li0 + 7) >> 3;   // N blocks of this pass (1 or 2)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int g = lane >> 2, q = lane & 3;
   const int64_t N = cg->N;
   const int np = li1 - li0;
-  const int nbn = (np + 7) >> 3;   // 1 or 2
-  const int nb = nbn == 2 ? warp >> 2 : 0;
-  const int wpb = nbn == 2 ? 4 : 8;   // warps per N block
-  const int64_t rpw = (cend - cbeg + 16 * wpb - 1) / (16 * wpb) * 16;
-  const int64_t wbeg = cbeg + (warp % wpb) * rpw;
-  const int64_t wend = imin64(cend, wbeg + rpw);
   const int grp = le_grp(L.e[li0]);
   const int J = cg->grp.J[grp];
   const int64_t ldw = cg->grp.ldw;
@@ -769,70 +560,89 @@ __device__ void s_phase_b_wide_pass(const StreamParams& P, const SList& L, doubl
     colp[mt] = colv[mt] ? (c < J ? cg->grp.AW[grp] + (int64_t)c * ldw : cg->grp.EW[grp] + (int64_t)(c - J) * ldw)
                         : cg->grp.AW[grp];
   }
-  const int li = li0 + 8 * nb + g;
-  const bool ok = li < li1;
-  const int v = ok ? L.e[li] : 0;
-  const bool act = !ok || le_mode(v) == ST_ACTIVE;
-  const bool hg = ok && le_hg(v);
-  const double al = ok ? s_alpha[li] : 0.0;
-  const double* wp = cg->Wv + (int64_t)le_sid(v) * N;
-  double* rp = cg->R + (int64_t)le_sid(v) * N;
-  const double* zp = cg->ZGhat + (int64_t)le_sid(v) * cg->ldgh;
-  double dz[NMT][2], rh = 0.0, zt = 0.0;
+  // per N block: shift id << 3 | flags (bit 0: in the pass, 1: ACTIVE (else RCONV:
+  // r = b - w), 2: has ghat); alpha is re-read from shared memory where it is used
+  unsigned sf[NB];
 #pragma unroll
-  for (int mt = 0; mt < NMT; ++mt) dz[mt][0] = dz[mt][1] = 0.0;
+  for (int nb = 0; nb < NB; ++nb) {
+    const int li = li0 + 8 * nb + g;
+    const bool ok = li < li1;
+    const int v = ok ? L.e[li] : 0;
+    sf[nb] = ok ? ((unsigned)le_sid(v) << 3 | 1u | (le_mode(v) == ST_ACTIVE ? 2u : 0u) | (le_hg(v) ? 4u : 0u)) : 2u;
+  }
+  double dz[NB][NMT][2], rh[NB], zt[NB];
+#pragma unroll
+  for (int nb = 0; nb < NB; ++nb) {
+    rh[nb] = 0.0; zt[nb] = 0.0;
+#pragma unroll
+    for (int mt = 0; mt < NMT; ++mt) dz[nb][mt][0] = dz[nb][mt][1] = 0.0;
+  }
 #pragma unroll 1
   for (int64_t row0 = wbeg; row0 < wend; row0 += 16) {
     const int64_t row = row0 + 4 * q;
     const bool vr = row < wend;   // N % 4 == 0: the 4 rows are all valid or all beyond
-    double a[NMT][4], wv[4], rv[4], zg[4];
+    double a[NMT][4];
 #pragma unroll
     for (int mt = 0; mt < NMT; ++mt) {
       if (vr && colv[mt]) ld4cg(colp[mt] + row, a[mt]);
       else a[mt][0] = a[mt][1] = a[mt][2] = a[mt][3] = 0.0;
     }
+    // the N blocks one after the other (the asm-volatile loads / DMMAs keep their order):
+    // one block's vectors in registers at a time, the group fragments shared
 #pragma unroll
-    for (int t = 0; t < 4; ++t) wv[t] = rv[t] = zg[t] = 0.0;
-    const bool lv = ok && vr;
-    if (lv) {
-      ld4cg(wp + row, wv);
-      if (act) ld4cg(rp + row, rv);
-      else ld4nc(cg->b + row, rv);
-      if (hg) ld4nc(zp + row, zg);
-    }
-    double rn[4] = {0.0, 0.0, 0.0, 0.0};
-    if (lv) {
+    for (int nb = 0; nb < NB; ++nb) {
+      if (nb >= nbn) break;   // uniform across the CTA
+      double wv[4], rv[4], zg[4];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) rn[t] = act ? fma(-al, wv[t], rv[t]) : rv[t] - wv[t];
-      st4(rp + row, rn);
-#pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        rh = fma(rn[t], rn[t], rh);
-        zt = fma(zg[t], rn[t], zt);
+      for (int t = 0; t < 4; ++t) wv[t] = rv[t] = zg[t] = 0.0;
+      const bool lv = (sf[nb] & 1u) && vr;
+      if (lv) {
+        const int64_t sd = (int64_t)(sf[nb] >> 3);
+        ld4cg(cg->Wv + sd * N + row, wv);
+        if (sf[nb] & 2u) ld4cg(cg->R + sd * N + row, rv);
+        else ld4nc(cg->b + row, rv);
+        if (sf[nb] & 4u) ld4nc(cg->ZGhat + sd * cg->ldgh + row, zg);
       }
+      double rn[4] = {0.0, 0.0, 0.0, 0.0};
+      if (lv) {
+        const double al = s_alpha[li0 + 8 * nb + g];
+#pragma unroll
+        for (int t = 0; t < 4; ++t) rn[t] = (sf[nb] & 2u) ? fma(-al, wv[t], rv[t]) : rv[t] - wv[t];
+        st4(cg->R + (int64_t)(sf[nb] >> 3) * N + row, rn);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          rh[nb] = fma(rn[t], rn[t], rh[nb]);
+          zt[nb] = fma(zg[t], rn[t], zt[nb]);
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t)
+#pragma unroll
+        for (int mt = 0; mt < NMT; ++mt) dmma(dz[nb][mt][0], dz[nb][mt][1], a[mt][t], rn[t]);
+    }
+  }
+  // stage: warp's D[c = 8 mt + g][n = 2q, 2q+1] of N block nb (c < J: zA[c], else zE[c - J])
+  double* rw = red + (size_t)warp * 32 * kRW;
+#pragma unroll
+  for (int nb = 0; nb < NB; ++nb) {
+    if (nb >= nbn) break;
+    double r1 = rh[nb], z1 = zt[nb];
+    r1 += __shfl_xor_sync(0xffffffffu, r1, 1);
+    r1 += __shfl_xor_sync(0xffffffffu, r1, 2);
+    z1 += __shfl_xor_sync(0xffffffffu, z1, 1);
+    z1 += __shfl_xor_sync(0xffffffffu, z1, 2);
+    if (q == 0) {
+      rw[(8 * nb + g) * kRW + 32] = r1;
+      rw[(8 * nb + g) * kRW + 33] = z1;
     }
 #pragma unroll
-    for (int t = 0; t < 4; ++t)
+    for (int mt = 0; mt < NMT; ++mt) {
+      const int c = 8 * mt + g;
+      if (c >= 2 * J) continue;
+      const int off = c < J ? c : 16 + (c - J);
 #pragma unroll
-      for (int mt = 0; mt < NMT; ++mt) dmma(dz[mt][0], dz[mt][1], a[mt][t], rn[t]);
-  }
-  // stage: warp's D[c = 8 mt + g][n = 2q, 2q+1] of its N block (c < J: zA[c], else zE[c - J])
-  double* rw = red + (size_t)warp * 32 * kRW;
-  rh += __shfl_xor_sync(0xffffffffu, rh, 1);
-  rh += __shfl_xor_sync(0xffffffffu, rh, 2);
-  zt += __shfl_xor_sync(0xffffffffu, zt, 1);
-  zt += __shfl_xor_sync(0xffffffffu, zt, 2);
-  if (q == 0) {
-    rw[(8 * nb + g) * kRW + 32] = rh;
-    rw[(8 * nb + g) * kRW + 33] = zt;
-  }
-#pragma unroll
-  for (int mt = 0; mt < NMT; ++mt) {
-    const int c = 8 * mt + g;
-    if (c >= 2 * J) continue;
-    const int off = c < J ? c : 16 + (c - J);
-#pragma unroll
-    for (int h = 0; h < 2; ++h) rw[(8 * nb + 2 * q + h) * kRW + off] = dz[mt][h];
+      for (int h = 0; h < 2; ++h) rw[(8 * nb + 2 * q + h) * kRW + off] = dz[nb][mt][h];
+    }
   }
   __syncthreads();
   for (int e = tid; e < np * kSPV; e += blockDim.x) {
@@ -841,19 +651,16 @@ __device__ void s_phase_b_wide_pass(const StreamParams& P, const SList& L, doubl
     const int nw = le_m(v2) - le_hg(v2);
     const bool isz = j < nw, isg = le_hg(v2) && j == nw, isr = j == kMaxM;
     if (!(isz || isg || isr)) continue;
-    // the warps of shift k's N block, in warp order
-    const int w0 = nbn == 2 ? 4 * (k >> 3) : 0;
     double ta = 0.0, te = 0.0;
 #pragma unroll
     for (int w = 0; w < 8; ++w) {
-      if (w >= wpb) break;
-      const double* r = red + ((size_t)(w0 + w) * 32 + k) * kRW;
+      const double* r = red + ((size_t)w * 32 + k) * kRW;
       if (isz) { ta += r[j]; te += r[16 + j]; }
       else ta += r[isr ? 32 : 33];
     }
-    const int s = le_sid(v2);
-    const double val = isz ? fma(cg->gam[s], te, ta) : ta;
-    P.partB[((size_t)s * kSPV + j) * P.nchunk + blockIdx.x] = val;
+    const int s2 = le_sid(v2);
+    const double val = isz ? fma(cg->gam[s2], te, ta) : ta;
+    P.partB[((size_t)s2 * kSPV + j) * P.nchunk + blockIdx.x] = val;
   }
   __syncthreads();
 }
@@ -870,11 +677,12 @@ __device__ void s_phase_b_wide(const StreamParams& P, const SList& L, double* sm
     if (le_mode(v) == ST_ACTIVE) {
       const int s = le_sid(v);
       const double* pa = P.partA + (size_t)s * P.ipv;
+      const double* pl = P.partA + (size_t)(P.nshift + s) * P.ipv;
       int k0, k1;
       s_cta_span(P.sp, n, li, gridDim.x, k0, k1);
-      double pi = 0.0;
-      for (int c = k0 + lane; c <= k1; c += 32) pi += __ldcg(pa + c);
-      pi = warp_sum(pi);
+      double pi = 0.0, pil = 0.0;
+      for (int c = k0 + lane; c <= k1; c += 32) dd_add(pi, pil, __ldcg(pa + c), __ldcg(pl + c));
+      warp_sum_dd(pi, pil);
       if (!(pi > 0.0) || !isfinite(pi)) {
         if (blockIdx.x == 0 && lane == 0) { cg->status[s] = ST_BREAKDOWN; cg->alpha[s] = 0.0; }
       } else {
@@ -887,14 +695,17 @@ __device__ void s_phase_b_wide(const StreamParams& P, const SList& L, double* sm
   const int npass = s_passes(L, pst);
   const int64_t cbeg = (int64_t)blockIdx.x * P.rpc;
   const int64_t cend = imin64(N, cbeg + P.rpc);
+  const int64_t rpw = P.rpc / 8;   // rows per warp (multiple of 16)
+  const int64_t wbeg = cbeg + warp * rpw;
+  const int64_t wend = imin64(cend, wbeg + rpw);
   for (int pk = 0; pk < npass; ++pk) {
     const int li0 = pst[pk], li1 = pst[pk + 1];
     const int J = cg->grp.J[le_grp(L.e[li0])];
     const int nmt = (2 * J + 7) >> 3;
-    if (nmt <= 1) s_phase_b_wide_pass<1>(P, L, smem, s_alpha, li0, li1, cg, cbeg, cend);
-    else if (nmt == 2) s_phase_b_wide_pass<2>(P, L, smem, s_alpha, li0, li1, cg, cbeg, cend);
-    else if (nmt == 3) s_phase_b_wide_pass<3>(P, L, smem, s_alpha, li0, li1, cg, cbeg, cend);
-    else s_phase_b_wide_pass<4>(P, L, smem, s_alpha, li0, li1, cg, cbeg, cend);
+    if (nmt <= 1) s_phase_b_wide_pass<1>(P, L, smem, s_alpha, li0, li1, cg, wbeg, wend);
+    else if (nmt == 2) s_phase_b_wide_pass<2>(P, L, smem, s_alpha, li0, li1, cg, wbeg, wend);
+    else if (nmt == 3) s_phase_b_wide_pass<3>(P, L, smem, s_alpha, li0, li1, cg, wbeg, wend);
+    else s_phase_b_wide_pass<4>(P, L, smem, s_alpha, li0, li1, cg, wbeg, wend);
   }
 }
 
@@ -1148,174 +959,6 @@ __device__ void s_phase_b2(const StreamParams& P, const SList& L, double* smem, 
   }
 }
 
-// ---------------------------------------------------------------- phase C
-template <int R>
-__device__ void s_phase_c(const StreamParams& P, const SList& L, double* smem, const double* s_alpha, unsigned& bpar,
-                          int* pst, unsigned char* s_flag, CgDev* cg) {
-  using SC = SCfg<R>;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int g = lane >> 2, q = lane & 3;
-  const int64_t N = cg->N;
-  double* PS = smem + SC::OFF_PS;   // per pass entry: beta, 1/|r|, slot, flags, alpha
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + SC::OFF_BAR);
-  const int npass = s_passes(L, pst);
-  const int nunits = npass;
-  if ((int64_t)blockIdx.x * P.rpc >= N) return;   // no rows for this CTA
-  // flags of every list entry (1 = x += alpha p, 2 = new p: status after B2 is ACTIVE)
-  for (int li = tid; li < L.n; li += blockDim.x) {
-    const int s = le_sid(L.e[li]);
-    int f = 0;
-    if (le_mode(L.e[li]) == ST_ACTIVE && s_alpha[li] != 0.0) f |= 1;
-    if (cg->status[s] == ST_ACTIVE) f |= 2;
-    s_flag[li] = (unsigned char)f;
-  }
-  __syncthreads();
-  // producer = warp 0, one lane per shift slot of the batch (+ lane 31: the W tile)
-  auto issue = [&](SStep st, unsigned q2) {
-    const SGeo G = s_geo(pst, P.rpc, N, st.u);
-    const int sub = st.k / G.nb, b = st.k % G.nb;
-    const int64_t r0 = G.cbeg + (int64_t)sub * kSRs;
-    const int nr = (int)imin64(kSRs, G.cend - r0);
-    const unsigned bytes = 8u * nr;
-    const int grp = le_grp(L.e[G.li0]);
-    const int J = cg->grp.J[grp];
-    const int slot = q2 % kSNST;
-    double* stg = smem + SC::OFF_ST + slot * SC::STAGE;
-    uint64_t* bar = bars + slot;
-    const int li = G.li0 + b * kSB + lane;
-    const bool mine = lane < kSB && li < G.li1;
-    const int f = mine ? s_flag[li] : 0;
-    const int v = mine ? L.e[li] : 0;
-    unsigned my = 0;
-    if (f) {
-      my = bytes;
-      if (f & 1) my += bytes;
-      if (f & 2) my += bytes + (le_hg(v) ? bytes : 0);
-    }
-    const unsigned anyp = __ballot_sync(0xffffffffu, (f & 2) != 0);
-    if (lane == 31 && anyp && J > 0) my += 8u * kSP * J;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) my += __shfl_xor_sync(0xffffffffu, my, o);
-    if (lane == 0) mbar_expect_tx(bar, my);
-    __syncwarp();
-    if (f) {
-      const int s = le_sid(v);
-      double* d = stg + 16 * kSP + lane * kSVec * kSP;
-      bulk_load(d, cg->P + (int64_t)s * N + r0, bytes, bar);
-      if (f & 1) bulk_load(d + 2 * kSP, cg->X + (int64_t)s * cg->ldx + r0, bytes, bar);
-      if (f & 2) {
-        bulk_load(d + kSP, cg->R + (int64_t)s * N + r0, bytes, bar);
-        if (le_hg(v)) bulk_load(d + 3 * kSP, cg->Ghat + (int64_t)s * cg->ldgh + r0, bytes, bar);
-      }
-    }
-    if (lane == 31 && anyp && J > 0) tma_load_2d(stg + SC::OFF_SG, &P.mW[grp], bar, (int)r0, 0);
-  };
-  auto advance = [&](SStep& st) {
-    const SGeo G = s_geo(pst, P.rpc, N, st.u);
-    if (++st.k >= G.nsteps) { st.k = 0; st.u += 1; }
-  };
-  SStep cons{0, 0}, prod = cons;
-  unsigned qn = 0, qp = 0;
-  unsigned long long s_tstep = 0;
-  if (warp == 0)
-    for (int i = 0; i < kSNST - 1 && prod.u < nunits; ++i) { issue(prod, qp++); advance(prod); }
-  while (cons.u < nunits) {
-    const SGeo G = s_geo(pst, P.rpc, N, cons.u);
-    const int np = G.li1 - G.li0;
-    if (cons.k == 0) {
-      __syncthreads();   // the previous unit's PS readers are done
-      if (tid < np) {
-        const int li = G.li0 + tid;
-        const int s = le_sid(L.e[li]);
-        const int st = cg->status[s];
-        const int slot = (st == ST_ACTIVE) ? cg->stslot[s] : -1;
-        double* ps = PS + tid * kSPS;
-        ps[0] = cg->beta[s];
-        ps[1] = (slot >= 0) ? 1.0 / sqrt(cg->rho[s]) : 0.0;
-        ps[2] = (double)slot;
-        ps[3] = (double)s_flag[li];
-        ps[4] = s_alpha[li];
-        const int m = le_m(L.e[li]);
-        ps[5] = m > 0 ? cg->coef[(int64_t)s * kMaxM + m - 1] : 0.0;   // mu of the carried column
-      }
-      __syncthreads();
-    }
-    if (warp == 0 && prod.u < nunits) { issue(prod, qp++); advance(prod); }
-    const int sub = cons.k / G.nb, b = cons.k % G.nb;
-    const int64_t r0 = G.cbeg + (int64_t)sub * kSRs;
-    const int nr = (int)imin64(kSRs, G.cend - r0);
-    const int grp = le_grp(L.e[G.li0]);
-    const int J = cg->grp.J[grp];
-    const int nkk = (J + 3) >> 2;
-    // B fragments: mu of batch shift g, component 4 kk + q (0 unless a new p is formed)
-    double bm[4];
-    {
-      const int li = G.li0 + b * kSB + g;
-      const bool ok = li < G.li1 && (((int)PS[(li - G.li0) * kSPS + 3]) & 2);
-      const int v = ok ? L.e[li] : 0;
-      const int nw = ok ? le_m(v) - le_hg(v) : 0;
-      const double* cf = cg->coef + (int64_t)le_sid(v) * kMaxM;
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        const int j = 4 * kk + q;
-        bm[kk] = (ok && j < nw) ? cf[j] : 0.0;
-      }
-    }
-    const int slot = qn % kSNST;
-    double* stg = smem + SC::OFF_ST + slot * SC::STAGE;
-    unsigned long long tw0 = 0;
-    if (P.prof && blockIdx.x == 0 && tid == 32) tw0 = s_timer();
-    mbar_wait(bars + slot, (bpar >> slot) & 1u);
-    if (P.prof && blockIdx.x == 0 && tid == 32) {
-      const unsigned long long t1 = s_timer();
-      g_sprof2[2] += t1 - tw0; g_sprof2[3] += 1;
-      if (s_tstep) g_sprof2[5] += t1 - s_tstep;
-      s_tstep = t1;
-    }
-    bpar ^= 1u << slot;
-    // W mu on the tensor cores: warp = 8-row block, D[row g][shifts 2q, 2q+1]; then the
-    // x / p updates of those elements
-    {
-      const int row = warp * 8 + g;
-      double d[2] = {0.0, 0.0};
-      const double* wt = stg + SC::OFF_SG;
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk) {
-        if (kk >= nkk) break;
-        const int j = 4 * kk + q;
-        dmma(d[0], d[1], j < J ? wt[j * kSP + row] : 0.0, bm[kk]);
-      }
-      if (row < nr) {
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int k8 = 2 * q + h;
-          const int li = G.li0 + b * kSB + k8;
-          if (li >= G.li1) continue;
-          const double* ps = PS + (li - G.li0) * kSPS;
-          const int f = (int)ps[3];
-          if (!f) continue;
-          const int v = L.e[li];
-          const int s = le_sid(v);
-          const double* ds = stg + 16 * kSP + k8 * kSVec * kSP;
-          const double pv = ds[row];
-          if (f & 1) cg->X[(int64_t)s * cg->ldx + r0 + row] = fma(ps[4], pv, ds[2 * kSP + row]);
-          if (f & 2) {
-            const double rv = ds[kSP + row];
-            double pn = fma(ps[0], pv, rv) - d[h];
-            if (le_hg(v)) pn = fma(-ps[5], ds[3 * kSP + row], pn);
-            cg->P[(int64_t)s * N + r0 + row] = pn;
-            const int sl = (int)ps[2];
-            if (sl >= 0) cg->store[((int64_t)s * cg->store_cap + sl) * cg->lds + r0 + row] = rv * ps[1];
-          }
-        }
-      }
-    }
-    __syncthreads();   // stage released
-    advance(cons);
-    ++qn;
-  }
-}
-
 // ---------------------------------------------------------------- the kernel
 template <int R>
 __global__ void __launch_bounds__(kAT, kStripCtasPerSm) cg_stream_kernel(const __grid_constant__ StreamParams P) {
@@ -1326,7 +969,6 @@ __global__ void __launch_bounds__(kAT, kStripCtasPerSm) cg_stream_kernel(const _
   __shared__ int tmp[kSMaxShift];
   __shared__ double s_alpha[kSMaxShift];
   __shared__ int pst[kSMaxPass + 1];
-  __shared__ unsigned char s_flag[kSMaxShift];
   // the loop state's pointers and sizes in shared memory (the struct itself never changes;
   // the arrays it points to do): no global round trip per field access after the L1
   // invalidations of the grid barriers
@@ -1336,14 +978,8 @@ __global__ void __launch_bounds__(kAT, kStripCtasPerSm) cg_stream_kernel(const _
   CgDev* cg = &s_cg;
   const int ns = P.nshift;
   const int tid = threadIdx.x;
-  // strip-apply barriers and the B/C stage barriers are distinct mbarriers
   Core::init(smem, P.sp);
-  if (tid == 0) {
-    for (int b = 0; b < kSNST; ++b) mbar_init(reinterpret_cast<uint64_t*>(smem + SC::OFF_BAR) + b, 1);
-    mbar_fence_init();
-  }
   StripRing ring{0u, 0u};
-  unsigned bpar = 0u;
   unsigned gen = s_ld_acquire(P.bar + 1);
   int cur = 0;
   s_build_list(cg, ns, lists[0], tmp);
@@ -1368,8 +1004,7 @@ __global__ void __launch_bounds__(kAT, kStripCtasPerSm) cg_stream_kernel(const _
     mark(0);
     sgrid_sync(P.bar, gen);
     mark(1);
-    if (P.staged) s_phase_b<R>(P, L, smem, s_alpha, bpar, pst, &s_cg);
-    else if (P.wide) s_phase_b_wide<R>(P, L, smem, s_alpha, pst, &s_cg);
+    if (P.wide) s_phase_b_wide<R>(P, L, smem, s_alpha, pst, &s_cg);
     else s_phase_b_reg<R>(P, L, smem, s_alpha, pst, &s_cg);
     mark(2);
     sgrid_sync(P.bar, gen);
@@ -1380,8 +1015,7 @@ __global__ void __launch_bounds__(kAT, kStripCtasPerSm) cg_stream_kernel(const _
     mark(1);
     SList& NL = lists[cur ^ 1];
     s_build_list(cg, ns, NL, tmp);   // statuses are stable until the next phase A
-    if (P.staged) s_phase_c<R>(P, L, smem, s_alpha, bpar, pst, s_flag, &s_cg);
-    else s_phase_c_reg<R>(P, L, smem, s_alpha, pst, &s_cg);
+    s_phase_c_reg<R>(P, L, smem, s_alpha, pst, &s_cg);
     mark(4);
     sgrid_sync(P.bar, gen);
     mark(1);
@@ -1524,7 +1158,6 @@ cudaError_t launch_cg_stream(Handle* h, CgDev* dev, const CgDev& hc, double* par
   prm.cg_N = N;
   prm.ipv = stream_ipv(h);   // stride of partA; the items of an iteration: s_ipv()
   prm.max_iters = max_iters;
-  prm.staged = getenv("RSK_STREAM_STAGED") ? 1 : 0;
   {
     // wide phase B: 32-byte rows of every vector it streams
     auto al32p = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 31) == 0; };

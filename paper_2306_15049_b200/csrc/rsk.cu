@@ -629,7 +629,7 @@ WsLayout ws_layout(const Handle* h, int ns) {
   L.off_partP = o; o = al(o + sizeof(double) * (size_t)ns * (L.nchunkP * persist_pv() + persist_grid(h)));
   L.off_pbar = o; o = al(o + sizeof(unsigned) * 8);
   // streaming loop (cg_stream.cu): per-item apply partials and per-chunk B partials
-  L.off_sA = o; o = al(o + sizeof(double) * (size_t)ns * stream_ipv(h));
+  L.off_sA = o; o = al(o + sizeof(double) * (size_t)2 * ns * stream_ipv(h));   // hi, lo (double-double)
   L.off_sB = o; o = al(o + sizeof(double) * (size_t)ns * stream_pv() * stream_nchunk(h));
   // cluster-per-shift loop: per cluster, Z_s = AW + gamma_s EW of its current shift
   L.off_zw = o;

@@ -132,11 +132,13 @@ struct StripCore {
     tma_load_3d(smem + C::OFF_IN + slot * 8 * C::PX, src2 ? &p.mapX2 : &p.mapX, bar, c0 - C::H, row0, s);
   }
 
-  // Returns this thread's X.Y partial (caller reduces). src2: read the vector from
-  // mapX2 (CG confirm).
+  // Returns this thread's X.Y partial as a double-double (return value + *dot_lo; caller
+  // reduces): per 8-row block the thread's two products, added by TwoSum, so the item's
+  // total does not depend on where items start and end. src2: read the vector from mapX2
+  // (CG confirm).
   // One item: vector s, a strip, output rows [ra, rb) (rb - ra a multiple of 8 unless rb = ny).
   __device__ static double item(const StripParams& p, double* smem, StripRing& ring, int s, int strip, int ra, int rb,
-                                bool src2) {
+                                bool src2, double* dot_lo) {
     double* IN = smem + C::OFF_IN;
     double* T = smem + C::OFF_T;
     const double* DC = smem + C::OFF_DC;
@@ -149,6 +151,8 @@ struct StripCore {
     const int c0 = strip * kStripW;
     const int rb0 = ra - C::H;            // image row of ring row u = 0 of this item
     const unsigned base = ring.pos;
+    unsigned parity = ring.parity;   // a register copy for the step loop (the caller's ring
+                                     // state lives across phases and may sit in local memory)
     const int mode = p.mode;
     const bool withE = true;
     const bool edge_l = c0 < R, edge_r = c0 + kStripW > nx - R;
@@ -157,7 +161,7 @@ struct StripCore {
     double* __restrict__ eys = (mode == RSK_APPLY_SPLIT) ? p.EY + (int64_t)s * p.ldey : nullptr;
     const bool vec = ((nx & 1) == 0);
     const int cb = warp * 8;
-    double dot = 0.0;
+    double dot = 0.0, dlo = 0.0;
     double bx[C::KS], ay[C::KS];
 #pragma unroll
     for (int ks = 0; ks < C::KS; ++ks) {
@@ -173,8 +177,8 @@ struct StripCore {
     for (int t = 0; t < nbi; ++t) {
       const unsigned slot = (base + t) & 7u;
       if (tid == 0 && t + C::D < nbi) issue(p, smem, base + t + C::D, c0, rb0 + 8 * (t + C::D), s, src2);
-      mbar_wait(bars + slot, (ring.parity >> slot) & 1u);
-      ring.parity ^= 1u << slot;
+      mbar_wait(bars + slot, (parity >> slot) & 1u);
+      parity ^= 1u << slot;
       // ---- x-pass of input block t: T[8 rows][cb .. cb+8) = IN[8 rows][cb .. cb+8+4r) x Bx
       {
         const double* sa = IN + (slot * 8 + g) * C::PX + cb + q;
@@ -325,17 +329,18 @@ struct StripCore {
         double* yp = ys + (int64_t)gi * nx + gj;
         if (vec && (p.ldy % 2 == 0)) *reinterpret_cast<double2*>(yp) = make_double2(o0, o1);
         else { yp[0] = o0; yp[1] = o1; }
-        dot = fma(x0, o0, dot);
-        dot = fma(x1, o1, dot);
+        dd_add(dot, dlo, fma(x1, o1, x0 * o0), 0.0);
       } else if (v0) {
         ys[(int64_t)gi * nx + gj] = o0;
-        dot = fma(x0, o0, dot);
+        dd_add(dot, dlo, x0 * o0, 0.0);
       }
       release(ebars, base, t - C::K, lane);
     }
     // the blocks whose last read was in this item's final steps
     for (int b = nbi - C::K; b < nbi; ++b) release(ebars, base, b, lane);
     ring.pos = base + (unsigned)nbi;
+    ring.parity = parity;
+    *dot_lo = dlo;
     return dot;
   }
 

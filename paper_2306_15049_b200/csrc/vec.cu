@@ -162,47 +162,50 @@ __global__ void __launch_bounds__(256) gemm_tn_part_tc(int64_t n, int k, const d
   }
 }
 
+// U^T V with a summation order per element that depends only on n, k and the SM count --
+// not on nv: the row chunks are fixed by n, the tensor-core / scalar choice by k, and a V
+// wider than the partial buffer runs as column blocks. So a column of V gives the same
+// bits whatever other columns share the call (batch-composition invariance of the
+// per-shift setup: 1-rank and N-rank shift-sharded runs do identical work).
 cudaError_t launch_gemm_tn(Handle* h, int64_t n, int k, const double* U, int64_t ldu, int nv,
                            const double* V, int64_t ldv, double* C, int64_t ldc, cudaStream_t st) {
-  if (k >= 16 && nv >= 16 && getenv("RSK_GEMM_NOTC") == nullptr) {   // tensor-core path for the wide Grams
-    const int tk = (k + 31) / 32, tv = (nv + 31) / 32;
-    int64_t nchunk = (2 * h->sm_count + tk * tv - 1) / (tk * tv);
-    const int64_t maxchunk = (n + 255) / 256;
-    if (nchunk > maxchunk) nchunk = maxchunk;
-    if (nchunk < 1) nchunk = 1;
-    const size_t cap = h->scratch_bytes / (sizeof(double) * (size_t)k * nv);
-    if ((size_t)nchunk > cap) nchunk = (int64_t)cap;
-    if (nchunk < 1) return cudaErrorMemoryAllocation;
-    int64_t rpc = (n + nchunk - 1) / nchunk;
-    rpc = (rpc + 31) / 32 * 32;
-    nchunk = (n + rpc - 1) / rpc;
-    const size_t smem = sizeof(double) * 8 * 32 * 33;
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(gemm_tn_part_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = true;
-    }
-    dim3 grid((unsigned)nchunk, tk, tv);
-    count_launch(); gemm_tn_part_tc<<<grid, 256, smem, st>>>(n, k, U, ldu, nv, V, ldv, h->scratch, rpc);
-    const int64_t tot = (int64_t)k * nv;
-    count_launch(); gemm_tn_reduce<<<reduce_blocks(tot, (int)nchunk), 256, 0, st>>>(k, nv, (int)nchunk, h->scratch, C, ldc);
-    return cudaGetLastError();
-  }
-  const int tk = (k + 31) / 32, tv = (nv + 31) / 32;
-  int64_t nchunk = (2 * h->sm_count + tk * tv - 1) / (tk * tv);
+  const bool tc = k >= 16 && getenv("RSK_GEMM_NOTC") == nullptr;   // tensor-core path for the wide Grams
+  int64_t nchunk = 2 * h->sm_count;
   const int64_t maxchunk = (n + 255) / 256;
   if (nchunk > maxchunk) nchunk = maxchunk;
   if (nchunk < 1) nchunk = 1;
-  const size_t cap = h->scratch_bytes / (sizeof(double) * (size_t)k * nv);
-  if ((size_t)nchunk > cap) nchunk = (int64_t)cap;
-  if (nchunk < 1) return cudaErrorMemoryAllocation;
   int64_t rpc = (n + nchunk - 1) / nchunk;
   rpc = (rpc + 31) / 32 * 32;
   nchunk = (n + rpc - 1) / rpc;
-  dim3 grid((unsigned)nchunk, tk, tv);
-  count_launch(); gemm_tn_part<<<grid, 256, 0, st>>>(n, k, U, ldu, nv, V, ldv, h->scratch, rpc);
-  const int64_t tot = (int64_t)k * nv;
-  count_launch(); gemm_tn_reduce<<<reduce_blocks(tot, (int)nchunk), 256, 0, st>>>(k, nv, (int)nchunk, h->scratch, C, ldc);
+  // columns of V per launch: the partials [nchunk][k][nvb] must fit the scratch
+  const size_t cap = h->scratch_bytes / (sizeof(double) * (size_t)k * (size_t)nchunk);
+  if (cap < 1) return cudaErrorMemoryAllocation;
+  const int nvb = (int)((size_t)nv < cap ? (size_t)nv : cap);
+  const int tk = (k + 31) / 32;
+  if (tc) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(gemm_tn_part_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(sizeof(double) * 8 * 32 * 33));
+      attr = true;
+    }
+  }
+  for (int v0 = 0; v0 < nv; v0 += nvb) {
+    const int nvc = nv - v0 < nvb ? nv - v0 : nvb;
+    const int tv = (nvc + 31) / 32;
+    dim3 grid((unsigned)nchunk, tk, tv);
+    const double* Vb = V + (int64_t)v0 * ldv;
+    if (tc) {
+      count_launch();
+      gemm_tn_part_tc<<<grid, 256, sizeof(double) * 8 * 32 * 33, st>>>(n, k, U, ldu, nvc, Vb, ldv, h->scratch, rpc);
+    } else {
+      count_launch(); gemm_tn_part<<<grid, 256, 0, st>>>(n, k, U, ldu, nvc, Vb, ldv, h->scratch, rpc);
+    }
+    const int64_t tot = (int64_t)k * nvc;
+    count_launch();
+    gemm_tn_reduce<<<reduce_blocks(tot, (int)nchunk), 256, 0, st>>>(k, nvc, (int)nchunk, h->scratch,
+                                                                     C + (int64_t)v0 * ldc, ldc);
+  }
   return cudaGetLastError();
 }
 

@@ -123,9 +123,42 @@ def test_persistent_loop_multi_pass_two_groups(torch_dev, monkeypatch, n, r, nL,
         assert np.linalg.norm(Xh[l] - x) <= 1e-8 * np.linalg.norm(x), l
         g_ref = x - (_CTX["xp"][:, l] if _CTX["has_xp"][l] else 0.0)
         assert np.linalg.norm(Gh[l] - g_ref) <= 1e-8 * np.linalg.norm(x), l
-        # the accounting beyond the iterations (r_p apply, confirmations) is identical
-        assert int(res["applies"][l]) - int(res["iters"][l]) == ap - it, l
+        # the accounting beyond the iterations (r_p apply, true-residual confirmations, G14):
+        # identical up to one confirmation -- whether the recursive residual reaches tol one
+        # iteration before the true one is a rounding-order event (reading G27)
+        assert abs((int(res["applies"][l]) - int(res["iters"][l])) - (ap - it)) <= 1, l
     # iterations: reading G27 -- +-2 on >= 95 % of the shifts, +-max(2, 1 %) on all
     # (summation order alone moves counts by up to ~1 % at these condition numbers)
     d_it = np.abs(res["iters"].astype(np.int64) - its)
     assert np.mean(d_it <= 2) >= 0.95 and np.all(d_it <= np.maximum(2, np.ceil(0.01 * its))), (res["iters"], its)
+
+
+def test_stream_loop_batch_composition_invariant(torch_dev, monkeypatch):
+    """A shift's trajectory in the streaming loop does not depend on which other shifts
+    share its batch: the phase-A p.w partials are double-double per CTA block range (their
+    rounded total is grouping-independent) and every other sum has a fixed order in N and
+    the launch geometry. So a sub-batch reproduces the full batch's solutions and
+    iteration counts bit for bit -- the property that makes an N-GPU shift-sharded run
+    (shard.py) do exactly the 1-GPU work."""
+    monkeypatch.setenv("RSK_CG_NOCLUSTER", "1")
+    monkeypatch.setenv("RSK_CG_STREAM", "1")
+    torch, dev = torch_dev
+    import dataclasses
+    n, r, nL, nR = 100, 7, 40, 9
+    M = nL + nR
+    cfg = dataclasses.replace(S.small_config(n=n, M=M, r=r, sigma=1.0 + 0.3 * r, tol=1e-10), maxit=20000)
+    gam = np.logspace(-4, 1.5, M)
+    sol, groups, ghat, X0 = _setup(torch, dev, cfg, nL, nR, 12, 900 + n, gam)
+    X = X0.clone()
+    res = sol.cg(list(range(M)), X, _CTX["has_xp"], groups=groups, ghat=ghat)
+    assert int(res["prof"][7]) == 3
+    sub = [3, 17, 25, 39, 41, 44, 47]
+    Xs = X0[sub].clone()
+    gs = dict(groups, of_shift=np.asarray(groups["of_shift"])[sub])
+    Gh, ZGh, hg = ghat
+    rs = sol.cg(sub, Xs, _CTX["has_xp"][sub], groups=gs, ghat=(Gh[sub].contiguous(), ZGh[sub].contiguous(),
+                                                               np.asarray(hg)[sub]))
+    assert int(rs["prof"][7]) == 3
+    np.testing.assert_array_equal(rs["iters"], res["iters"][sub])
+    np.testing.assert_array_equal(rs["applies"], res["applies"][sub])
+    assert torch.equal(Xs, X[sub]), "sub-batch solutions must be bitwise equal to the full batch's"
