@@ -79,27 +79,25 @@ __device__ __forceinline__ unsigned long long s_timer() {
   return t;
 }
 
-// sense-reversing grid barrier (cooperative launch: all CTAs co-resident). Generic and
-// async-proxy (TMA, bulk copy) accesses on either side are ordered by the proxy fences.
-__device__ __forceinline__ void sgrid_sync(unsigned* bar, unsigned& gen) {
+// counting grid barrier (cooperative launch: all CTAs co-resident): bar[0] counts the
+// arrivals since the launch (the host zeroes it before every launch); barrier i of the
+// launch completes when it reaches i x gridDim. Thread 0 arrives with a fire-and-forget
+// release reduction and polls with acquire loads -- one L2 round trip less than the
+// sense-reversing form (last arriver resets and releases). Generic and async-proxy (TMA)
+// accesses on either side are ordered by the proxy fences.
+__device__ __forceinline__ void sgrid_sync(unsigned* bar, unsigned& target) {
   asm volatile("fence.proxy.async.global;\n" ::: "memory");
   asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
   __syncthreads();
+  target += gridDim.x;
   if (threadIdx.x == 0) {
     __threadfence();
-    const unsigned arrived = atomicAdd(bar, 1u) + 1u;
-    if (arrived == gridDim.x) {
-      bar[0] = 0u;
-      __threadfence();
-      s_st_release(bar + 1, gen + 1u);
-    } else {
-      while (s_ld_acquire(bar + 1) == gen) {
-      }
+    asm volatile("red.release.gpu.global.add.u32 [%0], 1;\n" ::"l"(bar) : "memory");
+    while (s_ld_acquire(bar) < target) {
     }
     __threadfence();
     asm volatile("fence.proxy.async.global;\n" ::: "memory");
   }
-  gen += 1u;
   __syncthreads();
 }
 
@@ -980,7 +978,7 @@ __global__ void __launch_bounds__(kAT, kStripCtasPerSm) cg_stream_kernel(const _
   const int tid = threadIdx.x;
   Core::init(smem, P.sp);
   StripRing ring{0u, 0u};
-  unsigned gen = s_ld_acquire(P.bar + 1);
+  unsigned gen = 0u;   // barrier target (bar[0] is zeroed before the launch)
   int cur = 0;
   s_build_list(cg, ns, lists[0], tmp);
   sgrid_sync(P.bar, gen);

@@ -956,6 +956,7 @@ extern "C" rsk_status rsk_cg_recycled_batch(rsk_handle h, const rsk_cg_desc* d, 
     int64_t pguard = 0;
     for (;;) {
       bool ok = false;
+      RSK_CUDA(cudaMemsetAsync(pbar, 0, sizeof(unsigned), st));   // the counting grid barrier
       RSK_CUDA(launch_cg_stream(h, dev, hc, reinterpret_cast<double*>(base + L.off_sA),
                                 reinterpret_cast<double*>(base + L.off_sB), pbar, pna, pna + 1, kChunkIters, st, &ok));
       if (!ok) break;

@@ -4,8 +4,8 @@ the principal recycle space U and AU are broadcast once per outer step").
 Reading D3 makes all shifts of an outer step independent, so one exchange per outer
 step suffices and the CG loop has no per-iteration communication:
 
-  rank 0     builds U~ (seeds + Ritz at k = 0, [V_i1, X^(k-1)] after), A U~, E U~
-  broadcast  U~, A U~, E U~  (3 x n_c x N doubles)
+  rank 0     builds U~ (seeds + Ritz at k = 0, [V_i1, X^(k-1)] after)
+  broadcast  U~ (n_c x N doubles); A U~, E U~ column-split across the ranks, all-gathered
   all ranks  anchor QR + Grams, guesses and group blocks (deterministic, identical)
   each rank  batched deflated CG on ITS shifts (assignment below)
   allgather  X^(k), G^(k) (M x N each), iteration counts, L-curve norms
@@ -16,10 +16,12 @@ LPT of group_lpt_assign on the previous step's per-shift iteration counts (the c
 model of SURVEY §8(e)), ties broken by shift index, so every rank computes the same
 assignment.
 
-The cluster-per-shift loop (images in L2) computes each shift independently of the
-batch it shares, so a G-rank run reproduces the 1-rank solutions bit for bit there; the
-lockstep loops for larger images sum some partials per CTA range of the whole batch, so
-their solutions agree to rounding (iterations within the stepwise bars), not bitwise.
+Every device loop computes a shift independently of the batch it shares: the
+cluster-per-shift loop trivially, the streaming lockstep loop (images beyond L2) by fixed
+row ranges and double-double p.w partials, and U^T V by row chunks fixed by N
+(DESIGN.md §4.2). So a G-rank run reproduces the 1-rank solutions and iteration counts
+bit for bit (validated for C4 by tools/validate_multirank.sh; the tiled persistent loop
+between those sizes is not covered by this guarantee).
 This module holds only host logic and collectives; it works on CPU tensors under gloo
 (tests) and on CUDA tensors under NCCL (bench).
 """
