@@ -3,8 +3,9 @@ and the nested solve use (the oracle runs its per-shift solves in forked process
 per host core -- its only parallelism, across shifts):
 
 * C4 (1024 x 1024, 15 x 15 PSF, all 128 shifts, two groups of |J| = 12, carried columns,
-  principal guesses): the persistent lockstep loop over the whole ladder for a fixed 30
-  iterations; eight sampled shifts (l = 1, 17, ..., 113, 128) are recomputed by the oracle
+  principal guesses) and C3 (512 x 512, 64 shifts, |J| = 10): the persistent lockstep loop
+  over the whole ladder for a fixed 30 iterations; nine sampled shifts (C4: l = 1, 17,
+  ..., 113, 128) are recomputed by the oracle
   one by one and compared element by element (the iterates of 30 CG steps agree to
   rounding: 1e-10 relative 2-norm) with the same apply accounting.
 * C2 (256 x 256, 32 shifts): outer steps k = 0 and k = 1 stepwise (reading G28: the
@@ -86,10 +87,13 @@ def torch_dev():
     return torch, torch.device("cuda", 0)
 
 
-def test_c4_full_ladder_fixed_iterations(torch_dev):
+@pytest.mark.parametrize("cfgname", ["C3", "C4"])
+def test_c4_full_ladder_fixed_iterations(torch_dev, cfgname):
+    """C4 (and C3: 512^2, 64 shifts, |J| = 10, the same streaming loop at another
+    geometry) -- the whole ladder for 30 lockstep iterations, sampled shifts by the oracle."""
     torch, dev = torch_dev
     from paper_2306_15049_b200.pipeline import GpuSolver
-    cfg = dataclasses.replace(S.CONFIGS["C4"], tol=1e-30, maxit=30)
+    cfg = dataclasses.replace(S.CONFIGS[cfgname], tol=1e-30, maxit=30)
     inp = S.make_inputs(cfg)
     n, N, M, J = cfg.n, cfg.N, cfg.M, cfg.J
     psf, gam = inp["psf"], inp["gamma"]
@@ -105,8 +109,8 @@ def test_c4_full_ladder_fixed_iterations(torch_dev):
     AWs, EWs = [AWall[:, :J], AWall[:, J:]], [EWall[:, :J], EWall[:, J:]]
     nL = int(round(0.75 * M))
     grp = np.array([0 if l < nL else 1 for l in range(M)], dtype=np.int32)
-    sample = [0, 16, 32, 48, 64, 80, 96, 112, 127]
-    gidx = sorted(set(sample[::2] + [5, 40, 100, 120]))         # shifts with a carried column
+    sample = sorted(set([0] + [int(round(f * (M - 1))) for f in np.linspace(0.125, 1.0, 8)]))
+    gidx = sorted(set(sample[::2] + [int(M * f) for f in (0.04, 0.31, 0.78, 0.94)]))   # carried columns
     gh = rng.standard_normal((N, len(gidx)))
     for j, l in enumerate(gidx):
         W = Ws[grp[l]]
