@@ -163,6 +163,20 @@ rsk_status rsk_apply_shifted(rsk_handle h, int nvec, const double* X, int64_t ld
                              const double* gamma, double* Y, int64_t ldy, double* EY,
                              int64_t ldey, double* xdoty, int mode, void* stream);
 
+/* rsk_apply_shifted_rows -- rsk_apply_shifted restricted to the output rows
+ * [row0, row1) of the handle's image (0 <= row0 < row1 <= ny): Y_s (and EY_s) rows
+ * outside the range are left untouched; xdoty[s] = X_s . Y_s over the range's rows. The
+ * operator itself is unchanged (each output row reads X rows row -/+ 2r, as the full
+ * apply): the row-slab solver computes the interior rows, which need no
+ * halo, while the halo rows are still in flight, then the rows next to the halos.
+ * SHIFTED and SPLIT modes, streaming strip core only (images of >= 512^2 pixels, even
+ * widths): otherwise RSK_EUNSUPPORTED and nothing is enqueued (use rsk_apply_shifted).
+ * Counts nvec applies only when the range is the whole image. */
+rsk_status rsk_apply_shifted_rows(rsk_handle h, int nvec, const double* X, int64_t ldx,
+                                  const double* gamma, double* Y, int64_t ldy, double* EY,
+                                  int64_t ldey, double* xdoty, int mode, int64_t row0, int64_t row1,
+                                  void* stream);
+
 /* rsk_recycle_project -- tall-skinny recycle-space products (U^T r, U c; the
  * Grams of eq:orthupdate and eq:hq):
  *   RSK_PROJ_UTV : Cm (k x nv, column-major, ldc >= k) = U^T V

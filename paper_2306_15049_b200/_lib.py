@@ -87,6 +87,8 @@ _SIGS = {
     "rsk_set_weights": (C.c_int, [C.c_void_p, _dp, _dp, C.c_void_p]),
     "rsk_apply_shifted": (C.c_int, [C.c_void_p, C.c_int, _dp, _i64, _dp, _dp, _i64, _dp, _i64, _dp,
                                     C.c_int, C.c_void_p]),
+    "rsk_apply_shifted_rows": (C.c_int, [C.c_void_p, C.c_int, _dp, _i64, _dp, _dp, _i64, _dp, _i64, _dp,
+                                         C.c_int, _i64, _i64, C.c_void_p]),
     "rsk_recycle_project": (C.c_int, [C.c_void_p, C.c_int, _i64, C.c_int, _dp, _i64, C.c_int, _dp,
                                       _i64, _dp, _i64, C.c_void_p]),
     "rsk_irn_weights": (C.c_int, [C.c_void_p, _dp, C.c_double, _dp, _dp, _dp, C.c_void_p]),

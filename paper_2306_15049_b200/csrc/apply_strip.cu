@@ -31,8 +31,8 @@ __global__ void __launch_bounds__(kAT, kStripCtasPerSm)
     const int strip = ss % p.nstrip, seg = ss / p.nstrip;
     const int s = list ? list[li] : li;
     double lo;
-    const double dot = Core::item(p, smem, ring, s, strip, seg * p.seg_rows, min(p.ny, (seg + 1) * p.seg_rows), false,
-                                  &lo) + lo;
+    const int ra = p.row0 + seg * p.seg_rows;
+    const double dot = Core::item(p, smem, ring, s, strip, ra, min(p.row1, ra + p.seg_rows), false, &lo) + lo;
     if (p.want_dot) {
       const double bs = block_sum(dot, smem + C::OFF_RED);
       if (threadIdx.x == 0) p.part[(int64_t)li * ipv + ss] = bs;
@@ -93,6 +93,8 @@ bool strip_fill_params(Handle* h, StripParams& p, const double* X, int64_t ldx, 
   p.ny = (int)h->ny; p.nx = (int)h->nx;
   p.nstrip = (int)((h->nx + kStripW - 1) / kStripW);
   p.seg_rows = seg_rows;
+  p.row0 = 0;
+  p.row1 = (int)h->ny;
   p.nseg = (int)((h->ny + seg_rows - 1) / seg_rows);
   p.mode = mode;
   p.prefetch_w = getenv("RSK_STRIP_NOPF") ? 0 : 1;
@@ -132,15 +134,20 @@ size_t strip_smem_bytes(int r) {
 
 // Returns cudaErrorNotSupported (nothing enqueued) when the strip path does not apply
 // (odd widths / misaligned batches: no TMA map); the caller then uses the tiled core.
-cudaError_t launch_apply_strip(Handle* h, const ApplyLaunch& a, cudaStream_t st) {
+// rows [row0, row1) of the output only (row1 <= 0: the whole image)
+cudaError_t launch_apply_strip(Handle* h, const ApplyLaunch& a, cudaStream_t st, int row0, int row1) {
   if (!(a.mode == RSK_APPLY_SHIFTED || a.mode == RSK_APPLY_SPLIT) || a.cg || a.nlist <= 0 || h->ct)
     return cudaErrorNotSupported;
+  if (row1 <= 0) { row0 = 0; row1 = (int)h->ny; }
   const int64_t nv = (a.list || a.nvec_total > 0) ? a.nvec_total : a.nlist;
   const int ctas = kStripCtasPerSm * h->sm_count;
-  const int seg = strip_seg_rows(h->ny, h->nx, a.nlist, ctas);
+  const int seg = strip_seg_rows(row1 - row0, h->nx, a.nlist, ctas);
   StripParams p;
   if (!strip_fill_params(h, p, a.X, a.ldx, nullptr, 0, nv, a.Y, a.ldy, a.EY, a.ldey, a.gamma, a.mode, seg))
     return cudaErrorNotSupported;
+  p.row0 = row0;
+  p.row1 = row1;
+  p.nseg = (row1 - row0 + seg - 1) / seg;
   p.want_dot = a.xdoty != nullptr;
   const int ipv = p.nseg * p.nstrip;
   if (a.xdoty && sizeof(double) * (size_t)ipv * (size_t)a.nlist > h->scratch_bytes) return cudaErrorNotSupported;

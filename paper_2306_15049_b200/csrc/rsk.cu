@@ -302,6 +302,52 @@ extern "C" rsk_status rsk_set_weights(rsk_handle h, const double* wx, const doub
   return RSK_OK;
 }
 
+extern "C" rsk_status rsk_apply_shifted_rows(rsk_handle h, int nvec, const double* X, int64_t ldx,
+                                             const double* gamma, double* Y, int64_t ldy, double* EY,
+                                             int64_t ldey, double* xdoty, int mode, int64_t row0, int64_t row1,
+                                             void* stream) {
+  if (!h) return RSK_EINVAL;
+  const int64_t N = h->ny * h->nx;
+  RSK_ARG(nvec >= 0, "rsk_apply_shifted_rows: nvec < 0");
+  RSK_ARG(row0 >= 0 && row0 < row1 && row1 <= h->ny, "rsk_apply_shifted_rows: bad row range");
+  if (nvec == 0) return RSK_OK;
+  RSK_ARG(mode >= RSK_APPLY_SHIFTED && mode <= RSK_APPLY_CT_ONLY, "rsk_apply_shifted_rows: bad mode");
+  if (mode != RSK_APPLY_SHIFTED && mode != RSK_APPLY_SPLIT) {
+    h->err = "rsk_apply_shifted_rows: SHIFTED and SPLIT only";
+    return RSK_EUNSUPPORTED;
+  }
+  RSK_ARG(X && Y && aligned8(X) && aligned8(Y), "rsk_apply_shifted_rows: null/misaligned X or Y");
+  RSK_ARG(ldx >= N && ldy >= N, "rsk_apply_shifted_rows: ld < N");
+  RSK_ARG(mode != RSK_APPLY_SHIFTED || gamma, "rsk_apply_shifted_rows: gamma required");
+  RSK_ARG(mode != RSK_APPLY_SPLIT || (EY && ldey >= N), "rsk_apply_shifted_rows: EY required for SPLIT");
+  {
+    const char* xb = (const char*)X;
+    const char* xe = (const char*)(X + (nvec - 1) * ldx + N);
+    const char* yb = (const char*)Y;
+    const char* ye = (const char*)(Y + (nvec - 1) * ldy + N);
+    RSK_ARG(ye <= xb || yb >= xe, "rsk_apply_shifted_rows: X and Y overlap");
+  }
+  if (N < kStripMinN || h->rank != 1 || h->ct) {
+    h->err = "rsk_apply_shifted_rows: only the streaming strip core takes a row range";
+    return RSK_EUNSUPPORTED;
+  }
+  ApplyLaunch a{};
+  a.X = X; a.ldx = ldx; a.Y = Y; a.ldy = ldy; a.EY = EY; a.ldey = ldey;
+  a.gamma = gamma; a.list = nullptr; a.nlist = nvec; a.mode = mode; a.xdoty = xdoty;
+  a.cg = nullptr; a.cg_alpha = false;
+  const cudaError_t e = launch_apply_strip(h, a, S(stream), (int)row0, (int)row1);
+  if (e == cudaErrorNotSupported) {
+    h->err = "rsk_apply_shifted_rows: strip core not applicable (width / alignment)";
+    return RSK_EUNSUPPORTED;
+  }
+  RSK_CUDA(e);
+  if (row0 == 0 && row1 == h->ny) {
+    h->nA += nvec;
+    h->nE += nvec;
+  }
+  return RSK_OK;
+}
+
 extern "C" rsk_status rsk_apply_shifted(rsk_handle h, int nvec, const double* X, int64_t ldx,
                                         const double* gamma, double* Y, int64_t ldy, double* EY,
                                         int64_t ldey, double* xdoty, int mode, void* stream) {

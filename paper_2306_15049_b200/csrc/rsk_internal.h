@@ -167,7 +167,7 @@ cudaError_t launch_apply_taps(Handle* h, const ApplyLaunch& a, const double* cx,
 cudaError_t launch_apply_rank2(Handle* h, const ApplyLaunch& a, cudaStream_t st);
 // streaming strip apply for large images (apply_strip.cu); cudaErrorNotSupported = not applicable
 constexpr int64_t kStripMinN = 512 * 512;
-cudaError_t launch_apply_strip(Handle* h, const ApplyLaunch& a, cudaStream_t st);
+cudaError_t launch_apply_strip(Handle* h, const ApplyLaunch& a, cudaStream_t st, int row0 = 0, int row1 = 0);
 cudaError_t launch_ct_apply(Handle* h, const ApplyLaunch& a, cudaStream_t st);   // ct.cu
 int apply_tiles(const Handle* h);
 int apply_tile_rows(int r);

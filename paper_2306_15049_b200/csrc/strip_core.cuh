@@ -83,6 +83,7 @@ struct alignas(64) StripParams {
   double* part;          // X.Y partial per (vector id, segment x strip)
   int ny, nx;
   int nstrip, nseg, seg_rows;
+  int row0, row1;        // output rows [row0, row1) (segments start at row0; default 0, ny)
   int mode;              // RSK_APPLY_SHIFTED or RSK_APPLY_SPLIT
   int want_dot;
   int prefetch_w;        // L1 prefetch of the weights two blocks ahead (RSK_STRIP_NOPF=1: off)

@@ -147,6 +147,19 @@ class Handle:
                                         _dptr(xdoty), mode, _stream(stream))
         self._check(st, "rsk_apply_shifted")
 
+    def apply_shifted_rows(self, X, Y, row0, row1, gamma=None, EY=None, xdoty=None, mode=L.RSK_APPLY_SHIFTED,
+                           stream=None, nvec=None):
+        """rsk_apply_shifted on the output rows [row0, row1) only. Returns False (nothing
+        enqueued) where the library has no row-range path (RSK_EUNSUPPORTED)."""
+        nv = nvec if nvec is not None else _nv(X)
+        st = self.lib.rsk_apply_shifted_rows(self.h, nv, _dptr(X), _ld(X), _dptr(gamma), _dptr(Y), _ld(Y),
+                                             _dptr(EY), _ld(EY) if EY is not None else self.N,
+                                             _dptr(xdoty), mode, int(row0), int(row1), _stream(stream))
+        if st == L.RSK_EUNSUPPORTED:
+            return False
+        self._check(st, "rsk_apply_shifted_rows")
+        return True
+
     def recycle_project(self, op, U, V, Cm, k=None, nv=None, stream=None):
         """op = RSK_PROJ_UTV (Cm = U^T V), RSK_ADD_UC (V += U Cm), RSK_SUB_UC (V -= U Cm).
         U: (k, n) tensor, V: (nv, n), Cm: (nv, k) tensor (= column-major k x nv)."""

@@ -23,6 +23,7 @@ ever waits on another rank's kernel, the host moves the halo rows between launch
 from __future__ import annotations
 
 import dataclasses
+import os
 import threading
 
 import numpy as np
@@ -106,6 +107,12 @@ class DistComm:
 
     def halo(self, T: torch.Tensor):
         """T: (nv, ext_rows*nx). Fill the halo rows from the neighbours' owned rows."""
+        self.halo_finish(self.halo_start(T))
+
+    def halo_start(self, T: torch.Tensor):
+        """Post the halo exchange of T (send buffers are copies of the owned boundary rows;
+        under NCCL the transfers run on NCCL's stream, concurrently with work the caller
+        enqueues next on the current stream). Returns the pending state for halo_finish."""
         import torch.distributed as dist
         p, k, nx = self.plan, self.rank, self.plan.nx
         s = p.slabs[k]
@@ -124,9 +131,15 @@ class DistComm:
             buf = torch.empty(T.shape[0], s.bot * nx, dtype=T.dtype, device=bdev)
             ops += [dist.P2POp(dist.isend, send, k + 1), dist.P2POp(dist.irecv, buf, k + 1)]
             recv.append((buf, (off + s.own_rows) * nx))
-        if ops:
-            for req in dist.batch_isend_irecv(ops):
-                req.wait()
+        reqs = dist.batch_isend_irecv(ops) if ops else []
+        return T, reqs, recv, ops
+
+    def halo_finish(self, pend):
+        """Wait for the posted exchange (the current stream waits under NCCL) and copy the
+        received rows into T's halo."""
+        T, reqs, recv, _ops = pend
+        for req in reqs:
+            req.wait()
         for buf, at in recv:
             T[:, at:at + buf.shape[1]].copy_(buf)
 
@@ -166,6 +179,13 @@ class ThreadComm:
         g.bar.wait()
         t.copy_(tot)
         self._sync(t)
+
+    def halo_start(self, T: torch.Tensor):
+        self.halo(T)      # host threads: the exchange completes here
+        return None
+
+    def halo_finish(self, pend):
+        pass
 
     def halo(self, T: torch.Tensor):
         g, p, k, nx = self.g, self.plan, self.rank, self.plan.nx
@@ -231,6 +251,7 @@ class SlabOps:
         self.own_n = self.s.own_rows * plan.nx
         self.dev = torch.device("cuda", device)
         self.h = Handle.slab(plan.ny, plan.nx, self.s.row0, self.s.own_rows, psf, plan.H, device)
+        self.overlap = os.environ.get("RSK_SLAB_OVERLAP", "1") != "0"   # halo / interior overlap
         assert self.h.slab_info[1:3] == (self.s.ext0, self.s.ext1), (self.h.slab_info, self.s)
         self.lib = L.load()
         self.f = dict(dtype=torch.float64, device=self.dev)
@@ -251,8 +272,30 @@ class SlabOps:
 
     def apply(self, X: torch.Tensor, Y: torch.Tensor, gamma: torch.Tensor | None = None,
               mode=L.RSK_APPLY_SHIFTED, EY: torch.Tensor | None = None):
-        """Y = A_gamma X on the owned rows (X: extended vectors, halo refreshed here)."""
-        self.comm.halo(X)
+        """Y = A_gamma X on the owned rows (X: extended vectors, halo refreshed here).
+        The halo exchange is overlapped with the interior rows: an owned row
+        at least H = 2r rows from a neighbour's slab reads only owned rows, so those rows
+        are computed (rsk_apply_shifted_rows) while the halo rows are in flight, and the H
+        rows next to each neighbour after they arrived. Handles without a row-range path
+        (images below the strip core's size) exchange first and apply whole."""
+        s, k, H = self.s, self.rank, self.plan.H
+        # every range starts on a multiple of 8 rows of the slab image, as the whole-image
+        # apply's 8-row output blocks do: the rows come out bit for bit as without overlap
+        lo, hi = s.top, s.top + s.own_rows
+        i0 = -(-(lo + (H if k > 0 else 0)) // 8) * 8
+        i1 = (hi - (H if k < self.plan.nranks - 1 else 0)) // 8 * 8
+        if self.overlap and i1 > i0 and mode in (L.RSK_APPLY_SHIFTED, L.RSK_APPLY_SPLIT):
+            pend = self.comm.halo_start(X)
+            if self.h.apply_shifted_rows(X, Y, i0, i1, gamma=gamma, EY=EY, mode=mode):
+                self.comm.halo_finish(pend)
+                if i0 > lo:
+                    self.h.apply_shifted_rows(X, Y, lo // 8 * 8, i0, gamma=gamma, EY=EY, mode=mode)
+                if i1 < hi:
+                    self.h.apply_shifted_rows(X, Y, i1, hi, gamma=gamma, EY=EY, mode=mode)
+                return
+            self.comm.halo_finish(pend)
+        else:
+            self.comm.halo(X)
         self.h.apply_shifted(X, Y, gamma=gamma, EY=EY, mode=mode)
 
     def dot(self, X, Y) -> torch.Tensor:

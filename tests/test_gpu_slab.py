@@ -205,3 +205,48 @@ def test_slab_nested_outer_step_matches_single_domain(torch_dev, nranks):
     for l in range(cfg.M):
         rel = np.linalg.norm(Xs[l] - X_ref[l]) / np.linalg.norm(X_ref[l])
         assert rel <= 1e-7, (l, rel)
+
+
+@pytest.mark.parametrize("n,r", [(512, 7), (520, 10)])
+def test_apply_shifted_rows_matches_full_apply(torch_dev, n, r):
+    """rsk_apply_shifted_rows (the row-slab overlap's interior / boundary applies): rows
+    [row0, row1) equal to the whole-image apply (bit for bit when row0 is a multiple of 8,
+    the whole apply's output-block grid; to 1e-13 otherwise), the other rows untouched,
+    xdoty over the range's rows; and a cover of the image by ragged ranges reproduces the
+    whole apply. Below the strip core's size the call declines (RSK_EUNSUPPORTED)."""
+    torch, dev = torch_dev
+    from paper_2306_15049_b200 import _lib as L
+    from paper_2306_15049_b200.rsk import Handle
+    psf = S.gaussian_psf(r, 1.0 + 0.3 * r)
+    wx, wy = S.random_weights(5 + n, n)
+    wxd, wyd = (torch.from_numpy(np.ascontiguousarray(a.ravel())).to(dev) for a in (wx, wy))
+    X = torch.from_numpy(S.random_vectors(3 + n, (3, n * n))).to(dev)
+    gam = torch.tensor([0.0, 0.7, 25.0], dtype=torch.float64, device=dev)
+    h = Handle(n, n, psf, 0)
+    h.set_weights(wxd, wyd)
+    Y = torch.empty_like(X)
+    h.apply_shifted(X, Y, gamma=gam)
+    for row0, row1 in [(40, 301), (0, 8), (n - 24, n), (37, 301), (n - 21, n)]:
+        Yr = torch.full_like(X, float("nan"))
+        xd = torch.zeros(3, dtype=torch.float64, device=dev)
+        assert h.apply_shifted_rows(X, Yr, row0, row1, gamma=gam, xdoty=xd)
+        a, b = row0 * n, row1 * n
+        if row0 % 8 == 0:   # the same 8-row output blocks as the whole apply: same bits
+            assert torch.equal(Yr[:, a:b], Y[:, a:b]), (row0, row1)
+        else:               # another grouping of the y-pass k-steps: the apply bar (1e-13)
+            err = ((Yr[:, a:b] - Y[:, a:b]).abs().max(dim=1).values / Y[:, a:b].abs().max(dim=1).values)
+            assert float(err.max()) <= 1e-13, (row0, row1, err)
+        assert torch.isnan(Yr[:, :a]).all() and torch.isnan(Yr[:, b:]).all()
+        ref = (X[:, a:b] * Y[:, a:b]).sum(dim=1)
+        assert torch.allclose(xd, ref, rtol=1e-13, atol=0), (xd, ref)
+    Ys = torch.full_like(X, float("nan"))
+    EYs = torch.full_like(X, float("nan"))
+    for row0, row1 in [(0, 16), (16, 248), (248, n)]:
+        assert h.apply_shifted_rows(X, Ys, row0, row1, EY=EYs, mode=L.RSK_APPLY_SPLIT)
+    Ya = torch.empty_like(X)
+    EYa = torch.empty_like(X)
+    h.apply_shifted(X, Ya, EY=EYa, mode=L.RSK_APPLY_SPLIT)
+    assert torch.equal(Ys, Ya) and torch.equal(EYs, EYa)
+    small = Handle(64, 64, psf, 0)
+    Z = torch.zeros(1, 64 * 64, dtype=torch.float64, device=dev)
+    assert not small.apply_shifted_rows(Z, torch.empty_like(Z), 8, 40, gamma=gam)
