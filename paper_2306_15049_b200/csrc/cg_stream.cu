@@ -1,26 +1,25 @@
 // Streaming persistent lockstep loop of the batched deflated CG (rsk_cg_recycled_batch)
-// for images beyond L2 (C3, C4, C5): DESIGN.md §4.2b.
+// for images beyond L2 (C3, C4, C5): DESIGN.md §4.2.
 //
 // Same recurrences as cg_persist.cu and the oracle O4 (oracle/defcg.py, reading D1):
 //
 //   A  w = A_gamma p (ACTIVE) or w = A_gamma x (RCONV: true-residual confirm): the strip
-//      apply (strip_core.cuh), items = (shift, 64-column strip, row segment), one X.Y
-//      partial per item                                                     -- barrier
-//   B  alpha = rho / p.w from the item partials (fixed order); per 1024-row chunk and
-//      pass of <= 32 shifts of one group: r = r - alpha w (or b - w), partial sums of
-//      rho' = r.r, zeta = ZGhat.r and z = [AW ; EW]^T r (FP64 tensor cores)   -- barrier
+//      apply (strip_core.cuh) over balanced 8-row-block ranges of all (shift, strip)
+//      columns; one double-double p.w partial per (shift, CTA)            -- barrier
+//   B  alpha = rho / p.w (double-double sum of the partials); per CTA row range and pass
+//      of <= 16 shifts of one group: r = r - alpha w (or b - w), partial sums of
+//      rho' = r.r, zeta = ZGhat.r and z = [AW ; EW]^T r (FP64 tensor cores) -- barrier
 //   B2 one CTA per shift: chunk sums in fixed order, mu = G^-1 z, beta, status -- barrier
 //   C  x += alpha p ; p = r + beta p - W mu_W - ghat mu_g (W mu on the tensor cores);
-//      residual store                                                         -- barrier
+//      residual store                                                      -- barrier
 //
-// Data movement: the per-shift vectors of phases B and C stream through two shared-
-// memory stages of 8 shifts x 128 rows by 1-D bulk copies (cp.async.bulk, mbarrier
-// completion) and go back by bulk stores, so the bytes in flight do not depend on
-// registers or occupancy (two 8-warp CTAs per SM, <= 128 registers). The group columns
-// AW, EW, W are read once per (chunk, pass) from HBM into L1 by the DMMA fragment loads
-// and re-read from L1 by the other shift batches of the pass.
-// Every sum has a fixed order that depends only on N and the launch geometry (segment
-// rows, chunk rows): results per shift do not depend on the other shifts of the batch.
+// Data movement: phases B and C stream the per-shift vectors and the group columns
+// straight into DMMA fragment registers (wide B: 32-byte lane loads, 128-byte runs per
+// shift / column per warp instruction; C: 16-byte pairs, 128-byte runs), every load of a
+// super-step issued before its arithmetic; two 8-warp CTAs per SM, <= 128 registers.
+// Every sum has a fixed order that depends only on N and the launch geometry (CTA and
+// warp row ranges, nchunk): results per shift do not depend on the other shifts of the
+// batch (the N-rank shift-sharded run does the 1-rank work bit for bit).
 #include <cooperative_groups.h>
 #include <cuda_runtime.h>
 
@@ -34,8 +33,6 @@ namespace rsk {
 
 constexpr int kSMaxShift = 256;
 constexpr int kSPV = kMaxM + 1;     // partial slots per (shift, chunk): z_0..z_{m-1}, rho at kMaxM
-constexpr int kSB = 8;              // shifts per stage batch
-constexpr int kSVec = 4;            // vectors per shift in a stage
 
 __device__ unsigned long long g_sprof[8];   // per-phase ns (RSK_PERSIST_PROF), block 0's view
 __device__ unsigned long long g_sprof3[8];
@@ -44,9 +41,6 @@ __device__ unsigned long long g_sprof2[8];  // block 0, warp 1: B wait ns, B ste
 
 struct alignas(64) StreamParams {
   StripParams sp;     // apply: mapX over P (ld N), mapX2 over the iterates X (ld ldx), Y = Wv
-  CUtensorMap mAW[RSK_MAX_GROUPS];   // 2-D {N, J} maps of the group blocks, box {kSP, J}
-  CUtensorMap mEW[RSK_MAX_GROUPS];
-  CUtensorMap mW[RSK_MAX_GROUPS];
   CgDev* cg;
   double* partA;      // [shift][ipv]
   double* partB;      // [shift][kSPV][nchunk]
@@ -55,7 +49,7 @@ struct alignas(64) StreamParams {
   int* iters_done;
   int nshift;
   int nchunk;         // partial slots per shift = the grid (one row range per CTA)
-  int64_t rpc;        // rows per CTA (multiple of kSRs)
+  int64_t rpc;        // rows per CTA (multiple of 128)
   int64_t cg_N;
   int ipv;            // apply items per vector (segments x strips)
   int max_iters;
@@ -101,29 +95,12 @@ __device__ __forceinline__ void sgrid_sync(unsigned* bar, unsigned& target) {
   __syncthreads();
 }
 
-__device__ __forceinline__ void bulk_load(void* dst, const void* src, unsigned bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-__device__ __forceinline__ void bulk_store(void* dst, const void* src, unsigned bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(smem_u32(src)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
 // group-block loads: read once per pass and CTA range -- L2 only (RSK_GRP_L1 kept them in L1)
 #ifdef RSK_GRP_L1
 __device__ __forceinline__ double2 ldgrp(const double2* p) { return __ldg(p); }
 #else
 __device__ __forceinline__ double2 ldgrp(const double2* p) { return __ldcg(p); }
 #endif
-__device__ __forceinline__ void prefetch_l2(const void* p) { asm volatile("prefetch.global.L2 [%0];\n" ::"l"(p)); }
-__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
 // ---------------------------------------------------------------- active list
 // one int per entry: sid | mode << 9 | grp << 12 | m << 14 | hg << 19
@@ -170,74 +147,29 @@ __device__ __forceinline__ int s_pass_end(const SList& L, int li0) {
   while (li1 < L.n && li1 < li0 + kSPass && le_grp(L.e[li1]) == g) ++li1;
   return li1;
 }
-__device__ __forceinline__ int s_npass(const SList& L) {
-  int np = 0;
-  for (int li = 0; li < L.n; li = s_pass_end(L, li)) ++np;
-  return np;
-}
-__device__ __forceinline__ int s_pass_start(const SList& L, int k) {
-  int li = 0;
-  for (int i = 0; i < k; ++i) li = s_pass_end(L, li);
-  return li;
-}
-
 // ---------------------------------------------------------------- shared memory plan
 // [0, SCRATCH): the strip apply's input / x-pass rings (phase A) or the B / C stages,
 // pass accumulators, cross-warp reduction and per-pass scalars (phases B, B2, C);
 // [SCRATCH, ...): the strip apply's persistent tail (corrections, mbarriers) + 2 stage
 // mbarriers -- never touched by another phase
 constexpr int kSPS = 8;        // per pass entry: beta, 1/|r|, slot, flags, alpha
-constexpr int kSRs = 64;       // rows per stage step
-constexpr int kSP = 68;        // staged pitch (rows + 4: 4 mod 8 doubles, conflict-free fragments)
-constexpr int kSNST = 3;       // stages
 constexpr int kSMaxPass = 24;  // passes per phase (<= 256 shifts / 16 + groups)
+constexpr int kRW = 34;        // phase B staging per (warp, shift): zA[16], zE[16], rho, zeta
 template <int R>
 struct SCfg {
-  // stage: group tiles [2][16][kSP] (phase B: AW, EW; phase C: W) + shift part
-  // [8][4][kSP] (B: w, r, zg; C: p, r, x, ghat)
-  static constexpr int OFF_SG = 0;
-  static constexpr int OFF_SS = 2 * 16 * kSP;
-  static constexpr int STAGE = OFF_SS + kSB * 3 * kSP;   // B: AW, EW tiles + 8 x (w, r, zg);
-  // C: the W tile + 8 x (p, r, x, ghat) = 16 kSP + 32 kSP <= STAGE
-  static_assert(16 * kSP + kSB * kSVec * kSP <= OFF_SS + kSB * 3 * kSP, "phase C stage");
-  static constexpr int OFF_ST = 0;                            // kSNST stages
-  static constexpr int OFF_RED = OFF_ST + kSNST * STAGE;      // [8 warps][64] D tile partials
-  static constexpr int OFF_PS = OFF_RED + 8 * 64;             // [32][kSPS] (B: rho / zeta partials)
-  static constexpr int BC_END = OFF_PS + 32 * kSPS;
+  // phases B, B2, C reuse the strip apply's rings: B's per-warp partials [8][32][kRW], B2's
+  // sums and Cholesky factor, C's per-pass scalars [32][kSPS] and mu [32][kMaxM]
+  static constexpr int B_END = 8 * 32 * kRW;
+  static constexpr int B2_END = 32 + kMaxM * kMaxM;
+  static constexpr int C_END = 32 * kSPS + 32 * kMaxM;
+  static constexpr int BC_END = B_END > B2_END ? (B_END > C_END ? B_END : C_END) : (B2_END > C_END ? B2_END : C_END);
   static constexpr int RING_END = StripCfg<R>::RING_END;
   static constexpr int SCRATCH = al16(BC_END > RING_END ? BC_END : RING_END);
   using Strip = StripCfg<R, SCRATCH>;
-  static constexpr int OFF_BAR = Strip::DBL;                  // kSNST stage mbarriers
-  static constexpr int DBL = OFF_BAR + kSNST;
+  static constexpr int DBL = Strip::DBL;
   static constexpr size_t SMEM = sizeof(double) * (size_t)DBL;
 };
 
-// A unit is (1024-row chunk, pass of <= 32 shifts of one group); its steps are
-// (64-row sub-chunk, batch of <= 8 shifts), batches innermost (the group tile of a
-// sub-chunk is re-read from L2 by the later batches).
-struct SStep {
-  int u, k;
-};
-struct SGeo {
-  int c, pk, li0, li1, nb, nsub, nsteps;
-  int64_t cbeg, cend;
-};
-// unit = pass pk of this CTA's row range [c * rpc, min(N, (c + 1) * rpc)): the rows are
-// split evenly over the CTAs (multiples of 64), so every CTA moves the same bytes
-__device__ __forceinline__ SGeo s_geo(const int* pst, int64_t rpc, int64_t N, int pk) {
-  SGeo G;
-  G.c = blockIdx.x;
-  G.pk = pk;
-  G.li0 = pst[pk];
-  G.li1 = pst[pk + 1];
-  G.nb = (G.li1 - G.li0 + kSB - 1) / kSB;
-  G.cbeg = (int64_t)G.c * rpc;
-  G.cend = imin64(N, G.cbeg + rpc);
-  const int64_t rows = G.cend > G.cbeg ? G.cend - G.cbeg : 0;
-  G.nsub = (int)((rows + kSRs - 1) / kSRs);
-  G.nsteps = G.nsub * G.nb;
-  return G;
-}
 // pass boundaries of the list (pst[0..npass]), computed by every CTA identically
 __device__ __forceinline__ int s_passes(const SList& L, int* pst) {
   __syncthreads();
@@ -338,7 +270,6 @@ __device__ __forceinline__ void s_phase_a(const StreamParams& P, const SList& L,
 // fragments (group columns 8 mb + g, row q) of AW / EW, shared by the four 8-shift N
 // blocks of a pass of <= 32 shifts. Every load of a group of k-steps is issued before
 // the arithmetic that consumes it. Partials per (shift, CTA row range), fixed order.
-constexpr int kRW = 34;   // per (warp, shift) staging: zA[16], zE[16], rho, zeta
 template <int R>
 __device__ void s_phase_b_reg(const StreamParams& P, const SList& L, double* smem, double* s_alpha, int* pst,
                               CgDev* cg) {
@@ -1030,7 +961,6 @@ __global__ void __launch_bounds__(kAT, kStripCtasPerSm) cg_stream_kernel(const _
 bool strip_fill_params(Handle* h, StripParams& p, const double* X, int64_t ldx, const double* X2, int64_t ldx2,
                        int64_t nvec_map, double* Y, int64_t ldy, double* EY, int64_t ldey, const double* gamma,
                        int mode, int seg_rows);
-bool make_map2s(CUtensorMap* m, const double* base, int64_t inner, int64_t outer, int64_t pitch, int bw, int bh);
 
 int stream_seg_rows(int64_t ny) { return ny > 512 ? 256 : 128; }
 // partial slots per shift: the largest item count, 64-row segments (s_seg_rows)
@@ -1136,15 +1066,11 @@ cudaError_t launch_cg_stream(Handle* h, CgDev* dev, const CgDev& hc, double* par
                          RSK_APPLY_SHIFTED, seg))
     return cudaSuccess;
   prm.sp.want_dot = 1;
-  // group tiles: 2-D maps {N, J_g} with box {kSP rows, J_g columns}
+  // group blocks: |J| <= 16 and 16-byte rows (the register-form fragment loads)
   for (int gi = 0; gi < RSK_MAX_GROUPS; ++gi) {
     const int J = hc.grp.J[gi];
     if (J <= 0 || !hc.grp.AW[gi]) continue;
     if (J > 16 || !al16p(hc.grp.AW[gi]) || !al16p(hc.grp.EW[gi]) || !al16p(hc.grp.W[gi])) return cudaSuccess;
-    if (!make_map2s(&prm.mAW[gi], hc.grp.AW[gi], N, J, hc.grp.ldw, kSP, J) ||
-        !make_map2s(&prm.mEW[gi], hc.grp.EW[gi], N, J, hc.grp.ldw, kSP, J) ||
-        !make_map2s(&prm.mW[gi], hc.grp.W[gi], N, J, hc.grp.ldw, kSP, J))
-      return cudaSuccess;
   }
   prm.cg = dev;
   prm.partA = partA;
