@@ -87,13 +87,17 @@ def torch_dev():
     return torch, torch.device("cuda", 0)
 
 
-@pytest.mark.parametrize("cfgname", ["C3", "C4"])
+@pytest.mark.parametrize("cfgname", ["C3", "C4", "C5"])
 def test_c4_full_ladder_fixed_iterations(torch_dev, cfgname):
     """C4 (and C3: 512^2, 64 shifts, |J| = 10, the same streaming loop at another
-    geometry) -- the whole ladder for 30 lockstep iterations, sampled shifts by the oracle."""
+    geometry) -- the whole ladder for 30 lockstep iterations, sampled shifts by the oracle.
+    C5 (4096^2, r = 10, 16 shifts, |J| = 8): the oracle's 21 x 21 convolution takes ~50 s
+    per apply at this size, so 2 lockstep iterations and the two largest shifts (the
+    survey's d4 plan for C5)."""
     torch, dev = torch_dev
     from paper_2306_15049_b200.pipeline import GpuSolver
-    cfg = dataclasses.replace(S.CONFIGS[cfgname], tol=1e-30, maxit=30)
+    its = 2 if cfgname == "C5" else 30
+    cfg = dataclasses.replace(S.CONFIGS[cfgname], tol=1e-30, maxit=its)
     inp = S.make_inputs(cfg)
     n, N, M, J = cfg.n, cfg.N, cfg.M, cfg.J
     psf, gam = inp["psf"], inp["gamma"]
@@ -110,6 +114,8 @@ def test_c4_full_ladder_fixed_iterations(torch_dev, cfgname):
     nL = int(round(0.75 * M))
     grp = np.array([0 if l < nL else 1 for l in range(M)], dtype=np.int32)
     sample = sorted(set([0] + [int(round(f * (M - 1))) for f in np.linspace(0.125, 1.0, 8)]))
+    if cfgname == "C5":
+        sample = [M - 2, M - 1]
     gidx = sorted(set(sample[::2] + [int(M * f) for f in (0.04, 0.31, 0.78, 0.94)]))   # carried columns
     gh = rng.standard_normal((N, len(gidx)))
     for j, l in enumerate(gidx):
