@@ -95,11 +95,37 @@ __device__ __forceinline__ void sgrid_sync(unsigned* bar, unsigned& target) {
   __syncthreads();
 }
 
+// Streaming loads of phases B / C carry the L2 prefetch-size hint (.L2::256B: a miss fills
+// the aligned 256-byte block, i.e. this warp's next 16-row super-step too -- more bytes in
+// flight without registers or prefetch instructions). A/B on one box (session 3): per
+// lockstep iteration at 1 / 4 / 16 / 32 shifts 140 / 306 / 585 / 1053 -> 133 / 297 / 575 /
+// 1030 us, C4 k = 1 step 12.18 -> 11.93 s. -DRSK_NO_L2PF builds the plain loads.
+#ifndef RSK_NO_L2PF
+#define RSK_L2PF 1
+#define RSK_PF ".L2::256B"
+#else
+#define RSK_PF ""
+#endif
+#ifdef RSK_L2PF
+__device__ __forceinline__ double2 ld2cg(const double* p) {
+  double2 v;
+  asm volatile("ld.global.cg" RSK_PF ".v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double2 ld2nc(const double* p) {
+  double2 v;
+  asm volatile("ld.global.nc" RSK_PF ".v2.f64 {%0,%1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+#else
+__device__ __forceinline__ double2 ld2cg(const double* p) { return __ldcg(reinterpret_cast<const double2*>(p)); }
+__device__ __forceinline__ double2 ld2nc(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+#endif
 // group-block loads: read once per pass and CTA range -- L2 only (RSK_GRP_L1 kept them in L1)
 #ifdef RSK_GRP_L1
 __device__ __forceinline__ double2 ldgrp(const double2* p) { return __ldg(p); }
 #else
-__device__ __forceinline__ double2 ldgrp(const double2* p) { return __ldcg(p); }
+__device__ __forceinline__ double2 ldgrp(const double2* p) { return ld2cg(reinterpret_cast<const double*>(p)); }
 #endif
 
 // ---------------------------------------------------------------- active list
@@ -450,12 +476,12 @@ __device__ void s_phase_b_reg(const StreamParams& P, const SList& L, double* sme
 // near 3 TB/s (tools/stream_bw.cu: 64-byte runs 2.6-3.1 TB/s, 128-byte 5.4-6.3 TB/s).
 // Needs N, ldw, ldgh multiples of 4 and 32-byte aligned vectors (launch_cg_stream).
 __device__ __forceinline__ void ld4cg(const double* p, double* v) {
-  asm volatile("ld.global.cg.v4.f64 {%0,%1,%2,%3}, [%4];"
+  asm volatile("ld.global.cg" RSK_PF ".v4.f64 {%0,%1,%2,%3}, [%4];"
                : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
                : "l"(p));
 }
 __device__ __forceinline__ void ld4nc(const double* p, double* v) {
-  asm volatile("ld.global.nc.v4.f64 {%0,%1,%2,%3}, [%4];"
+  asm volatile("ld.global.nc" RSK_PF ".v4.f64 {%0,%1,%2,%3}, [%4];"
                : "=d"(v[0]), "=d"(v[1]), "=d"(v[2]), "=d"(v[3])
                : "l"(p));
 }
@@ -736,11 +762,11 @@ __device__ void s_phase_c_reg(const StreamParams& P, const SList& L, double* sme
             const int v = L.e[li0 + k];
             const int s = le_sid(v);
             const int64_t o = (int64_t)s * N + row;
-            pv[h] = __ldcg(reinterpret_cast<const double2*>(cg->P + o));
-            if (f & 1) xv[h] = __ldcg(reinterpret_cast<const double2*>(cg->X + (int64_t)s * cg->ldx + row));
+            pv[h] = ld2cg(cg->P + o);
+            if (f & 1) xv[h] = ld2cg(cg->X + (int64_t)s * cg->ldx + row);
             if (f & 2) {
-              rv[h] = __ldcg(reinterpret_cast<const double2*>(cg->R + o));
-              if (le_hg(v)) gv[h] = __ldg(reinterpret_cast<const double2*>(cg->Ghat + (int64_t)s * cg->ldgh + row));
+              rv[h] = ld2cg(cg->R + o);
+              if (le_hg(v)) gv[h] = ld2nc(cg->Ghat + (int64_t)s * cg->ldgh + row);
             }
           }
         }
