@@ -983,6 +983,172 @@ __global__ void __launch_bounds__(kAT, kStripCtasPerSm) cg_stream_kernel(const _
   }
 }
 
+// ---------------------------------------------------------------- the skewed kernel
+// RSK_STREAM_SKEW=1 (session 4). The lockstep loop above runs a compute-bound phase (A: the
+// apply on the FP64 tensor cores, 16 B/px of DRAM traffic) and two DRAM-bound phases (B, C)
+// one after the other, so the DMMA pipe idles in B / C and HBM idles in A. Here the active
+// shifts of a launch are split into two halves H0 / H1 (contiguous in the group-sorted
+// list) and H1 runs one slot behind H0:
+//     slot 1: B(H0) | A(H1)     slot 2: B2(H0) | B(H1)
+//     slot 3: C(H0) | B2(H1)    slot 4: A(H0, next iteration) | C(H1)
+// In slots 1 and 4 the CTAs of one SM take the two tasks in opposite order (one streams
+// while the other computes). Every per-shift operation, sum order and partial slot is the
+// one of the lockstep kernel (the phases are batch-composition invariant), so the results
+// are bitwise the same; the price is that a group's blocks are read once per half.
+__device__ unsigned g_smslot[512];
+constexpr int kSkewDefault = 0;   // RSK_STREAM_SKEW overrides
+// between the two tasks of a slot: the next task may reuse the shared scratch through the
+// other proxy (TMA ring of phase A vs generic stores of B / B2 / C)
+__device__ __forceinline__ void s_task_switch() {
+  asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+  __syncthreads();
+}
+
+__device__ void s_build_list_half(const CgDev* cg, int ns, SList& L, int* tmp, const unsigned char* half, int h) {
+  for (int s = threadIdx.x; s < ns; s += blockDim.x) tmp[s] = cg->status[s] | (cg->group[s] << 8);
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    int n = 0;
+    for (int g = 0; g < RSK_MAX_GROUPS; ++g)
+      for (int s0 = 0; s0 < ns; s0 += 32) {
+        const int s = s0 + lane;
+        const int v = s < ns ? tmp[s] : -1;
+        const int st = v & 0xff;
+        const bool in = s < ns && (v >> 8) == g && (st == ST_ACTIVE || st == ST_RCONV) && half[s] == h;
+        const unsigned bal = __ballot_sync(0xffffffffu, in);
+        if (in) {
+          const int pos = n + __popc(bal & ((1u << lane) - 1u));
+          L.e[pos] = s | (st << 9) | (g << 12) | (cg->mloc[s] << 14) | (cg->hasg[s] << 19);
+        }
+        n += __popc(bal);
+      }
+    if (lane == 0) L.n = n;
+  }
+  __syncthreads();
+}
+
+template <int R>
+__global__ void __launch_bounds__(kAT, kStripCtasPerSm) cg_stream_skew_kernel(const __grid_constant__ StreamParams P) {
+  extern __shared__ __align__(128) double smem[];
+  using SC = SCfg<R>;
+  using Core = StripCore<R, SC::SCRATCH>;
+  __shared__ SList lists[2][2];
+  __shared__ int tmp[kSMaxShift];
+  __shared__ double s_alpha[2][kSMaxShift];
+  __shared__ int pst[kSMaxPass + 1];
+  __shared__ unsigned char half[kSMaxShift];
+  __shared__ int s_flip;
+  __shared__ CgDev s_cg;
+  if (threadIdx.x == 0) {
+    s_cg = *P.cg;
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    s_flip = (int)(atomicAdd(&g_smslot[smid & 511u], 1u) & 1u);
+  }
+  CgDev* cg = &s_cg;
+  const int ns = P.nshift;
+  const int tid = threadIdx.x;
+  Core::init(smem, P.sp);
+  StripRing ring{0u, 0u};
+  unsigned gen = 0u;
+  // the launch's split: first half of the group-sorted active list -> H0, the rest -> H1
+  s_build_list(cg, ns, lists[0][0], tmp);
+  {
+    const SList& F = lists[0][0];
+    const int n0 = (F.n + 1) >> 1;
+    for (int li = tid; li < F.n; li += blockDim.x) half[le_sid(F.e[li])] = li < n0 ? 0 : 1;
+  }
+  __syncthreads();
+  const bool flip = s_flip != 0;
+  s_build_list_half(cg, ns, lists[1][0], tmp, half, 1);
+  s_build_list_half(cg, ns, lists[0][0], tmp, half, 0);
+  sgrid_sync(P.bar, gen);
+
+  int it = 0;
+  unsigned long long t0 = 0;
+  auto mark = [&](int ph) {
+    if (P.prof && blockIdx.x == 0 && tid == 0) {
+      const unsigned long long t1 = s_timer();
+      if (t0) g_sprof[ph] += t1 - t0;
+      t0 = t1;
+    }
+  };
+  int cur0 = 0, cur1 = 0;
+  mark(7);
+  // one call site per phase (a task table per slot): the phases are inlined once, as in
+  // the lockstep kernel
+  enum { T_NONE = 0, T_A, T_B, T_B2, T_C };
+  auto run = [&](int kind, const SList* L, int h) {
+    switch (kind) {
+      case T_A: s_phase_a<R>(P, *L, smem, ring); break;
+      case T_B:
+        if (P.wide) s_phase_b_wide<R>(P, *L, smem, s_alpha[h], pst, &s_cg);
+        else s_phase_b_reg<R>(P, *L, smem, s_alpha[h], pst, &s_cg);
+        break;
+      case T_B2: s_phase_b2(P, *L, smem, &s_cg); break;
+      case T_C: s_phase_c_reg<R>(P, *L, smem, s_alpha[h], pst, &s_cg); break;
+      default: break;
+    }
+  };
+  if (lists[0][0].n + lists[1][0].n > 0 && P.max_iters > 0) {
+    // slots -1 (A(H0) alone), then 0..3 per iteration
+    int slot = -1;
+    bool done = false;
+#pragma unroll 1
+    while (!done) {
+      const SList* L0 = &lists[0][cur0];
+      const SList* L1 = &lists[1][cur1];
+      int k0 = T_NONE, k1 = T_NONE, h0 = 0, h1 = 1;
+      const SList* a0 = L0;
+      const SList* a1 = L1;
+      bool swap = false;
+      if (slot == -1) {
+        k0 = T_A;
+      } else if (slot == 0) {   // B(H0) | A(H1)
+        k0 = T_B; k1 = T_A; swap = flip;
+      } else if (slot == 1) {   // B2(H0) | B(H1)
+        k0 = T_B2; k1 = T_B;
+      } else if (slot == 2) {   // C(H0) | B2(H1); H0's statuses are stable: its next list
+        s_build_list_half(cg, ns, lists[0][cur0 ^ 1], tmp, half, 0);
+        k0 = T_C; k1 = T_B2;
+      } else {                  // A(H0) of the next iteration | C(H1)
+        s_build_list_half(cg, ns, lists[1][cur1 ^ 1], tmp, half, 1);
+        k0 = (it + 1 < P.max_iters) ? T_A : T_NONE;
+        a0 = &lists[0][cur0 ^ 1];
+        k1 = T_C; swap = !flip;
+      }
+      if (swap) {
+        const int tk = k0; k0 = k1; k1 = tk;
+        const int th = h0; h0 = h1; h1 = th;
+        const SList* tl = a0; a0 = a1; a1 = tl;
+      }
+#pragma unroll 1
+      for (int q = 0; q < 2; ++q) {
+        if (q) s_task_switch();
+        run(q ? k1 : k0, q ? a1 : a0, q ? h1 : h0);
+      }
+      mark(slot < 0 ? 7 : (slot == 0 ? 0 : slot + 1));
+      sgrid_sync(P.bar, gen);
+      mark(1);
+      if (slot == 3) {
+        if (P.prof && blockIdx.x == 0 && tid == 0) g_sprof[5] += 1;
+        cur0 ^= 1;
+        cur1 ^= 1;
+        ++it;
+        if (it >= P.max_iters || lists[0][cur0].n + lists[1][cur1].n == 0) done = true;
+        slot = 0;
+      } else {
+        ++slot;
+      }
+    }
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    *P.nactive = lists[0][cur0].n + lists[1][cur1].n;
+    *P.iters_done = it;
+  }
+}
+
 // ---------------------------------------------------------------- host side
 bool strip_fill_params(Handle* h, StripParams& p, const double* X, int64_t ldx, const double* X2, int64_t ldx2,
                        int64_t nvec_map, double* Y, int64_t ldy, double* EY, int64_t ldey, const double* gamma,
@@ -1040,8 +1206,12 @@ template <int R>
 static cudaError_t launch_stream_r(StreamParams& prm, int sm_count, cudaStream_t st, bool* ok) {
   using SC = SCfg<R>;
   // two CTAs per SM up to r = 10 (the configs); the occupancy query decides beyond
-  auto kfn = cg_stream_kernel<R>;
-  static int b = 0;
+  // read per launch (a launch is 512 lockstep iterations): tests toggle it in-process
+  const char* sk = getenv("RSK_STREAM_SKEW");
+  const int skew = sk ? (atoi(sk) != 0) : kSkewDefault;
+  auto kfn = skew ? cg_stream_skew_kernel<R> : cg_stream_kernel<R>;
+  static int bs[2] = {0, 0};
+  int& b = bs[skew];
   if (b == 0) {
     cudaError_t e = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SC::SMEM);
     if (e != cudaSuccess) return e;

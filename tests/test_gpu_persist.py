@@ -95,15 +95,18 @@ def _setup(torch, dev, cfg, nL, nR, J, seed, gam):
 
 
 @pytest.mark.parametrize("n,r,nL,nR,loop", [(112, 3, 44, 10, "stream"), (100, 7, 40, 9, "stream"),
-                                            (100, 7, 40, 9, "stream-narrow"), (100, 7, 40, 9, "tiled")])
+                                            (100, 7, 40, 9, "stream-narrow"), (100, 7, 40, 9, "tiled"),
+                                            (100, 7, 40, 9, "stream-skew")])
 def test_persistent_loop_multi_pass_two_groups(torch_dev, monkeypatch, n, r, nL, nR, loop):
     """loop = "stream": cg_stream.cu (the default for N >= 512^2; phase B in its wide form,
     N % 4 == 0); "stream-narrow": the same loop with the 16-byte-lane phase B (the form odd
-    leading dimensions take); "tiled": cg_persist.cu."""
+    leading dimensions take); "tiled": cg_persist.cu; "stream-skew": the streaming loop's
+    skewed two-half schedule (RSK_STREAM_SKEW=1)."""
     monkeypatch.setenv("RSK_CG_NOCLUSTER", "1")
     monkeypatch.setenv("RSK_CG_STREAM", "0" if loop == "tiled" else "1")
     if loop == "stream-narrow":
         monkeypatch.setenv("RSK_STREAM_NARROW", "1")
+    monkeypatch.setenv("RSK_STREAM_SKEW", "1" if loop == "stream-skew" else "0")
     torch, dev = torch_dev
     import dataclasses
     M = nL + nR
@@ -162,3 +165,33 @@ def test_stream_loop_batch_composition_invariant(torch_dev, monkeypatch):
     np.testing.assert_array_equal(rs["iters"], res["iters"][sub])
     np.testing.assert_array_equal(rs["applies"], res["applies"][sub])
     assert torch.equal(Xs, X[sub]), "sub-batch solutions must be bitwise equal to the full batch's"
+
+
+def test_stream_loop_skewed_schedule_bitwise(torch_dev, monkeypatch):
+    """The skewed schedule of the streaming loop (cg_stream_skew_kernel: the launch's active
+    shifts in two halves one slot apart, so that one half's apply overlaps the other half's
+    DRAM-bound phases) runs the same per-shift operations in the same order as the lockstep
+    schedule: solutions, iteration counts and accounting are bitwise equal."""
+    monkeypatch.setenv("RSK_CG_NOCLUSTER", "1")
+    monkeypatch.setenv("RSK_CG_STREAM", "1")
+    torch, dev = torch_dev
+    import dataclasses
+    n, r, nL, nR = 100, 7, 23, 9
+    M = nL + nR
+    cfg = dataclasses.replace(S.small_config(n=n, M=M, r=r, sigma=1.0 + 0.3 * r, tol=1e-10), maxit=20000)
+    gam = np.logspace(-4, 1.5, M)
+    sol, groups, ghat, X0 = _setup(torch, dev, cfg, nL, nR, 12, 1900 + n, gam)
+    out = []
+    for skew in ("0", "1"):
+        monkeypatch.setenv("RSK_STREAM_SKEW", skew)
+        X = X0.clone()
+        G = torch.empty_like(X)
+        res = sol.cg(list(range(M)), X, _CTX["has_xp"], Gout=G, groups=groups, ghat=ghat)
+        assert int(res["prof"][7]) == 3
+        assert np.all(res["status"] == 0)
+        out.append((X, G, res))
+    (X_a, G_a, r_a), (X_b, G_b, r_b) = out
+    assert int(r_a["iters"].max()) > 600, "several 512-iteration launches (the halves are re-split per launch)"
+    np.testing.assert_array_equal(r_a["iters"], r_b["iters"])
+    np.testing.assert_array_equal(r_a["applies"], r_b["applies"])
+    assert torch.equal(X_a, X_b) and torch.equal(G_a, G_b)

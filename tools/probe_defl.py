@@ -1,7 +1,7 @@
 """ncu / timing target: the batched deflated CG loop at a config's grid with M shifts in
 two groups, |J| random Ritz-like columns (images by the library's own apply), carried
 columns, a fixed number of lockstep iterations.
-  python tools/probe_defl.py [C4] [M] [iters] [J]"""
+  python tools/probe_defl.py [C4] [M] [iters] [J]      (PROBE_ONE_GROUP=1: one group)"""
 import os
 import sys
 
@@ -40,6 +40,8 @@ for g in range(2):
     sol.h.apply_shifted(W, AW, EY=EW, mode=L.RSK_APPLY_SPLIT)
     Ws.append(W); AWs.append(AW); EWs.append(EW)
 grp = np.array([0 if l < M // 2 else 1 for l in range(M)], dtype=np.int32)
+if os.environ.get("PROBE_ONE_GROUP"):   # the tail of a C4 step: every active shift in one group
+    grp[:] = 0
 Gh = torch.randn(M, N, **f)
 Gh /= Gh.norm(dim=1, keepdim=True)
 ZGh = torch.empty_like(Gh)
