@@ -576,7 +576,7 @@ def main():
     ap.add_argument("--step", default="outer", choices=["outer", "nested"])
     ap.add_argument("--check-every", type=int, default=8)
     ap.add_argument("--cpu-budget", type=float, default=15.0)
-    ap.add_argument("--ref-budget", type=float, default=10.0)
+    ap.add_argument("--ref-budget", type=float, default=5.0)
     ap.add_argument("--nested-budget", type=float, default=300.0)
     ap.add_argument("--no-nested", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
