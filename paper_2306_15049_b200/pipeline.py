@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import dataclasses
 import math
+import os
 import time
 
 import numpy as np
@@ -602,22 +603,74 @@ class GpuSolver:
         self.h.set_weights(self.wx, self.wy, stream=self.stream)
         self.cur_w = (self.wx, self.wy)
 
-    def run(self, K_out: int | None = None):
+    # ---- on-disk state of the nested solve between outer steps (checkpoint /
+    # hand-off). What outer step k+1 needs from step k (Alg. 5): the weights
+    # W_{k+1} (and W_k for eq:delta, D_k under Gazzola's rule), X^(k), G^(k), V_i1, x*.
+    _STATE_TENSORS = ("X_prev", "G_prev", "V_i1", "xstar")
+
+    def save_state(self, path: str, k_next: int, st: dict, lstars=()) -> None:
+        """Writes the state from which outer step `k_next` starts (after next_weights)."""
+        cpu = lambda t: None if t is None else t.detach().cpu()
+        blob = {"format": 1, "config": self.cfg.name, "N": self.N, "M": self.M, "k_next": int(k_next),
+                "gamma": np.asarray(self.gamma, dtype=np.float64), "lstars": [int(x) for x in lstars],
+                "prev_iters": None if st.get("prev_iters") is None else np.asarray(st["prev_iters"]),
+                "W_cur": tuple(cpu(t) for t in self.cur_w),
+                "W_prev": None if st.get("W_prev") is None else tuple(cpu(t) for t in st["W_prev"]),
+                "D": tuple(cpu(t) for t in (self.Dx, self.Dy)) if hasattr(self, "Dx") else None}
+        for name in self._STATE_TENSORS:
+            blob[name] = cpu(st.get(name))
+        tmp = path + ".tmp"
+        torch.save(blob, tmp)
+        os.replace(tmp, path)
+
+    def load_state(self, path: str) -> tuple[int, dict, list]:
+        """Adopts a saved state (weights into the handle) and returns (k_next, st, l* so far).
+        set_data must have been called with the same data; refuses another problem."""
+        blob = torch.load(path, map_location="cpu", weights_only=False)
+        if blob.get("format") != 1 or blob["N"] != self.N or blob["M"] != self.M or \
+                not np.array_equal(blob["gamma"], np.asarray(self.gamma, dtype=np.float64)):
+            raise ValueError(f"{path}: state of another problem (config {blob.get('config')!r}, "
+                             f"N = {blob.get('N')}, M = {blob.get('M')})")
+        dev = self.wx.device
+        self.wx.copy_(blob["W_cur"][0])
+        self.wy.copy_(blob["W_cur"][1])
+        self.h.set_weights(self.wx, self.wy, stream=self.stream)
+        self.cur_w = (self.wx, self.wy)
+        if blob["D"] is not None:   # Gazzola's rule: D_k
+            self.Dx, self.Dy = blob["D"][0].to(dev), blob["D"][1].to(dev)
+        st = {name: (None if blob[name] is None else blob[name].to(dev)) for name in self._STATE_TENSORS}
+        st = {k_: v for k_, v in st.items() if v is not None}
+        if blob["prev_iters"] is not None:
+            st["prev_iters"] = blob["prev_iters"]
+        if blob["W_prev"] is not None:
+            st["W_prev"] = tuple(t.to(dev) for t in blob["W_prev"])
+            self.w_prev = st["W_prev"]
+        return int(blob["k_next"]), st, list(blob["lstars"])
+
+    def run(self, K_out: int | None = None, checkpoint: str | None = None, resume: str | None = None):
         """The whole nested solve: up to K_out outer steps from W_0 = I; with
         cfg.stop == "lstar3" it also stops once l* is the same for three consecutive
-        steps (P:1042)."""
-        self.reset_weights()
-        st: dict = {}
-        outs = []
+        steps. checkpoint: a file rewritten (atomically) after every outer step
+        with the state the next step starts from; resume: such a file to continue from
+        (the returned list then holds the remaining steps only)."""
         K = K_out or self.cfg.K_out
         settle = getattr(self.cfg, "stop", "fixed") == "lstar3"
-        for k in range(K):
+        if resume:
+            k0, st, lst = self.load_state(resume)
+        else:
+            self.reset_weights()
+            k0, st, lst = 0, {}, []
+        outs = []
+        for k in range(k0, K):
             o, st = self.outer_step(k, st)
             outs.append(o)
-            if settle and len(outs) >= 3 and len({x.lstar for x in outs[-3:]}) == 1:
+            lst.append(int(o.lstar))
+            if settle and len(lst) >= 3 and len(set(lst[-3:])) == 1:
                 break
             if k + 1 < K:
                 self.next_weights(st["xstar"])
                 st["W_prev"] = self.w_prev
+                if checkpoint and self.dist.rank == 0:   # every rank holds the full state
+                    self.save_state(checkpoint, k + 1, st, lst)
         self.final = st
         return outs

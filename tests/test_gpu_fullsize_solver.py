@@ -198,3 +198,43 @@ def test_c2_stepwise_k0_k1(torch_dev):
         nwx, nwy = ops.irn_weights(xstar, cfg.tau)
         st = opipe.StepState(k + 1, nwx, nwy, rs.X, rs.G, rs.V_i1)
     assert limited <= 0.1 * 2 * M, f"{limited} tolerance-limited solutions"
+
+
+def test_checkpoint_resume_is_bitwise(tmp_path):
+    """SURVEY §5 (checkpoint / hand-off): the nested solve resumed from the on-disk state
+    written after outer step 1 finishes with the same bits as the uninterrupted run (the
+    state is everything step k+1 reads: W_{k+1}, W_k, X^(k), G^(k), V_i1, x*)."""
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA")
+    from paper_2306_15049_b200.pipeline import GpuSolver
+    cfg = S.CONFIGS["C1"]
+    inp = S.make_inputs(cfg)
+    dev = torch.device("cuda", 0)
+    xt, xi = torch.from_numpy(inp["x_true"]).to(dev), torch.from_numpy(inp["xi"]).to(dev)
+    ck = str(tmp_path / "state.pt")
+
+    sol = GpuSolver(cfg, inp["psf"], inp["gamma"])
+    sol.set_data(xt, xi)
+    full = sol.run(K_out=3)
+    X_full = sol.final["X_prev"].clone()
+
+    sol_a = GpuSolver(cfg, inp["psf"], inp["gamma"])
+    sol_a.set_data(xt, xi)
+    first = sol_a.run(K_out=2, checkpoint=ck)      # writes the state step 1 starts from
+    assert len(first) == 2
+    del sol_a
+    sol_b = GpuSolver(cfg, inp["psf"], inp["gamma"])
+    sol_b.set_data(xt, xi)
+    k_next, _, lst = sol_b.load_state(ck)
+    assert k_next == 1 and lst == [int(full[0].lstar)]
+    rest = sol_b.run(K_out=3, resume=ck)
+    assert [o.k for o in rest] == [1, 2]
+    for o, ref in zip(rest, full[1:]):
+        np.testing.assert_array_equal(o.iters, ref.iters)
+        np.testing.assert_array_equal(o.applies, ref.applies)
+        assert o.lstar == ref.lstar and o.nc == ref.nc
+    assert torch.equal(sol_b.final["X_prev"], X_full)
+    other = GpuSolver(S.CONFIGS["C2"], S.make_inputs(S.CONFIGS["C2"])["psf"], S.make_inputs(S.CONFIGS["C2"])["gamma"])
+    with pytest.raises(ValueError):
+        other.load_state(ck)
